@@ -1,0 +1,202 @@
+/*
+ * autx.h — C ABI of the B200-native Autellix scheduler hot path (arXiv 2502.13965).
+ *
+ * One autx_ctx = one serving engine on one GPU ("each LLM engine replica runs in a
+ * dedicated process"; here: one process per GPU).  All device work is stream-ordered on the
+ * stream given in autx_config.stream.  All arithmetic is integer; time is measured in engine
+ * steps (one decode iteration; SURVEY reading R17).  No function throws or aborts: every
+ * entry point returns an autx_status and, on failure, leaves a message for autx_last_error().
+ * Asynchronous CUDA failures surface as AUTX_E_CUDA from the next call.
+ *
+ * Citations: P:L<n> = line n of the paper text; "Alg. 1 l.k" = Algorithm 1 line k
+ * (P:L149-194); "Alg. 2 l.k" = Algorithm 2 line k; R<n> = reading n of the
+ * ambiguity register in DESIGN.md §3 (= SURVEY.md §8(c)).
+ *
+ * Per-step protocol (SURVEY §8(c) "Oracle step t"; event order of S:L572, reading R10):
+ *     autx_complete(ids of calls that finished in step t-1)   -> process-table update  (a1)
+ *     autx_register_call(arrivals of step t, canonical order)  -> registration           (a2)
+ *     autx_sched_step(t, &out)          demotion, anti-starvation, order, cutoff     (a3-a6)
+ *     autx_kv_swap(&layout, &stats)     swap-out of out.preempt, swap-in of out.admit (a7)
+ * Multi-engine routing (a8) is autx_route_* (see below).
+ */
+#ifndef AUTX_H
+#define AUTX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct autx_ctx autx_ctx;
+
+typedef enum {
+  AUTX_OK = 0,
+  AUTX_E_INVAL = 1,  /* bad argument / config, non-canonical arrival order, kvb > P at arrival (R13) */
+  AUTX_E_NOENT = 2,  /* unknown call or program id ("missing entry")                      */
+  AUTX_E_EXIST = 3,  /* duplicate call id                                                           */
+  AUTX_E_NOMEM = 4,  /* call table / program table / GPU block pool / host arena full; kvb > P (R14) */
+  AUTX_E_STATE = 5,  /* protocol violation: completing a call that did not run in the last step,
+                        registering after sched_step of the same step, step not increasing        */
+  AUTX_E_CUDA = 6,   /* CUDA runtime error (possibly from earlier asynchronous work)               */
+  AUTX_E_NCCL = 7
+} autx_status;
+
+typedef enum { AUTX_FCFS = 0, AUTX_MLFQ = 1, AUTX_PLAS = 2, AUTX_ATLAS = 3 } autx_policy;
+
+/* Ordering strategy for step a5 (both produce the identical batch: the key is unique).
+ *  AUTX_ORDER_SELECT: top-BS selection over the table kept in (arrival, seq) order.
+ *  AUTX_ORDER_RADIX : full stable LSD radix sort, one byte per digit, of packed 64-bit keys
+ *                     (queue:4 | arrival:27 | not-running:1 | seq:32) over every active call. */
+typedef enum { AUTX_ORDER_SELECT = 0, AUTX_ORDER_RADIX = 1 } autx_order_mode;
+
+#define AUTX_INF 0xFFFFFFFFu /* infinite quantum / budget */
+
+typedef struct {
+  int32_t policy;            /* autx_policy                                                         */
+  uint32_t K;                /* number of queues, 1..16                                     */
+  uint32_t q_hi[15];         /* PLAS/ATLAS entry bounds Q_i^hi, i < K-1, ascending; queue i covers
+                                [q_hi[i-1], q_hi[i]) with q_hi[-1] = 0 and Q_K^hi = inf (R1) */
+  uint32_t quanta[16];       /* per-queue quantum in steps, >= 1; AUTX_INF = infinite (Alg. 1 l.13)   */
+  uint32_t beta_num;         /* anti-starvation threshold beta = beta_num / beta_den    */
+  uint32_t beta_den;         /* 0 -> beta = infinity: never promote (R3)                             */
+  uint32_t max_batch;        /* BS, 1..4096 (P:L184 can_fit)                                          */
+  uint32_t kv_budget_blocks; /* P: KV blocks the batch may hold; AUTX_INF = unbounded (R13, R14)     */
+  uint32_t block_tokens;     /* tokens per KV block (16); kvb(c) = ceil((input+exec+1)/block_tokens) */
+  uint32_t max_calls;        /* call-table rows (active calls + completed holes before compaction)   */
+  uint32_t max_programs;     /* process-table rows                                                   */
+  uint32_t token_threshold;  /* Alg. 2 l.2 short/long threshold (2048)                               */
+  uint32_t order_mode;       /* autx_order_mode                                                      */
+  uint32_t n_gpu_blocks;     /* GPU KV pool size in blocks; 0 disables the block allocator/swap      */
+  uint32_t max_blocks_per_call; /* block-table width per resident call                              */
+  uint64_t host_pages;       /* host swap arena size in logical blocks (pages)                       */
+  int32_t device;            /* CUDA device ordinal                                                  */
+  void* stream;              /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL =
+                                the library creates its own non-blocking stream                      */
+  int32_t rank, nranks;      /* engine id and engine count (routing)                                 */
+} autx_config;
+
+/* One arriving LLM call (Alg. 1 l.9).  Arrays of these must be in canonical order
+ * (arrival_step, program_arrival_step, program_id, call_id); arrival_step must equal
+ * the step of the next autx_sched_step.  input_tokens = full input context (drives kvb and
+ * Alg. 2's LEN, R21). */
+typedef struct {
+  uint64_t call_id;
+  uint64_t program_id;
+  uint32_t arrival_step;
+  uint32_t program_arrival_step;
+  uint32_t input_tokens;
+  uint32_t _pad;
+} autx_call_desc;
+
+/* Result of one scheduling step.  Device lists stay valid until the next autx_sched_step;
+ * the host mirrors (pinned, library-owned) and the counts are valid once `done` (a
+ * cudaEvent_t) has completed — autx_step_wait() waits for it. */
+typedef struct {
+  const uint64_t* batch;       /* device: call ids of the batch, in key order (Alg. 1 l.32-39) */
+  const uint64_t* admit;       /* device: batch calls not resident before this step, batch order */
+  const uint64_t* preempt;     /* device: resident calls not in the batch, previous-batch order  */
+  const uint64_t* h_batch;     /* host mirrors of the three lists                                */
+  const uint64_t* h_admit;
+  const uint64_t* h_preempt;
+  uint32_t n_batch, n_admit, n_preempt, n_active;
+  uint64_t swap_out_blocks;    /* sum over preempt of held blocks ceil((input+exec)/bt)  (R15) */
+  uint64_t swap_in_blocks;     /* sum over admit with a host copy of held blocks               */
+  uint64_t kv_blocks;          /* sum over the batch of kvb                                    */
+  uint32_t n_promoted;         /* anti-starvation promotions this step (diagnostic)            */
+  uint32_t _pad;
+  void* done;                  /* cudaEvent_t recorded after the step's device work            */
+} autx_step_out;
+
+/* Caller-owned paged KV pools (vLLM-style): for layer l, k_pool[l] and
+ * v_pool[l] are device base pointers of [n_gpu_blocks][chunk_bytes] arrays; one (layer, K|V,
+ * block) chunk is chunk_bytes.  host_arena: pinned (cudaHostAlloc / torch pin_memory) buffer
+ * of host_pages * n_layers * 2 * chunk_bytes bytes; a swapped call occupies one contiguous
+ * range laid out [block][layer][K|V][chunk] ("consolidate all KV blocks into a single
+ * contiguous chunk").  Pointer arrays are host arrays read during the call. */
+typedef struct {
+  void* const* k_pool;
+  void* const* v_pool;
+  uint32_t n_layers;
+  uint32_t chunk_bytes;       /* multiple of 16 */
+  void* host_arena;
+  uint64_t host_arena_bytes;
+} autx_kv_layout;
+
+typedef enum { AUTX_SWAP_SM = 0, AUTX_SWAP_PER_CHUNK_MEMCPY = 1, AUTX_SWAP_STAGED_DMA = 2 } autx_swap_mode;
+
+typedef struct {
+  uint64_t bytes_d2h, bytes_h2d;  /* bytes moved over the host link by this call               */
+  uint32_t chunks_d2h, chunks_h2d;
+  float ms;                       /* device time of the swap (CUDA events), valid after return */
+} autx_swap_stats;
+
+/* ---- lifecycle -------------------------------------------------------------------------- */
+autx_status autx_create(const autx_config* cfg, autx_ctx** out);
+autx_status autx_destroy(autx_ctx* ctx);
+const char* autx_last_error(const autx_ctx* ctx);   /* never NULL; "" when no error */
+const char* autx_version(void);
+
+/* ---- per-step calls (host arrays, borrowed for the duration of the call) ------------------ */
+/* start_session: optional explicit program creation; register_call creates on first
+ * sight.  E_EXIST if the program exists. */
+autx_status autx_start_program(autx_ctx* ctx, uint64_t program_id);
+/* end_session: removes the process-table entry.  E_STATE if the program still
+ * has active calls; E_NOENT if unknown. */
+autx_status autx_end_program(autx_ctx* ctx, uint64_t program_id);
+/* Calls that finished decoding in the previous step (Alg. 1 l.16-18, UPDATE_PROCESS_TABLE
+ * l.1-7).  Each must have been in the previous batch (E_STATE) and be known (E_NOENT). Blocks
+ * until the previous step's `done`. */
+autx_status autx_complete(autx_ctx* ctx, const uint64_t* call_ids, uint32_t n);
+/* Arrivals of the current step (Alg. 1 l.9-14), canonical order (E_INVAL otherwise). */
+autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n);
+/* One scheduling step t (Alg. 1 l.15-39): demotion, anti-starvation, ordering, cutoff,
+ * admit/preempt lists, step accounting.  t must increase by >= 1 per call (steps with no
+ * active call may be skipped). */
+autx_status autx_sched_step(autx_ctx* ctx, uint32_t step, autx_step_out* out);
+autx_status autx_step_wait(autx_ctx* ctx, autx_step_out* out);  /* waits for out->done, fills counts */
+
+/* ---- KV swap (a7) --------------------------------------------------------------------- */
+/* Executes the last step's swap plan: swap-out (GPU blocks -> host arena) of every preempted
+ * call, then swap-in (host arena -> newly allocated GPU blocks) of every admitted call with a
+ * host copy.  Requires n_gpu_blocks > 0. */
+autx_status autx_kv_swap(autx_ctx* ctx, const autx_kv_layout* layout, int32_t mode,
+                         autx_swap_stats* stats);
+/* Block table of the last batch as CSR: d_offsets[n_batch+1], d_blocks[...] (device pointers,
+ * valid until the next autx_sched_step). */
+autx_status autx_block_table(autx_ctx* ctx, const uint32_t** d_offsets, const uint32_t** d_blocks);
+/* Host copy of the same CSR: h_offsets[n_batch+1] (capacity max_batch+1), h_blocks[cap]. */
+autx_status autx_block_table_host(autx_ctx* ctx, uint32_t* h_offsets, uint32_t* h_blocks, uint32_t cap,
+                                  uint32_t* n_batch);
+
+/* ---- multi-engine routing (a8, Alg. 2) --------------------------------------------------- */
+/* Routing epoch, split around the caller's all-gather (torch.distributed / NCCL): pack this
+ * engine's epoch record (load = queued + running calls after this step's completions, R21, and
+ * the completion records of this step) into a device buffer of autx_route_record_bytes(), then
+ * after the all-gather of nranks records apply the peers' completion records to the
+ * replicated process table (R22) and route `calls` (replicated, canonical order) with Alg. 2;
+ * engine_out[i] receives the engine of calls[i] (host array); pins are replicated. */
+uint64_t autx_route_record_bytes(const autx_ctx* ctx);
+autx_status autx_route_pack(autx_ctx* ctx, void* d_record);
+autx_status autx_route_apply(autx_ctx* ctx, const void* d_records, const autx_call_desc* calls,
+                             uint32_t n, int32_t* engine_out);
+
+/* ---- introspection for tests and benchmarks -------------------------------------------- */
+typedef struct {
+  uint64_t call_id;
+  uint32_t q, quanta, wait, mtime, exec, totwait, inh, input_tokens, arrival_step, flags;
+} autx_call_state;                 /* flags: 1 running, 2 resident, 4 host copy */
+/* Copies the state of every active call, in (arrival, seq) order, as of the end of the last
+ * sched_step, to a host array of capacity `cap`; *n receives the count. */
+autx_status autx_dump_calls(autx_ctx* ctx, autx_call_state* out, uint32_t cap, uint32_t* n);
+autx_status autx_program_state(autx_ctx* ctx, uint64_t program_id, uint32_t* svc, uint64_t* pwait);
+/* Device-time of the kernels of the last sched_step (CUDA events around each phase). */
+typedef struct { float complete_ms, register_ms, scan_ms, select_ms, finalize_ms, total_ms; } autx_step_timing;
+autx_status autx_last_step_timing(autx_ctx* ctx, autx_step_timing* t);
+autx_status autx_set_timing(autx_ctx* ctx, int32_t on);
+uint32_t autx_num_active(const autx_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUTX_H */

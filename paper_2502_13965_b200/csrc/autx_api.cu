@@ -1,0 +1,885 @@
+// Host side of the autx C ABI (include/autx.h): context, id maps, protocol checks, staging.
+// All scheduling arithmetic runs in the sm_100a kernels (sched_kernels.cu, swap_kernels.cu);
+// this file only validates, maps 64-bit ids to table rows, stages records in pinned memory
+// and launches.
+#include <algorithm>
+#include <cstdarg>
+#include <cstddef>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/autx.h"
+#include "autx_internal.cuh"
+
+using namespace autx;
+
+struct autx_ctx {
+  autx_config cfg{};
+  Policy pol{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  CallTable ct{};
+  ProgTable pt{};
+  Ctl* ctl = nullptr;
+  Outputs out{};
+  KvState kv{};
+  bool kv_on = false;
+  // pinned staging (device reads it through UVA)
+  uint32_t* h_cslots = nullptr;  // [max_batch * 4] completion slots
+  uint32_t cslots_cap = 0;
+  ArrivalRec* h_arr = nullptr;
+  uint32_t arr_cap = 0;
+  uint32_t* d_cslots = nullptr;
+  ArrivalRec* d_arr = nullptr;
+  // host-side maps
+  std::unordered_map<uint64_t, uint32_t> call_slot;   // active call id -> row
+  std::unordered_map<uint64_t, uint32_t> prog_row;    // program id -> process-table row
+  std::vector<uint32_t> prog_free;
+  uint32_t prog_next = 0;
+  std::vector<uint32_t> prog_active;                  // active calls per program row
+  std::vector<uint32_t> slot_prog;                    // row -> program row (host mirror)
+  std::unordered_set<uint64_t> last_batch;
+  bool last_batch_valid = false;
+  uint32_t tail = 0;
+  // protocol state
+  bool stepped = false;       // at least one sched_step done
+  uint32_t t_last = 0;        // last step scheduled
+  bool pending_done = false;  // a sched_step whose `done` was not waited on
+  uint32_t pend_t = 0;        // step the pending records belong to (0 = unset)
+  bool pend_set = false;
+  bool completed_this = false, registered_this = false;
+  uint32_t n_completed_pending = 0;
+  uint64_t last_key[4] = {0, 0, 0, 0};
+  bool have_last_key = false;
+  uint32_t seqno = 0;
+  cudaEvent_t done = nullptr;
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  autx_step_timing last_timing{};
+  // kv swap scratch
+  void** d_pools = nullptr;  // [2 * n_layers]
+  uint32_t pools_cap = 0;
+  void** h_pools = nullptr;
+  char* staging = nullptr;
+  size_t staging_bytes = 0;
+  cudaEvent_t sev[2] = {};
+  // routing epoch (a8)
+  char* d_route_local = nullptr;   // RouteHdr + max_batch CompRec: this step's completion records
+  RouteHdr* h_hdr = nullptr;       // pinned staging for the header
+  int8_t* d_pin = nullptr;         // [max_programs] Alg. 2 pin table (-1 = none)
+  RouteArr* h_rarr = nullptr;
+  RouteArr* d_rarr = nullptr;
+  int32_t* d_rout = nullptr;
+  uint32_t rarr_cap = 0;
+  bool routed_this = false;
+  uint32_t n_reg_this = 0;
+  std::string err;
+};
+
+static autx_status fail(autx_ctx* c, autx_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(ctx, AUTX_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                            \
+  } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t n) {
+  return cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+}
+
+extern "C" const char* autx_version(void) { return "autx 0.1 (sm_100a)"; }
+
+extern "C" const char* autx_last_error(const autx_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+static autx_status alloc_tables(autx_ctx* ctx) {
+  const autx_config& c = ctx->cfg;
+  size_t rows = ((size_t)c.max_calls + TILE - 1) / TILE * TILE;  // padded to whole tiles
+  CallTable& t = ctx->ct;
+  CK(dalloc(&t.cid, rows)); CK(dalloc(&t.prog, rows)); CK(dalloc(&t.arr, rows));
+  CK(dalloc(&t.qf, rows)); CK(dalloc(&t.base, rows)); CK(dalloc(&t.mtime, rows));
+  CK(dalloc(&t.exec, rows)); CK(dalloc(&t.quanta, rows)); CK(dalloc(&t.inh, rows));
+  CK(dalloc(&t.tok, rows)); CK(dalloc(&t.loc, rows)); CK(dalloc(&t.hcls, rows));
+  CK(cudaMemsetAsync(t.qf, QF_DEAD, rows, ctx->stream));
+  CK(cudaMemsetAsync(t.prog, 0, rows * 4, ctx->stream));
+  CK(cudaMemsetAsync(t.base, 0, rows * 4, ctx->stream));
+  CK(cudaMemsetAsync(t.mtime, 0, rows * 4, ctx->stream));
+  ProgTable& p = ctx->pt;
+  size_t P = std::max<uint32_t>(c.max_programs, 1);
+  CK(dalloc(&p.svc, P)); CK(dalloc(&p.pwait, P)); CK(dalloc(&p.last_arr, P)); CK(dalloc(&p.last_comp, P));
+  CK(cudaMemsetAsync(p.svc, 0, P * 4, ctx->stream));
+  CK(cudaMemsetAsync(p.pwait, 0, P * 8, ctx->stream));
+  CK(dalloc(&ctx->ctl, 1));
+  CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
+  Outputs& o = ctx->out;
+  uint32_t BS = c.max_batch;
+  size_t ntiles = rows / TILE + 1;
+  CK(dalloc(&o.batch_slots, BS)); CK(dalloc(&o.batch_ids, BS)); CK(dalloc(&o.admit_ids, BS));
+  CK(dalloc(&o.preempt_ids, BS)); CK(dalloc(&o.prev_slots, BS)); CK(dalloc(&o.preempt_slots, BS));
+  CK(dalloc(&o.admit_slots, BS));
+  o.cand_cap = 2 * BS;
+  CK(dalloc(&o.cand, o.cand_cap));
+  CK(dalloc(&o.tile_cnt, ntiles * MAX_K)); CK(dalloc(&o.tile_off, ntiles + 1));
+  CK(dalloc(&o.tile_pre, ntiles + 1));
+  CK(cudaHostAlloc((void**)&o.hout, sizeof(HostOut), cudaHostAllocMapped));
+  CK(cudaHostAlloc((void**)&o.h_batch, BS * 8, cudaHostAllocMapped));
+  CK(cudaHostAlloc((void**)&o.h_admit, BS * 8, cudaHostAllocMapped));
+  CK(cudaHostAlloc((void**)&o.h_preempt, BS * 8, cudaHostAllocMapped));
+  memset(o.hout, 0, sizeof(HostOut));
+  ctx->cslots_cap = 4 * BS;
+  CK(cudaHostAlloc((void**)&ctx->h_cslots, ctx->cslots_cap * 4, cudaHostAllocMapped));
+  ctx->arr_cap = 4 * BS;
+  CK(cudaHostAlloc((void**)&ctx->h_arr, ctx->arr_cap * sizeof(ArrivalRec), cudaHostAllocMapped));
+  CK(dalloc(&ctx->d_cslots, ctx->cslots_cap));
+  CK(dalloc(&ctx->d_arr, ctx->arr_cap));
+  CK(dalloc(&ctx->d_route_local, sizeof(RouteHdr) + (size_t)BS * sizeof(CompRec)));
+  CK(cudaMemsetAsync(ctx->d_route_local, 0, sizeof(RouteHdr), ctx->stream));
+  CK(cudaHostAlloc((void**)&ctx->h_hdr, sizeof(RouteHdr), 0));
+  CK(dalloc(&ctx->d_pin, P));
+  CK(cudaMemsetAsync(ctx->d_pin, 0xff, P, ctx->stream));
+  ctx->prog_active.assign(P, 0);
+  ctx->slot_prog.assign(rows, 0);
+  // KV block allocator
+  if (c.n_gpu_blocks > 0) {
+    CK(cudaStreamSynchronize(ctx->stream));  // the async memsets above precede the copies below
+    ctx->kv_on = true;
+    KvState& kv = ctx->kv;
+    uint32_t W = c.max_blocks_per_call;
+    CK(dalloc(&kv.free_stack, c.n_gpu_blocks));
+    CK(dalloc(&kv.rs_free, BS)); CK(dalloc(&kv.rs_nblk, BS));
+    CK(dalloc(&kv.rs_blocks, (size_t)BS * W));
+    CK(cudaMemsetAsync(kv.rs_nblk, 0, BS * 4, ctx->stream));
+    // free stacks: block ids n-1..0 so that pops hand out 0,1,2,... first
+    std::vector<uint32_t> fs(c.n_gpu_blocks), rs(BS);
+    for (uint32_t i = 0; i < c.n_gpu_blocks; ++i) fs[i] = c.n_gpu_blocks - 1 - i;
+    for (uint32_t i = 0; i < BS; ++i) rs[i] = BS - 1 - i;
+    CK(cudaMemcpy(kv.free_stack, fs.data(), fs.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(kv.rs_free, rs.data(), rs.size() * 4, cudaMemcpyHostToDevice));
+    uint64_t hp = std::min<uint64_t>(c.host_pages, 0xFFFFFFF0ull);
+    kv.host_free_cap = (uint32_t)std::max<uint64_t>(hp, 1);
+    CK(dalloc(&kv.host_free, (size_t)32 * kv.host_free_cap));
+    CK(dalloc(&kv.plan_out, BS)); CK(dalloc(&kv.plan_in, BS));
+    kv.plan_cap = c.n_gpu_blocks;
+    CK(dalloc(&kv.plan_out_blocks, kv.plan_cap)); CK(dalloc(&kv.plan_in_blocks, kv.plan_cap));
+    CK(dalloc(&kv.bt_offsets, BS + 1)); CK(dalloc(&kv.bt_blocks, kv.plan_cap));
+    Ctl init{};
+    memset(&init, 0, sizeof init);
+    init.free_top = c.n_gpu_blocks;
+    init.rs_free_top = BS;
+    CK(cudaMemcpy(ctx->ctl, &init, sizeof init, cudaMemcpyHostToDevice));
+  }
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
+  if (!cfg || !outp) return AUTX_E_INVAL;
+  *outp = nullptr;
+  autx_ctx* ctx = new autx_ctx();
+  const autx_config& c = *cfg;
+  auto bad = [&](const char* m) {
+    autx_status s = fail(ctx, AUTX_E_INVAL, "config: %s", m);
+    fprintf(stderr, "autx_create: %s\n", ctx->err.c_str());
+    delete ctx;
+    return s;
+  };
+  if (c.policy < AUTX_FCFS || c.policy > AUTX_ATLAS) return bad("policy");
+  if (c.K < 1 || c.K > 16) return bad("K must be 1..16");
+  for (uint32_t i = 0; i + 1 < c.K; ++i) {
+    if (i > 0 && c.q_hi[i] < c.q_hi[i - 1]) return bad("q_hi must be ascending");
+  }
+  for (uint32_t i = 0; i < c.K; ++i)
+    if (c.quanta[i] == 0) return bad("quanta must be >= 1");
+  if (c.max_batch < 1 || c.max_batch > 4096) return bad("max_batch must be 1..4096");
+  if (c.block_tokens < 1) return bad("block_tokens");
+  if (c.max_calls < 1 || c.max_programs < 1) return bad("capacities");
+  if (c.max_calls > 0x7FFFFFFFu) return bad("max_calls too large");
+  if (c.n_gpu_blocks > 0 && (c.max_blocks_per_call < 1 || c.host_pages < 1))
+    return bad("n_gpu_blocks needs max_blocks_per_call and host_pages");
+  if (c.n_gpu_blocks > 0 && c.kv_budget_blocks != AUTX_INF && c.kv_budget_blocks > c.n_gpu_blocks)
+    return bad("kv_budget_blocks exceeds n_gpu_blocks");
+  if (c.order_mode != AUTX_ORDER_SELECT && c.order_mode != AUTX_ORDER_RADIX) return bad("order_mode");
+  ctx->cfg = c;
+  Policy& p = ctx->pol;
+  p.policy = c.policy;
+  p.K = c.K;
+  memcpy(p.q_hi, c.q_hi, sizeof p.q_hi);
+  memcpy(p.quanta, c.quanta, sizeof p.quanta);
+  p.beta_num = c.beta_num;
+  p.beta_den = c.beta_den;
+  p.max_batch = c.max_batch;
+  p.kv_budget = c.kv_budget_blocks;
+  p.block_tokens = c.block_tokens;
+  p.n_gpu_blocks = c.n_gpu_blocks;
+  p.max_blocks_per_call = c.max_blocks_per_call;
+  p.host_pages_lo = (uint32_t)std::min<uint64_t>(c.host_pages, 0xFFFFFFF0ull);
+  ctx->device = c.device;
+  if (cudaSetDevice(c.device) != cudaSuccess) {
+    autx_status s = fail(ctx, AUTX_E_CUDA, "cudaSetDevice(%d) failed", c.device);
+    delete ctx;
+    return s;
+  }
+  if (c.stream) {
+    ctx->stream = (cudaStream_t)c.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return AUTX_E_CUDA;
+    }
+    ctx->own_stream = true;
+  }
+  autx_status s = alloc_tables(ctx);
+  if (s == AUTX_OK) {
+    if (cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming) != cudaSuccess) s = AUTX_E_CUDA;
+    for (auto& e : ctx->ev) cudaEventCreate(&e);
+    for (auto& e : ctx->sev) cudaEventCreate(&e);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) s = fail(ctx, AUTX_E_CUDA, "init sync");
+  }
+  if (s != AUTX_OK) {
+    fprintf(stderr, "autx_create: %s\n", ctx->err.c_str());
+    autx_destroy(ctx);
+    return s;
+  }
+  *outp = ctx;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_destroy(autx_ctx* ctx) {
+  if (!ctx) return AUTX_E_INVAL;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  CallTable& t = ctx->ct;
+  void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
+                 t.loc, t.hcls, ctx->pt.svc, ctx->pt.pwait, ctx->pt.last_arr, ctx->pt.last_comp,
+                 ctx->ctl, ctx->out.batch_slots, ctx->out.batch_ids, ctx->out.admit_ids,
+                 ctx->out.preempt_ids, ctx->out.prev_slots, ctx->out.preempt_slots,
+                 ctx->out.admit_slots, ctx->out.cand, ctx->out.tile_cnt, ctx->out.tile_off,
+                 ctx->out.tile_pre, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
+                 ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
+                 ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
+                 ctx->kv.bt_offsets, ctx->kv.bt_blocks, ctx->d_pools, ctx->staging,
+                 ctx->d_route_local, ctx->d_pin, ctx->d_rarr, ctx->d_rout};
+  for (void* p : dev) if (p) cudaFree(p);
+  void* host[] = {ctx->out.hout, ctx->out.h_batch, ctx->out.h_admit, ctx->out.h_preempt,
+                  ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr};
+  for (void* p : host) if (p) cudaFreeHost(p);
+  if (ctx->done) cudaEventDestroy(ctx->done);
+  for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->sev) if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return AUTX_OK;
+}
+
+// Wait for the last step and make its batch available to the host-side protocol checks.
+static autx_status sync_last(autx_ctx* ctx) {
+  if (ctx->pending_done) {
+    CK(cudaEventSynchronize(ctx->done));
+    ctx->pending_done = false;
+  }
+  if (!ctx->last_batch_valid) {
+    ctx->last_batch.clear();
+    if (ctx->stepped) {
+      const HostOut& h = *ctx->out.hout;
+      if (h.err) return fail(ctx, (autx_status)h.err, "device error %u in step %u", h.err, ctx->t_last);
+      for (uint32_t i = 0; i < h.n_batch; ++i) ctx->last_batch.insert(ctx->out.h_batch[i]);
+    }
+    ctx->last_batch_valid = true;
+  }
+  return AUTX_OK;
+}
+
+static uint32_t next_step(const autx_ctx* ctx) { return ctx->stepped ? ctx->t_last + 1 : 0; }
+
+// Creates a process-table entry (session start): zeroed service/wait, no pin.
+static autx_status new_program(autx_ctx* ctx, uint64_t pid, uint32_t* row_out) {
+  uint32_t row;
+  if (!ctx->prog_free.empty()) { row = ctx->prog_free.back(); ctx->prog_free.pop_back(); }
+  else if (ctx->prog_next < ctx->cfg.max_programs) row = ctx->prog_next++;
+  else return fail(ctx, AUTX_E_NOMEM, "process table full (%u programs)", ctx->cfg.max_programs);
+  ctx->prog_row[pid] = row;
+  ctx->prog_active[row] = 0;
+  // zero the entry (stream-ordered before any later kernel reads it)
+  CK(cudaMemsetAsync(ctx->pt.svc + row, 0, 4, ctx->stream));
+  CK(cudaMemsetAsync(ctx->pt.pwait + row, 0, 8, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_pin + row, 0xff, 1, ctx->stream));
+  if (row_out) *row_out = row;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_start_program(autx_ctx* ctx, uint64_t pid) {
+  if (!ctx) return AUTX_E_INVAL;
+  if (ctx->prog_row.count(pid)) return fail(ctx, AUTX_E_EXIST, "program %llu exists", (unsigned long long)pid);
+  return new_program(ctx, pid, nullptr);
+}
+
+extern "C" autx_status autx_end_program(autx_ctx* ctx, uint64_t pid) {
+  if (!ctx) return AUTX_E_INVAL;
+  auto it = ctx->prog_row.find(pid);
+  if (it == ctx->prog_row.end()) return fail(ctx, AUTX_E_NOENT, "unknown program %llu", (unsigned long long)pid);
+  if (ctx->prog_active[it->second] != 0)
+    return fail(ctx, AUTX_E_STATE, "program %llu still has %u active calls", (unsigned long long)pid,
+                ctx->prog_active[it->second]);
+  ctx->prog_free.push_back(it->second);
+  ctx->prog_row.erase(it);
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_t n) {
+  if (!ctx || (n && !ids)) return AUTX_E_INVAL;
+  if (n == 0) return AUTX_OK;
+  autx_status s = sync_last(ctx);
+  if (s) return s;
+  if (ctx->registered_this)
+    return fail(ctx, AUTX_E_STATE, "autx_complete after autx_register_call in the same step");
+  if (ctx->completed_this)
+    return fail(ctx, AUTX_E_STATE, "autx_complete called twice in one step");
+  if (n > ctx->cfg.max_batch) return fail(ctx, AUTX_E_INVAL, "too many completions (%u)", n);
+  if (ctx->routed_this) return fail(ctx, AUTX_E_STATE, "autx_complete after autx_route_apply");
+  // validate everything before mutating anything
+  std::unordered_set<uint64_t> seen;
+  for (uint32_t i = 0; i < n; ++i) {
+    auto it = ctx->call_slot.find(ids[i]);
+    if (it == ctx->call_slot.end()) return fail(ctx, AUTX_E_NOENT, "unknown call %llu", (unsigned long long)ids[i]);
+    if (!ctx->last_batch.count(ids[i]))
+      return fail(ctx, AUTX_E_STATE, "call %llu did not run in step %u", (unsigned long long)ids[i], ctx->t_last);
+    if (!seen.insert(ids[i]).second) return fail(ctx, AUTX_E_INVAL, "duplicate completion");
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    auto it = ctx->call_slot.find(ids[i]);
+    uint32_t slot = it->second;
+    ctx->h_cslots[i] = slot;
+    ctx->prog_active[ctx->slot_prog[slot]] -= 1;
+    ctx->call_slot.erase(it);
+    ctx->last_batch.erase(ids[i]);
+  }
+  uint32_t t = next_step(ctx);
+  CK(cudaMemcpyAsync(ctx->d_cslots, ctx->h_cslots, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
+  CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
+  CK(launch_complete(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->d_cslots, n, t, ctx->kv,
+                     ctx->kv_on, recs, ctx->cfg.nranks <= 1));
+  if (ctx->timing) cudaEventRecord(ctx->ev[5], ctx->stream);
+  ctx->completed_this = true;
+  ctx->n_completed_pending = n;
+  return AUTX_OK;
+}
+
+static autx_status compact(autx_ctx* ctx);
+
+extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n) {
+  if (!ctx || (n && !calls)) return AUTX_E_INVAL;
+  if (n == 0) return AUTX_OK;
+  autx_status s = sync_last(ctx);
+  if (s) return s;
+  const uint32_t t = calls[0].arrival_step;
+  if (t < next_step(ctx)) return fail(ctx, AUTX_E_INVAL, "arrival_step %u is in the past", t);
+  if (!ctx->call_slot.empty() && t != next_step(ctx))
+    return fail(ctx, AUTX_E_STATE, "steps may only be skipped when no call is active");
+  if (ctx->completed_this && t != next_step(ctx))
+    return fail(ctx, AUTX_E_STATE, "arrivals after completions must be for step %u", next_step(ctx));
+  if (ctx->pend_set && ctx->pend_t != t) return fail(ctx, AUTX_E_INVAL, "arrivals of two steps in one batch");
+  // validate: canonical order, uniqueness, capacities, kvb <= P (R13)
+  std::unordered_map<uint64_t, int> new_prog_seen;
+  uint32_t new_progs = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const autx_call_desc& d = calls[i];
+    if (d.arrival_step != t) return fail(ctx, AUTX_E_INVAL, "mixed arrival steps in one batch");
+    uint64_t key[4] = {d.arrival_step, d.program_arrival_step, d.program_id, d.call_id};
+    const uint64_t* prev = ctx->have_last_key ? ctx->last_key : nullptr;
+    if (i > 0) {
+      const autx_call_desc& q = calls[i - 1];
+      uint64_t pk[4] = {q.arrival_step, q.program_arrival_step, q.program_id, q.call_id};
+      prev = nullptr;
+      if (!std::lexicographical_compare(pk, pk + 4, key, key + 4))
+        return fail(ctx, AUTX_E_INVAL, "arrivals not in canonical order at index %u", i);
+    } else if (prev && ctx->pend_set) {
+      if (!std::lexicographical_compare(prev, prev + 4, key, key + 4))
+        return fail(ctx, AUTX_E_INVAL, "arrivals not in canonical order across calls");
+    }
+    if (ctx->call_slot.count(d.call_id)) return fail(ctx, AUTX_E_EXIST, "duplicate call %llu", (unsigned long long)d.call_id);
+    if (i > 0 && calls[i - 1].call_id == d.call_id) return fail(ctx, AUTX_E_EXIST, "duplicate call");
+    uint64_t kvb0 = ((uint64_t)d.input_tokens + 1 + ctx->cfg.block_tokens - 1) / ctx->cfg.block_tokens;
+    if (ctx->cfg.kv_budget_blocks != AUTX_INF && kvb0 > ctx->cfg.kv_budget_blocks)
+      return fail(ctx, AUTX_E_INVAL, "call %llu needs %llu KV blocks > budget %u", (unsigned long long)d.call_id,
+                  (unsigned long long)kvb0, ctx->cfg.kv_budget_blocks);
+    if (!ctx->prog_row.count(d.program_id) && !new_prog_seen.count(d.program_id)) {
+      new_prog_seen[d.program_id] = 1;
+      ++new_progs;
+    }
+  }
+  if (ctx->prog_free.size() + (ctx->cfg.max_programs - ctx->prog_next) < new_progs)
+    return fail(ctx, AUTX_E_NOMEM, "process table full");
+  if ((uint64_t)ctx->call_slot.size() + n > ctx->cfg.max_calls)
+    return fail(ctx, AUTX_E_NOMEM, "call table full (%u active)", (unsigned)ctx->call_slot.size());
+  if ((uint64_t)ctx->tail + n > ctx->cfg.max_calls) {
+    s = compact(ctx);
+    if (s) return s;
+  }
+  // staging buffer growth for bulk registration
+  if (n > ctx->arr_cap) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFreeHost(ctx->h_arr);
+    cudaFree(ctx->d_arr);
+    ctx->arr_cap = n;
+    CK(cudaHostAlloc((void**)&ctx->h_arr, (size_t)n * sizeof(ArrivalRec), cudaHostAllocMapped));
+    CK(dalloc(&ctx->d_arr, n));
+  } else if (ctx->registered_this) {
+    // the previous registration of this step may still be reading the staging buffer
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  // map program ids, build records
+  std::unordered_set<uint64_t> first_done;
+  for (uint32_t i = 0; i < n; ++i) {
+    const autx_call_desc& d = calls[i];
+    uint32_t flags = 0;
+    auto it = ctx->prog_row.find(d.program_id);
+    uint32_t row;
+    if (it == ctx->prog_row.end()) {
+      if (!ctx->prog_free.empty()) { row = ctx->prog_free.back(); ctx->prog_free.pop_back(); }
+      else row = ctx->prog_next++;
+      ctx->prog_row[d.program_id] = row;
+      ctx->prog_active[row] = 0;
+      CK(cudaMemsetAsync(ctx->d_pin + row, 0xff, 1, ctx->stream));
+      flags = 3;  // new program, first record
+      first_done.insert(d.program_id);
+    } else {
+      row = it->second;
+      if (new_prog_seen.count(d.program_id)) flags = 1;  // new in this batch, not first
+    }
+    ArrivalRec r{};
+    r.cid = d.call_id;
+    r.prog = row;
+    r.tok = d.input_tokens;
+    r.flags = flags;
+    ctx->h_arr[i] = r;
+    uint32_t slot = ctx->tail + i;
+    ctx->call_slot[d.call_id] = slot;
+    ctx->slot_prog[slot] = row;
+    ctx->prog_active[row] += 1;
+  }
+  const autx_call_desc& l = calls[n - 1];
+  ctx->last_key[0] = l.arrival_step; ctx->last_key[1] = l.program_arrival_step;
+  ctx->last_key[2] = l.program_id; ctx->last_key[3] = l.call_id;
+  ctx->have_last_key = true;
+  CK(cudaMemcpyAsync(ctx->d_arr, ctx->h_arr, (size_t)n * sizeof(ArrivalRec), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  if (ctx->timing) cudaEventRecord(ctx->ev[6], ctx->stream);
+  CK(launch_register(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->d_arr, n, ctx->tail, t));
+  if (ctx->timing) cudaEventRecord(ctx->ev[7], ctx->stream);
+  ctx->tail += n;
+  ctx->n_reg_this += n;
+  ctx->registered_this = true;
+  ctx->pend_set = true;
+  ctx->pend_t = t;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out* out) {
+  if (!ctx || !out) return AUTX_E_INVAL;
+  autx_status s = sync_last(ctx);
+  if (s) return s;
+  if (ctx->stepped && t <= ctx->t_last) return fail(ctx, AUTX_E_STATE, "step %u <= last step %u", t, ctx->t_last);
+  if (ctx->pend_set && ctx->pend_t != t)
+    return fail(ctx, AUTX_E_STATE, "registered arrivals are for step %u, not %u", ctx->pend_t, t);
+  if (ctx->completed_this && t != next_step(ctx))
+    return fail(ctx, AUTX_E_STATE, "completions are processed at step %u, not %u", next_step(ctx), t);
+  if (ctx->stepped && t != ctx->t_last + 1 && ctx->call_slot.size() > ctx->n_reg_this)
+    return fail(ctx, AUTX_E_STATE, "cannot skip steps while calls are active");
+  if (ctx->cfg.nranks > 1 && !ctx->routed_this)
+    return fail(ctx, AUTX_E_STATE, "multi-engine: autx_route_apply must run every step");
+  ++ctx->seqno;
+  CK(launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv, ctx->kv_on, t,
+                 ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr));
+  CK(cudaEventRecord(ctx->done, ctx->stream));
+  ctx->pending_done = true;
+  ctx->last_batch_valid = false;
+  ctx->stepped = true;
+  ctx->t_last = t;
+  ctx->pend_set = false;
+  ctx->completed_this = ctx->registered_this = false;
+  ctx->routed_this = false;
+  ctx->n_reg_this = 0;
+  ctx->n_completed_pending = 0;
+  ctx->have_last_key = false;
+  memset(out, 0, sizeof *out);
+  out->batch = ctx->out.batch_ids;
+  out->admit = ctx->out.admit_ids;
+  out->preempt = ctx->out.preempt_ids;
+  out->h_batch = ctx->out.h_batch;
+  out->h_admit = ctx->out.h_admit;
+  out->h_preempt = ctx->out.h_preempt;
+  out->done = (void*)ctx->done;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_step_wait(autx_ctx* ctx, autx_step_out* out) {
+  if (!ctx || !out) return AUTX_E_INVAL;
+  autx_status s = sync_last(ctx);
+  if (s) return s;
+  const HostOut& h = *ctx->out.hout;
+  if (h.seqno != ctx->seqno) return fail(ctx, AUTX_E_CUDA, "step output sequence mismatch");
+  out->n_batch = h.n_batch;
+  out->n_admit = h.n_admit;
+  out->n_preempt = h.n_preempt;
+  out->n_active = h.n_active;
+  out->swap_out_blocks = h.swap_out_blocks;
+  out->swap_in_blocks = h.swap_in_blocks;
+  out->kv_blocks = h.kv_blocks;
+  out->n_promoted = h.n_promoted;
+  if (ctx->timing) {
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+    ctx->last_timing.scan_ms = a;
+    ctx->last_timing.select_ms = b;
+    ctx->last_timing.finalize_ms = c;
+    ctx->last_timing.total_ms = a + b + c;
+  }
+  return AUTX_OK;
+}
+
+// G8: stable compaction.  Live rows in table order are exactly the active calls sorted by row.
+static autx_status compact(autx_ctx* ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::vector<std::pair<uint32_t, uint64_t>> live;
+  live.reserve(ctx->call_slot.size());
+  for (auto& kv : ctx->call_slot) live.emplace_back(kv.second, kv.first);
+  std::sort(live.begin(), live.end());
+  uint32_t n = (uint32_t)live.size();
+  std::vector<uint32_t> lv(n), old2new(std::max<uint32_t>(ctx->tail, 1), NONE);
+  for (uint32_t i = 0; i < n; ++i) {
+    lv[i] = live[i].first;
+    old2new[lv[i]] = i;
+  }
+  size_t rows = ((size_t)ctx->cfg.max_calls + TILE - 1) / TILE * TILE;
+  CallTable tmp{};
+  CK(dalloc(&tmp.cid, n)); CK(dalloc(&tmp.prog, n)); CK(dalloc(&tmp.arr, n)); CK(dalloc(&tmp.qf, n));
+  CK(dalloc(&tmp.base, n)); CK(dalloc(&tmp.mtime, n)); CK(dalloc(&tmp.exec, n));
+  CK(dalloc(&tmp.quanta, n)); CK(dalloc(&tmp.inh, n)); CK(dalloc(&tmp.tok, n)); CK(dalloc(&tmp.loc, n));
+  CK(dalloc(&tmp.hcls, n));
+  uint32_t *d_live = nullptr, *d_map = nullptr;
+  CK(dalloc(&d_live, n));
+  CK(dalloc(&d_map, old2new.size()));
+  CK(cudaMemcpy(d_live, lv.data(), (size_t)n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_map, old2new.data(), old2new.size() * 4, cudaMemcpyHostToDevice));
+  CK(launch_compact(ctx->stream, ctx->ct, tmp, d_live, n));
+  CallTable& t = ctx->ct;
+  auto cp = [&](void* dst, void* src, size_t bytes) { return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream); };
+  CK(cp(t.cid, tmp.cid, (size_t)n * 8)); CK(cp(t.prog, tmp.prog, (size_t)n * 4)); CK(cp(t.arr, tmp.arr, (size_t)n * 4));
+  CK(cp(t.qf, tmp.qf, n)); CK(cp(t.base, tmp.base, (size_t)n * 4)); CK(cp(t.mtime, tmp.mtime, (size_t)n * 4));
+  CK(cp(t.exec, tmp.exec, (size_t)n * 4)); CK(cp(t.quanta, tmp.quanta, (size_t)n * 4));
+  CK(cp(t.inh, tmp.inh, (size_t)n * 4)); CK(cp(t.tok, tmp.tok, (size_t)n * 4)); CK(cp(t.loc, tmp.loc, (size_t)n * 4));
+  CK(cp(t.hcls, tmp.hcls, (size_t)n * 4));
+  CK(cudaMemsetAsync(t.qf + n, QF_DEAD, rows - n, ctx->stream));
+  // remap the previous batch (its completed rows were DEAD and are gone from the list: the
+  // previous batch entries that are not live map to NONE and must be dropped)
+  HostOut h = *ctx->out.hout;
+  std::vector<uint32_t> prev(h.n_batch);
+  CK(cudaMemcpyAsync(prev.data(), ctx->out.prev_slots, (size_t)h.n_batch * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::vector<uint32_t> np;
+  for (uint32_t s : prev) if (s < old2new.size() && old2new[s] != NONE) np.push_back(old2new[s]);
+  if (!np.empty()) CK(cudaMemcpy(ctx->out.prev_slots, np.data(), np.size() * 4, cudaMemcpyHostToDevice));
+  uint32_t npv = (uint32_t)np.size();
+  CK(cudaMemcpy(reinterpret_cast<char*>(ctx->ctl) + offsetof(Ctl, n_prev), &npv, 4, cudaMemcpyHostToDevice));
+  for (auto& kv : ctx->call_slot) kv.second = old2new[kv.second];
+  std::vector<uint32_t> sp(rows, 0);
+  for (uint32_t i = 0; i < n; ++i) sp[i] = ctx->slot_prog[lv[i]];
+  ctx->slot_prog.swap(sp);
+  ctx->tail = n;
+  void* f[] = {tmp.cid, tmp.prog, tmp.arr, tmp.qf, tmp.base, tmp.mtime, tmp.exec, tmp.quanta, tmp.inh,
+               tmp.tok, tmp.loc, tmp.hcls, d_live, d_map};
+  for (void* p : f) cudaFree(p);
+  return AUTX_OK;
+}
+
+// ---- KV swap ------------------------------------------------------------------------------
+extern "C" autx_status autx_kv_swap(autx_ctx* ctx, const autx_kv_layout* L, int32_t mode,
+                                    autx_swap_stats* stats) {
+  if (!ctx || !L || !stats) return AUTX_E_INVAL;
+  if (!ctx->kv_on) return fail(ctx, AUTX_E_INVAL, "KV allocator disabled (n_gpu_blocks == 0)");
+  if (L->chunk_bytes % 16 || L->n_layers == 0 || !L->host_arena)
+    return fail(ctx, AUTX_E_INVAL, "bad kv layout");
+  uint64_t page = (uint64_t)L->n_layers * 2 * L->chunk_bytes;
+  if (L->host_arena_bytes < ctx->cfg.host_pages * page)
+    return fail(ctx, AUTX_E_INVAL, "host arena smaller than host_pages * page bytes");
+  autx_status s = sync_last(ctx);
+  if (s) return s;
+  if (2 * L->n_layers > ctx->pools_cap) {
+    if (ctx->d_pools) cudaFree(ctx->d_pools);
+    if (ctx->h_pools) cudaFreeHost(ctx->h_pools);
+    ctx->pools_cap = 2 * L->n_layers;
+    CK(dalloc(&ctx->d_pools, ctx->pools_cap));
+    CK(cudaHostAlloc((void**)&ctx->h_pools, ctx->pools_cap * sizeof(void*), 0));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));  // h_pools reuse
+  for (uint32_t l = 0; l < L->n_layers; ++l) {
+    ctx->h_pools[l] = L->k_pool[l];
+    ctx->h_pools[L->n_layers + l] = L->v_pool[l];
+  }
+  CK(cudaMemcpyAsync(ctx->d_pools, ctx->h_pools, 2 * L->n_layers * sizeof(void*), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  Ctl c;
+  CK(cudaMemcpyAsync(&c, ctx->ctl, sizeof c, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  memset(stats, 0, sizeof *stats);
+  stats->bytes_d2h = (uint64_t)c.plan_out_chunks * page;
+  stats->bytes_h2d = (uint64_t)c.plan_in_chunks * page;
+  stats->chunks_d2h = c.plan_out_chunks * L->n_layers * 2;
+  stats->chunks_h2d = c.plan_in_chunks * L->n_layers * 2;
+  void** kp = ctx->d_pools;
+  void** vp = ctx->d_pools + L->n_layers;
+  char* arena = (char*)L->host_arena;
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  CK(cudaEventRecord(ctx->sev[0], ctx->stream));
+  if (mode == AUTX_SWAP_SM) {
+    if (c.plan_out_chunks) CK(launch_swap(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, arena, 0, dev_sms * 4));
+    if (c.plan_in_chunks) CK(launch_swap(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, arena, 1, dev_sms * 4));
+  } else if (mode == AUTX_SWAP_PER_CHUNK_MEMCPY || mode == AUTX_SWAP_STAGED_DMA) {
+    // both comparators need the plan on the host
+    std::vector<PlanItem> po(c.n_plan_out), pi(c.n_plan_in);
+    std::vector<uint32_t> bo(c.plan_out_chunks), bi(c.plan_in_chunks);
+    if (c.n_plan_out) CK(cudaMemcpy(po.data(), ctx->kv.plan_out, po.size() * sizeof(PlanItem), cudaMemcpyDeviceToHost));
+    if (c.n_plan_in) CK(cudaMemcpy(pi.data(), ctx->kv.plan_in, pi.size() * sizeof(PlanItem), cudaMemcpyDeviceToHost));
+    if (c.plan_out_chunks) CK(cudaMemcpy(bo.data(), ctx->kv.plan_out_blocks, bo.size() * 4, cudaMemcpyDeviceToHost));
+    if (c.plan_in_chunks) CK(cudaMemcpy(bi.data(), ctx->kv.plan_in_blocks, bi.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaEventRecord(ctx->sev[0], ctx->stream));
+    if (mode == AUTX_SWAP_PER_CHUNK_MEMCPY) {
+      // vLLM v0.6.1 behaviour: one cudaMemcpyAsync per (layer, K|V, block)
+      for (int dir = 0; dir < 2; ++dir) {
+        auto& items = dir == 0 ? po : pi;
+        auto& blks = dir == 0 ? bo : bi;
+        for (auto& it : items)
+          for (uint32_t j = 0; j < it.nblk; ++j)
+            for (uint32_t l = 0; l < L->n_layers; ++l)
+              for (int kvs = 0; kvs < 2; ++kvs) {
+                char* dev = (char*)(kvs ? L->v_pool[l] : L->k_pool[l]) + (uint64_t)blks[it.blk_off + j] * L->chunk_bytes;
+                char* host = arena + it.host_page * page + ((uint64_t)j * L->n_layers + l) * 2 * L->chunk_bytes +
+                             (uint64_t)kvs * L->chunk_bytes;
+                if (dir == 0) CK(cudaMemcpyAsync(host, dev, L->chunk_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+                else CK(cudaMemcpyAsync(dev, host, L->chunk_bytes, cudaMemcpyHostToDevice, ctx->stream));
+              }
+      }
+    } else {
+      // the paper's scheme: gather into a contiguous buffer, one bulk transfer
+      // per call
+      size_t need = (size_t)std::max(c.plan_out_chunks, c.plan_in_chunks) * page;
+      if (need > ctx->staging_bytes) {
+        if (ctx->staging) cudaFree(ctx->staging);
+        ctx->staging = nullptr;
+        CK(cudaMalloc((void**)&ctx->staging, need));
+        ctx->staging_bytes = need;
+        CK(cudaEventRecord(ctx->sev[0], ctx->stream));
+      }
+      if (c.plan_out_chunks) {
+        CK(launch_stage(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, ctx->staging, 0, dev_sms * 4));
+        for (auto& it : po)
+          CK(cudaMemcpyAsync(arena + it.host_page * page, ctx->staging + (uint64_t)it.blk_off * page,
+                             (uint64_t)it.nblk * page, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+      if (c.plan_in_chunks) {
+        for (auto& it : pi)
+          CK(cudaMemcpyAsync(ctx->staging + (uint64_t)it.blk_off * page, arena + it.host_page * page,
+                             (uint64_t)it.nblk * page, cudaMemcpyHostToDevice, ctx->stream));
+        CK(launch_stage(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, ctx->staging, 1, dev_sms * 4));
+      }
+    }
+  } else {
+    return fail(ctx, AUTX_E_INVAL, "unknown swap mode %d", mode);
+  }
+  CK(cudaEventRecord(ctx->sev[1], ctx->stream));
+  CK(cudaEventSynchronize(ctx->sev[1]));
+  CK(cudaEventElapsedTime(&stats->ms, ctx->sev[0], ctx->sev[1]));
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_block_table(autx_ctx* ctx, const uint32_t** off, const uint32_t** blk) {
+  if (!ctx || !off || !blk) return AUTX_E_INVAL;
+  if (!ctx->kv_on) return fail(ctx, AUTX_E_INVAL, "KV allocator disabled");
+  *off = ctx->kv.bt_offsets;
+  *blk = ctx->kv.bt_blocks;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_block_table_host(autx_ctx* ctx, uint32_t* h_off, uint32_t* h_blk, uint32_t cap,
+                                             uint32_t* n_batch) {
+  if (!ctx || !h_off || !n_batch) return AUTX_E_INVAL;
+  if (!ctx->kv_on) return fail(ctx, AUTX_E_INVAL, "KV allocator disabled");
+  autx_status s = sync_last(ctx);
+  if (s) return s;
+  CK(cudaStreamSynchronize(ctx->stream));
+  uint32_t n = ctx->out.hout->n_batch;
+  CK(cudaMemcpy(h_off, ctx->kv.bt_offsets, (size_t)(n + 1) * 4, cudaMemcpyDeviceToHost));
+  uint32_t nb = h_off[n];
+  if (nb > cap) return fail(ctx, AUTX_E_INVAL, "block table needs %u entries", nb);
+  if (nb) CK(cudaMemcpy(h_blk, ctx->kv.bt_blocks, (size_t)nb * 4, cudaMemcpyDeviceToHost));
+  *n_batch = n;
+  return AUTX_OK;
+}
+
+// ---- introspection ---------------------------------------------------------------------------
+extern "C" autx_status autx_dump_calls(autx_ctx* ctx, autx_call_state* outp, uint32_t cap, uint32_t* n) {
+  if (!ctx || !n) return AUTX_E_INVAL;
+  autx_status s = sync_last(ctx);
+  if (s) return s;
+  CK(cudaStreamSynchronize(ctx->stream));
+  uint32_t T = ctx->tail;
+  std::vector<uint64_t> cid(T);
+  std::vector<uint32_t> arr(T), base(T), mt(T), ex(T), qt(T), inh(T), tok(T);
+  std::vector<uint8_t> qf(T);
+  const CallTable& t = ctx->ct;
+  if (T) {
+    CK(cudaMemcpy(cid.data(), t.cid, (size_t)T * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(arr.data(), t.arr, (size_t)T * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(base.data(), t.base, (size_t)T * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(mt.data(), t.mtime, (size_t)T * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ex.data(), t.exec, (size_t)T * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(qt.data(), t.quanta, (size_t)T * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(inh.data(), t.inh, (size_t)T * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(tok.data(), t.tok, (size_t)T * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(qf.data(), t.qf, T, cudaMemcpyDeviceToHost));
+  }
+  const uint32_t now = ctx->stepped ? ctx->t_last + 1 : 0;  // counters include step t_last
+  uint32_t k = 0;
+  for (uint32_t r = 0; r < T; ++r) {
+    if (qf[r] & QF_DEAD) continue;
+    if (outp && k < cap) {
+      autx_call_state& o = outp[k];
+      o.call_id = cid[r];
+      o.q = qf[r] & QF_QMASK;
+      o.quanta = qt[r];
+      o.mtime = mt[r];
+      o.wait = (now - base[r]) - mt[r];
+      o.exec = ex[r];
+      o.totwait = (now - arr[r]) - ex[r];
+      o.inh = inh[r];
+      o.input_tokens = tok[r];
+      o.arrival_step = arr[r];
+      o.flags = ((qf[r] & QF_RUN) ? 1u : 0u) | ((qf[r] & QF_RES) ? 2u : 0u) |
+                ((!(qf[r] & QF_RES) && ex[r] > 0) ? 4u : 0u);
+    }
+    ++k;
+  }
+  *n = k;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_program_state(autx_ctx* ctx, uint64_t pid, uint32_t* svc, uint64_t* pwait) {
+  if (!ctx) return AUTX_E_INVAL;
+  auto it = ctx->prog_row.find(pid);
+  if (it == ctx->prog_row.end()) return fail(ctx, AUTX_E_NOENT, "unknown program");
+  CK(cudaStreamSynchronize(ctx->stream));
+  uint32_t s = 0;
+  unsigned long long w = 0;
+  CK(cudaMemcpy(&s, ctx->pt.svc + it->second, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&w, ctx->pt.pwait + it->second, 8, cudaMemcpyDeviceToHost));
+  if (svc) *svc = s;
+  if (pwait) *pwait = w;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_last_step_timing(autx_ctx* ctx, autx_step_timing* t) {
+  if (!ctx || !t) return AUTX_E_INVAL;
+  *t = ctx->last_timing;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_set_timing(autx_ctx* ctx, int32_t on) {
+  if (!ctx) return AUTX_E_INVAL;
+  ctx->timing = on != 0;
+  return AUTX_OK;
+}
+
+extern "C" uint32_t autx_num_active(const autx_ctx* ctx) { return ctx ? (uint32_t)ctx->call_slot.size() : 0; }
+
+// ---- routing (a8) ----------------------------------------------------------------------------
+extern "C" uint64_t autx_route_record_bytes(const autx_ctx* ctx) {
+  return ctx ? sizeof(RouteHdr) + (uint64_t)ctx->cfg.max_batch * sizeof(CompRec) : 0;
+}
+
+extern "C" autx_status autx_route_pack(autx_ctx* ctx, void* d_record) {
+  if (!ctx || !d_record) return AUTX_E_INVAL;
+  autx_status s = sync_last(ctx);
+  if (s) return s;
+  if (ctx->registered_this) return fail(ctx, AUTX_E_STATE, "autx_route_pack after autx_register_call");
+  CK(cudaStreamSynchronize(ctx->stream));  // h_hdr reuse
+  ctx->h_hdr->load = ctx->call_slot.size();  // queued + running after this step's completions
+  ctx->h_hdr->n_comp = ctx->completed_this ? ctx->n_completed_pending : 0;
+  ctx->h_hdr->_pad = 0;
+  CK(cudaMemcpyAsync(d_record, ctx->h_hdr, sizeof(RouteHdr), cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->h_hdr->n_comp)
+    CK(cudaMemcpyAsync((char*)d_record + sizeof(RouteHdr), ctx->d_route_local + sizeof(RouteHdr),
+                       (size_t)ctx->h_hdr->n_comp * sizeof(CompRec), cudaMemcpyDeviceToDevice, ctx->stream));
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_route_apply(autx_ctx* ctx, const void* d_records, const autx_call_desc* calls,
+                                        uint32_t n, int32_t* engine_out) {
+  if (!ctx || !d_records || (n && (!calls || !engine_out))) return AUTX_E_INVAL;
+  uint32_t G = (uint32_t)std::max(ctx->cfg.nranks, 1);
+  if (G > 8) return fail(ctx, AUTX_E_INVAL, "at most 8 engines");
+  if (ctx->registered_this) return fail(ctx, AUTX_E_STATE, "autx_route_apply after autx_register_call");
+  if (ctx->routed_this) return fail(ctx, AUTX_E_STATE, "autx_route_apply twice in one step");
+  uint32_t t = next_step(ctx);
+  uint64_t stride = autx_route_record_bytes(ctx);
+  if (ctx->cfg.nranks > 1) CK(launch_apply(ctx->stream, ctx->pol, ctx->pt, d_records, stride, G, t));
+  if (n > ctx->rarr_cap) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_rarr) cudaFreeHost(ctx->h_rarr);
+    if (ctx->d_rarr) cudaFree(ctx->d_rarr);
+    if (ctx->d_rout) cudaFree(ctx->d_rout);
+    ctx->rarr_cap = n;
+    CK(cudaHostAlloc((void**)&ctx->h_rarr, (size_t)n * sizeof(RouteArr), 0));
+    CK(dalloc(&ctx->d_rarr, n));
+    CK(dalloc(&ctx->d_rout, n));
+  } else {
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  // replicated process-table rows: created in canonical arrival order on every rank
+  for (uint32_t i = 0; i < n; ++i) {
+    const autx_call_desc& d = calls[i];
+    if (i > 0) {
+      const autx_call_desc& q = calls[i - 1];
+      uint64_t a[4] = {q.arrival_step, q.program_arrival_step, q.program_id, q.call_id};
+      uint64_t b[4] = {d.arrival_step, d.program_arrival_step, d.program_id, d.call_id};
+      if (!std::lexicographical_compare(a, a + 4, b, b + 4))
+        return fail(ctx, AUTX_E_INVAL, "routing batch not in canonical order");
+    }
+    auto it = ctx->prog_row.find(d.program_id);
+    uint32_t row;
+    if (it == ctx->prog_row.end()) {
+      autx_status s2 = new_program(ctx, d.program_id, &row);
+      if (s2) return s2;
+    } else {
+      row = it->second;
+    }
+    ctx->h_rarr[i] = RouteArr{row, d.input_tokens};
+  }
+  if (n) {
+    CK(cudaMemcpyAsync(ctx->d_rarr, ctx->h_rarr, (size_t)n * sizeof(RouteArr), cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_route(ctx->stream, d_records, stride, G, ctx->d_rarr, n, ctx->d_pin, ctx->cfg.token_threshold,
+                    ctx->d_rout));
+    CK(cudaMemcpyAsync(engine_out, ctx->d_rout, (size_t)n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  ctx->routed_this = true;
+  return AUTX_OK;
+}

@@ -1,0 +1,194 @@
+// Internal definitions shared by the autx host code and its sm_100a kernels.
+// Nothing here is part of the C ABI (include/autx.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace autx {
+
+// ---- per-call flag byte (qf) ---------------------------------------------------------------
+constexpr uint8_t QF_QMASK = 0x0F;  // queue index q (0 = Q_1, highest priority)
+constexpr uint8_t QF_RUN = 0x10;    // in the previous step's batch ("running", key tie R12)
+constexpr uint8_t QF_RES = 0x20;    // KV resident on the GPU (eager eviction: == RUN after a step)
+constexpr uint8_t QF_DEAD = 0x40;   // empty row (completed call / never used)
+constexpr uint8_t QF_INB = 0x80;    // scratch: member of the batch being formed (finalize only)
+
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr int MAX_K = 16;
+constexpr int SCAN_THREADS = 256;
+constexpr int ROWS_PER_THREAD = 4;
+constexpr int TILE = SCAN_THREADS * ROWS_PER_THREAD;  // rows per scan tile (1024)
+constexpr int FIN_THREADS = 1024;
+
+// Device-resident call table, struct-of-arrays, rows in (arrival, seq) order.  Row index ==
+// registration order, so the paper's FCFS tie `seq` is the row index.
+struct CallTable {
+  uint64_t* cid;     // call id
+  uint32_t* prog;    // process-table row of the call's program
+  uint32_t* arr;     // arrival step
+  uint8_t* qf;       // queue | flags
+  uint32_t* base;    // step of the last reset of (wait, mtime): arrival or promotion
+  uint32_t* mtime;   // c.model_time since the last reset (Alg. 1 l.25, l.29)
+  uint32_t* exec;    // t_k: executed steps, never reset (R6)
+  uint32_t* quanta;  // remaining quantum (AUTX_INF = infinite)
+  uint32_t* inh;     // service inherited at arrival (Alg. 1 l.11)
+  uint32_t* tok;     // input tokens (context)
+  uint32_t* loc;     // resident slot (if RES) or host arena page offset (if swapped), else NONE
+  uint32_t* hcls;    // host allocation size class (if swapped)
+};
+
+// Process table, one row per program.
+struct ProgTable {
+  uint32_t* svc;        // PLAS: sum of completed t_k; ATLAS: longest critical path (Alg. 1 l.4)
+  unsigned long long* pwait;  // total waiting time of completed calls (W_p)
+  uint32_t* last_arr;   // most recent call arrival
+  uint32_t* last_comp;  // most recent call completion
+};
+
+struct Policy {
+  int32_t policy;
+  uint32_t K;
+  uint32_t q_hi[15];
+  uint32_t quanta[16];
+  uint32_t beta_num, beta_den;
+  uint32_t max_batch;
+  uint32_t kv_budget;
+  uint32_t block_tokens;
+  uint32_t n_gpu_blocks;
+  uint32_t max_blocks_per_call;
+  uint32_t host_pages_lo;  // host arena pages (capped to 2^32-1)
+};
+
+// Step control block in device memory (written by the prologue kernels).
+struct Ctl {
+  uint32_t t;          // current step
+  uint32_t n_rows;     // rows in use (tail)
+  uint32_t ntiles;
+  uint32_t tiles_done; // last-CTA ticket for the scan kernel
+  // selection result (scan kernel's last CTA)
+  uint32_t qstar;      // boundary queue (K if all live calls are candidates)
+  uint32_t mprime;     // rows of q* to take in table order
+  uint32_t n_cand_a;   // candidates from the table scan
+  uint32_t n_cand_b;   // extra running candidates of queue q*
+  uint32_t n_promoted;
+  uint32_t n_live;
+  // finalize results
+  uint32_t n_prev;     // previous batch size (slots in prev_slots)
+  uint32_t err;        // sticky device error code (autx_status)
+  uint32_t err_info;
+  uint32_t n_plan_out, n_plan_in;   // swap plan items
+  uint32_t plan_out_chunks, plan_in_chunks;
+  // allocator state
+  uint32_t free_top;       // GPU block free stack size
+  uint32_t rs_free_top;    // resident-slot free stack size
+  uint32_t host_bump;      // host arena bump pointer (pages)
+  uint32_t _pad;
+  uint32_t host_free_top[32];  // per size class free-stack size
+};
+
+// Host-visible step output written by the finalize kernel into mapped pinned memory.
+struct HostOut {
+  uint32_t n_batch, n_admit, n_preempt, n_active;
+  unsigned long long swap_out_blocks, swap_in_blocks, kv_blocks;
+  uint32_t n_promoted, err;
+  uint32_t seqno;  // step sequence number, for sanity
+  uint32_t _pad;
+};
+
+// Swap plan (built by finalize, executed by autx_kv_swap).
+struct PlanItem {
+  unsigned long long host_page;  // page offset in the host arena
+  uint32_t nblk;                 // number of blocks
+  uint32_t blk_off;              // offset into plan block list
+};
+
+struct KvState {
+  uint32_t* free_stack;     // [n_gpu_blocks]
+  uint32_t* rs_free;        // [max_batch] resident-slot free stack
+  uint32_t* rs_nblk;        // [max_batch] blocks held per resident slot
+  uint32_t* rs_blocks;      // [max_batch * max_blocks_per_call]
+  uint32_t* host_free;      // [32][host_free_cap] per-class free stacks of page offsets
+  uint32_t host_free_cap;
+  PlanItem* plan_out;       // [max_batch]
+  PlanItem* plan_in;        // [max_batch]
+  uint32_t* plan_out_blocks;   // [kv cap]
+  uint32_t* plan_in_blocks;    // [kv cap]
+  uint32_t* bt_offsets;     // [max_batch+1] block table CSR of the batch
+  uint32_t* bt_blocks;      // [kv cap]
+  uint32_t plan_cap;        // capacity of the plan block lists
+};
+
+struct Outputs {
+  uint32_t* batch_slots;     // [max_batch]
+  uint64_t* batch_ids;       // [max_batch]
+  uint64_t* admit_ids;       // [max_batch]
+  uint64_t* preempt_ids;     // [max_batch]
+  uint32_t* prev_slots;      // [max_batch] previous batch (slots), ctl->n_prev entries
+  uint32_t* preempt_slots;   // [max_batch]
+  uint32_t* admit_slots;     // [max_batch]
+  uint32_t* cand;            // [cand_cap] candidate slots
+  uint32_t cand_cap;
+  uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
+  uint32_t* tile_off;        // [ntiles_cap+1] candidate offsets
+  uint32_t* tile_pre;        // [ntiles_cap] q* rows in earlier tiles
+  HostOut* hout;             // mapped pinned host
+  uint64_t* h_batch;         // mapped pinned host mirrors
+  uint64_t* h_admit;
+  uint64_t* h_preempt;
+};
+
+// Completion record (one per completed call): what UPDATE_PROCESS_TABLE needs.
+struct CompRec {
+  uint32_t prog;  // process-table row (identical on every rank: rows are created in the
+                  // replicated routing order)
+  uint32_t exec;  // t_k
+  uint32_t cp;    // inh + t_k (ATLAS critical path candidate)
+  uint32_t tw;    // total waiting steps
+};
+
+// Routing-epoch record of one engine, followed by max_batch CompRec.
+struct RouteHdr {
+  unsigned long long load;  // queued + running calls after this step's completions (R21)
+  uint32_t n_comp;
+  uint32_t _pad;
+};
+
+struct RouteArr {
+  uint32_t prog;
+  uint32_t tok;
+};
+
+// Arrival record staged by the host.
+struct ArrivalRec {
+  uint64_t cid;
+  uint32_t prog;
+  uint32_t tok;
+  uint32_t flags;  // bit0: program is new in this batch (inh = 0); bit1: first record of it
+  uint32_t _pad;
+};
+
+// ---- kernel launchers (sched_kernels.cu / swap_kernels.cu) ----------------------------------
+cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                            const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
+                            CompRec* rec_out, bool apply);
+cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,
+                         uint64_t stride, uint32_t G, uint32_t t);
+cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,
+                         const RouteArr* arr, uint32_t n, int8_t* pin, uint32_t threshold,
+                         int32_t* out);
+cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt,
+                            const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t);
+cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                        Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
+                        uint32_t seqno, cudaEvent_t* ev /* 5 events or null */);
+cudaError_t launch_swap(cudaStream_t s, const Ctl* ctl, KvState kv, void* const* d_kpool,
+                        void* const* d_vpool, uint32_t n_layers, uint32_t chunk_bytes,
+                        char* host_arena, int direction, int n_ctas);
+cudaError_t launch_stage(cudaStream_t s, const Ctl* ctl, KvState kv, void* const* d_kpool,
+                         void* const* d_vpool, uint32_t n_layers, uint32_t chunk_bytes,
+                         char* staging, int direction, int n_ctas);
+cudaError_t launch_compact(cudaStream_t s, CallTable src, CallTable dst, const uint32_t* live,
+                           uint32_t n_live);
+cudaError_t launch_remap(cudaStream_t s, uint32_t* slots, uint32_t n, const uint32_t* old2new);
+
+}  // namespace autx

@@ -1,0 +1,147 @@
+// Warp/block primitives (scans, segmented scans, bitonic sort) written for sm_100a.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace autx {
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T u = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane_id() >= (uint32_t)d) v += u;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
+// Block-wide exclusive scan; every thread of the block must call it.  smem: >= 33 T.
+template <typename T, int NT>
+__device__ __forceinline__ T block_excl_scan(T v, T* smem, T* total) {
+  constexpr int NW = NT / 32;
+  T inc = warp_incl_scan(v);
+  if (lane_id() == 31) smem[warp_id()] = inc;
+  __syncthreads();
+  if (warp_id() == 0) {
+    T w = lane_id() < NW ? smem[lane_id()] : T(0);
+    T wi = warp_incl_scan(w);
+    if (lane_id() < NW) smem[lane_id()] = wi - w;
+    if (lane_id() == NW - 1) smem[32] = wi;
+  }
+  __syncthreads();
+  T r = smem[warp_id()] + inc - v;
+  if (total) *total = smem[32];
+  __syncthreads();
+  return r;
+}
+
+template <typename T, int NT>
+__device__ __forceinline__ T block_sum(T v, T* smem) {
+  T tot;
+  block_excl_scan<T, NT>(v, smem, &tot);
+  return tot;
+}
+
+// ---- segmented inclusive scan (head flags), warp shuffles + one cross-warp pass -------------
+struct OpSum {
+  template <typename T>
+  __device__ __forceinline__ T operator()(T a, T b) const { return a + b; }
+};
+struct OpMax {
+  template <typename T>
+  __device__ __forceinline__ T operator()(T a, T b) const { return a > b ? a : b; }
+};
+
+// Inclusive segmented scan over the block in thread order.  `head` marks the first element
+// of a segment.  smem_v: >= 32 T, smem_f: >= 32 uint32.
+template <typename T, int NT, typename Op>
+__device__ __forceinline__ T block_seg_scan(T v, bool head, Op op, T* smem_v, uint32_t* smem_f) {
+  uint32_t f = head;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T u = __shfl_up_sync(0xffffffffu, v, d);
+    uint32_t fu = __shfl_up_sync(0xffffffffu, f, d);
+    if (lane_id() >= (uint32_t)d) {
+      if (!f) v = op(u, v);
+      f |= fu;
+    }
+  }
+  constexpr int NW = NT / 32;
+  if (lane_id() == 31) {
+    smem_v[warp_id()] = v;
+    smem_f[warp_id()] = f;
+  }
+  __syncthreads();
+  if (warp_id() == 0) {
+    // exclusive segmented scan of the warp aggregates
+    T w = lane_id() < NW ? smem_v[lane_id()] : T(0);
+    uint32_t wf = lane_id() < NW ? smem_f[lane_id()] : 1u;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      T u = __shfl_up_sync(0xffffffffu, w, d);
+      uint32_t fu = __shfl_up_sync(0xffffffffu, wf, d);
+      if (lane_id() >= (uint32_t)d) {
+        if (!wf) w = op(u, w);
+        wf |= fu;
+      }
+    }
+    // shift to exclusive: carry into warp i = inclusive aggregate of warp i-1
+    T prev = __shfl_up_sync(0xffffffffu, w, 1);
+    uint32_t has = lane_id() > 0;
+    if (lane_id() < NW) {
+      smem_v[lane_id()] = prev;
+      smem_f[lane_id()] = has;
+    }
+  }
+  __syncthreads();
+  if (!f && smem_f[warp_id()]) v = op(smem_v[warp_id()], v);
+  __syncthreads();
+  return v;
+}
+
+// ---- bitonic sort of (hi, lo) pairs in shared memory, ascending lexicographic -------------
+__device__ __forceinline__ bool pair_gt(uint64_t ah, uint32_t al, uint64_t bh, uint32_t bl) {
+  return ah > bh || (ah == bh && al > bl);
+}
+
+template <int NT>
+__device__ void bitonic_sort_pairs(uint64_t* hi, uint32_t* lo, uint32_t np) {
+  for (uint32_t k = 2; k <= np; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < np / 2; i += NT) {
+        // index of the lower element of the i-th compare-exchange pair
+        uint32_t a = 2 * i - (i & (j - 1));
+        uint32_t b = a + j;
+        bool up = (a & k) == 0;
+        uint64_t ah = hi[a], bh = hi[b];
+        uint32_t al = lo[a], bl = lo[b];
+        if (pair_gt(ah, al, bh, bl) == up) {
+          hi[a] = bh; lo[a] = bl;
+          hi[b] = ah; lo[b] = al;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// 128-bit compare: a*b >= c*d for u64 a, c and u32 b, d.
+__device__ __forceinline__ bool mul_ge(uint64_t a, uint32_t b, uint64_t c, uint32_t d) {
+  uint64_t l1 = a * (uint64_t)b, h1 = __umul64hi(a, (uint64_t)b);
+  uint64_t l2 = c * (uint64_t)d, h2 = __umul64hi(c, (uint64_t)d);
+  return h1 > h2 || (h1 == h2 && l1 >= l2);
+}
+
+__device__ __forceinline__ uint32_t ceil_div_u32(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+
+}  // namespace autx

@@ -1,0 +1,841 @@
+// sm_100a kernels of one Autellix scheduling step.
+//
+//   k_complete   (a1)  completion records -> process table, warp-shuffle segmented reduce
+//   k_register   (a2)  arrivals appended to the call table, inherit service, placed in a queue
+//   k_scan       (a4)  dense pass over every call: anti-starvation (integer cross-multiply)
+//                      + per-tile per-queue counts; the last CTA picks the boundary queue q*
+//   k_gather     (a5)  emits the candidate set (<= BS rows of the lowest queues, table order)
+//   k_finalize   (a5, a6, a3, a7 plan)  sorts candidates by the unique key, prefix cutoff on
+//                      BS and the KV budget, admit/preempt lists, step accounting and eager
+//                      demotion, GPU block allocation and the swap plan
+//
+// Every step of Alg. 1 runs here; the host only stages records.  Citations: see autx.h.
+#include "autx_internal.cuh"
+#include "block_prims.cuh"
+#include "../../include/autx.h"
+
+namespace autx {
+
+__device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc) {
+  // Alg. 1 l.12, half-open [lo, hi) (R1); FCFS/MLFQ: all new calls enter Q_1.
+  if (pol.policy == AUTX_FCFS || pol.policy == AUTX_MLFQ) return 0;
+  uint32_t q = 0;
+  for (uint32_t i = 0; i + 1 < pol.K; ++i)
+    if (svc >= pol.q_hi[i]) q = i + 1;
+  return q;
+}
+
+__device__ __forceinline__ void set_err(Ctl* ctl, uint32_t code, uint32_t info) {
+  if (atomicCAS(&ctl->err, 0u, code) == 0u) ctl->err_info = info;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a1: UPDATE_PROCESS_TABLE (Alg. 1 l.1-7) for the calls that finished in step t-1.
+//   PLAS (Eq. 1): svc[p] += sum exec;  ATLAS (l.4): svc[p] = max(svc[p], max(inh + exec));
+//   pwait[p] += sum totwait (R5), totwait(c) = (t - arr) - exec (active steps not running).
+// Records are sorted by program in shared memory; a warp-shuffle segmented scan reduces each
+// program's run and the segment tail writes the row: one write per program, deterministic.
+// ---------------------------------------------------------------------------------------------
+// Applies one chunk of <= FIN_THREADS completion records to the process table.
+__device__ void apply_record_chunk(const Policy& pol, ProgTable pt, const CompRec* recs, uint32_t n,
+                                   uint32_t t) {
+  __shared__ uint64_t skey[FIN_THREADS];
+  __shared__ uint32_t sdummy[FIN_THREADS];
+  __shared__ CompRec srec[FIN_THREADS];
+  __shared__ uint64_t red_v[33];
+  __shared__ uint32_t red_f[33];
+  const uint32_t tid = threadIdx.x;
+  bool valid = tid < n;
+  if (valid) srec[tid] = recs[tid];
+  skey[tid] = valid ? ((uint64_t)recs[tid].prog << 32 | tid) : ~0ull;
+  sdummy[tid] = 0;
+  __syncthreads();
+  bitonic_sort_pairs<FIN_THREADS>(skey, sdummy, FIN_THREADS);
+  uint64_t k = skey[tid];
+  bool v2 = k != ~0ull;
+  uint32_t o = (uint32_t)k, pp = (uint32_t)(k >> 32);
+  bool head = tid == 0 || (skey[tid - 1] >> 32) != pp;
+  bool tail = tid == FIN_THREADS - 1 || skey[tid + 1] == ~0ull || (skey[tid + 1] >> 32) != pp;
+  uint64_t ex = v2 ? srec[o].exec : 0, tw = v2 ? srec[o].tw : 0, cp = v2 ? srec[o].cp : 0;
+  uint64_t sum_ex = block_seg_scan<uint64_t, FIN_THREADS>(ex, head, OpSum(), red_v, red_f);
+  uint64_t sum_tw = block_seg_scan<uint64_t, FIN_THREADS>(tw, head, OpSum(), red_v, red_f);
+  uint64_t max_cp = block_seg_scan<uint64_t, FIN_THREADS>(cp, head, OpMax(), red_v, red_f);
+  if (v2 && tail) {
+    if (pol.policy == AUTX_ATLAS) {
+      uint32_t cur = pt.svc[pp];
+      pt.svc[pp] = max_cp > cur ? (uint32_t)max_cp : cur;  // Alg. 1 l.4
+    } else {
+      pt.svc[pp] += (uint32_t)sum_ex;                       // Eq. 1
+    }
+    pt.pwait[pp] += sum_tw;                                 // Alg. 1 l.5-6, R5
+    pt.last_comp[pp] = t;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(FIN_THREADS) k_complete(Policy pol, CallTable ct, ProgTable pt,
+                                                          Ctl* ctl, const uint32_t* slots,
+                                                          uint32_t n, uint32_t t, KvState kv,
+                                                          bool kv_on, CompRec* rec_out, bool apply) {
+  __shared__ uint32_t red_u[33];
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t base = 0; base < n; base += FIN_THREADS) {
+    uint32_t i = base + tid;
+    bool valid = i < n;
+    uint32_t s = valid ? slots[i] : 0;
+    if (valid) {
+      uint32_t e = ct.exec[s];
+      CompRec r;
+      r.prog = ct.prog[s];
+      r.exec = e;
+      r.cp = ct.inh[s] + e;
+      r.tw = (t - ct.arr[s]) - e;  // totwait: active steps arr..t-1 that did not run
+      rec_out[i] = r;
+    }
+    __syncthreads();
+    if (apply) apply_record_chunk(pol, pt, rec_out + base, min(n - base, (uint32_t)FIN_THREADS), t);
+    // release the row and its KV (completed calls ran in step t-1, hence are resident)
+    uint32_t nfree = 0, rslot = NONE;
+    if (valid) {
+      uint8_t qf = ct.qf[s];
+      if (kv_on && (qf & QF_RES)) {
+        rslot = ct.loc[s];
+        nfree = kv.rs_nblk[rslot];
+      }
+      ct.qf[s] = QF_DEAD;
+      ct.loc[s] = NONE;
+    }
+    if (kv_on) {
+      uint32_t tot;
+      uint32_t off = block_excl_scan<uint32_t, FIN_THREADS>(nfree, red_u, &tot);
+      uint32_t has = rslot != NONE, rtot;
+      uint32_t roff = block_excl_scan<uint32_t, FIN_THREADS>(has, red_u, &rtot);
+      uint32_t top = ctl->free_top, rtop = ctl->rs_free_top;
+      if (rslot != NONE) {
+        const uint32_t* src = kv.rs_blocks + (size_t)rslot * pol.max_blocks_per_call;
+        for (uint32_t j = 0; j < nfree; ++j) kv.free_stack[top + off + j] = src[j];
+        kv.rs_nblk[rslot] = 0;
+        kv.rs_free[rtop + roff] = rslot;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        ctl->free_top = top + tot;
+        ctl->rs_free_top = rtop + rtot;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) ctl->t = t;
+}
+
+// Multi-engine: apply every engine's completion records (R22: sums and maxima commute, so the
+// replicated tables stay identical whatever the order).  recs of rank r start at
+// base + r * stride bytes, after a RouteHdr.
+__global__ void __launch_bounds__(FIN_THREADS) k_apply(Policy pol, ProgTable pt, const char* base,
+                                                       uint64_t stride, uint32_t G, uint32_t t) {
+  for (uint32_t r = 0; r < G; ++r) {
+    const RouteHdr* h = reinterpret_cast<const RouteHdr*>(base + r * stride);
+    const CompRec* recs = reinterpret_cast<const CompRec*>(h + 1);
+    uint32_t n = h->n_comp;
+    for (uint32_t b = 0; b < n; b += FIN_THREADS)
+      apply_record_chunk(pol, pt, recs + b, min(n - b, (uint32_t)FIN_THREADS), t);
+  }
+}
+
+// Alg. 2 over the replicated arrival batch, canonical order: tokens <= threshold -> argmin load
+// (ties -> lowest engine id); else the program's pinned engine, or argmin + pin (l.5-10).  The
+// chosen engine's load is incremented after each assignment (R23).  One thread: the recurrence
+// through `load` is sequential by definition; G <= 8 loads stay in registers.
+__global__ void k_route(const char* base, uint64_t stride, uint32_t G, const RouteArr* arr,
+                        uint32_t n, int8_t* pin, uint32_t threshold, int32_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint64_t load[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    load[e] = e < (int)G ? reinterpret_cast<const RouteHdr*>(base + e * stride)->load : ~0ull;
+  for (uint32_t i = 0; i < n; ++i) {
+    RouteArr a = arr[i];
+    int e;
+    int pinned = a.tok > threshold ? pin[a.prog] : -1;
+    if (a.tok > threshold && pinned >= 0) {
+      e = pinned;
+    } else {
+      e = 0;
+      uint64_t best = load[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k)
+        if (load[k] < best) { best = load[k]; e = k; }
+      if (a.tok > threshold) pin[a.prog] = (int8_t)e;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k == e) load[k] += 1;
+    out[i] = e;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a2: arrivals (Alg. 1 l.9-14).  Rows are appended in canonical order; row index = seq.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const ArrivalRec* recs,
+                           uint32_t n, uint32_t first_slot, uint32_t t) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  ArrivalRec r = recs[i];
+  uint32_t p = r.prog;
+  if (r.flags & 2u) {  // first record of a program new in this batch: create its entry
+    pt.svc[p] = 0;
+    pt.pwait[p] = 0;
+    pt.last_comp[p] = NONE;
+  }
+  uint32_t inh = (r.flags & 1u) ? 0u : pt.svc[p];  // Alg. 1 l.11
+  pt.last_arr[p] = t;
+  uint32_t q = place_queue(pol, inh);             // Alg. 1 l.12
+  uint32_t s = first_slot + i;
+  ct.cid[s] = r.cid;
+  ct.prog[s] = p;
+  ct.arr[s] = t;
+  ct.qf[s] = (uint8_t)q;
+  ct.base[s] = t;
+  ct.mtime[s] = 0;
+  ct.exec[s] = 0;
+  ct.quanta[s] = pol.quanta[q];                   // Alg. 1 l.13
+  ct.inh[s] = inh;
+  ct.tok[s] = r.tok;
+  ct.loc[s] = NONE;
+  ct.hcls[s] = 0;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a4 + counting: the dense pass.  Every live call: wait = (t - base) - mtime (every active step
+// since the last reset either ran or waited), W = pwait[p] + wait, T = svc[p] + mtime; promote
+// to Q_1 iff W * beta_den >= beta_num * T and not 0/0 (Alg. 1 l.24-30, R3/R4/R7).  Demotion
+// (l.20-23) was applied eagerly by the previous step's finalize (only batch calls can exhaust a
+// quantum, and nothing in between reads q).  Bytes per call: qf 1 + prog 4 + base 4 + mtime 4
+// read; base/mtime/qf/quanta written only for promoted calls.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void count_q(uint64_t& c0, uint64_t& c1, uint64_t& c2, uint64_t& c3,
+                                        uint32_t q) {
+  uint64_t inc = 1ull << ((q & 3) * 16);
+  uint32_t g = q >> 2;
+  c0 += g == 0 ? inc : 0;
+  c1 += g == 1 ? inc : 0;
+  c2 += g == 2 ? inc : 0;
+  c3 += g == 3 ? inc : 0;
+}
+
+__device__ void select_boundary(const Policy& pol, Ctl* ctl, Outputs out, uint32_t ntiles);
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(Policy pol, CallTable ct, ProgTable pt,
+                                                       Ctl* ctl, Outputs out, uint32_t t,
+                                                       uint32_t n_rows) {
+  const uint32_t tile = blockIdx.x;
+  const uint32_t row0 = tile * TILE + threadIdx.x * ROWS_PER_THREAD;
+  uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  uint32_t npromo = 0, nlive = 0;
+  if (row0 < n_rows) {
+    uint32_t qw = *reinterpret_cast<const uint32_t*>(ct.qf + row0);
+    uint4 pg = *reinterpret_cast<const uint4*>(ct.prog + row0);
+    uint4 bs = *reinterpret_cast<const uint4*>(ct.base + row0);
+    uint4 mt = *reinterpret_cast<const uint4*>(ct.mtime + row0);
+    uint32_t prog[4] = {pg.x, pg.y, pg.z, pg.w};
+    uint32_t base[4] = {bs.x, bs.y, bs.z, bs.w};
+    uint32_t mtim[4] = {mt.x, mt.y, mt.z, mt.w};
+    uint32_t qn = qw;
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < ROWS_PER_THREAD; ++j) {
+      uint32_t qf = (qw >> (8 * j)) & 0xffu;
+      if (qf & QF_DEAD) continue;
+      ++nlive;
+      uint32_t q = qf & QF_QMASK;
+      if (pol.beta_den != 0) {
+        uint32_t p = prog[j];
+        uint64_t W = pt.pwait[p] + (uint64_t)(t - base[j] - mtim[j]);
+        uint64_t T = (uint64_t)pt.svc[p] + mtim[j];
+        if (!(W == 0 && T == 0) && mul_ge(W, pol.beta_den, T, pol.beta_num)) {
+          q = 0;
+          qn = (qn & ~(0xffu << (8 * j))) | ((qf & ~QF_QMASK) << (8 * j));
+          base[j] = t;
+          mtim[j] = 0;
+          ct.quanta[row0 + j] = pol.quanta[0];
+          any = true;
+          ++npromo;
+        }
+      }
+      count_q(c0, c1, c2, c3, q);
+    }
+    if (any) {
+      *reinterpret_cast<uint32_t*>(ct.qf + row0) = qn;
+      *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
+      *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
+    }
+  }
+  // per-tile per-queue counts: warp reduce of packed 16-bit fields, then across warps
+  __shared__ uint64_t wc[SCAN_THREADS / 32][4];
+  __shared__ uint32_t wn[SCAN_THREADS / 32][2];
+  c0 = warp_sum(c0); c1 = warp_sum(c1); c2 = warp_sum(c2); c3 = warp_sum(c3);
+  npromo = warp_sum(npromo); nlive = warp_sum(nlive);
+  if (lane_id() == 0) {
+    wc[warp_id()][0] = c0; wc[warp_id()][1] = c1; wc[warp_id()][2] = c2; wc[warp_id()][3] = c3;
+    wn[warp_id()][0] = npromo; wn[warp_id()][1] = nlive;
+  }
+  __syncthreads();
+  if (threadIdx.x < MAX_K) {
+    uint32_t k = threadIdx.x, sum = 0;
+    for (int w = 0; w < SCAN_THREADS / 32; ++w) sum += (uint32_t)(wc[w][k >> 2] >> ((k & 3) * 16)) & 0xffffu;
+    out.tile_cnt[(size_t)tile * MAX_K + k] = sum;
+  }
+  if (threadIdx.x == 0) {
+    uint32_t a = 0, b = 0;
+    for (int w = 0; w < SCAN_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
+    if (a) atomicAdd(&ctl->n_promoted, a);
+    if (b) atomicAdd(&ctl->n_live, b);
+  }
+  // last CTA to finish selects the boundary queue and the per-tile candidate offsets
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&ctl->tiles_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    select_boundary(pol, ctl, out, gridDim.x);
+  }
+}
+
+// q* = smallest q with sum_{k<=q} total_k >= BS (K if none); m' = BS - sum_{k<q*} total_k.
+// Candidates: every live row with q < q*, plus the first m' rows of q* in table order.  Any
+// call among the BS smallest keys is a candidate or a running call of q* (finalize adds those):
+// inside q* the key order (arr, not-running, seq) differs from table order (arr, seq) only by
+// moving running calls forward within an arrival group.
+__device__ void select_boundary(const Policy& pol, Ctl* ctl, Outputs out, uint32_t ntiles) {
+  __shared__ uint32_t tot[MAX_K];
+  __shared__ uint32_t red[33];
+  __shared__ uint32_t s_qstar, s_m;
+  const uint32_t tid = threadIdx.x;
+  if (tid < MAX_K) tot[tid] = 0;
+  __syncthreads();
+  uint32_t acc[MAX_K];
+#pragma unroll
+  for (int k = 0; k < MAX_K; ++k) acc[k] = 0;
+  for (uint32_t tl = tid; tl < ntiles; tl += SCAN_THREADS) {
+    const uint4* c = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)tl * MAX_K);
+#pragma unroll
+    for (int v = 0; v < MAX_K / 4; ++v) {
+      uint4 x = __ldcg(c + v);
+      acc[4 * v] += x.x; acc[4 * v + 1] += x.y; acc[4 * v + 2] += x.z; acc[4 * v + 3] += x.w;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < MAX_K; ++k) {
+    uint32_t w = warp_sum(acc[k]);
+    if (lane_id() == 0 && w) atomicAdd(&tot[k], w);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t cum = 0, qs = pol.K, m = 0;
+    for (uint32_t k = 0; k < pol.K; ++k) {
+      if (cum + tot[k] >= pol.max_batch) { qs = k; m = pol.max_batch - cum; break; }
+      cum += tot[k];
+    }
+    s_qstar = qs;
+    s_m = m;
+    ctl->qstar = qs;
+    ctl->mprime = m;
+  }
+  __syncthreads();
+  const uint32_t qs = s_qstar, m = s_m;
+  // each thread owns a contiguous range of tiles
+  uint32_t per = (ntiles + SCAN_THREADS - 1) / SCAN_THREADS;
+  uint32_t t0 = tid * per, t1 = min(ntiles, t0 + per);
+  uint32_t my_qs = 0;
+  if (qs < pol.K)
+    for (uint32_t tl = t0; tl < t1; ++tl) my_qs += __ldcg(out.tile_cnt + (size_t)tl * MAX_K + qs);
+  uint32_t pre_qs = block_excl_scan<uint32_t, SCAN_THREADS>(my_qs, red, nullptr);
+  uint32_t my_c = 0;
+  for (uint32_t tl = t0; tl < t1; ++tl) {
+    const uint32_t* c = out.tile_cnt + (size_t)tl * MAX_K;
+    uint32_t a = 0;
+    for (uint32_t k = 0; k < qs && k < pol.K; ++k) a += __ldcg(c + k);
+    out.tile_pre[tl] = pre_qs;
+    if (qs < pol.K) {
+      uint32_t cq = __ldcg(c + qs);
+      uint32_t take = pre_qs >= m ? 0 : min(cq, m - pre_qs);
+      a += take;
+      pre_qs += cq;
+    }
+    out.tile_off[tl] = a;  // count for now
+    my_c += a;
+  }
+  uint32_t total;
+  uint32_t off = block_excl_scan<uint32_t, SCAN_THREADS>(my_c, red, &total);
+  uint32_t run = off;  // counts -> exclusive offsets
+  for (uint32_t tl = t0; tl < t1; ++tl) {
+    uint32_t a = out.tile_off[tl];
+    out.tile_off[tl] = run;
+    run += a;
+  }
+  if (tid == SCAN_THREADS - 1) out.tile_off[ntiles] = total;
+  if (tid == 0) {
+    ctl->n_cand_a = total;
+    ctl->tiles_done = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a5 candidate gather: tiles with candidates re-read their 1 KB of qf and emit row indices in
+// table order; the emitted rows are marked QF_INB so finalize can add the running calls of q*
+// that were not emitted.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable ct, const Ctl* ctl,
+                                                         Outputs out, uint32_t n_rows) {
+  const uint32_t tile = blockIdx.x;
+  const uint32_t off = out.tile_off[tile];
+  const uint32_t cnt = out.tile_off[tile + 1] - off;
+  if (cnt == 0) return;
+  __shared__ uint32_t red[33];
+  const uint32_t qs = ctl->qstar, m = ctl->mprime;
+  const uint32_t row0 = tile * TILE + threadIdx.x * ROWS_PER_THREAD;
+  uint32_t qw = row0 < n_rows ? *reinterpret_cast<const uint32_t*>(ct.qf + row0) : 0x40404040u;
+  // q* rows of this tile before this thread, plus the q* prefix of earlier tiles
+  uint32_t nq = 0;
+#pragma unroll
+  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
+    uint32_t qf = (qw >> (8 * j)) & 0xffu;
+    nq += (!(qf & QF_DEAD) && (qf & QF_QMASK) == qs) ? 1u : 0u;
+  }
+  const uint32_t tile_pre = out.tile_pre[tile];
+  uint32_t rq = tile_pre + block_excl_scan<uint32_t, SCAN_THREADS>(nq, red, nullptr);
+  uint32_t flags = 0, nsel = 0;
+#pragma unroll
+  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
+    uint32_t qf = (qw >> (8 * j)) & 0xffu;
+    if (qf & QF_DEAD) continue;
+    uint32_t q = qf & QF_QMASK;
+    bool sel = q < qs;
+    if (q == qs) { sel = rq < m; ++rq; }
+    if (sel) { flags |= 1u << j; ++nsel; }
+  }
+  uint32_t pos = off + block_excl_scan<uint32_t, SCAN_THREADS>(nsel, red, nullptr);
+  if (flags) {
+    uint32_t qn = qw;
+#pragma unroll
+    for (int j = 0; j < ROWS_PER_THREAD; ++j)
+      if (flags & (1u << j)) {
+        out.cand[pos++] = row0 + j;
+        qn |= (uint32_t)QF_INB << (8 * j);
+      }
+    *reinterpret_cast<uint32_t*>(ct.qf + row0) = qn;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// a5/a6/a3/a7-plan: one CTA.  Sort <= 2 BS candidates by the unique key
+// (q, arrival, not-running, seq) (R11, R12), cut the longest prefix with count <= BS and
+// sum kvb <= P (Alg. 1 l.32-39, first misfit stops, R13), emit batch/admit/preempt, account
+// (batch: exec++, mtime++, quanta--, running; others implicitly wait++ via the closed form),
+// demote batch calls whose quantum is exhausted (Alg. 1 l.20-23), allocate KV blocks and build
+// the swap plan.
+// ---------------------------------------------------------------------------------------------
+extern __shared__ unsigned char fin_smem[];
+
+__device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
+
+__global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable ct, Ctl* ctl,
+                                                          Outputs out, KvState kv, bool kv_on,
+                                                          uint32_t t, uint32_t np, uint32_t seqno) {
+  uint64_t* khi = reinterpret_cast<uint64_t*>(fin_smem);
+  uint32_t* klo = reinterpret_cast<uint32_t*>(khi + np);
+  __shared__ unsigned long long red64[33];
+  __shared__ uint32_t red[33];
+  __shared__ uint32_t s_nb;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t BS = pol.max_batch;
+  const uint32_t nA = ctl->n_cand_a, qs = ctl->qstar, n_prev = ctl->n_prev;
+  if (tid == 0) s_nb = 0;
+  __syncthreads();
+  // ---- candidate keys --------------------------------------------------------------------
+  for (uint32_t i = tid; i < np; i += FIN_THREADS) { khi[i] = ~0ull; klo[i] = ~0u; }
+  __syncthreads();
+  for (uint32_t i = tid; i < n_prev; i += FIN_THREADS) {
+    uint32_t s = out.prev_slots[i];
+    uint32_t qf = ct.qf[s];
+    if (!(qf & QF_DEAD) && (qf & QF_QMASK) == qs && !(qf & QF_INB)) {
+      uint32_t j = nA + atomicAdd(&s_nb, 1u);
+      khi[j] = ((uint64_t)qs << 33) | ((uint64_t)ct.arr[s] << 1);  // running: bit 0 clear
+      klo[j] = s;
+    }
+  }
+  __syncthreads();  // INB of region-A rows read above before it is cleared below
+  for (uint32_t i = tid; i < nA; i += FIN_THREADS) {
+    uint32_t s = out.cand[i];
+    uint32_t qf = ct.qf[s];
+    khi[i] = ((uint64_t)(qf & QF_QMASK) << 33) | ((uint64_t)ct.arr[s] << 1) | ((qf & QF_RUN) ? 0u : 1u);
+    klo[i] = s;
+    ct.qf[s] = (uint8_t)(qf & ~QF_INB);
+  }
+  __syncthreads();
+  const uint32_t ncand = nA + s_nb;
+  bitonic_sort_pairs<FIN_THREADS>(khi, klo, np);
+  // ---- prefix cutoff on BS and P ------------------------------------------------------------
+  const uint32_t m = min(BS, ncand);
+  uint32_t kvb_mine[4];
+  uint32_t nb_local = 0;
+  // up to 4 candidates per thread (BS <= 4096)
+  unsigned long long carry = 0;
+#pragma unroll
+  for (uint32_t r = 0; r < 4; ++r) {
+    uint32_t i = r * FIN_THREADS + tid;
+    uint32_t kb = 0;
+    if (i < m) {
+      uint32_t s = klo[i];
+      kb = ceil_div_u32(ct.tok[s] + ct.exec[s] + 1, pol.block_tokens);
+    }
+    kvb_mine[r] = kb;
+    unsigned long long tot;
+    unsigned long long pre = block_excl_scan<unsigned long long, FIN_THREADS>(kb, red64, &tot);
+    unsigned long long incl = carry + pre + kb;
+    if (i < m && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) ++nb_local;
+    carry += tot;
+  }
+  const uint32_t n_batch = block_sum<uint32_t, FIN_THREADS>(nb_local, red);
+  if (tid == 0 && ncand > 0 && n_batch == 0) {
+    if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u) ctl->err_info = klo[0];
+  }
+  // ---- batch list, INB marks ---------------------------------------------------------------
+  unsigned long long kv_sum = 0;
+#pragma unroll
+  for (uint32_t r = 0; r < 4; ++r) {
+    uint32_t i = r * FIN_THREADS + tid;
+    if (i < n_batch) {
+      uint32_t s = klo[i];
+      out.batch_slots[i] = s;
+      uint64_t id = ct.cid[s];
+      out.batch_ids[i] = id;
+      out.h_batch[i] = id;
+      ct.qf[s] = (uint8_t)(ct.qf[s] | QF_INB);
+      kv_sum += kvb_mine[r];
+    }
+  }
+  kv_sum = block_sum<unsigned long long, FIN_THREADS>(kv_sum, red64);
+  __syncthreads();
+  // ---- preempt = resident (previous batch, still active) not in the batch --------------------
+  unsigned long long swap_out = 0, swap_in = 0;
+  uint32_t n_preempt = 0;
+  {
+    uint32_t base_off = 0;
+    for (uint32_t c0 = 0; c0 < n_prev; c0 += FIN_THREADS) {
+      uint32_t i = c0 + tid;
+      uint32_t s = i < n_prev ? out.prev_slots[i] : 0;
+      uint32_t qf = i < n_prev ? ct.qf[s] : QF_DEAD;
+      uint32_t is_pre = (!(qf & QF_DEAD) && !(qf & QF_INB)) ? 1u : 0u;
+      uint32_t tot;
+      uint32_t pos = base_off + block_excl_scan<uint32_t, FIN_THREADS>(is_pre, red, &tot);
+      if (is_pre) {
+        uint32_t held = ceil_div_u32(ct.tok[s] + ct.exec[s], pol.block_tokens);
+        swap_out += held;
+        uint64_t id = ct.cid[s];
+        out.preempt_ids[pos] = id;
+        out.h_preempt[pos] = id;
+        out.preempt_slots[pos] = s;
+        ct.qf[s] = (uint8_t)(qf & ~(QF_RUN | QF_RES));
+      }
+      base_off += tot;
+    }
+    n_preempt = base_off;
+  }
+  // ---- admit = batch calls not resident --------------------------------------------------------
+  uint32_t n_admit = 0;
+  {
+    uint32_t base_off = 0;
+    for (uint32_t c0 = 0; c0 < n_batch; c0 += FIN_THREADS) {
+      uint32_t i = c0 + tid;
+      uint32_t s = i < n_batch ? klo[i] : 0;
+      uint32_t qf = i < n_batch ? ct.qf[s] : QF_RES;
+      uint32_t is_ad = (qf & QF_RES) ? 0u : 1u;
+      uint32_t tot;
+      uint32_t pos = base_off + block_excl_scan<uint32_t, FIN_THREADS>(is_ad, red, &tot);
+      if (is_ad) {
+        uint64_t id = ct.cid[s];
+        out.admit_ids[pos] = id;
+        out.h_admit[pos] = id;
+        out.admit_slots[pos] = s;
+        uint32_t ex = ct.exec[s];
+        if (ex > 0) swap_in += ceil_div_u32(ct.tok[s] + ex, pol.block_tokens);
+      }
+      base_off += tot;
+    }
+    n_admit = base_off;
+  }
+  swap_out = block_sum<unsigned long long, FIN_THREADS>(swap_out, red64);
+  swap_in = block_sum<unsigned long long, FIN_THREADS>(swap_in, red64);
+
+  // ---- KV blocks: swap plan + allocation (a7) --------------------------------------------------
+  if (kv_on) {
+    const uint32_t W = pol.max_blocks_per_call;
+    // (1) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots
+    uint32_t base_blk = 0, base_free = 0;
+    const uint32_t top0 = ctl->free_top, rtop0 = ctl->rs_free_top;
+    for (uint32_t c0 = 0; c0 < n_preempt; c0 += FIN_THREADS) {
+      uint32_t i = c0 + tid;
+      uint32_t s = 0, rslot = 0, nb = 0;
+      if (i < n_preempt) {
+        s = out.preempt_slots[i];
+        rslot = ct.loc[s];
+        nb = kv.rs_nblk[rslot];
+      }
+      uint32_t tot;
+      uint32_t boff = base_blk + block_excl_scan<uint32_t, FIN_THREADS>(nb, red, &tot);
+      if (i < n_preempt) {
+        uint32_t cls = ceil_log2(nb);
+        // pop a page range of 2^cls pages from the class stack, else bump-allocate
+        uint32_t page;
+        uint32_t k = atomicSub(&ctl->host_free_top[cls], 1u);
+        if ((int32_t)k > 0) {
+          page = kv.host_free[(size_t)cls * kv.host_free_cap + k - 1];
+        } else {
+          atomicAdd(&ctl->host_free_top[cls], 1u);
+          page = atomicAdd(&ctl->host_bump, 1u << cls);
+          if ((uint64_t)page + (1u << cls) > pol.host_pages_lo) set_err(ctl, AUTX_E_NOMEM, 1);
+        }
+        ct.loc[s] = page;
+        ct.hcls[s] = cls;
+        kv.plan_out[i] = PlanItem{page, nb, boff};
+        const uint32_t* src = kv.rs_blocks + (size_t)rslot * W;
+        for (uint32_t j = 0; j < nb; ++j) {
+          uint32_t b = src[j];
+          kv.plan_out_blocks[boff + j] = b;
+          kv.free_stack[top0 + boff + j] = b;
+        }
+        kv.rs_nblk[rslot] = 0;
+      }
+      uint32_t rt;
+      uint32_t roff = base_free + block_excl_scan<uint32_t, FIN_THREADS>(i < n_preempt ? 1u : 0u, red, &rt);
+      if (i < n_preempt) kv.rs_free[rtop0 + roff] = rslot;
+      base_blk += tot;
+      base_free += rt;
+    }
+    __syncthreads();
+    uint32_t top = top0 + base_blk, rtop = rtop0 + base_free;
+    // (2) batch calls: grow/allocate to kvb; admitted calls take a resident slot
+    uint32_t pop_base = 0, rs_pop = 0, in_blk = 0, in_items = 0;
+    for (uint32_t c0 = 0; c0 < n_batch; c0 += FIN_THREADS) {
+      uint32_t i = c0 + tid;
+      uint32_t s = 0, need = 0, have = 0, rslot = NONE, admit = 0, held = 0;
+      if (i < n_batch) {
+        s = klo[i];
+        uint32_t qf = ct.qf[s];
+        need = ceil_div_u32(ct.tok[s] + ct.exec[s] + 1, pol.block_tokens);
+        if (need > W) set_err(ctl, AUTX_E_NOMEM, 2);
+        if (qf & QF_RES) {
+          rslot = ct.loc[s];
+          have = kv.rs_nblk[rslot];
+        } else {
+          admit = 1;
+          if (ct.exec[s] > 0) held = ceil_div_u32(ct.tok[s] + ct.exec[s], pol.block_tokens);
+        }
+      }
+      uint32_t alloc = need > have ? need - have : 0;
+      uint32_t tot, rt, ht, it;
+      uint32_t aoff = pop_base + block_excl_scan<uint32_t, FIN_THREADS>(alloc, red, &tot);
+      uint32_t roff = rs_pop + block_excl_scan<uint32_t, FIN_THREADS>(admit, red, &rt);
+      uint32_t hoff = in_blk + block_excl_scan<uint32_t, FIN_THREADS>(held, red, &ht);
+      uint32_t ioff = in_items + block_excl_scan<uint32_t, FIN_THREADS>(held ? 1u : 0u, red, &it);
+      if (i < n_batch) {
+        if (admit) {
+          if (roff >= rtop) set_err(ctl, AUTX_E_NOMEM, 3);
+          rslot = kv.rs_free[rtop - 1 - roff];
+        }
+        if (aoff + alloc > top) set_err(ctl, AUTX_E_NOMEM, 4);
+        uint32_t* dst = kv.rs_blocks + (size_t)rslot * W;
+        for (uint32_t j = 0; j < alloc && have + j < W && aoff + j < top; ++j)
+          dst[have + j] = kv.free_stack[top - 1 - aoff - j];
+        kv.rs_nblk[rslot] = need;
+        if (held) {
+          // swap-in: host copy -> the first `held` blocks of the new list; free host pages after
+          uint32_t page = ct.loc[s];
+          kv.plan_in[ioff] = PlanItem{page, held, hoff};
+          for (uint32_t j = 0; j < held; ++j) kv.plan_in_blocks[hoff + j] = dst[j];
+        }
+        ct.loc[s] = rslot;
+      }
+      pop_base += tot;
+      rs_pop += rt;
+      in_blk += ht;
+      in_items += it;
+    }
+    __syncthreads();
+    // (3) free the host ranges of swapped-in calls (after this step's swap-out allocations)
+    for (uint32_t c0 = 0; c0 < n_batch; c0 += FIN_THREADS) {
+      uint32_t i = c0 + tid;
+      if (i < in_items) {
+        PlanItem it = kv.plan_in[i];
+        uint32_t cls = ceil_log2(it.nblk);
+        uint32_t k = atomicAdd(&ctl->host_free_top[cls], 1u);
+        kv.host_free[(size_t)cls * kv.host_free_cap + k] = (uint32_t)it.host_page;
+      }
+    }
+    // (4) block table CSR of the batch
+    uint32_t b0 = 0;
+    for (uint32_t c0 = 0; c0 < n_batch; c0 += FIN_THREADS) {
+      uint32_t i = c0 + tid;
+      uint32_t need = 0, rslot = 0;
+      if (i < n_batch) { rslot = ct.loc[klo[i]]; need = kv.rs_nblk[rslot]; }
+      uint32_t tot;
+      uint32_t o = b0 + block_excl_scan<uint32_t, FIN_THREADS>(need, red, &tot);
+      if (i < n_batch) {
+        kv.bt_offsets[i] = o;
+        const uint32_t* src = kv.rs_blocks + (size_t)rslot * W;
+        for (uint32_t j = 0; j < need && o + j < kv.plan_cap; ++j) kv.bt_blocks[o + j] = src[j];
+      }
+      b0 += tot;
+    }
+    if (tid == 0) {
+      kv.bt_offsets[n_batch] = b0;
+      ctl->free_top = top - pop_base;
+      ctl->rs_free_top = rtop - rs_pop;
+      ctl->n_plan_out = n_preempt;
+      ctl->n_plan_in = in_items;
+      ctl->plan_out_chunks = base_blk;
+      ctl->plan_in_chunks = in_blk;
+    }
+    __syncthreads();
+  }
+
+  // ---- step accounting + eager demotion (Alg. 1 l.20-23) for the batch --------------------
+  for (uint32_t i = tid; i < n_batch; i += FIN_THREADS) {
+    uint32_t s = klo[i];
+    uint32_t qf = ct.qf[s];
+    uint32_t q = qf & QF_QMASK;
+    ct.exec[s] += 1;
+    ct.mtime[s] += 1;
+    uint32_t qt = ct.quanta[s];
+    if (qt != AUTX_INF) {
+      qt -= 1;
+      if (qt == 0) {
+        q = min(q + 1, pol.K - 1);
+        qt = pol.quanta[q];
+      }
+      ct.quanta[s] = qt;
+    }
+    ct.qf[s] = (uint8_t)(q | QF_RUN | QF_RES);
+    out.prev_slots[i] = s;
+  }
+  if (tid == 0) {
+    ctl->n_prev = n_batch;
+    HostOut h;
+    h.n_batch = n_batch;
+    h.n_admit = n_admit;
+    h.n_preempt = n_preempt;
+    h.n_active = ctl->n_live;
+    h.swap_out_blocks = swap_out;
+    h.swap_in_blocks = swap_in;
+    h.kv_blocks = kv_sum;
+    h.n_promoted = ctl->n_promoted;
+    h.err = ctl->err;
+    h.seqno = seqno;
+    h._pad = 0;
+    *out.hout = h;
+    ctl->n_promoted = 0;
+    ctl->n_live = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------------------------
+cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                            const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
+                            CompRec* rec_out, bool apply) {
+  k_complete<<<1, FIN_THREADS, 0, s>>>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,
+                         uint64_t stride, uint32_t G, uint32_t t) {
+  k_apply<<<1, FIN_THREADS, 0, s>>>(pol, pt, (const char*)base, stride, G, t);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,
+                         const RouteArr* arr, uint32_t n, int8_t* pin, uint32_t threshold,
+                         int32_t* out) {
+  if (n) k_route<<<1, 32, 0, s>>>((const char*)base, stride, G, arr, n, pin, threshold, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt,
+                            const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t) {
+  if (n == 0) return cudaSuccess;
+  k_register<<<(n + 255) / 256, 256, 0, s>>>(pol, ct, pt, recs, n, first_slot, t);
+  return cudaGetLastError();
+}
+
+static uint32_t pow2_at_least(uint32_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                        Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
+                        uint32_t seqno, cudaEvent_t* ev) {
+  uint32_t ntiles = (n_rows + TILE - 1) / TILE;
+  if (ntiles == 0) ntiles = 1;
+  if (ev) cudaEventRecord(ev[0], s);
+  k_scan<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, pt, ctl, out, t, n_rows);
+  if (ev) cudaEventRecord(ev[1], s);
+  k_gather<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, ctl, out, n_rows);
+  if (ev) cudaEventRecord(ev[2], s);
+  uint32_t np = pow2_at_least(2 * pol.max_batch);
+  size_t smem = (size_t)np * (sizeof(uint64_t) + sizeof(uint32_t));
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  k_finalize<<<1, FIN_THREADS, smem, s>>>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  if (ev) cudaEventRecord(ev[3], s);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// G8: stable compaction of the call table (drop completed rows, keep (arrival, seq) order).
+// live[i] = old row of the i-th live row in table order; dst gets rows 0..n_live-1.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_compact(CallTable src, CallTable dst, const uint32_t* live, uint32_t n_live) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_live) return;
+  uint32_t s = live[i];
+  dst.cid[i] = src.cid[s];
+  dst.prog[i] = src.prog[s];
+  dst.arr[i] = src.arr[s];
+  dst.qf[i] = src.qf[s];
+  dst.base[i] = src.base[s];
+  dst.mtime[i] = src.mtime[s];
+  dst.exec[i] = src.exec[s];
+  dst.quanta[i] = src.quanta[s];
+  dst.inh[i] = src.inh[s];
+  dst.tok[i] = src.tok[s];
+  dst.loc[i] = src.loc[s];
+  dst.hcls[i] = src.hcls[s];
+}
+
+__global__ void k_remap(uint32_t* slots, uint32_t n, const uint32_t* old2new) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) slots[i] = old2new[slots[i]];
+}
+
+cudaError_t launch_compact(cudaStream_t s, CallTable src, CallTable dst, const uint32_t* live,
+                           uint32_t n_live) {
+  if (n_live) k_compact<<<(n_live + 255) / 256, 256, 0, s>>>(src, dst, live, n_live);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_remap(cudaStream_t s, uint32_t* slots, uint32_t n, const uint32_t* old2new) {
+  if (n) k_remap<<<(n + 255) / 256, 256, 0, s>>>(slots, n, old2new);
+  return cudaGetLastError();
+}
+
+}  // namespace autx

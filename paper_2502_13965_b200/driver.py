@@ -1,0 +1,114 @@
+"""Workload driver for the CUDA scheduler: feeds a synthetic trace through the C ABI step by
+step.  It plays the roles the paper puts outside the scheduler: the agentic programs (DAG
+readiness after parents finish plus interrupt delays), the frontend's
+session start/end, and the model executor's decode lengths (hidden from the scheduler:
+non-clairvoyance).  It holds none of the scheduling arithmetic.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .autx import CALL_DESC
+
+
+class TraceDriver:
+    def __init__(self, trace, sched, log_lists=True):
+        self.tr = trace
+        self.s = sched
+        self.log_lists = log_lists
+        C = trace.n_calls
+        self.remaining = trace.decode.astype(np.int64).copy()
+        self.n_par_left = np.diff(trace.par_ptr).astype(np.int64)
+        # child adjacency (CSR) from the parent lists
+        cnt = np.bincount(trace.par, minlength=C) if len(trace.par) else np.zeros(C, np.int64)
+        self.cptr = np.concatenate([[0], np.cumsum(cnt)])
+        owner = np.repeat(np.arange(C), np.diff(trace.par_ptr))
+        self.child = owner[np.argsort(trace.par, kind="stable")]
+        self.calls_left = np.diff(trace.first_call).astype(np.int64)
+        self.ready = {}
+        roots = np.nonzero(self.n_par_left == 0)[0]
+        rt = trace.prog_arrival[trace.call_prog[roots]] + trace.delay[roots]
+        for step in np.unique(rt):
+            self.ready[int(step)] = list(roots[rt == step])
+        self.pending = np.zeros(0, np.int64)   # call indices completed in the last step
+        self.done = 0
+        self.t = 0
+        self.log = []
+        self.total_wait = 0
+
+    def idx_of(self, cids):
+        cids = np.asarray(cids, np.uint64)
+        prog = (cids >> np.uint64(16)).astype(np.int64)
+        return self.tr.first_call[prog] + (cids & np.uint64(0xFFFF)).astype(np.int64)
+
+    def finished(self):
+        return self.done == self.tr.n_calls
+
+    def _release(self, t, done_idx):
+        tr = self.tr
+        ended = []
+        for c in done_idx:
+            self.done += 1
+            p = tr.call_prog[c]
+            self.calls_left[p] -= 1
+            if self.calls_left[p] == 0:
+                ended.append(int(tr.prog_id[p]))
+            for ch in self.child[self.cptr[c]:self.cptr[c + 1]]:
+                self.n_par_left[ch] -= 1
+                if self.n_par_left[ch] == 0:
+                    self.ready.setdefault(int(t + tr.delay[ch]), []).append(ch)
+        return ended
+
+    def arrivals(self, t):
+        tr = self.tr
+        cs = np.asarray(self.ready.pop(t, []), np.int64)
+        d = np.zeros(len(cs), CALL_DESC)
+        if len(cs) == 0:
+            return d
+        p = tr.call_prog[cs]
+        d["call_id"] = tr.call_id[cs]
+        d["program_id"] = tr.prog_id[p]
+        d["arrival_step"] = t
+        d["program_arrival_step"] = tr.prog_arrival[p]
+        d["input_tokens"] = tr.input_tokens[cs]
+        order = np.lexsort((d["call_id"], d["program_id"], d["program_arrival_step"]))
+        return d[order]
+
+    def step(self):
+        """One engine step through the C ABI; returns the decision record."""
+        t = self.t
+        s = self.s
+        if len(self.pending):
+            s.complete(self.tr.call_id[self.pending])
+        ended = self._release(t, self.pending)
+        for pid in ended:
+            s.end_program(pid)
+        arr = self.arrivals(t)
+        if len(arr):
+            s.register(arr)
+        out = s.sched_step(t)
+        batch, admit, preempt = s.lists()
+        rec = dict(t=t, n_batch=int(out.n_batch), swap_out_blocks=int(out.swap_out_blocks),
+                   swap_in_blocks=int(out.swap_in_blocks), kv_blocks=int(out.kv_blocks),
+                   n_active=int(out.n_active), n_promoted=int(out.n_promoted))
+        if self.log_lists:
+            rec.update(batch=[int(x) for x in batch], admit=[int(x) for x in admit],
+                       preempt=[int(x) for x in preempt])
+        self.log.append(rec)
+        # engine model: one decode step for every batch call
+        bi = self.idx_of(batch)
+        self.remaining[bi] -= 1
+        self.pending = bi[self.remaining[bi] == 0]
+        self.t = t + 1
+        return rec
+
+    def run(self, max_steps=10 ** 9):
+        for _ in range(max_steps):
+            if self.finished():
+                break
+            if len(self.pending) == 0 and self.s.num_active() == 0 and self.t not in self.ready:
+                if not self.ready:
+                    break
+                self.t = min(self.ready)   # idle: jump to the next arrival
+            self.step()
+        return self.log
