@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the Autellix scheduler hot path on B200 (BASELINE.json metric:
+"sched decisions/s at 1M active calls; KV swap GB/s; % roofline at 1/2/4/8 GPUs").
+
+A step = one pass of SURVEY §8(a) rows a1-a6 (+ a8 when N > 1) through the C ABI over the
+whole active set: completions of the previous step, arrivals, demotion, anti-starvation,
+ordering, cutoff, admit/preempt lists and accounting.  Workload (BASELINE configs[3]): an
+offline burst of 50/50 LATS-MCTS and map-reduce DAG programs with ~1M calls ready at
+step 0, ATLAS, SPEC ladder (K=8), beta=2, BS=1024, KV budget 32768 blocks of 16 tokens;
+decisions/s = active calls ranked per step / device step time.  The KV swap (row a7) is timed
+in a second phase on the ReAct-shaped config with 8B-geometry pools (32 layers x 32 KiB
+chunks) and reported under "swap".
+
+Timing: W warm-up steps, then K steps; before each step L2 is flushed (a 512 MiB write) and a
+spin kernel gates the stream while the host enqueues the step, so CUDA events around the step
+measure device time only.  Multi-GPU: one rank per GPU (torchrun), each rank runs its own
+1M-call shard (weak scaling); every step includes the routing epoch (completion records + load
+all-gathered over NCCL, Alg. 2 over the replicated arrivals).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+SCAN_BYTES_PER_CALL = 13      # qf 1 + prog 4 + base 4 + mtime 4
+PROMOTE_BYTES = 13            # qf 1 + base 4 + mtime 4 + quanta 4 written per promotion
+PROG_BYTES = 12               # svc 4 + pwait 8 gathered per program
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="autx", choices=["autx", "reference"])
+    ap.add_argument("--active", type=int, default=1_000_000)
+    ap.add_argument("--ff", type=int, default=100, help="fast-forward steps before warm-up")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-swap", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--swap-steps", type=int, default=60)
+    ap.add_argument("--order", default="select", choices=["select", "radix"])
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        d = json.load(open(MEASURED_PEAKS))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def spec_ladder():
+    """SPEC default ladder: K=8, hi_i = 2*4^(i-1), quanta = band widths."""
+    hi = tuple(2 * 4 ** i for i in range(7))
+    lo = (0,) + hi
+    quanta = tuple(hi[i] - lo[i] for i in range(7)) + (None,)
+    return dict(K=8, q_hi=hi, quanta=quanta)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, path):
+        self.path = path
+        self.p = None
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self, device=0):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or f[0] != str(device):
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init(n):
+    import torch
+    import torch.distributed as dist
+    if n <= 1 or "RANK" not in os.environ:
+        return 0, 1, 0
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------------------------------
+# reference arm: the CPU oracle as it stands, on a bounded sample of the same workload
+# ------------------------------------------------------------------------------------------
+def oracle_decisions_per_s(active, steps, warmup, seed_off=0):
+    from autx_workload import burst_mcts_mapreduce, BASE_SEED, CONFIG_INDEX
+    from oracle.autellix import Engine, Workload, Config
+    lad = spec_ladder()
+    tr = burst_mcts_mapreduce(active, seed=BASE_SEED + CONFIG_INDEX["mcts"] + seed_off)
+    cfg = Config(policy="atlas", beta=(2, 1), max_batch=1024, kv_budget=32768, **lad)
+    eng = Engine(cfg, check_formulations=False)
+    wl = Workload(tr)
+    completed = []
+    times, decisions = [], 0
+    t0 = time.perf_counter()
+    for t in range(1 + warmup + steps):
+        cids = [int(tr.call_id[c]) for c in completed]
+        ended = wl.release(t, completed)
+        s = time.perf_counter()
+        rec = eng.step(t, cids, wl.arrivals(t))
+        dt = time.perf_counter() - s
+        for pid in ended:
+            eng.table.end_program(pid)
+        completed = wl.ran(t, rec["batch"])
+        if t > warmup:  # step 0 registers the whole burst: setup, not timed
+            times.append(dt)
+            decisions += rec["n_active"]
+    return decisions / sum(times), sum(times) / len(times), time.perf_counter() - t0, tr.n_calls
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    active = max(10_000, args.active // 10)
+    steps = max(1, min(args.steps, 10))
+    v, per_step, wall, _ = oracle_decisions_per_s(active, steps, min(args.warmup, 3))
+    line = {"metric": "sched decisions/s at 1M active calls", "value": v, "unit": "decisions/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": min(args.warmup, 3),
+            "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "mcts_mapreduce_burst", "active_calls": active, "policy": "atlas",
+                       "max_batch": 1024, "kv_budget_blocks": 32768, "sample": "1/10 of the 1M burst"},
+            "cpu_baseline": {"value": v, "unit": "decisions/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{active}-call burst (1/10 of the 1M config), {steps} steps after setup"},
+            "e2e": {"value": v, "unit": "decisions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# KV swap phase (row a7)
+# ------------------------------------------------------------------------------------------
+def host_link_peak(torch, nbytes=1 << 30):
+    dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    res = {}
+    for name, (dst, src) in {"d2h": (host, dev), "h2d": (dev, host)}.items():
+        best = 0.0
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src, non_blocking=True)
+            b.record()
+            b.synchronize()
+            best = max(best, nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)
+        res[name] = best
+    del dev, host
+    return res
+
+
+def bench_swap(torch, args, link):
+    from autx_workload import react, BASE_SEED, CONFIG_INDEX
+    from paper_2502_13965_b200 import Scheduler, TraceDriver, SWAP_SM, SWAP_STAGED_DMA, SWAP_PER_CHUNK_MEMCPY
+    L, chunk = 32, 32 << 10                 # LLaMA-3.1-8B: 32 layers x 8 KV heads x 128 x bf16 x 16 tok
+    page = L * 2 * chunk                    # 2 MiB per logical block
+    P, host_pages = 2048, 6144
+    kp = [torch.empty(P, chunk, dtype=torch.uint8, device="cuda") for _ in range(L)]
+    vp = [torch.empty(P, chunk, dtype=torch.uint8, device="cuda") for _ in range(L)]
+    host = torch.empty(host_pages * page, dtype=torch.uint8).pin_memory()
+    lad = spec_ladder()
+    results = {}
+    for name, mode in (("sm", SWAP_SM), ("staged_dma", SWAP_STAGED_DMA), ("per_chunk_memcpy", SWAP_PER_CHUNK_MEMCPY)):
+        tr = react(3000, seed=BASE_SEED + CONFIG_INDEX["react"])
+        s = Scheduler(policy="plas", beta=(2, 1), max_batch=64, kv_budget=P, block_tokens=16,
+                      max_calls=1 << 16, max_programs=1 << 14, n_gpu_blocks=P, max_blocks_per_call=2048,
+                      host_pages=host_pages, **lad)
+        d = TraceDriver(tr, s, log_lists=False)
+        tot_b = tot_ms = 0.0
+        b_d2h = b_h2d = 0
+        n = 0
+        t_at_peak = 0.0
+        for i in range(args.swap_steps + 20):
+            if not d.skip_idle():
+                break
+            d.step()
+            st = s.kv_swap([x.data_ptr() for x in kp], [x.data_ptr() for x in vp], chunk,
+                           host.data_ptr(), host.numel(), mode)
+            if i >= 20 and (st.bytes_d2h + st.bytes_h2d) > 0:
+                tot_b += st.bytes_d2h + st.bytes_h2d
+                tot_ms += st.ms
+                b_d2h += st.bytes_d2h
+                b_h2d += st.bytes_h2d
+                t_at_peak += st.bytes_d2h / (link["d2h"] * 1e9) + st.bytes_h2d / (link["h2d"] * 1e9)
+                n += 1
+        s.close()
+        if n:
+            gbs = tot_b / (tot_ms * 1e-3) / 1e9
+            results[name] = {"GB/s": round(gbs, 2), "steps": n, "bytes_d2h": b_d2h, "bytes_h2d": b_h2d,
+                             "ms_per_step": tot_ms / n, "frac_of_host_link": round(t_at_peak / (tot_ms * 1e-3), 4)}
+    del kp, vp, host
+    return results
+
+
+# ------------------------------------------------------------------------------------------
+# main arm
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    import torch
+    rank, world, local = dist_init(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch.distributed as dist
+    from autx_workload import burst_mcts_mapreduce, BASE_SEED, CONFIG_INDEX
+    from paper_2502_13965_b200 import Scheduler, TraceDriver, ORDER_SELECT, ORDER_RADIX
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    hbm_peak, peak_src = peaks()
+
+    t_gen = time.time()
+    tr = burst_mcts_mapreduce(args.active, seed=BASE_SEED + CONFIG_INDEX["mcts"] + 1000 * rank)
+    t_gen = time.time() - t_gen
+    lad = spec_ladder()
+    s = Scheduler(policy="atlas", beta=(2, 1), max_batch=1024, kv_budget=32768, block_tokens=16,
+                  max_calls=int(args.active * 1.25) + 4096, max_programs=tr.n_programs + 1024,
+                  order_mode=ORDER_RADIX if args.order == "radix" else ORDER_SELECT,
+                  device=local, stream=stream.cuda_stream, **lad)
+    d = TraceDriver(tr, s, log_lists=False)
+    t_setup = time.time()
+    d.step()                                  # step 0: registers the whole burst (setup)
+    for _ in range(args.ff):
+        d.step()
+    t_setup = time.time() - t_setup
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    s.set_timing(True)
+    gate_cycles = 2_000_000                   # ~1 ms spin while the host enqueues the step
+
+    def timed_step():
+        if not args.no_flush:
+            flush.zero_()
+        torch.cuda._sleep(gate_cycles)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        nc, na = d.issue()
+        b.record(stream)
+        rec = d.finish()
+        tm = s.last_step_timing()
+        return a.elapsed_time(b), rec, tm, nc, na
+
+    for _ in range(args.warmup):
+        timed_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_r{rank}.csv") if os.path.isdir(
+        os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_r{rank}.csv")
+    clocks.start()
+    ms, decisions, launches = [], 0, 0
+    scan_ms, fin_ms, sel_ms, comp_ms, reg_ms = [], [], [], [], []
+    scan_bytes = []
+    promoted = []
+    for _ in range(args.steps):
+        dt, rec, tm, nc, na = timed_step()
+        ms.append(dt)
+        decisions += rec["n_active"]
+        launches += 3 + (1 if nc else 0) + (1 if na else 0)
+        scan_ms.append(tm.scan_ms); sel_ms.append(tm.select_ms); fin_ms.append(tm.finalize_ms)
+        comp_ms.append(tm.complete_ms); reg_ms.append(tm.register_ms)
+        promoted.append(rec["n_promoted"])
+        scan_bytes.append(SCAN_BYTES_PER_CALL * rec["n_active"] + PROMOTE_BYTES * rec["n_promoted"]
+                          + PROG_BYTES * tr.n_programs)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop(local)
+    total_ms = sum(ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dd = torch.tensor([decisions], device=dev, dtype=torch.float64)
+        dist.all_reduce(dd)
+        decisions = float(dd.item())
+    value = decisions / (total_ms * 1e-3)
+    ms_per_step = total_ms / args.steps
+
+    # e2e: the same steps through the public API from the host, wall clock, no gate/flush
+    s.set_timing(False)
+    e2e_dec, e2e_s, h2d, d2h = 0, 0.0, 0, 0
+    for _ in range(min(args.steps, 100)):
+        nc = len(d.pending)
+        t0 = time.perf_counter()
+        _, na = d.issue()
+        rec = d.finish()
+        e2e_s += time.perf_counter() - t0
+        e2e_dec += rec["n_active"]
+        h2d += 4 * nc + 24 * na
+        d2h += 8 * (rec["n_batch"] + rec["n_admit"] + rec["n_preempt"]) + 48
+    e2e_steps = min(args.steps, 100)
+    s.close()
+
+    scan_avg_ms = statistics.mean(scan_ms)
+    achieved = statistics.mean(scan_bytes) / (scan_avg_ms * 1e-3) / 1e9
+    result = {
+        "metric": "sched decisions/s at 1M active calls", "value": value, "unit": "decisions/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": "mcts_mapreduce_burst (BASELINE configs[3])", "active_calls": args.active,
+                   "programs": tr.n_programs, "policy": "atlas", "ladder": "SPEC K=8", "beta": "2",
+                   "max_batch": 1024, "kv_budget_blocks": 32768, "fast_forward_steps": args.ff,
+                   "order": args.order, "l2": "flushed before every step (512 MiB write)" if not args.no_flush else "hot",
+                   "parallelism": f"engines{world} (one scheduler per GPU)"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "k_scan (dense anti-starvation + queue counts)",
+                     "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": int(statistics.mean(scan_bytes))},
+        "breakdown_ms": {"complete": statistics.mean(comp_ms), "register": statistics.mean(reg_ms),
+                         "scan": scan_avg_ms, "gather": statistics.mean(sel_ms),
+                         "finalize": statistics.mean(fin_ms),
+                         "step_p10": float(np.percentile(ms, 10)), "step_p50": float(np.percentile(ms, 50)),
+                         "step_p90": float(np.percentile(ms, 90))},
+        "promotions_per_step": statistics.mean(promoted),
+        "e2e": {"value": e2e_dec / e2e_s, "unit": "decisions/s", "h2d_bytes_per_step": h2d // e2e_steps,
+                "d2h_bytes_per_step": d2h // e2e_steps, "ms_per_step": e2e_s * 1e3 / e2e_steps},
+        "setup_s": {"generate": round(t_gen, 1), "register_and_fast_forward": round(t_setup, 1)},
+    }
+    if ck:
+        result["clocks"] = ck
+    if rank == 0 and world == 1 and not args.no_swap:
+        link = host_link_peak(torch)
+        sw = bench_swap(torch, args, link)
+        result["swap"] = {"host_link_peak_GBps": {k: round(v, 2) for k, v in link.items()},
+                          "config": "react (BFCL-shaped) 3000 programs, PLAS, BS=64, P=2048 blocks, 8B geometry "
+                                    "(32 layers x K|V x 32 KiB chunks = 2 MiB/block)", **sw}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, per_step, wall, _ = oracle_decisions_per_s(args.active, 2, 0)
+        result["cpu_baseline"] = {"value": v, "unit": "decisions/s", "cores": 1, "kind": "oracle",
+                                  "sample": f"the same {args.active}-call burst, 2 steps after the setup step, "
+                                            f"{per_step:.2f} s/step single-threaded Python",
+                                  "host_cores_available": os.cpu_count()}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -78,6 +78,8 @@ struct autx_ctx {
   uint32_t rarr_cap = 0;
   bool routed_this = false;
   uint32_t n_reg_this = 0;
+  bool timed_complete = false, timed_register = false;   // events 4-5 / 6-7 recorded this step
+  bool tc_step = false, tr_step = false;                  // ... for the step being waited on
   std::string err;
 };
 
@@ -374,7 +376,10 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
   CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
   CK(launch_complete(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->d_cslots, n, t, ctx->kv,
                      ctx->kv_on, recs, ctx->cfg.nranks <= 1));
-  if (ctx->timing) cudaEventRecord(ctx->ev[5], ctx->stream);
+  if (ctx->timing) {
+    cudaEventRecord(ctx->ev[5], ctx->stream);
+    ctx->timed_complete = true;
+  }
   ctx->completed_this = true;
   ctx->n_completed_pending = n;
   return AUTX_OK;
@@ -481,7 +486,10 @@ extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* c
                      ctx->stream));
   if (ctx->timing) cudaEventRecord(ctx->ev[6], ctx->stream);
   CK(launch_register(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->d_arr, n, ctx->tail, t));
-  if (ctx->timing) cudaEventRecord(ctx->ev[7], ctx->stream);
+  if (ctx->timing) {
+    cudaEventRecord(ctx->ev[7], ctx->stream);
+    ctx->timed_register = true;
+  }
   ctx->tail += n;
   ctx->n_reg_this += n;
   ctx->registered_this = true;
@@ -515,6 +523,9 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   ctx->completed_this = ctx->registered_this = false;
   ctx->routed_this = false;
   ctx->n_reg_this = 0;
+  ctx->tc_step = ctx->timed_complete;
+  ctx->tr_step = ctx->timed_register;
+  ctx->timed_complete = ctx->timed_register = false;
   ctx->n_completed_pending = 0;
   ctx->have_last_key = false;
   memset(out, 0, sizeof *out);
@@ -547,10 +558,15 @@ extern "C" autx_status autx_step_wait(autx_ctx* ctx, autx_step_out* out) {
     cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
     cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
     cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+    float d = 0, e = 0;
+    if (ctx->tc_step) cudaEventElapsedTime(&d, ctx->ev[4], ctx->ev[5]);
+    if (ctx->tr_step) cudaEventElapsedTime(&e, ctx->ev[6], ctx->ev[7]);
     ctx->last_timing.scan_ms = a;
     ctx->last_timing.select_ms = b;
     ctx->last_timing.finalize_ms = c;
-    ctx->last_timing.total_ms = a + b + c;
+    ctx->last_timing.complete_ms = d;
+    ctx->last_timing.register_ms = e;
+    ctx->last_timing.total_ms = a + b + c + d + e;
   }
   return AUTX_OK;
 }

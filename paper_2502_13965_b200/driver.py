@@ -74,11 +74,13 @@ class TraceDriver:
         order = np.lexsort((d["call_id"], d["program_id"], d["program_arrival_step"]))
         return d[order]
 
-    def step(self):
-        """One engine step through the C ABI; returns the decision record."""
+    def issue(self):
+        """Host half of one engine step: completions, session ends, arrivals, sched_step.
+        Returns (n_completions, n_arrivals) without waiting for the device."""
         t = self.t
         s = self.s
-        if len(self.pending):
+        nc = len(self.pending)
+        if nc:
             s.complete(self.tr.call_id[self.pending])
         ended = self._release(t, self.pending)
         for pid in ended:
@@ -86,29 +88,48 @@ class TraceDriver:
         arr = self.arrivals(t)
         if len(arr):
             s.register(arr)
-        out = s.sched_step(t)
+        s.sched_step(t, wait=False)
+        return nc, len(arr)
+
+    def finish(self):
+        """Waits for the step, logs it and runs the engine model (one decode step per batch
+        call; calls whose hidden decode length is reached complete)."""
+        t = self.t
+        s = self.s
+        out = s.step_wait()
         batch, admit, preempt = s.lists()
         rec = dict(t=t, n_batch=int(out.n_batch), swap_out_blocks=int(out.swap_out_blocks),
                    swap_in_blocks=int(out.swap_in_blocks), kv_blocks=int(out.kv_blocks),
-                   n_active=int(out.n_active), n_promoted=int(out.n_promoted))
+                   n_active=int(out.n_active), n_promoted=int(out.n_promoted),
+                   n_admit=int(out.n_admit), n_preempt=int(out.n_preempt))
         if self.log_lists:
             rec.update(batch=[int(x) for x in batch], admit=[int(x) for x in admit],
                        preempt=[int(x) for x in preempt])
         self.log.append(rec)
-        # engine model: one decode step for every batch call
         bi = self.idx_of(batch)
         self.remaining[bi] -= 1
         self.pending = bi[self.remaining[bi] == 0]
         self.t = t + 1
         return rec
 
+    def skip_idle(self):
+        """Jumps over steps with nothing active; returns False when the trace is done."""
+        if self.finished():
+            return False
+        if len(self.pending) == 0 and self.s.num_active() == 0 and self.t not in self.ready:
+            if not self.ready:
+                return False
+            self.t = min(self.ready)
+        return True
+
+    def step(self):
+        """One engine step through the C ABI; returns the decision record."""
+        self.issue()
+        return self.finish()
+
     def run(self, max_steps=10 ** 9):
         for _ in range(max_steps):
-            if self.finished():
+            if not self.skip_idle():
                 break
-            if len(self.pending) == 0 and self.s.num_active() == 0 and self.t not in self.ready:
-                if not self.ready:
-                    break
-                self.t = min(self.ready)   # idle: jump to the next arrival
             self.step()
         return self.log

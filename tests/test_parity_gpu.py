@@ -135,7 +135,7 @@ def test_state_after_every_step(seed):
     s.close()
 
 
-@pytest.mark.parametrize("policy,kv", [(PLAS, None), (PLAS, 2000), (ATLAS, 3000), (MLFQ, 2000)])
+@pytest.mark.parametrize("policy,kv", [(PLAS, None), (PLAS, 2100), (ATLAS, 3000), (MLFQ, 2100)])
 def test_chatbot_slice(policy, kv):
     """ShareGPT-shaped chains, SPEC ladder, beta = 2, BS = 32, a binding KV
     budget: many preemptions, promotions and swaps."""
@@ -216,7 +216,7 @@ def test_kv_swap_round_trip_bytes(mode):
     from paper_2502_13965_b200 import TraceDriver
     tr = chatbot(120)
     L, chunk = 2, 1024
-    P = 1500
+    P = 2100
     nblk = P
     cfg = spec_ladder_config(PLAS, max_batch=16, kv_budget=P)
     want, _ = oracle_records(tr, cfg)
