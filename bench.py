@@ -285,6 +285,7 @@ def main():
         nc, na = d.issue()
         b.record(stream)
         rec = d.finish()
+        b.synchronize()
         tm = s.last_step_timing()
         return a.elapsed_time(b), rec, tm, nc, na
 

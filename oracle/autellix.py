@@ -135,6 +135,10 @@ class Call:
     held: int = 0           # KV blocks held (on GPU if resident, on host otherwise)
 
 
+class CapacityError(ValueError):
+    """KV need of a single call exceeds the budget P (reading R14; AUTX_E_NOMEM)."""
+
+
 def ceil_div(a, b):
     return -(-a // b)
 
@@ -272,6 +276,10 @@ class Engine:
     def schedule(self, t):
         """Phases 5-7; returns the decision record."""
         batch = self.order_sorted()
+        if self.calls and not batch:
+            # the head call alone needs more than P blocks: with Alg. 1's `break` nothing can
+            # ever run again; reading R14 makes this a capacity error (AUTX_E_NOMEM)
+            raise CapacityError(f"t={t}: a call's KV need exceeds the budget (reading R14)")
         if self.check:
             alt = self.order_queues()
             assert alt == batch, f"formulations disagree at t={t}: {batch} vs {alt}"

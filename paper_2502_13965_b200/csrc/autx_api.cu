@@ -43,6 +43,12 @@ struct autx_ctx {
   uint32_t prog_next = 0;
   std::vector<uint32_t> prog_active;                  // active calls per program row
   std::vector<uint32_t> slot_prog;                    // row -> program row (host mirror)
+  std::vector<uint32_t> slot_arr;                     // row -> arrival step (host mirror)
+  std::vector<uint8_t> slot_live;                     // row -> active?
+  uint32_t low = 0;                                   // no live row below this one
+  RadixState rx{};
+  bool radix = false;
+  uint32_t radix_passes = 0;
   std::unordered_set<uint64_t> last_batch;
   bool last_batch_valid = false;
   uint32_t tail = 0;
@@ -157,6 +163,17 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->d_pin, 0xff, P, ctx->stream));
   ctx->prog_active.assign(P, 0);
   ctx->slot_prog.assign(rows, 0);
+  ctx->slot_arr.assign(rows, 0);
+  ctx->slot_live.assign(rows, 0);
+  if (c.order_mode == AUTX_ORDER_RADIX) {
+    ctx->radix = true;
+    size_t npad = (rows + 4095) / 4096 * 4096;
+    CK(dalloc(&ctx->rx.keys, npad));
+    CK(dalloc(&ctx->rx.keys_alt, npad));
+    CK(dalloc(&ctx->rx.dig_hist, 4 * 256));
+    CK(cudaHostAlloc((void**)&ctx->rx.h_dig_hist, 4 * 256 * 4, 0));
+    CK(dalloc(&ctx->rx.tile_hist, 256 * (npad / 4096)));
+  }
   // KV block allocator
   if (c.n_gpu_blocks > 0) {
     CK(cudaStreamSynchronize(ctx->stream));  // the async memsets above precede the copies below
@@ -275,10 +292,12 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
                  ctx->kv.bt_offsets, ctx->kv.bt_blocks, ctx->d_pools, ctx->staging,
-                 ctx->d_route_local, ctx->d_pin, ctx->d_rarr, ctx->d_rout};
+                 ctx->d_route_local, ctx->d_pin, ctx->d_rarr, ctx->d_rout,
+                 ctx->rx.keys, ctx->rx.keys_alt, ctx->rx.dig_hist, ctx->rx.tile_hist};
   for (void* p : dev) if (p) cudaFree(p);
   void* host[] = {ctx->out.hout, ctx->out.h_batch, ctx->out.h_admit, ctx->out.h_preempt,
-                  ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr};
+                  ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr,
+                  ctx->rx.h_dig_hist};
   for (void* p : host) if (p) cudaFreeHost(p);
   if (ctx->done) cudaEventDestroy(ctx->done);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
@@ -366,6 +385,7 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
     auto it = ctx->call_slot.find(ids[i]);
     uint32_t slot = it->second;
     ctx->h_cslots[i] = slot;
+    ctx->slot_live[slot] = 0;
     ctx->prog_active[ctx->slot_prog[slot]] -= 1;
     ctx->call_slot.erase(it);
     ctx->last_batch.erase(ids[i]);
@@ -476,6 +496,8 @@ extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* c
     uint32_t slot = ctx->tail + i;
     ctx->call_slot[d.call_id] = slot;
     ctx->slot_prog[slot] = row;
+    ctx->slot_arr[slot] = t;
+    ctx->slot_live[slot] = 1;
     ctx->prog_active[row] += 1;
   }
   const autx_call_desc& l = calls[n - 1];
@@ -511,9 +533,16 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
     return fail(ctx, AUTX_E_STATE, "cannot skip steps while calls are active");
   if (ctx->cfg.nranks > 1 && !ctx->routed_this)
     return fail(ctx, AUTX_E_STATE, "multi-engine: autx_route_apply must run every step");
+  uint32_t arr_base = 0;
+  if (ctx->radix) {
+    while (ctx->low < ctx->tail && !ctx->slot_live[ctx->low]) ++ctx->low;
+    arr_base = ctx->low < ctx->tail ? ctx->slot_arr[ctx->low] : t;
+    if (t - arr_base >= (1u << 27)) return fail(ctx, AUTX_E_NOMEM, "arrival span exceeds the 27-bit key field");
+  }
   ++ctx->seqno;
   CK(launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv, ctx->kv_on, t,
-                 ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr));
+                 ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr, ctx->radix ? &ctx->rx : nullptr,
+                 arr_base, &ctx->radix_passes));
   CK(cudaEventRecord(ctx->done, ctx->stream));
   ctx->pending_done = true;
   ctx->last_batch_valid = false;
@@ -616,9 +645,17 @@ static autx_status compact(autx_ctx* ctx) {
   uint32_t npv = (uint32_t)np.size();
   CK(cudaMemcpy(reinterpret_cast<char*>(ctx->ctl) + offsetof(Ctl, n_prev), &npv, 4, cudaMemcpyHostToDevice));
   for (auto& kv : ctx->call_slot) kv.second = old2new[kv.second];
-  std::vector<uint32_t> sp(rows, 0);
-  for (uint32_t i = 0; i < n; ++i) sp[i] = ctx->slot_prog[lv[i]];
+  std::vector<uint32_t> sp(rows, 0), sa(rows, 0);
+  std::vector<uint8_t> sl(rows, 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    sp[i] = ctx->slot_prog[lv[i]];
+    sa[i] = ctx->slot_arr[lv[i]];
+    sl[i] = 1;
+  }
   ctx->slot_prog.swap(sp);
+  ctx->slot_arr.swap(sa);
+  ctx->slot_live.swap(sl);
+  ctx->low = 0;
   ctx->tail = n;
   void* f[] = {tmp.cid, tmp.prog, tmp.arr, tmp.qf, tmp.base, tmp.mtime, tmp.exec, tmp.quanta, tmp.inh,
                tmp.tok, tmp.loc, tmp.hcls, d_live, d_map};

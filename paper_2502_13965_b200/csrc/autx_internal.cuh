@@ -137,6 +137,15 @@ struct Outputs {
   uint64_t* h_preempt;
 };
 
+// AUTX_ORDER_RADIX buffers (radix_kernels.cu)
+struct RadixState {
+  uint64_t* keys;        // [rows padded to 4096]
+  uint64_t* keys_alt;
+  uint32_t* dig_hist;    // [4][256] global digit histograms (digits 4..7)
+  uint32_t* h_dig_hist;  // pinned mirror
+  uint32_t* tile_hist;   // [256][ntiles]
+};
+
 // Completion record (one per completed call): what UPDATE_PROCESS_TABLE needs.
 struct CompRec {
   uint32_t prog;  // process-table row (identical on every rank: rows are created in the
@@ -180,7 +189,12 @@ cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, Pro
                             const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t);
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
-                        uint32_t seqno, cudaEvent_t* ev /* 5 events or null */);
+                        uint32_t seqno, cudaEvent_t* ev /* 5 events or null */,
+                        const RadixState* rx /* non-null: AUTX_ORDER_RADIX */, uint32_t arr_base,
+                        uint32_t* radix_passes);
+cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                               Outputs out, RadixState rx, uint32_t t, uint32_t n_rows,
+                               uint32_t arr_base, int sms, uint32_t* passes_out);
 cudaError_t launch_swap(cudaStream_t s, const Ctl* ctl, KvState kv, void* const* d_kpool,
                         void* const* d_vpool, uint32_t n_layers, uint32_t chunk_bytes,
                         char* host_arena, int direction, int n_ctas);

@@ -780,13 +780,22 @@ static uint32_t pow2_at_least(uint32_t x) {
 
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
-                        uint32_t seqno, cudaEvent_t* ev) {
+                        uint32_t seqno, cudaEvent_t* ev, const RadixState* rx, uint32_t arr_base,
+                        uint32_t* radix_passes) {
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
   if (ev) cudaEventRecord(ev[0], s);
-  k_scan<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, pt, ctl, out, t, n_rows);
-  if (ev) cudaEventRecord(ev[1], s);
-  k_gather<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, ctl, out, n_rows);
+  if (rx) {
+    static int sms = 0;
+    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaError_t e = launch_radix_order(s, pol, ct, pt, ctl, out, *rx, t, n_rows, arr_base, sms, radix_passes);
+    if (e != cudaSuccess) return e;
+    if (ev) cudaEventRecord(ev[1], s);
+  } else {
+    k_scan<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, pt, ctl, out, t, n_rows);
+    if (ev) cudaEventRecord(ev[1], s);
+    k_gather<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, ctl, out, n_rows);
+  }
   if (ev) cudaEventRecord(ev[2], s);
   uint32_t np = pow2_at_least(2 * pol.max_batch);
   size_t smem = (size_t)np * (sizeof(uint64_t) + sizeof(uint32_t));

@@ -6,7 +6,7 @@ import pytest
 
 from autx_workload import fig2, random_tiny, atlas_dag_fixture, chatbot, react, mcts_mapreduce
 from oracle.autellix import (Config, Engine, Workload, simulate, fig2_config, spec_ladder_config,
-                             FCFS, MLFQ, PLAS, ATLAS)
+                             FCFS, MLFQ, PLAS, ATLAS, CapacityError)
 
 pytestmark = pytest.mark.gpu
 
@@ -78,6 +78,13 @@ def test_random_tiny(seed):
         cfg = tiny_cfg(seed * 4 + p, policy)
         try:
             want, _ = oracle_records(tr, cfg)
+        except CapacityError:
+            # a call outgrows P while decoding: the CUDA path must fail with E_NOMEM too
+            from paper_2502_13965_b200 import AutxError
+            with pytest.raises(AutxError) as e:
+                gpu_records(tr, tiny_cfg(seed * 4 + p, policy))
+            assert e.value.code == 4
+            continue
         except ValueError:
             continue  # a call's initial kvb exceeds P: the ABI rejects it too (tested below)
         assert_same(gpu_records(tr, tiny_cfg(seed * 4 + p, policy)), want)
@@ -135,7 +142,7 @@ def test_state_after_every_step(seed):
     s.close()
 
 
-@pytest.mark.parametrize("policy,kv", [(PLAS, None), (PLAS, 2100), (ATLAS, 3000), (MLFQ, 2100)])
+@pytest.mark.parametrize("policy,kv", [(PLAS, None), (PLAS, 2400), (ATLAS, 3000), (MLFQ, 2400)])
 def test_chatbot_slice(policy, kv):
     """ShareGPT-shaped chains, SPEC ladder, beta = 2, BS = 32, a binding KV
     budget: many preemptions, promotions and swaps."""
@@ -216,7 +223,7 @@ def test_kv_swap_round_trip_bytes(mode):
     from paper_2502_13965_b200 import TraceDriver
     tr = chatbot(120)
     L, chunk = 2, 1024
-    P = 2100
+    P = 2400
     nblk = P
     cfg = spec_ladder_config(PLAS, max_batch=16, kv_budget=P)
     want, _ = oracle_records(tr, cfg)
@@ -269,3 +276,28 @@ def test_kv_swap_round_trip_bytes(mode):
     assert_same(got, want)
     assert moved_out > 0 and moved_in > 0
     s.close()
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_radix_order_tiny(seed):
+    """AUTX_ORDER_RADIX (full LSD radix sort of packed keys) against the oracle."""
+    from paper_2502_13965_b200 import ORDER_RADIX
+    tr = random_tiny(seed)
+    policy = (FCFS, MLFQ, PLAS, ATLAS)[seed % 4]
+    cfg = tiny_cfg(seed * 3, policy)
+    try:
+        want, _ = oracle_records(tr, cfg)
+    except ValueError:
+        return
+    assert_same(gpu_records(tr, tiny_cfg(seed * 3, policy), order_mode=ORDER_RADIX), want)
+
+
+@pytest.mark.parametrize("policy", [PLAS, ATLAS])
+def test_radix_order_multi_tile(policy):
+    """Radix path over several 4096-key tiles with a ragged tail and a binding KV budget."""
+    from paper_2502_13965_b200 import ORDER_RADIX
+    tr = mcts_mapreduce(150) if policy == ATLAS else chatbot(1500)
+    cfg = spec_ladder_config(policy, max_batch=256, kv_budget=20000)
+    want, _ = oracle_records(tr, cfg)
+    assert_same(gpu_records(tr, spec_ladder_config(policy, max_batch=256, kv_budget=20000),
+                            order_mode=ORDER_RADIX, max_calls=1 << 16), want)
