@@ -1,0 +1,26 @@
+"""Multi-engine CUDA path: two engines (two processes sharing one B200, records exchanged
+over gloo) against the oracle's lockstep multi-engine simulation: per-engine
+decision logs and Alg. 2 routing decisions must be identical."""
+import pytest
+
+from multi_harness import run_world, oracle_multi
+
+pytestmark = pytest.mark.gpu
+
+CFGS = [
+    dict(policy="plas", K=2, q_hi=(1,), quanta=(1, None), max_batch=2, block_tokens=4, token_threshold=8),
+    dict(policy="atlas", K=3, q_hi=(2, 5), quanta=(1, 2, None), beta=(2, 1), max_batch=3,
+         block_tokens=4, token_threshold=10),
+    dict(policy="atlas", K=8, q_hi=(2, 8, 32, 128, 512, 2048, 8192), quanta=(2, 6, 24, 96, 384, 1536, 6144, None),
+         beta=(2, 1), max_batch=16, kv_budget=3000, token_threshold=2048),
+]
+
+
+@pytest.mark.parametrize("trace,seed,ci", [("tiny", 1, 0), ("tiny", 2, 1), ("tiny", 9, 1),
+                                           ("chatbot", 0, 2), ("mcts", 0, 2)])
+def test_two_engines_match_oracle(tmp_path, trace, seed, ci):
+    res = run_world(tmp_path, True, trace, seed, CFGS[ci])
+    want, routes = oracle_multi(trace, seed, CFGS[ci])
+    for r in range(2):
+        assert res[r]["log"] == want[r], f"engine {r}"
+        assert [x for x in res[r]["routes"] if x[1]] == [x for x in routes if x[1]]
