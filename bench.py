@@ -201,7 +201,7 @@ def bench_swap(torch, args, link):
     from paper_2502_13965_b200 import Scheduler, TraceDriver, SWAP_SM, SWAP_STAGED_DMA, SWAP_PER_CHUNK_MEMCPY
     L, chunk = 32, 32 << 10                 # LLaMA-3.1-8B: 32 layers x 8 KV heads x 128 x bf16 x 16 tok
     page = L * 2 * chunk                    # 2 MiB per logical block
-    P, host_pages = 2048, 6144
+    P, host_pages = 2560, 6144           # P >= the largest call's need (32768+4096 tokens)
     kp = [torch.empty(P, chunk, dtype=torch.uint8, device="cuda") for _ in range(L)]
     vp = [torch.empty(P, chunk, dtype=torch.uint8, device="cuda") for _ in range(L)]
     host = torch.empty(host_pages * page, dtype=torch.uint8).pin_memory()
@@ -210,7 +210,7 @@ def bench_swap(torch, args, link):
     for name, mode in (("sm", SWAP_SM), ("staged_dma", SWAP_STAGED_DMA), ("per_chunk_memcpy", SWAP_PER_CHUNK_MEMCPY)):
         tr = react(3000, seed=BASE_SEED + CONFIG_INDEX["react"])
         s = Scheduler(policy="plas", beta=(2, 1), max_batch=64, kv_budget=P, block_tokens=16,
-                      max_calls=1 << 16, max_programs=1 << 14, n_gpu_blocks=P, max_blocks_per_call=2048,
+                      max_calls=1 << 16, max_programs=1 << 14, n_gpu_blocks=P, max_blocks_per_call=P,
                       host_pages=host_pages, **lad)
         d = TraceDriver(tr, s, log_lists=False)
         tot_b = tot_ms = 0.0
@@ -370,9 +370,14 @@ def main():
     }
     if ck:
         result["clocks"] = ck
+    if rank == 0:
+        print("sched:", json.dumps(result), file=sys.stderr, flush=True)
     if rank == 0 and world == 1 and not args.no_swap:
         link = host_link_peak(torch)
-        sw = bench_swap(torch, args, link)
+        try:
+            sw = bench_swap(torch, args, link)
+        except Exception as e:  # keep the sched line even if the swap phase fails
+            sw = {"error": repr(e)}
         result["swap"] = {"host_link_peak_GBps": {k: round(v, 2) for k, v in link.items()},
                           "config": "react (BFCL-shaped) 3000 programs, PLAS, BS=64, P=2048 blocks, 8B geometry "
                                     "(32 layers x K|V x 32 KiB chunks = 2 MiB/block)", **sw}
