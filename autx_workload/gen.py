@@ -303,17 +303,82 @@ def _mapreduce_program(rng, fan):
 
 
 def mcts_mapreduce(n_programs=28_000, seed=None, rate=None, frac_mcts=0.5) -> Trace:
-    """50/50 LATS-MCTS and map-reduce DAG programs."""
+    """50/50 LATS-MCTS and map-reduce DAG programs, vectorised.
+
+    MCTS program with I iterations: calls 10r+i (i<5) are the expands E_{r,i}, each depending
+    on all evaluates of round r-1 (roots when r=0); calls 10r+5+i are the evaluates V_{r,i},
+    depending on E_{r,i} (same structure as `_mcts_program`).  Map-reduce program: F root maps,
+    then one reduce depending on all of them (`_mapreduce_program`)."""
     rng = rng_for(BASE_SEED + CONFIG_INDEX["mcts"] if seed is None else seed)
-    kinds = rng.random(n_programs) < frac_mcts
-    iters = lognormal_clipped(rng, *LATS_ITERS, n_programs)
-    fans = rng.integers(8, 129, n_programs)
-    progs = [_mcts_program(rng, int(iters[i])) if kinds[i] else _mapreduce_program(rng, int(fans[i]))
-             for i in range(n_programs)]
-    arr = _poisson_arrivals(rng, n_programs, rate)
-    t = _assemble("mcts_mapreduce", progs, arr)
+    n = n_programs
+    kinds = rng.random(n) < frac_mcts
+    iters = lognormal_clipped(rng, *LATS_ITERS, n)
+    fans = rng.integers(8, 129, n).astype(np.int64)
+    sizes = np.where(kinds, 2 * MCTS_WIDTH * iters, fans + 1).astype(np.int64)
+    first = np.zeros(n + 1, np.int64)
+    np.cumsum(sizes, out=first[1:])
+    C = int(first[-1])
+    call_prog = np.repeat(np.arange(n, dtype=np.int64), sizes)
+    local = np.arange(C, dtype=np.int64) - first[call_prog]
+    dec = lognormal_clipped(rng, *LATS_DECODE, C)
+    pre = lognormal_clipped(rng, *LATS_PREFILL, C)
+    is_m = kinds[call_prog]
+    W = MCTS_WIDTH
+    r = local // (2 * W)
+    k = local % (2 * W)
+    mE = is_m & (k < W) & (r >= 1)
+    mV = is_m & (k >= W)
+    mR = (~is_m) & (local == fans[call_prog])
+    cnt = np.zeros(C, np.int64)
+    cnt[mE] = W
+    cnt[mV] = 1
+    cnt[mR] = fans[call_prog[mR]]
+    par_ptr = np.zeros(C + 1, np.int64)
+    np.cumsum(cnt, out=par_ptr[1:])
+    par = np.empty(int(par_ptr[-1]), np.int64)
+    cE = np.nonzero(mE)[0]
+    baseE = first[call_prog[cE]] + 2 * W * (r[cE] - 1) + W          # V_{r-1,0}
+    par[(par_ptr[cE][:, None] + np.arange(W)).ravel()] = (baseE[:, None] + np.arange(W)).ravel()
+    cV = np.nonzero(mV)[0]
+    par[par_ptr[cV]] = cV - W                                        # E_{r,i}
+    cR = np.nonzero(mR)[0]
+    F = fans[call_prog[cR]]
+    pos = np.repeat(par_ptr[cR], F) + (np.arange(int(F.sum())) - np.repeat(np.cumsum(F) - F, F))
+    par[pos] = np.repeat(first[call_prog[cR]], F) + (pos - np.repeat(par_ptr[cR], F))
+    # contexts along the longest-token ancestor chain (S:L186)
+    ctx = pre.copy()
+    if len(cR):
+        mp = np.nonzero(~kinds)[0]
+        starts = first[mp]
+        best = _segmax(ctx + dec, starts, fans[mp])   # over the F maps of each program
+        ctx[first[mp] + fans[mp]] = pre[first[mp] + fans[mp]] + best
+    mps = np.nonzero(kinds)[0]
+    I = iters[mps]
+    for rr in range(int(I.max()) if len(I) else 0):
+        act = mps[I > rr]
+        E = (first[act] + 2 * W * rr)[:, None] + np.arange(W)
+        V = E + W
+        if rr > 0:
+            Vp = V - 2 * W
+            ctx[E] = pre[E] + (ctx[Vp] + dec[Vp]).max(axis=1)[:, None]
+        ctx[V] = pre[V] + ctx[E] + dec[E]
+    call_id = (call_prog.astype(np.uint64) << np.uint64(16)) | local.astype(np.uint64)
+    arr = _poisson_arrivals(rng, n, rate)
+    t = Trace(name="mcts_mapreduce", prog_id=np.arange(n, dtype=np.uint64), prog_arrival=arr,
+              first_call=first, call_prog=call_prog, call_idx=local, call_id=call_id, decode=dec,
+              prefill=pre, input_tokens=np.minimum(ctx, MAX_CONTEXT), delay=np.zeros(C, np.int64),
+              par_ptr=par_ptr, par=par)
     t.meta["is_mcts"] = kinds
     return t
+
+
+def _segmax(x, starts, lens):
+    """max of x[s:s+l] for each (s, l), vectorised."""
+    idx = np.repeat(starts, lens) + (np.arange(int(lens.sum())) - np.repeat(np.cumsum(lens) - lens, lens))
+    seg = np.repeat(np.arange(len(starts)), lens)
+    out = np.full(len(starts), np.iinfo(np.int64).min)
+    np.maximum.at(out, seg, x[idx])
+    return out
 
 
 def burst_mcts_mapreduce(target_active=1_000_000, seed=None) -> Trace:

@@ -39,3 +39,25 @@ def test_determinism_and_structure():
         [[4, 3, 1, 1], [3, 3, 4], [1, 2], [4]]
     for s in range(20):
         random_tiny(s).validate()
+
+
+def test_vectorised_dag_generator_structure():
+    """The vectorised MCTS/map-reduce generator gives the documented DAG (expands join all
+    evaluates of the previous round; reduce joins all maps) and contexts equal to the plain
+    longest-token ancestor recursion."""
+    from autx_workload.gen import _dag_ctx, MAX_CONTEXT
+    t = mcts_mapreduce(200)
+    t.validate()
+    for p in range(t.n_programs):
+        a, b = t.first_call[p], t.first_call[p + 1]
+        parents = [[int(x - a) for x in t.parents(c)] for c in range(a, b)]
+        ref = _dag_ctx(t.decode[a:b], t.prefill[a:b], parents)
+        assert np.array_equal(np.minimum(ref, MAX_CONTEXT), t.input_tokens[a:b])
+        if t.meta["is_mcts"][p]:
+            I = (b - a) // 10
+            for r in range(I):
+                for i in range(5):
+                    assert parents[10 * r + i] == ([] if r == 0 else list(range(10 * r - 5, 10 * r)))
+                    assert parents[10 * r + 5 + i] == [10 * r + i]
+        else:
+            assert parents[-1] == list(range(b - a - 1)) and all(not x for x in parents[:-1])
