@@ -254,7 +254,8 @@ def main():
     from paper_2502_13965_b200 import Scheduler, TraceDriver, ORDER_SELECT, ORDER_RADIX
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)   # one explicit stream for the library and the events
+    torch.cuda.set_stream(stream)
     hbm_peak, peak_src = peaks()
 
     t_gen = time.time()
@@ -301,6 +302,7 @@ def main():
     scan_ms, fin_ms, sel_ms, comp_ms, reg_ms = [], [], [], [], []
     scan_bytes = []
     promoted = []
+    phase = []
     for _ in range(args.steps):
         dt, rec, tm, nc, na = timed_step()
         ms.append(dt)
@@ -309,6 +311,8 @@ def main():
         scan_ms.append(tm.scan_ms); sel_ms.append(tm.select_ms); fin_ms.append(tm.finalize_ms)
         comp_ms.append(tm.complete_ms); reg_ms.append(tm.register_ms)
         promoted.append(rec["n_promoted"])
+        if len(phase) < 20:
+            phase.append(s.phase_times().astype(np.int64))
         scan_bytes.append(SCAN_BYTES_PER_CALL * rec["n_active"] + PROMOTE_BYTES * rec["n_promoted"]
                           + PROG_BYTES * tr.n_programs)
     torch.cuda.synchronize()
@@ -364,6 +368,8 @@ def main():
                          "step_p10": float(np.percentile(ms, 10)), "step_p50": float(np.percentile(ms, 50)),
                          "step_p90": float(np.percentile(ms, 90))},
         "promotions_per_step": statistics.mean(promoted),
+        "finalize_phases_us": [round(float(np.median([p[i + 1] - p[i] for p in phase])) / 1e3, 2) for i in range(8)],
+        "complete_phases_us": [round(float(np.median([p[i + 1] - p[i] for p in phase])) / 1e3, 2) for i in range(16, 19)],
         "e2e": {"value": e2e_dec / e2e_s, "unit": "decisions/s", "h2d_bytes_per_step": h2d // e2e_steps,
                 "d2h_bytes_per_step": d2h // e2e_steps, "ms_per_step": e2e_s * 1e3 / e2e_steps},
         "setup_s": {"generate": round(t_gen, 1), "register_and_fast_forward": round(t_setup, 1)},

@@ -71,8 +71,9 @@ typedef struct {
   uint32_t max_blocks_per_call; /* block-table width per resident call                              */
   uint64_t host_pages;       /* host swap arena size in logical blocks (pages)                       */
   int32_t device;            /* CUDA device ordinal                                                  */
-  void* stream;              /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL =
-                                the library creates its own non-blocking stream                      */
+  void* stream;              /* cudaStream_t all device work is ordered on (e.g.
+                                torch.cuda.current_stream().cuda_stream); NULL = the legacy default
+                                stream                                                               */
   int32_t rank, nranks;      /* engine id and engine count (routing)                                 */
 } autx_config;
 
@@ -195,6 +196,9 @@ typedef struct { float complete_ms, register_ms, scan_ms, select_ms, finalize_ms
 autx_status autx_last_step_timing(autx_ctx* ctx, autx_step_timing* t);
 autx_status autx_set_timing(autx_ctx* ctx, int32_t on);
 uint32_t autx_num_active(const autx_ctx* ctx);
+/* %globaltimer stamps (ns) recorded inside the single-CTA kernels of the last step, for
+ * profiling: [0..8] k_finalize phases, [16..19] k_complete phases; copies min(cap, 32). */
+autx_status autx_phase_times(autx_ctx* ctx, uint64_t* ns, uint32_t cap);
 
 #ifdef __cplusplus
 }

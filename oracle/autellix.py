@@ -369,7 +369,7 @@ class Workload:
         self.remaining = trace.decode.astype(np.int64).copy()
         self.calls_left = np.diff(trace.first_call).astype(np.int64)
         self.done = 0
-        self.index = {int(cid): i for i, cid in enumerate(trace.call_id)} if C < 2_000_000 else None
+        self.index = {int(cid): i for i, cid in enumerate(trace.call_id)}
         self.finish = {}
 
     def arrivals(self, t):

@@ -105,6 +105,7 @@ def load_library(path=LIB_PATH):
         "autx_last_step_timing": ([P, C.POINTER(StepTiming)], i32),
         "autx_set_timing": ([P, i32], i32),
         "autx_num_active": ([P], u32),
+        "autx_phase_times": ([P, P, u32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -120,7 +121,7 @@ def exported_symbols():
         "autx_end_program", "autx_complete", "autx_register_call", "autx_sched_step",
         "autx_step_wait", "autx_kv_swap", "autx_block_table", "autx_block_table_host", "autx_route_record_bytes",
         "autx_route_pack", "autx_route_apply", "autx_dump_calls", "autx_program_state",
-        "autx_last_step_timing", "autx_set_timing", "autx_num_active"]
+        "autx_last_step_timing", "autx_set_timing", "autx_num_active", "autx_phase_times"]
 
 
 def _ptr(a):
@@ -269,6 +270,11 @@ class Scheduler:
         t = StepTiming()
         self._check(self.lib.autx_last_step_timing(self.ctx, C.byref(t)))
         return t
+
+    def phase_times(self):
+        a = np.zeros(32, np.uint64)
+        self._check(self.lib.autx_phase_times(self.ctx, _ptr(a), 32))
+        return a
 
     def num_active(self):
         return int(self.lib.autx_num_active(self.ctx))

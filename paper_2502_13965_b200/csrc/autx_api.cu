@@ -145,6 +145,7 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&o.cand, o.cand_cap));
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K)); CK(dalloc(&o.tile_off, ntiles + 1));
   CK(dalloc(&o.tile_pre, ntiles + 1));
+  CK(dalloc(&o.tile_stat, ntiles + 1));
   CK(cudaHostAlloc((void**)&o.hout, sizeof(HostOut), cudaHostAllocMapped));
   CK(cudaHostAlloc((void**)&o.h_batch, BS * 8, cudaHostAllocMapped));
   CK(cudaHostAlloc((void**)&o.h_admit, BS * 8, cudaHostAllocMapped));
@@ -253,15 +254,9 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
     delete ctx;
     return s;
   }
-  if (c.stream) {
-    ctx->stream = (cudaStream_t)c.stream;
-  } else {
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
-      delete ctx;
-      return AUTX_E_CUDA;
-    }
-    ctx->own_stream = true;
-  }
+  // NULL = the legacy default stream (what torch.cuda.current_stream() is by default), so
+  // library work orders with the caller's default-stream work
+  ctx->stream = (cudaStream_t)c.stream;
   autx_status s = alloc_tables(ctx);
   if (s == AUTX_OK) {
     if (cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming) != cudaSuccess) s = AUTX_E_CUDA;
@@ -288,7 +283,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
                  ctx->ctl, ctx->out.batch_slots, ctx->out.batch_ids, ctx->out.admit_ids,
                  ctx->out.preempt_ids, ctx->out.prev_slots, ctx->out.preempt_slots,
                  ctx->out.admit_slots, ctx->out.cand, ctx->out.tile_cnt, ctx->out.tile_off,
-                 ctx->out.tile_pre, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
+                 ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
                  ctx->kv.bt_offsets, ctx->kv.bt_blocks, ctx->d_pools, ctx->staging,
@@ -934,5 +929,14 @@ extern "C" autx_status autx_route_apply(autx_ctx* ctx, const void* d_records, co
     CK(cudaStreamSynchronize(ctx->stream));
   }
   ctx->routed_this = true;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_phase_times(autx_ctx* ctx, uint64_t* ns, uint32_t cap) {
+  if (!ctx || !ns) return AUTX_E_INVAL;
+  CK(cudaStreamSynchronize(ctx->stream));
+  Ctl c;
+  CK(cudaMemcpy(&c, ctx->ctl, sizeof c, cudaMemcpyDeviceToHost));
+  memcpy(ns, c.dbg, std::min<uint32_t>(cap, 32) * 8);
   return AUTX_OK;
 }

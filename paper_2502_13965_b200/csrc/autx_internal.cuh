@@ -16,8 +16,8 @@ constexpr uint8_t QF_INB = 0x80;    // scratch: member of the batch being formed
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr int MAX_K = 16;
 constexpr int SCAN_THREADS = 256;
-constexpr int ROWS_PER_THREAD = 4;
-constexpr int TILE = SCAN_THREADS * ROWS_PER_THREAD;  // rows per scan tile (1024)
+constexpr int ROWS_PER_THREAD = 8;
+constexpr int TILE = SCAN_THREADS * ROWS_PER_THREAD;  // rows per scan tile (2048)
 constexpr int FIN_THREADS = 1024;
 
 // Device-resident call table, struct-of-arrays, rows in (arrival, seq) order.  Row index ==
@@ -84,6 +84,7 @@ struct Ctl {
   uint32_t host_bump;      // host arena bump pointer (pages)
   uint32_t _pad;
   uint32_t host_free_top[32];  // per size class free-stack size
+  unsigned long long dbg[32];  // %globaltimer stamps of kernel phases (autx_phase_times)
 };
 
 // Host-visible step output written by the finalize kernel into mapped pinned memory.
@@ -131,6 +132,7 @@ struct Outputs {
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* tile_off;        // [ntiles_cap+1] candidate offsets
   uint32_t* tile_pre;        // [ntiles_cap] q* rows in earlier tiles
+  uint2* tile_stat;          // [ntiles_cap] (promotions, live rows) per tile
   HostOut* hout;             // mapped pinned host
   uint64_t* h_batch;         // mapped pinned host mirrors
   uint64_t* h_admit;

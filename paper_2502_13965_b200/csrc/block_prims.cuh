@@ -142,6 +142,12 @@ __device__ __forceinline__ bool mul_ge(uint64_t a, uint32_t b, uint64_t c, uint3
   return h1 > h2 || (h1 == h2 && l1 >= l2);
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint32_t ceil_div_u32(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
 
 }  // namespace autx

@@ -25,6 +25,8 @@ __device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc)
   return q;
 }
 
+#define STAMP(i) do { if (threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
+
 __device__ __forceinline__ void set_err(Ctl* ctl, uint32_t code, uint32_t info) {
   if (atomicCAS(&ctl->err, 0u, code) == 0u) ctl->err_info = info;
 }
@@ -79,6 +81,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_complete(Policy pol, CallTable 
                                                           bool kv_on, CompRec* rec_out, bool apply) {
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
+  STAMP(16);
   for (uint32_t base = 0; base < n; base += FIN_THREADS) {
     uint32_t i = base + tid;
     bool valid = i < n;
@@ -93,7 +96,9 @@ __global__ void __launch_bounds__(FIN_THREADS) k_complete(Policy pol, CallTable 
       rec_out[i] = r;
     }
     __syncthreads();
+    STAMP(17);
     if (apply) apply_record_chunk(pol, pt, rec_out + base, min(n - base, (uint32_t)FIN_THREADS), t);
+    STAMP(18);
     // release the row and its KV (completed calls ran in step t-1, hence are resident)
     uint32_t nfree = 0, rslot = NONE;
     if (valid) {
@@ -126,6 +131,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_complete(Policy pol, CallTable 
     __syncthreads();
   }
   if (tid == 0) ctl->t = t;
+  STAMP(19);
 }
 
 // Multi-engine: apply every engine's completion records (R22: sums and maxima commute, so the
@@ -212,7 +218,9 @@ __global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const Arrival
 // to Q_1 iff W * beta_den >= beta_num * T and not 0/0 (Alg. 1 l.24-30, R3/R4/R7).  Demotion
 // (l.20-23) was applied eagerly by the previous step's finalize (only batch calls can exhaust a
 // quantum, and nothing in between reads q).  Bytes per call: qf 1 + prog 4 + base 4 + mtime 4
-// read; base/mtime/qf/quanta written only for promoted calls.
+// read; a promotion writes base (always: it becomes t) and only the fields that change: qf if
+// q != 0, mtime if != 0, quanta if q != 0 or mtime != 0 (a call in Q_1 that has not run since its
+// last reset already holds Q_1's quantum).
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ void count_q(uint64_t& c0, uint64_t& c1, uint64_t& c2, uint64_t& c3,
                                         uint32_t q) {
@@ -224,51 +232,71 @@ __device__ __forceinline__ void count_q(uint64_t& c0, uint64_t& c1, uint64_t& c2
   c3 += g == 3 ? inc : 0;
 }
 
-__device__ void select_boundary(const Policy& pol, Ctl* ctl, Outputs out, uint32_t ntiles);
-
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan(Policy pol, CallTable ct, ProgTable pt,
-                                                       Ctl* ctl, Outputs out, uint32_t t,
-                                                       uint32_t n_rows) {
+__global__ void __launch_bounds__(SCAN_THREADS, 3) k_scan(Policy pol, CallTable ct, ProgTable pt,
+                                                          Outputs out, uint32_t t, uint32_t n_rows) {
   const uint32_t tile = blockIdx.x;
   const uint32_t row0 = tile * TILE + threadIdx.x * ROWS_PER_THREAD;
   uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
   uint32_t npromo = 0, nlive = 0;
   if (row0 < n_rows) {
-    uint32_t qw = *reinterpret_cast<const uint32_t*>(ct.qf + row0);
-    uint4 pg = *reinterpret_cast<const uint4*>(ct.prog + row0);
-    uint4 bs = *reinterpret_cast<const uint4*>(ct.base + row0);
-    uint4 mt = *reinterpret_cast<const uint4*>(ct.mtime + row0);
-    uint32_t prog[4] = {pg.x, pg.y, pg.z, pg.w};
-    uint32_t base[4] = {bs.x, bs.y, bs.z, bs.w};
-    uint32_t mtim[4] = {mt.x, mt.y, mt.z, mt.w};
-    uint32_t qn = qw;
-    bool any = false;
+    const uint2 qv = __ldcs(reinterpret_cast<const uint2*>(ct.qf + row0));
+    const uint4 p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+    const uint4 p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    uint4 b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+    uint4 b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+    uint4 m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+    uint4 m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+    uint32_t qfs[8], prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
 #pragma unroll
-    for (int j = 0; j < ROWS_PER_THREAD; ++j) {
-      uint32_t qf = (qw >> (8 * j)) & 0xffu;
+    for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
+    // independent gathers of the program rows first (memory-level parallelism)
+    uint32_t sv[8];
+    unsigned long long pw[8];
+    if (pol.beta_den != 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bool live = !(qfs[j] & QF_DEAD);
+        sv[j] = live ? pt.svc[prog[j]] : 0u;
+        pw[j] = live ? pt.pwait[prog[j]] : 0ull;
+      }
+    }
+    bool wq = false, wb = false, wm = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t qf = qfs[j];
       if (qf & QF_DEAD) continue;
       ++nlive;
       uint32_t q = qf & QF_QMASK;
       if (pol.beta_den != 0) {
-        uint32_t p = prog[j];
-        uint64_t W = pt.pwait[p] + (uint64_t)(t - base[j] - mtim[j]);
-        uint64_t T = (uint64_t)pt.svc[p] + mtim[j];
+        uint64_t W = pw[j] + (uint64_t)(t - base[j] - mtim[j]);
+        uint64_t T = (uint64_t)sv[j] + mtim[j];
         if (!(W == 0 && T == 0) && mul_ge(W, pol.beta_den, T, pol.beta_num)) {
-          q = 0;
-          qn = (qn & ~(0xffu << (8 * j))) | ((qf & ~QF_QMASK) << (8 * j));
+          if (q != 0 || mtim[j] != 0) ct.quanta[row0 + j] = pol.quanta[0];
+          if (q != 0) { qfs[j] = qf & ~QF_QMASK; wq = true; }
+          if (mtim[j] != 0) { mtim[j] = 0; wm = true; }
           base[j] = t;
-          mtim[j] = 0;
-          ct.quanta[row0 + j] = pol.quanta[0];
-          any = true;
+          wb = true;
+          q = 0;
           ++npromo;
         }
       }
       count_q(c0, c1, c2, c3, q);
     }
-    if (any) {
-      *reinterpret_cast<uint32_t*>(ct.qf + row0) = qn;
+    if (wq) {
+      uint2 qn;
+      qn.x = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
+      qn.y = qfs[4] | (qfs[5] << 8) | (qfs[6] << 16) | (qfs[7] << 24);
+      *reinterpret_cast<uint2*>(ct.qf + row0) = qn;
+    }
+    if (wb) {
       *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
+      *reinterpret_cast<uint4*>(ct.base + row0 + 4) = make_uint4(base[4], base[5], base[6], base[7]);
+    }
+    if (wm) {
       *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
+      *reinterpret_cast<uint4*>(ct.mtime + row0 + 4) = make_uint4(mtim[4], mtim[5], mtim[6], mtim[7]);
     }
   }
   // per-tile per-queue counts: warp reduce of packed 16-bit fields, then across warps
@@ -283,54 +311,60 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(Policy pol, CallTable ct,
   __syncthreads();
   if (threadIdx.x < MAX_K) {
     uint32_t k = threadIdx.x, sum = 0;
+#pragma unroll
     for (int w = 0; w < SCAN_THREADS / 32; ++w) sum += (uint32_t)(wc[w][k >> 2] >> ((k & 3) * 16)) & 0xffffu;
     out.tile_cnt[(size_t)tile * MAX_K + k] = sum;
-  }
-  if (threadIdx.x == 0) {
+  } else if (threadIdx.x == 32) {
     uint32_t a = 0, b = 0;
+#pragma unroll
     for (int w = 0; w < SCAN_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
-    if (a) atomicAdd(&ctl->n_promoted, a);
-    if (b) atomicAdd(&ctl->n_live, b);
-  }
-  // last CTA to finish selects the boundary queue and the per-tile candidate offsets
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&ctl->tiles_done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    select_boundary(pol, ctl, out, gridDim.x);
+    out.tile_stat[tile] = make_uint2(a, b);
   }
 }
 
-// q* = smallest q with sum_{k<=q} total_k >= BS (K if none); m' = BS - sum_{k<q*} total_k.
-// Candidates: every live row with q < q*, plus the first m' rows of q* in table order.  Any
-// call among the BS smallest keys is a candidate or a running call of q* (finalize adds those):
-// inside q* the key order (arr, not-running, seq) differs from table order (arr, seq) only by
-// moving running calls forward within an arrival group.
-__device__ void select_boundary(const Policy& pol, Ctl* ctl, Outputs out, uint32_t ntiles) {
-  __shared__ uint32_t tot[MAX_K];
-  __shared__ uint32_t red[33];
+// One CTA: q* = smallest q with sum_{k<=q} total_k >= BS (K if none), m' = BS - sum_{k<q*}
+// total_k.  Candidates: every live row with q < q*, plus the first m' rows of q* in table order.
+// Any call among the BS smallest keys is a candidate or a running call of q* (finalize adds
+// those): inside q* the key order (arr, not-running, seq) differs from table order (arr, seq)
+// only by moving running calls forward within an arrival group.  Per tile: the q* rows of
+// earlier tiles (tile_pre) and the candidate output offset
+//     off(tile) = sum_{k<q*} prefix_k(tile) + min(prefix_{q*}(tile), m').
+constexpr int SEL_THREADS = 1024;
+__global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Outputs out,
+                                                        uint32_t ntiles) {
+  __shared__ uint32_t tot[MAX_K + 2];
+  __shared__ unsigned long long red[33];
   __shared__ uint32_t s_qstar, s_m;
   const uint32_t tid = threadIdx.x;
-  if (tid < MAX_K) tot[tid] = 0;
+  if (tid < MAX_K + 2) tot[tid] = 0;
   __syncthreads();
+  const uint32_t per = (ntiles + SEL_THREADS - 1) / SEL_THREADS;
+  const uint32_t t0 = min(ntiles, tid * per), t1 = min(ntiles, t0 + per);
   uint32_t acc[MAX_K];
 #pragma unroll
   for (int k = 0; k < MAX_K; ++k) acc[k] = 0;
-  for (uint32_t tl = tid; tl < ntiles; tl += SCAN_THREADS) {
+  uint32_t ap = 0, al = 0;
+  for (uint32_t tl = t0; tl < t1; ++tl) {
     const uint4* c = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)tl * MAX_K);
 #pragma unroll
     for (int v = 0; v < MAX_K / 4; ++v) {
-      uint4 x = __ldcg(c + v);
+      uint4 x = c[v];
       acc[4 * v] += x.x; acc[4 * v + 1] += x.y; acc[4 * v + 2] += x.z; acc[4 * v + 3] += x.w;
     }
+    uint2 st = out.tile_stat[tl];
+    ap += st.x;
+    al += st.y;
   }
 #pragma unroll
   for (int k = 0; k < MAX_K; ++k) {
     uint32_t w = warp_sum(acc[k]);
     if (lane_id() == 0 && w) atomicAdd(&tot[k], w);
+  }
+  ap = warp_sum(ap);
+  al = warp_sum(al);
+  if (lane_id() == 0) {
+    if (ap) atomicAdd(&tot[MAX_K], ap);
+    if (al) atomicAdd(&tot[MAX_K + 1], al);
   }
   __syncthreads();
   if (tid == 0) {
@@ -343,48 +377,43 @@ __device__ void select_boundary(const Policy& pol, Ctl* ctl, Outputs out, uint32
     s_m = m;
     ctl->qstar = qs;
     ctl->mprime = m;
+    ctl->n_promoted = tot[MAX_K];
+    ctl->n_live = tot[MAX_K + 1];
   }
   __syncthreads();
   const uint32_t qs = s_qstar, m = s_m;
-  // each thread owns a contiguous range of tiles
-  uint32_t per = (ntiles + SCAN_THREADS - 1) / SCAN_THREADS;
-  uint32_t t0 = tid * per, t1 = min(ntiles, t0 + per);
-  uint32_t my_qs = 0;
-  if (qs < pol.K)
-    for (uint32_t tl = t0; tl < t1; ++tl) my_qs += __ldcg(out.tile_cnt + (size_t)tl * MAX_K + qs);
-  uint32_t pre_qs = block_excl_scan<uint32_t, SCAN_THREADS>(my_qs, red, nullptr);
-  uint32_t my_c = 0;
+  // per thread: (rows of queues < q*, rows of q*) over its tile range, packed in one u64 scan
+  uint64_t mine = 0;
   for (uint32_t tl = t0; tl < t1; ++tl) {
     const uint32_t* c = out.tile_cnt + (size_t)tl * MAX_K;
     uint32_t a = 0;
-    for (uint32_t k = 0; k < qs && k < pol.K; ++k) a += __ldcg(c + k);
-    out.tile_pre[tl] = pre_qs;
-    if (qs < pol.K) {
-      uint32_t cq = __ldcg(c + qs);
-      uint32_t take = pre_qs >= m ? 0 : min(cq, m - pre_qs);
-      a += take;
-      pre_qs += cq;
-    }
-    out.tile_off[tl] = a;  // count for now
-    my_c += a;
+    for (uint32_t k = 0; k < qs && k < pol.K; ++k) a += c[k];
+    uint32_t cq = qs < pol.K ? c[qs] : 0;
+    mine += ((uint64_t)a << 32) | cq;
   }
-  uint32_t total;
-  uint32_t off = block_excl_scan<uint32_t, SCAN_THREADS>(my_c, red, &total);
-  uint32_t run = off;  // counts -> exclusive offsets
+  unsigned long long total;
+  uint64_t pre = block_excl_scan<unsigned long long, SEL_THREADS>(mine, red, &total);
+  uint32_t pre_a = (uint32_t)(pre >> 32), pre_q = (uint32_t)pre;
   for (uint32_t tl = t0; tl < t1; ++tl) {
-    uint32_t a = out.tile_off[tl];
-    out.tile_off[tl] = run;
-    run += a;
+    const uint32_t* c = out.tile_cnt + (size_t)tl * MAX_K;
+    uint32_t a = 0;
+    for (uint32_t k = 0; k < qs && k < pol.K; ++k) a += c[k];
+    uint32_t cq = qs < pol.K ? c[qs] : 0;
+    out.tile_pre[tl] = pre_q;
+    out.tile_off[tl] = pre_a + min(pre_q, m);
+    pre_a += a;
+    pre_q += cq;
   }
-  if (tid == SCAN_THREADS - 1) out.tile_off[ntiles] = total;
   if (tid == 0) {
-    ctl->n_cand_a = total;
-    ctl->tiles_done = 0;
+    uint32_t ta = (uint32_t)(total >> 32), tq = (uint32_t)total;
+    uint32_t n = ta + min(tq, m);
+    out.tile_off[ntiles] = n;
+    ctl->n_cand_a = n;
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-// a5 candidate gather: tiles with candidates re-read their 1 KB of qf and emit row indices in
+// a5 candidate gather: tiles with candidates re-read their 2 KB of qf and emit row indices in
 // table order; the emitted rows are marked QF_INB so finalize can add the running calls of q*
 // that were not emitted.
 // ---------------------------------------------------------------------------------------------
@@ -397,20 +426,18 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
   __shared__ uint32_t red[33];
   const uint32_t qs = ctl->qstar, m = ctl->mprime;
   const uint32_t row0 = tile * TILE + threadIdx.x * ROWS_PER_THREAD;
-  uint32_t qw = row0 < n_rows ? *reinterpret_cast<const uint32_t*>(ct.qf + row0) : 0x40404040u;
-  // q* rows of this tile before this thread, plus the q* prefix of earlier tiles
+  uint2 qv = row0 < n_rows ? *reinterpret_cast<const uint2*>(ct.qf + row0) : make_uint2(0x40404040u, 0x40404040u);
+  uint32_t qfs[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
   uint32_t nq = 0;
 #pragma unroll
-  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
-    uint32_t qf = (qw >> (8 * j)) & 0xffu;
-    nq += (!(qf & QF_DEAD) && (qf & QF_QMASK) == qs) ? 1u : 0u;
-  }
-  const uint32_t tile_pre = out.tile_pre[tile];
-  uint32_t rq = tile_pre + block_excl_scan<uint32_t, SCAN_THREADS>(nq, red, nullptr);
+  for (int j = 0; j < 8; ++j) nq += (!(qfs[j] & QF_DEAD) && (qfs[j] & QF_QMASK) == qs) ? 1u : 0u;
+  uint32_t rq = out.tile_pre[tile] + block_excl_scan<uint32_t, SCAN_THREADS>(nq, red, nullptr);
   uint32_t flags = 0, nsel = 0;
 #pragma unroll
-  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
-    uint32_t qf = (qw >> (8 * j)) & 0xffu;
+  for (int j = 0; j < 8; ++j) {
+    uint32_t qf = qfs[j];
     if (qf & QF_DEAD) continue;
     uint32_t q = qf & QF_QMASK;
     bool sel = q < qs;
@@ -419,14 +446,16 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
   }
   uint32_t pos = off + block_excl_scan<uint32_t, SCAN_THREADS>(nsel, red, nullptr);
   if (flags) {
-    uint32_t qn = qw;
 #pragma unroll
-    for (int j = 0; j < ROWS_PER_THREAD; ++j)
+    for (int j = 0; j < 8; ++j)
       if (flags & (1u << j)) {
         out.cand[pos++] = row0 + j;
-        qn |= (uint32_t)QF_INB << (8 * j);
+        qfs[j] |= QF_INB;
       }
-    *reinterpret_cast<uint32_t*>(ct.qf + row0) = qn;
+    uint2 qn;
+    qn.x = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
+    qn.y = qfs[4] | (qfs[5] << 8) | (qfs[6] << 16) | (qfs[7] << 24);
+    *reinterpret_cast<uint2*>(ct.qf + row0) = qn;
   }
 }
 
@@ -453,6 +482,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   const uint32_t tid = threadIdx.x;
   const uint32_t BS = pol.max_batch;
   const uint32_t nA = ctl->n_cand_a, qs = ctl->qstar, n_prev = ctl->n_prev;
+  STAMP(0);
   if (tid == 0) s_nb = 0;
   __syncthreads();
   // ---- candidate keys --------------------------------------------------------------------
@@ -476,8 +506,10 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     ct.qf[s] = (uint8_t)(qf & ~QF_INB);
   }
   __syncthreads();
+  STAMP(1);
   const uint32_t ncand = nA + s_nb;
   bitonic_sort_pairs<FIN_THREADS>(khi, klo, np);
+  STAMP(2);
   // ---- prefix cutoff on BS and P ------------------------------------------------------------
   const uint32_t m = min(BS, ncand);
   uint32_t kvb_mine[4];
@@ -500,6 +532,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     carry += tot;
   }
   const uint32_t n_batch = block_sum<uint32_t, FIN_THREADS>(nb_local, red);
+  STAMP(3);
   if (tid == 0 && ncand > 0 && n_batch == 0) {
     if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u) ctl->err_info = klo[0];
   }
@@ -520,6 +553,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   }
   kv_sum = block_sum<unsigned long long, FIN_THREADS>(kv_sum, red64);
   __syncthreads();
+  STAMP(4);
   // ---- preempt = resident (previous batch, still active) not in the batch --------------------
   unsigned long long swap_out = 0, swap_in = 0;
   uint32_t n_preempt = 0;
@@ -545,6 +579,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     }
     n_preempt = base_off;
   }
+  STAMP(5);
   // ---- admit = batch calls not resident --------------------------------------------------------
   uint32_t n_admit = 0;
   {
@@ -570,6 +605,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   }
   swap_out = block_sum<unsigned long long, FIN_THREADS>(swap_out, red64);
   swap_in = block_sum<unsigned long long, FIN_THREADS>(swap_in, red64);
+  STAMP(6);
 
   // ---- KV blocks: swap plan + allocation (a7) --------------------------------------------------
   if (kv_on) {
@@ -703,6 +739,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     __syncthreads();
   }
 
+  STAMP(7);
   // ---- step accounting + eager demotion (Alg. 1 l.20-23) for the batch --------------------
   for (uint32_t i = tid; i < n_batch; i += FIN_THREADS) {
     uint32_t s = klo[i];
@@ -740,6 +777,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     ctl->n_promoted = 0;
     ctl->n_live = 0;
   }
+  STAMP(8);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -792,8 +830,9 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[1], s);
   } else {
-    k_scan<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, pt, ctl, out, t, n_rows);
+    k_scan<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, pt, out, t, n_rows);
     if (ev) cudaEventRecord(ev[1], s);
+    k_select<<<1, SEL_THREADS, 0, s>>>(pol, ctl, out, ntiles);
     k_gather<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, ctl, out, n_rows);
   }
   if (ev) cudaEventRecord(ev[2], s);
