@@ -201,14 +201,14 @@ def bench_swap(torch, args, link):
     from paper_2502_13965_b200 import Scheduler, TraceDriver, SWAP_SM, SWAP_STAGED_DMA, SWAP_PER_CHUNK_MEMCPY
     L, chunk = 32, 32 << 10                 # LLaMA-3.1-8B: 32 layers x 8 KV heads x 128 x bf16 x 16 tok
     page = L * 2 * chunk                    # 2 MiB per logical block
-    P, host_pages = 2560, 6144           # P >= the largest call's need (32768+4096 tokens)
+    P, host_pages = 2560, 16384          # P >= the largest call's need (32768+4096 tokens)
     kp = [torch.empty(P, chunk, dtype=torch.uint8, device="cuda") for _ in range(L)]
     vp = [torch.empty(P, chunk, dtype=torch.uint8, device="cuda") for _ in range(L)]
     host = torch.empty(host_pages * page, dtype=torch.uint8).pin_memory()
     lad = spec_ladder()
     results = {}
     for name, mode in (("sm", SWAP_SM), ("staged_dma", SWAP_STAGED_DMA), ("per_chunk_memcpy", SWAP_PER_CHUNK_MEMCPY)):
-        tr = react(3000, seed=BASE_SEED + CONFIG_INDEX["react"])
+        tr = react(1000, seed=BASE_SEED + CONFIG_INDEX["react"])
         s = Scheduler(policy="plas", beta=(2, 1), max_batch=64, kv_budget=P, block_tokens=16,
                       max_calls=1 << 16, max_programs=1 << 14, n_gpu_blocks=P, max_blocks_per_call=P,
                       host_pages=host_pages, **lad)
@@ -368,7 +368,9 @@ def main():
                          "step_p10": float(np.percentile(ms, 10)), "step_p50": float(np.percentile(ms, 50)),
                          "step_p90": float(np.percentile(ms, 90))},
         "promotions_per_step": statistics.mean(promoted),
-        "finalize_phases_us": [round(float(np.median([p[i + 1] - p[i] for p in phase])) / 1e3, 2) for i in range(8)],
+        "finalize_phases_us": {n: round(float(np.median([p[b] - p[a] for p in phase])) / 1e3, 2) for n, a, b in (
+            ("load_prev", 0, 9), ("region_b", 9, 10), ("region_a", 10, 1), ("sort", 1, 2), ("cutoff", 2, 3),
+            ("batch_admit", 3, 4), ("preempt", 4, 5), ("kv", 6, 7), ("account", 7, 8))},
         "complete_phases_us": [round(float(np.median([p[i + 1] - p[i] for p in phase])) / 1e3, 2) for i in range(16, 19)],
         "e2e": {"value": e2e_dec / e2e_s, "unit": "decisions/s", "h2d_bytes_per_step": h2d // e2e_steps,
                 "d2h_bytes_per_step": d2h // e2e_steps, "ms_per_step": e2e_s * 1e3 / e2e_steps},
@@ -385,7 +387,7 @@ def main():
         except Exception as e:  # keep the sched line even if the swap phase fails
             sw = {"error": repr(e)}
         result["swap"] = {"host_link_peak_GBps": {k: round(v, 2) for k, v in link.items()},
-                          "config": "react (BFCL-shaped) 3000 programs, PLAS, BS=64, P=2048 blocks, 8B geometry "
+                          "config": "react (BFCL-shaped) 1000 programs, PLAS, BS=64, P=2560 blocks, 8B geometry "
                                     "(32 layers x K|V x 32 KiB chunks = 2 MiB/block)", **sw}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, per_step, wall, _ = oracle_decisions_per_s(args.active, 2, 0)

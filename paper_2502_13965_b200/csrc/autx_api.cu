@@ -312,7 +312,10 @@ static autx_status sync_last(autx_ctx* ctx) {
     ctx->last_batch.clear();
     if (ctx->stepped) {
       const HostOut& h = *ctx->out.hout;
-      if (h.err) return fail(ctx, (autx_status)h.err, "device error %u in step %u", h.err, ctx->t_last);
+      if (h.err)
+        return fail(ctx, (autx_status)h.err, "device error %u (site %u: 1 host arena full, 2 call needs more "
+                    "than max_blocks_per_call, 3 no resident slot, 4 GPU block pool empty, other: head call "
+                    "needs more than P) in step %u", h.err, h.err_info, ctx->t_last);
       for (uint32_t i = 0; i < h.n_batch; ++i) ctx->last_batch.insert(ctx->out.h_batch[i]);
     }
     ctx->last_batch_valid = true;

@@ -93,7 +93,7 @@ struct HostOut {
   unsigned long long swap_out_blocks, swap_in_blocks, kv_blocks;
   uint32_t n_promoted, err;
   uint32_t seqno;  // step sequence number, for sanity
-  uint32_t _pad;
+  uint32_t err_info;
 };
 
 // Swap plan (built by finalize, executed by autx_kv_swap).

@@ -38,30 +38,31 @@ __device__ __forceinline__ void set_err(Ctl* ctl, uint32_t code, uint32_t info) 
 // Records are sorted by program in shared memory; a warp-shuffle segmented scan reduces each
 // program's run and the segment tail writes the row: one write per program, deterministic.
 // ---------------------------------------------------------------------------------------------
-// Applies one chunk of <= FIN_THREADS completion records to the process table.
+// Applies one chunk of <= NT completion records to the process table (NT = block size).
+template <int NT>
 __device__ void apply_record_chunk(const Policy& pol, ProgTable pt, const CompRec* recs, uint32_t n,
                                    uint32_t t) {
-  __shared__ uint64_t skey[FIN_THREADS];
-  __shared__ uint32_t sdummy[FIN_THREADS];
-  __shared__ CompRec srec[FIN_THREADS];
+  __shared__ uint64_t skey[NT];
+  __shared__ uint32_t sdummy[NT];
+  __shared__ CompRec srec[NT];
   __shared__ uint64_t red_v[33];
   __shared__ uint32_t red_f[33];
   const uint32_t tid = threadIdx.x;
   bool valid = tid < n;
   if (valid) srec[tid] = recs[tid];
-  skey[tid] = valid ? ((uint64_t)recs[tid].prog << 32 | tid) : ~0ull;
+  skey[tid] = valid ? ((uint64_t)srec[tid].prog << 32 | tid) : ~0ull;
   sdummy[tid] = 0;
   __syncthreads();
-  bitonic_sort_pairs<FIN_THREADS>(skey, sdummy, FIN_THREADS);
+  bitonic_sort_pairs<NT>(skey, sdummy, NT);
   uint64_t k = skey[tid];
   bool v2 = k != ~0ull;
   uint32_t o = (uint32_t)k, pp = (uint32_t)(k >> 32);
   bool head = tid == 0 || (skey[tid - 1] >> 32) != pp;
-  bool tail = tid == FIN_THREADS - 1 || skey[tid + 1] == ~0ull || (skey[tid + 1] >> 32) != pp;
+  bool tail = tid == NT - 1 || skey[tid + 1] == ~0ull || (skey[tid + 1] >> 32) != pp;
   uint64_t ex = v2 ? srec[o].exec : 0, tw = v2 ? srec[o].tw : 0, cp = v2 ? srec[o].cp : 0;
-  uint64_t sum_ex = block_seg_scan<uint64_t, FIN_THREADS>(ex, head, OpSum(), red_v, red_f);
-  uint64_t sum_tw = block_seg_scan<uint64_t, FIN_THREADS>(tw, head, OpSum(), red_v, red_f);
-  uint64_t max_cp = block_seg_scan<uint64_t, FIN_THREADS>(cp, head, OpMax(), red_v, red_f);
+  uint64_t sum_ex = block_seg_scan<uint64_t, NT>(ex, head, OpSum(), red_v, red_f);
+  uint64_t sum_tw = block_seg_scan<uint64_t, NT>(tw, head, OpSum(), red_v, red_f);
+  uint64_t max_cp = block_seg_scan<uint64_t, NT>(cp, head, OpMax(), red_v, red_f);
   if (v2 && tail) {
     if (pol.policy == AUTX_ATLAS) {
       uint32_t cur = pt.svc[pp];
@@ -75,14 +76,15 @@ __device__ void apply_record_chunk(const Policy& pol, ProgTable pt, const CompRe
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(FIN_THREADS) k_complete(Policy pol, CallTable ct, ProgTable pt,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_complete(Policy pol, CallTable ct, ProgTable pt,
                                                           Ctl* ctl, const uint32_t* slots,
                                                           uint32_t n, uint32_t t, KvState kv,
                                                           bool kv_on, CompRec* rec_out, bool apply) {
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
   STAMP(16);
-  for (uint32_t base = 0; base < n; base += FIN_THREADS) {
+  for (uint32_t base = 0; base < n; base += NT) {
     uint32_t i = base + tid;
     bool valid = i < n;
     uint32_t s = valid ? slots[i] : 0;
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_complete(Policy pol, CallTable 
     }
     __syncthreads();
     STAMP(17);
-    if (apply) apply_record_chunk(pol, pt, rec_out + base, min(n - base, (uint32_t)FIN_THREADS), t);
+    if (apply) apply_record_chunk<NT>(pol, pt, rec_out + base, min(n - base, (uint32_t)NT), t);
     STAMP(18);
     // release the row and its KV (completed calls ran in step t-1, hence are resident)
     uint32_t nfree = 0, rslot = NONE;
@@ -112,9 +114,9 @@ __global__ void __launch_bounds__(FIN_THREADS) k_complete(Policy pol, CallTable 
     }
     if (kv_on) {
       uint32_t tot;
-      uint32_t off = block_excl_scan<uint32_t, FIN_THREADS>(nfree, red_u, &tot);
+      uint32_t off = block_excl_scan<uint32_t, NT>(nfree, red_u, &tot);
       uint32_t has = rslot != NONE, rtot;
-      uint32_t roff = block_excl_scan<uint32_t, FIN_THREADS>(has, red_u, &rtot);
+      uint32_t roff = block_excl_scan<uint32_t, NT>(has, red_u, &rtot);
       uint32_t top = ctl->free_top, rtop = ctl->rs_free_top;
       if (rslot != NONE) {
         const uint32_t* src = kv.rs_blocks + (size_t)rslot * pol.max_blocks_per_call;
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_apply(Policy pol, ProgTable pt,
     const CompRec* recs = reinterpret_cast<const CompRec*>(h + 1);
     uint32_t n = h->n_comp;
     for (uint32_t b = 0; b < n; b += FIN_THREADS)
-      apply_record_chunk(pol, pt, recs + b, min(n - b, (uint32_t)FIN_THREADS), t);
+      apply_record_chunk<FIN_THREADS>(pol, pt, recs + b, min(n - b, (uint32_t)FIN_THREADS), t);
   }
 }
 
@@ -478,133 +480,181 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   uint32_t* klo = reinterpret_cast<uint32_t*>(khi + np);
   __shared__ unsigned long long red64[33];
   __shared__ uint32_t red[33];
-  __shared__ uint32_t s_nb;
+  __shared__ uint32_t s_nb, s_nbatch;
   const uint32_t tid = threadIdx.x;
   const uint32_t BS = pol.max_batch;
   const uint32_t nA = ctl->n_cand_a, qs = ctl->qstar, n_prev = ctl->n_prev;
   STAMP(0);
   if (tid == 0) s_nb = 0;
   __syncthreads();
-  // ---- candidate keys --------------------------------------------------------------------
-  for (uint32_t i = tid; i < np; i += FIN_THREADS) { khi[i] = ~0ull; klo[i] = ~0u; }
-  __syncthreads();
-  for (uint32_t i = tid; i < n_prev; i += FIN_THREADS) {
-    uint32_t s = out.prev_slots[i];
-    uint32_t qf = ct.qf[s];
-    if (!(qf & QF_DEAD) && (qf & QF_QMASK) == qs && !(qf & QF_INB)) {
-      uint32_t j = nA + atomicAdd(&s_nb, 1u);
-      khi[j] = ((uint64_t)qs << 33) | ((uint64_t)ct.arr[s] << 1);  // running: bit 0 clear
-      klo[j] = s;
+  // ---- (1) previous batch = resident set: everything preempt needs, in one round trip --------
+  constexpr int R = 4;  // items per thread, blocked (i = tid * R + r); BS <= 4096
+  uint32_t p_s[R], p_qf[R], p_arr[R], p_tok[R], p_ex[R];
+  uint64_t p_cid[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    uint32_t i = tid * R + r;
+    p_qf[r] = QF_DEAD;
+    if (i < n_prev) {
+      uint32_t sl = out.prev_slots[i];
+      p_s[r] = sl;
+      p_qf[r] = ct.qf[sl];
+      p_arr[r] = ct.arr[sl];
+      p_tok[r] = ct.tok[sl];
+      p_ex[r] = ct.exec[sl];
+      p_cid[r] = ct.cid[sl];
     }
   }
-  __syncthreads();  // INB of region-A rows read above before it is cleared below
+  for (uint32_t i = tid; i < np; i += FIN_THREADS) { khi[i] = ~0ull; klo[i] = ~0u; }
+  __syncthreads();
+  STAMP(9);
+  // running calls of q* that the gather did not emit (region B)
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    uint32_t qf = p_qf[r];
+    if (!(qf & QF_DEAD) && (qf & QF_QMASK) == qs && !(qf & QF_INB)) {
+      uint32_t j = nA + atomicAdd(&s_nb, 1u);
+      khi[j] = ((uint64_t)qs << 33) | ((uint64_t)p_arr[r] << 1);  // running: not-running bit 0
+      klo[j] = p_s[r];
+    }
+  }
+  __syncthreads();  // INB of region-A rows was read above before it is cleared below
+  STAMP(10);
   for (uint32_t i = tid; i < nA; i += FIN_THREADS) {
-    uint32_t s = out.cand[i];
-    uint32_t qf = ct.qf[s];
-    khi[i] = ((uint64_t)(qf & QF_QMASK) << 33) | ((uint64_t)ct.arr[s] << 1) | ((qf & QF_RUN) ? 0u : 1u);
-    klo[i] = s;
-    ct.qf[s] = (uint8_t)(qf & ~QF_INB);
+    uint32_t sl = out.cand[i];
+    uint32_t qf = ct.qf[sl];
+    khi[i] = ((uint64_t)(qf & QF_QMASK) << 33) | ((uint64_t)ct.arr[sl] << 1) | ((qf & QF_RUN) ? 0u : 1u);
+    klo[i] = sl;
+    ct.qf[sl] = (uint8_t)(qf & ~QF_INB);
   }
   __syncthreads();
   STAMP(1);
   const uint32_t ncand = nA + s_nb;
-  bitonic_sort_pairs<FIN_THREADS>(khi, klo, np);
+  uint32_t np2 = 2;
+  while (np2 < ncand) np2 <<= 1;
+  bitonic_sort_pairs<FIN_THREADS>(khi, klo, min(np2, np));
   STAMP(2);
-  // ---- prefix cutoff on BS and P ------------------------------------------------------------
+  // ---- (2) the first m = min(BS, ncand) keys: load their fields once; prefix cutoff ---------
   const uint32_t m = min(BS, ncand);
-  uint32_t kvb_mine[4];
-  uint32_t nb_local = 0;
-  // up to 4 candidates per thread (BS <= 4096)
-  unsigned long long carry = 0;
+  uint32_t c_s[R], c_qf[R], c_tok[R], c_ex[R], c_mt[R], c_qt[R], c_kvb[R];
+  uint64_t c_cid[R];
+  unsigned long long my_kv = 0;
 #pragma unroll
-  for (uint32_t r = 0; r < 4; ++r) {
-    uint32_t i = r * FIN_THREADS + tid;
-    uint32_t kb = 0;
+  for (int r = 0; r < R; ++r) {
+    uint32_t i = tid * R + r;
+    c_kvb[r] = 0;
     if (i < m) {
-      uint32_t s = klo[i];
-      kb = ceil_div_u32(ct.tok[s] + ct.exec[s] + 1, pol.block_tokens);
+      uint32_t sl = klo[i];
+      c_s[r] = sl;
+      c_qf[r] = ct.qf[sl];
+      c_tok[r] = ct.tok[sl];
+      c_ex[r] = ct.exec[sl];
+      c_mt[r] = ct.mtime[sl];
+      c_qt[r] = ct.quanta[sl];
+      c_cid[r] = ct.cid[sl];
     }
-    kvb_mine[r] = kb;
-    unsigned long long tot;
-    unsigned long long pre = block_excl_scan<unsigned long long, FIN_THREADS>(kb, red64, &tot);
-    unsigned long long incl = carry + pre + kb;
-    if (i < m && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) ++nb_local;
-    carry += tot;
   }
-  const uint32_t n_batch = block_sum<uint32_t, FIN_THREADS>(nb_local, red);
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (tid * R + r < m) {
+      c_kvb[r] = ceil_div_u32(c_tok[r] + c_ex[r] + 1, pol.block_tokens);  // R14
+      my_kv += c_kvb[r];
+    }
+  unsigned long long kv_pre = block_excl_scan<unsigned long long, FIN_THREADS>(my_kv, red64, nullptr);
+  if (tid == 0) s_nbatch = 0;
+  __syncthreads();
+  // Alg. 1 l.34-37: take while count <= BS and sum kvb <= P; kvb >= 1 makes the prefix sums
+  // strictly increasing, so the fitting items are exactly a prefix: n_batch = max fitting i + 1
+  {
+    unsigned long long incl = kv_pre;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      uint32_t i = tid * R + r;
+      if (i < m) {
+        incl += c_kvb[r];
+        if (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget) atomicMax(&s_nbatch, i + 1);
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t n_batch = s_nbatch;
   STAMP(3);
   if (tid == 0 && ncand > 0 && n_batch == 0) {
     if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u) ctl->err_info = klo[0];
   }
-  // ---- batch list, INB marks ---------------------------------------------------------------
-  unsigned long long kv_sum = 0;
+  // ---- (3) batch list and admit = batch calls not resident (batch order) -------------------
+  unsigned long long my_ad = 0, kv_mine = 0;
 #pragma unroll
-  for (uint32_t r = 0; r < 4; ++r) {
-    uint32_t i = r * FIN_THREADS + tid;
+  for (int r = 0; r < R; ++r) {
+    uint32_t i = tid * R + r;
     if (i < n_batch) {
-      uint32_t s = klo[i];
-      out.batch_slots[i] = s;
-      uint64_t id = ct.cid[s];
-      out.batch_ids[i] = id;
-      out.h_batch[i] = id;
-      ct.qf[s] = (uint8_t)(ct.qf[s] | QF_INB);
-      kv_sum += kvb_mine[r];
+      out.batch_slots[i] = c_s[r];
+      out.batch_ids[i] = c_cid[r];
+      out.h_batch[i] = c_cid[r];
+      kv_mine += c_kvb[r];
+      if (!(c_qf[r] & QF_RES)) {
+        uint64_t held = c_ex[r] > 0 ? ceil_div_u32(c_tok[r] + c_ex[r], pol.block_tokens) : 0;  // R28
+        my_ad += (1ull << 44) | held;
+      }
     }
   }
-  kv_sum = block_sum<unsigned long long, FIN_THREADS>(kv_sum, red64);
-  __syncthreads();
+  unsigned long long ad_tot;
+  unsigned long long ad_pre = block_excl_scan<unsigned long long, FIN_THREADS>(my_ad, red64, &ad_tot);
+  {
+    uint32_t pos = (uint32_t)(ad_pre >> 44);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      uint32_t i = tid * R + r;
+      if (i < n_batch && !(c_qf[r] & QF_RES)) {
+        out.admit_ids[pos] = c_cid[r];
+        out.h_admit[pos] = c_cid[r];
+        out.admit_slots[pos] = c_s[r];
+        ++pos;
+      }
+    }
+  }
+  const uint32_t n_admit = (uint32_t)(ad_tot >> 44);
+  const unsigned long long swap_in = ad_tot & ((1ull << 44) - 1);
   STAMP(4);
-  // ---- preempt = resident (previous batch, still active) not in the batch --------------------
-  unsigned long long swap_out = 0, swap_in = 0;
-  uint32_t n_preempt = 0;
-  {
-    uint32_t base_off = 0;
-    for (uint32_t c0 = 0; c0 < n_prev; c0 += FIN_THREADS) {
-      uint32_t i = c0 + tid;
-      uint32_t s = i < n_prev ? out.prev_slots[i] : 0;
-      uint32_t qf = i < n_prev ? ct.qf[s] : QF_DEAD;
-      uint32_t is_pre = (!(qf & QF_DEAD) && !(qf & QF_INB)) ? 1u : 0u;
-      uint32_t tot;
-      uint32_t pos = base_off + block_excl_scan<uint32_t, FIN_THREADS>(is_pre, red, &tot);
-      if (is_pre) {
-        uint32_t held = ceil_div_u32(ct.tok[s] + ct.exec[s], pol.block_tokens);
-        swap_out += held;
-        uint64_t id = ct.cid[s];
-        out.preempt_ids[pos] = id;
-        out.h_preempt[pos] = id;
-        out.preempt_slots[pos] = s;
-        ct.qf[s] = (uint8_t)(qf & ~(QF_RUN | QF_RES));
+  // ---- (4) preempt = previous batch, still active, not in the batch (previous-batch order) ---
+  unsigned long long my_pre = 0;
+  uint32_t is_pre = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    uint32_t i = tid * R + r;
+    if (i < n_prev && !(p_qf[r] & QF_DEAD)) {
+      // membership: binary search of the row's key in the sorted batch prefix
+      uint64_t key = ((uint64_t)(p_qf[r] & QF_QMASK) << 33) | ((uint64_t)p_arr[r] << 1);
+      uint32_t lo = 0, hi = n_batch;
+      while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (pair_gt(key, p_s[r], khi[mid], klo[mid])) lo = mid + 1; else hi = mid;
       }
-      base_off += tot;
+      bool in = lo < n_batch && khi[lo] == key && klo[lo] == p_s[r];
+      if (!in) {
+        is_pre |= 1u << r;
+        my_pre += (1ull << 44) | ceil_div_u32(p_tok[r] + p_ex[r], pol.block_tokens);  // R28
+      }
     }
-    n_preempt = base_off;
   }
+  unsigned long long pre_tot;
+  unsigned long long pre_pre = block_excl_scan<unsigned long long, FIN_THREADS>(my_pre, red64, &pre_tot);
+  {
+    uint32_t pos = (uint32_t)(pre_pre >> 44);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (is_pre & (1u << r)) {
+        out.preempt_ids[pos] = p_cid[r];
+        out.h_preempt[pos] = p_cid[r];
+        out.preempt_slots[pos] = p_s[r];
+        ct.qf[p_s[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
+        ++pos;
+      }
+  }
+  const uint32_t n_preempt = (uint32_t)(pre_tot >> 44);
+  const unsigned long long swap_out = pre_tot & ((1ull << 44) - 1);
+  const unsigned long long kv_sum = block_sum<unsigned long long, FIN_THREADS>(kv_mine, red64);
   STAMP(5);
-  // ---- admit = batch calls not resident --------------------------------------------------------
-  uint32_t n_admit = 0;
-  {
-    uint32_t base_off = 0;
-    for (uint32_t c0 = 0; c0 < n_batch; c0 += FIN_THREADS) {
-      uint32_t i = c0 + tid;
-      uint32_t s = i < n_batch ? klo[i] : 0;
-      uint32_t qf = i < n_batch ? ct.qf[s] : QF_RES;
-      uint32_t is_ad = (qf & QF_RES) ? 0u : 1u;
-      uint32_t tot;
-      uint32_t pos = base_off + block_excl_scan<uint32_t, FIN_THREADS>(is_ad, red, &tot);
-      if (is_ad) {
-        uint64_t id = ct.cid[s];
-        out.admit_ids[pos] = id;
-        out.h_admit[pos] = id;
-        out.admit_slots[pos] = s;
-        uint32_t ex = ct.exec[s];
-        if (ex > 0) swap_in += ceil_div_u32(ct.tok[s] + ex, pol.block_tokens);
-      }
-      base_off += tot;
-    }
-    n_admit = base_off;
-  }
-  swap_out = block_sum<unsigned long long, FIN_THREADS>(swap_out, red64);
-  swap_in = block_sum<unsigned long long, FIN_THREADS>(swap_in, red64);
   STAMP(6);
 
   // ---- KV blocks: swap plan + allocation (a7) --------------------------------------------------
@@ -740,24 +790,27 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   }
 
   STAMP(7);
-  // ---- step accounting + eager demotion (Alg. 1 l.20-23) for the batch --------------------
-  for (uint32_t i = tid; i < n_batch; i += FIN_THREADS) {
-    uint32_t s = klo[i];
-    uint32_t qf = ct.qf[s];
-    uint32_t q = qf & QF_QMASK;
-    ct.exec[s] += 1;
-    ct.mtime[s] += 1;
-    uint32_t qt = ct.quanta[s];
-    if (qt != AUTX_INF) {
-      qt -= 1;
-      if (qt == 0) {
-        q = min(q + 1, pol.K - 1);
-        qt = pol.quanta[q];
+  // ---- step accounting + eager demotion (Alg. 1 l.20-23) for the batch, from registers ------
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    uint32_t i = tid * R + r;
+    if (i < n_batch) {
+      uint32_t sl = c_s[r];
+      uint32_t q = c_qf[r] & QF_QMASK;
+      ct.exec[sl] = c_ex[r] + 1;
+      ct.mtime[sl] = c_mt[r] + 1;
+      uint32_t qt = c_qt[r];
+      if (qt != AUTX_INF) {
+        qt -= 1;
+        if (qt == 0) {
+          q = min(q + 1, pol.K - 1);
+          qt = pol.quanta[q];
+        }
+        ct.quanta[sl] = qt;
       }
-      ct.quanta[s] = qt;
+      ct.qf[sl] = (uint8_t)(q | QF_RUN | QF_RES);
+      out.prev_slots[i] = sl;
     }
-    ct.qf[s] = (uint8_t)(q | QF_RUN | QF_RES);
-    out.prev_slots[i] = s;
   }
   if (tid == 0) {
     ctl->n_prev = n_batch;
@@ -772,7 +825,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     h.n_promoted = ctl->n_promoted;
     h.err = ctl->err;
     h.seqno = seqno;
-    h._pad = 0;
+    h.err_info = ctl->err_info;
     *out.hout = h;
     ctl->n_promoted = 0;
     ctl->n_live = 0;
@@ -786,7 +839,13 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
 cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                             const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
                             CompRec* rec_out, bool apply) {
-  k_complete<<<1, FIN_THREADS, 0, s>>>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+  // size the CTA to the record count: a typical step completes ~BS/mean-decode calls
+  if (n <= 32)
+    k_complete<32><<<1, 32, 0, s>>>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+  else if (n <= 256)
+    k_complete<256><<<1, 256, 0, s>>>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+  else
+    k_complete<FIN_THREADS><<<1, FIN_THREADS, 0, s>>>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
   return cudaGetLastError();
 }
 
