@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
 SCAN_BYTES_PER_CALL = 13      # qf 1 + prog 4 + base 4 + mtime 4
-PROMOTE_BYTES = 13            # qf 1 + base 4 + mtime 4 + quanta 4 written per promotion
+PROMOTE_BYTES = 4             # base written per promotion (other fields only if they change)
 PROG_BYTES = 12               # svc 4 + pwait 8 gathered per program
 
 
@@ -274,7 +274,6 @@ def main():
     t_setup = time.time() - t_setup
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    s.set_timing(True)
     gate_cycles = 2_000_000                   # ~1 ms spin while the host enqueues the step
 
     def timed_step():
@@ -287,9 +286,9 @@ def main():
         b.record(stream)
         rec = d.finish()
         b.synchronize()
-        tm = s.last_step_timing()
-        return a.elapsed_time(b), rec, tm, nc, na
+        return a.elapsed_time(b), rec, nc, na
 
+    s.set_timing(False)                      # no per-kernel events inside the timed steps
     for _ in range(args.warmup):
         timed_step()
     if world > 1:
@@ -299,26 +298,29 @@ def main():
         os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_r{rank}.csv")
     clocks.start()
     ms, decisions, launches = [], 0, 0
-    scan_ms, fin_ms, sel_ms, comp_ms, reg_ms = [], [], [], [], []
-    scan_bytes = []
-    promoted = []
-    phase = []
     for _ in range(args.steps):
-        dt, rec, tm, nc, na = timed_step()
+        dt, rec, nc, na = timed_step()
         ms.append(dt)
         decisions += rec["n_active"]
-        launches += 3 + (1 if nc else 0) + (1 if na else 0)
-        scan_ms.append(tm.scan_ms); sel_ms.append(tm.select_ms); fin_ms.append(tm.finalize_ms)
-        comp_ms.append(tm.complete_ms); reg_ms.append(tm.register_ms)
-        promoted.append(rec["n_promoted"])
-        if len(phase) < 20:
-            phase.append(s.phase_times().astype(np.int64))
-        scan_bytes.append(SCAN_BYTES_PER_CALL * rec["n_active"] + PROMOTE_BYTES * rec["n_promoted"]
-                          + PROG_BYTES * tr.n_programs)
+        launches += 4 + (1 if nc else 0) + (1 if na else 0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ck = clocks.stop(local)
+    # per-kernel breakdown: a separate run of steps with the library's CUDA events on
+    s.set_timing(True)
+    scan_ms, fin_ms, sel_ms, comp_ms, reg_ms = [], [], [], [], []
+    scan_bytes, promoted, phase = [], [], []
+    for _ in range(30):
+        _, rec, nc, na = timed_step()
+        tm = s.last_step_timing()
+        scan_ms.append(tm.scan_ms); sel_ms.append(tm.select_ms); fin_ms.append(tm.finalize_ms)
+        comp_ms.append(tm.complete_ms); reg_ms.append(tm.register_ms)
+        promoted.append(rec["n_promoted"])
+        phase.append(s.phase_times().astype(np.int64))
+        scan_bytes.append(SCAN_BYTES_PER_CALL * rec["n_active"] + PROMOTE_BYTES * rec["n_promoted"]
+                          + PROG_BYTES * tr.n_programs)
+    s.set_timing(False)
     total_ms = sum(ms)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -363,7 +365,7 @@ def main():
                      "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": int(statistics.mean(scan_bytes))},
         "breakdown_ms": {"complete": statistics.mean(comp_ms), "register": statistics.mean(reg_ms),
-                         "scan": scan_avg_ms, "gather": statistics.mean(sel_ms),
+                         "scan": scan_avg_ms, "select+gather": statistics.mean(sel_ms),
                          "finalize": statistics.mean(fin_ms),
                          "step_p10": float(np.percentile(ms, 10)), "step_p50": float(np.percentile(ms, 50)),
                          "step_p90": float(np.percentile(ms, 90))},

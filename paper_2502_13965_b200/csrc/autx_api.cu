@@ -143,6 +143,8 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&o.admit_slots, BS));
   o.cand_cap = 2 * BS;
   CK(dalloc(&o.cand, o.cand_cap));
+  CK(dalloc(&o.cand_rec, o.cand_cap));
+  CK(dalloc(&o.prev_rec, BS));
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K)); CK(dalloc(&o.tile_off, ntiles + 1));
   CK(dalloc(&o.tile_pre, ntiles + 1));
   CK(dalloc(&o.tile_stat, ntiles + 1));
@@ -282,7 +284,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
                  t.loc, t.hcls, ctx->pt.svc, ctx->pt.pwait, ctx->pt.last_arr, ctx->pt.last_comp,
                  ctx->ctl, ctx->out.batch_slots, ctx->out.batch_ids, ctx->out.admit_ids,
                  ctx->out.preempt_ids, ctx->out.prev_slots, ctx->out.preempt_slots,
-                 ctx->out.admit_slots, ctx->out.cand, ctx->out.tile_cnt, ctx->out.tile_off,
+                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.tile_cnt, ctx->out.tile_off,
                  ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
@@ -389,10 +391,10 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
     ctx->last_batch.erase(ids[i]);
   }
   uint32_t t = next_step(ctx);
-  CK(cudaMemcpyAsync(ctx->d_cslots, ctx->h_cslots, n * 4, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
   CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
-  CK(launch_complete(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->d_cslots, n, t, ctx->kv,
+  // the kernel reads the pinned staging directly (zero-copy, a few hundred bytes)
+  CK(launch_complete(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->h_cslots, n, t, ctx->kv,
                      ctx->kv_on, recs, ctx->cfg.nranks <= 1));
   if (ctx->timing) {
     cudaEventRecord(ctx->ev[5], ctx->stream);
@@ -502,10 +504,14 @@ extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* c
   ctx->last_key[0] = l.arrival_step; ctx->last_key[1] = l.program_arrival_step;
   ctx->last_key[2] = l.program_id; ctx->last_key[3] = l.call_id;
   ctx->have_last_key = true;
-  CK(cudaMemcpyAsync(ctx->d_arr, ctx->h_arr, (size_t)n * sizeof(ArrivalRec), cudaMemcpyHostToDevice,
-                     ctx->stream));
+  const ArrivalRec* recs = ctx->h_arr;  // zero-copy for per-step batches
+  if (n > 4096) {  // bulk registration (e.g. an offline burst): one DMA instead of PCIe reads
+    CK(cudaMemcpyAsync(ctx->d_arr, ctx->h_arr, (size_t)n * sizeof(ArrivalRec), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    recs = ctx->d_arr;
+  }
   if (ctx->timing) cudaEventRecord(ctx->ev[6], ctx->stream);
-  CK(launch_register(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->d_arr, n, ctx->tail, t));
+  CK(launch_register(ctx->stream, ctx->pol, ctx->ct, ctx->pt, recs, n, ctx->tail, t));
   if (ctx->timing) {
     cudaEventRecord(ctx->ev[7], ctx->stream);
     ctx->timed_register = true;

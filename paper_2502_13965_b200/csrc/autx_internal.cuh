@@ -119,6 +119,29 @@ struct KvState {
   uint32_t plan_cap;        // capacity of the plan block lists
 };
 
+// Candidate record written by the multi-CTA gather so that the single-CTA finalize reads
+// contiguous, L2-resident data instead of chasing random rows of the call table.
+struct CandRec {
+  unsigned long long cid;
+  uint32_t slot, arr, tok, exec, mtime, quanta, qf, _pad;
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void load_rec(const struct CallTable& ct, uint32_t s, CandRec* r) {
+  CandRec x;
+  x.cid = ct.cid[s];
+  x.slot = s;
+  x.arr = ct.arr[s];
+  x.tok = ct.tok[s];
+  x.exec = ct.exec[s];
+  x.mtime = ct.mtime[s];
+  x.quanta = ct.quanta[s];
+  x.qf = ct.qf[s];
+  x._pad = 0;
+  *r = x;
+}
+#endif
+
 struct Outputs {
   uint32_t* batch_slots;     // [max_batch]
   uint64_t* batch_ids;       // [max_batch]
@@ -127,8 +150,10 @@ struct Outputs {
   uint32_t* prev_slots;      // [max_batch] previous batch (slots), ctl->n_prev entries
   uint32_t* preempt_slots;   // [max_batch]
   uint32_t* admit_slots;     // [max_batch]
-  uint32_t* cand;            // [cand_cap] candidate slots
+  uint32_t* cand;            // [cand_cap] candidate slots (radix path)
   uint32_t cand_cap;
+  CandRec* cand_rec;         // [cand_cap] region-A candidate records
+  CandRec* prev_rec;         // [max_batch] records of the previous batch
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* tile_off;        // [ntiles_cap+1] candidate offsets
   uint32_t* tile_pre;        // [ntiles_cap] q* rows in earlier tiles
@@ -177,6 +202,24 @@ struct ArrivalRec {
   uint32_t flags;  // bit0: program is new in this batch (inh = 0); bit1: first record of it
   uint32_t _pad;
 };
+
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
+// predecessor in the stream still runs; it must call pdl_wait() before touching its inputs.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 
 // ---- kernel launchers (sched_kernels.cu / swap_kernels.cu) ----------------------------------
 cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,

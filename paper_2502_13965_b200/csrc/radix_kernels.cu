@@ -153,9 +153,14 @@ __global__ void __launch_bounds__(RX_THREADS) k_scatter(const uint64_t* in, uint
   }
 }
 
-__global__ void k_take(const uint64_t* keys, Ctl* ctl, Outputs out, uint32_t BS, uint32_t K) {
+__global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out, uint32_t BS, uint32_t K) {
   uint32_t n = min(BS, ctl->n_live);
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out.cand[i] = (uint32_t)keys[i];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    uint32_t sl = (uint32_t)keys[i];
+    out.cand[i] = sl;
+    load_rec(ct, sl, out.cand_rec + i);
+  }
+  for (uint32_t j = threadIdx.x; j < ctl->n_prev; j += blockDim.x) load_rec(ct, out.prev_slots[j], out.prev_rec + j);
   if (threadIdx.x == 0) {
     ctl->n_cand_a = n;
     ctl->qstar = K;  // no extra running candidates: the sort already ordered them
@@ -190,7 +195,7 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
     std::swap(a, b);
     ++passes;
   }
-  k_take<<<1, 1024, 0, s>>>(a, ctl, out, pol.max_batch, pol.K);
+  k_take<<<1, 1024, 0, s>>>(a, ct, ctl, out, pol.max_batch, pol.K);
   if (passes_out) *passes_out = passes;
   return cudaGetLastError();
 }

@@ -81,6 +81,8 @@ __global__ void __launch_bounds__(NT) k_complete(Policy pol, CallTable ct, ProgT
                                                           Ctl* ctl, const uint32_t* slots,
                                                           uint32_t n, uint32_t t, KvState kv,
                                                           bool kv_on, CompRec* rec_out, bool apply) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
   STAMP(16);
@@ -187,6 +189,8 @@ __global__ void k_route(const char* base, uint64_t stride, uint32_t G, const Rou
 // ---------------------------------------------------------------------------------------------
 __global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const ArrivalRec* recs,
                            uint32_t n, uint32_t first_slot, uint32_t t) {
+  pdl_wait();
+  pdl_trigger();
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   ArrivalRec r = recs[i];
@@ -236,6 +240,8 @@ __device__ __forceinline__ void count_q(uint64_t& c0, uint64_t& c1, uint64_t& c2
 
 __global__ void __launch_bounds__(SCAN_THREADS, 3) k_scan(Policy pol, CallTable ct, ProgTable pt,
                                                           Outputs out, uint32_t t, uint32_t n_rows) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t tile = blockIdx.x;
   const uint32_t row0 = tile * TILE + threadIdx.x * ROWS_PER_THREAD;
   uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
@@ -334,6 +340,8 @@ __global__ void __launch_bounds__(SCAN_THREADS, 3) k_scan(Policy pol, CallTable 
 constexpr int SEL_THREADS = 1024;
 __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Outputs out,
                                                         uint32_t ntiles) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t tot[MAX_K + 2];
   __shared__ unsigned long long red[33];
   __shared__ uint32_t s_qstar, s_m;
@@ -415,13 +423,20 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
 }
 
 // ---------------------------------------------------------------------------------------------
-// a5 candidate gather: tiles with candidates re-read their 2 KB of qf and emit row indices in
-// table order; the emitted rows are marked QF_INB so finalize can add the running calls of q*
-// that were not emitted.
+// a5 candidate gather: tiles with candidates re-read their 2 KB of qf and emit one CandRec per
+// candidate (q < q*, or among the first m' rows of q*) in table order.  CTAs past the last tile
+// write the records of the previous batch (the resident set) for preempt/region B.
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable ct, const Ctl* ctl,
-                                                         Outputs out, uint32_t n_rows) {
+                                                         Outputs out, uint32_t n_rows, uint32_t ntiles) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t tile = blockIdx.x;
+  if (tile >= ntiles) {
+    uint32_t j = (tile - ntiles) * SCAN_THREADS + threadIdx.x;
+    if (j < ctl->n_prev) load_rec(ct, out.prev_slots[j], out.prev_rec + j);
+    return;
+  }
   const uint32_t off = out.tile_off[tile];
   const uint32_t cnt = out.tile_off[tile + 1] - off;
   if (cnt == 0) return;
@@ -447,37 +462,45 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
     if (sel) { flags |= 1u << j; ++nsel; }
   }
   uint32_t pos = off + block_excl_scan<uint32_t, SCAN_THREADS>(nsel, red, nullptr);
-  if (flags) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (flags & (1u << j)) {
-        out.cand[pos++] = row0 + j;
-        qfs[j] |= QF_INB;
-      }
-    uint2 qn;
-    qn.x = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
-    qn.y = qfs[4] | (qfs[5] << 8) | (qfs[6] << 16) | (qfs[7] << 24);
-    *reinterpret_cast<uint2*>(ct.qf + row0) = qn;
-  }
+  for (int j = 0; j < 8; ++j)
+    if (flags & (1u << j)) {
+      out.cand[pos] = row0 + j;
+      load_rec(ct, row0 + j, out.cand_rec + pos);
+      ++pos;
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
-// a5/a6/a3/a7-plan: one CTA.  Sort <= 2 BS candidates by the unique key
-// (q, arrival, not-running, seq) (R11, R12), cut the longest prefix with count <= BS and
-// sum kvb <= P (Alg. 1 l.32-39, first misfit stops, R13), emit batch/admit/preempt, account
-// (batch: exec++, mtime++, quanta--, running; others implicitly wait++ via the closed form),
-// demote batch calls whose quantum is exhausted (Alg. 1 l.20-23), allocate KV blocks and build
-// the swap plan.
+// a5/a6/a3/a7-plan: one CTA.  Sort <= 2 BS candidate keys
+//     q:4 | arrival (relative to t):27 | not-running:1 | seq (row):31       (R11, R12)
+// (region A from the gather, plus the previous batch's calls of q*, de-duplicated), cut the
+// longest prefix with count <= BS and sum kvb <= P (Alg. 1 l.32-39, first misfit stops, R13),
+// emit batch/admit/preempt, account (batch: exec++, mtime++, quanta--, running; everyone else
+// waits implicitly via the closed-form counters), demote batch calls whose quantum is exhausted
+// (Alg. 1 l.20-23), allocate KV blocks and build the swap plan.
 // ---------------------------------------------------------------------------------------------
 extern __shared__ unsigned char fin_smem[];
 
 __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
+constexpr uint32_t REC_PREV = 0x80000000u;  // index flag: record lives in prev_rec
+
+__device__ __forceinline__ uint64_t cand_key(const CandRec& r, uint32_t t) {
+  uint64_t arel = (uint64_t)((1u << 27) - 1 - (t - r.arr)) & ((1u << 27) - 1);  // later arrival: larger
+  return ((uint64_t)(r.qf & QF_QMASK) << 59) | (arel << 32) | ((uint64_t)((r.qf & QF_RUN) ? 0u : 1u) << 31) |
+         (r.slot & 0x7FFFFFFFu);
+}
+
 __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable ct, Ctl* ctl,
                                                           Outputs out, KvState kv, bool kv_on,
                                                           uint32_t t, uint32_t np, uint32_t seqno) {
-  uint64_t* khi = reinterpret_cast<uint64_t*>(fin_smem);
-  uint32_t* klo = reinterpret_cast<uint32_t*>(khi + np);
+  pdl_wait();
+  pdl_trigger();
+  uint64_t* khi = reinterpret_cast<uint64_t*>(fin_smem);   // [np] keys
+  uint64_t* uk = khi + np;                                   // [np] unique sorted keys
+  uint32_t* klo = reinterpret_cast<uint32_t*>(uk + np);      // [np] record index
+  uint32_t* ui = klo + np;                                   // [np] record index (unique)
   __shared__ unsigned long long red64[33];
   __shared__ uint32_t red[33];
   __shared__ uint32_t s_nb, s_nbatch;
@@ -485,57 +508,51 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   const uint32_t BS = pol.max_batch;
   const uint32_t nA = ctl->n_cand_a, qs = ctl->qstar, n_prev = ctl->n_prev;
   STAMP(0);
-  if (tid == 0) s_nb = 0;
-  __syncthreads();
-  // ---- (1) previous batch = resident set: everything preempt needs, in one round trip --------
-  constexpr int R = 4;  // items per thread, blocked (i = tid * R + r); BS <= 4096
-  uint32_t p_s[R], p_qf[R], p_arr[R], p_tok[R], p_ex[R];
-  uint64_t p_cid[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    uint32_t i = tid * R + r;
-    p_qf[r] = QF_DEAD;
-    if (i < n_prev) {
-      uint32_t sl = out.prev_slots[i];
-      p_s[r] = sl;
-      p_qf[r] = ct.qf[sl];
-      p_arr[r] = ct.arr[sl];
-      p_tok[r] = ct.tok[sl];
-      p_ex[r] = ct.exec[sl];
-      p_cid[r] = ct.cid[sl];
-    }
-  }
+  if (tid == 0) { s_nb = 0; s_nbatch = 0; }
   for (uint32_t i = tid; i < np; i += FIN_THREADS) { khi[i] = ~0ull; klo[i] = ~0u; }
   __syncthreads();
-  STAMP(9);
-  // running calls of q* that the gather did not emit (region B)
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    uint32_t qf = p_qf[r];
-    if (!(qf & QF_DEAD) && (qf & QF_QMASK) == qs && !(qf & QF_INB)) {
-      uint32_t j = nA + atomicAdd(&s_nb, 1u);
-      khi[j] = ((uint64_t)qs << 33) | ((uint64_t)p_arr[r] << 1);  // running: not-running bit 0
-      klo[j] = p_s[r];
-    }
-  }
-  __syncthreads();  // INB of region-A rows was read above before it is cleared below
-  STAMP(10);
+  // ---- (1) keys: region A + the previous batch's calls of q* (may duplicate A) ---------------
   for (uint32_t i = tid; i < nA; i += FIN_THREADS) {
-    uint32_t sl = out.cand[i];
-    uint32_t qf = ct.qf[sl];
-    khi[i] = ((uint64_t)(qf & QF_QMASK) << 33) | ((uint64_t)ct.arr[sl] << 1) | ((qf & QF_RUN) ? 0u : 1u);
-    klo[i] = sl;
-    ct.qf[sl] = (uint8_t)(qf & ~QF_INB);
+    khi[i] = cand_key(out.cand_rec[i], t);
+    klo[i] = i;
+  }
+  for (uint32_t j = tid; j < n_prev; j += FIN_THREADS) {
+    CandRec r = out.prev_rec[j];
+    if (!(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == qs) {
+      uint32_t p = nA + atomicAdd(&s_nb, 1u);
+      khi[p] = cand_key(r, t);
+      klo[p] = REC_PREV | j;
+    }
   }
   __syncthreads();
   STAMP(1);
-  const uint32_t ncand = nA + s_nb;
+  const uint32_t n_all = nA + s_nb;
   uint32_t np2 = 2;
-  while (np2 < ncand) np2 <<= 1;
+  while (np2 < n_all) np2 <<= 1;
   bitonic_sort_pairs<FIN_THREADS>(khi, klo, min(np2, np));
   STAMP(2);
-  // ---- (2) the first m = min(BS, ncand) keys: load their fields once; prefix cutoff ---------
+  // ---- (2) de-duplicate (a running call of q* can be both in A and in the previous batch) ----
+  constexpr int D = 8;  // keys per thread, blocked; np <= 8192
+  uint32_t keep = 0, nkeep = 0;
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    uint32_t i = tid * D + r;
+    if (i < n_all && (i == 0 || khi[i] != khi[i - 1])) { keep |= 1u << r; ++nkeep; }
+  }
+  uint32_t ntot;
+  uint32_t kpos = block_excl_scan<uint32_t, FIN_THREADS>(nkeep, red, &ntot);
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+    if (keep & (1u << r)) {
+      uk[kpos] = khi[tid * D + r];
+      ui[kpos] = klo[tid * D + r];
+      ++kpos;
+    }
+  __syncthreads();
+  const uint32_t ncand = ntot;
+  // ---- (3) the first m = min(BS, ncand) keys: fields from the records; prefix cutoff ---------
   const uint32_t m = min(BS, ncand);
+  constexpr int R = 4;  // items per thread, blocked (i = tid * R + r); BS <= 4096
   uint32_t c_s[R], c_qf[R], c_tok[R], c_ex[R], c_mt[R], c_qt[R], c_kvb[R];
   uint64_t c_cid[R];
   unsigned long long my_kv = 0;
@@ -544,25 +561,20 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     uint32_t i = tid * R + r;
     c_kvb[r] = 0;
     if (i < m) {
-      uint32_t sl = klo[i];
-      c_s[r] = sl;
-      c_qf[r] = ct.qf[sl];
-      c_tok[r] = ct.tok[sl];
-      c_ex[r] = ct.exec[sl];
-      c_mt[r] = ct.mtime[sl];
-      c_qt[r] = ct.quanta[sl];
-      c_cid[r] = ct.cid[sl];
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (tid * R + r < m) {
+      uint32_t x = ui[i];
+      const CandRec& rc = (x & REC_PREV) ? out.prev_rec[x & ~REC_PREV] : out.cand_rec[x];
+      c_s[r] = rc.slot;
+      c_qf[r] = rc.qf;
+      c_tok[r] = rc.tok;
+      c_ex[r] = rc.exec;
+      c_mt[r] = rc.mtime;
+      c_qt[r] = rc.quanta;
+      c_cid[r] = rc.cid;
       c_kvb[r] = ceil_div_u32(c_tok[r] + c_ex[r] + 1, pol.block_tokens);  // R14
       my_kv += c_kvb[r];
     }
+  }
   unsigned long long kv_pre = block_excl_scan<unsigned long long, FIN_THREADS>(my_kv, red64, nullptr);
-  if (tid == 0) s_nbatch = 0;
-  __syncthreads();
   // Alg. 1 l.34-37: take while count <= BS and sum kvb <= P; kvb >= 1 makes the prefix sums
   // strictly increasing, so the fitting items are exactly a prefix: n_batch = max fitting i + 1
   {
@@ -580,9 +592,9 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   const uint32_t n_batch = s_nbatch;
   STAMP(3);
   if (tid == 0 && ncand > 0 && n_batch == 0) {
-    if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u) ctl->err_info = klo[0];
+    if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u) ctl->err_info = (uint32_t)(uk[0] & 0x7FFFFFFF);
   }
-  // ---- (3) batch list and admit = batch calls not resident (batch order) -------------------
+  // ---- (4) batch list and admit = batch calls not resident (batch order) -------------------
   unsigned long long my_ad = 0, kv_mine = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -616,24 +628,31 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   const uint32_t n_admit = (uint32_t)(ad_tot >> 44);
   const unsigned long long swap_in = ad_tot & ((1ull << 44) - 1);
   STAMP(4);
-  // ---- (4) preempt = previous batch, still active, not in the batch (previous-batch order) ---
+  // ---- (5) preempt = previous batch, still active, not in the batch (previous-batch order) ---
   unsigned long long my_pre = 0;
   uint32_t is_pre = 0;
+  uint32_t p_s[R], p_qf[R];
+  uint64_t p_cid[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t i = tid * R + r;
-    if (i < n_prev && !(p_qf[r] & QF_DEAD)) {
-      // membership: binary search of the row's key in the sorted batch prefix
-      uint64_t key = ((uint64_t)(p_qf[r] & QF_QMASK) << 33) | ((uint64_t)p_arr[r] << 1);
-      uint32_t lo = 0, hi = n_batch;
-      while (lo < hi) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (pair_gt(key, p_s[r], khi[mid], klo[mid])) lo = mid + 1; else hi = mid;
-      }
-      bool in = lo < n_batch && khi[lo] == key && klo[lo] == p_s[r];
-      if (!in) {
-        is_pre |= 1u << r;
-        my_pre += (1ull << 44) | ceil_div_u32(p_tok[r] + p_ex[r], pol.block_tokens);  // R28
+    if (i < n_prev) {
+      CandRec pr = out.prev_rec[i];
+      p_s[r] = pr.slot;
+      p_qf[r] = pr.qf;
+      p_cid[r] = pr.cid;
+      if (!(pr.qf & QF_DEAD)) {
+        // membership: binary search of the row's (unique) key in the sorted batch prefix
+        uint64_t key = cand_key(pr, t);
+        uint32_t lo = 0, hi = n_batch;
+        while (lo < hi) {
+          uint32_t mid = (lo + hi) >> 1;
+          if (uk[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        if (!(lo < n_batch && uk[lo] == key)) {
+          is_pre |= 1u << r;
+          my_pre += (1ull << 44) | ceil_div_u32(pr.tok + pr.exec, pol.block_tokens);  // R28
+        }
       }
     }
   }
@@ -710,7 +729,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
       uint32_t i = c0 + tid;
       uint32_t s = 0, need = 0, have = 0, rslot = NONE, admit = 0, held = 0;
       if (i < n_batch) {
-        s = klo[i];
+        s = (uint32_t)(uk[i] & 0x7FFFFFFFu);
         uint32_t qf = ct.qf[s];
         need = ceil_div_u32(ct.tok[s] + ct.exec[s] + 1, pol.block_tokens);
         if (need > W) set_err(ctl, AUTX_E_NOMEM, 2);
@@ -767,7 +786,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     for (uint32_t c0 = 0; c0 < n_batch; c0 += FIN_THREADS) {
       uint32_t i = c0 + tid;
       uint32_t need = 0, rslot = 0;
-      if (i < n_batch) { rslot = ct.loc[klo[i]]; need = kv.rs_nblk[rslot]; }
+      if (i < n_batch) { rslot = ct.loc[(uint32_t)(uk[i] & 0x7FFFFFFFu)]; need = kv.rs_nblk[rslot]; }
       uint32_t tot;
       uint32_t o = b0 + block_excl_scan<uint32_t, FIN_THREADS>(need, red, &tot);
       if (i < n_batch) {
@@ -841,11 +860,11 @@ cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, Pro
                             CompRec* rec_out, bool apply) {
   // size the CTA to the record count: a typical step completes ~BS/mean-decode calls
   if (n <= 32)
-    k_complete<32><<<1, 32, 0, s>>>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+    return launch_pdl(k_complete<32>, 1, 32, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
   else if (n <= 256)
-    k_complete<256><<<1, 256, 0, s>>>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+    return launch_pdl(k_complete<256>, 1, 256, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
   else
-    k_complete<FIN_THREADS><<<1, FIN_THREADS, 0, s>>>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+    return launch_pdl(k_complete<FIN_THREADS>, 1, FIN_THREADS, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
   return cudaGetLastError();
 }
 
@@ -865,7 +884,7 @@ cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint
 cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt,
                             const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t) {
   if (n == 0) return cudaSuccess;
-  k_register<<<(n + 255) / 256, 256, 0, s>>>(pol, ct, pt, recs, n, first_slot, t);
+  return launch_pdl(k_register, (n + 255) / 256, 256, 0, s, pol, ct, pt, recs, n, first_slot, t);
   return cudaGetLastError();
 }
 
@@ -889,20 +908,21 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[1], s);
   } else {
-    k_scan<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, pt, out, t, n_rows);
+    launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, out, t, n_rows);
     if (ev) cudaEventRecord(ev[1], s);
-    k_select<<<1, SEL_THREADS, 0, s>>>(pol, ctl, out, ntiles);
-    k_gather<<<ntiles, SCAN_THREADS, 0, s>>>(pol, ct, ctl, out, n_rows);
+    launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
+    launch_pdl(k_gather, ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS, SCAN_THREADS, 0, s, pol,
+               ct, ctl, out, n_rows, ntiles);
   }
   if (ev) cudaEventRecord(ev[2], s);
   uint32_t np = pow2_at_least(2 * pol.max_batch);
-  size_t smem = (size_t)np * (sizeof(uint64_t) + sizeof(uint32_t));
+  size_t smem = (size_t)np * 2 * (sizeof(uint64_t) + sizeof(uint32_t));
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  k_finalize<<<1, FIN_THREADS, smem, s>>>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  launch_pdl(k_finalize, 1, FIN_THREADS, smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
   if (ev) cudaEventRecord(ev[3], s);
   return cudaGetLastError();
 }
