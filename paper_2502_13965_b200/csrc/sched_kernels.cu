@@ -348,6 +348,68 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
   const uint32_t tid = threadIdx.x;
   if (tid < MAX_K + 2) tot[tid] = 0;
   __syncthreads();
+  if (ntiles <= SEL_THREADS) {
+    // fast path: one tile per thread, its 16 counters stay in registers (one load round trip)
+    uint32_t x[MAX_K];
+    uint2 st = make_uint2(0, 0);
+    if (tid < ntiles) {
+      const uint4* c = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)tid * MAX_K);
+#pragma unroll
+      for (int v = 0; v < MAX_K / 4; ++v) {
+        uint4 y = c[v];
+        x[4 * v] = y.x; x[4 * v + 1] = y.y; x[4 * v + 2] = y.z; x[4 * v + 3] = y.w;
+      }
+      st = out.tile_stat[tid];
+    } else {
+#pragma unroll
+      for (int k = 0; k < MAX_K; ++k) x[k] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < MAX_K; ++k) {
+      uint32_t w = warp_sum(x[k]);
+      if (lane_id() == 0 && w) atomicAdd(&tot[k], w);
+    }
+    uint32_t ap = warp_sum(st.x), al = warp_sum(st.y);
+    if (lane_id() == 0) {
+      if (ap) atomicAdd(&tot[MAX_K], ap);
+      if (al) atomicAdd(&tot[MAX_K + 1], al);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t cum = 0, qs = pol.K, m = 0;
+      for (uint32_t k = 0; k < pol.K; ++k) {
+        if (cum + tot[k] >= pol.max_batch) { qs = k; m = pol.max_batch - cum; break; }
+        cum += tot[k];
+      }
+      s_qstar = qs;
+      s_m = m;
+      ctl->qstar = qs;
+      ctl->mprime = m;
+      ctl->n_promoted = tot[MAX_K];
+      ctl->n_live = tot[MAX_K + 1];
+    }
+    __syncthreads();
+    const uint32_t qs = s_qstar, m = s_m;
+    uint32_t a = 0, cq = 0;
+#pragma unroll
+    for (int k = 0; k < MAX_K; ++k) {
+      a += (uint32_t)k < qs ? x[k] : 0u;
+      cq += (uint32_t)k == qs ? x[k] : 0u;
+    }
+    unsigned long long total;
+    uint64_t pre = block_excl_scan<unsigned long long, SEL_THREADS>(((uint64_t)a << 32) | cq, red, &total);
+    if (tid < ntiles) {
+      uint32_t pre_a = (uint32_t)(pre >> 32), pre_q = (uint32_t)pre;
+      out.tile_pre[tid] = pre_q;
+      out.tile_off[tid] = pre_a + min(pre_q, m);
+    }
+    if (tid == 0) {
+      uint32_t n = (uint32_t)(total >> 32) + min((uint32_t)total, m);
+      out.tile_off[ntiles] = n;
+      ctl->n_cand_a = n;
+    }
+    return;
+  }
   const uint32_t per = (ntiles + SEL_THREADS - 1) / SEL_THREADS;
   const uint32_t t0 = min(ntiles, tid * per), t1 = min(ntiles, t0 + per);
   uint32_t acc[MAX_K];
@@ -919,7 +981,9 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   size_t smem = (size_t)np * 2 * (sizeof(uint64_t) + sizeof(uint32_t));
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // 2 x np x (8 B key + 4 B index) <= 192 KiB at BS = 4096; the rest of the 227 KiB is static
+    cudaError_t e = cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
     attr_set = true;
   }
   launch_pdl(k_finalize, 1, FIN_THREADS, smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
