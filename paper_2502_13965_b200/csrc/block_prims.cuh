@@ -135,6 +135,61 @@ __device__ void bitonic_sort_pairs(uint64_t* hi, uint32_t* lo, uint32_t np) {
   }
 }
 
+// Bitonic sort of exactly 2*NT (key, payload) pairs held two per thread (element i lives in
+// thread i/2, slot i%2).  Partner distance j = 1 is a register swap, 2 <= j <= 32 a warp
+// shuffle, j >= 64 goes through shared memory (sk/sp: 2*NT entries).  Keys must be unique or
+// payload-tied; ascending order on (key, payload).
+template <int NT>
+__device__ void bitonic_sort_reg2(uint64_t& k0, uint32_t& v0, uint64_t& k1, uint32_t& v1, uint64_t* sk,
+                                  uint32_t* sp) {
+  constexpr uint32_t N = 2 * NT;
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t k = 2; k <= N; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j == 1) {
+        const bool asc = ((2 * tid) & k) == 0;
+        if (pair_gt(k0, v0, k1, v1) == asc) {
+          uint64_t tk = k0; k0 = k1; k1 = tk;
+          uint32_t tv = v0; v0 = v1; v1 = tv;
+        }
+      } else if (j <= 32) {
+        const uint32_t lanemask = j >> 1;  // partner thread = tid ^ (j/2), same warp
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          uint64_t& kk = r ? k1 : k0;
+          uint32_t& vv = r ? v1 : v0;
+          const uint32_t i = 2 * tid + r;
+          uint64_t pk = __shfl_xor_sync(0xffffffffu, kk, lanemask);
+          uint32_t pv = __shfl_xor_sync(0xffffffffu, vv, lanemask);
+          const bool asc = (i & k) == 0;
+          const bool lower = (i & j) == 0;           // i < partner
+          const bool keep_min = lower == asc;
+          const bool gt = pair_gt(kk, vv, pk, pv);
+          if (keep_min ? gt : !gt) { kk = pk; vv = pv; }
+        }
+      } else {
+        sk[2 * tid] = k0; sp[2 * tid] = v0;
+        sk[2 * tid + 1] = k1; sp[2 * tid + 1] = v1;
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          uint64_t& kk = r ? k1 : k0;
+          uint32_t& vv = r ? v1 : v0;
+          const uint32_t i = 2 * tid + r;
+          const uint32_t l = i ^ j;
+          uint64_t pk = sk[l];
+          uint32_t pv = sp[l];
+          const bool asc = (i & k) == 0;
+          const bool keep_min = (i < l) == asc;
+          const bool gt = pair_gt(kk, vv, pk, pv);
+          if (keep_min ? gt : !gt) { kk = pk; vv = pv; }
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
 // 128-bit compare: a*b >= c*d for u64 a, c and u32 b, d.
 __device__ __forceinline__ bool mul_ge(uint64_t a, uint32_t b, uint64_t c, uint32_t d) {
   uint64_t l1 = a * (uint64_t)b, h1 = __umul64hi(a, (uint64_t)b);

@@ -10,6 +10,9 @@
 //                      demotion, GPU block allocation and the swap plan
 //
 // Every step of Alg. 1 runs here; the host only stages records.  Citations: see autx.h.
+#include <algorithm>
+#include <cstdlib>
+
 #include "autx_internal.cuh"
 #include "block_prims.cuh"
 #include "../../include/autx.h"
@@ -330,6 +333,159 @@ __global__ void __launch_bounds__(SCAN_THREADS, 3) k_scan(Policy pol, CallTable 
   }
 }
 
+// Persistent, TMA-staged variant of the dense pass (the default): each CTA walks tiles
+// blockIdx.x, +gridDim.x, ...; one thread keeps SCAN_STAGES tiles in flight with
+// cp.async.bulk (global -> shared, completion counted on an mbarrier), so HBM keeps streaming
+// while the CTA gathers program rows and computes on the current tile.  Per-row arithmetic and
+// outputs are identical to k_scan.
+constexpr int SCAN_STAGES = 3;
+constexpr uint32_t STAGE_QF = TILE;             // bytes of qf per tile
+constexpr uint32_t STAGE_U32 = TILE * 4;        // bytes of one u32 field per tile
+constexpr uint32_t STAGE_BYTES = STAGE_QF + 3 * STAGE_U32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void issue_tile(const CallTable& ct, uint32_t tile, unsigned char* st, uint64_t* bar) {
+  const size_t r0 = (size_t)tile * TILE;
+  mbar_expect_tx(bar, STAGE_BYTES);
+  bulk_g2s(st, ct.qf + r0, STAGE_QF, bar);
+  bulk_g2s(st + STAGE_QF, ct.prog + r0, STAGE_U32, bar);
+  bulk_g2s(st + STAGE_QF + STAGE_U32, ct.base + r0, STAGE_U32, bar);
+  bulk_g2s(st + STAGE_QF + 2 * STAGE_U32, ct.mtime + r0, STAGE_U32, bar);
+}
+
+extern __shared__ __align__(128) unsigned char scan_smem[];
+
+__global__ void __launch_bounds__(SCAN_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt,
+                                                               Outputs out, uint32_t t, uint32_t ntiles) {
+  pdl_wait();
+  __shared__ __align__(8) uint64_t bars[SCAN_STAGES];
+  __shared__ uint64_t wc[SCAN_THREADS / 32][4];
+  __shared__ uint32_t wn[SCAN_THREADS / 32][2];
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < SCAN_STAGES; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 0; i < SCAN_STAGES; ++i) {
+      uint32_t tl = blockIdx.x + i * gridDim.x;
+      if (tl < ntiles) issue_tile(ct, tl, scan_smem + i * STAGE_BYTES, &bars[i]);
+    }
+  pdl_trigger();
+  uint32_t it = 0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const uint32_t stage = it % SCAN_STAGES;
+    unsigned char* st = scan_smem + stage * STAGE_BYTES;
+    mbar_wait(&bars[stage], (it / SCAN_STAGES) & 1);
+    const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+    const uint32_t lr = tid * ROWS_PER_THREAD;
+    const uint2 qv = *reinterpret_cast<const uint2*>(st + lr);
+    const uint4 p0 = *reinterpret_cast<const uint4*>(st + STAGE_QF + lr * 4);
+    const uint4 p1 = *reinterpret_cast<const uint4*>(st + STAGE_QF + lr * 4 + 16);
+    const uint4 b0 = *reinterpret_cast<const uint4*>(st + STAGE_QF + STAGE_U32 + lr * 4);
+    const uint4 b1 = *reinterpret_cast<const uint4*>(st + STAGE_QF + STAGE_U32 + lr * 4 + 16);
+    const uint4 m0 = *reinterpret_cast<const uint4*>(st + STAGE_QF + 2 * STAGE_U32 + lr * 4);
+    const uint4 m1 = *reinterpret_cast<const uint4*>(st + STAGE_QF + 2 * STAGE_U32 + lr * 4 + 16);
+    __syncthreads();  // every thread has its rows in registers: the stage can be refilled
+    if (tid == 0) {
+      uint32_t nxt = tile + SCAN_STAGES * gridDim.x;
+      if (nxt < ntiles) issue_tile(ct, nxt, st, &bars[stage]);
+    }
+    uint32_t qfs[8], prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
+    uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    uint32_t npromo = 0, nlive = 0;
+    uint32_t sv[8];
+    unsigned long long pw[8];
+    if (pol.beta_den != 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bool live = !(qfs[j] & QF_DEAD);
+        sv[j] = live ? pt.svc[prog[j]] : 0u;
+        pw[j] = live ? pt.pwait[prog[j]] : 0ull;
+      }
+    }
+    bool wq = false, wb = false, wm = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t qf = qfs[j];
+      if (qf & QF_DEAD) continue;
+      ++nlive;
+      uint32_t q = qf & QF_QMASK;
+      if (pol.beta_den != 0) {
+        uint64_t W = pw[j] + (uint64_t)(t - base[j] - mtim[j]);
+        uint64_t T = (uint64_t)sv[j] + mtim[j];
+        if (!(W == 0 && T == 0) && mul_ge(W, pol.beta_den, T, pol.beta_num)) {  // Alg. 1 l.26
+          if (q != 0 || mtim[j] != 0) ct.quanta[row0 + j] = pol.quanta[0];
+          if (q != 0) { qfs[j] = qf & ~QF_QMASK; wq = true; }
+          if (mtim[j] != 0) { mtim[j] = 0; wm = true; }
+          base[j] = t;
+          wb = true;
+          q = 0;
+          ++npromo;
+        }
+      }
+      count_q(c0, c1, c2, c3, q);
+    }
+    if (wq) {
+      uint2 qn;
+      qn.x = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
+      qn.y = qfs[4] | (qfs[5] << 8) | (qfs[6] << 16) | (qfs[7] << 24);
+      *reinterpret_cast<uint2*>(ct.qf + row0) = qn;
+    }
+    if (wb) {
+      *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
+      *reinterpret_cast<uint4*>(ct.base + row0 + 4) = make_uint4(base[4], base[5], base[6], base[7]);
+    }
+    if (wm) {
+      *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
+      *reinterpret_cast<uint4*>(ct.mtime + row0 + 4) = make_uint4(mtim[4], mtim[5], mtim[6], mtim[7]);
+    }
+    c0 = warp_sum(c0); c1 = warp_sum(c1); c2 = warp_sum(c2); c3 = warp_sum(c3);
+    npromo = warp_sum(npromo); nlive = warp_sum(nlive);
+    if (lane_id() == 0) {
+      wc[warp_id()][0] = c0; wc[warp_id()][1] = c1; wc[warp_id()][2] = c2; wc[warp_id()][3] = c3;
+      wn[warp_id()][0] = npromo; wn[warp_id()][1] = nlive;
+    }
+    __syncthreads();
+    if (tid < MAX_K) {
+      uint32_t k = tid, sum = 0;
+#pragma unroll
+      for (int w = 0; w < SCAN_THREADS / 32; ++w) sum += (uint32_t)(wc[w][k >> 2] >> ((k & 3) * 16)) & 0xffffu;
+      out.tile_cnt[(size_t)tile * MAX_K + k] = sum;
+    } else if (tid == 32) {
+      uint32_t a = 0, b = 0;
+#pragma unroll
+      for (int w = 0; w < SCAN_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
+      out.tile_stat[tile] = make_uint2(a, b);
+    }
+    __syncthreads();  // wc/wn reuse
+  }
+}
+
 // One CTA: q* = smallest q with sum_{k<=q} total_k >= BS (K if none), m' = BS - sum_{k<q*}
 // total_k.  Candidates: every live row with q < q*, plus the first m' rows of q* in table order.
 // Any call among the BS smallest keys is a candidate or a running call of q* (finalize adds
@@ -591,7 +747,18 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   const uint32_t n_all = nA + s_nb;
   uint32_t np2 = 2;
   while (np2 < n_all) np2 <<= 1;
-  bitonic_sort_pairs<FIN_THREADS>(khi, klo, min(np2, np));
+  if (np == 2 * FIN_THREADS) {
+    // register/shuffle network, 2 keys per thread (BS <= 1024)
+    uint64_t k0 = khi[2 * tid], k1 = khi[2 * tid + 1];
+    uint32_t v0 = klo[2 * tid], v1 = klo[2 * tid + 1];
+    __syncthreads();
+    bitonic_sort_reg2<FIN_THREADS>(k0, v0, k1, v1, khi, klo);
+    khi[2 * tid] = k0; klo[2 * tid] = v0;
+    khi[2 * tid + 1] = k1; klo[2 * tid + 1] = v1;
+    __syncthreads();
+  } else {
+    bitonic_sort_pairs<FIN_THREADS>(khi, klo, min(np2, np));
+  }
   STAMP(2);
   // ---- (2) de-duplicate (a running call of q* can be both in A and in the previous batch) ----
   constexpr int D = 8;  // keys per thread, blocked; np <= 8192
@@ -970,14 +1137,26 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[1], s);
   } else {
-    launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, out, t, n_rows);
+    static int scan_ctas = 0;
+    static bool simple = getenv("AUTX_SCAN_SIMPLE") != nullptr;  // A/B switch for profiling
+    if (!scan_ctas) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+      scan_ctas = 2 * sms;
+      cudaFuncSetAttribute(k_scan_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
+    }
+    if (simple)
+      launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, out, t, n_rows);
+    else
+      launch_pdl(k_scan_bulk, std::min<uint32_t>(ntiles, scan_ctas), SCAN_THREADS,
+                 (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, out, t, ntiles);
     if (ev) cudaEventRecord(ev[1], s);
     launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
     launch_pdl(k_gather, ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS, SCAN_THREADS, 0, s, pol,
                ct, ctl, out, n_rows, ntiles);
   }
   if (ev) cudaEventRecord(ev[2], s);
-  uint32_t np = pow2_at_least(2 * pol.max_batch);
+  uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2 * FIN_THREADS);
   size_t smem = (size_t)np * 2 * (sizeof(uint64_t) + sizeof(uint32_t));
   static bool attr_set = false;
   if (!attr_set) {
