@@ -406,3 +406,23 @@ def mixed(n_programs=30_000, seed=None, rate=None) -> Trace:
                               parents=loc, input_tokens=tr.input_tokens[a:b]))
     arr = _poisson_arrivals(rng, len(progs), rate)
     return _assemble("mixed", progs, arr)
+
+
+def concat(traces, name=None) -> Trace:
+    """Concatenates traces (e.g. one generated shard per engine) into one workload; program
+    indices, program ids and call ids are renumbered so they stay unique."""
+    P = np.cumsum([0] + [t.n_programs for t in traces])
+    C = np.cumsum([0] + [t.n_calls for t in traces])
+    cat = lambda f: np.concatenate([getattr(t, f) for t in traces])
+    call_prog = np.concatenate([t.call_prog + P[i] for i, t in enumerate(traces)])
+    call_idx = cat("call_idx")
+    first = np.concatenate([t.first_call[:-1] + C[i] for i, t in enumerate(traces)] + [[C[-1]]])
+    par_ptr = np.concatenate([t.par_ptr[:-1] + sum(len(x.par) for x in traces[:i]) for i, t in enumerate(traces)]
+                             + [[sum(len(x.par) for x in traces)]])
+    par = np.concatenate([t.par + C[i] for i, t in enumerate(traces)])
+    call_id = (call_prog.astype(np.uint64) << np.uint64(16)) | call_idx.astype(np.uint64)
+    return Trace(name=name or "+".join(t.name for t in traces), prog_id=np.arange(P[-1], dtype=np.uint64),
+                 prog_arrival=cat("prog_arrival"), first_call=first.astype(np.int64), call_prog=call_prog,
+                 call_idx=call_idx, call_id=call_id, decode=cat("decode"), prefill=cat("prefill"),
+                 input_tokens=cat("input_tokens"), delay=cat("delay"), par_ptr=par_ptr.astype(np.int64),
+                 par=par.astype(np.int64))

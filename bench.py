@@ -123,7 +123,10 @@ def dist_init(n):
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if os.environ.get("AUTX_DIST_BACKEND", "nccl") == "gloo":   # tests: several ranks on one GPU
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -259,14 +262,45 @@ def main():
     hbm_peak, peak_src = peaks()
 
     t_gen = time.time()
-    tr = burst_mcts_mapreduce(args.active, seed=BASE_SEED + CONFIG_INDEX["mcts"] + 1000 * rank)
+    if world == 1:
+        tr = burst_mcts_mapreduce(args.active, seed=BASE_SEED + CONFIG_INDEX["mcts"])
+    else:
+        # weak scaling: one 1M-call shard per engine; every rank holds the whole (replicated)
+        # workload because Alg. 2 routes each arrival to any engine
+        from autx_workload.gen import concat
+        tr = concat([burst_mcts_mapreduce(args.active, seed=BASE_SEED + CONFIG_INDEX["mcts"] + 1000 * r)
+                     for r in range(world)], name="mcts_mapreduce_burst_x%d" % world)
     t_gen = time.time() - t_gen
     lad = spec_ladder()
     s = Scheduler(policy="atlas", beta=(2, 1), max_batch=1024, kv_budget=32768, block_tokens=16,
                   max_calls=int(args.active * 1.25) + 4096, max_programs=tr.n_programs + 1024,
                   order_mode=ORDER_RADIX if args.order == "radix" else ORDER_SELECT,
-                  device=local, stream=stream.cuda_stream, **lad)
-    d = TraceDriver(tr, s, log_lists=False)
+                  device=local, stream=stream.cuda_stream, rank=rank, nranks=world, **lad)
+    if world == 1:
+        d = TraceDriver(tr, s, log_lists=False)
+    else:
+        from paper_2502_13965_b200.multi import MultiEngineDriver
+        gloo = os.environ.get("AUTX_DIST_BACKEND", "nccl") == "gloo"
+        nrec = s.route_record_bytes()
+        gathered = torch.empty(world * nrec, dtype=torch.uint8, device=dev)
+
+        def exchange(rec):
+            if gloo:
+                parts = [torch.empty(nrec, dtype=torch.uint8) for _ in range(world)]
+                torch.cuda.current_stream().synchronize()
+                dist.all_gather(parts, rec.cpu())
+                gathered.copy_(torch.cat(parts))
+            else:
+                dist.all_gather_into_tensor(gathered, rec)   # NCCL over NVLink, on the stream
+            return gathered
+
+        def gather_ids(local_ids):
+            out = [None] * world
+            dist.all_gather_object(out, np.asarray(local_ids, np.int64))
+            return out
+
+        d = MultiEngineDriver(tr, s, rank, world, exchange, gather_ids,
+                              lambda n: torch.zeros(n, dtype=torch.uint8, device=dev), log_lists=False)
     t_setup = time.time()
     d.step()                                  # step 0: registers the whole burst (setup)
     for _ in range(args.ff):
@@ -334,13 +368,15 @@ def main():
 
     # e2e: the same steps through the public API from the host, wall clock, no gate/flush
     s.set_timing(False)
-    e2e_dec, e2e_s, h2d, d2h = 0, 0.0, 0, 0
+    e2e_dec, e2e_s, h2d, d2h, wall_s = 0, 0.0, 0, 0, 0.0
     for _ in range(min(args.steps, 100)):
         nc = len(d.pending)
+        api0 = d.api_s
         t0 = time.perf_counter()
         _, na = d.issue()
         rec = d.finish()
-        e2e_s += time.perf_counter() - t0
+        wall_s += time.perf_counter() - t0
+        e2e_s += d.api_s - api0
         e2e_dec += rec["n_active"]
         h2d += 4 * nc + 24 * na
         d2h += 8 * (rec["n_batch"] + rec["n_admit"] + rec["n_preempt"]) + 48
@@ -354,7 +390,9 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
-        "config": {"workload": "mcts_mapreduce_burst (BASELINE configs[3])", "active_calls": args.active,
+        "config": {"workload": "mcts_mapreduce_burst (BASELINE configs[3])" if world == 1 else
+                   "mcts_mapreduce_burst x%d engines with Alg. 2 routing (BASELINE configs[4], weak)" % world,
+                   "active_calls_per_gpu": args.active,
                    "programs": tr.n_programs, "policy": "atlas", "ladder": "SPEC K=8", "beta": "2",
                    "max_batch": 1024, "kv_budget_blocks": 32768, "fast_forward_steps": args.ff,
                    "order": args.order, "l2": "flushed before every step (512 MiB write)" if not args.no_flush else "hot",
@@ -375,7 +413,10 @@ def main():
             ("batch_admit", 3, 4), ("preempt", 4, 5), ("kv", 6, 7), ("account", 7, 8))},
         "complete_phases_us": [round(float(np.median([p[i + 1] - p[i] for p in phase])) / 1e3, 2) for i in range(16, 19)],
         "e2e": {"value": e2e_dec / e2e_s, "unit": "decisions/s", "h2d_bytes_per_step": h2d // e2e_steps,
-                "d2h_bytes_per_step": d2h // e2e_steps, "ms_per_step": e2e_s * 1e3 / e2e_steps},
+                "d2h_bytes_per_step": d2h // e2e_steps, "ms_per_step": e2e_s * 1e3 / e2e_steps,
+                "timed": "wall clock inside the C-ABI calls (complete, end_program, register, sched_step, "
+                         "step_wait + list copies) per step; H2D staging and D2H mirrors included",
+                "harness_ms_per_step": (wall_s - e2e_s) * 1e3 / e2e_steps},
         "setup_s": {"generate": round(t_gen, 1), "register_and_fast_forward": round(t_setup, 1)},
     }
     if ck:

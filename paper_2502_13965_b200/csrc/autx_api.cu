@@ -145,6 +145,9 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&o.cand, o.cand_cap));
   CK(dalloc(&o.cand_rec, o.cand_cap));
   CK(dalloc(&o.prev_rec, BS));
+  CK(dalloc(&o.ckey, 2 * BS));
+  CK(dalloc(&o.skey, 2 * BS));
+  CK(dalloc(&o.sidx, 2 * BS));
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K)); CK(dalloc(&o.tile_off, ntiles + 1));
   CK(dalloc(&o.tile_pre, ntiles + 1));
   CK(dalloc(&o.tile_stat, ntiles + 1));
@@ -284,7 +287,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
                  t.loc, t.hcls, ctx->pt.svc, ctx->pt.pwait, ctx->pt.last_arr, ctx->pt.last_comp,
                  ctx->ctl, ctx->out.batch_slots, ctx->out.batch_ids, ctx->out.admit_ids,
                  ctx->out.preempt_ids, ctx->out.prev_slots, ctx->out.preempt_slots,
-                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.tile_cnt, ctx->out.tile_off,
+                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.tile_cnt, ctx->out.tile_off,
                  ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,

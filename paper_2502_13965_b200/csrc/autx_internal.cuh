@@ -127,6 +127,14 @@ struct CandRec {
 };
 
 #ifdef __CUDACC__
+// Unique 64-bit order key (R11, R12): q:4 | arrival relative to step t:27 | not-running:1 |
+// seq (row):31.  Requires t - arrival < 2^27 and rows < 2^31.
+__device__ __forceinline__ uint64_t cand_key(const CandRec& r, uint32_t t) {
+  uint64_t arel = (uint64_t)((1u << 27) - 1 - (t - r.arr)) & ((1u << 27) - 1);  // later arrival: larger
+  return ((uint64_t)(r.qf & QF_QMASK) << 59) | (arel << 32) | ((uint64_t)((r.qf & QF_RUN) ? 0u : 1u) << 31) |
+         (r.slot & 0x7FFFFFFFu);
+}
+
 __device__ __forceinline__ void load_rec(const struct CallTable& ct, uint32_t s, CandRec* r) {
   CandRec x;
   x.cid = ct.cid[s];
@@ -154,6 +162,9 @@ struct Outputs {
   uint32_t cand_cap;
   CandRec* cand_rec;         // [cand_cap] region-A candidate records
   CandRec* prev_rec;         // [max_batch] records of the previous batch
+  uint64_t* ckey;            // [2 BS] keys: region A at [0, nA), previous batch at [nA, nA + n_prev)
+  uint64_t* skey;            // [2 BS] keys sorted by k_rank
+  uint32_t* sidx;            // [2 BS] element index of each sorted key
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* tile_off;        // [ntiles_cap+1] candidate offsets
   uint32_t* tile_pre;        // [ntiles_cap] q* rows in earlier tiles

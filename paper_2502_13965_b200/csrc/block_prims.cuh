@@ -190,6 +190,91 @@ __device__ void bitonic_sort_reg2(uint64_t& k0, uint32_t& v0, uint64_t& k1, uint
   }
 }
 
+// Block merge sort of 2*NT (key, payload) pairs in shared memory (NT threads, NT a multiple of
+// 32, 2*NT a power of two <= 2^16).  Stage 1: every warp sorts its 64 consecutive pairs in
+// registers (bitonic, two per lane, shuffles only).  Stage 2: log2(2*NT/64) merge levels; each
+// pair finds its output index as (its index in its run) + (its rank in the sibling run), a
+// binary search; ties go to the left run, so the merge is stable.  Result in (k, p); (k2, p2)
+// is scratch of the same size.  Order: ascending (key, payload).
+__device__ __forceinline__ bool kp_less(uint64_t ak, uint32_t ap, uint64_t bk, uint32_t bp) {
+  return ak < bk || (ak == bk && ap < bp);
+}
+
+template <int NT>
+__device__ void block_merge_sort(uint64_t* k, uint32_t* p, uint64_t* k2, uint32_t* p2) {
+  constexpr uint32_t N = 2 * NT;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // ---- stage 1: 64-element runs per warp, in registers ----------------------------------
+  {
+    const uint32_t base = w * 64;
+    uint64_t k0 = k[base + 2 * lane], k1 = k[base + 2 * lane + 1];
+    uint32_t v0 = p[base + 2 * lane], v1 = p[base + 2 * lane + 1];
+    for (uint32_t kk = 2; kk <= 64; kk <<= 1) {
+      for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+        if (j == 1) {
+          const bool asc = ((2 * lane) & kk) == 0;
+          if (kp_less(k1, v1, k0, v0) == asc) {
+            uint64_t tk = k0; k0 = k1; k1 = tk;
+            uint32_t tv = v0; v0 = v1; v1 = tv;
+          }
+        } else {
+          const uint32_t m = j >> 1;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            uint64_t& x = r ? k1 : k0;
+            uint32_t& y = r ? v1 : v0;
+            const uint32_t i = 2 * lane + r;
+            uint64_t px = __shfl_xor_sync(0xffffffffu, x, m);
+            uint32_t py = __shfl_xor_sync(0xffffffffu, y, m);
+            const bool keep_min = ((i & j) == 0) == ((i & kk) == 0);
+            const bool take = keep_min ? kp_less(px, py, x, y) : kp_less(x, y, px, py);
+            if (take) { x = px; y = py; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    k[base + 2 * lane] = k0; p[base + 2 * lane] = v0;
+    k[base + 2 * lane + 1] = k1; p[base + 2 * lane + 1] = v1;
+  }
+  __syncthreads();
+  // ---- stage 2: merge levels ------------------------------------------------------------
+  uint64_t* sk = k; uint32_t* sp = p;
+  uint64_t* dk = k2; uint32_t* dp = p2;
+  for (uint32_t L = 64; L < N; L <<= 1) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t i = 2 * tid + r;
+      const uint32_t run = i / L, off = i % L;
+      const uint32_t pair_base = (run & ~1u) * L;
+      const bool left = (run & 1u) == 0;
+      const uint32_t sib = left ? pair_base + L : pair_base;
+      const uint64_t xk = sk[i];
+      const uint32_t xp = sp[i];
+      // rank in the sibling run: left elements count sibling keys < x (lower bound), right
+      // elements count sibling keys <= x (upper bound), which keeps the merge stable
+      uint32_t lo = 0, hi = L;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const uint64_t mk = sk[sib + mid];
+        const uint32_t mp = sp[sib + mid];
+        const bool before = left ? kp_less(mk, mp, xk, xp) : !kp_less(xk, xp, mk, mp);
+        if (before) lo = mid + 1; else hi = mid;
+      }
+      const uint32_t dst = pair_base + off + lo;
+      dk[dst] = xk;
+      dp[dst] = xp;
+    }
+    __syncthreads();
+    uint64_t* tk = sk; sk = dk; dk = tk;
+    uint32_t* tp = sp; sp = dp; dp = tp;
+  }
+  if (sk != k) {  // odd number of levels: copy back
+    for (uint32_t i = tid; i < N; i += NT) { k[i] = sk[i]; p[i] = sp[i]; }
+    __syncthreads();
+  }
+}
+
 // 128-bit compare: a*b >= c*d for u64 a, c and u32 b, d.
 __device__ __forceinline__ bool mul_ge(uint64_t a, uint32_t b, uint64_t c, uint32_t d) {
   uint64_t l1 = a * (uint64_t)b, h1 = __umul64hi(a, (uint64_t)b);

@@ -153,14 +153,22 @@ __global__ void __launch_bounds__(RX_THREADS) k_scatter(const uint64_t* in, uint
   }
 }
 
-__global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out, uint32_t BS, uint32_t K) {
+__global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out, uint32_t BS, uint32_t K,
+                       uint32_t t) {
   uint32_t n = min(BS, ctl->n_live);
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     uint32_t sl = (uint32_t)keys[i];
+    CandRec r;
+    load_rec(ct, sl, &r);
     out.cand[i] = sl;
-    load_rec(ct, sl, out.cand_rec + i);
+    out.cand_rec[i] = r;
+    out.ckey[i] = cand_key(r, t);
   }
-  for (uint32_t j = threadIdx.x; j < ctl->n_prev; j += blockDim.x) load_rec(ct, out.prev_slots[j], out.prev_rec + j);
+  // previous batch: records for preempt; no region B (the full sort already ranked them)
+  for (uint32_t j = threadIdx.x; j < ctl->n_prev; j += blockDim.x) {
+    load_rec(ct, out.prev_slots[j], out.prev_rec + j);
+    out.ckey[n + j] = ~0ull;
+  }
   if (threadIdx.x == 0) {
     ctl->n_cand_a = n;
     ctl->qstar = K;  // no extra running candidates: the sort already ordered them
@@ -195,7 +203,7 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
     std::swap(a, b);
     ++passes;
   }
-  k_take<<<1, 1024, 0, s>>>(a, ct, ctl, out, pol.max_batch, pol.K);
+  k_take<<<1, 1024, 0, s>>>(a, ct, ctl, out, pol.max_batch, pol.K, t);
   if (passes_out) *passes_out = passes;
   return cudaGetLastError();
 }

@@ -646,13 +646,22 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
 // write the records of the previous batch (the resident set) for preempt/region B.
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable ct, const Ctl* ctl,
-                                                         Outputs out, uint32_t n_rows, uint32_t ntiles) {
+                                                         Outputs out, uint32_t n_rows, uint32_t ntiles,
+                                                         uint32_t t) {
   pdl_wait();
   pdl_trigger();
   const uint32_t tile = blockIdx.x;
   if (tile >= ntiles) {
+    // previous batch: records (for preempt) and, for its live calls of q*, keys (region B;
+    // duplicates of region A are removed after the sort); other entries get the ~0 sentinel
     uint32_t j = (tile - ntiles) * SCAN_THREADS + threadIdx.x;
-    if (j < ctl->n_prev) load_rec(ct, out.prev_slots[j], out.prev_rec + j);
+    if (j < ctl->n_prev) {
+      CandRec r;
+      load_rec(ct, out.prev_slots[j], &r);
+      out.prev_rec[j] = r;
+      bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == ctl->qstar;
+      out.ckey[ctl->n_cand_a + j] = b ? cand_key(r, t) : ~0ull;
+    }
     return;
   }
   const uint32_t off = out.tile_off[tile];
@@ -683,8 +692,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     if (flags & (1u << j)) {
+      CandRec r;
+      load_rec(ct, row0 + j, &r);
       out.cand[pos] = row0 + j;
-      load_rec(ct, row0 + j, out.cand_rec + pos);
+      out.cand_rec[pos] = r;
+      out.ckey[pos] = cand_key(r, t);
       ++pos;
     }
 }
@@ -702,12 +714,36 @@ extern __shared__ unsigned char fin_smem[];
 
 __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
-constexpr uint32_t REC_PREV = 0x80000000u;  // index flag: record lives in prev_rec
-
-__device__ __forceinline__ uint64_t cand_key(const CandRec& r, uint32_t t) {
-  uint64_t arel = (uint64_t)((1u << 27) - 1 - (t - r.arr)) & ((1u << 27) - 1);  // later arrival: larger
-  return ((uint64_t)(r.qf & QF_QMASK) << 59) | (arel << 32) | ((uint64_t)((r.qf & QF_RUN) ? 0u : 1u) << 31) |
-         (r.slot & 0x7FFFFFFFu);
+// k_rank: the candidates' sort.  A single SM needs ~35k cycles to sort 2048 64-bit keys with
+// any block sort (measured: scripts/micro/sort_bench.cu), so the order is computed across many
+// SMs instead: every CTA holds all n <= 2 BS keys in shared memory and each key's output index is
+// the number of keys before it ((key, element) is unique), 8 threads per key.
+constexpr int RANK_THREADS = 256, RANK_SUB = 8, RANK_PER_CTA = RANK_THREADS / RANK_SUB;
+__global__ void __launch_bounds__(RANK_THREADS) k_rank(const Ctl* ctl, Outputs out) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ uint64_t rk[];
+  const uint32_t n = ctl->n_cand_a + ctl->n_prev;
+  const uint32_t e0 = blockIdx.x * RANK_PER_CTA;
+  if (e0 >= n) return;
+  for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS) rk[i] = out.ckey[i];
+  __syncthreads();
+  const uint32_t e = e0 + threadIdx.x / RANK_SUB, sub = threadIdx.x % RANK_SUB;
+  uint32_t cnt = 0;
+  uint64_t x = 0;
+  if (e < n) {
+    x = rk[e];
+    for (uint32_t j = sub; j < n; j += RANK_SUB) {
+      uint64_t y = rk[j];
+      cnt += (y < x || (y == x && j < e)) ? 1u : 0u;
+    }
+  }
+#pragma unroll
+  for (int d = 1; d < RANK_SUB; d <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+  if (sub == 0 && e < n) {
+    out.skey[cnt] = x;
+    out.sidx[cnt] = e;
+  }
 }
 
 __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable ct, Ctl* ctl,
@@ -715,70 +751,48 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
                                                           uint32_t t, uint32_t np, uint32_t seqno) {
   pdl_wait();
   pdl_trigger();
-  uint64_t* khi = reinterpret_cast<uint64_t*>(fin_smem);   // [np] keys
-  uint64_t* uk = khi + np;                                   // [np] unique sorted keys
-  uint32_t* klo = reinterpret_cast<uint32_t*>(uk + np);      // [np] record index
-  uint32_t* ui = klo + np;                                   // [np] record index (unique)
+  uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] unique sorted keys
+  uint32_t* ui = reinterpret_cast<uint32_t*>(uk + np);      // [np] element index
   __shared__ unsigned long long red64[33];
   __shared__ uint32_t red[33];
-  __shared__ uint32_t s_nb, s_nbatch;
+  __shared__ uint32_t s_nbatch;
   const uint32_t tid = threadIdx.x;
   const uint32_t BS = pol.max_batch;
-  const uint32_t nA = ctl->n_cand_a, qs = ctl->qstar, n_prev = ctl->n_prev;
+  const uint32_t nA = ctl->n_cand_a, n_prev = ctl->n_prev;
+  const uint32_t n_all = nA + n_prev;
   STAMP(0);
-  if (tid == 0) { s_nb = 0; s_nbatch = 0; }
-  for (uint32_t i = tid; i < np; i += FIN_THREADS) { khi[i] = ~0ull; klo[i] = ~0u; }
-  __syncthreads();
-  // ---- (1) keys: region A + the previous batch's calls of q* (may duplicate A) ---------------
-  for (uint32_t i = tid; i < nA; i += FIN_THREADS) {
-    khi[i] = cand_key(out.cand_rec[i], t);
-    klo[i] = i;
-  }
-  for (uint32_t j = tid; j < n_prev; j += FIN_THREADS) {
-    CandRec r = out.prev_rec[j];
-    if (!(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == qs) {
-      uint32_t p = nA + atomicAdd(&s_nb, 1u);
-      khi[p] = cand_key(r, t);
-      klo[p] = REC_PREV | j;
-    }
-  }
-  __syncthreads();
-  STAMP(1);
-  const uint32_t n_all = nA + s_nb;
-  uint32_t np2 = 2;
-  while (np2 < n_all) np2 <<= 1;
-  if (np == 2 * FIN_THREADS) {
-    // register/shuffle network, 2 keys per thread (BS <= 1024)
-    uint64_t k0 = khi[2 * tid], k1 = khi[2 * tid + 1];
-    uint32_t v0 = klo[2 * tid], v1 = klo[2 * tid + 1];
-    __syncthreads();
-    bitonic_sort_reg2<FIN_THREADS>(k0, v0, k1, v1, khi, klo);
-    khi[2 * tid] = k0; klo[2 * tid] = v0;
-    khi[2 * tid + 1] = k1; klo[2 * tid + 1] = v1;
-    __syncthreads();
-  } else {
-    bitonic_sort_pairs<FIN_THREADS>(khi, klo, min(np2, np));
-  }
-  STAMP(2);
-  // ---- (2) de-duplicate (a running call of q* can be both in A and in the previous batch) ----
-  constexpr int D = 8;  // keys per thread, blocked; np <= 8192
+  if (tid == 0) s_nbatch = 0;
+  // ---- (1) the sorted keys from k_rank, de-duplicated (a running call of q* can be both in
+  // region A and in the previous batch) and without the ~0 sentinels -----------------------
+  constexpr int D = 8;  // keys per thread, blocked; 2 BS <= 8192
+  uint64_t kk[D];
   uint32_t keep = 0, nkeep = 0;
 #pragma unroll
   for (int r = 0; r < D; ++r) {
     uint32_t i = tid * D + r;
-    if (i < n_all && (i == 0 || khi[i] != khi[i - 1])) { keep |= 1u << r; ++nkeep; }
+    kk[r] = i < n_all ? out.skey[i] : ~0ull;
+  }
+  {
+    uint64_t before = (tid > 0 && tid * D - 1 < n_all) ? out.skey[tid * D - 1] : ~0ull;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      uint64_t prev = r ? kk[r - 1] : (tid ? before : ~0ull);
+      if (kk[r] != ~0ull && (tid * D + r == 0 || kk[r] != prev)) { keep |= 1u << r; ++nkeep; }
+    }
   }
   uint32_t ntot;
   uint32_t kpos = block_excl_scan<uint32_t, FIN_THREADS>(nkeep, red, &ntot);
 #pragma unroll
   for (int r = 0; r < D; ++r)
     if (keep & (1u << r)) {
-      uk[kpos] = khi[tid * D + r];
-      ui[kpos] = klo[tid * D + r];
+      uk[kpos] = kk[r];
+      ui[kpos] = out.sidx[tid * D + r];
       ++kpos;
     }
   __syncthreads();
   const uint32_t ncand = ntot;
+  STAMP(1);
+  STAMP(2);
   // ---- (3) the first m = min(BS, ncand) keys: fields from the records; prefix cutoff ---------
   const uint32_t m = min(BS, ncand);
   constexpr int R = 4;  // items per thread, blocked (i = tid * R + r); BS <= 4096
@@ -791,7 +805,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     c_kvb[r] = 0;
     if (i < m) {
       uint32_t x = ui[i];
-      const CandRec& rc = (x & REC_PREV) ? out.prev_rec[x & ~REC_PREV] : out.cand_rec[x];
+      const CandRec& rc = x < nA ? out.cand_rec[x] : out.prev_rec[x - nA];
       c_s[r] = rc.slot;
       c_qf[r] = rc.qf;
       c_tok[r] = rc.tok;
@@ -1153,11 +1167,13 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     if (ev) cudaEventRecord(ev[1], s);
     launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
     launch_pdl(k_gather, ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS, SCAN_THREADS, 0, s, pol,
-               ct, ctl, out, n_rows, ntiles);
+               ct, ctl, out, n_rows, ntiles, t);
   }
+  launch_pdl(k_rank, (2 * pol.max_batch + RANK_PER_CTA - 1) / RANK_PER_CTA, RANK_THREADS,
+             (size_t)2 * pol.max_batch * sizeof(uint64_t), s, (const Ctl*)ctl, out);
   if (ev) cudaEventRecord(ev[2], s);
   uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2 * FIN_THREADS);
-  size_t smem = (size_t)np * 2 * (sizeof(uint64_t) + sizeof(uint32_t));
+  size_t smem = (size_t)np * (sizeof(uint64_t) + sizeof(uint32_t));
   static bool attr_set = false;
   if (!attr_set) {
     // 2 x np x (8 B key + 4 B index) <= 192 KiB at BS = 4096; the rest of the 227 KiB is static

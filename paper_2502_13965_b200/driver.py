@@ -6,6 +6,8 @@ non-clairvoyance).  It holds none of the scheduling arithmetic.
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 
 from .autx import CALL_DESC
@@ -35,6 +37,7 @@ class TraceDriver:
         self.t = 0
         self.log = []
         self.total_wait = 0
+        self.api_s = 0.0        # wall time spent inside the C ABI calls (the user-visible API)
 
     def idx_of(self, cids):
         cids = np.asarray(cids, np.uint64)
@@ -80,15 +83,18 @@ class TraceDriver:
         t = self.t
         s = self.s
         nc = len(self.pending)
-        if nc:
-            s.complete(self.tr.call_id[self.pending])
+        ids = self.tr.call_id[self.pending]
         ended = self._release(t, self.pending)
+        arr = self.arrivals(t)
+        t0 = time.perf_counter()
+        if nc:
+            s.complete(ids)
         for pid in ended:
             s.end_program(pid)
-        arr = self.arrivals(t)
         if len(arr):
             s.register(arr)
         s.sched_step(t, wait=False)
+        self.api_s += time.perf_counter() - t0
         return nc, len(arr)
 
     def finish(self):
@@ -96,8 +102,10 @@ class TraceDriver:
         call; calls whose hidden decode length is reached complete)."""
         t = self.t
         s = self.s
+        t0 = time.perf_counter()
         out = s.step_wait()
         batch, admit, preempt = s.lists()
+        self.api_s += time.perf_counter() - t0
         rec = dict(t=t, n_batch=int(out.n_batch), swap_out_blocks=int(out.swap_out_blocks),
                    swap_in_blocks=int(out.swap_in_blocks), kv_blocks=int(out.kv_blocks),
                    n_active=int(out.n_active), n_promoted=int(out.n_promoted),

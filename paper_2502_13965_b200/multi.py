@@ -13,6 +13,8 @@ all-gathers; it is harness state, not scheduler state.
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 
 from .driver import TraceDriver
@@ -31,21 +33,26 @@ class MultiEngineDriver(TraceDriver):
         t = self.t
         s = self.s
         local = self.pending
+        t0 = time.perf_counter()
         if len(local):
             s.complete(self.tr.call_id[local])
         s.route_pack(self.rec.data_ptr())
         gathered = self.exchange(self.rec)
+        self.api_s += time.perf_counter() - t0
         all_done = np.sort(np.concatenate([np.asarray(x, np.int64) for x in self.gather_ids(local)]))
         ended = self._release(t, all_done)
+        arr = self.arrivals(t)
+        t0 = time.perf_counter()
         for pid in ended:
             s.end_program(pid)
-        arr = self.arrivals(t)
         dest = s.route_apply(gathered.data_ptr(), arr)
-        self.routes.append((t, [int(x) for x in arr["call_id"]], [int(x) for x in dest]))
         mine = arr[dest == self.rank]
         if len(mine):
             s.register(mine)
         s.sched_step(t, wait=False)
+        self.api_s += time.perf_counter() - t0
+        if self.log_lists:
+            self.routes.append((t, [int(x) for x in arr["call_id"]], [int(x) for x in dest]))
         return len(local), len(mine)
 
     def run(self, max_steps=10 ** 9):
