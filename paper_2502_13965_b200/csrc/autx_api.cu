@@ -130,9 +130,8 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(cudaMemsetAsync(t.mtime, 0, rows * 4, ctx->stream));
   ProgTable& p = ctx->pt;
   size_t P = std::max<uint32_t>(c.max_programs, 1);
-  CK(dalloc(&p.svc, P)); CK(dalloc(&p.pwait, P)); CK(dalloc(&p.last_arr, P)); CK(dalloc(&p.last_comp, P));
-  CK(cudaMemsetAsync(p.svc, 0, P * 4, ctx->stream));
-  CK(cudaMemsetAsync(p.pwait, 0, P * 8, ctx->stream));
+  CK(dalloc(&p.info, P)); CK(dalloc(&p.last_arr, P)); CK(dalloc(&p.last_comp, P));
+  CK(cudaMemsetAsync(p.info, 0, P * sizeof(PInfo), ctx->stream));
   CK(dalloc(&ctx->ctl, 1));
   CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
   Outputs& o = ctx->out;
@@ -284,7 +283,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   CallTable& t = ctx->ct;
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
-                 t.loc, t.hcls, ctx->pt.svc, ctx->pt.pwait, ctx->pt.last_arr, ctx->pt.last_comp,
+                 t.loc, t.hcls, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp,
                  ctx->ctl, ctx->out.batch_slots, ctx->out.batch_ids, ctx->out.admit_ids,
                  ctx->out.preempt_ids, ctx->out.prev_slots, ctx->out.preempt_slots,
                  ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.tile_cnt, ctx->out.tile_off,
@@ -339,8 +338,7 @@ static autx_status new_program(autx_ctx* ctx, uint64_t pid, uint32_t* row_out) {
   ctx->prog_row[pid] = row;
   ctx->prog_active[row] = 0;
   // zero the entry (stream-ordered before any later kernel reads it)
-  CK(cudaMemsetAsync(ctx->pt.svc + row, 0, 4, ctx->stream));
-  CK(cudaMemsetAsync(ctx->pt.pwait + row, 0, 8, ctx->stream));
+  CK(cudaMemsetAsync(ctx->pt.info + row, 0, sizeof(PInfo), ctx->stream));
   CK(cudaMemsetAsync(ctx->d_pin + row, 0xff, 1, ctx->stream));
   if (row_out) *row_out = row;
   return AUTX_OK;
@@ -847,12 +845,10 @@ extern "C" autx_status autx_program_state(autx_ctx* ctx, uint64_t pid, uint32_t*
   auto it = ctx->prog_row.find(pid);
   if (it == ctx->prog_row.end()) return fail(ctx, AUTX_E_NOENT, "unknown program");
   CK(cudaStreamSynchronize(ctx->stream));
-  uint32_t s = 0;
-  unsigned long long w = 0;
-  CK(cudaMemcpy(&s, ctx->pt.svc + it->second, 4, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(&w, ctx->pt.pwait + it->second, 8, cudaMemcpyDeviceToHost));
-  if (svc) *svc = s;
-  if (pwait) *pwait = w;
+  PInfo pi;
+  CK(cudaMemcpy(&pi, ctx->pt.info + it->second, sizeof pi, cudaMemcpyDeviceToHost));
+  if (svc) *svc = pi.svc;
+  if (pwait) *pwait = pi.pwait;
   return AUTX_OK;
 }
 

@@ -37,10 +37,17 @@ struct CallTable {
   uint32_t* hcls;    // host allocation size class (if swapped)
 };
 
+// Process-table fields the dense pass gathers for every call, packed so that one 16-byte load
+// fetches both.
+struct __align__(16) PInfo {
+  uint32_t svc;               // PLAS: sum of completed t_k; ATLAS: longest critical path (Alg. 1 l.4)
+  uint32_t _pad;
+  unsigned long long pwait;   // total waiting time of completed calls (W_p)
+};
+
 // Process table, one row per program.
 struct ProgTable {
-  uint32_t* svc;        // PLAS: sum of completed t_k; ATLAS: longest critical path (Alg. 1 l.4)
-  unsigned long long* pwait;  // total waiting time of completed calls (W_p)
+  PInfo* info;          // service + waiting time
   uint32_t* last_arr;   // most recent call arrival
   uint32_t* last_comp;  // most recent call completion
 };

@@ -277,6 +277,7 @@ __device__ void block_merge_sort(uint64_t* k, uint32_t* p, uint64_t* k2, uint32_
 
 // 128-bit compare: a*b >= c*d for u64 a, c and u32 b, d.
 __device__ __forceinline__ bool mul_ge(uint64_t a, uint32_t b, uint64_t c, uint32_t d) {
+  if (((a | c) >> 32) == 0) return a * (uint64_t)b >= c * (uint64_t)d;  // both products < 2^64
   uint64_t l1 = a * (uint64_t)b, h1 = __umul64hi(a, (uint64_t)b);
   uint64_t l2 = c * (uint64_t)d, h2 = __umul64hi(c, (uint64_t)d);
   return h1 > h2 || (h1 == h2 && l1 >= l2);

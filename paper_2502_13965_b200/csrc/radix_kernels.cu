@@ -42,8 +42,9 @@ __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, P
         uint32_t q = qf & QF_QMASK;
         if (pol.beta_den != 0) {
           uint32_t p = ct.prog[r], b = ct.base[r], m = ct.mtime[r];
-          uint64_t W = pt.pwait[p] + (uint64_t)(t - b - m);
-          uint64_t T = (uint64_t)pt.svc[p] + m;
+          const PInfo pi = pt.info[p];
+          uint64_t W = pi.pwait + (uint64_t)(t - b - m);
+          uint64_t T = (uint64_t)pi.svc + m;
           if (!(W == 0 && T == 0) && mul_ge(W, pol.beta_den, T, pol.beta_num)) {  // Alg. 1 l.26
             q = 0;
             ct.qf[r] = (uint8_t)(qf & ~QF_QMASK);

@@ -67,13 +67,13 @@ __device__ void apply_record_chunk(const Policy& pol, ProgTable pt, const CompRe
   uint64_t sum_tw = block_seg_scan<uint64_t, NT>(tw, head, OpSum(), red_v, red_f);
   uint64_t max_cp = block_seg_scan<uint64_t, NT>(cp, head, OpMax(), red_v, red_f);
   if (v2 && tail) {
-    if (pol.policy == AUTX_ATLAS) {
-      uint32_t cur = pt.svc[pp];
-      pt.svc[pp] = max_cp > cur ? (uint32_t)max_cp : cur;  // Alg. 1 l.4
-    } else {
-      pt.svc[pp] += (uint32_t)sum_ex;                       // Eq. 1
-    }
-    pt.pwait[pp] += sum_tw;                                 // Alg. 1 l.5-6, R5
+    PInfo pi = pt.info[pp];
+    if (pol.policy == AUTX_ATLAS)
+      pi.svc = max_cp > pi.svc ? (uint32_t)max_cp : pi.svc;  // Alg. 1 l.4
+    else
+      pi.svc += (uint32_t)sum_ex;                            // Eq. 1
+    pi.pwait += sum_tw;                                      // Alg. 1 l.5-6, R5
+    pt.info[pp] = pi;
     pt.last_comp[pp] = t;
   }
   __syncthreads();
@@ -199,11 +199,10 @@ __global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const Arrival
   ArrivalRec r = recs[i];
   uint32_t p = r.prog;
   if (r.flags & 2u) {  // first record of a program new in this batch: create its entry
-    pt.svc[p] = 0;
-    pt.pwait[p] = 0;
+    pt.info[p] = PInfo{0, 0, 0ull};
     pt.last_comp[p] = NONE;
   }
-  uint32_t inh = (r.flags & 1u) ? 0u : pt.svc[p];  // Alg. 1 l.11
+  uint32_t inh = (r.flags & 1u) ? 0u : pt.info[p].svc;  // Alg. 1 l.11
   pt.last_arr[p] = t;
   uint32_t q = place_queue(pol, inh);             // Alg. 1 l.12
   uint32_t s = first_slot + i;
@@ -269,8 +268,9 @@ __global__ void __launch_bounds__(SCAN_THREADS, 3) k_scan(Policy pol, CallTable 
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         bool live = !(qfs[j] & QF_DEAD);
-        sv[j] = live ? pt.svc[prog[j]] : 0u;
-        pw[j] = live ? pt.pwait[prog[j]] : 0ull;
+        PInfo pi = live ? pt.info[prog[j]] : PInfo{0, 0, 0ull};
+        sv[j] = pi.svc;
+        pw[j] = pi.pwait;
       }
     }
     bool wq = false, wb = false, wm = false;
@@ -374,12 +374,15 @@ __device__ __forceinline__ void issue_tile(const CallTable& ct, uint32_t tile, u
 
 extern __shared__ __align__(128) unsigned char scan_smem[];
 
-__global__ void __launch_bounds__(SCAN_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt,
+constexpr int BULK_THREADS = 512;                 // 16 warps per CTA, 4 rows per thread
+constexpr int BULK_ROWS = TILE / BULK_THREADS;
+
+__global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt,
                                                                Outputs out, uint32_t t, uint32_t ntiles) {
   pdl_wait();
   __shared__ __align__(8) uint64_t bars[SCAN_STAGES];
-  __shared__ uint64_t wc[SCAN_THREADS / 32][4];
-  __shared__ uint32_t wn[SCAN_THREADS / 32][2];
+  __shared__ uint64_t wc[BULK_THREADS / 32][4];
+  __shared__ uint32_t wn[BULK_THREADS / 32][2];
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
     for (int i = 0; i < SCAN_STAGES; ++i) mbar_init(&bars[i], 1);
@@ -392,52 +395,44 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) k_scan_bulk(Policy pol, CallT
       if (tl < ntiles) issue_tile(ct, tl, scan_smem + i * STAGE_BYTES, &bars[i]);
     }
   pdl_trigger();
+  const bool anti = pol.beta_den != 0;
   uint32_t it = 0;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const uint32_t stage = it % SCAN_STAGES;
     unsigned char* st = scan_smem + stage * STAGE_BYTES;
     mbar_wait(&bars[stage], (it / SCAN_STAGES) & 1);
-    const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
-    const uint32_t lr = tid * ROWS_PER_THREAD;
-    const uint2 qv = *reinterpret_cast<const uint2*>(st + lr);
-    const uint4 p0 = *reinterpret_cast<const uint4*>(st + STAGE_QF + lr * 4);
-    const uint4 p1 = *reinterpret_cast<const uint4*>(st + STAGE_QF + lr * 4 + 16);
-    const uint4 b0 = *reinterpret_cast<const uint4*>(st + STAGE_QF + STAGE_U32 + lr * 4);
-    const uint4 b1 = *reinterpret_cast<const uint4*>(st + STAGE_QF + STAGE_U32 + lr * 4 + 16);
-    const uint4 m0 = *reinterpret_cast<const uint4*>(st + STAGE_QF + 2 * STAGE_U32 + lr * 4);
-    const uint4 m1 = *reinterpret_cast<const uint4*>(st + STAGE_QF + 2 * STAGE_U32 + lr * 4 + 16);
+    const uint32_t lr = tid * BULK_ROWS;
+    const uint32_t row0 = tile * TILE + lr;
+    const uint32_t qv = *reinterpret_cast<const uint32_t*>(st + lr);
+    const uint4 pg = *reinterpret_cast<const uint4*>(st + STAGE_QF + lr * 4);
+    const uint4 bs = *reinterpret_cast<const uint4*>(st + STAGE_QF + STAGE_U32 + lr * 4);
+    const uint4 mt = *reinterpret_cast<const uint4*>(st + STAGE_QF + 2 * STAGE_U32 + lr * 4);
     __syncthreads();  // every thread has its rows in registers: the stage can be refilled
     if (tid == 0) {
       uint32_t nxt = tile + SCAN_STAGES * gridDim.x;
       if (nxt < ntiles) issue_tile(ct, nxt, st, &bars[stage]);
     }
-    uint32_t qfs[8], prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-    uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-    uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+    uint32_t qfs[4], prog[4] = {pg.x, pg.y, pg.z, pg.w}, base[4] = {bs.x, bs.y, bs.z, bs.w},
+             mtim[4] = {mt.x, mt.y, mt.z, mt.w};
 #pragma unroll
-    for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
+    for (int j = 0; j < 4; ++j) qfs[j] = (qv >> (8 * j)) & 0xffu;
+    PInfo pi[4];
+    if (anti) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) pi[j] = !(qfs[j] & QF_DEAD) ? pt.info[prog[j]] : PInfo{0, 0, 0ull};
+    }
     uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
     uint32_t npromo = 0, nlive = 0;
-    uint32_t sv[8];
-    unsigned long long pw[8];
-    if (pol.beta_den != 0) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        bool live = !(qfs[j] & QF_DEAD);
-        sv[j] = live ? pt.svc[prog[j]] : 0u;
-        pw[j] = live ? pt.pwait[prog[j]] : 0ull;
-      }
-    }
     bool wq = false, wb = false, wm = false;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 4; ++j) {
       uint32_t qf = qfs[j];
       if (qf & QF_DEAD) continue;
       ++nlive;
       uint32_t q = qf & QF_QMASK;
-      if (pol.beta_den != 0) {
-        uint64_t W = pw[j] + (uint64_t)(t - base[j] - mtim[j]);
-        uint64_t T = (uint64_t)sv[j] + mtim[j];
+      if (anti) {
+        uint64_t W = pi[j].pwait + (uint64_t)(t - base[j] - mtim[j]);
+        uint64_t T = (uint64_t)pi[j].svc + mtim[j];
         if (!(W == 0 && T == 0) && mul_ge(W, pol.beta_den, T, pol.beta_num)) {  // Alg. 1 l.26
           if (q != 0 || mtim[j] != 0) ct.quanta[row0 + j] = pol.quanta[0];
           if (q != 0) { qfs[j] = qf & ~QF_QMASK; wq = true; }
@@ -450,20 +445,9 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) k_scan_bulk(Policy pol, CallT
       }
       count_q(c0, c1, c2, c3, q);
     }
-    if (wq) {
-      uint2 qn;
-      qn.x = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
-      qn.y = qfs[4] | (qfs[5] << 8) | (qfs[6] << 16) | (qfs[7] << 24);
-      *reinterpret_cast<uint2*>(ct.qf + row0) = qn;
-    }
-    if (wb) {
-      *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
-      *reinterpret_cast<uint4*>(ct.base + row0 + 4) = make_uint4(base[4], base[5], base[6], base[7]);
-    }
-    if (wm) {
-      *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
-      *reinterpret_cast<uint4*>(ct.mtime + row0 + 4) = make_uint4(mtim[4], mtim[5], mtim[6], mtim[7]);
-    }
+    if (wq) *reinterpret_cast<uint32_t*>(ct.qf + row0) = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
+    if (wb) *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
+    if (wm) *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
     c0 = warp_sum(c0); c1 = warp_sum(c1); c2 = warp_sum(c2); c3 = warp_sum(c3);
     npromo = warp_sum(npromo); nlive = warp_sum(nlive);
     if (lane_id() == 0) {
@@ -474,12 +458,12 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) k_scan_bulk(Policy pol, CallT
     if (tid < MAX_K) {
       uint32_t k = tid, sum = 0;
 #pragma unroll
-      for (int w = 0; w < SCAN_THREADS / 32; ++w) sum += (uint32_t)(wc[w][k >> 2] >> ((k & 3) * 16)) & 0xffffu;
+      for (int w = 0; w < BULK_THREADS / 32; ++w) sum += (uint32_t)(wc[w][k >> 2] >> ((k & 3) * 16)) & 0xffffu;
       out.tile_cnt[(size_t)tile * MAX_K + k] = sum;
     } else if (tid == 32) {
       uint32_t a = 0, b = 0;
 #pragma unroll
-      for (int w = 0; w < SCAN_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
+      for (int w = 0; w < BULK_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
       out.tile_stat[tile] = make_uint2(a, b);
     }
     __syncthreads();  // wc/wn reuse
@@ -718,7 +702,7 @@ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 
 // any block sort (measured: scripts/micro/sort_bench.cu), so the order is computed across many
 // SMs instead: every CTA holds all n <= 2 BS keys in shared memory and each key's output index is
 // the number of keys before it ((key, element) is unique), 8 threads per key.
-constexpr int RANK_THREADS = 256, RANK_SUB = 8, RANK_PER_CTA = RANK_THREADS / RANK_SUB;
+constexpr int RANK_THREADS = 256, RANK_SUB = 16, RANK_PER_CTA = RANK_THREADS / RANK_SUB;
 __global__ void __launch_bounds__(RANK_THREADS) k_rank(const Ctl* ctl, Outputs out) {
   pdl_wait();
   pdl_trigger();
@@ -1162,7 +1146,7 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     if (simple)
       launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, out, t, n_rows);
     else
-      launch_pdl(k_scan_bulk, std::min<uint32_t>(ntiles, scan_ctas), SCAN_THREADS,
+      launch_pdl(k_scan_bulk, std::min<uint32_t>(ntiles, scan_ctas), BULK_THREADS,
                  (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, out, t, ntiles);
     if (ev) cudaEventRecord(ev[1], s);
     launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
