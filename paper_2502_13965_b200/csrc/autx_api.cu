@@ -84,6 +84,9 @@ struct autx_ctx {
   uint32_t rarr_cap = 0;
   bool routed_this = false;
   uint32_t n_reg_this = 0;
+  // work staged for the next sched_step's prologue kernel (single-engine mode)
+  uint32_t n_comp_staged = 0, n_arr_staged = 0, arr_first_slot = 0;
+  std::unordered_set<uint64_t> staged_new_progs;
   bool timed_complete = false, timed_register = false;   // events 4-5 / 6-7 recorded this step
   bool tc_step = false, tr_step = false;                  // ... for the step being waited on
   std::string err;
@@ -392,14 +395,18 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
     ctx->last_batch.erase(ids[i]);
   }
   uint32_t t = next_step(ctx);
-  if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
-  CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
-  // the kernel reads the pinned staging directly (zero-copy, a few hundred bytes)
-  CK(launch_complete(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->h_cslots, n, t, ctx->kv,
-                     ctx->kv_on, recs, ctx->cfg.nranks <= 1));
-  if (ctx->timing) {
-    cudaEventRecord(ctx->ev[5], ctx->stream);
-    ctx->timed_complete = true;
+  if (ctx->cfg.nranks <= 1) {
+    ctx->n_comp_staged = n;  // applied by the next sched_step's prologue kernel
+  } else {
+    // multi-engine: the records are needed now by autx_route_pack
+    if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
+    CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
+    CK(launch_complete(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->h_cslots, n, t, ctx->kv,
+                       ctx->kv_on, recs, false));
+    if (ctx->timing) {
+      cudaEventRecord(ctx->ev[5], ctx->stream);
+      ctx->timed_complete = true;
+    }
   }
   ctx->completed_this = true;
   ctx->n_completed_pending = n;
@@ -407,6 +414,46 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
 }
 
 static autx_status compact(autx_ctx* ctx);
+
+// Launches the staged completions and arrivals of step t: one prologue kernel whose inputs ride
+// in the kernel parameters when small; bulk arrivals (an offline burst) go through one DMA and
+// the multi-CTA registration kernel.
+static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
+  if (ctx->n_comp_staged == 0 && ctx->n_arr_staged == 0) return AUTX_OK;
+  const bool bulk = ctx->n_arr_staged > 4096;
+  PrologueArgs a;
+  memset(&a, 0, offsetof(PrologueArgs, comp));
+  a.n_comp = ctx->n_comp_staged;
+  a.n_arr = bulk ? 0 : ctx->n_arr_staged;
+  a.first_slot = ctx->arr_first_slot;
+  a.t = t;
+  if (a.n_comp <= (uint32_t)PRO_INLINE) memcpy(a.comp, ctx->h_cslots, a.n_comp * sizeof(uint32_t));
+  else a.comp_ptr = ctx->h_cslots;
+  if (a.n_arr <= (uint32_t)PRO_INLINE) memcpy(a.arr, ctx->h_arr, a.n_arr * sizeof(ArrivalRec));
+  else a.arr_ptr = ctx->h_arr;
+  CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
+  if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
+  if (a.n_comp || a.n_arr)
+    CK(launch_prologue(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->kv, ctx->kv_on, recs, a));
+  if (ctx->timing) {
+    cudaEventRecord(ctx->ev[5], ctx->stream);
+    ctx->timed_complete = true;
+  }
+  if (bulk) {
+    if (ctx->timing) cudaEventRecord(ctx->ev[6], ctx->stream);
+    CK(cudaMemcpyAsync(ctx->d_arr, ctx->h_arr, (size_t)ctx->n_arr_staged * sizeof(ArrivalRec),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_register(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->d_arr, ctx->n_arr_staged,
+                       ctx->arr_first_slot, t));
+    if (ctx->timing) {
+      cudaEventRecord(ctx->ev[7], ctx->stream);
+      ctx->timed_register = true;
+    }
+  }
+  ctx->n_comp_staged = ctx->n_arr_staged = 0;
+  ctx->staged_new_progs.clear();
+  return AUTX_OK;
+}
 
 extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n) {
   if (!ctx || (n && !calls)) return AUTX_E_INVAL;
@@ -454,23 +501,27 @@ extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* c
   if ((uint64_t)ctx->call_slot.size() + n > ctx->cfg.max_calls)
     return fail(ctx, AUTX_E_NOMEM, "call table full (%u active)", (unsigned)ctx->call_slot.size());
   if ((uint64_t)ctx->tail + n > ctx->cfg.max_calls) {
+    s = flush_staged(ctx, t);  // staged rows must exist on the device before they move
+    if (s) return s;
     s = compact(ctx);
     if (s) return s;
   }
-  // staging buffer growth for bulk registration
-  if (n > ctx->arr_cap) {
+  // staging buffer growth, keeping records already staged for this step
+  const uint32_t need = ctx->n_arr_staged + n;
+  if (need > ctx->arr_cap) {
     CK(cudaStreamSynchronize(ctx->stream));
+    ArrivalRec* nh = nullptr;
+    CK(cudaHostAlloc((void**)&nh, (size_t)need * sizeof(ArrivalRec), cudaHostAllocMapped));
+    if (ctx->n_arr_staged) memcpy(nh, ctx->h_arr, (size_t)ctx->n_arr_staged * sizeof(ArrivalRec));
     cudaFreeHost(ctx->h_arr);
     cudaFree(ctx->d_arr);
-    ctx->arr_cap = n;
-    CK(cudaHostAlloc((void**)&ctx->h_arr, (size_t)n * sizeof(ArrivalRec), cudaHostAllocMapped));
-    CK(dalloc(&ctx->d_arr, n));
-  } else if (ctx->registered_this) {
-    // the previous registration of this step may still be reading the staging buffer
-    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->h_arr = nh;
+    ctx->arr_cap = need;
+    CK(dalloc(&ctx->d_arr, need));
   }
+  if (ctx->n_arr_staged == 0) ctx->arr_first_slot = ctx->tail;
+  ArrivalRec* stage = ctx->h_arr + ctx->n_arr_staged;
   // map program ids, build records
-  std::unordered_set<uint64_t> first_done;
   for (uint32_t i = 0; i < n; ++i) {
     const autx_call_desc& d = calls[i];
     uint32_t flags = 0;
@@ -482,18 +533,19 @@ extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* c
       ctx->prog_row[d.program_id] = row;
       ctx->prog_active[row] = 0;
       CK(cudaMemsetAsync(ctx->d_pin + row, 0xff, 1, ctx->stream));
-      flags = 3;  // new program, first record
-      first_done.insert(d.program_id);
+      flags = 3;  // new program, first record: the prologue zeroes its entry
+      ctx->staged_new_progs.insert(d.program_id);
     } else {
       row = it->second;
-      if (new_prog_seen.count(d.program_id)) flags = 1;  // new in this batch, not first
+      // created earlier in this (not yet launched) step: inherit 0 without reading the entry
+      if (ctx->staged_new_progs.count(d.program_id)) flags = 1;
     }
     ArrivalRec r{};
     r.cid = d.call_id;
     r.prog = row;
     r.tok = d.input_tokens;
     r.flags = flags;
-    ctx->h_arr[i] = r;
+    stage[i] = r;
     uint32_t slot = ctx->tail + i;
     ctx->call_slot[d.call_id] = slot;
     ctx->slot_prog[slot] = row;
@@ -505,18 +557,7 @@ extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* c
   ctx->last_key[0] = l.arrival_step; ctx->last_key[1] = l.program_arrival_step;
   ctx->last_key[2] = l.program_id; ctx->last_key[3] = l.call_id;
   ctx->have_last_key = true;
-  const ArrivalRec* recs = ctx->h_arr;  // zero-copy for per-step batches
-  if (n > 4096) {  // bulk registration (e.g. an offline burst): one DMA instead of PCIe reads
-    CK(cudaMemcpyAsync(ctx->d_arr, ctx->h_arr, (size_t)n * sizeof(ArrivalRec), cudaMemcpyHostToDevice,
-                       ctx->stream));
-    recs = ctx->d_arr;
-  }
-  if (ctx->timing) cudaEventRecord(ctx->ev[6], ctx->stream);
-  CK(launch_register(ctx->stream, ctx->pol, ctx->ct, ctx->pt, recs, n, ctx->tail, t));
-  if (ctx->timing) {
-    cudaEventRecord(ctx->ev[7], ctx->stream);
-    ctx->timed_register = true;
-  }
+  ctx->n_arr_staged += n;  // registered on the device by the next sched_step's prologue
   ctx->tail += n;
   ctx->n_reg_this += n;
   ctx->registered_this = true;
@@ -544,6 +585,8 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
     arr_base = ctx->low < ctx->tail ? ctx->slot_arr[ctx->low] : t;
     if (t - arr_base >= (1u << 27)) return fail(ctx, AUTX_E_NOMEM, "arrival span exceeds the 27-bit key field");
   }
+  s = flush_staged(ctx, t);
+  if (s) return s;
   ++ctx->seqno;
   CK(launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv, ctx->kv_on, t,
                  ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr, ctx->radix ? &ctx->rx : nullptr,

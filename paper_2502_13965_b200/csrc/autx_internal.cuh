@@ -239,10 +239,23 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// Inputs of the fused step prologue (completions + arrivals), passed by value as kernel
+// parameters when they fit (PRO_INLINE each), else through the pointers.
+constexpr int PRO_INLINE = 96;
+struct PrologueArgs {
+  uint32_t n_comp, n_arr, first_slot, t;
+  const uint32_t* comp_ptr;
+  const ArrivalRec* arr_ptr;
+  uint32_t comp[PRO_INLINE];
+  ArrivalRec arr[PRO_INLINE];
+};
+
 // ---- kernel launchers (sched_kernels.cu / swap_kernels.cu) ----------------------------------
 cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                             const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
                             CompRec* rec_out, bool apply);
+cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl, KvState kv,
+                            bool kv_on, CompRec* rec_out, const PrologueArgs& a);
 cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,
                          uint64_t stride, uint32_t G, uint32_t t);
 cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,

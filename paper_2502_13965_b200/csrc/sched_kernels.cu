@@ -56,7 +56,9 @@ __device__ void apply_record_chunk(const Policy& pol, ProgTable pt, const CompRe
   skey[tid] = valid ? ((uint64_t)srec[tid].prog << 32 | tid) : ~0ull;
   sdummy[tid] = 0;
   __syncthreads();
-  bitonic_sort_pairs<NT>(skey, sdummy, NT);
+  uint32_t np = 2;
+  while (np < n) np <<= 1;
+  bitonic_sort_pairs<NT>(skey, sdummy, min(np, (uint32_t)NT));
   uint64_t k = skey[tid];
   bool v2 = k != ~0ull;
   uint32_t o = (uint32_t)k, pp = (uint32_t)(k >> 32);
@@ -80,12 +82,8 @@ __device__ void apply_record_chunk(const Policy& pol, ProgTable pt, const CompRe
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_complete(Policy pol, CallTable ct, ProgTable pt,
-                                                          Ctl* ctl, const uint32_t* slots,
-                                                          uint32_t n, uint32_t t, KvState kv,
-                                                          bool kv_on, CompRec* rec_out, bool apply) {
-  pdl_wait();
-  pdl_trigger();
+__device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, Ctl* ctl, const uint32_t* slots,
+                              uint32_t n, uint32_t t, KvState& kv, bool kv_on, CompRec* rec_out, bool apply) {
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
   STAMP(16);
@@ -141,6 +139,15 @@ __global__ void __launch_bounds__(NT) k_complete(Policy pol, CallTable ct, ProgT
   STAMP(19);
 }
 
+template <int NT>
+__global__ void __launch_bounds__(NT) k_complete(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                                                 const uint32_t* slots, uint32_t n, uint32_t t, KvState kv,
+                                                 bool kv_on, CompRec* rec_out, bool apply) {
+  pdl_wait();
+  pdl_trigger();
+  complete_body<NT>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+}
+
 // Multi-engine: apply every engine's completion records (R22: sums and maxima commute, so the
 // replicated tables stay identical whatever the order).  recs of rank r start at
 // base + r * stride bytes, after a RouteHdr.
@@ -190,13 +197,8 @@ __global__ void k_route(const char* base, uint64_t stride, uint32_t G, const Rou
 // ---------------------------------------------------------------------------------------------
 // a2: arrivals (Alg. 1 l.9-14).  Rows are appended in canonical order; row index = seq.
 // ---------------------------------------------------------------------------------------------
-__global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const ArrivalRec* recs,
-                           uint32_t n, uint32_t first_slot, uint32_t t) {
-  pdl_wait();
-  pdl_trigger();
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  ArrivalRec r = recs[i];
+__device__ __forceinline__ void register_one(const Policy& pol, CallTable& ct, ProgTable& pt, const ArrivalRec& r,
+                                             uint32_t s, uint32_t t) {
   uint32_t p = r.prog;
   if (r.flags & 2u) {  // first record of a program new in this batch: create its entry
     pt.info[p] = PInfo{0, 0, 0ull};
@@ -205,7 +207,6 @@ __global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const Arrival
   uint32_t inh = (r.flags & 1u) ? 0u : pt.info[p].svc;  // Alg. 1 l.11
   pt.last_arr[p] = t;
   uint32_t q = place_queue(pol, inh);             // Alg. 1 l.12
-  uint32_t s = first_slot + i;
   ct.cid[s] = r.cid;
   ct.prog[s] = p;
   ct.arr[s] = t;
@@ -218,6 +219,44 @@ __global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const Arrival
   ct.tok[s] = r.tok;
   ct.loc[s] = NONE;
   ct.hcls[s] = 0;
+}
+
+__global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const ArrivalRec* recs,
+                           uint32_t n, uint32_t first_slot, uint32_t t) {
+  pdl_wait();
+  pdl_trigger();
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) register_one(pol, ct, pt, recs[i], first_slot + i, t);
+}
+
+// Fused prologue of one step: completions (a1) then arrivals (a2), one CTA; a typical step's
+// records travel inside the kernel parameters (no PCIe reads), larger batches through pointers.
+constexpr int PRO_THREADS = 256;
+__global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                                                          KvState kv, bool kv_on, CompRec* rec_out,
+                                                          const PrologueArgs a) {
+  __shared__ uint32_t s_comp[PRO_INLINE];
+  __shared__ ArrivalRec s_arr[PRO_INLINE];
+  const uint32_t tid = threadIdx.x;
+  const bool comp_inline = a.n_comp <= PRO_INLINE, arr_inline = a.n_arr <= PRO_INLINE;
+  if (comp_inline)
+    for (uint32_t i = tid; i < a.n_comp; i += PRO_THREADS) s_comp[i] = a.comp[i];
+  if (arr_inline)
+    for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) s_arr[i] = a.arr[i];
+  pdl_wait();
+  pdl_trigger();
+  __syncthreads();
+  if (a.n_comp)
+    complete_body<PRO_THREADS>(pol, ct, pt, ctl, comp_inline ? s_comp : a.comp_ptr, a.n_comp, a.t, kv, kv_on,
+                               rec_out, true);
+  __syncthreads();  // arrivals inherit the service updated by this step's completions (R10)
+  const ArrivalRec* arr = arr_inline ? s_arr : a.arr_ptr;
+  for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) register_one(pol, ct, pt, arr[i], a.first_slot + i, a.t);
+}
+
+cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl, KvState kv,
+                            bool kv_on, CompRec* rec_out, const PrologueArgs& a) {
+  return launch_pdl(k_prologue, 1, PRO_THREADS, 0, s, pol, ct, pt, ctl, kv, kv_on, rec_out, a);
 }
 
 // ---------------------------------------------------------------------------------------------
