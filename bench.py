@@ -121,7 +121,7 @@ def dist_init(n):
         return 0, 1, 0
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    local = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if os.environ.get("AUTX_DIST_BACKEND", "nccl") == "gloo":   # tests: several ranks on one GPU
         dist.init_process_group("gloo")

@@ -427,6 +427,7 @@ static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
   a.n_arr = bulk ? 0 : ctx->n_arr_staged;
   a.first_slot = ctx->arr_first_slot;
   a.t = t;
+  a.n_prog_rows = ctx->prog_next;
   if (a.n_comp <= (uint32_t)PRO_INLINE) memcpy(a.comp, ctx->h_cslots, a.n_comp * sizeof(uint32_t));
   else a.comp_ptr = ctx->h_cslots;
   if (a.n_arr <= (uint32_t)PRO_INLINE) memcpy(a.arr, ctx->h_arr, a.n_arr * sizeof(ArrivalRec));

@@ -89,7 +89,7 @@ struct Ctl {
   uint32_t free_top;       // GPU block free stack size
   uint32_t rs_free_top;    // resident-slot free stack size
   uint32_t host_bump;      // host arena bump pointer (pages)
-  uint32_t _pad;
+  uint32_t rank_done;      // last-CTA ticket of k_rank (fused finalize)
   uint32_t host_free_top[32];  // per size class free-stack size
   unsigned long long dbg[32];  // %globaltimer stamps of kernel phases (autx_phase_times)
 };
@@ -244,6 +244,7 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
 constexpr int PRO_INLINE = 96;
 struct PrologueArgs {
   uint32_t n_comp, n_arr, first_slot, t;
+  uint32_t n_prog_rows, _pad[3];  // process-table rows in use (prefetched into L2 for the scan)
   const uint32_t* comp_ptr;
   const ArrivalRec* arr_ptr;
   uint32_t comp[PRO_INLINE];

@@ -243,6 +243,13 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
     for (uint32_t i = tid; i < a.n_comp; i += PRO_THREADS) s_comp[i] = a.comp[i];
   if (arr_inline)
     for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) s_arr[i] = a.arr[i];
+  // the dense pass gathers the process table for every call: pull its lines into L2 now
+  {
+    const char* base = reinterpret_cast<const char*>(pt.info);
+    const uint32_t lines = (uint32_t)(((uint64_t)a.n_prog_rows * sizeof(PInfo) + 127) / 128);
+    for (uint32_t l = tid; l < lines; l += PRO_THREADS)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)l * 128));
+  }
   pdl_wait();
   pdl_trigger();
   __syncthreads();
@@ -416,7 +423,10 @@ extern __shared__ __align__(128) unsigned char scan_smem[];
 constexpr int BULK_THREADS = 512;                 // 16 warps per CTA, 4 rows per thread
 constexpr int BULK_ROWS = TILE / BULK_THREADS;
 
-__global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt,
+template <int NT>
+__device__ void select_body(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t ntiles);
+
+__global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                                Outputs out, uint32_t t, uint32_t ntiles) {
   pdl_wait();
   __shared__ __align__(8) uint64_t bars[SCAN_STAGES];
@@ -507,6 +517,16 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
     }
     __syncthreads();  // wc/wn reuse
   }
+  // the last CTA to finish picks the boundary queue and the tile offsets (k_select's work)
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(&ctl->tiles_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (tid == 0) ctl->tiles_done = 0;
+  select_body<BULK_THREADS>(pol, ctl, out, ntiles);
 }
 
 // One CTA: q* = smallest q with sum_{k<=q} total_k >= BS (K if none), m' = BS - sum_{k<q*}
@@ -517,17 +537,15 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
 // earlier tiles (tile_pre) and the candidate output offset
 //     off(tile) = sum_{k<q*} prefix_k(tile) + min(prefix_{q*}(tile), m').
 constexpr int SEL_THREADS = 1024;
-__global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Outputs out,
-                                                        uint32_t ntiles) {
-  pdl_wait();
-  pdl_trigger();
+template <int NT>
+__device__ void select_body(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t ntiles) {
   __shared__ uint32_t tot[MAX_K + 2];
   __shared__ unsigned long long red[33];
   __shared__ uint32_t s_qstar, s_m;
   const uint32_t tid = threadIdx.x;
   if (tid < MAX_K + 2) tot[tid] = 0;
   __syncthreads();
-  if (ntiles <= SEL_THREADS) {
+  if (ntiles <= NT) {
     // fast path: one tile per thread, its 16 counters stay in registers (one load round trip)
     uint32_t x[MAX_K];
     uint2 st = make_uint2(0, 0);
@@ -535,10 +553,10 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
       const uint4* c = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)tid * MAX_K);
 #pragma unroll
       for (int v = 0; v < MAX_K / 4; ++v) {
-        uint4 y = c[v];
+        uint4 y = __ldcg(c + v);
         x[4 * v] = y.x; x[4 * v + 1] = y.y; x[4 * v + 2] = y.z; x[4 * v + 3] = y.w;
       }
-      st = out.tile_stat[tid];
+      st = __ldcg(out.tile_stat + tid);
     } else {
 #pragma unroll
       for (int k = 0; k < MAX_K; ++k) x[k] = 0;
@@ -576,7 +594,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
       cq += (uint32_t)k == qs ? x[k] : 0u;
     }
     unsigned long long total;
-    uint64_t pre = block_excl_scan<unsigned long long, SEL_THREADS>(((uint64_t)a << 32) | cq, red, &total);
+    uint64_t pre = block_excl_scan<unsigned long long, NT>(((uint64_t)a << 32) | cq, red, &total);
     if (tid < ntiles) {
       uint32_t pre_a = (uint32_t)(pre >> 32), pre_q = (uint32_t)pre;
       out.tile_pre[tid] = pre_q;
@@ -589,7 +607,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
     }
     return;
   }
-  const uint32_t per = (ntiles + SEL_THREADS - 1) / SEL_THREADS;
+  const uint32_t per = (ntiles + NT - 1) / NT;
   const uint32_t t0 = min(ntiles, tid * per), t1 = min(ntiles, t0 + per);
   uint32_t acc[MAX_K];
 #pragma unroll
@@ -599,10 +617,10 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
     const uint4* c = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)tl * MAX_K);
 #pragma unroll
     for (int v = 0; v < MAX_K / 4; ++v) {
-      uint4 x = c[v];
+      uint4 x = __ldcg(c + v);
       acc[4 * v] += x.x; acc[4 * v + 1] += x.y; acc[4 * v + 2] += x.z; acc[4 * v + 3] += x.w;
     }
-    uint2 st = out.tile_stat[tl];
+    uint2 st = __ldcg(out.tile_stat + tl);
     ap += st.x;
     al += st.y;
   }
@@ -643,7 +661,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
     mine += ((uint64_t)a << 32) | cq;
   }
   unsigned long long total;
-  uint64_t pre = block_excl_scan<unsigned long long, SEL_THREADS>(mine, red, &total);
+  uint64_t pre = block_excl_scan<unsigned long long, NT>(mine, red, &total);
   uint32_t pre_a = (uint32_t)(pre >> 32), pre_q = (uint32_t)pre;
   for (uint32_t tl = t0; tl < t1; ++tl) {
     const uint32_t* c = out.tile_cnt + (size_t)tl * MAX_K;
@@ -661,6 +679,12 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
     out.tile_off[ntiles] = n;
     ctl->n_cand_a = n;
   }
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Outputs out, uint32_t ntiles) {
+  pdl_wait();
+  pdl_trigger();
+  select_body<SEL_THREADS>(pol, ctl, out, ntiles);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -734,6 +758,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
 // (Alg. 1 l.20-23), allocate KV blocks and build the swap plan.
 // ---------------------------------------------------------------------------------------------
 extern __shared__ unsigned char fin_smem[];
+template <int NT>
+__device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
+                              uint32_t t, uint32_t np, uint32_t seqno);
 
 __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
@@ -742,38 +769,50 @@ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 
 // SMs instead: every CTA holds all n <= 2 BS keys in shared memory and each key's output index is
 // the number of keys before it ((key, element) is unique), 8 threads per key.
 constexpr int RANK_THREADS = 256, RANK_SUB = 16, RANK_PER_CTA = RANK_THREADS / RANK_SUB;
-__global__ void __launch_bounds__(RANK_THREADS) k_rank(const Ctl* ctl, Outputs out) {
+template <bool FUSED>
+__global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
+                                                       bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ uint64_t rk[];
+  uint64_t* rk = reinterpret_cast<uint64_t*>(fin_smem);
   const uint32_t n = ctl->n_cand_a + ctl->n_prev;
   const uint32_t e0 = blockIdx.x * RANK_PER_CTA;
-  if (e0 >= n) return;
-  for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS) rk[i] = out.ckey[i];
-  __syncthreads();
-  const uint32_t e = e0 + threadIdx.x / RANK_SUB, sub = threadIdx.x % RANK_SUB;
-  uint32_t cnt = 0;
-  uint64_t x = 0;
-  if (e < n) {
-    x = rk[e];
-    for (uint32_t j = sub; j < n; j += RANK_SUB) {
-      uint64_t y = rk[j];
-      cnt += (y < x || (y == x && j < e)) ? 1u : 0u;
+  if (e0 < n) {
+    for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS) rk[i] = out.ckey[i];
+    __syncthreads();
+    const uint32_t e = e0 + threadIdx.x / RANK_SUB, sub = threadIdx.x % RANK_SUB;
+    uint32_t cnt = 0;
+    uint64_t x = 0;
+    if (e < n) {
+      x = rk[e];
+      for (uint32_t j = sub; j < n; j += RANK_SUB) {
+        uint64_t y = rk[j];
+        cnt += (y < x || (y == x && j < e)) ? 1u : 0u;
+      }
+    }
+#pragma unroll
+    for (int d = 1; d < RANK_SUB; d <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    if (sub == 0 && e < n) {
+      out.skey[cnt] = x;
+      out.sidx[cnt] = e;
     }
   }
-#pragma unroll
-  for (int d = 1; d < RANK_SUB; d <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-  if (sub == 0 && e < n) {
-    out.skey[cnt] = x;
-    out.sidx[cnt] = e;
-  }
+  if (!FUSED) return;
+  // the last CTA to finish runs finalize on the sorted keys (saves a dependent launch)
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&ctl->rank_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) ctl->rank_done = 0;
+  finalize_body<RANK_THREADS>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
 }
 
-__global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable ct, Ctl* ctl,
-                                                          Outputs out, KvState kv, bool kv_on,
-                                                          uint32_t t, uint32_t np, uint32_t seqno) {
-  pdl_wait();
-  pdl_trigger();
+template <int NT>
+__device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
+                              uint32_t t, uint32_t np, uint32_t seqno) {
   uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] unique sorted keys
   uint32_t* ui = reinterpret_cast<uint32_t*>(uk + np);      // [np] element index
   __shared__ unsigned long long red64[33];
@@ -793,10 +832,10 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
 #pragma unroll
   for (int r = 0; r < D; ++r) {
     uint32_t i = tid * D + r;
-    kk[r] = i < n_all ? out.skey[i] : ~0ull;
+    kk[r] = i < n_all ? __ldcg(out.skey + i) : ~0ull;
   }
   {
-    uint64_t before = (tid > 0 && tid * D - 1 < n_all) ? out.skey[tid * D - 1] : ~0ull;
+    uint64_t before = (tid > 0 && tid * D - 1 < n_all) ? __ldcg(out.skey + tid * D - 1) : ~0ull;
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       uint64_t prev = r ? kk[r - 1] : (tid ? before : ~0ull);
@@ -804,12 +843,12 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     }
   }
   uint32_t ntot;
-  uint32_t kpos = block_excl_scan<uint32_t, FIN_THREADS>(nkeep, red, &ntot);
+  uint32_t kpos = block_excl_scan<uint32_t, NT>(nkeep, red, &ntot);
 #pragma unroll
   for (int r = 0; r < D; ++r)
     if (keep & (1u << r)) {
       uk[kpos] = kk[r];
-      ui[kpos] = out.sidx[tid * D + r];
+      ui[kpos] = __ldcg(out.sidx + tid * D + r);
       ++kpos;
     }
   __syncthreads();
@@ -840,7 +879,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
       my_kv += c_kvb[r];
     }
   }
-  unsigned long long kv_pre = block_excl_scan<unsigned long long, FIN_THREADS>(my_kv, red64, nullptr);
+  unsigned long long kv_pre = block_excl_scan<unsigned long long, NT>(my_kv, red64, nullptr);
   // Alg. 1 l.34-37: take while count <= BS and sum kvb <= P; kvb >= 1 makes the prefix sums
   // strictly increasing, so the fitting items are exactly a prefix: n_batch = max fitting i + 1
   {
@@ -877,7 +916,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     }
   }
   unsigned long long ad_tot;
-  unsigned long long ad_pre = block_excl_scan<unsigned long long, FIN_THREADS>(my_ad, red64, &ad_tot);
+  unsigned long long ad_pre = block_excl_scan<unsigned long long, NT>(my_ad, red64, &ad_tot);
   {
     uint32_t pos = (uint32_t)(ad_pre >> 44);
 #pragma unroll
@@ -923,7 +962,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     }
   }
   unsigned long long pre_tot;
-  unsigned long long pre_pre = block_excl_scan<unsigned long long, FIN_THREADS>(my_pre, red64, &pre_tot);
+  unsigned long long pre_pre = block_excl_scan<unsigned long long, NT>(my_pre, red64, &pre_tot);
   {
     uint32_t pos = (uint32_t)(pre_pre >> 44);
 #pragma unroll
@@ -938,7 +977,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
   }
   const uint32_t n_preempt = (uint32_t)(pre_tot >> 44);
   const unsigned long long swap_out = pre_tot & ((1ull << 44) - 1);
-  const unsigned long long kv_sum = block_sum<unsigned long long, FIN_THREADS>(kv_mine, red64);
+  const unsigned long long kv_sum = block_sum<unsigned long long, NT>(kv_mine, red64);
   STAMP(5);
   STAMP(6);
 
@@ -948,7 +987,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     // (1) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots
     uint32_t base_blk = 0, base_free = 0;
     const uint32_t top0 = ctl->free_top, rtop0 = ctl->rs_free_top;
-    for (uint32_t c0 = 0; c0 < n_preempt; c0 += FIN_THREADS) {
+    for (uint32_t c0 = 0; c0 < n_preempt; c0 += NT) {
       uint32_t i = c0 + tid;
       uint32_t s = 0, rslot = 0, nb = 0;
       if (i < n_preempt) {
@@ -957,7 +996,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
         nb = kv.rs_nblk[rslot];
       }
       uint32_t tot;
-      uint32_t boff = base_blk + block_excl_scan<uint32_t, FIN_THREADS>(nb, red, &tot);
+      uint32_t boff = base_blk + block_excl_scan<uint32_t, NT>(nb, red, &tot);
       if (i < n_preempt) {
         uint32_t cls = ceil_log2(nb);
         // pop a page range of 2^cls pages from the class stack, else bump-allocate
@@ -982,7 +1021,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
         kv.rs_nblk[rslot] = 0;
       }
       uint32_t rt;
-      uint32_t roff = base_free + block_excl_scan<uint32_t, FIN_THREADS>(i < n_preempt ? 1u : 0u, red, &rt);
+      uint32_t roff = base_free + block_excl_scan<uint32_t, NT>(i < n_preempt ? 1u : 0u, red, &rt);
       if (i < n_preempt) kv.rs_free[rtop0 + roff] = rslot;
       base_blk += tot;
       base_free += rt;
@@ -991,7 +1030,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     uint32_t top = top0 + base_blk, rtop = rtop0 + base_free;
     // (2) batch calls: grow/allocate to kvb; admitted calls take a resident slot
     uint32_t pop_base = 0, rs_pop = 0, in_blk = 0, in_items = 0;
-    for (uint32_t c0 = 0; c0 < n_batch; c0 += FIN_THREADS) {
+    for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
       uint32_t i = c0 + tid;
       uint32_t s = 0, need = 0, have = 0, rslot = NONE, admit = 0, held = 0;
       if (i < n_batch) {
@@ -1009,10 +1048,10 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
       }
       uint32_t alloc = need > have ? need - have : 0;
       uint32_t tot, rt, ht, it;
-      uint32_t aoff = pop_base + block_excl_scan<uint32_t, FIN_THREADS>(alloc, red, &tot);
-      uint32_t roff = rs_pop + block_excl_scan<uint32_t, FIN_THREADS>(admit, red, &rt);
-      uint32_t hoff = in_blk + block_excl_scan<uint32_t, FIN_THREADS>(held, red, &ht);
-      uint32_t ioff = in_items + block_excl_scan<uint32_t, FIN_THREADS>(held ? 1u : 0u, red, &it);
+      uint32_t aoff = pop_base + block_excl_scan<uint32_t, NT>(alloc, red, &tot);
+      uint32_t roff = rs_pop + block_excl_scan<uint32_t, NT>(admit, red, &rt);
+      uint32_t hoff = in_blk + block_excl_scan<uint32_t, NT>(held, red, &ht);
+      uint32_t ioff = in_items + block_excl_scan<uint32_t, NT>(held ? 1u : 0u, red, &it);
       if (i < n_batch) {
         if (admit) {
           if (roff >= rtop) set_err(ctl, AUTX_E_NOMEM, 3);
@@ -1038,7 +1077,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     }
     __syncthreads();
     // (3) free the host ranges of swapped-in calls (after this step's swap-out allocations)
-    for (uint32_t c0 = 0; c0 < n_batch; c0 += FIN_THREADS) {
+    for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
       uint32_t i = c0 + tid;
       if (i < in_items) {
         PlanItem it = kv.plan_in[i];
@@ -1049,12 +1088,12 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     }
     // (4) block table CSR of the batch
     uint32_t b0 = 0;
-    for (uint32_t c0 = 0; c0 < n_batch; c0 += FIN_THREADS) {
+    for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
       uint32_t i = c0 + tid;
       uint32_t need = 0, rslot = 0;
       if (i < n_batch) { rslot = ct.loc[(uint32_t)(uk[i] & 0x7FFFFFFFu)]; need = kv.rs_nblk[rslot]; }
       uint32_t tot;
-      uint32_t o = b0 + block_excl_scan<uint32_t, FIN_THREADS>(need, red, &tot);
+      uint32_t o = b0 + block_excl_scan<uint32_t, NT>(need, red, &tot);
       if (i < n_batch) {
         kv.bt_offsets[i] = o;
         const uint32_t* src = kv.rs_blocks + (size_t)rslot * W;
@@ -1116,6 +1155,14 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(Policy pol, CallTable 
     ctl->n_live = 0;
   }
   STAMP(8);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
+                                                 bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
+  pdl_wait();
+  pdl_trigger();
+  finalize_body<NT>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1182,29 +1229,41 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       scan_ctas = 2 * sms;
       cudaFuncSetAttribute(k_scan_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
     }
-    if (simple)
+    if (simple) {
       launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, out, t, n_rows);
-    else
+      if (ev) cudaEventRecord(ev[1], s);
+      launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
+    } else {
       launch_pdl(k_scan_bulk, std::min<uint32_t>(ntiles, scan_ctas), BULK_THREADS,
-                 (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, out, t, ntiles);
-    if (ev) cudaEventRecord(ev[1], s);
-    launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
+                 (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, ctl, out, t, ntiles);
+      if (ev) cudaEventRecord(ev[1], s);
+    }
     launch_pdl(k_gather, ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS, SCAN_THREADS, 0, s, pol,
                ct, ctl, out, n_rows, ntiles, t);
   }
-  launch_pdl(k_rank, (2 * pol.max_batch + RANK_PER_CTA - 1) / RANK_PER_CTA, RANK_THREADS,
-             (size_t)2 * pol.max_batch * sizeof(uint64_t), s, (const Ctl*)ctl, out);
-  if (ev) cudaEventRecord(ev[2], s);
-  uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2 * FIN_THREADS);
-  size_t smem = (size_t)np * (sizeof(uint64_t) + sizeof(uint32_t));
+  uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
+  size_t fin_smem_bytes = (size_t)np * (sizeof(uint64_t) + sizeof(uint32_t));
+  size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch * sizeof(uint64_t), fin_smem_bytes);
   static bool attr_set = false;
   if (!attr_set) {
-    // 2 x np x (8 B key + 4 B index) <= 192 KiB at BS = 4096; the rest of the 227 KiB is static
-    cudaError_t e = cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_finalize<FIN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_rank<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_rank<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  launch_pdl(k_finalize, 1, FIN_THREADS, smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  const uint32_t rank_grid = (2 * pol.max_batch + RANK_PER_CTA - 1) / RANK_PER_CTA;
+  if (ev) cudaEventRecord(ev[2], s);
+  if (pol.max_batch <= 1024) {
+    // rank + finalize in one launch: the last rank CTA (256 threads = 4 candidates each) finalizes
+    launch_pdl(k_rank<true>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  } else {
+    launch_pdl(k_rank<false>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+    launch_pdl(k_finalize<FIN_THREADS>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np,
+               seqno);
+  }
   if (ev) cudaEventRecord(ev[3], s);
   return cudaGetLastError();
 }
