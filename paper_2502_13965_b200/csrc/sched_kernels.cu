@@ -736,16 +736,43 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
     if (sel) { flags |= 1u << j; ++nsel; }
   }
   uint32_t pos = off + block_excl_scan<uint32_t, SCAN_THREADS>(nsel, red, nullptr);
+  if (flags) {
+    // the thread's 8 consecutive rows: all fields with independent vector loads (one DRAM round
+    // trip), then one record + key per selected row
+    const uint4* cidv = reinterpret_cast<const uint4*>(ct.cid + row0);
+    uint4 c4[4];
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (flags & (1u << j)) {
-      CandRec r;
-      load_rec(ct, row0 + j, &r);
-      out.cand[pos] = row0 + j;
-      out.cand_rec[pos] = r;
-      out.ckey[pos] = cand_key(r, t);
-      ++pos;
+    for (int v = 0; v < 4; ++v) c4[v] = cidv[v];
+    uint4 ar[2], tk[2], ex[2], mt[2], qt[2];
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      ar[v] = reinterpret_cast<const uint4*>(ct.arr + row0)[v];
+      tk[v] = reinterpret_cast<const uint4*>(ct.tok + row0)[v];
+      ex[v] = reinterpret_cast<const uint4*>(ct.exec + row0)[v];
+      mt[v] = reinterpret_cast<const uint4*>(ct.mtime + row0)[v];
+      qt[v] = reinterpret_cast<const uint4*>(ct.quanta + row0)[v];
     }
+    auto lane4 = [](const uint4& a, int k) { return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : a.w; };
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (flags & (1u << j)) {
+        CandRec r;
+        const uint4& cc = c4[j >> 1];
+        r.cid = (j & 1) ? ((uint64_t)cc.w << 32 | cc.z) : ((uint64_t)cc.y << 32 | cc.x);
+        r.slot = row0 + j;
+        r.arr = lane4(ar[j >> 2], j & 3);
+        r.tok = lane4(tk[j >> 2], j & 3);
+        r.exec = lane4(ex[j >> 2], j & 3);
+        r.mtime = lane4(mt[j >> 2], j & 3);
+        r.quanta = lane4(qt[j >> 2], j & 3);
+        r.qf = qfs[j];
+        r._pad = 0;
+        out.cand[pos] = row0 + j;
+        out.cand_rec[pos] = r;
+        out.ckey[pos] = cand_key(r, t);
+        ++pos;
+      }
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -818,6 +845,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   __shared__ unsigned long long red64[33];
   __shared__ uint32_t red[33];
   __shared__ uint32_t s_nbatch;
+  __shared__ HostOut s_hout;
   const uint32_t tid = threadIdx.x;
   const uint32_t BS = pol.max_batch;
   const uint32_t nA = ctl->n_cand_a, n_prev = ctl->n_prev;
@@ -907,7 +935,6 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     if (i < n_batch) {
       out.batch_slots[i] = c_s[r];
       out.batch_ids[i] = c_cid[r];
-      out.h_batch[i] = c_cid[r];
       kv_mine += c_kvb[r];
       if (!(c_qf[r] & QF_RES)) {
         uint64_t held = c_ex[r] > 0 ? ceil_div_u32(c_tok[r] + c_ex[r], pol.block_tokens) : 0;  // R28
@@ -924,7 +951,6 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       uint32_t i = tid * R + r;
       if (i < n_batch && !(c_qf[r] & QF_RES)) {
         out.admit_ids[pos] = c_cid[r];
-        out.h_admit[pos] = c_cid[r];
         out.admit_slots[pos] = c_s[r];
         ++pos;
       }
@@ -969,7 +995,6 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     for (int r = 0; r < R; ++r)
       if (is_pre & (1u << r)) {
         out.preempt_ids[pos] = p_cid[r];
-        out.h_preempt[pos] = p_cid[r];
         out.preempt_slots[pos] = p_s[r];
         ct.qf[p_s[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
         ++pos;
@@ -1150,9 +1175,27 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     h.err = ctl->err;
     h.seqno = seqno;
     h.err_info = ctl->err_info;
-    *out.hout = h;
     ctl->n_promoted = 0;
     ctl->n_live = 0;
+    s_hout = h;
+  }
+  // host mirrors: coalesced 16-byte zero-copy stores (few PCIe write TLPs) after the device lists
+  __syncthreads();
+  {
+    const uint32_t nb = s_hout.n_batch, na = s_hout.n_admit, np_ = s_hout.n_preempt;
+    auto mirror = [&](uint64_t* dst, const uint64_t* src, uint32_t n) {
+      for (uint32_t i = tid; i < n / 2; i += NT)
+        reinterpret_cast<uint4*>(dst)[i] = __ldcg(reinterpret_cast<const uint4*>(src) + i);
+      if ((n & 1) && tid == 0) dst[n - 1] = __ldcg(src + n - 1);
+    };
+    mirror(out.h_batch, out.batch_ids, nb);
+    mirror(out.h_admit, out.admit_ids, na);
+    mirror(out.h_preempt, out.preempt_ids, np_);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence_system();
+      *out.hout = s_hout;  // counts last: valid once the lists are
+    }
   }
   STAMP(8);
 }
