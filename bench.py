@@ -53,6 +53,16 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per k_scan_bulk launch from the committed
+    `ncu --set full` capture summary (profiles/scan_traffic.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "scan_traffic.json")))
+        return d["dram_bytes_per_launch"], d.get("source")
+    except Exception:
+        return None, None
+
+
 def peaks():
     try:
         d = json.load(open(MEASURED_PEAKS))
@@ -384,6 +394,7 @@ def main():
     s.close()
 
     scan_avg_ms = statistics.mean(scan_ms)
+    traffic_bytes, traffic_src = ncu_traffic()
     achieved = statistics.mean(scan_bytes) / (scan_avg_ms * 1e-3) / 1e9
     result = {
         "metric": "sched decisions/s at 1M active calls", "value": value, "unit": "decisions/s",
@@ -400,7 +411,8 @@ def main():
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_scan (dense anti-starvation + queue counts)",
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+                     "frac": round(achieved / hbm_peak, 4), "traffic": traffic_bytes, "traffic_source": traffic_src,
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": int(statistics.mean(scan_bytes))},
         "breakdown_ms": {"complete": statistics.mean(comp_ms), "register": statistics.mean(reg_ms),
                          "scan": scan_avg_ms, "select+gather": statistics.mean(sel_ms),

@@ -74,6 +74,9 @@ struct autx_ctx {
   char* staging = nullptr;
   size_t staging_bytes = 0;
   cudaEvent_t sev[2] = {};
+  char* d_outblk = nullptr;  // [counts | batch | admit | preempt] on the device
+  char* h_outblk = nullptr;  // pinned mirror
+  size_t outblk_bytes = 0;
   // routing epoch (a8)
   char* d_route_local = nullptr;   // RouteHdr + max_batch CompRec: this step's completion records
   RouteHdr* h_hdr = nullptr;       // pinned staging for the header
@@ -140,8 +143,17 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   Outputs& o = ctx->out;
   uint32_t BS = c.max_batch;
   size_t ntiles = rows / TILE + 1;
-  CK(dalloc(&o.batch_slots, BS)); CK(dalloc(&o.batch_ids, BS)); CK(dalloc(&o.admit_ids, BS));
-  CK(dalloc(&o.preempt_ids, BS)); CK(dalloc(&o.prev_slots, BS)); CK(dalloc(&o.preempt_slots, BS));
+  CK(dalloc(&o.batch_slots, BS));
+  // one device block [counts | batch | admit | preempt] and its pinned mirror: one D2H per step
+  ctx->outblk_bytes = 64 + (size_t)3 * BS * 8;
+  CK(cudaMalloc((void**)&ctx->d_outblk, ctx->outblk_bytes));
+  CK(cudaHostAlloc((void**)&ctx->h_outblk, ctx->outblk_bytes, cudaHostAllocMapped));
+  memset(ctx->h_outblk, 0, ctx->outblk_bytes);
+  o.zero_copy = getenv("AUTX_ZEROCOPY_OUT") != nullptr;
+  o.d_hout = reinterpret_cast<HostOut*>(ctx->d_outblk);
+  o.batch_ids = reinterpret_cast<uint64_t*>(ctx->d_outblk + 64);
+  o.admit_ids = o.batch_ids + BS;
+  o.preempt_ids = o.admit_ids + BS; CK(dalloc(&o.prev_slots, BS)); CK(dalloc(&o.preempt_slots, BS));
   CK(dalloc(&o.admit_slots, BS));
   o.cand_cap = 2 * BS;
   CK(dalloc(&o.cand, o.cand_cap));
@@ -153,11 +165,10 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K)); CK(dalloc(&o.tile_off, ntiles + 1));
   CK(dalloc(&o.tile_pre, ntiles + 1));
   CK(dalloc(&o.tile_stat, ntiles + 1));
-  CK(cudaHostAlloc((void**)&o.hout, sizeof(HostOut), cudaHostAllocMapped));
-  CK(cudaHostAlloc((void**)&o.h_batch, BS * 8, cudaHostAllocMapped));
-  CK(cudaHostAlloc((void**)&o.h_admit, BS * 8, cudaHostAllocMapped));
-  CK(cudaHostAlloc((void**)&o.h_preempt, BS * 8, cudaHostAllocMapped));
-  memset(o.hout, 0, sizeof(HostOut));
+  o.hout = reinterpret_cast<HostOut*>(ctx->h_outblk);
+  o.h_batch = reinterpret_cast<uint64_t*>(ctx->h_outblk + 64);
+  o.h_admit = o.h_batch + BS;
+  o.h_preempt = o.h_admit + BS;
   ctx->cslots_cap = 4 * BS;
   CK(cudaHostAlloc((void**)&ctx->h_cslots, ctx->cslots_cap * 4, cudaHostAllocMapped));
   ctx->arr_cap = 4 * BS;
@@ -287,8 +298,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   CallTable& t = ctx->ct;
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
                  t.loc, t.hcls, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp,
-                 ctx->ctl, ctx->out.batch_slots, ctx->out.batch_ids, ctx->out.admit_ids,
-                 ctx->out.preempt_ids, ctx->out.prev_slots, ctx->out.preempt_slots,
+                 ctx->ctl, ctx->out.batch_slots, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
                  ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.tile_cnt, ctx->out.tile_off,
                  ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
@@ -297,7 +307,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
                  ctx->d_route_local, ctx->d_pin, ctx->d_rarr, ctx->d_rout,
                  ctx->rx.keys, ctx->rx.keys_alt, ctx->rx.dig_hist, ctx->rx.tile_hist};
   for (void* p : dev) if (p) cudaFree(p);
-  void* host[] = {ctx->out.hout, ctx->out.h_batch, ctx->out.h_admit, ctx->out.h_preempt,
+  void* host[] = {ctx->h_outblk,
                   ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr,
                   ctx->rx.h_dig_hist};
   for (void* p : host) if (p) cudaFreeHost(p);
@@ -592,6 +602,8 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   CK(launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv, ctx->kv_on, t,
                  ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr, ctx->radix ? &ctx->rx : nullptr,
                  arr_base, &ctx->radix_passes));
+  if (!ctx->out.zero_copy)
+    CK(cudaMemcpyAsync(ctx->h_outblk, ctx->d_outblk, ctx->outblk_bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->done, ctx->stream));
   ctx->pending_done = true;
   ctx->last_batch_valid = false;

@@ -176,8 +176,10 @@ struct Outputs {
   uint32_t* tile_off;        // [ntiles_cap+1] candidate offsets
   uint32_t* tile_pre;        // [ntiles_cap] q* rows in earlier tiles
   uint2* tile_stat;          // [ntiles_cap] (promotions, live rows) per tile
-  HostOut* hout;             // mapped pinned host
-  uint64_t* h_batch;         // mapped pinned host mirrors
+  HostOut* hout;             // host-visible counts (pinned)
+  HostOut* d_hout;           // device copy of the counts (copied out with the lists by one DMA)
+  int zero_copy;             // 1: finalize stores the host mirrors itself over PCIe (A/B switch)
+  uint64_t* h_batch;         // pinned host mirrors
   uint64_t* h_admit;
   uint64_t* h_preempt;
 };

@@ -1179,9 +1179,12 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     ctl->n_live = 0;
     s_hout = h;
   }
-  // host mirrors: coalesced 16-byte zero-copy stores (few PCIe write TLPs) after the device lists
+  // host-visible results: by default the device block (counts + lists) is copied out by one
+  // cudaMemcpyAsync after the kernel; the zero-copy variant stores the mirrors over PCIe here
   __syncthreads();
-  {
+  if (!out.zero_copy) {
+    if (tid == 0) *out.d_hout = s_hout;
+  } else {
     const uint32_t nb = s_hout.n_batch, na = s_hout.n_admit, np_ = s_hout.n_preempt;
     auto mirror = [&](uint64_t* dst, const uint64_t* src, uint32_t n) {
       for (uint32_t i = tid; i < n / 2; i += NT)
