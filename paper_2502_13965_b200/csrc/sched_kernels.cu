@@ -427,7 +427,8 @@ template <int NT>
 __device__ void select_body(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t ntiles);
 
 __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                               Outputs out, uint32_t t, uint32_t ntiles) {
+                                                               Outputs out, uint32_t t, uint32_t ntiles,
+                                                               bool fuse_select) {
   pdl_wait();
   __shared__ __align__(8) uint64_t bars[SCAN_STAGES];
   __shared__ uint64_t wc[BULK_THREADS / 32][4];
@@ -517,7 +518,8 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
     }
     __syncthreads();  // wc/wn reuse
   }
-  // the last CTA to finish picks the boundary queue and the tile offsets (k_select's work)
+  // optionally, the last CTA to finish picks the boundary queue and the tile offsets
+  if (!fuse_select) return;
   __shared__ bool last;
   __threadfence();
   __syncthreads();
@@ -1269,6 +1271,9 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   } else {
     static int scan_ctas = 0;
     static bool simple = getenv("AUTX_SCAN_SIMPLE") != nullptr;  // A/B switch for profiling
+    // last-CTA fusion of select into the scan and finalize into the rank kernel: measured slower
+    // than the PDL-chained separate kernels (fences vs hidden launch gaps), kept as an option
+    static bool fuse = getenv("AUTX_FUSE") != nullptr;
     if (!scan_ctas) {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -1281,8 +1286,9 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
     } else {
       launch_pdl(k_scan_bulk, std::min<uint32_t>(ntiles, scan_ctas), BULK_THREADS,
-                 (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, ctl, out, t, ntiles);
+                 (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, ctl, out, t, ntiles, fuse);
       if (ev) cudaEventRecord(ev[1], s);
+      if (!fuse) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
     }
     launch_pdl(k_gather, ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS, SCAN_THREADS, 0, s, pol,
                ct, ctl, out, n_rows, ntiles, t);
@@ -1294,6 +1300,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_finalize<FIN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_finalize<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_rank<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_rank<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1302,9 +1310,13 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   }
   const uint32_t rank_grid = (2 * pol.max_batch + RANK_PER_CTA - 1) / RANK_PER_CTA;
   if (ev) cudaEventRecord(ev[2], s);
-  if (pol.max_batch <= 1024) {
+  static bool fuse_fin = getenv("AUTX_FUSE") != nullptr;
+  if (pol.max_batch <= 1024 && fuse_fin) {
     // rank + finalize in one launch: the last rank CTA (256 threads = 4 candidates each) finalizes
     launch_pdl(k_rank<true>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  } else if (pol.max_batch <= 1024) {
+    launch_pdl(k_rank<false>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+    launch_pdl(k_finalize<256>, 1, 256, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
   } else {
     launch_pdl(k_rank<false>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
     launch_pdl(k_finalize<FIN_THREADS>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np,
