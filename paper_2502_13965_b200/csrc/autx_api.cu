@@ -145,7 +145,8 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   size_t ntiles = rows / TILE + 1;
   CK(dalloc(&o.batch_slots, BS));
   // one device block [counts | batch | admit | preempt] and its pinned mirror: one D2H per step
-  ctx->outblk_bytes = 64 + (size_t)3 * BS * 8;
+  const uint32_t BSp = (BS + 1) & ~1u;  // even list strides keep every list 16-byte aligned
+  ctx->outblk_bytes = 64 + (size_t)3 * BSp * 8;
   CK(cudaMalloc((void**)&ctx->d_outblk, ctx->outblk_bytes));
   CK(cudaHostAlloc((void**)&ctx->h_outblk, ctx->outblk_bytes, cudaHostAllocMapped));
   memset(ctx->h_outblk, 0, ctx->outblk_bytes);
@@ -153,8 +154,8 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   o.zero_copy = getenv("AUTX_DMA_OUT") == nullptr;
   o.d_hout = reinterpret_cast<HostOut*>(ctx->d_outblk);
   o.batch_ids = reinterpret_cast<uint64_t*>(ctx->d_outblk + 64);
-  o.admit_ids = o.batch_ids + BS;
-  o.preempt_ids = o.admit_ids + BS; CK(dalloc(&o.prev_slots, BS)); CK(dalloc(&o.preempt_slots, BS));
+  o.admit_ids = o.batch_ids + BSp;
+  o.preempt_ids = o.admit_ids + BSp; CK(dalloc(&o.prev_slots, BS)); CK(dalloc(&o.preempt_slots, BS));
   CK(dalloc(&o.admit_slots, BS));
   o.cand_cap = 2 * BS;
   CK(dalloc(&o.cand, o.cand_cap));
@@ -163,13 +164,14 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&o.ckey, 2 * BS));
   CK(dalloc(&o.skey, 2 * BS));
   CK(dalloc(&o.sidx, 2 * BS));
+  CK(dalloc(&o.srec, 2 * BS));
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K)); CK(dalloc(&o.tile_off, ntiles + 1));
   CK(dalloc(&o.tile_pre, ntiles + 1));
   CK(dalloc(&o.tile_stat, ntiles + 1));
   o.hout = reinterpret_cast<HostOut*>(ctx->h_outblk);
   o.h_batch = reinterpret_cast<uint64_t*>(ctx->h_outblk + 64);
-  o.h_admit = o.h_batch + BS;
-  o.h_preempt = o.h_admit + BS;
+  o.h_admit = o.h_batch + BSp;
+  o.h_preempt = o.h_admit + BSp;
   ctx->cslots_cap = 4 * BS;
   CK(cudaHostAlloc((void**)&ctx->h_cslots, ctx->cslots_cap * 4, cudaHostAllocMapped));
   ctx->arr_cap = 4 * BS;
@@ -300,7 +302,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
                  t.loc, t.hcls, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp,
                  ctx->ctl, ctx->out.batch_slots, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
-                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.tile_cnt, ctx->out.tile_off,
+                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.tile_off,
                  ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,

@@ -76,7 +76,8 @@ struct Ctl {
   uint32_t qstar;      // boundary queue (K if all live calls are candidates)
   uint32_t mprime;     // rows of q* to take in table order
   uint32_t n_cand_a;   // candidates from the table scan
-  uint32_t n_cand_b;   // extra running candidates of queue q*
+  uint32_t n_cand_b;   // extra running candidates of queue q* (previous batch, not in region A)
+  uint32_t qs_boundary;  // slot of the m'-th live row of q* (region A's last q* row)
   uint32_t n_promoted;
   uint32_t n_live;
   // finalize results
@@ -172,6 +173,7 @@ struct Outputs {
   uint64_t* ckey;            // [2 BS] keys: region A at [0, nA), previous batch at [nA, nA + n_prev)
   uint64_t* skey;            // [2 BS] keys sorted by k_rank
   uint32_t* sidx;            // [2 BS] element index of each sorted key
+  CandRec* srec;             // [2 BS] candidate records in sorted order
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* tile_off;        // [ntiles_cap+1] candidate offsets
   uint32_t* tile_pre;        // [ntiles_cap] q* rows in earlier tiles

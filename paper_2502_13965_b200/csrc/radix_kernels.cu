@@ -172,6 +172,7 @@ __global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out
   }
   if (threadIdx.x == 0) {
     ctl->n_cand_a = n;
+    ctl->n_cand_b = 0;
     ctl->qstar = K;  // no extra running candidates: the sort already ordered them
   }
 }

@@ -424,7 +424,7 @@ constexpr int BULK_THREADS = 512;                 // 16 warps per CTA, 4 rows pe
 constexpr int BULK_ROWS = TILE / BULK_THREADS;
 
 template <int NT>
-__device__ void select_body(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t ntiles);
+__device__ void select_body(const Policy& pol, const CallTable& ct, Ctl* ctl, Outputs& out, uint32_t ntiles);
 
 __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                                Outputs out, uint32_t t, uint32_t ntiles,
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
   if (!last) return;
   __threadfence();
   if (tid == 0) ctl->tiles_done = 0;
-  select_body<BULK_THREADS>(pol, ctl, out, ntiles);
+  select_body<BULK_THREADS>(pol, ct, ctl, out, ntiles);
 }
 
 // One CTA: q* = smallest q with sum_{k<=q} total_k >= BS (K if none), m' = BS - sum_{k<q*}
@@ -540,12 +540,17 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
 //     off(tile) = sum_{k<q*} prefix_k(tile) + min(prefix_{q*}(tile), m').
 constexpr int SEL_THREADS = 1024;
 template <int NT>
-__device__ void select_body(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t ntiles) {
+__device__ void find_boundary(const Policy& pol, const CallTable& ct, Ctl* ctl, uint32_t qs, uint32_t btile,
+                              uint32_t bk);
+
+template <int NT>
+__device__ void select_body(const Policy& pol, const CallTable& ct, Ctl* ctl, Outputs& out, uint32_t ntiles) {
   __shared__ uint32_t tot[MAX_K + 2];
   __shared__ unsigned long long red[33];
-  __shared__ uint32_t s_qstar, s_m;
+  __shared__ uint32_t s_qstar, s_m, s_btile, s_bk;
   const uint32_t tid = threadIdx.x;
   if (tid < MAX_K + 2) tot[tid] = 0;
+  if (tid == 0) { s_btile = NONE; s_bk = 0; }
   __syncthreads();
   if (ntiles <= NT) {
     // fast path: one tile per thread, its 16 counters stay in registers (one load round trip)
@@ -601,12 +606,16 @@ __device__ void select_body(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t 
       uint32_t pre_a = (uint32_t)(pre >> 32), pre_q = (uint32_t)pre;
       out.tile_pre[tid] = pre_q;
       out.tile_off[tid] = pre_a + min(pre_q, m);
+      if (pre_q < m && m <= pre_q + cq) { s_btile = tid; s_bk = m - 1 - pre_q; }
     }
     if (tid == 0) {
       uint32_t n = (uint32_t)(total >> 32) + min((uint32_t)total, m);
       out.tile_off[ntiles] = n;
       ctl->n_cand_a = n;
+      ctl->n_cand_b = 0;
     }
+    __syncthreads();
+    find_boundary<NT>(pol, ct, ctl, qs, s_btile, s_bk);
     return;
   }
   const uint32_t per = (ntiles + NT - 1) / NT;
@@ -672,6 +681,7 @@ __device__ void select_body(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t 
     uint32_t cq = qs < pol.K ? c[qs] : 0;
     out.tile_pre[tl] = pre_q;
     out.tile_off[tl] = pre_a + min(pre_q, m);
+    if (pre_q < m && m <= pre_q + cq) { s_btile = tl; s_bk = m - 1 - pre_q; }
     pre_a += a;
     pre_q += cq;
   }
@@ -680,13 +690,48 @@ __device__ void select_body(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t 
     uint32_t n = ta + min(tq, m);
     out.tile_off[ntiles] = n;
     ctl->n_cand_a = n;
+    ctl->n_cand_b = 0;
+  }
+  __syncthreads();
+  find_boundary<NT>(pol, ct, ctl, qs, s_btile, s_bk);
+}
+
+// Slot of region A's last row of q*: the bk-th (0-based) live row of q* inside tile btile.  Region
+// A's q* part is exactly the live q* rows with slot <= it (table order = slot order), which lets
+// the gather leave previous-batch rows already in A out of region B.
+template <int NT>
+__device__ void find_boundary(const Policy& pol, const CallTable& ct, Ctl* ctl, uint32_t qs, uint32_t btile,
+                              uint32_t bk) {
+  __shared__ uint32_t red_b[33];
+  if (btile == NONE) {  // q* = K (every live call is a candidate) or m' = 0
+    if (threadIdx.x == 0) ctl->qs_boundary = NONE;
+    return;
+  }
+  constexpr uint32_t CH = TILE / NT;  // qf bytes per thread
+  const uint32_t r0 = btile * TILE + threadIdx.x * CH;
+  uint32_t cnt = 0;
+  uint8_t b[CH];
+#pragma unroll
+  for (uint32_t j = 0; j < CH; ++j) {
+    b[j] = ct.qf[r0 + j];
+    cnt += (!(b[j] & QF_DEAD) && (b[j] & QF_QMASK) == qs) ? 1u : 0u;
+  }
+  uint32_t pre = block_excl_scan<uint32_t, NT>(cnt, red_b, nullptr);
+  if (pre <= bk && bk < pre + cnt) {
+    uint32_t k = pre;
+#pragma unroll
+    for (uint32_t j = 0; j < CH; ++j)
+      if (!(b[j] & QF_DEAD) && (b[j] & QF_QMASK) == qs) {
+        if (k == bk) ctl->qs_boundary = r0 + j;
+        ++k;
+      }
   }
 }
 
-__global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Outputs out, uint32_t ntiles) {
+__global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, CallTable ct, Ctl* ctl, Outputs out, uint32_t ntiles) {
   pdl_wait();
   pdl_trigger();
-  select_body<SEL_THREADS>(pol, ctl, out, ntiles);
+  select_body<SEL_THREADS>(pol, ct, ctl, out, ntiles);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -694,7 +739,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, Ctl* ctl, Ou
 // candidate (q < q*, or among the first m' rows of q*) in table order.  CTAs past the last tile
 // write the records of the previous batch (the resident set) for preempt/region B.
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable ct, const Ctl* ctl,
+__global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable ct, Ctl* ctl,
                                                          Outputs out, uint32_t n_rows, uint32_t ntiles,
                                                          uint32_t t) {
   pdl_wait();
@@ -708,8 +753,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
       CandRec r;
       load_rec(ct, out.prev_slots[j], &r);
       out.prev_rec[j] = r;
-      bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == ctl->qstar;
+      // region B: live calls of q* that region A (q* rows with slot <= boundary) does not hold
+      const uint32_t bnd = ctl->qs_boundary;
+      bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == ctl->qstar && (bnd == NONE || r.slot > bnd);
       out.ckey[ctl->n_cand_a + j] = b ? cand_key(r, t) : ~0ull;
+      if (b) atomicAdd(&ctl->n_cand_b, 1u);
     }
     return;
   }
@@ -824,6 +872,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     if (sub == 0 && e < n) {
       out.skey[cnt] = x;
       out.sidx[cnt] = e;
+      if (x != ~0ull) out.srec[cnt] = e < ctl->n_cand_a ? out.cand_rec[e] : out.prev_rec[e - ctl->n_cand_a];
     }
   }
   if (!FUSED) return;
@@ -842,62 +891,33 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
 template <int NT>
 __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
                               uint32_t t, uint32_t np, uint32_t seqno) {
-  uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] unique sorted keys
-  uint32_t* ui = reinterpret_cast<uint32_t*>(uk + np);      // [np] element index
+  uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] sorted keys of the first m candidates
   __shared__ unsigned long long red64[33];
   __shared__ uint32_t red[33];
   __shared__ uint32_t s_nbatch;
   __shared__ HostOut s_hout;
   const uint32_t tid = threadIdx.x;
   const uint32_t BS = pol.max_batch;
-  const uint32_t nA = ctl->n_cand_a, n_prev = ctl->n_prev;
-  const uint32_t n_all = nA + n_prev;
+  const uint32_t n_prev = ctl->n_prev;
+  // region A + region B (previous-batch calls of q* not in A): no duplicates, ~0 sentinels last
+  const uint32_t ncand = ctl->n_cand_a + ctl->n_cand_b;
   STAMP(0);
   if (tid == 0) s_nbatch = 0;
-  // ---- (1) the sorted keys from k_rank, de-duplicated (a running call of q* can be both in
-  // region A and in the previous batch) and without the ~0 sentinels -----------------------
-  constexpr int D = 8;  // keys per thread, blocked; 2 BS <= 8192
-  uint64_t kk[D];
-  uint32_t keep = 0, nkeep = 0;
-#pragma unroll
-  for (int r = 0; r < D; ++r) {
-    uint32_t i = tid * D + r;
-    kk[r] = i < n_all ? __ldcg(out.skey + i) : ~0ull;
-  }
-  {
-    uint64_t before = (tid > 0 && tid * D - 1 < n_all) ? __ldcg(out.skey + tid * D - 1) : ~0ull;
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-      uint64_t prev = r ? kk[r - 1] : (tid ? before : ~0ull);
-      if (kk[r] != ~0ull && (tid * D + r == 0 || kk[r] != prev)) { keep |= 1u << r; ++nkeep; }
-    }
-  }
-  uint32_t ntot;
-  uint32_t kpos = block_excl_scan<uint32_t, NT>(nkeep, red, &ntot);
-#pragma unroll
-  for (int r = 0; r < D; ++r)
-    if (keep & (1u << r)) {
-      uk[kpos] = kk[r];
-      ui[kpos] = __ldcg(out.sidx + tid * D + r);
-      ++kpos;
-    }
-  __syncthreads();
-  const uint32_t ncand = ntot;
-  STAMP(1);
-  STAMP(2);
-  // ---- (3) the first m = min(BS, ncand) keys: fields from the records; prefix cutoff ---------
+  // ---- (1) the first m = min(BS, ncand) candidates in key order: key + record, plus the
+  // previous batch's records (preempt), all in one round of independent loads --------------
   const uint32_t m = min(BS, ncand);
   constexpr int R = 4;  // items per thread, blocked (i = tid * R + r); BS <= 4096
   uint32_t c_s[R], c_qf[R], c_tok[R], c_ex[R], c_mt[R], c_qt[R], c_kvb[R];
   uint64_t c_cid[R];
+  uint32_t p_s[R], p_qf[R], p_held[R];  // previous batch: slot, flags, held blocks, order key
+  uint64_t p_cid[R], p_key[R];
   unsigned long long my_kv = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    uint32_t i = tid * R + r;
-    c_kvb[r] = 0;
+    const uint32_t i = tid * R + r;
     if (i < m) {
-      uint32_t x = ui[i];
-      const CandRec& rc = x < nA ? out.cand_rec[x] : out.prev_rec[x - nA];
+      uk[i] = __ldcg(out.skey + i);
+      const CandRec rc = out.srec[i];
       c_s[r] = rc.slot;
       c_qf[r] = rc.qf;
       c_tok[r] = rc.tok;
@@ -905,10 +925,26 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       c_mt[r] = rc.mtime;
       c_qt[r] = rc.quanta;
       c_cid[r] = rc.cid;
+    }
+    if (i < n_prev) {
+      const CandRec pr = out.prev_rec[i];
+      p_s[r] = pr.slot;
+      p_qf[r] = pr.qf;
+      p_cid[r] = pr.cid;
+      p_key[r] = cand_key(pr, t);
+      p_held[r] = ceil_div_u32(pr.tok + pr.exec, pol.block_tokens);  // R28
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    c_kvb[r] = 0;
+    if (tid * R + r < m) {
       c_kvb[r] = ceil_div_u32(c_tok[r] + c_ex[r] + 1, pol.block_tokens);  // R14
       my_kv += c_kvb[r];
     }
   }
+  STAMP(1);
+  STAMP(2);
   unsigned long long kv_pre = block_excl_scan<unsigned long long, NT>(my_kv, red64, nullptr);
   // Alg. 1 l.34-37: take while count <= BS and sum kvb <= P; kvb >= 1 makes the prefix sums
   // strictly increasing, so the fitting items are exactly a prefix: n_batch = max fitting i + 1
@@ -964,28 +1000,20 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   // ---- (5) preempt = previous batch, still active, not in the batch (previous-batch order) ---
   unsigned long long my_pre = 0;
   uint32_t is_pre = 0;
-  uint32_t p_s[R], p_qf[R];
-  uint64_t p_cid[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t i = tid * R + r;
-    if (i < n_prev) {
-      CandRec pr = out.prev_rec[i];
-      p_s[r] = pr.slot;
-      p_qf[r] = pr.qf;
-      p_cid[r] = pr.cid;
-      if (!(pr.qf & QF_DEAD)) {
-        // membership: binary search of the row's (unique) key in the sorted batch prefix
-        uint64_t key = cand_key(pr, t);
-        uint32_t lo = 0, hi = n_batch;
-        while (lo < hi) {
-          uint32_t mid = (lo + hi) >> 1;
-          if (uk[mid] < key) lo = mid + 1; else hi = mid;
-        }
-        if (!(lo < n_batch && uk[lo] == key)) {
-          is_pre |= 1u << r;
-          my_pre += (1ull << 44) | ceil_div_u32(pr.tok + pr.exec, pol.block_tokens);  // R28
-        }
+    if (i < n_prev && !(p_qf[r] & QF_DEAD)) {
+      // membership: binary search of the row's (unique) key in the sorted batch prefix
+      const uint64_t key = p_key[r];
+      uint32_t lo = 0, hi = n_batch;
+      while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (uk[mid] < key) lo = mid + 1; else hi = mid;
+      }
+      if (!(lo < n_batch && uk[lo] == key)) {
+        is_pre |= 1u << r;
+        my_pre += (1ull << 44) | p_held[r];
       }
     }
   }
@@ -1283,12 +1311,12 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     if (simple) {
       launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, out, t, n_rows);
       if (ev) cudaEventRecord(ev[1], s);
-      launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
+      launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     } else {
       launch_pdl(k_scan_bulk, std::min<uint32_t>(ntiles, scan_ctas), BULK_THREADS,
                  (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, ctl, out, t, ntiles, fuse);
       if (ev) cudaEventRecord(ev[1], s);
-      if (!fuse) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ctl, out, ntiles);
+      if (!fuse) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     }
     launch_pdl(k_gather, ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS, SCAN_THREADS, 0, s, pol,
                ct, ctl, out, n_rows, ntiles, t);
