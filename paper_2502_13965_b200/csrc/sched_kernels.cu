@@ -912,27 +912,40 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   uint32_t p_s[R], p_qf[R], p_held[R];  // previous batch: slot, flags, held blocks, order key
   uint64_t p_cid[R], p_key[R];
   unsigned long long my_kv = 0;
+  {
+    // all loads of this phase first, through restrict-qualified locals, so that they overlap
+    // (one L2 round trip instead of a chain of them)
+    const uint64_t* __restrict__ skey = out.skey;
+    const CandRec* __restrict__ srec = out.srec;
+    const CandRec* __restrict__ prec = out.prev_rec;
+    uint64_t kk[R];
+    CandRec rc[R], pr[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t i = tid * R + r;
-    if (i < m) {
-      uk[i] = __ldcg(out.skey + i);
-      const CandRec rc = out.srec[i];
-      c_s[r] = rc.slot;
-      c_qf[r] = rc.qf;
-      c_tok[r] = rc.tok;
-      c_ex[r] = rc.exec;
-      c_mt[r] = rc.mtime;
-      c_qt[r] = rc.quanta;
-      c_cid[r] = rc.cid;
+    for (int r = 0; r < R; ++r) {
+      const uint32_t i = tid * R + r;
+      if (i < m) { kk[r] = skey[i]; rc[r] = srec[i]; }
+      if (i < n_prev) pr[r] = prec[i];
     }
-    if (i < n_prev) {
-      const CandRec pr = out.prev_rec[i];
-      p_s[r] = pr.slot;
-      p_qf[r] = pr.qf;
-      p_cid[r] = pr.cid;
-      p_key[r] = cand_key(pr, t);
-      p_held[r] = ceil_div_u32(pr.tok + pr.exec, pol.block_tokens);  // R28
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t i = tid * R + r;
+      if (i < m) {
+        uk[i] = kk[r];
+        c_s[r] = rc[r].slot;
+        c_qf[r] = rc[r].qf;
+        c_tok[r] = rc[r].tok;
+        c_ex[r] = rc[r].exec;
+        c_mt[r] = rc[r].mtime;
+        c_qt[r] = rc[r].quanta;
+        c_cid[r] = rc[r].cid;
+      }
+      if (i < n_prev) {
+        p_s[r] = pr[r].slot;
+        p_qf[r] = pr[r].qf;
+        p_cid[r] = pr[r].cid;
+        p_key[r] = cand_key(pr[r], t);
+        p_held[r] = ceil_div_u32(pr[r].tok + pr[r].exec, pol.block_tokens);  // R28
+      }
     }
   }
 #pragma unroll
@@ -1216,14 +1229,26 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     if (tid == 0) *out.d_hout = s_hout;
   } else {
     const uint32_t nb = s_hout.n_batch, na = s_hout.n_admit, np_ = s_hout.n_preempt;
-    auto mirror = [&](uint64_t* dst, const uint64_t* src, uint32_t n) {
-      for (uint32_t i = tid; i < n / 2; i += NT)
-        reinterpret_cast<uint4*>(dst)[i] = __ldcg(reinterpret_cast<const uint4*>(src) + i);
-      if ((n & 1) && tid == 0) dst[n - 1] = __ldcg(src + n - 1);
-    };
-    mirror(out.h_batch, out.batch_ids, nb);
-    mirror(out.h_admit, out.admit_ids, na);
-    mirror(out.h_preempt, out.preempt_ids, np_);
+    // loads of all three lists first (independent), then the PCIe stores
+    constexpr int MR = 8;  // 16-B words per thread per list; BS <= 4096 with 256+ threads
+    uint4 vb[MR], va[MR], vp[MR];
+    const uint4* __restrict__ sb = reinterpret_cast<const uint4*>(out.batch_ids);
+    const uint4* __restrict__ sa = reinterpret_cast<const uint4*>(out.admit_ids);
+    const uint4* __restrict__ sp = reinterpret_cast<const uint4*>(out.preempt_ids);
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      const uint32_t i = tid + k * NT;
+      if (i < (nb + 1) / 2) vb[k] = __ldcg(sb + i);
+      if (i < (na + 1) / 2) va[k] = __ldcg(sa + i);
+      if (i < (np_ + 1) / 2) vp[k] = __ldcg(sp + i);
+    }
+#pragma unroll
+    for (int k = 0; k < MR; ++k) {
+      const uint32_t i = tid + k * NT;
+      if (i < (nb + 1) / 2) reinterpret_cast<uint4*>(out.h_batch)[i] = vb[k];
+      if (i < (na + 1) / 2) reinterpret_cast<uint4*>(out.h_admit)[i] = va[k];
+      if (i < (np_ + 1) / 2) reinterpret_cast<uint4*>(out.h_preempt)[i] = vp[k];
+    }
     __syncthreads();
     if (tid == 0) {
       __threadfence_system();
