@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--swap-steps", type=int, default=60)
     ap.add_argument("--order", default="select", choices=["select", "radix"])
+    ap.add_argument("--workload", default="mcts", choices=["mcts", "chatbot", "react"],
+                    help="mcts: BASELINE configs[3] (default, the headline); chatbot/react: configs[1]/[2]")
     return ap.parse_args()
 
 
@@ -273,7 +275,14 @@ def main():
 
     t_gen = time.time()
     if world == 1:
-        tr = burst_mcts_mapreduce(args.active, seed=BASE_SEED + CONFIG_INDEX["mcts"])
+        if args.workload == "chatbot":
+            from autx_workload import chatbot
+            tr = chatbot(10_000)          # configs[1]: 10k ShareGPT-shaped programs, all active
+        elif args.workload == "react":
+            from autx_workload import react
+            tr = react(100_000)           # configs[2]: 100k BFCL-shaped programs, all active
+        else:
+            tr = burst_mcts_mapreduce(args.active, seed=BASE_SEED + CONFIG_INDEX["mcts"])
     else:
         # weak scaling: one 1M-call shard per engine; every rank holds the whole (replicated)
         # workload because Alg. 2 routes each arrival to any engine
@@ -282,7 +291,10 @@ def main():
                      for r in range(world)], name="mcts_mapreduce_burst_x%d" % world)
     t_gen = time.time() - t_gen
     lad = spec_ladder()
-    s = Scheduler(policy="atlas", beta=(2, 1), max_batch=1024, kv_budget=32768, block_tokens=16,
+    wl = {"mcts": dict(policy="atlas", max_batch=1024, kv_budget=32768),
+          "chatbot": dict(policy="plas", max_batch=256, kv_budget=6000),
+          "react": dict(policy="plas", max_batch=256, kv_budget=8000)}[args.workload]
+    s = Scheduler(policy=wl["policy"], beta=(2, 1), max_batch=wl["max_batch"], kv_budget=wl["kv_budget"], block_tokens=16,
                   max_calls=int(args.active * 1.25) + 4096, max_programs=tr.n_programs + 1024,
                   order_mode=ORDER_RADIX if args.order == "radix" else ORDER_SELECT,
                   device=local, stream=stream.cuda_stream, rank=rank, nranks=world, **lad)
@@ -401,11 +413,13 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
-        "config": {"workload": "mcts_mapreduce_burst (BASELINE configs[3])" if world == 1 else
+        "config": {"workload": {"chatbot": "chatbot 10k ShareGPT-shaped programs (BASELINE configs[1])",
+                                "react": "ReAct 100k BFCL-shaped programs (BASELINE configs[2])"}.get(
+                       args.workload, "mcts_mapreduce_burst (BASELINE configs[3])") if world == 1 else
                    "mcts_mapreduce_burst x%d engines with Alg. 2 routing (BASELINE configs[4], weak)" % world,
-                   "active_calls_per_gpu": args.active,
-                   "programs": tr.n_programs, "policy": "atlas", "ladder": "SPEC K=8", "beta": "2",
-                   "max_batch": 1024, "kv_budget_blocks": 32768, "fast_forward_steps": args.ff,
+                   "mean_active_calls_per_gpu": int(decisions / args.steps / world),
+                   "programs": tr.n_programs, "policy": wl["policy"], "ladder": "SPEC K=8", "beta": "2",
+                   "max_batch": wl["max_batch"], "kv_budget_blocks": wl["kv_budget"], "fast_forward_steps": args.ff,
                    "order": args.order, "l2": "flushed before every step (512 MiB write)" if not args.no_flush else "hot",
                    "parallelism": f"engines{world} (one scheduler per GPU)"},
         "gpu_launches": launches,

@@ -266,6 +266,10 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
   p.max_batch = c.max_batch;
   p.kv_budget = c.kv_budget_blocks;
   p.block_tokens = c.block_tokens;
+  p.bt_shift = 0xFFu;
+  if ((c.block_tokens & (c.block_tokens - 1)) == 0)
+    for (uint32_t b = 0; b < 32; ++b)
+      if ((1u << b) == c.block_tokens) p.bt_shift = b;
   p.n_gpu_blocks = c.n_gpu_blocks;
   p.max_blocks_per_call = c.max_blocks_per_call;
   p.host_pages_lo = (uint32_t)std::min<uint64_t>(c.host_pages, 0xFFFFFFF0ull);

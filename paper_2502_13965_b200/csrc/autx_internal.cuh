@@ -64,6 +64,7 @@ struct Policy {
   uint32_t n_gpu_blocks;
   uint32_t max_blocks_per_call;
   uint32_t host_pages_lo;  // host arena pages (capped to 2^32-1)
+  uint32_t bt_shift;       // log2(block_tokens) if a power of two, else 0xFF
 };
 
 // Step control block in device memory (written by the prologue kernels).

@@ -30,6 +30,12 @@ __device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc)
 
 #define STAMP(i) do { if (threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
 
+// ceil(tokens / block_tokens) (R14, R28): a shift when block_tokens is a power of two
+__device__ __forceinline__ uint32_t blocks_for(const Policy& pol, uint32_t tokens) {
+  return pol.bt_shift != 0xFFu ? (tokens + pol.block_tokens - 1) >> pol.bt_shift
+                               : (tokens + pol.block_tokens - 1) / pol.block_tokens;
+}
+
 __device__ __forceinline__ void set_err(Ctl* ctl, uint32_t code, uint32_t info) {
   if (atomicCAS(&ctl->err, 0u, code) == 0u) ctl->err_info = info;
 }
@@ -243,13 +249,6 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
     for (uint32_t i = tid; i < a.n_comp; i += PRO_THREADS) s_comp[i] = a.comp[i];
   if (arr_inline)
     for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) s_arr[i] = a.arr[i];
-  // the dense pass gathers the process table for every call: pull its lines into L2 now
-  {
-    const char* base = reinterpret_cast<const char*>(pt.info);
-    const uint32_t lines = (uint32_t)(((uint64_t)a.n_prog_rows * sizeof(PInfo) + 127) / 128);
-    for (uint32_t l = tid; l < lines; l += PRO_THREADS)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)l * 128));
-  }
   pdl_wait();
   pdl_trigger();
   __syncthreads();
@@ -944,7 +943,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         p_qf[r] = pr[r].qf;
         p_cid[r] = pr[r].cid;
         p_key[r] = cand_key(pr[r], t);
-        p_held[r] = ceil_div_u32(pr[r].tok + pr[r].exec, pol.block_tokens);  // R28
+        p_held[r] = blocks_for(pol, pr[r].tok + pr[r].exec);  // R28
       }
     }
   }
@@ -952,7 +951,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   for (int r = 0; r < R; ++r) {
     c_kvb[r] = 0;
     if (tid * R + r < m) {
-      c_kvb[r] = ceil_div_u32(c_tok[r] + c_ex[r] + 1, pol.block_tokens);  // R14
+      c_kvb[r] = blocks_for(pol, c_tok[r] + c_ex[r] + 1);  // R14
       my_kv += c_kvb[r];
     }
   }
@@ -988,7 +987,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       out.batch_ids[i] = c_cid[r];
       kv_mine += c_kvb[r];
       if (!(c_qf[r] & QF_RES)) {
-        uint64_t held = c_ex[r] > 0 ? ceil_div_u32(c_tok[r] + c_ex[r], pol.block_tokens) : 0;  // R28
+        uint64_t held = c_ex[r] > 0 ? blocks_for(pol, c_tok[r] + c_ex[r]) : 0;  // R28
         my_ad += (1ull << 44) | held;
       }
     }
@@ -1250,10 +1249,8 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       if (i < (np_ + 1) / 2) reinterpret_cast<uint4*>(out.h_preempt)[i] = vp[k];
     }
     __syncthreads();
-    if (tid == 0) {
-      __threadfence_system();
-      *out.hout = s_hout;  // counts last: valid once the lists are
-    }
+    // the host reads after the stream event that follows this kernel, which orders every store
+    if (tid == 0) *out.hout = s_hout;
   }
   STAMP(8);
 }
