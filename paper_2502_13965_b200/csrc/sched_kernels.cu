@@ -275,6 +275,29 @@ cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, Pro
 // q != 0, mtime if != 0, quanta if q != 0 or mtime != 0 (a call in Q_1 that has not run since its
 // last reset already holds Q_1's quantum).
 // ---------------------------------------------------------------------------------------------
+// Per-thread queue histogram: 16 queues x 4-bit fields in one u64 (<= 15 rows per thread), one
+// shift + add per row.  Warp reduction splits even/odd queues into 8-bit fields (<= 15 x 32 = 480
+// would overflow, so callers keep <= 8 rows per thread: <= 256 -> use 8-bit after summing <= 32
+// lanes of <= 8).
+__device__ __forceinline__ void hist_add(uint64_t& h, uint32_t q) { h += 1ull << (4 * q); }
+
+// Reduces the 4-bit histograms of a CTA into per-queue counts (written by the first 16 threads to
+// dst[0..16)); wh: [NW][2] shared scratch.
+template <int NT>
+__device__ __forceinline__ void hist_reduce(uint64_t h, uint64_t (*wh)[2], uint32_t* dst) {
+  constexpr uint64_t M = 0x0F0F0F0F0F0F0F0Full;
+  uint64_t lo = warp_sum(h & M), hi = warp_sum((h >> 4) & M);  // 8-bit fields: <= 8 rows x 32 lanes
+  if (lane_id() == 0) { wh[warp_id()][0] = lo; wh[warp_id()][1] = hi; }
+  __syncthreads();
+  if (threadIdx.x < MAX_K) {
+    const uint32_t k = threadIdx.x, sh = 8 * (k >> 1);
+    uint32_t sum = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) sum += (uint32_t)(wh[w][k & 1] >> sh) & 0xffu;
+    dst[k] = sum;
+  }
+}
+
 __device__ __forceinline__ void count_q(uint64_t& c0, uint64_t& c1, uint64_t& c2, uint64_t& c3,
                                         uint32_t q) {
   uint64_t inc = 1ull << ((q & 3) * 16);
@@ -430,7 +453,7 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
                                                                bool fuse_select) {
   pdl_wait();
   __shared__ __align__(8) uint64_t bars[SCAN_STAGES];
-  __shared__ uint64_t wc[BULK_THREADS / 32][4];
+  __shared__ uint64_t wh[BULK_THREADS / 32][2];
   __shared__ uint32_t wn[BULK_THREADS / 32][2];
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
@@ -470,7 +493,7 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
 #pragma unroll
       for (int j = 0; j < 4; ++j) pi[j] = !(qfs[j] & QF_DEAD) ? pt.info[prog[j]] : PInfo{0, 0, 0ull};
     }
-    uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    uint64_t hq = 0;
     uint32_t npromo = 0, nlive = 0;
     bool wq = false, wb = false, wm = false;
 #pragma unroll
@@ -492,30 +515,21 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
           ++npromo;
         }
       }
-      count_q(c0, c1, c2, c3, q);
+      hist_add(hq, q);
     }
     if (wq) *reinterpret_cast<uint32_t*>(ct.qf + row0) = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
     if (wb) *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
     if (wm) *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
-    c0 = warp_sum(c0); c1 = warp_sum(c1); c2 = warp_sum(c2); c3 = warp_sum(c3);
-    npromo = warp_sum(npromo); nlive = warp_sum(nlive);
-    if (lane_id() == 0) {
-      wc[warp_id()][0] = c0; wc[warp_id()][1] = c1; wc[warp_id()][2] = c2; wc[warp_id()][3] = c3;
-      wn[warp_id()][0] = npromo; wn[warp_id()][1] = nlive;
-    }
-    __syncthreads();
-    if (tid < MAX_K) {
-      uint32_t k = tid, sum = 0;
-#pragma unroll
-      for (int w = 0; w < BULK_THREADS / 32; ++w) sum += (uint32_t)(wc[w][k >> 2] >> ((k & 3) * 16)) & 0xffffu;
-      out.tile_cnt[(size_t)tile * MAX_K + k] = sum;
-    } else if (tid == 32) {
+    const uint32_t pl = warp_sum((npromo << 16) | nlive);  // <= 128 each per warp
+    if (lane_id() == 0) { wn[warp_id()][0] = pl >> 16; wn[warp_id()][1] = pl & 0xffffu; }
+    hist_reduce<BULK_THREADS>(hq, wh, out.tile_cnt + (size_t)tile * MAX_K);
+    if (tid == 32) {
       uint32_t a = 0, b = 0;
 #pragma unroll
       for (int w = 0; w < BULK_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
       out.tile_stat[tile] = make_uint2(a, b);
     }
-    __syncthreads();  // wc/wn reuse
+    __syncthreads();  // wh/wn reuse
   }
   // optionally, the last CTA to finish picks the boundary queue and the tile offsets
   if (!fuse_select) return;
@@ -1012,20 +1026,28 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   // ---- (5) preempt = previous batch, still active, not in the batch (previous-batch order) ---
   unsigned long long my_pre = 0;
   uint32_t is_pre = 0;
+  {
+    // membership of each previous-batch row in the sorted batch prefix: fixed-length branchless
+    // binary searches, the R of a thread interleaved (independent smem chains)
+    uint32_t pos[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    uint32_t i = tid * R + r;
-    if (i < n_prev && !(p_qf[r] & QF_DEAD)) {
-      // membership: binary search of the row's (unique) key in the sorted batch prefix
-      const uint64_t key = p_key[r];
-      uint32_t lo = 0, hi = n_batch;
-      while (lo < hi) {
-        uint32_t mid = (lo + hi) >> 1;
-        if (uk[mid] < key) lo = mid + 1; else hi = mid;
+    for (int r = 0; r < R; ++r) pos[r] = 0;
+    for (uint32_t step = 1u << 12; step > 0; step >>= 1) {  // n_batch <= 4096
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t probe = pos[r] + step;
+        if (probe <= n_batch && uk[probe - 1] < p_key[r]) pos[r] = probe;  // pos = #keys < key
       }
-      if (!(lo < n_batch && uk[lo] == key)) {
-        is_pre |= 1u << r;
-        my_pre += (1ull << 44) | p_held[r];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t i = tid * R + r;
+      if (i < n_prev && !(p_qf[r] & QF_DEAD)) {
+        const bool in = pos[r] < n_batch && uk[pos[r]] == p_key[r];
+        if (!in) {
+          is_pre |= 1u << r;
+          my_pre += (1ull << 44) | p_held[r];
+        }
       }
     }
   }
