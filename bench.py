@@ -353,12 +353,14 @@ def main():
     clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_r{rank}.csv") if os.path.isdir(
         os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_r{rank}.csv")
     clocks.start()
-    ms, decisions, launches = [], 0, 0
+    from paper_2502_13965_b200.autx import kernel_launches
+    ms, decisions = [], 0
+    launches0 = kernel_launches()
     for _ in range(args.steps):
         dt, rec, nc, na = timed_step()
         ms.append(dt)
         decisions += rec["n_active"]
-        launches += 4 + (1 if nc else 0) + (1 if na else 0)
+    launches = kernel_launches() - launches0  # counted by the library at every launch
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

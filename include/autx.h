@@ -199,6 +199,8 @@ uint32_t autx_num_active(const autx_ctx* ctx);
 /* %globaltimer stamps (ns) recorded inside the single-CTA kernels of the last step, for
  * profiling: [0..8] k_finalize phases, [16..19] k_complete phases; copies min(cap, 32). */
 autx_status autx_phase_times(autx_ctx* ctx, uint64_t* ns, uint32_t cap);
+/* Number of kernels this library has launched so far (all contexts of the process). */
+uint64_t autx_kernel_launches(void);
 
 #ifdef __cplusplus
 }

@@ -106,6 +106,7 @@ def load_library(path=LIB_PATH):
         "autx_set_timing": ([P, i32], i32),
         "autx_num_active": ([P], u32),
         "autx_phase_times": ([P, P, u32], i32),
+        "autx_kernel_launches": ([], u64),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -121,7 +122,12 @@ def exported_symbols():
         "autx_end_program", "autx_complete", "autx_register_call", "autx_sched_step",
         "autx_step_wait", "autx_kv_swap", "autx_block_table", "autx_block_table_host", "autx_route_record_bytes",
         "autx_route_pack", "autx_route_apply", "autx_dump_calls", "autx_program_state",
-        "autx_last_step_timing", "autx_set_timing", "autx_num_active", "autx_phase_times"]
+        "autx_last_step_timing", "autx_set_timing", "autx_num_active", "autx_phase_times", "autx_kernel_launches"]
+
+
+def kernel_launches():
+    """Kernels launched by libautx.so so far in this process."""
+    return int(load_library().autx_kernel_launches())
 
 
 def _ptr(a):

@@ -17,6 +17,12 @@
 
 using namespace autx;
 
+unsigned long long autx::g_kernel_launches = 0;
+
+extern "C" uint64_t autx_kernel_launches(void) {
+  return __atomic_load_n(&g_kernel_launches, __ATOMIC_RELAXED);
+}
+
 struct autx_ctx {
   autx_config cfg{};
   Policy pol{};

@@ -228,6 +228,8 @@ struct ArrivalRec {
 
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
 // predecessor in the stream still runs; it must call pdl_wait() before touching its inputs.
+extern unsigned long long g_kernel_launches;  // every library kernel launch (autx_kernel_launches)
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args) {
@@ -241,6 +243,7 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 

@@ -184,6 +184,7 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
   const uint32_t n_pad = ntiles * RX_TILE;
   cudaMemsetAsync(rx.dig_hist, 0, 4 * 256 * sizeof(uint32_t), s);
   uint32_t grid = std::min<uint32_t>(ntiles * RX_ITEMS, (uint32_t)sms * 8);
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   k_keys<<<grid, RX_THREADS, 0, s>>>(pol, ct, pt, ctl, rx, t, n_rows, arr_base);
   // skip detection needs the digit histograms on the host (a 4 KB read; this mode is the
   // contract path, the selection path is the fast path)
@@ -199,12 +200,16 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
       if (rx.h_dig_hist[d * 256 + v] == n_pad) uniform = true;
     if (uniform) continue;
     int shift = 32 + 8 * d;
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
     k_hist<<<ntiles, RX_THREADS, 0, s>>>(a, rx.tile_hist, ntiles, shift);
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
     k_scan_h<<<1, 1024, 0, s>>>(rx.tile_hist, 256 * ntiles);
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
     k_scatter<<<ntiles, RX_THREADS, 0, s>>>(a, b, rx.tile_hist, ntiles, shift);
     std::swap(a, b);
     ++passes;
   }
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   k_take<<<1, 1024, 0, s>>>(a, ct, ctl, out, pol.max_batch, pol.K, t);
   if (passes_out) *passes_out = passes;
   return cudaGetLastError();

@@ -1303,6 +1303,7 @@ cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, Pro
 
 cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,
                          uint64_t stride, uint32_t G, uint32_t t) {
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   k_apply<<<1, FIN_THREADS, 0, s>>>(pol, pt, (const char*)base, stride, G, t);
   return cudaGetLastError();
 }
@@ -1310,6 +1311,7 @@ cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const 
 cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,
                          const RouteArr* arr, uint32_t n, int8_t* pin, uint32_t threshold,
                          int32_t* out) {
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   if (n) k_route<<<1, 32, 0, s>>>((const char*)base, stride, G, arr, n, pin, threshold, out);
   return cudaGetLastError();
 }
@@ -1427,11 +1429,13 @@ __global__ void k_remap(uint32_t* slots, uint32_t n, const uint32_t* old2new) {
 
 cudaError_t launch_compact(cudaStream_t s, CallTable src, CallTable dst, const uint32_t* live,
                            uint32_t n_live) {
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   if (n_live) k_compact<<<(n_live + 255) / 256, 256, 0, s>>>(src, dst, live, n_live);
   return cudaGetLastError();
 }
 
 cudaError_t launch_remap(cudaStream_t s, uint32_t* slots, uint32_t n, const uint32_t* old2new) {
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   if (n) k_remap<<<(n + 255) / 256, 256, 0, s>>>(slots, n, old2new);
   return cudaGetLastError();
 }

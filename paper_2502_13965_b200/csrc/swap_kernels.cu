@@ -101,6 +101,7 @@ cudaError_t launch_swap(cudaStream_t s, const Ctl* ctl, KvState kv, void* const*
                         void* const* d_vpool, uint32_t n_layers, uint32_t chunk_bytes,
                         char* host_arena, int direction, int n_ctas) {
   SwapGeom g{n_layers, chunk_bytes, (uint64_t)n_layers * 2 * chunk_bytes};
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   k_swap_sm<<<n_ctas, 256, 0, s>>>(ctl, kv, d_kpool, d_vpool, g, host_arena, direction);
   return cudaGetLastError();
 }
@@ -109,6 +110,7 @@ cudaError_t launch_stage(cudaStream_t s, const Ctl* ctl, KvState kv, void* const
                          void* const* d_vpool, uint32_t n_layers, uint32_t chunk_bytes,
                          char* staging, int direction, int n_ctas) {
   SwapGeom g{n_layers, chunk_bytes, (uint64_t)n_layers * 2 * chunk_bytes};
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   k_stage<<<n_ctas, 256, 0, s>>>(ctl, kv, d_kpool, d_vpool, g, staging, direction);
   return cudaGetLastError();
 }
