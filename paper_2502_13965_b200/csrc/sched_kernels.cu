@@ -36,6 +36,17 @@ __device__ __forceinline__ uint32_t blocks_for(const Policy& pol, uint32_t token
                                : (tokens + pol.block_tokens - 1) / pol.block_tokens;
 }
 
+// Alg. 1 l.24-26 (R3, R4): W = pwait[p] + wait_c, T = svc[p] + mtime_c; promote iff not 0/0 and
+// W * beta_den >= beta_num * T.  Fast path: W and T fit in 32 bits (no carry), so the products
+// are single 32x32->64 multiplies; otherwise the 128-bit-exact comparison.
+__device__ __forceinline__ bool starving(const Policy& pol, const PInfo& pi, uint32_t wait, uint32_t mtime) {
+  const uint32_t W32 = (uint32_t)pi.pwait + wait, T32 = pi.svc + mtime;
+  if ((uint32_t)(pi.pwait >> 32) == 0 && W32 >= wait && T32 >= pi.svc)
+    return (W32 | T32) != 0 && (uint64_t)W32 * pol.beta_den >= (uint64_t)T32 * pol.beta_num;
+  const uint64_t W = pi.pwait + (uint64_t)wait, T = (uint64_t)pi.svc + mtime;
+  return !(W == 0 && T == 0) && mul_ge(W, pol.beta_den, T, pol.beta_num);
+}
+
 __device__ __forceinline__ void set_err(Ctl* ctl, uint32_t code, uint32_t info) {
   if (atomicCAS(&ctl->err, 0u, code) == 0u) ctl->err_info = info;
 }
@@ -503,9 +514,7 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
       ++nlive;
       uint32_t q = qf & QF_QMASK;
       if (anti) {
-        uint64_t W = pi[j].pwait + (uint64_t)(t - base[j] - mtim[j]);
-        uint64_t T = (uint64_t)pi[j].svc + mtim[j];
-        if (!(W == 0 && T == 0) && mul_ge(W, pol.beta_den, T, pol.beta_num)) {  // Alg. 1 l.26
+        if (starving(pol, pi[j], t - base[j] - mtim[j], mtim[j])) {  // Alg. 1 l.26
           if (q != 0 || mtim[j] != 0) ct.quanta[row0 + j] = pol.quanta[0];
           if (q != 0) { qfs[j] = qf & ~QF_QMASK; wq = true; }
           if (mtim[j] != 0) { mtim[j] = 0; wm = true; }
