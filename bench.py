@@ -294,7 +294,7 @@ def main():
     wl = {"mcts": dict(policy="atlas", max_batch=1024, kv_budget=32768),
           "chatbot": dict(policy="plas", max_batch=256, kv_budget=6000),
           "react": dict(policy="plas", max_batch=256, kv_budget=8000)}[args.workload]
-    s = Scheduler(policy=wl["policy"], beta=(2, 1), max_batch=wl["max_batch"], kv_budget=wl["kv_budget"], block_tokens=16,
+    s = Scheduler(policy=wl["policy"], beta=(1, 0) if os.environ.get("AUTX_BENCH_BETA_INF") else (2, 1), max_batch=wl["max_batch"], kv_budget=wl["kv_budget"], block_tokens=16,
                   max_calls=int(args.active * 1.25) + 4096, max_programs=tr.n_programs + 1024,
                   order_mode=ORDER_RADIX if args.order == "radix" else ORDER_SELECT,
                   device=local, stream=stream.cuda_stream, rank=rank, nranks=world, **lad)
@@ -437,8 +437,8 @@ def main():
                          "step_p90": float(np.percentile(ms, 90))},
         "promotions_per_step": statistics.mean(promoted),
         "finalize_phases_us": {n: round(float(np.median([p[b] - p[a] for p in phase])) / 1e3, 2) for n, a, b in (
-            ("load_prev", 0, 9), ("region_b", 9, 10), ("region_a", 10, 1), ("sort", 1, 2), ("cutoff", 2, 3),
-            ("batch_admit", 3, 4), ("preempt", 4, 5), ("kv", 6, 7), ("account", 7, 8))},
+            ("loads", 0, 1), ("cutoff", 2, 3), ("batch_admit", 3, 4), ("preempt", 4, 5), ("kv", 6, 7),
+            ("account_mirror", 7, 8))},
         "complete_phases_us": [round(float(np.median([p[i + 1] - p[i] for p in phase])) / 1e3, 2) for i in range(16, 19)],
         "e2e": {"value": e2e_dec / e2e_s, "unit": "decisions/s", "h2d_bytes_per_step": h2d // e2e_steps,
                 "d2h_bytes_per_step": d2h // e2e_steps, "ms_per_step": e2e_s * 1e3 / e2e_steps,

@@ -24,7 +24,8 @@ def stale():
 def build(force=False, verbose=False):
     if not force and not stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
+    extra = os.environ.get("AUTX_NVCC_FLAGS", "").split()  # e.g. -DAUTX_PHASE_SYNC (profiling)
+    cmd = [NVCC, *FLAGS, *extra, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

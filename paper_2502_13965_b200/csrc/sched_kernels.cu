@@ -28,7 +28,13 @@ __device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc)
   return q;
 }
 
+#ifdef AUTX_PHASE_SYNC
+// profiling build: a barrier that must complete (its result is consumed) before the stamp, so
+// deferred-blocking barriers cannot shift time into the next phase
+#define STAMP(i) do { if (__syncthreads_count(1) && threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
+#else
 #define STAMP(i) do { if (threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
+#endif
 
 // ceil(tokens / block_tokens) (R14, R28): a shift when block_tokens is a power of two
 __device__ __forceinline__ uint32_t blocks_for(const Policy& pol, uint32_t tokens) {
