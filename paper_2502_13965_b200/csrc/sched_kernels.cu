@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
 // (Alg. 1 l.20-23), allocate KV blocks and build the swap plan.
 // ---------------------------------------------------------------------------------------------
 extern __shared__ unsigned char fin_smem[];
-template <int NT>
+template <int NT, int R>
 __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
                               uint32_t t, uint32_t np, uint32_t seqno);
 
@@ -913,10 +913,10 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   if (!last) return;
   __threadfence();
   if (threadIdx.x == 0) ctl->rank_done = 0;
-  finalize_body<RANK_THREADS>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  finalize_body<RANK_THREADS, 4>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
 }
 
-template <int NT>
+template <int NT, int R>
 __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
                               uint32_t t, uint32_t np, uint32_t seqno) {
   uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] sorted keys of the first m candidates
@@ -934,7 +934,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   // ---- (1) the first m = min(BS, ncand) candidates in key order: key + record, plus the
   // previous batch's records (preempt), all in one round of independent loads --------------
   const uint32_t m = min(BS, ncand);
-  constexpr int R = 4;  // items per thread, blocked (i = tid * R + r); BS <= 4096
+  // R items per thread, blocked (i = tid * R + r): NT * R >= BS
   uint32_t c_s[R], c_qf[R], c_tok[R], c_ex[R], c_mt[R], c_qt[R], c_kvb[R];
   uint64_t c_cid[R];
   uint32_t p_s[R], p_qf[R], p_held[R];  // previous batch: slot, flags, held blocks, order key
@@ -1292,12 +1292,12 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   STAMP(8);
 }
 
-template <int NT>
+template <int NT, int R>
 __global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
                                                  bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
   pdl_wait();
   pdl_trigger();
-  finalize_body<NT>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  finalize_body<NT, R>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1387,9 +1387,11 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch * sizeof(uint64_t), fin_smem_bytes);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_finalize<FIN_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_finalize<FIN_THREADS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_finalize<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    e = cudaFuncSetAttribute(k_finalize<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_finalize<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_rank<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
@@ -1404,11 +1406,17 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     // rank + finalize in one launch: the last rank CTA (256 threads = 4 candidates each) finalizes
     launch_pdl(k_rank<true>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
   } else if (pol.max_batch <= 1024) {
+    // 512 threads x 2 candidates: 4 warps per scheduler to hide the phase's latency chains
+    // (1024 threads hit the 64-register cap and spill; 256 threads leave 2 warps per scheduler)
+    static bool fin256 = getenv("AUTX_FIN256") != nullptr;
     launch_pdl(k_rank<false>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
-    launch_pdl(k_finalize<256>, 1, 256, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+    if (fin256)
+      launch_pdl(k_finalize<256, 4>, 1, 256, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+    else
+      launch_pdl(k_finalize<512, 2>, 1, 512, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
   } else {
     launch_pdl(k_rank<false>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
-    launch_pdl(k_finalize<FIN_THREADS>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np,
+    launch_pdl(k_finalize<FIN_THREADS, 4>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np,
                seqno);
   }
   if (ev) cudaEventRecord(ev[3], s);
