@@ -67,7 +67,7 @@ __device__ __forceinline__ void set_err(Ctl* ctl, uint32_t code, uint32_t info) 
 // Applies one chunk of <= NT completion records to the process table (NT = block size).
 template <int NT>
 __device__ void apply_record_chunk(const Policy& pol, ProgTable pt, const CompRec* recs, uint32_t n,
-                                   uint32_t t) {
+                                   uint32_t t, const CompRec* mine = nullptr) {
   __shared__ uint64_t skey[NT];
   __shared__ uint32_t sdummy[NT];
   __shared__ CompRec srec[NT];
@@ -75,7 +75,7 @@ __device__ void apply_record_chunk(const Policy& pol, ProgTable pt, const CompRe
   __shared__ uint32_t red_f[33];
   const uint32_t tid = threadIdx.x;
   bool valid = tid < n;
-  if (valid) srec[tid] = recs[tid];
+  if (valid) srec[tid] = mine ? *mine : recs[tid];  // the caller's own record, if given, skips a load
   skey[tid] = valid ? ((uint64_t)srec[tid].prog << 32 | tid) : ~0ull;
   sdummy[tid] = 0;
   __syncthreads();
@@ -114,23 +114,25 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
     uint32_t i = base + tid;
     bool valid = i < n;
     uint32_t s = valid ? slots[i] : 0;
+    CompRec r{};
+    uint8_t qf0 = QF_DEAD;
     if (valid) {
       uint32_t e = ct.exec[s];
-      CompRec r;
+      qf0 = ct.qf[s];  // loaded with the record fields: one round trip
       r.prog = ct.prog[s];
       r.exec = e;
       r.cp = ct.inh[s] + e;
       r.tw = (t - ct.arr[s]) - e;  // totwait: active steps arr..t-1 that did not run
       rec_out[i] = r;
     }
-    __syncthreads();
     STAMP(17);
-    if (apply) apply_record_chunk<NT>(pol, pt, rec_out + base, min(n - base, (uint32_t)NT), t);
+    if (apply) apply_record_chunk<NT>(pol, pt, rec_out + base, min(n - base, (uint32_t)NT), t, &r);
+    else __syncthreads();
     STAMP(18);
     // release the row and its KV (completed calls ran in step t-1, hence are resident)
     uint32_t nfree = 0, rslot = NONE;
     if (valid) {
-      uint8_t qf = ct.qf[s];
+      uint8_t qf = qf0;
       if (kv_on && (qf & QF_RES)) {
         rslot = ct.loc[s];
         nfree = kv.rs_nblk[rslot];
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
 // only by moving running calls forward within an arrival group.  Per tile: the q* rows of
 // earlier tiles (tile_pre) and the candidate output offset
 //     off(tile) = sum_{k<q*} prefix_k(tile) + min(prefix_{q*}(tile), m').
-constexpr int SEL_THREADS = 1024;
+constexpr int SEL_THREADS = 512;  // one tile per thread up to 512 tiles (1M rows); fewer warps
 template <int NT>
 __device__ void find_boundary(const Policy& pol, const CallTable& ct, Ctl* ctl, uint32_t qs, uint32_t btile,
                               uint32_t bk);
