@@ -409,6 +409,9 @@ def main():
 
     scan_avg_ms = statistics.mean(scan_ms)
     traffic_bytes, traffic_src = ncu_traffic()
+    if args.workload != "mcts" or args.order != "select":
+        # the committed capture is of the default configuration's scan kernel only
+        traffic_bytes, traffic_src = None, "no ncu capture of this configuration"
     achieved = statistics.mean(scan_bytes) / (scan_avg_ms * 1e-3) / 1e9
     result = {
         "metric": "sched decisions/s at 1M active calls", "value": value, "unit": "decisions/s",
@@ -425,7 +428,8 @@ def main():
                    "order": args.order, "l2": "flushed before every step (512 MiB write)" if not args.no_flush else "hot",
                    "parallelism": f"engines{world} (one scheduler per GPU)"},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "k_scan (dense anti-starvation + queue counts)",
+        "roofline": {"bound": "hbm", "kernel": "k_scan_bulk (dense anti-starvation + queue counts)"
+                     if args.order == "select" else "radix order (k_keys + LSD passes + k_take)",
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic_bytes, "traffic_source": traffic_src,
                      "peak_source": peak_src,
