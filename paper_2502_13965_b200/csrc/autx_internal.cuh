@@ -93,6 +93,11 @@ struct Ctl {
   uint32_t host_bump;      // host arena bump pointer (pages)
   uint32_t rank_done;      // last-CTA ticket of k_rank (fused finalize)
   uint32_t host_free_top[32];  // per size class free-stack size
+  // self-selecting gather (default select path): live rows per queue after anti-starvation,
+  // accumulated by the scan's CTAs; slot + 1 of region A's last q* row (0 = none).  Both are
+  // reset by finalize.
+  uint32_t qtot[MAX_K];
+  uint32_t qs_bnd1;
   unsigned long long dbg[32];  // %globaltimer stamps of kernel phases (autx_phase_times)
 };
 

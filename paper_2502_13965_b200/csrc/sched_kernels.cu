@@ -301,9 +301,9 @@ cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, Pro
 __device__ __forceinline__ void hist_add(uint64_t& h, uint32_t q) { h += 1ull << (4 * q); }
 
 // Reduces the 4-bit histograms of a CTA into per-queue counts (written by the first 16 threads to
-// dst[0..16)); wh: [NW][2] shared scratch.
+// dst[0..16) and returned to thread k = queue k); wh: [NW][2] shared scratch.
 template <int NT>
-__device__ __forceinline__ void hist_reduce(uint64_t h, uint64_t (*wh)[2], uint32_t* dst) {
+__device__ __forceinline__ uint32_t hist_reduce(uint64_t h, uint64_t (*wh)[2], uint32_t* dst) {
   constexpr uint64_t M = 0x0F0F0F0F0F0F0F0Full;
   uint64_t lo = warp_sum(h & M), hi = warp_sum((h >> 4) & M);  // 8-bit fields: <= 8 rows x 32 lanes
   if (lane_id() == 0) { wh[warp_id()][0] = lo; wh[warp_id()][1] = hi; }
@@ -314,7 +314,9 @@ __device__ __forceinline__ void hist_reduce(uint64_t h, uint64_t (*wh)[2], uint3
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) sum += (uint32_t)(wh[w][k & 1] >> sh) & 0xffu;
     dst[k] = sum;
+    return sum;
   }
+  return 0;
 }
 
 __device__ __forceinline__ void count_q(uint64_t& c0, uint64_t& c1, uint64_t& c2, uint64_t& c3,
@@ -460,6 +462,7 @@ __device__ __forceinline__ void issue_tile(const CallTable& ct, uint32_t tile, u
 }
 
 extern __shared__ __align__(128) unsigned char scan_smem[];
+enum { SEL_KERNEL = 0, SEL_FUSED = 1, SEL_GATHER = 2 };
 
 constexpr int BULK_THREADS = 512;                 // 16 warps per CTA, 4 rows per thread
 constexpr int BULK_ROWS = TILE / BULK_THREADS;
@@ -469,7 +472,9 @@ __device__ void select_body(const Policy& pol, const CallTable& ct, Ctl* ctl, Ou
 
 __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                                Outputs out, uint32_t t, uint32_t ntiles,
-                                                               bool fuse_select) {
+                                                               int sel_mode) {
+  // sel_mode: SEL_KERNEL = per-tile counts + stats for k_select; SEL_FUSED = the last CTA runs the
+  // selection; SEL_GATHER = per-tile counts + per-queue totals (global atomics) for k_gather_ss
   pdl_wait();
   __shared__ __align__(8) uint64_t bars[SCAN_STAGES];
   __shared__ uint64_t wh[BULK_THREADS / 32][2];
@@ -539,17 +544,23 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
     if (wm) *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
     const uint32_t pl = warp_sum((npromo << 16) | nlive);  // <= 128 each per warp
     if (lane_id() == 0) { wn[warp_id()][0] = pl >> 16; wn[warp_id()][1] = pl & 0xffffu; }
-    hist_reduce<BULK_THREADS>(hq, wh, out.tile_cnt + (size_t)tile * MAX_K);
+    const uint32_t qc = hist_reduce<BULK_THREADS>(hq, wh, out.tile_cnt + (size_t)tile * MAX_K);
+    if (sel_mode == SEL_GATHER && qc) atomicAdd(&ctl->qtot[tid], qc);  // tid < MAX_K
     if (tid == 32) {
       uint32_t a = 0, b = 0;
 #pragma unroll
       for (int w = 0; w < BULK_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
-      out.tile_stat[tile] = make_uint2(a, b);
+      if (sel_mode == SEL_GATHER) {
+        if (a) atomicAdd(&ctl->n_promoted, a);
+        if (b) atomicAdd(&ctl->n_live, b);
+      } else {
+        out.tile_stat[tile] = make_uint2(a, b);
+      }
     }
     __syncthreads();  // wh/wn reuse
   }
   // optionally, the last CTA to finish picks the boundary queue and the tile offsets
-  if (!fuse_select) return;
+  if (sel_mode != SEL_FUSED) return;
   __shared__ bool last;
   __threadfence();
   __syncthreads();
@@ -855,6 +866,174 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
   }
 }
 
+// Self-selecting gather (default): no separate selection kernel.  Every CTA derives q* and m'
+// from the per-queue totals the scan accumulated (ctl->qtot), and a tile CTA derives its own
+// candidate offset from the per-tile counts of the earlier tiles (one round of L2 loads):
+//     off(T) = pre_a(T) + min(pre_q(T), m'),   pre_a = sum_{T'<T} sum_{k<q*} cnt,  pre_q = sum_{T'<T} cnt_q*.
+// Inside the tile, a thread's first candidate position follows from the exclusive counts of
+// earlier threads (A = live rows with q < q*, Q = live rows of q*) without a second scan, since
+// the q* rows are taken in table order:  pos = off + A + min(Q, m' - min(pre_q, m')).
+// The thread taking the m'-th q* row publishes its slot (region A's boundary); the previous-batch
+// CTAs emit keys for every live q* call of the previous batch and k_rank drops those with
+// slot <= boundary (they are in region A).
+__global__ void __launch_bounds__(SCAN_THREADS) k_gather_ss(Policy pol, CallTable ct, Ctl* ctl, Outputs out,
+                                                            uint32_t n_rows, uint32_t ntiles, uint32_t t) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int NT = SCAN_THREADS, NW = NT / 32;
+  __shared__ uint32_t s_qs, s_m;
+  __shared__ unsigned long long s_pref[NW];
+  __shared__ uint32_t s_cnt[NW];
+  const uint32_t tid = threadIdx.x, tile = blockIdx.x;
+  const uint32_t K = pol.K, BS = pol.max_batch;
+  const uint32_t tq = tid < K ? __ldcg(ctl->qtot + tid) : 0u;
+  if (tile >= ntiles) {
+    // previous batch: records (for preempt) and region-B keys
+    const uint32_t j = (tile - ntiles) * NT + tid;
+    const uint32_t n_prev = ctl->n_prev;
+    CandRec r;
+    if (j < n_prev) load_rec(ct, out.prev_slots[j], &r);
+    if (tid < 32) {
+      const uint32_t incl = warp_incl_scan(tq);
+      const uint32_t b = __ballot_sync(0xffffffffu, tid < K && incl >= BS);
+      const uint32_t qs = b ? __ffs(b) - 1 : K;
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (tid == 0) { s_qs = qs; s_m = qs < K ? BS : tot; }  // s_m: n_cand_a here
+    }
+    __syncthreads();
+    if (j < n_prev) {
+      out.prev_rec[j] = r;
+      const bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == s_qs;
+      out.ckey[s_m + j] = b ? cand_key(r, t) : ~0ull;
+    }
+    return;
+  }
+  // (1) independent loads: this tile's qf, the earlier tiles' per-queue counts
+  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  const uint2 qv = row0 < n_rows ? *reinterpret_cast<const uint2*>(ct.qf + row0) : make_uint2(0x40404040u, 0x40404040u);
+  uint32_t acc[MAX_K];
+#pragma unroll
+  for (int k = 0; k < MAX_K; ++k) acc[k] = 0;
+  for (uint32_t tl = tid; tl < tile; tl += 2 * NT) {
+    const uint4* c0 = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)tl * MAX_K);
+    const uint4* c1 = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)(tl + NT) * MAX_K);
+    const bool two = tl + NT < tile;
+    uint4 x[MAX_K / 4], y[MAX_K / 4];
+#pragma unroll
+    for (int v = 0; v < MAX_K / 4; ++v) {
+      x[v] = 4 * v < (int)K ? __ldcg(c0 + v) : make_uint4(0, 0, 0, 0);
+      y[v] = two && 4 * v < (int)K ? __ldcg(c1 + v) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int v = 0; v < MAX_K / 4; ++v) {
+      acc[4 * v] += x[v].x + y[v].x;
+      acc[4 * v + 1] += x[v].y + y[v].y;
+      acc[4 * v + 2] += x[v].z + y[v].z;
+      acc[4 * v + 3] += x[v].w + y[v].w;
+    }
+  }
+  // (2) q*, m' from the totals (warp 0)
+  if (tid < 32) {
+    const uint32_t incl = warp_incl_scan(tq);
+    const uint32_t b = __ballot_sync(0xffffffffu, tid < K && incl >= BS);
+    const uint32_t qs = b ? __ffs(b) - 1 : K;
+    const uint32_t excl = __shfl_sync(0xffffffffu, incl - tq, qs & 31);
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (tid == 0) {
+      s_qs = qs;
+      s_m = qs < K ? BS - excl : 0;
+      if (tile == 0) {
+        ctl->qstar = qs;
+        ctl->mprime = qs < K ? BS - excl : 0;
+        ctl->n_cand_a = qs < K ? BS : tot;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t qs = s_qs, m = s_m;
+  uint32_t qfs[8], na = 0, nq = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
+    const bool live = !(qfs[j] & QF_DEAD);
+    const uint32_t q = qfs[j] & QF_QMASK;
+    na += (live && q < qs) ? 1u : 0u;
+    nq += (live && q == qs) ? 1u : 0u;
+  }
+  uint32_t pa = 0, pq = 0;
+#pragma unroll
+  for (int k = 0; k < MAX_K; ++k) {
+    pa += (uint32_t)k < qs ? acc[k] : 0u;
+    pq += (uint32_t)k == qs ? acc[k] : 0u;
+  }
+  // (3) one combined pass: sum of the earlier tiles' counts, exclusive (A, Q) counts in the tile
+  const unsigned long long pw = warp_sum(((unsigned long long)pa << 32) | pq);
+  const uint32_t v = (na << 16) | nq;  // <= 2048 each
+  const uint32_t vin = warp_incl_scan(v);
+  if (lane_id() == 31) { s_pref[warp_id()] = pw; s_cnt[warp_id()] = vin; }
+  __syncthreads();
+  unsigned long long pref = 0;
+  uint32_t vex = vin - v;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    pref += s_pref[w];
+    vex += (uint32_t)w < warp_id() ? s_cnt[w] : 0u;
+  }
+  const uint32_t pre_a = (uint32_t)(pref >> 32), pre_q = (uint32_t)pref;
+  const uint32_t mq = m - min(pre_q, m);  // q* rows still to take at this tile's start
+  uint32_t rq = pre_q + (vex & 0xffffu);
+  uint32_t pos = pre_a + min(pre_q, m) + (vex >> 16) + min(vex & 0xffffu, mq);
+  uint32_t flags = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t qf = qfs[j];
+    if (qf & QF_DEAD) continue;
+    const uint32_t q = qf & QF_QMASK;
+    bool sel = q < qs;
+    if (q == qs) {
+      sel = rq < m;
+      if (rq + 1 == m) ctl->qs_bnd1 = row0 + j + 1;
+      ++rq;
+    }
+    if (sel) flags |= 1u << j;
+  }
+  if (flags) {
+    const uint4* cidv = reinterpret_cast<const uint4*>(ct.cid + row0);
+    uint4 c4[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) c4[w] = cidv[w];
+    uint4 ar[2], tk[2], ex[2], mt[2], qt[2];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      ar[w] = reinterpret_cast<const uint4*>(ct.arr + row0)[w];
+      tk[w] = reinterpret_cast<const uint4*>(ct.tok + row0)[w];
+      ex[w] = reinterpret_cast<const uint4*>(ct.exec + row0)[w];
+      mt[w] = reinterpret_cast<const uint4*>(ct.mtime + row0)[w];
+      qt[w] = reinterpret_cast<const uint4*>(ct.quanta + row0)[w];
+    }
+    auto lane4 = [](const uint4& a, int k) { return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : a.w; };
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (flags & (1u << j)) {
+        CandRec r;
+        const uint4& cc = c4[j >> 1];
+        r.cid = (j & 1) ? ((uint64_t)cc.w << 32 | cc.z) : ((uint64_t)cc.y << 32 | cc.x);
+        r.slot = row0 + j;
+        r.arr = lane4(ar[j >> 2], j & 3);
+        r.tok = lane4(tk[j >> 2], j & 3);
+        r.exec = lane4(ex[j >> 2], j & 3);
+        r.mtime = lane4(mt[j >> 2], j & 3);
+        r.quanta = lane4(qt[j >> 2], j & 3);
+        r.qf = qfs[j];
+        r._pad = 0;
+        out.cand[pos] = row0 + j;
+        out.cand_rec[pos] = r;
+        out.ckey[pos] = cand_key(r, t);
+        ++pos;
+      }
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // a5/a6/a3/a7-plan: one CTA.  Sort <= 2 BS candidate keys
 //     q:4 | arrival (relative to t):27 | not-running:1 | seq (row):31       (R11, R12)
@@ -882,11 +1061,29 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   pdl_wait();
   pdl_trigger();
   uint64_t* rk = reinterpret_cast<uint64_t*>(fin_smem);
-  const uint32_t n = ctl->n_cand_a + ctl->n_prev;
+  __shared__ uint32_t s_valid;
+  const uint32_t na = ctl->n_cand_a;
+  const uint32_t n = na + ctl->n_prev;
   const uint32_t e0 = blockIdx.x * RANK_PER_CTA;
   if (e0 < n) {
-    for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS) rk[i] = out.ckey[i];
+    // previous-batch keys at or before region A's boundary are region A's already (self-selecting
+    // gather; bnd1 = 0 otherwise); CTA 0 counts the remaining keys for finalize
+    const uint32_t bnd1 = ctl->qs_bnd1;
+    if (threadIdx.x == 0) s_valid = 0;
     __syncthreads();
+    uint32_t nv = 0;
+    for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS) {
+      uint64_t k = out.ckey[i];
+      if (i >= na && (uint32_t)(k & 0x7FFFFFFFu) < bnd1) k = ~0ull;
+      nv += k != ~0ull ? 1u : 0u;
+      rk[i] = k;
+    }
+    if (blockIdx.x == 0) {
+      nv = warp_sum(nv);
+      if (lane_id() == 0 && nv) atomicAdd(&s_valid, nv);
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->n_cand_b = s_valid - na;
     const uint32_t e = e0 + threadIdx.x / RANK_SUB, sub = threadIdx.x % RANK_SUB;
     uint32_t cnt = 0;
     uint64_t x = 0;
@@ -1258,8 +1455,11 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     h.err_info = ctl->err_info;
     ctl->n_promoted = 0;
     ctl->n_live = 0;
+    ctl->qs_bnd1 = 0;
+    ctl->n_cand_b = 0;
     s_hout = h;
   }
+  if (tid < MAX_K) ctl->qtot[tid] = 0;
   // host-visible results: by default the device block (counts + lists) is copied out by one
   // cudaMemcpyAsync after the kernel; the zero-copy variant stores the mirrors over PCIe here
   __syncthreads();
@@ -1365,6 +1565,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     // last-CTA fusion of select into the scan and finalize into the rank kernel: measured slower
     // than the PDL-chained separate kernels (fences vs hidden launch gaps), kept as an option
     static bool fuse = getenv("AUTX_FUSE") != nullptr;
+    // a separate one-CTA selection kernel between the scan and the gather (the previous default)
+    static bool sel_kernel = getenv("AUTX_SELECT_KERNEL") != nullptr;
     if (!scan_ctas) {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -1376,13 +1578,17 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       if (ev) cudaEventRecord(ev[1], s);
       launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     } else {
+      const int mode = fuse ? SEL_FUSED : sel_kernel ? SEL_KERNEL : SEL_GATHER;
       launch_pdl(k_scan_bulk, std::min<uint32_t>(ntiles, scan_ctas), BULK_THREADS,
-                 (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, ctl, out, t, ntiles, fuse);
+                 (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, ctl, out, t, ntiles, mode);
       if (ev) cudaEventRecord(ev[1], s);
-      if (!fuse) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
+      if (mode == SEL_KERNEL) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     }
-    launch_pdl(k_gather, ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS, SCAN_THREADS, 0, s, pol,
-               ct, ctl, out, n_rows, ntiles, t);
+    const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
+    if (simple || fuse || sel_kernel)
+      launch_pdl(k_gather, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t);
+    else
+      launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t);
   }
   uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
   size_t fin_smem_bytes = (size_t)np * (sizeof(uint64_t) + sizeof(uint32_t));
