@@ -55,6 +55,26 @@ def parse():
     return ap.parse_args()
 
 
+def chain_spans(phase):
+    """Median (start, end) in us of each step-chain kernel relative to the first one's start, from
+    a -DAUTX_CHAIN_STAMPS build's stamps (None in a normal build)."""
+    names = ["prologue", "scan", "select", "gather", "rank", "finalize"]
+    rows = []
+    for p in phase:
+        c = [int(x) for x in p[48:60]]
+        starts = [c[2 * k] for k in range(6) if c[2 * k]]
+        if not starts:
+            return None
+        t0 = min(starts)
+        rows.append({n: (c[2 * k] - t0, c[2 * k + 1] - t0) for k, n in enumerate(names) if c[2 * k]})
+    out = {}
+    for n in names:
+        v = [r[n] for r in rows if n in r]
+        if v:
+            out[n] = [round(float(np.median([a for a, _ in v])) / 1e3, 2), round(float(np.median([b for _, b in v])) / 1e3, 2)]
+    return out
+
+
 def ncu_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum per k_scan_bulk launch from the committed
     `ncu --set full` capture summary (profiles/scan_traffic.json), or None."""
@@ -356,10 +376,14 @@ def main():
     from paper_2502_13965_b200.autx import kernel_launches
     ms, decisions = [], 0
     launches0 = kernel_launches()
+    chain_phase = []
+    want_chain = bool(os.environ.get("AUTX_BENCH_CHAIN"))  # with a -DAUTX_CHAIN_STAMPS build
     for _ in range(args.steps):
         dt, rec, nc, na = timed_step()
         ms.append(dt)
         decisions += rec["n_active"]
+        if want_chain:
+            chain_phase.append(s.phase_times().astype(np.int64))
     launches = kernel_launches() - launches0  # counted by the library at every launch
     torch.cuda.synchronize()
     if world > 1:
@@ -440,6 +464,7 @@ def main():
                          "step_p10": float(np.percentile(ms, 10)), "step_p50": float(np.percentile(ms, 50)),
                          "step_p90": float(np.percentile(ms, 90))},
         "promotions_per_step": statistics.mean(promoted),
+        "chain_us": chain_spans(chain_phase) if chain_phase else None,
         "finalize_phases_us": {n: round(float(np.median([p[b] - p[a] for p in phase])) / 1e3, 2) for n, a, b in (
             ("loads", 0, 1), ("cutoff", 2, 3), ("batch_admit", 3, 4), ("preempt", 4, 5), ("kv", 6, 7),
             ("account_mirror", 7, 8))},

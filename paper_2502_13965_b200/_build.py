@@ -13,8 +13,17 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v"]
 
 
+def _extra():
+    return os.environ.get("AUTX_NVCC_FLAGS", "").split()  # e.g. -DAUTX_PHASE_SYNC (profiling)
+
+
 def stale():
     if not os.path.exists(LIB):
+        return True
+    try:
+        if open(LIB + ".flags").read() != " ".join(_extra()):  # built with other extra flags
+            return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.abspath(__file__)]
@@ -24,7 +33,7 @@ def stale():
 def build(force=False, verbose=False):
     if not force and not stale():
         return LIB
-    extra = os.environ.get("AUTX_NVCC_FLAGS", "").split()  # e.g. -DAUTX_PHASE_SYNC (profiling)
+    extra = _extra()
     cmd = [NVCC, *FLAGS, *extra, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -33,6 +42,8 @@ def build(force=False, verbose=False):
     if verbose:
         sys.stderr.write(r.stderr)
     os.replace(LIB + ".tmp", LIB)
+    with open(LIB + ".flags", "w") as f:
+        f.write(" ".join(extra))
     return LIB
 
 

@@ -172,6 +172,8 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&o.sidx, 2 * BS));
   CK(dalloc(&o.srec, 2 * BS));
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K)); CK(dalloc(&o.tile_off, ntiles + 1));
+  CK(dalloc(&o.sup_cnt, (ntiles / SUP_TILES + 1) * MAX_K));
+  CK(cudaMemset(o.sup_cnt, 0, (ntiles / SUP_TILES + 1) * MAX_K * sizeof(uint32_t)));
   CK(dalloc(&o.tile_pre, ntiles + 1));
   CK(dalloc(&o.tile_stat, ntiles + 1));
   o.hout = reinterpret_cast<HostOut*>(ctx->h_outblk);
@@ -312,7 +314,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
                  t.loc, t.hcls, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp,
                  ctx->ctl, ctx->out.batch_slots, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
-                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.tile_off,
+                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->out.tile_off,
                  ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
@@ -1014,6 +1016,6 @@ extern "C" autx_status autx_phase_times(autx_ctx* ctx, uint64_t* ns, uint32_t ca
   CK(cudaStreamSynchronize(ctx->stream));
   Ctl c;
   CK(cudaMemcpy(&c, ctx->ctl, sizeof c, cudaMemcpyDeviceToHost));
-  memcpy(ns, c.dbg, std::min<uint32_t>(cap, 32) * 8);
+  memcpy(ns, c.dbg, std::min<uint32_t>(cap, 64) * 8);
   return AUTX_OK;
 }

@@ -15,6 +15,8 @@ constexpr uint8_t QF_INB = 0x80;    // scratch: member of the batch being formed
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr int MAX_K = 16;
+constexpr int QP_LINES = 16;
+constexpr int SUP_TILES = 16;  // tiles per super-tile (the gather's two-level prefix)
 constexpr int SCAN_THREADS = 256;
 constexpr int ROWS_PER_THREAD = 8;
 constexpr int TILE = SCAN_THREADS * ROWS_PER_THREAD;  // rows per scan tile (2048)
@@ -93,12 +95,13 @@ struct Ctl {
   uint32_t host_bump;      // host arena bump pointer (pages)
   uint32_t rank_done;      // last-CTA ticket of k_rank (fused finalize)
   uint32_t host_free_top[32];  // per size class free-stack size
-  // self-selecting gather (default select path): live rows per queue after anti-starvation,
-  // accumulated by the scan's CTAs; slot + 1 of region A's last q* row (0 = none).  Both are
-  // reset by finalize.
-  uint32_t qtot[MAX_K];
+  // self-selecting gather (default select path): slot + 1 of region A's last q* row (0 = none),
+  // and the scan's partial totals, spread over QP_LINES 128-B lines (scan CTA b adds into line
+  // b % QP_LINES: same-address reductions serialise at L2): [0, MAX_K) live rows per queue after
+  // anti-starvation, [MAX_K] promotions, [MAX_K + 1] live rows.  Reset by finalize.
   uint32_t qs_bnd1;
-  unsigned long long dbg[32];  // %globaltimer stamps of kernel phases (autx_phase_times)
+  alignas(128) uint32_t qpart[QP_LINES][32];
+  unsigned long long dbg[64];  // [32, 44) live chain stamps, [48, 60) last step's (AUTX_CHAIN_STAMPS)  // %globaltimer stamps of kernel phases (autx_phase_times)
 };
 
 // Host-visible step output written by the finalize kernel into mapped pinned memory.
@@ -181,6 +184,9 @@ struct Outputs {
   uint32_t* sidx;            // [2 BS] element index of each sorted key
   CandRec* srec;             // [2 BS] candidate records in sorted order
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
+  uint32_t* sup_cnt;         // [ceil(ntiles_cap / SUP_TILES) * MAX_K] per-queue counts of super-tiles
+                             // (scan: atomics; gather: prefix; finalize: reset)
+  uint32_t n_sup;            // super-tiles in use this step (set per launch; finalize resets them)
   uint32_t* tile_off;        // [ntiles_cap+1] candidate offsets
   uint32_t* tile_pre;        // [ntiles_cap] q* rows in earlier tiles
   uint2* tile_stat;          // [ntiles_cap] (promotions, live rows) per tile

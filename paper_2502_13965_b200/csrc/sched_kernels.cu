@@ -1,13 +1,17 @@
-// sm_100a kernels of one Autellix scheduling step.
+// sm_100a kernels of one Autellix scheduling step.  Default chain,
+// PDL-linked on one stream:
 //
-//   k_complete   (a1)  completion records -> process table, warp-shuffle segmented reduce
-//   k_register   (a2)  arrivals appended to the call table, inherit service, placed in a queue
-//   k_scan       (a4)  dense pass over every call: anti-starvation (integer cross-multiply)
-//                      + per-tile per-queue counts; the last CTA picks the boundary queue q*
-//   k_gather     (a5)  emits the candidate set (<= BS rows of the lowest queues, table order)
-//   k_finalize   (a5, a6, a3, a7 plan)  sorts candidates by the unique key, prefix cutoff on
-//                      BS and the KV budget, admit/preempt lists, step accounting and eager
-//                      demotion, GPU block allocation and the swap plan
+//   k_prologue   (a1, a2)  completion records -> process table (commutative reductions), rows
+//                          released; arrivals appended, inherit service, placed in a queue
+//   k_scan_bulk  (a4)      dense TMA-staged pass over every call: anti-starvation (integer
+//                          cross-multiply) + per-tile / per-super-tile queue counts
+//   k_gather_ss  (a5)      q*, m' and each tile's candidate offset from the counts; emits the
+//                          candidate set (<= BS rows of the lowest queues, table order) and the
+//                          previous batch's records and region-B keys
+//   k_rank       (a5)      multi-CTA rank counting of the <= 2 BS unique keys
+//   k_finalize   (a5, a6, a3, a7 plan)  prefix cutoff on BS and the KV budget, admit/preempt
+//                          lists, step accounting and eager demotion, GPU block allocation and
+//                          the swap plan, host mirrors
 //
 // Every step of Alg. 1 runs here; the host only stages records.  Citations: see autx.h.
 #include <algorithm>
@@ -36,6 +40,16 @@ __device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc)
 #define STAMP(i) do { if (threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
 #endif
 
+// profiling build (-DAUTX_CHAIN_STAMPS): per kernel of the step chain, %globaltimer when CTA 0
+// passes griddepcontrol.wait and the latest CTA end; finalize moves them to dbg[48, 60)
+#ifdef AUTX_CHAIN_STAMPS
+#define CHAIN_BEGIN(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[32 + 2 * (k)] = globaltimer(); } while (0)
+#define CHAIN_END(k) do { if (threadIdx.x == 0) atomicMax(&ctl->dbg[33 + 2 * (k)], globaltimer()); } while (0)
+#else
+#define CHAIN_BEGIN(k) do { } while (0)
+#define CHAIN_END(k) do { } while (0)
+#endif
+
 // ceil(tokens / block_tokens) (R14, R28): a shift when block_tokens is a power of two
 __device__ __forceinline__ uint32_t blocks_for(const Policy& pol, uint32_t tokens) {
   return pol.bt_shift != 0xFFu ? (tokens + pol.block_tokens - 1) >> pol.bt_shift
@@ -61,47 +75,16 @@ __device__ __forceinline__ void set_err(Ctl* ctl, uint32_t code, uint32_t info) 
 // a1: UPDATE_PROCESS_TABLE (Alg. 1 l.1-7) for the calls that finished in step t-1.
 //   PLAS (Eq. 1): svc[p] += sum exec;  ATLAS (l.4): svc[p] = max(svc[p], max(inh + exec));
 //   pwait[p] += sum totwait (R5), totwait(c) = (t - arr) - exec (active steps not running).
-// Records are sorted by program in shared memory; a warp-shuffle segmented scan reduces each
-// program's run and the segment tail writes the row: one write per program, deterministic.
+// Each record updates its program's row with one reduction per field (PLAS: add, ATLAS: max;
+// pwait: add).  Integer sums and maxima commute, so the row is the same whatever order the records
+// arrive in (deterministic), and fire-and-forget reductions put no round trip on the step's path.
 // ---------------------------------------------------------------------------------------------
-// Applies one chunk of <= NT completion records to the process table (NT = block size).
-template <int NT>
-__device__ void apply_record_chunk(const Policy& pol, ProgTable pt, const CompRec* recs, uint32_t n,
-                                   uint32_t t, const CompRec* mine = nullptr) {
-  __shared__ uint64_t skey[NT];
-  __shared__ uint32_t sdummy[NT];
-  __shared__ CompRec srec[NT];
-  __shared__ uint64_t red_v[33];
-  __shared__ uint32_t red_f[33];
-  const uint32_t tid = threadIdx.x;
-  bool valid = tid < n;
-  if (valid) srec[tid] = mine ? *mine : recs[tid];  // the caller's own record, if given, skips a load
-  skey[tid] = valid ? ((uint64_t)srec[tid].prog << 32 | tid) : ~0ull;
-  sdummy[tid] = 0;
-  __syncthreads();
-  uint32_t np = 2;
-  while (np < n) np <<= 1;
-  bitonic_sort_pairs<NT>(skey, sdummy, min(np, (uint32_t)NT));
-  uint64_t k = skey[tid];
-  bool v2 = k != ~0ull;
-  uint32_t o = (uint32_t)k, pp = (uint32_t)(k >> 32);
-  bool head = tid == 0 || (skey[tid - 1] >> 32) != pp;
-  bool tail = tid == NT - 1 || skey[tid + 1] == ~0ull || (skey[tid + 1] >> 32) != pp;
-  uint64_t ex = v2 ? srec[o].exec : 0, tw = v2 ? srec[o].tw : 0, cp = v2 ? srec[o].cp : 0;
-  uint64_t sum_ex = block_seg_scan<uint64_t, NT>(ex, head, OpSum(), red_v, red_f);
-  uint64_t sum_tw = block_seg_scan<uint64_t, NT>(tw, head, OpSum(), red_v, red_f);
-  uint64_t max_cp = block_seg_scan<uint64_t, NT>(cp, head, OpMax(), red_v, red_f);
-  if (v2 && tail) {
-    PInfo pi = pt.info[pp];
-    if (pol.policy == AUTX_ATLAS)
-      pi.svc = max_cp > pi.svc ? (uint32_t)max_cp : pi.svc;  // Alg. 1 l.4
-    else
-      pi.svc += (uint32_t)sum_ex;                            // Eq. 1
-    pi.pwait += sum_tw;                                      // Alg. 1 l.5-6, R5
-    pt.info[pp] = pi;
-    pt.last_comp[pp] = t;
-  }
-  __syncthreads();
+__device__ __forceinline__ void apply_record(const Policy& pol, ProgTable pt, const CompRec& r, uint32_t t) {
+  PInfo* pi = pt.info + r.prog;
+  if (pol.policy == AUTX_ATLAS) atomicMax(&pi->svc, r.cp);  // Alg. 1 l.4
+  else atomicAdd(&pi->svc, r.exec);                          // Eq. 1
+  if (r.tw) atomicAdd(&pi->pwait, (unsigned long long)r.tw);  // Alg. 1 l.5-6, R5
+  pt.last_comp[r.prog] = t;
 }
 
 template <int NT>
@@ -126,8 +109,7 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       rec_out[i] = r;
     }
     STAMP(17);
-    if (apply) apply_record_chunk<NT>(pol, pt, rec_out + base, min(n - base, (uint32_t)NT), t, &r);
-    else __syncthreads();
+    if (apply && valid) apply_record(pol, pt, r, t);
     STAMP(18);
     // release the row and its KV (completed calls ran in step t-1, hence are resident)
     uint32_t nfree = 0, rslot = NONE;
@@ -181,9 +163,8 @@ __global__ void __launch_bounds__(FIN_THREADS) k_apply(Policy pol, ProgTable pt,
   for (uint32_t r = 0; r < G; ++r) {
     const RouteHdr* h = reinterpret_cast<const RouteHdr*>(base + r * stride);
     const CompRec* recs = reinterpret_cast<const CompRec*>(h + 1);
-    uint32_t n = h->n_comp;
-    for (uint32_t b = 0; b < n; b += FIN_THREADS)
-      apply_record_chunk<FIN_THREADS>(pol, pt, recs + b, min(n - b, (uint32_t)FIN_THREADS), t);
+    const uint32_t n = h->n_comp;
+    for (uint32_t i = threadIdx.x; i < n; i += FIN_THREADS) apply_record(pol, pt, recs[i], t);
   }
 }
 
@@ -229,7 +210,7 @@ __device__ __forceinline__ void register_one(const Policy& pol, CallTable& ct, P
     pt.info[p] = PInfo{0, 0, 0ull};
     pt.last_comp[p] = NONE;
   }
-  uint32_t inh = (r.flags & 1u) ? 0u : pt.info[p].svc;  // Alg. 1 l.11
+  uint32_t inh = (r.flags & 1u) ? 0u : __ldcg(&pt.info[p].svc);  // Alg. 1 l.11 (L2: see k_prologue)
   pt.last_arr[p] = t;
   uint32_t q = place_queue(pol, inh);             // Alg. 1 l.12
   ct.cid[s] = r.cid;
@@ -270,13 +251,18 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
     for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) s_arr[i] = a.arr[i];
   pdl_wait();
   pdl_trigger();
+  CHAIN_BEGIN(0);
   __syncthreads();
   if (a.n_comp)
     complete_body<PRO_THREADS>(pol, ct, pt, ctl, comp_inline ? s_comp : a.comp_ptr, a.n_comp, a.t, kv, kv_on,
                                rec_out, true);
-  __syncthreads();  // arrivals inherit the service updated by this step's completions (R10)
+  // arrivals inherit the service updated by this step's completions (R10): the reductions are
+  // performed at L2 before the barrier releases (fence), and register_one reads svc from L2
+  if (a.n_comp && a.n_arr) __threadfence();
+  __syncthreads();
   const ArrivalRec* arr = arr_inline ? s_arr : a.arr_ptr;
   for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) register_one(pol, ct, pt, arr[i], a.first_slot + i, a.t);
+  CHAIN_END(0);
 }
 
 cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl, KvState kv,
@@ -305,8 +291,15 @@ __device__ __forceinline__ void hist_add(uint64_t& h, uint32_t q) { h += 1ull <<
 template <int NT>
 __device__ __forceinline__ uint32_t hist_reduce(uint64_t h, uint64_t (*wh)[2], uint32_t* dst) {
   constexpr uint64_t M = 0x0F0F0F0F0F0F0F0Full;
-  uint64_t lo = warp_sum(h & M), hi = warp_sum((h >> 4) & M);  // 8-bit fields: <= 8 rows x 32 lanes
-  if (lane_id() == 0) { wh[warp_id()][0] = lo; wh[warp_id()][1] = hi; }
+  // even / odd queues in 8-bit fields (<= 8 rows x 32 lanes = 256 would overflow: callers keep
+  // <= 7 rows per thread), each 32-bit half summed over the warp by one redux.sync
+  const uint64_t e = h & M, o = (h >> 4) & M;
+  const uint32_t e0 = __reduce_add_sync(0xffffffffu, (uint32_t)e), e1 = __reduce_add_sync(0xffffffffu, (uint32_t)(e >> 32));
+  const uint32_t o0 = __reduce_add_sync(0xffffffffu, (uint32_t)o), o1 = __reduce_add_sync(0xffffffffu, (uint32_t)(o >> 32));
+  if (lane_id() == 0) {
+    wh[warp_id()][0] = (uint64_t)e1 << 32 | e0;
+    wh[warp_id()][1] = (uint64_t)o1 << 32 | o0;
+  }
   __syncthreads();
   if (threadIdx.x < MAX_K) {
     const uint32_t k = threadIdx.x, sh = 8 * (k >> 1);
@@ -470,12 +463,13 @@ constexpr int BULK_ROWS = TILE / BULK_THREADS;
 template <int NT>
 __device__ void select_body(const Policy& pol, const CallTable& ct, Ctl* ctl, Outputs& out, uint32_t ntiles);
 
+template <int sel_mode>
 __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                               Outputs out, uint32_t t, uint32_t ntiles,
-                                                               int sel_mode) {
+                                                               Outputs out, uint32_t t, uint32_t ntiles) {
   // sel_mode: SEL_KERNEL = per-tile counts + stats for k_select; SEL_FUSED = the last CTA runs the
   // selection; SEL_GATHER = per-tile counts + per-queue totals (global atomics) for k_gather_ss
   pdl_wait();
+  CHAIN_BEGIN(1);
   __shared__ __align__(8) uint64_t bars[SCAN_STAGES];
   __shared__ uint64_t wh[BULK_THREADS / 32][2];
   __shared__ uint32_t wn[BULK_THREADS / 32][2];
@@ -492,6 +486,7 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
     }
   pdl_trigger();
   const bool anti = pol.beta_den != 0;
+  const uint32_t bnum = pol.beta_num, bden = pol.beta_den, quanta0 = pol.quanta[0];
   uint32_t it = 0;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const uint32_t stage = it % SCAN_STAGES;
@@ -517,50 +512,60 @@ __global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallT
 #pragma unroll
       for (int j = 0; j < 4; ++j) pi[j] = !(qfs[j] & QF_DEAD) ? pt.info[prog[j]] : PInfo{0, 0, 0ull};
     }
+    // per row, branch-free except the rare wide-arithmetic path of the starvation test
     uint64_t hq = 0;
     uint32_t npromo = 0, nlive = 0;
     bool wq = false, wb = false, wm = false;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      uint32_t qf = qfs[j];
-      if (qf & QF_DEAD) continue;
-      ++nlive;
+      const uint32_t qf = qfs[j];
+      const bool live = !(qf & QF_DEAD);
       uint32_t q = qf & QF_QMASK;
+      bool pr = false;
       if (anti) {
-        if (starving(pol, pi[j], t - base[j] - mtim[j], mtim[j])) {  // Alg. 1 l.26
-          if (q != 0 || mtim[j] != 0) ct.quanta[row0 + j] = pol.quanta[0];
-          if (q != 0) { qfs[j] = qf & ~QF_QMASK; wq = true; }
-          if (mtim[j] != 0) { mtim[j] = 0; wm = true; }
-          base[j] = t;
-          wb = true;
-          q = 0;
-          ++npromo;
-        }
+        const uint32_t wait = t - base[j] - mtim[j];
+        const uint32_t W32 = (uint32_t)pi[j].pwait + wait, T32 = pi[j].svc + mtim[j];
+        const bool fast = (uint32_t)(pi[j].pwait >> 32) == 0 && W32 >= wait && T32 >= pi[j].svc;
+        bool st = (W32 | T32) != 0 && (uint64_t)W32 * bden >= (uint64_t)T32 * bnum;
+        if (!fast) st = starving(pol, pi[j], wait, mtim[j]);
+        pr = live && st;  // Alg. 1 l.26
       }
-      hist_add(hq, q);
+      if (pr && (q | mtim[j])) ct.quanta[row0 + j] = quanta0;
+      wq |= pr && q != 0;
+      wm |= pr && mtim[j] != 0;
+      wb |= pr;
+      qfs[j] = pr ? (qf & ~(uint32_t)QF_QMASK) : qf;
+      mtim[j] = pr ? 0u : mtim[j];
+      base[j] = pr ? t : base[j];
+      q = pr ? 0u : q;
+      npromo += pr ? 1u : 0u;
+      nlive += live ? 1u : 0u;
+      hq += live ? (1ull << (4 * q)) : 0ull;
     }
     if (wq) *reinterpret_cast<uint32_t*>(ct.qf + row0) = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
     if (wb) *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
     if (wm) *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
-    const uint32_t pl = warp_sum((npromo << 16) | nlive);  // <= 128 each per warp
+    const uint32_t pl = __reduce_add_sync(0xffffffffu, (npromo << 16) | nlive);  // <= 128 each per warp
     if (lane_id() == 0) { wn[warp_id()][0] = pl >> 16; wn[warp_id()][1] = pl & 0xffffu; }
     const uint32_t qc = hist_reduce<BULK_THREADS>(hq, wh, out.tile_cnt + (size_t)tile * MAX_K);
-    if (sel_mode == SEL_GATHER && qc) atomicAdd(&ctl->qtot[tid], qc);  // tid < MAX_K
+    uint32_t* qp = ctl->qpart[blockIdx.x % QP_LINES];
+    if (sel_mode == SEL_GATHER && qc) atomicAdd(out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, qc);  // tid < MAX_K
     if (tid == 32) {
       uint32_t a = 0, b = 0;
 #pragma unroll
       for (int w = 0; w < BULK_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
       if (sel_mode == SEL_GATHER) {
-        if (a) atomicAdd(&ctl->n_promoted, a);
-        if (b) atomicAdd(&ctl->n_live, b);
+        if (a) atomicAdd(qp + MAX_K, a);
+        if (b) atomicAdd(qp + MAX_K + 1, b);
       } else {
         out.tile_stat[tile] = make_uint2(a, b);
       }
     }
     __syncthreads();  // wh/wn reuse
   }
+  CHAIN_END(1);
   // optionally, the last CTA to finish picks the boundary queue and the tile offsets
-  if (sel_mode != SEL_FUSED) return;
+  if constexpr (sel_mode != SEL_FUSED) return;
   __shared__ bool last;
   __threadfence();
   __syncthreads();
@@ -772,7 +777,9 @@ __device__ void find_boundary(const Policy& pol, const CallTable& ct, Ctl* ctl, 
 __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, CallTable ct, Ctl* ctl, Outputs out, uint32_t ntiles) {
   pdl_wait();
   pdl_trigger();
+  CHAIN_BEGIN(2);
   select_body<SEL_THREADS>(pol, ct, ctl, out, ntiles);
+  CHAIN_END(2);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -780,11 +787,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, CallTable ct
 // candidate (q < q*, or among the first m' rows of q*) in table order.  CTAs past the last tile
 // write the records of the previous batch (the resident set) for preempt/region B.
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable ct, Ctl* ctl,
-                                                         Outputs out, uint32_t n_rows, uint32_t ntiles,
-                                                         uint32_t t) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void gather_body(Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, uint32_t n_rows, uint32_t ntiles, uint32_t t) {
   const uint32_t tile = blockIdx.x;
   if (tile >= ntiles) {
     // previous batch: records (for preempt) and, for its live calls of q*, keys (region B;
@@ -866,9 +869,21 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
   }
 }
 
+__global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable ct, Ctl* ctl, Outputs out,
+                                                         uint32_t n_rows, uint32_t ntiles, uint32_t t) {
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(3);
+  gather_body(pol, ct, ctl, out, n_rows, ntiles, t);
+  CHAIN_END(3);
+}
+
 // Self-selecting gather (default): no separate selection kernel.  Every CTA derives q* and m'
-// from the per-queue totals the scan accumulated (ctl->qtot), and a tile CTA derives its own
-// candidate offset from the per-tile counts of the earlier tiles (one round of L2 loads):
+// from the per-queue totals, and a tile CTA its candidate offset from the counts of the earlier
+// tiles, both from a two-level table the scan fills: per-tile counts (tile_cnt) and per-super-tile
+// counts (sup_cnt, SUP_TILES tiles each, accumulated with atomics).  The prefix of tile T is the
+// super-tiles before T's plus the <= SUP_TILES - 1 tiles of T's super-tile before T: one round of
+// a few loads per thread (half-warp h, lane k = queue k).
 //     off(T) = pre_a(T) + min(pre_q(T), m'),   pre_a = sum_{T'<T} sum_{k<q*} cnt,  pre_q = sum_{T'<T} cnt_q*.
 // Inside the tile, a thread's first candidate position follows from the exclusive counts of
 // earlier threads (A = live rows with q < q*, Q = live rows of q*) without a second scan, since
@@ -876,24 +891,52 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
 // The thread taking the m'-th q* row publishes its slot (region A's boundary); the previous-batch
 // CTAs emit keys for every live q* call of the previous batch and k_rank drops those with
 // slot <= boundary (they are in region A).
-__global__ void __launch_bounds__(SCAN_THREADS) k_gather_ss(Policy pol, CallTable ct, Ctl* ctl, Outputs out,
-                                                            uint32_t n_rows, uint32_t ntiles, uint32_t t) {
-  pdl_wait();
-  pdl_trigger();
-  constexpr int NT = SCAN_THREADS, NW = NT / 32;
-  __shared__ uint32_t s_qs, s_m;
-  __shared__ unsigned long long s_pref[NW];
+__device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, uint32_t n_rows, uint32_t ntiles, uint32_t t) {
+  constexpr int NT = SCAN_THREADS, NW = NT / 32, NH = NT / MAX_K;  // NH half-warps of MAX_K lanes
+  __shared__ uint32_t s_tot[NH][MAX_K], s_pre[NH][MAX_K];
+  __shared__ uint32_t s_qs, s_m, s_prea, s_preq;
   __shared__ uint32_t s_cnt[NW];
   const uint32_t tid = threadIdx.x, tile = blockIdx.x;
   const uint32_t K = pol.K, BS = pol.max_batch;
-  const uint32_t tq = tid < K ? __ldcg(ctl->qtot + tid) : 0u;
-  if (tile >= ntiles) {
+  const bool is_tile = tile < ntiles;
+  // (1) one round of independent loads
+  {
+    const uint32_t h = tid / MAX_K, k = tid % MAX_K;
+    const uint32_t nsup = (ntiles + SUP_TILES - 1) / SUP_TILES, my_sup = tile / SUP_TILES;
+    uint32_t tot = 0, pre = 0;
+    if (k < K) {
+      for (uint32_t S = h; S < nsup; S += NH) {
+        const uint32_t v = __ldcg(out.sup_cnt + S * MAX_K + k);
+        tot += v;
+        pre += (is_tile && S < my_sup) ? v : 0u;
+      }
+      const uint32_t tr = my_sup * SUP_TILES + h;  // earlier tile of the same super-tile
+      if (is_tile && tr < tile) pre += __ldcg(out.tile_cnt + (size_t)tr * MAX_K + k);
+    }
+    s_tot[h][k] = tot;
+    s_pre[h][k] = pre;
+    if (tile == 0 && tid < 32) {
+      // promotions (even lanes) and live rows (odd lanes) for finalize's host record
+      uint32_t stat = tid < 2 * QP_LINES ? __ldcg(&ctl->qpart[tid >> 1][MAX_K + (tid & 1)]) : 0u;
+#pragma unroll
+      for (int d = 2; d < 32; d <<= 1) stat += __shfl_xor_sync(0xffffffffu, stat, d);
+      if (tid == 0) ctl->n_promoted = stat;
+      if (tid == 1) ctl->n_live = stat;
+    }
+  }
+  if (!is_tile) {
     // previous batch: records (for preempt) and region-B keys
     const uint32_t j = (tile - ntiles) * NT + tid;
     const uint32_t n_prev = ctl->n_prev;
     CandRec r;
     if (j < n_prev) load_rec(ct, out.prev_slots[j], &r);
+    __syncthreads();
     if (tid < 32) {
+      uint32_t tq = 0;
+      if (tid < MAX_K) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) tq += s_tot[h][tid];
+      }
       const uint32_t incl = warp_incl_scan(tq);
       const uint32_t b = __ballot_sync(0xffffffffu, tid < K && incl >= BS);
       const uint32_t qs = b ? __ffs(b) - 1 : K;
@@ -908,43 +951,32 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather_ss(Policy pol, CallTabl
     }
     return;
   }
-  // (1) independent loads: this tile's qf, the earlier tiles' per-queue counts
   const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
   const uint2 qv = row0 < n_rows ? *reinterpret_cast<const uint2*>(ct.qf + row0) : make_uint2(0x40404040u, 0x40404040u);
-  uint32_t acc[MAX_K];
-#pragma unroll
-  for (int k = 0; k < MAX_K; ++k) acc[k] = 0;
-  for (uint32_t tl = tid; tl < tile; tl += 2 * NT) {
-    const uint4* c0 = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)tl * MAX_K);
-    const uint4* c1 = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)(tl + NT) * MAX_K);
-    const bool two = tl + NT < tile;
-    uint4 x[MAX_K / 4], y[MAX_K / 4];
-#pragma unroll
-    for (int v = 0; v < MAX_K / 4; ++v) {
-      x[v] = 4 * v < (int)K ? __ldcg(c0 + v) : make_uint4(0, 0, 0, 0);
-      y[v] = two && 4 * v < (int)K ? __ldcg(c1 + v) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int v = 0; v < MAX_K / 4; ++v) {
-      acc[4 * v] += x[v].x + y[v].x;
-      acc[4 * v + 1] += x[v].y + y[v].y;
-      acc[4 * v + 2] += x[v].z + y[v].z;
-      acc[4 * v + 3] += x[v].w + y[v].w;
-    }
-  }
-  // (2) q*, m' from the totals (warp 0)
+  __syncthreads();
+  // (2) q*, m', and this tile's prefix (warp 0, lane k = queue k)
   if (tid < 32) {
+    uint32_t tq = 0, pk = 0;
+    if (tid < MAX_K) {
+#pragma unroll
+      for (int h = 0; h < NH; ++h) { tq += s_tot[h][tid]; pk += s_pre[h][tid]; }
+    }
     const uint32_t incl = warp_incl_scan(tq);
     const uint32_t b = __ballot_sync(0xffffffffu, tid < K && incl >= BS);
     const uint32_t qs = b ? __ffs(b) - 1 : K;
     const uint32_t excl = __shfl_sync(0xffffffffu, incl - tq, qs & 31);
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t pa = warp_sum(tid < qs ? pk : 0u);
+    const uint32_t pq = __shfl_sync(0xffffffffu, pk, qs & 31);
     if (tid == 0) {
+      const uint32_t m = qs < K ? BS - excl : 0;
       s_qs = qs;
-      s_m = qs < K ? BS - excl : 0;
+      s_m = m;
+      s_prea = pa;
+      s_preq = qs < K ? pq : 0;
       if (tile == 0) {
         ctl->qstar = qs;
-        ctl->mprime = qs < K ? BS - excl : 0;
+        ctl->mprime = m;
         ctl->n_cand_a = qs < K ? BS : tot;
       }
     }
@@ -960,26 +992,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather_ss(Policy pol, CallTabl
     na += (live && q < qs) ? 1u : 0u;
     nq += (live && q == qs) ? 1u : 0u;
   }
-  uint32_t pa = 0, pq = 0;
-#pragma unroll
-  for (int k = 0; k < MAX_K; ++k) {
-    pa += (uint32_t)k < qs ? acc[k] : 0u;
-    pq += (uint32_t)k == qs ? acc[k] : 0u;
-  }
-  // (3) one combined pass: sum of the earlier tiles' counts, exclusive (A, Q) counts in the tile
-  const unsigned long long pw = warp_sum(((unsigned long long)pa << 32) | pq);
+  // (3) exclusive (A, Q) counts of the earlier threads of this tile
   const uint32_t v = (na << 16) | nq;  // <= 2048 each
   const uint32_t vin = warp_incl_scan(v);
-  if (lane_id() == 31) { s_pref[warp_id()] = pw; s_cnt[warp_id()] = vin; }
+  if (lane_id() == 31) s_cnt[warp_id()] = vin;
   __syncthreads();
-  unsigned long long pref = 0;
   uint32_t vex = vin - v;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    pref += s_pref[w];
-    vex += (uint32_t)w < warp_id() ? s_cnt[w] : 0u;
-  }
-  const uint32_t pre_a = (uint32_t)(pref >> 32), pre_q = (uint32_t)pref;
+  for (int w = 0; w < NW; ++w) vex += (uint32_t)w < warp_id() ? s_cnt[w] : 0u;
+  const uint32_t pre_a = s_prea, pre_q = s_preq;
   const uint32_t mq = m - min(pre_q, m);  // q* rows still to take at this tile's start
   uint32_t rq = pre_q + (vex & 0xffffu);
   uint32_t pos = pre_a + min(pre_q, m) + (vex >> 16) + min(vex & 0xffffu, mq);
@@ -1034,6 +1055,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather_ss(Policy pol, CallTabl
   }
 }
 
+__global__ void __launch_bounds__(SCAN_THREADS, 4) k_gather_ss(Policy pol, CallTable ct, Ctl* ctl, Outputs out,
+                                                               uint32_t n_rows, uint32_t ntiles, uint32_t t) {
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(3);
+  gather_ss_body(pol, ct, ctl, out, n_rows, ntiles, t);
+  CHAIN_END(3);
+}
+
 // ---------------------------------------------------------------------------------------------
 // a5/a6/a3/a7-plan: one CTA.  Sort <= 2 BS candidate keys
 //     q:4 | arrival (relative to t):27 | not-running:1 | seq (row):31       (R11, R12)
@@ -1060,6 +1090,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
                                                        bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
   pdl_wait();
   pdl_trigger();
+  CHAIN_BEGIN(4);
   uint64_t* rk = reinterpret_cast<uint64_t*>(fin_smem);
   __shared__ uint32_t s_valid;
   const uint32_t na = ctl->n_cand_a;
@@ -1102,6 +1133,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
       if (x != ~0ull) out.srec[cnt] = e < ctl->n_cand_a ? out.cand_rec[e] : out.prev_rec[e - ctl->n_cand_a];
     }
   }
+  CHAIN_END(4);
   if (!FUSED) return;
   // the last CTA to finish runs finalize on the sorted keys (saves a dependent launch)
   __shared__ bool last;
@@ -1119,9 +1151,13 @@ template <int NT, int R>
 __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
                               uint32_t t, uint32_t np, uint32_t seqno) {
   uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] sorted keys of the first m candidates
+  // admit / preempt id lists staged in shared memory for the host mirrors (16-B aligned)
+  uint64_t* s_ad = uk + np;
+  uint64_t* s_pr = s_ad + ((pol.max_batch + 1) & ~1u);
   __shared__ unsigned long long red64[33];
   __shared__ uint32_t red[33];
   __shared__ uint32_t s_nbatch;
+  __shared__ unsigned long long s_kvsum;
   __shared__ HostOut s_hout;
   const uint32_t tid = threadIdx.x;
   const uint32_t BS = pol.max_batch;
@@ -1188,13 +1224,16 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   unsigned long long kv_pre = block_excl_scan<unsigned long long, NT>(my_kv, red64, nullptr);
   // Alg. 1 l.34-37: take while count <= BS and sum kvb <= P; kvb >= 1 makes the prefix sums
   // strictly increasing, so the fitting items are exactly a prefix: n_batch = max fitting i + 1
+  unsigned long long c_incl[R];  // inclusive kvb prefix at each item
   {
     unsigned long long incl = kv_pre;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       uint32_t i = tid * R + r;
+      c_incl[r] = 0;
       if (i < m) {
         incl += c_kvb[r];
+        c_incl[r] = incl;
         if (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget) atomicMax(&s_nbatch, i + 1);
       }
     }
@@ -1206,14 +1245,15 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u) ctl->err_info = (uint32_t)(uk[0] & 0x7FFFFFFF);
   }
   // ---- (4) batch list and admit = batch calls not resident (batch order) -------------------
-  unsigned long long my_ad = 0, kv_mine = 0;
+  unsigned long long my_ad = 0;
+  if (n_batch == 0 && tid == 0) s_kvsum = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t i = tid * R + r;
+    if (i + 1 == n_batch) s_kvsum = c_incl[r];  // sum kvb over the batch (read after the scans below)
     if (i < n_batch) {
       out.batch_slots[i] = c_s[r];
       out.batch_ids[i] = c_cid[r];
-      kv_mine += c_kvb[r];
       if (!(c_qf[r] & QF_RES)) {
         uint64_t held = c_ex[r] > 0 ? blocks_for(pol, c_tok[r] + c_ex[r]) : 0;  // R28
         my_ad += (1ull << 44) | held;
@@ -1229,6 +1269,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       uint32_t i = tid * R + r;
       if (i < n_batch && !(c_qf[r] & QF_RES)) {
         out.admit_ids[pos] = c_cid[r];
+        s_ad[pos] = c_cid[r];
         out.admit_slots[pos] = c_s[r];
         ++pos;
       }
@@ -1273,6 +1314,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     for (int r = 0; r < R; ++r)
       if (is_pre & (1u << r)) {
         out.preempt_ids[pos] = p_cid[r];
+        s_pr[pos] = p_cid[r];
         out.preempt_slots[pos] = p_s[r];
         ct.qf[p_s[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
         ++pos;
@@ -1280,7 +1322,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   }
   const uint32_t n_preempt = (uint32_t)(pre_tot >> 44);
   const unsigned long long swap_out = pre_tot & ((1ull << 44) - 1);
-  const unsigned long long kv_sum = block_sum<unsigned long long, NT>(kv_mine, red64);
+  const unsigned long long kv_sum = s_kvsum;
   STAMP(5);
   STAMP(6);
 
@@ -1459,7 +1501,8 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     ctl->n_cand_b = 0;
     s_hout = h;
   }
-  if (tid < MAX_K) ctl->qtot[tid] = 0;
+  for (uint32_t i = tid; i < QP_LINES * 32; i += NT) (&ctl->qpart[0][0])[i] = 0;
+  for (uint32_t i = tid; i < out.n_sup * MAX_K; i += NT) out.sup_cnt[i] = 0;
   // host-visible results: by default the device block (counts + lists) is copied out by one
   // cudaMemcpyAsync after the kernel; the zero-copy variant stores the mirrors over PCIe here
   __syncthreads();
@@ -1467,26 +1510,21 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     if (tid == 0) *out.d_hout = s_hout;
   } else {
     const uint32_t nb = s_hout.n_batch, na = s_hout.n_admit, np_ = s_hout.n_preempt;
-    // loads of all three lists first (independent), then the PCIe stores
-    constexpr int MR = 8;  // 16-B words per thread per list; BS <= 4096 with 256+ threads
-    uint4 vb[MR], va[MR], vp[MR];
-    const uint4* __restrict__ sb = reinterpret_cast<const uint4*>(out.batch_ids);
-    const uint4* __restrict__ sa = reinterpret_cast<const uint4*>(out.admit_ids);
-    const uint4* __restrict__ sp = reinterpret_cast<const uint4*>(out.preempt_ids);
+    // 16-B posted stores over PCIe: batch ids straight from registers (a thread's R blocked
+    // items are R/2 consecutive words), admit/preempt ids from their shared-memory copies
+    static_assert(R % 2 == 0, "blocked items pair into 16-B words");
 #pragma unroll
-    for (int k = 0; k < MR; ++k) {
-      const uint32_t i = tid + k * NT;
-      if (i < (nb + 1) / 2) vb[k] = __ldcg(sb + i);
-      if (i < (na + 1) / 2) va[k] = __ldcg(sa + i);
-      if (i < (np_ + 1) / 2) vp[k] = __ldcg(sp + i);
+    for (int k = 0; k < R / 2; ++k) {
+      const uint32_t i = tid * (R / 2) + k;
+      if (i < (nb + 1) / 2)
+        reinterpret_cast<uint4*>(out.h_batch)[i] =
+            make_uint4((uint32_t)c_cid[2 * k], (uint32_t)(c_cid[2 * k] >> 32), (uint32_t)c_cid[2 * k + 1],
+                       (uint32_t)(c_cid[2 * k + 1] >> 32));
     }
-#pragma unroll
-    for (int k = 0; k < MR; ++k) {
-      const uint32_t i = tid + k * NT;
-      if (i < (nb + 1) / 2) reinterpret_cast<uint4*>(out.h_batch)[i] = vb[k];
-      if (i < (na + 1) / 2) reinterpret_cast<uint4*>(out.h_admit)[i] = va[k];
-      if (i < (np_ + 1) / 2) reinterpret_cast<uint4*>(out.h_preempt)[i] = vp[k];
-    }
+    const uint4* sa = reinterpret_cast<const uint4*>(s_ad);
+    const uint4* sp = reinterpret_cast<const uint4*>(s_pr);
+    for (uint32_t i = tid; i < (na + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_admit)[i] = sa[i];
+    for (uint32_t i = tid; i < (np_ + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_preempt)[i] = sp[i];
     __syncthreads();
     // the host reads after the stream event that follows this kernel, which orders every store
     if (tid == 0) *out.hout = s_hout;
@@ -1499,7 +1537,15 @@ __global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* 
                                                  bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
   pdl_wait();
   pdl_trigger();
+  CHAIN_BEGIN(5);
   finalize_body<NT, R>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+#ifdef AUTX_CHAIN_STAMPS
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->dbg[43] = globaltimer();
+    for (int i = 0; i < 12; ++i) { ctl->dbg[48 + i] = ctl->dbg[32 + i]; ctl->dbg[32 + i] = 0; }
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1552,6 +1598,7 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
                         uint32_t* radix_passes) {
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
+  out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
   if (ev) cudaEventRecord(ev[0], s);
   if (rx) {
     static int sms = 0;
@@ -1571,7 +1618,9 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
       scan_ctas = 2 * sms;
-      cudaFuncSetAttribute(k_scan_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
+      cudaFuncSetAttribute(k_scan_bulk<SEL_KERNEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
+      cudaFuncSetAttribute(k_scan_bulk<SEL_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
+      cudaFuncSetAttribute(k_scan_bulk<SEL_GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
     }
     if (simple) {
       launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, out, t, n_rows);
@@ -1579,8 +1628,11 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     } else {
       const int mode = fuse ? SEL_FUSED : sel_kernel ? SEL_KERNEL : SEL_GATHER;
-      launch_pdl(k_scan_bulk, std::min<uint32_t>(ntiles, scan_ctas), BULK_THREADS,
-                 (size_t)SCAN_STAGES * STAGE_BYTES, s, pol, ct, pt, ctl, out, t, ntiles, mode);
+      const uint32_t sgrid = std::min<uint32_t>(ntiles, scan_ctas);
+      const size_t ssmem = (size_t)SCAN_STAGES * STAGE_BYTES;
+      if (mode == SEL_GATHER) launch_pdl(k_scan_bulk<SEL_GATHER>, sgrid, BULK_THREADS, ssmem, s, pol, ct, pt, ctl, out, t, ntiles);
+      else if (mode == SEL_FUSED) launch_pdl(k_scan_bulk<SEL_FUSED>, sgrid, BULK_THREADS, ssmem, s, pol, ct, pt, ctl, out, t, ntiles);
+      else launch_pdl(k_scan_bulk<SEL_KERNEL>, sgrid, BULK_THREADS, ssmem, s, pol, ct, pt, ctl, out, t, ntiles);
       if (ev) cudaEventRecord(ev[1], s);
       if (mode == SEL_KERNEL) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     }
@@ -1591,7 +1643,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t);
   }
   uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
-  size_t fin_smem_bytes = (size_t)np * (sizeof(uint64_t) + sizeof(uint32_t));
+  // sorted keys [np] + admit and preempt id staging [2 x even(BS)]
+  size_t fin_smem_bytes = ((size_t)np + 2 * ((pol.max_batch + 1) & ~1u)) * sizeof(uint64_t);
   size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch * sizeof(uint64_t), fin_smem_bytes);
   static bool attr_set = false;
   if (!attr_set) {
