@@ -61,17 +61,19 @@ def chain_spans(phase):
     names = ["prologue", "scan", "select", "gather", "rank", "finalize"]
     rows = []
     for p in phase:
-        c = [int(x) for x in p[48:60]]
-        starts = [c[2 * k] for k in range(6) if c[2 * k]]
+        c = [int(x) for x in p[64:96]]
+        starts = [c[3 * k] for k in range(6) if c[3 * k]]
         if not starts:
             return None
         t0 = min(starts)
-        rows.append({n: (c[2 * k] - t0, c[2 * k + 1] - t0) for k, n in enumerate(names) if c[2 * k]})
+        rows.append({n: (c[3 * k] - t0, c[3 * k + 1] - t0, c[3 * k + 2] - t0) for k, n in enumerate(names) if c[3 * k]})
+        rows[-1]["rank_keys"] = (c[20], c[21], 0)
     out = {}
-    for n in names:
+    for n in names + ["rank_keys"]:
         v = [r[n] for r in rows if n in r]
         if v:
-            out[n] = [round(float(np.median([a for a, _ in v])) / 1e3, 2), round(float(np.median([b for _, b in v])) / 1e3, 2)]
+            div = 1 if n == "rank_keys" else 1e3
+            out[n] = [round(float(np.median([x[i] for x in v])) / div, 2) for i in range(2 if n == "rank_keys" else 3)]
     return out
 
 

@@ -198,9 +198,9 @@ autx_status autx_set_timing(autx_ctx* ctx, int32_t on);
 uint32_t autx_num_active(const autx_ctx* ctx);
 /* %globaltimer stamps (ns) recorded inside the kernels of the last step, for profiling:
  * [0..8] k_finalize phases, [16..19] k_complete phases, and in a -DAUTX_CHAIN_STAMPS build
- * [48 + 2k, 48 + 2k + 1] = (CTA 0 past griddepcontrol.wait, latest CTA end) of chain kernel k
- * (0 prologue, 1 scan, 2 select, 3 gather, 4 rank, 5 finalize; 0 = did not run); copies
- * min(cap, 64). */
+ * [64 + 3k, 64 + 3k + 2] = (CTA 0 past griddepcontrol.wait, latest CTA end, latest CTA past the
+ * wait) of chain kernel k (0 prologue, 1 scan, 2 select, 3 gather, 4 rank, 5 finalize; 0 = did
+ * not run), [84, 85] = (ranked keys, key slots) of k_rank; copies min(cap, 96). */
 autx_status autx_phase_times(autx_ctx* ctx, uint64_t* ns, uint32_t cap);
 /* Number of kernels this library has launched so far (all contexts of the process). */
 uint64_t autx_kernel_launches(void);

@@ -278,8 +278,8 @@ class Scheduler:
         return t
 
     def phase_times(self):
-        a = np.zeros(64, np.uint64)
-        self._check(self.lib.autx_phase_times(self.ctx, _ptr(a), 64))
+        a = np.zeros(96, np.uint64)
+        self._check(self.lib.autx_phase_times(self.ctx, _ptr(a), 96))
         return a
 
     def num_active(self):

@@ -101,7 +101,7 @@ struct Ctl {
   // anti-starvation, [MAX_K] promotions, [MAX_K + 1] live rows.  Reset by finalize.
   uint32_t qs_bnd1;
   alignas(128) uint32_t qpart[QP_LINES][32];
-  unsigned long long dbg[64];  // [32, 44) live chain stamps, [48, 60) last step's (AUTX_CHAIN_STAMPS)  // %globaltimer stamps of kernel phases (autx_phase_times)
+  unsigned long long dbg[96];  // [32, 64) live chain stamps, [64, 96) last step's (AUTX_CHAIN_STAMPS)  // %globaltimer stamps of kernel phases (autx_phase_times)
 };
 
 // Host-visible step output written by the finalize kernel into mapped pinned memory.
@@ -287,7 +287,7 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev /* 5 events or null */,
                         const RadixState* rx /* non-null: AUTX_ORDER_RADIX */, uint32_t arr_base,
-                        uint32_t* radix_passes);
+                        uint32_t* radix_passes, uint32_t pre_rows = 0);
 cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                Outputs out, RadixState rx, uint32_t t, uint32_t n_rows,
                                uint32_t arr_base, int sms, uint32_t* passes_out);

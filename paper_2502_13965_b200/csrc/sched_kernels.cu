@@ -40,11 +40,13 @@ __device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc)
 #define STAMP(i) do { if (threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
 #endif
 
-// profiling build (-DAUTX_CHAIN_STAMPS): per kernel of the step chain, %globaltimer when CTA 0
-// passes griddepcontrol.wait and the latest CTA end; finalize moves them to dbg[48, 60)
+// profiling build (-DAUTX_CHAIN_STAMPS): per kernel k of the step chain, %globaltimer when CTA 0
+// passes griddepcontrol.wait (dbg[32 + 3k]), the latest CTA end (33 + 3k) and the latest CTA
+// start past the wait (34 + 3k); finalize moves dbg[32, 64) to dbg[64, 96) at the step's end
 #ifdef AUTX_CHAIN_STAMPS
-#define CHAIN_BEGIN(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[32 + 2 * (k)] = globaltimer(); } while (0)
-#define CHAIN_END(k) do { if (threadIdx.x == 0) atomicMax(&ctl->dbg[33 + 2 * (k)], globaltimer()); } while (0)
+#define CHAIN_BEGIN(k) do { if (threadIdx.x == 0) { const unsigned long long g_ = globaltimer(); \
+    if (blockIdx.x == 0) ctl->dbg[32 + 3 * (k)] = g_; atomicMax(&ctl->dbg[34 + 3 * (k)], g_); } } while (0)
+#define CHAIN_END(k) do { if (threadIdx.x == 0) atomicMax(&ctl->dbg[33 + 3 * (k)], globaltimer()); } while (0)
 #else
 #define CHAIN_BEGIN(k) do { } while (0)
 #define CHAIN_END(k) do { } while (0)
@@ -415,6 +417,147 @@ __global__ void __launch_bounds__(SCAN_THREADS, 3) k_scan(Policy pol, CallTable 
   }
 }
 
+enum { SEL_KERNEL = 0, SEL_FUSED = 1, SEL_GATHER = 2 };
+// One-tile-per-CTA variant of the dense pass sized for one wave: 256 threads x 8 rows, <= 64
+// registers so that 4 CTAs fit per SM (592 tiles = 1.2M rows resident at once).  Every row's
+// program-row gather is issued in one round (no per-tile serialisation as in the persistent
+// kernel), which is what bounds this latency-bound pass.  Per-row arithmetic is identical.
+template <int sel_mode>
+__global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                                                               Outputs out, uint32_t t, uint32_t n_rows,
+                                                               uint32_t pre_rows) {
+  constexpr int NW = SCAN_THREADS / 32;
+  __shared__ uint32_t wq16[NW][MAX_K / 2];  // per warp: 16-bit counts of queues 2w, 2w + 1
+  __shared__ uint32_t wn[NW];
+  const uint32_t tid = threadIdx.x, tile = blockIdx.x;
+  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  // prog, base and mtime of rows that existed before this step's prologue are not written by it
+  // (completions only mark rows dead; arrivals append): when the prologue precedes this kernel
+  // (pre_rows > 0), load them before griddepcontrol.wait, overlapping the prologue.  qf and the
+  // program rows (which the prologue does change) are read after the wait.
+  const bool early = row0 + ROWS_PER_THREAD <= pre_rows;
+  uint4 p0, p1, b0, b1, m0, m1;
+  if (early) {
+    p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+    p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+    b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+    m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+    m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ct.qf + row0));
+  }
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(1);
+  uint64_t hq = 0;
+  uint32_t npromo = 0, nlive = 0;
+  if (row0 < n_rows) {
+    const uint2 qv = __ldcs(reinterpret_cast<const uint2*>(ct.qf + row0));
+    if (!early) {
+      p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+      p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+      b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+      b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+      m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+      m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+    }
+    uint32_t qfs[8], prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
+    const bool anti = pol.beta_den != 0;
+    const uint32_t bnum = pol.beta_num, bden = pol.beta_den, quanta0 = pol.quanta[0];
+    // the program rows of all 8 rows in one round (svc and pwait only: 12 of the 16 bytes)
+    uint32_t svc[8];
+    unsigned long long pw[8];
+    if (anti) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool live = !(qfs[j] & QF_DEAD);
+        svc[j] = live ? __ldg(&pt.info[prog[j]].svc) : 0u;
+        pw[j] = live ? __ldg(&pt.info[prog[j]].pwait) : 0ull;
+      }
+    }
+    bool wq = false, wb = false, wm = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t qf = qfs[j];
+      const bool live = !(qf & QF_DEAD);
+      uint32_t q = qf & QF_QMASK;
+      bool pr = false;
+      if (anti) {
+        const uint32_t wait = t - base[j] - mtim[j];
+        const uint32_t W32 = (uint32_t)pw[j] + wait, T32 = svc[j] + mtim[j];
+        const bool fast = (uint32_t)(pw[j] >> 32) == 0 && W32 >= wait && T32 >= svc[j];
+        bool st = (W32 | T32) != 0 && (uint64_t)W32 * bden >= (uint64_t)T32 * bnum;
+        if (!fast) st = starving(pol, PInfo{svc[j], 0, pw[j]}, wait, mtim[j]);
+        pr = live && st;  // Alg. 1 l.26
+      }
+      if (pr && (q | mtim[j])) ct.quanta[row0 + j] = quanta0;
+      wq |= pr && q != 0;
+      wm |= pr && mtim[j] != 0;
+      wb |= pr;
+      qfs[j] = pr ? (qf & ~(uint32_t)QF_QMASK) : qf;
+      mtim[j] = pr ? 0u : mtim[j];
+      base[j] = pr ? t : base[j];
+      q = pr ? 0u : q;
+      npromo += pr ? 1u : 0u;
+      nlive += live ? 1u : 0u;
+      hq += live ? (1ull << (4 * q)) : 0ull;
+    }
+    if (wq) {
+      uint2 qn;
+      qn.x = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
+      qn.y = qfs[4] | (qfs[5] << 8) | (qfs[6] << 16) | (qfs[7] << 24);
+      *reinterpret_cast<uint2*>(ct.qf + row0) = qn;
+    }
+    if (wb) {
+      *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
+      *reinterpret_cast<uint4*>(ct.base + row0 + 4) = make_uint4(base[4], base[5], base[6], base[7]);
+    }
+    if (wm) {
+      *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
+      *reinterpret_cast<uint4*>(ct.mtime + row0 + 4) = make_uint4(mtim[4], mtim[5], mtim[6], mtim[7]);
+    }
+  }
+  // per-queue counts: the 4-bit per-thread fields widened to 16 bits (<= 256 per warp), two
+  // queues per word, one redux.sync per word of the K queues in use
+  const uint32_t K = pol.K;
+#pragma unroll
+  for (int w = 0; w < MAX_K / 2; ++w) {
+    if ((uint32_t)(2 * w) < K) {
+      const uint32_t f = (uint32_t)(hq >> (8 * w));
+      const uint32_t v = __reduce_add_sync(0xffffffffu, (f & 0xFu) | ((f & 0xF0u) << 12));
+      if (lane_id() == 0) wq16[warp_id()][w] = v;
+    }
+  }
+  const uint32_t pl = __reduce_add_sync(0xffffffffu, (npromo << 16) | nlive);  // <= 256 each per warp
+  if (lane_id() == 0) wn[warp_id()] = pl;
+  __syncthreads();
+  if (tid < MAX_K) {
+    uint32_t c = 0;
+    if (tid < K) {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) c += (wq16[w][tid >> 1] >> (16 * (tid & 1))) & 0xFFFFu;
+    }
+    out.tile_cnt[(size_t)tile * MAX_K + tid] = c;
+    if (sel_mode == SEL_GATHER && c) atomicAdd(out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, c);
+  } else if (tid == 32) {
+    uint32_t a = 0, b = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) { a += wn[w] >> 16; b += wn[w] & 0xFFFFu; }
+    if (sel_mode == SEL_GATHER) {
+      uint32_t* qp = ctl->qpart[blockIdx.x % QP_LINES];
+      if (a) atomicAdd(qp + MAX_K, a);
+      if (b) atomicAdd(qp + MAX_K + 1, b);
+    } else {
+      out.tile_stat[tile] = make_uint2(a, b);
+    }
+  }
+  CHAIN_END(1);
+}
+
 // Persistent, TMA-staged variant of the dense pass (the default): each CTA walks tiles
 // blockIdx.x, +gridDim.x, ...; one thread keeps SCAN_STAGES tiles in flight with
 // cp.async.bulk (global -> shared, completion counted on an mbarrier), so HBM keeps streaming
@@ -455,7 +598,6 @@ __device__ __forceinline__ void issue_tile(const CallTable& ct, uint32_t tile, u
 }
 
 extern __shared__ __align__(128) unsigned char scan_smem[];
-enum { SEL_KERNEL = 0, SEL_FUSED = 1, SEL_GATHER = 2 };
 
 constexpr int BULK_THREADS = 512;                 // 16 warps per CTA, 4 rows per thread
 constexpr int BULK_ROWS = TILE / BULK_THREADS;
@@ -792,33 +934,36 @@ __device__ __forceinline__ void gather_body(Policy& pol, CallTable& ct, Ctl* ctl
   if (tile >= ntiles) {
     // previous batch: records (for preempt) and, for its live calls of q*, keys (region B;
     // duplicates of region A are removed after the sort); other entries get the ~0 sentinel
-    uint32_t j = (tile - ntiles) * SCAN_THREADS + threadIdx.x;
-    if (j < ctl->n_prev) {
+    // (the slot load covers the buffer's capacity so that it does not wait for n_prev; k_rank
+    // counts the keys that remain)
+    const uint32_t j = (tile - ntiles) * SCAN_THREADS + threadIdx.x;
+    const uint32_t n_prev = ctl->n_prev, bnd = ctl->qs_boundary, qs = ctl->qstar, na = ctl->n_cand_a;
+    const uint32_t sl = j < pol.max_batch ? out.prev_slots[j] : 0u;
+    if (j < n_prev) {
       CandRec r;
-      load_rec(ct, out.prev_slots[j], &r);
+      load_rec(ct, sl, &r);
       out.prev_rec[j] = r;
       // region B: live calls of q* that region A (q* rows with slot <= boundary) does not hold
-      const uint32_t bnd = ctl->qs_boundary;
-      bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == ctl->qstar && (bnd == NONE || r.slot > bnd);
-      out.ckey[ctl->n_cand_a + j] = b ? cand_key(r, t) : ~0ull;
-      if (b) atomicAdd(&ctl->n_cand_b, 1u);
+      bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == qs && (bnd == NONE || r.slot > bnd);
+      out.ckey[na + j] = b ? cand_key(r, t) : ~0ull;
     }
     return;
   }
+  // every load of this phase in one round, before the early exit of tiles without candidates
   const uint32_t off = out.tile_off[tile];
   const uint32_t cnt = out.tile_off[tile + 1] - off;
-  if (cnt == 0) return;
-  __shared__ uint32_t red[33];
-  const uint32_t qs = ctl->qstar, m = ctl->mprime;
+  const uint32_t qs = ctl->qstar, m = ctl->mprime, pre_tile = out.tile_pre[tile];
   const uint32_t row0 = tile * TILE + threadIdx.x * ROWS_PER_THREAD;
   uint2 qv = row0 < n_rows ? *reinterpret_cast<const uint2*>(ct.qf + row0) : make_uint2(0x40404040u, 0x40404040u);
+  if (cnt == 0) return;
+  __shared__ uint32_t red[33];
   uint32_t qfs[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
   uint32_t nq = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) nq += (!(qfs[j] & QF_DEAD) && (qfs[j] & QF_QMASK) == qs) ? 1u : 0u;
-  uint32_t rq = out.tile_pre[tile] + block_excl_scan<uint32_t, SCAN_THREADS>(nq, red, nullptr);
+  uint32_t rq = pre_tile + block_excl_scan<uint32_t, SCAN_THREADS>(nq, red, nullptr);
   uint32_t flags = 0, nsel = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -894,7 +1039,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable c
 __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, uint32_t n_rows, uint32_t ntiles, uint32_t t) {
   constexpr int NT = SCAN_THREADS, NW = NT / 32, NH = NT / MAX_K;  // NH half-warps of MAX_K lanes
   __shared__ uint32_t s_tot[NH][MAX_K], s_pre[NH][MAX_K];
-  __shared__ uint32_t s_qs, s_m, s_prea, s_preq;
+  __shared__ uint32_t s_qs, s_m, s_prea, s_preq, s_has;
+  __shared__ uint32_t s_own[MAX_K];
   __shared__ uint32_t s_cnt[NW];
   const uint32_t tid = threadIdx.x, tile = blockIdx.x;
   const uint32_t K = pol.K, BS = pol.max_batch;
@@ -910,8 +1056,12 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
         tot += v;
         pre += (is_tile && S < my_sup) ? v : 0u;
       }
-      const uint32_t tr = my_sup * SUP_TILES + h;  // earlier tile of the same super-tile
-      if (is_tile && tr < tile) pre += __ldcg(out.tile_cnt + (size_t)tr * MAX_K + k);
+      const uint32_t tr = my_sup * SUP_TILES + h;  // earlier tile of the same super-tile, or this one
+      if (is_tile && tr <= tile) {
+        const uint32_t c = __ldcg(out.tile_cnt + (size_t)tr * MAX_K + k);
+        if (tr < tile) pre += c;
+        else s_own[k] = c;
+      }
     }
     s_tot[h][k] = tot;
     s_pre[h][k] = pre;
@@ -968,12 +1118,17 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
     const uint32_t pa = warp_sum(tid < qs ? pk : 0u);
     const uint32_t pq = __shfl_sync(0xffffffffu, pk, qs & 31);
+    // this tile's own live rows below q* and of q*: no candidate unless one of them is taken
+    const uint32_t own = tid < K ? s_own[tid] : 0u;
+    const uint32_t oa = warp_sum(tid < qs ? own : 0u);
+    const uint32_t oq = __shfl_sync(0xffffffffu, own, qs & 31);
     if (tid == 0) {
       const uint32_t m = qs < K ? BS - excl : 0;
       s_qs = qs;
       s_m = m;
       s_prea = pa;
       s_preq = qs < K ? pq : 0;
+      s_has = oa > 0 || (qs < K && oq > 0 && pq < m);
       if (tile == 0) {
         ctl->qstar = qs;
         ctl->mprime = m;
@@ -982,6 +1137,9 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
     }
   }
   __syncthreads();
+  // tiles without candidates leave now (their SM slots go to the next kernel's CTAs); the
+  // boundary row is always in a tile with candidates
+  if (!s_has) return;
   const uint32_t qs = s_qs, m = s_m;
   uint32_t qfs[8], na = 0, nq = 0;
 #pragma unroll
@@ -1083,7 +1241,7 @@ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 
 // k_rank: the candidates' sort.  A single SM needs ~35k cycles to sort 2048 64-bit keys with
 // any block sort (measured: scripts/micro/sort_bench.cu), so the order is computed across many
 // SMs instead: every CTA holds all n <= 2 BS keys in shared memory and each key's output index is
-// the number of keys before it ((key, element) is unique), 8 threads per key.
+// the number of keys before it (the keys are unique), RANK_SUB threads per key.
 constexpr int RANK_THREADS = 256, RANK_SUB = 16, RANK_PER_CTA = RANK_THREADS / RANK_SUB;
 template <bool FUSED>
 __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
@@ -1091,46 +1249,71 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   pdl_wait();
   pdl_trigger();
   CHAIN_BEGIN(4);
-  uint64_t* rk = reinterpret_cast<uint64_t*>(fin_smem);
-  __shared__ uint32_t s_valid;
+  __shared__ uint32_t red_r[33];
   const uint32_t na = ctl->n_cand_a;
   const uint32_t n = na + ctl->n_prev;
+  uint64_t* rk = reinterpret_cast<uint64_t*>(fin_smem);  // [n] keys, ~0 = no candidate
+  uint64_t* ck = rk + n;                                 // [n_valid] the candidates' keys
+  uint32_t* ci = reinterpret_cast<uint32_t*>(ck + n);    // [n_valid] their element index
   const uint32_t e0 = blockIdx.x * RANK_PER_CTA;
-  if (e0 < n) {
-    // previous-batch keys at or before region A's boundary are region A's already (self-selecting
-    // gather; bnd1 = 0 otherwise); CTA 0 counts the remaining keys for finalize
-    const uint32_t bnd1 = ctl->qs_bnd1;
-    if (threadIdx.x == 0) s_valid = 0;
-    __syncthreads();
-    uint32_t nv = 0;
-    for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS) {
-      uint64_t k = out.ckey[i];
-      if (i >= na && (uint32_t)(k & 0x7FFFFFFFu) < bnd1) k = ~0ull;
-      nv += k != ~0ull ? 1u : 0u;
-      rk[i] = k;
+  const uint32_t bnd1 = ctl->qs_bnd1;
+  // (1) keys into shared memory; previous-batch keys at or before region A's boundary are region
+  // A's already (self-selecting gather; bnd1 = 0 otherwise) and become sentinels.  The key loads
+  // cover the buffer's capacity, so they need not wait for the counts above (one round trip).
+  constexpr int RK = 8;
+  const uint32_t cap = 2 * pol.max_batch;
+  uint32_t nv = 0;
+  for (uint32_t c0 = 0; c0 < cap; c0 += RK * RANK_THREADS) {
+    uint64_t kk[RK];
+#pragma unroll
+    for (int r = 0; r < RK; ++r) {
+      const uint32_t i = c0 + r * RANK_THREADS + threadIdx.x;
+      kk[r] = i < cap ? __ldcg(out.ckey + i) : ~0ull;
     }
-    if (blockIdx.x == 0) {
-      nv = warp_sum(nv);
-      if (lane_id() == 0 && nv) atomicAdd(&s_valid, nv);
-    }
-    __syncthreads();
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->n_cand_b = s_valid - na;
-    const uint32_t e = e0 + threadIdx.x / RANK_SUB, sub = threadIdx.x % RANK_SUB;
-    uint32_t cnt = 0;
-    uint64_t x = 0;
-    if (e < n) {
-      x = rk[e];
-      for (uint32_t j = sub; j < n; j += RANK_SUB) {
-        uint64_t y = rk[j];
-        cnt += (y < x || (y == x && j < e)) ? 1u : 0u;
+#pragma unroll
+    for (int r = 0; r < RK; ++r) {
+      const uint32_t i = c0 + r * RANK_THREADS + threadIdx.x;
+      if (i < n) {
+        uint64_t k = kk[r];
+        if (i >= na && (uint32_t)(k & 0x7FFFFFFFu) < bnd1) k = ~0ull;
+        nv += k != ~0ull ? 1u : 0u;
+        rk[i] = k;
       }
+    }
+  }
+  if (e0 < n) {
+    // (2) compact the candidates (same deterministic order in every CTA): sentinels rank last and
+    // nobody reads them, so only the n_valid candidates are ranked and compared against
+    uint32_t n_valid;
+    uint32_t off = block_excl_scan<uint32_t, RANK_THREADS>(nv, red_r, &n_valid);
+    for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS)
+      if (rk[i] != ~0ull) { ck[off] = rk[i]; ci[off] = i; ++off; }
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctl->n_cand_b = n_valid - na;
+#ifdef AUTX_CHAIN_STAMPS
+      ctl->dbg[52] = n_valid;
+      ctl->dbg[53] = n;
+#endif
+    }
+    // (3) rank = number of smaller keys (keys are unique), RANK_SUB threads per key; the record
+    // load is issued before the count so that its latency hides behind it
+    const uint32_t e = e0 + threadIdx.x / RANK_SUB, sub = threadIdx.x % RANK_SUB;
+    uint32_t cnt = 0, eo = 0;
+    uint64_t x = 0;
+    CandRec rec;
+    if (e < n_valid) {
+      x = ck[e];
+      eo = ci[e];
+      if (sub == 0) rec = eo < na ? out.cand_rec[eo] : out.prev_rec[eo - na];
+      for (uint32_t j = sub; j < n_valid; j += RANK_SUB) cnt += ck[j] < x ? 1u : 0u;
     }
 #pragma unroll
     for (int d = 1; d < RANK_SUB; d <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-    if (sub == 0 && e < n) {
+    if (sub == 0 && e < n_valid) {
       out.skey[cnt] = x;
-      out.sidx[cnt] = e;
-      if (x != ~0ull) out.srec[cnt] = e < ctl->n_cand_a ? out.cand_rec[e] : out.prev_rec[e - ctl->n_cand_a];
+      out.sidx[cnt] = eo;
+      out.srec[cnt] = rec;
     }
   }
   CHAIN_END(4);
@@ -1164,6 +1347,9 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   const uint32_t n_prev = ctl->n_prev;
   // region A + region B (previous-batch calls of q* not in A): no duplicates, ~0 sentinels last
   const uint32_t ncand = ctl->n_cand_a + ctl->n_cand_b;
+  // host-record fields, loaded with everything else in the first round
+  uint32_t c_live = 0, c_promo = 0, c_err = 0, c_einfo = 0;
+  if (tid == 0) { c_live = ctl->n_live; c_promo = ctl->n_promoted; c_err = ctl->err; c_einfo = ctl->err_info; }
   STAMP(0);
   if (tid == 0) s_nbatch = 0;
   // ---- (1) the first m = min(BS, ncand) candidates in key order: key + record, plus the
@@ -1185,9 +1371,9 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     CandRec rc[R], pr[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
+      // unconditional below BS (buffers hold >= BS entries): the loads do not wait for the counts
       const uint32_t i = tid * R + r;
-      if (i < m) { kk[r] = skey[i]; rc[r] = srec[i]; }
-      if (i < n_prev) pr[r] = prec[i];
+      if (i < BS) { kk[r] = skey[i]; rc[r] = srec[i]; pr[r] = prec[i]; }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1487,14 +1673,15 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     h.n_batch = n_batch;
     h.n_admit = n_admit;
     h.n_preempt = n_preempt;
-    h.n_active = ctl->n_live;
+    h.n_active = c_live;
     h.swap_out_blocks = swap_out;
     h.swap_in_blocks = swap_in;
     h.kv_blocks = kv_sum;
-    h.n_promoted = ctl->n_promoted;
-    h.err = ctl->err;
+    h.n_promoted = c_promo;
+    const bool may_err = kv_on || n_batch == 0;  // the only places this kernel sets an error
+    h.err = may_err ? ctl->err : c_err;
     h.seqno = seqno;
-    h.err_info = ctl->err_info;
+    h.err_info = may_err ? ctl->err_info : c_einfo;
     ctl->n_promoted = 0;
     ctl->n_live = 0;
     ctl->qs_bnd1 = 0;
@@ -1542,8 +1729,8 @@ __global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* 
 #ifdef AUTX_CHAIN_STAMPS
   __syncthreads();
   if (threadIdx.x == 0) {
-    ctl->dbg[43] = globaltimer();
-    for (int i = 0; i < 12; ++i) { ctl->dbg[48 + i] = ctl->dbg[32 + i]; ctl->dbg[32 + i] = 0; }
+    ctl->dbg[33 + 3 * 5] = globaltimer();
+    for (int i = 0; i < 32; ++i) { ctl->dbg[64 + i] = ctl->dbg[32 + i]; ctl->dbg[32 + i] = 0; }
   }
 #endif
 }
@@ -1595,7 +1782,7 @@ static uint32_t pow2_at_least(uint32_t x) {
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev, const RadixState* rx, uint32_t arr_base,
-                        uint32_t* radix_passes) {
+                        uint32_t* radix_passes, uint32_t pre_rows) {
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
   out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
@@ -1612,8 +1799,10 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     // last-CTA fusion of select into the scan and finalize into the rank kernel: measured slower
     // than the PDL-chained separate kernels (fences vs hidden launch gaps), kept as an option
     static bool fuse = getenv("AUTX_FUSE") != nullptr;
-    // a separate one-CTA selection kernel between the scan and the gather (the previous default)
-    static bool sel_kernel = getenv("AUTX_SELECT_KERNEL") != nullptr;
+    // selection: a one-CTA kernel between the scan and the gather (default), or derived by every
+    // gather CTA from two-level counts (AUTX_GATHER_SS; fewer kernels but measured slower in the
+    // PDL chain: its 4-per-SM grid delays the rank kernel's CTAs)
+    static bool sel_kernel = getenv("AUTX_GATHER_SS") == nullptr;
     if (!scan_ctas) {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -1622,10 +1811,18 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       cudaFuncSetAttribute(k_scan_bulk<SEL_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
       cudaFuncSetAttribute(k_scan_bulk<SEL_GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
     }
+    static bool bulk = getenv("AUTX_SCAN_BULK") != nullptr;  // the persistent TMA-staged pass
     if (simple) {
       launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, out, t, n_rows);
       if (ev) cudaEventRecord(ev[1], s);
       launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
+    } else if (!bulk && !fuse) {
+      // rows loadable before the wait: only when no event separates the prologue from the scan
+      // does it matter, and it is safe either way (an event only delays the scan further)
+      if (sel_kernel) launch_pdl(k_scan_tile<SEL_KERNEL>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, pre_rows);
+      else launch_pdl(k_scan_tile<SEL_GATHER>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, pre_rows);
+      if (ev) cudaEventRecord(ev[1], s);
+      if (sel_kernel) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     } else {
       const int mode = fuse ? SEL_FUSED : sel_kernel ? SEL_KERNEL : SEL_GATHER;
       const uint32_t sgrid = std::min<uint32_t>(ntiles, scan_ctas);
@@ -1645,7 +1842,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
   // sorted keys [np] + admit and preempt id staging [2 x even(BS)]
   size_t fin_smem_bytes = ((size_t)np + 2 * ((pol.max_batch + 1) & ~1u)) * sizeof(uint64_t);
-  size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch * sizeof(uint64_t), fin_smem_bytes);
+  // keys, compacted keys, element indices of <= 2 BS candidates (fused: finalize's layout after)
+  size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch * (2 * sizeof(uint64_t) + sizeof(uint32_t)), fin_smem_bytes);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_finalize<FIN_THREADS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

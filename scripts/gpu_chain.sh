@@ -3,7 +3,7 @@
 # spans in the PDL-chained step for the default path and each env setting in AB.
 mkdir -p gpurun_out
 AUTX_NVCC_FLAGS=-DAUTX_CHAIN_STAMPS python -c "import __graft_entry__ as g; g.build()" > gpurun_out/chain_build.log 2>&1
-for e in base $AB; do
+for e in AUTX_DEFAULT=1 $AB; do
   env $e AUTX_BENCH_CHAIN=1 timeout 600 python bench.py --steps 100 --no-swap --no-cpu-baseline > gpurun_out/chain_$e.json 2>> gpurun_out/chain.err
   python -c "import json;d=json.loads(open('gpurun_out/chain_$e.json').read().splitlines()[-1]);print('$e', round(d['ms_per_step']*1e3,2), d['chain_us'])"
 done
