@@ -68,8 +68,10 @@ def chain_spans(phase):
         t0 = min(starts)
         rows.append({n: (c[3 * k] - t0, c[3 * k + 1] - t0, c[3 * k + 2] - t0) for k, n in enumerate(names) if c[3 * k]})
         rows[-1]["rank_keys"] = (c[20], c[21], 0)
+        if c[22]:  # k_rank CTA 0: keys loaded, compacted, counted
+            rows[-1]["rank_phases"] = tuple(c[22 + i] - t0 for i in range(3))
     out = {}
-    for n in names + ["rank_keys"]:
+    for n in names + ["rank_keys", "rank_phases"]:
         v = [r[n] for r in rows if n in r]
         if v:
             div = 1 if n == "rank_keys" else 1e3

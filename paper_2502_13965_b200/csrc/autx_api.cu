@@ -448,7 +448,8 @@ static autx_status compact(autx_ctx* ctx);
 // the multi-CTA registration kernel.
 static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
   if (ctx->n_comp_staged == 0 && ctx->n_arr_staged == 0) return AUTX_OK;
-  ctx->pre_rows = ctx->n_arr_staged ? ctx->arr_first_slot : ctx->tail;
+  // measured: loading the scan's rows before its PDL wait slows the prologue by as much as it
+  // saves (both wait on DRAM), so the scan loads after the wait (pre_rows stays 0)
   const bool bulk = ctx->n_arr_staged > 4096;
   PrologueArgs a;
   memset(&a, 0, offsetof(PrologueArgs, comp));

@@ -1284,11 +1284,17 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   if (e0 < n) {
     // (2) compact the candidates (same deterministic order in every CTA): sentinels rank last and
     // nobody reads them, so only the n_valid candidates are ranked and compared against
+#ifdef AUTX_CHAIN_STAMPS
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[54] = globaltimer();
+#endif
     uint32_t n_valid;
     uint32_t off = block_excl_scan<uint32_t, RANK_THREADS>(nv, red_r, &n_valid);
     for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS)
       if (rk[i] != ~0ull) { ck[off] = rk[i]; ci[off] = i; ++off; }
     __syncthreads();
+#ifdef AUTX_CHAIN_STAMPS
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[55] = globaltimer();
+#endif
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       ctl->n_cand_b = n_valid - na;
 #ifdef AUTX_CHAIN_STAMPS
@@ -1310,6 +1316,9 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     }
 #pragma unroll
     for (int d = 1; d < RANK_SUB; d <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+#ifdef AUTX_CHAIN_STAMPS
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[56] = globaltimer();
+#endif
     if (sub == 0 && e < n_valid) {
       out.skey[cnt] = x;
       out.sidx[cnt] = eo;
@@ -1799,10 +1808,10 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     // last-CTA fusion of select into the scan and finalize into the rank kernel: measured slower
     // than the PDL-chained separate kernels (fences vs hidden launch gaps), kept as an option
     static bool fuse = getenv("AUTX_FUSE") != nullptr;
-    // selection: a one-CTA kernel between the scan and the gather (default), or derived by every
-    // gather CTA from two-level counts (AUTX_GATHER_SS; fewer kernels but measured slower in the
-    // PDL chain: its 4-per-SM grid delays the rank kernel's CTAs)
-    static bool sel_kernel = getenv("AUTX_GATHER_SS") == nullptr;
+    // selection: derived by every gather CTA from two-level counts (default), or a one-CTA
+    // kernel between the scan and the gather (AUTX_SELECT_KERNEL; one more kernel in the chain,
+    // measured ~4 us slower per step)
+    static bool sel_kernel = getenv("AUTX_SELECT_KERNEL") != nullptr;
     if (!scan_ctas) {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -1844,6 +1853,10 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   size_t fin_smem_bytes = ((size_t)np + 2 * ((pol.max_batch + 1) & ~1u)) * sizeof(uint64_t);
   // keys, compacted keys, element indices of <= 2 BS candidates (fused: finalize's layout after)
   size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch * (2 * sizeof(uint64_t) + sizeof(uint32_t)), fin_smem_bytes);
+  // at most one rank CTA per SM: the CTAs are dispatched while the previous kernel still holds
+  // most SMs, and two packed on one SM halve each other's issue rate (measured: the count loop
+  // ran 2x slower behind the self-selecting gather's grid)
+  rank_smem = std::max<size_t>(rank_smem, 120 * 1024);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k_finalize<FIN_THREADS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

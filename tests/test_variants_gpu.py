@@ -1,0 +1,34 @@
+"""GPU parity of the alternative kernel pipelines behind environment switches (read once per
+process by the library, hence one subprocess per variant): each must reach the oracle's decisions
+exactly, like the default pipeline does in test_parity_gpu.py."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+VARIANTS = {
+    "select_kernel": {"AUTX_SELECT_KERNEL": "1"},  # one-CTA selection kernel before the gather
+    "scan_bulk": {"AUTX_SCAN_BULK": "1"},        # persistent TMA-staged dense pass
+    "scan_bulk_select": {"AUTX_SCAN_BULK": "1", "AUTX_SELECT_KERNEL": "1"},
+    "scan_simple": {"AUTX_SCAN_SIMPLE": "1"},    # plain per-tile pass + selection kernel
+    "fused": {"AUTX_FUSE": "1"},                 # last-CTA fusions (select into scan, finalize into rank)
+    "dma_out": {"AUTX_DMA_OUT": "1"},            # host lists by one copy instead of zero-copy stores
+}
+
+SUBSET = "fig2 or atlas_dag or mcts or chatbot or compaction or react or (random_tiny and 7)"
+
+
+@pytest.mark.parametrize("name", sorted(VARIANTS))
+def test_variant_parity(name):
+    env = dict(os.environ, **VARIANTS[name])
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(ROOT, "tests", "test_parity_gpu.py"), "-k", SUBSET],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, f"variant {name} failed:\n{tail}"
+    assert " passed" in r.stdout and "failed" not in r.stdout, tail
