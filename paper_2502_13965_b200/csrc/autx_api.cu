@@ -95,9 +95,6 @@ struct autx_ctx {
   uint32_t n_reg_this = 0;
   // work staged for the next sched_step's prologue kernel (single-engine mode)
   uint32_t n_comp_staged = 0, n_arr_staged = 0, arr_first_slot = 0;
-  // rows the scan may load before griddepcontrol.wait this step: set when a kernel of this step
-  // (which waited for the previous step) precedes the scan; rows appended this step excluded
-  uint32_t pre_rows = 0;
   std::unordered_set<uint64_t> staged_new_progs;
   bool timed_complete = false, timed_register = false;   // events 4-5 / 6-7 recorded this step
   bool tc_step = false, tr_step = false;                  // ... for the step being waited on
@@ -448,8 +445,6 @@ static autx_status compact(autx_ctx* ctx);
 // the multi-CTA registration kernel.
 static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
   if (ctx->n_comp_staged == 0 && ctx->n_arr_staged == 0) return AUTX_OK;
-  // measured: loading the scan's rows before its PDL wait slows the prologue by as much as it
-  // saves (both wait on DRAM), so the scan loads after the wait (pre_rows stays 0)
   const bool bulk = ctx->n_arr_staged > 4096;
   PrologueArgs a;
   memset(&a, 0, offsetof(PrologueArgs, comp));
@@ -616,13 +611,12 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
     arr_base = ctx->low < ctx->tail ? ctx->slot_arr[ctx->low] : t;
     if (t - arr_base >= (1u << 27)) return fail(ctx, AUTX_E_NOMEM, "arrival span exceeds the 27-bit key field");
   }
-  ctx->pre_rows = 0;
   s = flush_staged(ctx, t);
   if (s) return s;
   ++ctx->seqno;
   CK(launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv, ctx->kv_on, t,
                  ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr, ctx->radix ? &ctx->rx : nullptr,
-                 arr_base, &ctx->radix_passes, ctx->pre_rows));
+                 arr_base, &ctx->radix_passes));
   if (!ctx->out.zero_copy)
     CK(cudaMemcpyAsync(ctx->h_outblk, ctx->d_outblk, ctx->outblk_bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->done, ctx->stream));

@@ -287,7 +287,7 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev /* 5 events or null */,
                         const RadixState* rx /* non-null: AUTX_ORDER_RADIX */, uint32_t arr_base,
-                        uint32_t* radix_passes, uint32_t pre_rows = 0);
+                        uint32_t* radix_passes);
 cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                Outputs out, RadixState rx, uint32_t t, uint32_t n_rows,
                                uint32_t arr_base, int sms, uint32_t* passes_out);

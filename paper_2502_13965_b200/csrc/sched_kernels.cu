@@ -424,43 +424,27 @@ enum { SEL_KERNEL = 0, SEL_FUSED = 1, SEL_GATHER = 2 };
 // kernel), which is what bounds this latency-bound pass.  Per-row arithmetic is identical.
 template <int sel_mode>
 __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                               Outputs out, uint32_t t, uint32_t n_rows,
-                                                               uint32_t pre_rows) {
+                                                               Outputs out, uint32_t t, uint32_t n_rows) {
+  // (loading prog/base/mtime before the PDL wait, overlapping the prologue, was measured: the
+  // prologue's loads then queue behind these in DRAM and the step gains nothing)
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(1);
   constexpr int NW = SCAN_THREADS / 32;
   __shared__ uint32_t wq16[NW][MAX_K / 2];  // per warp: 16-bit counts of queues 2w, 2w + 1
   __shared__ uint32_t wn[NW];
   const uint32_t tid = threadIdx.x, tile = blockIdx.x;
   const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
-  // prog, base and mtime of rows that existed before this step's prologue are not written by it
-  // (completions only mark rows dead; arrivals append): when the prologue precedes this kernel
-  // (pre_rows > 0), load them before griddepcontrol.wait, overlapping the prologue.  qf and the
-  // program rows (which the prologue does change) are read after the wait.
-  const bool early = row0 + ROWS_PER_THREAD <= pre_rows;
-  uint4 p0, p1, b0, b1, m0, m1;
-  if (early) {
-    p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
-    p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
-    b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
-    b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
-    m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
-    m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(ct.qf + row0));
-  }
-  pdl_wait();
-  pdl_trigger();
-  CHAIN_BEGIN(1);
   uint64_t hq = 0;
   uint32_t npromo = 0, nlive = 0;
   if (row0 < n_rows) {
     const uint2 qv = __ldcs(reinterpret_cast<const uint2*>(ct.qf + row0));
-    if (!early) {
-      p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
-      p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
-      b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
-      b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
-      m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
-      m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
-    }
+    const uint4 p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+    const uint4 p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    const uint4 b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+    const uint4 b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+    const uint4 m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+    const uint4 m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
     uint32_t qfs[8], prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
     uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
     uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
@@ -1791,7 +1775,7 @@ static uint32_t pow2_at_least(uint32_t x) {
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev, const RadixState* rx, uint32_t arr_base,
-                        uint32_t* radix_passes, uint32_t pre_rows) {
+                        uint32_t* radix_passes) {
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
   out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
@@ -1826,10 +1810,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       if (ev) cudaEventRecord(ev[1], s);
       launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     } else if (!bulk && !fuse) {
-      // rows loadable before the wait: only when no event separates the prologue from the scan
-      // does it matter, and it is safe either way (an event only delays the scan further)
-      if (sel_kernel) launch_pdl(k_scan_tile<SEL_KERNEL>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, pre_rows);
-      else launch_pdl(k_scan_tile<SEL_GATHER>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, pre_rows);
+      if (sel_kernel) launch_pdl(k_scan_tile<SEL_KERNEL>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows);
+      else launch_pdl(k_scan_tile<SEL_GATHER>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows);
       if (ev) cudaEventRecord(ev[1], s);
       if (sel_kernel) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     } else {
