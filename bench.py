@@ -421,6 +421,7 @@ def main():
     # e2e: the same steps through the public API from the host, wall clock, no gate/flush
     s.set_timing(False)
     e2e_dec, e2e_s, h2d, d2h, wall_s = 0, 0.0, 0, 0, 0.0
+    split0 = dict(d.api_split)
     for _ in range(min(args.steps, 100)):
         nc = len(d.pending)
         api0 = d.api_s
@@ -477,7 +478,9 @@ def main():
                 "d2h_bytes_per_step": d2h // e2e_steps, "ms_per_step": e2e_s * 1e3 / e2e_steps,
                 "timed": "wall clock inside the C-ABI calls (complete, end_program, register, sched_step, "
                          "step_wait + list copies) per step; H2D staging and D2H mirrors included",
-                "harness_ms_per_step": (wall_s - e2e_s) * 1e3 / e2e_steps},
+                "harness_ms_per_step": (wall_s - e2e_s) * 1e3 / e2e_steps,
+                "api_us_per_step": {k: round((v - split0.get(k, 0.0)) * 1e6 / e2e_steps, 1)
+                                    for k, v in d.api_split.items()}},
         "setup_s": {"generate": round(t_gen, 1), "register_and_fast_forward": round(t_setup, 1)},
     }
     if ck:

@@ -91,7 +91,8 @@ __device__ __forceinline__ void apply_record(const Policy& pol, ProgTable pt, co
 
 template <int NT>
 __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, Ctl* ctl, const uint32_t* slots,
-                              uint32_t n, uint32_t t, KvState& kv, bool kv_on, CompRec* rec_out, bool apply) {
+                              uint32_t n, uint32_t t, KvState& kv, bool kv_on, CompRec* rec_out, bool apply,
+                              CompRec* s_rec = nullptr) {
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
   STAMP(16);
@@ -109,6 +110,7 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       r.cp = ct.inh[s] + e;
       r.tw = (t - ct.arr[s]) - e;  // totwait: active steps arr..t-1 that did not run
       rec_out[i] = r;
+      if (s_rec) s_rec[i] = r;  // the caller's shared-memory copy (n <= NT)
     }
     STAMP(17);
     if (apply && valid) apply_record(pol, pt, r, t);
@@ -206,13 +208,15 @@ __global__ void k_route(const char* base, uint64_t stride, uint32_t G, const Rou
 // a2: arrivals (Alg. 1 l.9-14).  Rows are appended in canonical order; row index = seq.
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ void register_one(const Policy& pol, CallTable& ct, ProgTable& pt, const ArrivalRec& r,
-                                             uint32_t s, uint32_t t) {
+                                             uint32_t s, uint32_t t, bool have_inh = false, uint32_t inh_given = 0) {
   uint32_t p = r.prog;
   if (r.flags & 2u) {  // first record of a program new in this batch: create its entry
     pt.info[p] = PInfo{0, 0, 0ull};
     pt.last_comp[p] = NONE;
   }
-  uint32_t inh = (r.flags & 1u) ? 0u : __ldcg(&pt.info[p].svc);  // Alg. 1 l.11 (L2: see k_prologue)
+  // Alg. 1 l.11: the service after this step's completions (given by the caller, or read from L2
+  // after the caller's fence: see k_prologue)
+  uint32_t inh = have_inh ? inh_given : (r.flags & 1u) ? 0u : __ldcg(&pt.info[p].svc);
   pt.last_arr[p] = t;
   uint32_t q = place_queue(pol, inh);             // Alg. 1 l.12
   ct.cid[s] = r.cid;
@@ -255,6 +259,30 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
   pdl_trigger();
   CHAIN_BEGIN(0);
   __syncthreads();
+  if (comp_inline && arr_inline) {
+    // typical step: arrivals inherit the service after this step's completions (R10) computed
+    // here (old row value combined with the step's records of the same program, exactly what the
+    // reductions leave in the row), so the row loads go out with the completion loads: one round
+    __shared__ CompRec s_rec[PRO_INLINE];
+    uint32_t svc_old = 0;
+    const bool my_arr = tid < a.n_arr;
+    if (my_arr && !(s_arr[tid].flags & 1u)) svc_old = __ldcg(&pt.info[s_arr[tid].prog].svc);
+    if (a.n_comp)
+      complete_body<PRO_THREADS>(pol, ct, pt, ctl, s_comp, a.n_comp, a.t, kv, kv_on, rec_out, true, s_rec);
+    __syncthreads();
+    if (my_arr) {
+      const ArrivalRec r = s_arr[tid];
+      uint32_t inh = 0;
+      if (!(r.flags & 1u)) {
+        inh = svc_old;
+        for (uint32_t i = 0; i < a.n_comp; ++i)
+          if (s_rec[i].prog == r.prog) inh = pol.policy == AUTX_ATLAS ? max(inh, s_rec[i].cp) : inh + s_rec[i].exec;
+      }
+      register_one(pol, ct, pt, r, a.first_slot + tid, a.t, true, inh);
+    }
+    CHAIN_END(0);
+    return;
+  }
   if (a.n_comp)
     complete_body<PRO_THREADS>(pol, ct, pt, ctl, comp_inline ? s_comp : a.comp_ptr, a.n_comp, a.t, kv, kv_on,
                                rec_out, true);

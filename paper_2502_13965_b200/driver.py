@@ -38,6 +38,7 @@ class TraceDriver:
         self.log = []
         self.total_wait = 0
         self.api_s = 0.0        # wall time spent inside the C ABI calls (the user-visible API)
+        self.api_split = {}     # the same, per call
 
     def idx_of(self, cids):
         cids = np.asarray(cids, np.uint64)
@@ -86,15 +87,22 @@ class TraceDriver:
         ids = self.tr.call_id[self.pending]
         ended = self._release(t, self.pending)
         arr = self.arrivals(t)
-        t0 = time.perf_counter()
+        pc = time.perf_counter
+        t0 = pc()
         if nc:
             s.complete(ids)
+        t1 = pc()
         for pid in ended:
             s.end_program(pid)
+        t2 = pc()
         if len(arr):
             s.register(arr)
+        t3 = pc()
         s.sched_step(t, wait=False)
-        self.api_s += time.perf_counter() - t0
+        t4 = pc()
+        self.api_s += t4 - t0
+        for k, dt in (("complete", t1 - t0), ("end_program", t2 - t1), ("register", t3 - t2), ("sched_step", t4 - t3)):
+            self.api_split[k] = self.api_split.get(k, 0.0) + dt
         return nc, len(arr)
 
     def finish(self):
@@ -104,8 +112,12 @@ class TraceDriver:
         s = self.s
         t0 = time.perf_counter()
         out = s.step_wait()
+        t1 = time.perf_counter()
         batch, admit, preempt = s.lists()
-        self.api_s += time.perf_counter() - t0
+        t2 = time.perf_counter()
+        self.api_s += t2 - t0
+        self.api_split["step_wait"] = self.api_split.get("step_wait", 0.0) + t1 - t0
+        self.api_split["lists"] = self.api_split.get("lists", 0.0) + t2 - t1
         rec = dict(t=t, n_batch=int(out.n_batch), swap_out_blocks=int(out.swap_out_blocks),
                    swap_in_blocks=int(out.swap_in_blocks), kv_blocks=int(out.kv_blocks),
                    n_active=int(out.n_active), n_promoted=int(out.n_promoted),

@@ -13,5 +13,5 @@ timeout 600 python bench.py --workload chatbot --steps 100 --no-swap --no-cpu-ba
 timeout 600 python bench.py --workload react --steps 100 --no-swap --no-cpu-baseline > gpurun_out/bench_react.json 2> gpurun_out/bench_react.err
 AUTX_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 20 --warmup 3 --ff 10 --active 300000 --no-swap --no-cpu-baseline > gpurun_out/bench_gloo2.json 2> gpurun_out/bench_gloo2.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv --log-file gpurun_out/launches_final.csv python bench.py --steps 5 --warmup 3 --ff 20 --no-swap --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scan_bulk|k_finalize|k_rank|k_gather|k_prologue|k_select" -s 60 -c 6 -o gpurun_out/prof_final python bench.py --steps 3 --warmup 3 --ff 20 --no-swap --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scan_tile|k_gather_ss|k_rank|k_finalize|k_prologue" -s 50 -c 5 -o gpurun_out/prof_final python bench.py --steps 3 --warmup 3 --ff 20 --no-swap --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log; cat gpurun_out/bench_final.json | cut -c1-400
