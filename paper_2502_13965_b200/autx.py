@@ -170,6 +170,7 @@ class Scheduler:
             raise AutxError(st, "autx_create failed (see stderr)")
         self.out = StepOut()
         self.max_batch = max_batch
+        self._views = None
 
     def _check(self, st):
         if st != 0:
@@ -215,8 +216,12 @@ class Scheduler:
     def lists(self):
         """(batch, admit, preempt) call-id arrays of the last waited step (copies)."""
         o = self.out
-        f = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
-        return f(o.h_batch, o.n_batch), f(o.h_admit, o.n_admit), f(o.h_preempt, o.n_preempt)
+        if self._views is None:
+            # the pinned mirrors live as long as the context: wrap them once
+            f = lambda p: np.ctypeslib.as_array(p, shape=(max(self.max_batch, 1),))
+            self._views = (f(o.h_batch), f(o.h_admit), f(o.h_preempt))
+        vb, va, vp = self._views
+        return vb[:o.n_batch].copy(), va[:o.n_admit].copy(), vp[:o.n_preempt].copy()
 
     def kv_swap(self, k_ptrs, v_ptrs, chunk_bytes, host_ptr, host_bytes, mode=SWAP_SM):
         L = len(k_ptrs)

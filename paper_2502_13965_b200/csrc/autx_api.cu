@@ -55,8 +55,10 @@ struct autx_ctx {
   RadixState rx{};
   bool radix = false;
   uint32_t radix_passes = 0;
-  std::unordered_set<uint64_t> last_batch;
+  // slots of the last step's batch: ran_seq[slot] == seqno (from the mirrored batch slots)
+  std::vector<uint32_t> ran_seq;
   bool last_batch_valid = false;
+  std::vector<uint32_t> comp_scratch;
   uint32_t tail = 0;
   // protocol state
   bool stepped = false;       // at least one sched_step done
@@ -149,10 +151,11 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   Outputs& o = ctx->out;
   uint32_t BS = c.max_batch;
   size_t ntiles = rows / TILE + 1;
-  CK(dalloc(&o.batch_slots, BS));
-  // one device block [counts | batch | admit | preempt] and its pinned mirror: one D2H per step
+  // one device block [counts | batch | admit | preempt | batch slots] and its pinned mirror: one
+  // D2H per step (the slots let the host check completions without an id set)
   const uint32_t BSp = (BS + 1) & ~1u;  // even list strides keep every list 16-byte aligned
-  ctx->outblk_bytes = 64 + (size_t)3 * BSp * 8;
+  const uint32_t BS4 = (BS + 3) & ~3u;
+  ctx->outblk_bytes = 64 + (size_t)3 * BSp * 8 + (size_t)BS4 * 4;
   CK(cudaMalloc((void**)&ctx->d_outblk, ctx->outblk_bytes));
   CK(cudaHostAlloc((void**)&ctx->h_outblk, ctx->outblk_bytes, cudaHostAllocMapped));
   memset(ctx->h_outblk, 0, ctx->outblk_bytes);
@@ -162,6 +165,7 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   o.batch_ids = reinterpret_cast<uint64_t*>(ctx->d_outblk + 64);
   o.admit_ids = o.batch_ids + BSp;
   o.preempt_ids = o.admit_ids + BSp; CK(dalloc(&o.prev_slots, BS)); CK(dalloc(&o.preempt_slots, BS));
+  o.batch_slots = reinterpret_cast<uint32_t*>(o.preempt_ids + BSp);
   CK(dalloc(&o.admit_slots, BS));
   o.cand_cap = 2 * BS;
   CK(dalloc(&o.cand, o.cand_cap));
@@ -180,6 +184,8 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   o.h_batch = reinterpret_cast<uint64_t*>(ctx->h_outblk + 64);
   o.h_admit = o.h_batch + BSp;
   o.h_preempt = o.h_admit + BSp;
+  o.h_batch_slots = reinterpret_cast<uint32_t*>(o.h_preempt + BSp);
+  ctx->ran_seq.assign(rows, 0);
   ctx->cslots_cap = 4 * BS;
   CK(cudaHostAlloc((void**)&ctx->h_cslots, ctx->cslots_cap * 4, cudaHostAllocMapped));
   ctx->arr_cap = 4 * BS;
@@ -313,7 +319,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   CallTable& t = ctx->ct;
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
                  t.loc, t.hcls, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp,
-                 ctx->ctl, ctx->out.batch_slots, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
+                 ctx->ctl, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
                  ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->out.tile_off,
                  ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
@@ -341,14 +347,14 @@ static autx_status sync_last(autx_ctx* ctx) {
     ctx->pending_done = false;
   }
   if (!ctx->last_batch_valid) {
-    ctx->last_batch.clear();
     if (ctx->stepped) {
       const HostOut& h = *ctx->out.hout;
       if (h.err)
         return fail(ctx, (autx_status)h.err, "device error %u (site %u: 1 host arena full, 2 call needs more "
                     "than max_blocks_per_call, 3 no resident slot, 4 GPU block pool empty, other: head call "
                     "needs more than P) in step %u", h.err, h.err_info, ctx->t_last);
-      for (uint32_t i = 0; i < h.n_batch; ++i) ctx->last_batch.insert(ctx->out.h_batch[i]);
+      const uint32_t* bs = ctx->out.h_batch_slots;
+      for (uint32_t i = 0; i < h.n_batch; ++i) ctx->ran_seq[bs[i]] = ctx->seqno;
     }
     ctx->last_batch_valid = true;
   }
@@ -402,22 +408,27 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
   if (n > ctx->cfg.max_batch) return fail(ctx, AUTX_E_INVAL, "too many completions (%u)", n);
   if (ctx->routed_this) return fail(ctx, AUTX_E_STATE, "autx_complete after autx_route_apply");
   // validate everything before mutating anything
-  std::unordered_set<uint64_t> seen;
+  std::vector<uint32_t>& sl = ctx->comp_scratch;
+  sl.resize(n);
   for (uint32_t i = 0; i < n; ++i) {
     auto it = ctx->call_slot.find(ids[i]);
     if (it == ctx->call_slot.end()) return fail(ctx, AUTX_E_NOENT, "unknown call %llu", (unsigned long long)ids[i]);
-    if (!ctx->last_batch.count(ids[i]))
+    if (!ctx->stepped || ctx->ran_seq[it->second] != ctx->seqno)
       return fail(ctx, AUTX_E_STATE, "call %llu did not run in step %u", (unsigned long long)ids[i], ctx->t_last);
-    if (!seen.insert(ids[i]).second) return fail(ctx, AUTX_E_INVAL, "duplicate completion");
+    sl[i] = it->second;
+  }
+  {
+    std::vector<uint32_t> srt(sl);
+    std::sort(srt.begin(), srt.end());
+    if (std::adjacent_find(srt.begin(), srt.end()) != srt.end()) return fail(ctx, AUTX_E_INVAL, "duplicate completion");
   }
   for (uint32_t i = 0; i < n; ++i) {
-    auto it = ctx->call_slot.find(ids[i]);
-    uint32_t slot = it->second;
+    const uint32_t slot = sl[i];
     ctx->h_cslots[i] = slot;
     ctx->slot_live[slot] = 0;
     ctx->prog_active[ctx->slot_prog[slot]] -= 1;
-    ctx->call_slot.erase(it);
-    ctx->last_batch.erase(ids[i]);
+    ctx->call_slot.erase(ids[i]);
+    ctx->ran_seq[slot] = 0;
   }
   uint32_t t = next_step(ctx);
   if (ctx->cfg.nranks <= 1) {

@@ -196,6 +196,7 @@ struct Outputs {
   uint64_t* h_batch;         // pinned host mirrors
   uint64_t* h_admit;
   uint64_t* h_preempt;
+  uint32_t* h_batch_slots;   // pinned mirror of batch_slots (host-side completion checks)
 };
 
 // AUTX_ORDER_RADIX buffers (radix_kernels.cu)

@@ -1729,6 +1729,12 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
             make_uint4((uint32_t)c_cid[2 * k], (uint32_t)(c_cid[2 * k] >> 32), (uint32_t)c_cid[2 * k + 1],
                        (uint32_t)(c_cid[2 * k + 1] >> 32));
     }
+    // batch slots, R consecutive u32 per thread (8- or 16-byte stores)
+    if (tid * R < nb) {
+      if constexpr (R == 2) reinterpret_cast<uint2*>(out.h_batch_slots)[tid] = make_uint2(c_s[0], c_s[1]);
+      else if constexpr (R == 4) reinterpret_cast<uint4*>(out.h_batch_slots)[tid] = make_uint4(c_s[0], c_s[1], c_s[2], c_s[3]);
+      else for (int r = 0; r < R; ++r) out.h_batch_slots[tid * R + r] = c_s[r];
+    }
     const uint4* sa = reinterpret_cast<const uint4*>(s_ad);
     const uint4* sp = reinterpret_cast<const uint4*>(s_pr);
     for (uint32_t i = tid; i < (na + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_admit)[i] = sa[i];
