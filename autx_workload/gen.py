@@ -165,6 +165,19 @@ def _dag_ctx(decode, prefill, parents, system_prompt=0):
     return ctx
 
 
+def dag_trace(name, programs, arrivals) -> Trace:
+    """A trace from explicit per-program lists: each program is a dict with decode, parents
+    (local indices) and optionally delay / prefill (default 0 / 1)."""
+    progs = []
+    for p in programs:
+        n = len(p["decode"])
+        dec = np.asarray(p["decode"], np.int64)
+        pre = np.asarray(p.get("prefill", [1] * n), np.int64)
+        progs.append(dict(decode=dec, prefill=pre, delay=np.asarray(p.get("delay", [0] * n), np.int64),
+                          parents=p["parents"], input_tokens=_dag_ctx(dec, pre, p["parents"])))
+    return _assemble(name, progs, arrivals)
+
+
 def fig2() -> Trace:
     """Fig. 2a: decode steps per LLM call, BS=2, all programs at t=0."""
     dec = {"A": [4, 3, 1, 1], "B": [3, 3, 4], "C": [1, 2], "D": [4]}

@@ -15,6 +15,8 @@ engine step t (time unit = one decode iteration, reading R17):
         ATLAS:                svc[p] = max(svc[p], inh(c)+exec(c)) Alg.1 l.4
         all:                  pwait[p] += totwait(c)              Alg.1 l.5-6, reading R5
   2. arrivals at step t, canonical order, inherit svc[p]        Alg.1 l.9-14
+        ATLAS_EQ2 (exact Eq. 2): inherit max over the call's
+        parents of (p(parent) + t_parent), 0 for a root            reading R31
         q = min{i : inh < hi_i} (PLAS/ATLAS) or 0 (FCFS/MLFQ)   P:L253, reading R1
         quanta = Q[q]                                            Alg.1 l.13
   3. demotion: quanta <= 0 -> q = min(q+1, K-1), quanta = Q[q]  Alg.1 l.20-23
@@ -43,6 +45,9 @@ import numpy as np
 INF = None  # infinite quantum / budget / beta marker
 
 FCFS, MLFQ, PLAS, ATLAS = "fcfs", "mlfq", "plas", "atlas"
+# Exact Eq. 2 ATLAS: a new call inherits max over its parents of
+# (parent's priority + parent's execution time) instead of the program's scalar (reading R31)
+ATLAS_EQ2 = "atlas_eq2"
 
 
 @dataclass
@@ -59,7 +64,7 @@ class Config:
     token_threshold: int = 2048      # Alg. 2 line 2
 
     def check(self):
-        assert self.policy in (FCFS, MLFQ, PLAS, ATLAS)
+        assert self.policy in (FCFS, MLFQ, PLAS, ATLAS, ATLAS_EQ2)
         assert 1 <= self.K <= 16 and len(self.q_hi) == self.K - 1 and len(self.quanta) == self.K
         assert list(self.q_hi) == sorted(self.q_hi)
         assert all(q is None or q >= 1 for q in self.quanta)
@@ -103,7 +108,7 @@ class ProgramTable:
 
     def apply_completion(self, policy, pid, exec_steps, inh, totwait, t):
         """UPDATE_PROCESS_TABLE, Alg. 1 l.1-7."""
-        if policy == ATLAS:
+        if policy in (ATLAS, ATLAS_EQ2):
             self.svc[pid] = max(self.svc[pid], inh + exec_steps)  # Alg. 1 l.4 / Eq. 2 scalar
         else:
             self.svc[pid] = self.svc[pid] + exec_steps               # Eq. 1 sum
@@ -154,6 +159,8 @@ class Engine:
         self.prev_batch = []     # cids of the previous step's batch, in batch order
         self.check = check_formulations
         self.last_arrival_key = None
+        self.crit = {}           # ATLAS_EQ2: completed cid -> p(c) + t_c (Eq. 2 operand)
+        self.crit_of_prog = {}   # pid -> completed cids kept in self.crit
 
     # -- Alg. 1 helpers ------------------------------------------------------------
     def quantum(self, q):
@@ -184,6 +191,9 @@ class Engine:
             if not c.running:
                 raise ValueError(f"call {cid} completed but did not run in step {t-1}")
             recs.append((c.pid, c.exec, c.inh, c.totwait))
+            if self.cfg.policy == ATLAS_EQ2:
+                self.crit[cid] = c.inh + c.exec                   # p(c_k) + t_k, Eq. 2
+                self.crit_of_prog.setdefault(c.pid, []).append(cid)
             del self.calls[cid]
         self.prev_batch = [x for x in self.prev_batch if x in self.calls]
         return recs
@@ -192,9 +202,27 @@ class Engine:
         for pid, ex, inh, tw in recs:
             self.table.apply_completion(self.cfg.policy, pid, ex, inh, tw, t)
 
-    def register(self, t, arrivals):
+    def eq2_priority(self, pid, parents):
+        """Eq. 2: 0 for a root, else max over the parents c_k of p(c_k) + t_k.  The
+        parents must be completed calls of the same program ("parents P(c_j) in the same
+        program")."""
+        if not parents:
+            return 0
+        for k in parents:
+            if k not in self.crit or k not in self.crit_of_prog.get(pid, ()):
+                raise KeyError(f"parent {k} is not a completed call of program {pid}")
+        return max(self.crit[k] for k in parents)
+
+    def end_program(self, pid):
+        """end_session: the table entry and the program's Eq. 2 operands go."""
+        self.table.end_program(pid)
+        for k in self.crit_of_prog.pop(pid, []):
+            del self.crit[k]
+
+    def register(self, t, arrivals, parents=None):
         """Phase 2: arrivals = list of (cid, pid, arrival_step, program_arrival_step,
-        input_tokens) in canonical order: (arr, parr, pid, cid)."""
+        input_tokens) in canonical order: (arr, parr, pid, cid).  ATLAS_EQ2 also
+        takes parents: cid -> list of parent cids."""
         for (cid, pid, arr, parr, tok) in arrivals:
             k = (arr, parr, pid, cid)
             if self.last_arrival_key is not None and k <= self.last_arrival_key:
@@ -206,7 +234,10 @@ class Engine:
                 raise ValueError("duplicate call id")
             self.table.ensure(pid, t)
             self.table.last_arrival[pid] = t
-            inh = self.table.svc[pid]                       # Alg. 1 l.11
+            if self.cfg.policy == ATLAS_EQ2:
+                inh = self.eq2_priority(pid, (parents or {}).get(cid, ()))   # Eq. 2
+            else:
+                inh = self.table.svc[pid]                   # Alg. 1 l.11
             q = self.place(inh)                              # Alg. 1 l.12
             c = Call(cid=cid, pid=pid, arr=arr, parr=parr, seq=self.next_seq, input_tokens=tok,
                      inh=inh, q=q, quanta=self.quantum(q))   # Alg. 1 l.13
@@ -312,10 +343,10 @@ class Engine:
         return dict(t=t, batch=batch, admit=admit, preempt=preempt, swap_out=swap_out,
                     swap_in=swap_in, kv_blocks=blocks, n_active=len(self.calls))
 
-    def step(self, t, completed, arrivals):
+    def step(self, t, completed, arrivals, parents=None):
         recs = self.complete(t, completed)
         self.apply_records(t, recs)
-        self.register(t, arrivals)
+        self.register(t, arrivals, parents)
         self.demote_and_promote()
         return self.schedule(t)
 
@@ -414,31 +445,46 @@ class Workload:
     def finished(self):
         return self.done == self.tr.n_calls
 
+    def parents_of(self, arrivals):
+        """Parent call ids of each arrival (the DAG is the workload's; the scheduler
+        learns a call's parents only when it arrives: non-clairvoyance)."""
+        tr = self.tr
+        out = {}
+        for a in arrivals:
+            c = self.index[a[0]]
+            out[a[0]] = [int(tr.call_id[k]) for k in tr.parents(c)]
+        return out
 
-def simulate(trace, cfg: Config, max_steps=1_000_000, check_formulations=True):
-    """Run a whole trace on one engine; returns (log, metrics)."""
+
+def simulate(trace, cfg: Config, max_steps=1_000_000, check_formulations=True, start=0):
+    """Run a whole trace on one engine from step `start` (the trace's first arrival must not
+    precede it); returns (log, metrics)."""
     eng = Engine(cfg, check_formulations=check_formulations)
     wl = Workload(trace)
     log = []
     completed = []
     total_wait = 0
     gantt = {}
-    for t in range(max_steps):
+    inh = {}
+    for t in range(start, start + max_steps):
         if wl.finished():
             break
         done_cids = [int(trace.call_id[c]) for c in completed]
         for cid in done_cids:
             total_wait += eng.calls[cid].totwait
         ended = wl.release(t, completed)
-        rec = eng.step(t, done_cids, wl.arrivals(t))
+        arr = wl.arrivals(t)
+        rec = eng.step(t, done_cids, arr, wl.parents_of(arr) if cfg.policy == ATLAS_EQ2 else None)
+        for a in arr:
+            inh[a[0]] = eng.calls[a[0]].inh
         for pid in ended:
-            eng.table.end_program(pid)
+            eng.end_program(pid)
         log.append(rec)
         for cid in rec["batch"]:
             gantt.setdefault(cid, []).append(t)
         completed = wl.ran(t, rec["batch"])
     assert wl.finished(), "simulation did not finish"
-    return log, dict(total_wait=total_wait, finish=dict(wl.finish), gantt=gantt, steps=len(log))
+    return log, dict(total_wait=total_wait, finish=dict(wl.finish), gantt=gantt, steps=len(log), inh=inh)
 
 
 def gantt_strings(trace, gantt):
@@ -462,6 +508,7 @@ def simulate_multi(trace, cfg: Config, n_engines: int, max_steps=1_000_000):
     """G engines step together.  Per step: local completions -> all completion
     records applied to the (replicated) table -> loads -> Alg. 2 routing of the
     step's arrivals in canonical order -> each engine schedules."""
+    assert cfg.policy != ATLAS_EQ2, "Eq. 2 mode is single-engine (parents may run on other engines)"
     table = ProgramTable()
     engines = [Engine(cfg, table=table, check_formulations=False) for _ in range(n_engines)]
     wl = Workload(trace)
