@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--swap-steps", type=int, default=60)
     ap.add_argument("--order", default="select", choices=["select", "radix"])
+    ap.add_argument("--policy", default=None, choices=["atlas", "atlas_eq2", "plas"],
+                    help="override the workload's policy (atlas_eq2: exact Eq. 2, SURVEY 8(f) item 2)")
     ap.add_argument("--workload", default="mcts", choices=["mcts", "chatbot", "react"],
                     help="mcts: BASELINE configs[3] (default, the headline); chatbot/react: configs[1]/[2]")
     return ap.parse_args()
@@ -80,7 +82,7 @@ def chain_spans(phase):
 
 
 def ncu_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per k_scan_bulk launch from the committed
+    """dram__bytes_read.sum + dram__bytes_write.sum per k_scan_tile launch from the committed
     `ncu --set full` capture summary (profiles/scan_traffic.json), or None."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "scan_traffic.json")))
@@ -318,6 +320,8 @@ def main():
     wl = {"mcts": dict(policy="atlas", max_batch=1024, kv_budget=32768),
           "chatbot": dict(policy="plas", max_batch=256, kv_budget=6000),
           "react": dict(policy="plas", max_batch=256, kv_budget=8000)}[args.workload]
+    if args.policy:
+        wl["policy"] = args.policy
     s = Scheduler(policy=wl["policy"], beta=(1, 0) if os.environ.get("AUTX_BENCH_BETA_INF") else (2, 1), max_batch=wl["max_batch"], kv_budget=wl["kv_budget"], block_tokens=16,
                   max_calls=int(args.active * 1.25) + 4096, max_programs=tr.n_programs + 1024,
                   order_mode=ORDER_RADIX if args.order == "radix" else ORDER_SELECT,
@@ -438,7 +442,7 @@ def main():
 
     scan_avg_ms = statistics.mean(scan_ms)
     traffic_bytes, traffic_src = ncu_traffic()
-    if args.workload != "mcts" or args.order != "select":
+    if args.workload != "mcts" or args.order != "select" or wl["policy"] != "atlas":
         # the committed capture is of the default configuration's scan kernel only
         traffic_bytes, traffic_src = None, "no ncu capture of this configuration"
     achieved = statistics.mean(scan_bytes) / (scan_avg_ms * 1e-3) / 1e9
@@ -457,7 +461,7 @@ def main():
                    "order": args.order, "l2": "flushed before every step (512 MiB write)" if not args.no_flush else "hot",
                    "parallelism": f"engines{world} (one scheduler per GPU)"},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "k_scan_bulk (dense anti-starvation + queue counts)"
+        "roofline": {"bound": "hbm", "kernel": "k_scan_tile (dense anti-starvation + queue counts)"
                      if args.order == "select" else "radix order (k_keys + LSD passes + k_take)",
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic_bytes, "traffic_source": traffic_src,

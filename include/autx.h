@@ -42,7 +42,12 @@ typedef enum {
   AUTX_E_NCCL = 7
 } autx_status;
 
-typedef enum { AUTX_FCFS = 0, AUTX_MLFQ = 1, AUTX_PLAS = 2, AUTX_ATLAS = 3 } autx_policy;
+/* AUTX_ATLAS is Alg. 1's scalar ATLAS (every new call inherits its program's longest observed
+ * critical path, l.4 / l.11).  AUTX_ATLAS_EQ2 is the exact Eq. 2: a new call
+ * inherits max over its parents c_k of p(c_k) + t_k (0 for a root), parents given through
+ * autx_register_call_dag; the process table is still updated by Alg. 1 l.4 (it feeds the
+ * anti-starvation ratio).  Single-engine only (nranks == 1); reading R31. */
+typedef enum { AUTX_FCFS = 0, AUTX_MLFQ = 1, AUTX_PLAS = 2, AUTX_ATLAS = 3, AUTX_ATLAS_EQ2 = 4 } autx_policy;
 
 /* Ordering strategy for step a5 (both produce the identical batch: the key is unique).
  *  AUTX_ORDER_SELECT: top-BS selection over the table kept in (arrival, seq) order.
@@ -149,8 +154,20 @@ autx_status autx_end_program(autx_ctx* ctx, uint64_t program_id);
  * l.1-7).  Each must have been in the previous batch (E_STATE) and be known (E_NOENT). Blocks
  * until the previous step's `done`. */
 autx_status autx_complete(autx_ctx* ctx, const uint64_t* call_ids, uint32_t n);
-/* Arrivals of the current step (Alg. 1 l.9-14), canonical order (E_INVAL otherwise). */
+/* Arrivals of the current step (Alg. 1 l.9-14), canonical order (E_INVAL otherwise).  Under
+ * AUTX_ATLAS_EQ2 these are roots (Eq. 2: priority 0). */
 autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n);
+/* AUTX_ATLAS_EQ2 arrivals with their DAG parents ("its parents P(c_j) in the same
+ * program"; the DAG is learned as calls arrive).  parent_offsets: host array of n+1
+ * ascending offsets into parent_ids (host array of call ids); call i's parents are
+ * parent_ids[parent_offsets[i] .. parent_offsets[i+1]).  Every parent must be a call of the
+ * same program that has completed (autx_complete, this step or earlier) and whose program has
+ * not ended: unknown id -> E_NOENT, still active -> E_STATE, other program -> E_INVAL.  The
+ * priority p(c_i) = max_k p(c_k) + t_k is computed on the device from the parents' completion
+ * records (a call with no parents is a root: 0).  Other policies: E_INVAL.  The completed
+ * calls' p + t values are kept until their program ends (capacity 4 x max_calls: E_NOMEM). */
+autx_status autx_register_call_dag(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n,
+                                   const uint32_t* parent_offsets, const uint64_t* parent_ids);
 /* One scheduling step t (Alg. 1 l.15-39): demotion, anti-starvation, ordering, cutoff,
  * admit/preempt lists, step accounting.  t must increase by >= 1 per call (steps with no
  * active call may be skipped). */

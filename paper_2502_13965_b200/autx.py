@@ -12,7 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libautx.so")
 
 FCFS, MLFQ, PLAS, ATLAS = 0, 1, 2, 3
-POLICY = {"fcfs": FCFS, "mlfq": MLFQ, "plas": PLAS, "atlas": ATLAS}
+ATLAS_EQ2 = 4
+POLICY = {"fcfs": FCFS, "mlfq": MLFQ, "plas": PLAS, "atlas": ATLAS, "atlas_eq2": ATLAS_EQ2}
 ORDER_SELECT, ORDER_RADIX = 0, 1
 SWAP_SM, SWAP_PER_CHUNK_MEMCPY, SWAP_STAGED_DMA = 0, 1, 2
 INF = 0xFFFFFFFF
@@ -92,6 +93,7 @@ def load_library(path=LIB_PATH):
         "autx_end_program": ([P, u64], i32),
         "autx_complete": ([P, P, u32], i32),
         "autx_register_call": ([P, P, u32], i32),
+        "autx_register_call_dag": ([P, P, u32, P, P], i32),
         "autx_sched_step": ([P, u32, C.POINTER(StepOut)], i32),
         "autx_step_wait": ([P, C.POINTER(StepOut)], i32),
         "autx_kv_swap": ([P, C.POINTER(KvLayout), i32, C.POINTER(SwapStats)], i32),
@@ -119,7 +121,7 @@ def load_library(path=LIB_PATH):
 def exported_symbols():
     return [
         "autx_create", "autx_destroy", "autx_last_error", "autx_version", "autx_start_program",
-        "autx_end_program", "autx_complete", "autx_register_call", "autx_sched_step",
+        "autx_end_program", "autx_complete", "autx_register_call", "autx_register_call_dag", "autx_sched_step",
         "autx_step_wait", "autx_kv_swap", "autx_block_table", "autx_block_table_host", "autx_route_record_bytes",
         "autx_route_pack", "autx_route_apply", "autx_dump_calls", "autx_program_state",
         "autx_last_step_timing", "autx_set_timing", "autx_num_active", "autx_phase_times", "autx_kernel_launches"]
@@ -164,6 +166,7 @@ class Scheduler:
         cfg.stream = stream
         cfg.rank, cfg.nranks = rank, nranks
         self.cfg = cfg
+        self.eq2 = cfg.policy == ATLAS_EQ2
         self.ctx = C.c_void_p()
         st = self.lib.autx_create(C.byref(cfg), C.byref(self.ctx))
         if st != 0:
@@ -202,6 +205,14 @@ class Scheduler:
         """descs: structured array of CALL_DESC in canonical order."""
         a = np.ascontiguousarray(descs, dtype=CALL_DESC)
         self._check(self.lib.autx_register_call(self.ctx, _ptr(a), len(a)))
+
+    def register_dag(self, descs, parent_offsets, parent_ids):
+        """AUTX_ATLAS_EQ2 arrivals with their DAG parents (CSR: offsets[n+1] into parent ids)."""
+        a = np.ascontiguousarray(descs, dtype=CALL_DESC)
+        off = np.ascontiguousarray(parent_offsets, dtype=np.uint32)
+        ids = np.ascontiguousarray(parent_ids, dtype=np.uint64)
+        assert len(off) == len(a) + 1
+        self._check(self.lib.autx_register_call_dag(self.ctx, _ptr(a), len(a), _ptr(off), _ptr(ids)))
 
     def sched_step(self, t, wait=True):
         self._check(self.lib.autx_sched_step(self.ctx, int(t), C.byref(self.out)))

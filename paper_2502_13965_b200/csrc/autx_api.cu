@@ -98,6 +98,17 @@ struct autx_ctx {
   // work staged for the next sched_step's prologue kernel (single-engine mode)
   uint32_t n_comp_staged = 0, n_arr_staged = 0, arr_first_slot = 0;
   std::unordered_set<uint64_t> staged_new_progs;
+  // AUTX_ATLAS_EQ2 (Eq. 2): every call of a live program holds a lineage index; at
+  // completion the device stores p(c) + t_c there, and arrivals name their parents' indices
+  bool eq2 = false;
+  std::unordered_map<uint64_t, uint32_t> lin_of;   // call id -> lineage index
+  std::vector<uint32_t> lin_prog;                  // lineage index -> program row
+  std::vector<std::vector<uint64_t>> prog_calls;   // program row -> its calls' ids (lineage holders)
+  std::vector<uint32_t> lin_free;
+  uint32_t lin_next = 0, lin_cap = 0;
+  uint32_t* h_clin = nullptr;                      // [cslots_cap] lineage of each completion (pinned)
+  uint32_t* h_par = nullptr;                       // parents' lineage indices of staged arrivals (pinned)
+  uint32_t par_cap = 0, n_par_staged = 0;
   bool timed_complete = false, timed_register = false;   // events 4-5 / 6-7 recorded this step
   bool tc_step = false, tr_step = false;                  // ... for the step being waited on
   std::string err;
@@ -201,6 +212,16 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   ctx->slot_prog.assign(rows, 0);
   ctx->slot_arr.assign(rows, 0);
   ctx->slot_live.assign(rows, 0);
+  if (c.policy == AUTX_ATLAS_EQ2) {
+    ctx->eq2 = true;
+    ctx->lin_cap = (uint32_t)std::min<uint64_t>(4ull * c.max_calls, 0xFFFFFFF0ull);
+    CK(dalloc(&p.crit, ctx->lin_cap));
+    ctx->lin_prog.assign(ctx->lin_cap, 0);
+    ctx->prog_calls.assign(P, {});
+    CK(cudaHostAlloc((void**)&ctx->h_clin, ctx->cslots_cap * 4, cudaHostAllocMapped));
+    ctx->par_cap = 16 * BS;
+    CK(cudaHostAlloc((void**)&ctx->h_par, (size_t)ctx->par_cap * 4, cudaHostAllocMapped));
+  }
   if (c.order_mode == AUTX_ORDER_RADIX) {
     ctx->radix = true;
     size_t npad = (rows + 4095) / 4096 * 4096;
@@ -253,7 +274,8 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
     delete ctx;
     return s;
   };
-  if (c.policy < AUTX_FCFS || c.policy > AUTX_ATLAS) return bad("policy");
+  if (c.policy < AUTX_FCFS || c.policy > AUTX_ATLAS_EQ2) return bad("policy");
+  if (c.policy == AUTX_ATLAS_EQ2 && c.nranks > 1) return bad("AUTX_ATLAS_EQ2 is single-engine (nranks must be 1)");
   if (c.K < 1 || c.K > 16) return bad("K must be 1..16");
   for (uint32_t i = 0; i + 1 < c.K; ++i) {
     if (i > 0 && c.q_hi[i] < c.q_hi[i - 1]) return bad("q_hi must be ascending");
@@ -318,7 +340,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   CallTable& t = ctx->ct;
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
-                 t.loc, t.hcls, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp,
+                 t.loc, t.hcls, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
                  ctx->ctl, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
                  ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->out.tile_off,
                  ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
@@ -329,7 +351,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
                  ctx->rx.keys, ctx->rx.keys_alt, ctx->rx.dig_hist, ctx->rx.tile_hist};
   for (void* p : dev) if (p) cudaFree(p);
   void* host[] = {ctx->h_outblk,
-                  ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr,
+                  ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr, ctx->h_clin, ctx->h_par,
                   ctx->rx.h_dig_hist};
   for (void* p : host) if (p) cudaFreeHost(p);
   if (ctx->done) cudaEventDestroy(ctx->done);
@@ -391,6 +413,14 @@ extern "C" autx_status autx_end_program(autx_ctx* ctx, uint64_t pid) {
   if (ctx->prog_active[it->second] != 0)
     return fail(ctx, AUTX_E_STATE, "program %llu still has %u active calls", (unsigned long long)pid,
                 ctx->prog_active[it->second]);
+  if (ctx->eq2) {  // the program's Eq. 2 operands go with it
+    for (uint64_t cid : ctx->prog_calls[it->second]) {
+      auto l = ctx->lin_of.find(cid);
+      ctx->lin_free.push_back(l->second);
+      ctx->lin_of.erase(l);
+    }
+    ctx->prog_calls[it->second].clear();
+  }
   ctx->prog_free.push_back(it->second);
   ctx->prog_row.erase(it);
   return AUTX_OK;
@@ -425,6 +455,7 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
   for (uint32_t i = 0; i < n; ++i) {
     const uint32_t slot = sl[i];
     ctx->h_cslots[i] = slot;
+    if (ctx->eq2) ctx->h_clin[i] = ctx->lin_of.at(ids[i]);
     ctx->slot_live[slot] = 0;
     ctx->prog_active[ctx->slot_prog[slot]] -= 1;
     ctx->call_slot.erase(ids[i]);
@@ -468,6 +499,8 @@ static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
   else a.comp_ptr = ctx->h_cslots;
   if (a.n_arr <= (uint32_t)PRO_INLINE) memcpy(a.arr, ctx->h_arr, a.n_arr * sizeof(ArrivalRec));
   else a.arr_ptr = ctx->h_arr;
+  a.comp_lin = ctx->h_clin;  // AUTX_ATLAS_EQ2 only (read through UVA)
+  a.par = ctx->h_par;
   CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
   if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
   if (a.n_comp || a.n_arr)
@@ -481,18 +514,35 @@ static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
     CK(cudaMemcpyAsync(ctx->d_arr, ctx->h_arr, (size_t)ctx->n_arr_staged * sizeof(ArrivalRec),
                        cudaMemcpyHostToDevice, ctx->stream));
     CK(launch_register(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->d_arr, ctx->n_arr_staged,
-                       ctx->arr_first_slot, t));
+                       ctx->arr_first_slot, t, ctx->h_par));
     if (ctx->timing) {
       cudaEventRecord(ctx->ev[7], ctx->stream);
       ctx->timed_register = true;
     }
   }
   ctx->n_comp_staged = ctx->n_arr_staged = 0;
+  ctx->n_par_staged = 0;
   ctx->staged_new_progs.clear();
   return AUTX_OK;
 }
 
+static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n, const uint32_t* poff,
+                                 const uint64_t* pids);
+
 extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n) {
+  return register_impl(ctx, calls, n, nullptr, nullptr);
+}
+
+extern "C" autx_status autx_register_call_dag(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n,
+                                              const uint32_t* poff, const uint64_t* pids) {
+  if (!ctx) return AUTX_E_INVAL;
+  if (!ctx->eq2) return fail(ctx, AUTX_E_INVAL, "autx_register_call_dag needs policy AUTX_ATLAS_EQ2");
+  if (n && !poff) return AUTX_E_INVAL;
+  return register_impl(ctx, calls, n, poff, pids);
+}
+
+static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n, const uint32_t* poff,
+                                 const uint64_t* pids) {
   if (!ctx || (n && !calls)) return AUTX_E_INVAL;
   if (n == 0) return AUTX_OK;
   autx_status s = sync_last(ctx);
@@ -535,6 +585,42 @@ extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* c
   }
   if (ctx->prog_free.size() + (ctx->cfg.max_programs - ctx->prog_next) < new_progs)
     return fail(ctx, AUTX_E_NOMEM, "process table full");
+  // Eq. 2 parents: completed calls of the same, live program (validated before any mutation)
+  uint32_t n_par = 0;
+  if (poff) {
+    if (poff[n] < poff[0]) return fail(ctx, AUTX_E_INVAL, "parent offsets not ascending");
+    n_par = poff[n] - poff[0];
+    if (n_par && !pids) return AUTX_E_INVAL;
+    for (uint32_t i = 0; i < n; ++i) {
+      if (poff[i + 1] < poff[i]) return fail(ctx, AUTX_E_INVAL, "parent offsets not ascending");
+      if (poff[i + 1] - poff[i] >= (1u << 24)) return fail(ctx, AUTX_E_INVAL, "too many parents");
+      auto pr = ctx->prog_row.find(calls[i].program_id);
+      for (uint32_t k = poff[i]; k < poff[i + 1]; ++k) {
+        auto l = ctx->lin_of.find(pids[k]);
+        if (l == ctx->lin_of.end())
+          return fail(ctx, AUTX_E_NOENT, "parent %llu of call %llu is unknown", (unsigned long long)pids[k],
+                      (unsigned long long)calls[i].call_id);
+        if (ctx->call_slot.count(pids[k]))
+          return fail(ctx, AUTX_E_STATE, "parent %llu of call %llu has not completed", (unsigned long long)pids[k],
+                      (unsigned long long)calls[i].call_id);
+        if (pr == ctx->prog_row.end() || ctx->lin_prog[l->second] != pr->second)
+          return fail(ctx, AUTX_E_INVAL, "parent %llu of call %llu is in another program",
+                      (unsigned long long)pids[k], (unsigned long long)calls[i].call_id);
+      }
+    }
+  }
+  if (ctx->eq2 && ctx->lin_free.size() + (ctx->lin_cap - ctx->lin_next) < n)
+    return fail(ctx, AUTX_E_NOMEM, "Eq. 2 lineage capacity (%u) exhausted", ctx->lin_cap);
+  if (ctx->n_par_staged + n_par > ctx->par_cap) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    const uint32_t cap = std::max(ctx->n_par_staged + n_par, 2 * ctx->par_cap);
+    uint32_t* nh = nullptr;
+    CK(cudaHostAlloc((void**)&nh, (size_t)cap * 4, cudaHostAllocMapped));
+    if (ctx->n_par_staged) memcpy(nh, ctx->h_par, (size_t)ctx->n_par_staged * 4);
+    cudaFreeHost(ctx->h_par);
+    ctx->h_par = nh;
+    ctx->par_cap = cap;
+  }
   if ((uint64_t)ctx->call_slot.size() + n > ctx->cfg.max_calls)
     return fail(ctx, AUTX_E_NOMEM, "call table full (%u active)", (unsigned)ctx->call_slot.size());
   if ((uint64_t)ctx->tail + n > ctx->cfg.max_calls) {
@@ -581,6 +667,21 @@ extern "C" autx_status autx_register_call(autx_ctx* ctx, const autx_call_desc* c
     r.cid = d.call_id;
     r.prog = row;
     r.tok = d.input_tokens;
+    if (ctx->eq2) {
+      uint32_t np = 0;
+      if (poff) {
+        np = poff[i + 1] - poff[i];
+        r.par = ctx->n_par_staged;
+        for (uint32_t k = poff[i]; k < poff[i + 1]; ++k) ctx->h_par[ctx->n_par_staged++] = ctx->lin_of[pids[k]];
+      }
+      flags |= np << 8;
+      uint32_t L;
+      if (!ctx->lin_free.empty()) { L = ctx->lin_free.back(); ctx->lin_free.pop_back(); }
+      else L = ctx->lin_next++;
+      ctx->lin_of[d.call_id] = L;
+      ctx->lin_prog[L] = row;
+      ctx->prog_calls[row].push_back(d.call_id);
+    }
     r.flags = flags;
     stage[i] = r;
     uint32_t slot = ctx->tail + i;
@@ -622,12 +723,14 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
     arr_base = ctx->low < ctx->tail ? ctx->slot_arr[ctx->low] : t;
     if (t - arr_base >= (1u << 27)) return fail(ctx, AUTX_E_NOMEM, "arrival span exceeds the 27-bit key field");
   }
+  // rows registered in this step start here (the scan reads older rows before the prologue ends)
+  const uint32_t first_new = ctx->n_arr_staged ? ctx->arr_first_slot : ctx->tail;
   s = flush_staged(ctx, t);
   if (s) return s;
   ++ctx->seqno;
   CK(launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv, ctx->kv_on, t,
                  ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr, ctx->radix ? &ctx->rx : nullptr,
-                 arr_base, &ctx->radix_passes));
+                 arr_base, &ctx->radix_passes, first_new));
   if (!ctx->out.zero_copy)
     CK(cudaMemcpyAsync(ctx->h_outblk, ctx->d_outblk, ctx->outblk_bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->done, ctx->stream));

@@ -52,6 +52,7 @@ struct ProgTable {
   PInfo* info;          // service + waiting time
   uint32_t* last_arr;   // most recent call arrival
   uint32_t* last_comp;  // most recent call completion
+  uint32_t* crit;       // AUTX_ATLAS_EQ2: p(c) + t_c of completed calls, by lineage index (Eq. 2)
 };
 
 struct Policy {
@@ -234,8 +235,9 @@ struct ArrivalRec {
   uint64_t cid;
   uint32_t prog;
   uint32_t tok;
-  uint32_t flags;  // bit0: program is new in this batch (inh = 0); bit1: first record of it
-  uint32_t _pad;
+  uint32_t flags;  // bit0: program is new in this batch (inh = 0); bit1: first record of it;
+                   // bits 8-31 (AUTX_ATLAS_EQ2): number of DAG parents
+  uint32_t par;    // AUTX_ATLAS_EQ2: offset of the parents' lineage indices in PrologueArgs::par
 };
 
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
@@ -267,6 +269,8 @@ struct PrologueArgs {
   uint32_t n_prog_rows, _pad[3];  // process-table rows in use (prefetched into L2 for the scan)
   const uint32_t* comp_ptr;
   const ArrivalRec* arr_ptr;
+  const uint32_t* comp_lin;  // AUTX_ATLAS_EQ2: lineage index of each completion (mapped pinned)
+  const uint32_t* par;       // AUTX_ATLAS_EQ2: parents' lineage indices (mapped pinned)
   uint32_t comp[PRO_INLINE];
   ArrivalRec arr[PRO_INLINE];
 };
@@ -283,12 +287,13 @@ cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint
                          const RouteArr* arr, uint32_t n, int8_t* pin, uint32_t threshold,
                          int32_t* out);
 cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt,
-                            const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t);
+                            const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t,
+                            const uint32_t* par = nullptr);
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev /* 5 events or null */,
                         const RadixState* rx /* non-null: AUTX_ORDER_RADIX */, uint32_t arr_base,
-                        uint32_t* radix_passes);
+                        uint32_t* radix_passes, uint32_t first_new /* first row registered this step */);
 cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                Outputs out, RadixState rx, uint32_t t, uint32_t n_rows,
                                uint32_t arr_base, int sms, uint32_t* passes_out);

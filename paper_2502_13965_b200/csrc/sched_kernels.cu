@@ -83,7 +83,7 @@ __device__ __forceinline__ void set_err(Ctl* ctl, uint32_t code, uint32_t info) 
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ void apply_record(const Policy& pol, ProgTable pt, const CompRec& r, uint32_t t) {
   PInfo* pi = pt.info + r.prog;
-  if (pol.policy == AUTX_ATLAS) atomicMax(&pi->svc, r.cp);  // Alg. 1 l.4
+  if (pol.policy == AUTX_ATLAS || pol.policy == AUTX_ATLAS_EQ2) atomicMax(&pi->svc, r.cp);  // Alg. 1 l.4
   else atomicAdd(&pi->svc, r.exec);                          // Eq. 1
   if (r.tw) atomicAdd(&pi->pwait, (unsigned long long)r.tw);  // Alg. 1 l.5-6, R5
   pt.last_comp[r.prog] = t;
@@ -92,7 +92,7 @@ __device__ __forceinline__ void apply_record(const Policy& pol, ProgTable pt, co
 template <int NT>
 __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, Ctl* ctl, const uint32_t* slots,
                               uint32_t n, uint32_t t, KvState& kv, bool kv_on, CompRec* rec_out, bool apply,
-                              CompRec* s_rec = nullptr) {
+                              CompRec* s_rec = nullptr, const uint32_t* lin = nullptr) {
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
   STAMP(16);
@@ -111,6 +111,7 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       r.tw = (t - ct.arr[s]) - e;  // totwait: active steps arr..t-1 that did not run
       rec_out[i] = r;
       if (s_rec) s_rec[i] = r;  // the caller's shared-memory copy (n <= NT)
+      if (lin) pt.crit[lin[i]] = r.cp;  // AUTX_ATLAS_EQ2: p(c) + t_c, an Eq. 2 operand
     }
     STAMP(17);
     if (apply && valid) apply_record(pol, pt, r, t);
@@ -233,12 +234,25 @@ __device__ __forceinline__ void register_one(const Policy& pol, CallTable& ct, P
   ct.hcls[s] = 0;
 }
 
+// Eq. 2: p(c_j) = 0 for a root, else max over the parents c_k of p(c_k) + t_k; the
+// parents' values were stored at their completion (complete_body), in this kernel before a
+// barrier or in an earlier one, hence read from L2.
+__device__ __forceinline__ uint32_t eq2_priority(const ProgTable& pt, const uint32_t* par, const ArrivalRec& r) {
+  uint32_t p = 0;
+  const uint32_t np = r.flags >> 8;
+  for (uint32_t k = 0; k < np; ++k) p = max(p, __ldcg(&pt.crit[par[r.par + k]]));
+  return p;
+}
+
 __global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const ArrivalRec* recs,
-                           uint32_t n, uint32_t first_slot, uint32_t t) {
+                           uint32_t n, uint32_t first_slot, uint32_t t, const uint32_t* par) {
   pdl_wait();
   pdl_trigger();
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) register_one(pol, ct, pt, recs[i], first_slot + i, t);
+  if (i >= n) return;
+  const ArrivalRec r = recs[i];
+  if (pol.policy == AUTX_ATLAS_EQ2) register_one(pol, ct, pt, r, first_slot + i, t, true, eq2_priority(pt, par, r));
+  else register_one(pol, ct, pt, r, first_slot + i, t);
 }
 
 // Fused prologue of one step: completions (a1) then arrivals (a2), one CTA; a typical step's
@@ -265,15 +279,19 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
     // reductions leave in the row), so the row loads go out with the completion loads: one round
     __shared__ CompRec s_rec[PRO_INLINE];
     uint32_t svc_old = 0;
+    const bool eq2 = pol.policy == AUTX_ATLAS_EQ2;
     const bool my_arr = tid < a.n_arr;
-    if (my_arr && !(s_arr[tid].flags & 1u)) svc_old = __ldcg(&pt.info[s_arr[tid].prog].svc);
+    if (my_arr && !eq2 && !(s_arr[tid].flags & 1u)) svc_old = __ldcg(&pt.info[s_arr[tid].prog].svc);
     if (a.n_comp)
-      complete_body<PRO_THREADS>(pol, ct, pt, ctl, s_comp, a.n_comp, a.t, kv, kv_on, rec_out, true, s_rec);
+      complete_body<PRO_THREADS>(pol, ct, pt, ctl, s_comp, a.n_comp, a.t, kv, kv_on, rec_out, true, s_rec,
+                                 eq2 ? a.comp_lin : nullptr);
     __syncthreads();
     if (my_arr) {
       const ArrivalRec r = s_arr[tid];
       uint32_t inh = 0;
-      if (!(r.flags & 1u)) {
+      if (eq2) {
+        inh = eq2_priority(pt, a.par, r);  // parents completed this step are stored above the barrier
+      } else if (!(r.flags & 1u)) {
         inh = svc_old;
         for (uint32_t i = 0; i < a.n_comp; ++i)
           if (s_rec[i].prog == r.prog) inh = pol.policy == AUTX_ATLAS ? max(inh, s_rec[i].cp) : inh + s_rec[i].exec;
@@ -283,15 +301,19 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
     CHAIN_END(0);
     return;
   }
+  const bool eq2 = pol.policy == AUTX_ATLAS_EQ2;
   if (a.n_comp)
     complete_body<PRO_THREADS>(pol, ct, pt, ctl, comp_inline ? s_comp : a.comp_ptr, a.n_comp, a.t, kv, kv_on,
-                               rec_out, true);
+                               rec_out, true, nullptr, eq2 ? a.comp_lin : nullptr);
   // arrivals inherit the service updated by this step's completions (R10): the reductions are
   // performed at L2 before the barrier releases (fence), and register_one reads svc from L2
   if (a.n_comp && a.n_arr) __threadfence();
   __syncthreads();
   const ArrivalRec* arr = arr_inline ? s_arr : a.arr_ptr;
-  for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) register_one(pol, ct, pt, arr[i], a.first_slot + i, a.t);
+  for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) {
+    if (eq2) register_one(pol, ct, pt, arr[i], a.first_slot + i, a.t, true, eq2_priority(pt, a.par, arr[i]));
+    else register_one(pol, ct, pt, arr[i], a.first_slot + i, a.t);
+  }
   CHAIN_END(0);
 }
 
@@ -450,29 +472,70 @@ enum { SEL_KERNEL = 0, SEL_FUSED = 1, SEL_GATHER = 2 };
 // registers so that 4 CTAs fit per SM (592 tiles = 1.2M rows resident at once).  Every row's
 // program-row gather is issued in one round (no per-tile serialisation as in the persistent
 // kernel), which is what bounds this latency-bound pass.  Per-row arithmetic is identical.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// pre (A/B switch AUTX_SCAN_PRE): what a CTA does while it waits for the prologue (PDL).  Rows
+// below first_new (this step's first arrival slot) keep prog/base/mtime through the prologue
+// (it writes only new rows and the qf/loc of completed ones; everything earlier in the stream
+// is complete once this grid runs), so they may be read before the wait; qf, the program rows
+// and new rows are read after it.  0: nothing early; 1: prog early + L2 prefetch of the rows'
+// program entries and of the previous batch's records (the gather's cold reads); 2: prog, base
+// and mtime early + the same prefetches.
 template <int sel_mode>
 __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                               Outputs out, uint32_t t, uint32_t n_rows) {
-  // (loading prog/base/mtime before the PDL wait, overlapping the prologue, was measured: the
-  // prologue's loads then queue behind these in DRAM and the step gains nothing)
-  pdl_wait();
-  pdl_trigger();
-  CHAIN_BEGIN(1);
+                                                               Outputs out, uint32_t t, uint32_t n_rows,
+                                                               uint32_t first_new, uint32_t pre) {
   constexpr int NW = SCAN_THREADS / 32;
   __shared__ uint32_t wq16[NW][MAX_K / 2];  // per warp: 16-bit counts of queues 2w, 2w + 1
   __shared__ uint32_t wn[NW];
   const uint32_t tid = threadIdx.x, tile = blockIdx.x;
   const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  const bool early = pre != 0 && row0 + ROWS_PER_THREAD <= first_new;
+  uint4 p0, p1, b0, b1, m0, m1;
+  if (early) {
+    p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+    p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    if (pre >= 2) {
+      b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+      b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+      m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+      m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+    }
+  }
+  if (pre != 0) {
+    // the previous batch's records: region B and most of region A in the gather
+    const uint32_t i = (gridDim.x - 1 - tile) * SCAN_THREADS + tid;
+    if (i < ctl->n_prev) {
+      const uint32_t sl = out.prev_slots[i];
+      prefetch_l2(ct.cid + sl); prefetch_l2(ct.arr + sl); prefetch_l2(ct.tok + sl);
+      prefetch_l2(ct.exec + sl); prefetch_l2(ct.mtime + sl); prefetch_l2(ct.quanta + sl);
+    }
+    if (early && pol.beta_den != 0) {
+      const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j == 0 || pr[j] != pr[j - 1]) prefetch_l2(pt.info + pr[j]);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(1);
   uint64_t hq = 0;
   uint32_t npromo = 0, nlive = 0;
   if (row0 < n_rows) {
     const uint2 qv = __ldcs(reinterpret_cast<const uint2*>(ct.qf + row0));
-    const uint4 p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
-    const uint4 p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
-    const uint4 b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
-    const uint4 b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
-    const uint4 m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
-    const uint4 m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+    if (!early) {
+      p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+      p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    }
+    if (!early || pre < 2) {
+      b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+      b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+      m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+      m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+    }
     uint32_t qfs[8], prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
     uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
     uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
@@ -481,14 +544,39 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallT
     const bool anti = pol.beta_den != 0;
     const uint32_t bnum = pol.beta_num, bden = pol.beta_den, quanta0 = pol.quanta[0];
     // the program rows of all 8 rows in one round (svc and pwait only: 12 of the 16 bytes)
-    uint32_t svc[8];
-    unsigned long long pw[8];
+    uint32_t svc[8], pwl[8];
+    uint32_t big = t & 0x80000000u;  // any operand >= 2^31: this thread needs the exact path
     if (anti) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const bool live = !(qfs[j] & QF_DEAD);
+        const uint2 pw = live ? __ldg(reinterpret_cast<const uint2*>(&pt.info[prog[j]].pwait)) : make_uint2(0u, 0u);
         svc[j] = live ? __ldg(&pt.info[prog[j]].svc) : 0u;
-        pw[j] = live ? __ldg(&pt.info[prog[j]].pwait) : 0ull;
+        pwl[j] = pw.x;
+        big |= pw.y | ((pw.x | svc[j]) & 0x80000000u);
+      }
+    }
+    // Alg. 1 l.24-26 (R3, R4).  With t, svc and pwait below 2^31 (wait, mtime <= t), W and T
+    // are below 2^32, so W * beta_den >= beta_num * T is exact as two 32x32->64 products.  A
+    // warp holding any larger operand takes the 128-bit comparison (starving()) for all its rows.
+    uint32_t stv = 0;  // bit j: row j starving (not 0/0 and the ratio test holds)
+    if (anti) {
+      // (lanes past n_rows skip this block: vote among the lanes present; each lane still sees
+      // its own operand, so the choice is exact whichever lanes take part)
+      if (__any_sync(__activemask(), big != 0)) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool live = !(qfs[j] & QF_DEAD);
+          const PInfo pi = live ? pt.info[ct.prog[row0 + j]] : PInfo{0, 0, 0ull};  // rare: reload
+          stv |= starving(pol, pi, t - base[j] - mtim[j], mtim[j]) ? 1u << j : 0u;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t W = pwl[j] + (t - base[j] - mtim[j]), T = svc[j] + mtim[j];
+          const bool st = (W | T) != 0 && (uint64_t)W * bden >= (uint64_t)T * bnum;
+          stv |= st ? 1u << j : 0u;
+        }
       }
     }
     bool wq = false, wb = false, wm = false;
@@ -497,15 +585,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallT
       const uint32_t qf = qfs[j];
       const bool live = !(qf & QF_DEAD);
       uint32_t q = qf & QF_QMASK;
-      bool pr = false;
-      if (anti) {
-        const uint32_t wait = t - base[j] - mtim[j];
-        const uint32_t W32 = (uint32_t)pw[j] + wait, T32 = svc[j] + mtim[j];
-        const bool fast = (uint32_t)(pw[j] >> 32) == 0 && W32 >= wait && T32 >= svc[j];
-        bool st = (W32 | T32) != 0 && (uint64_t)W32 * bden >= (uint64_t)T32 * bnum;
-        if (!fast) st = starving(pol, PInfo{svc[j], 0, pw[j]}, wait, mtim[j]);
-        pr = live && st;  // Alg. 1 l.26
-      }
+      const bool pr = live && ((stv >> j) & 1u);  // Alg. 1 l.26
       if (pr && (q | mtim[j])) ct.quanta[row0 + j] = quanta0;
       wq |= pr && q != 0;
       wm |= pr && mtim[j] != 0;
@@ -1794,9 +1874,10 @@ cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint
 }
 
 cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt,
-                            const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t) {
+                            const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t,
+                            const uint32_t* par) {
   if (n == 0) return cudaSuccess;
-  return launch_pdl(k_register, (n + 255) / 256, 256, 0, s, pol, ct, pt, recs, n, first_slot, t);
+  return launch_pdl(k_register, (n + 255) / 256, 256, 0, s, pol, ct, pt, recs, n, first_slot, t, par);
   return cudaGetLastError();
 }
 
@@ -1809,7 +1890,7 @@ static uint32_t pow2_at_least(uint32_t x) {
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev, const RadixState* rx, uint32_t arr_base,
-                        uint32_t* radix_passes) {
+                        uint32_t* radix_passes, uint32_t first_new) {
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
   out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
@@ -1844,8 +1925,11 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       if (ev) cudaEventRecord(ev[1], s);
       launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     } else if (!bulk && !fuse) {
-      if (sel_kernel) launch_pdl(k_scan_tile<SEL_KERNEL>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows);
-      else launch_pdl(k_scan_tile<SEL_GATHER>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows);
+      static const uint32_t pre = getenv("AUTX_SCAN_PRE") ? (uint32_t)atoi(getenv("AUTX_SCAN_PRE")) : 0u;
+      if (sel_kernel)
+        launch_pdl(k_scan_tile<SEL_KERNEL>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, first_new, pre);
+      else
+        launch_pdl(k_scan_tile<SEL_GATHER>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, first_new, pre);
       if (ev) cudaEventRecord(ev[1], s);
       if (sel_kernel) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     } else {

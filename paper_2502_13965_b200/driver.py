@@ -67,6 +67,7 @@ class TraceDriver:
         tr = self.tr
         cs = np.asarray(self.ready.pop(t, []), np.int64)
         d = np.zeros(len(cs), CALL_DESC)
+        self.arr_idx = cs
         if len(cs) == 0:
             return d
         p = tr.call_prog[cs]
@@ -76,7 +77,18 @@ class TraceDriver:
         d["program_arrival_step"] = tr.prog_arrival[p]
         d["input_tokens"] = tr.input_tokens[cs]
         order = np.lexsort((d["call_id"], d["program_id"], d["program_arrival_step"]))
+        self.arr_idx = cs[order]
         return d[order]
+
+    def parents_csr(self, idx):
+        """The arrivals' DAG parents as (offsets[n+1], parent call ids): the program tells the
+        scheduler a call's parents when the call arrives."""
+        tr = self.tr
+        cnt = tr.par_ptr[idx + 1] - tr.par_ptr[idx]
+        off = np.zeros(len(idx) + 1, np.int64)
+        np.cumsum(cnt, out=off[1:])
+        pos = np.repeat(tr.par_ptr[idx] - off[:-1], cnt) + np.arange(int(off[-1]))
+        return off.astype(np.uint32), tr.call_id[tr.par[pos]]
 
     def issue(self):
         """Host half of one engine step: completions, session ends, arrivals, sched_step.
@@ -96,7 +108,10 @@ class TraceDriver:
             s.end_program(pid)
         t2 = pc()
         if len(arr):
-            s.register(arr)
+            if getattr(s, "eq2", False):
+                s.register_dag(arr, *self.parents_csr(self.arr_idx))
+            else:
+                s.register(arr)
         t3 = pc()
         s.sched_step(t, wait=False)
         t4 = pc()

@@ -18,6 +18,8 @@ VARIANTS = {
     "scan_simple": {"AUTX_SCAN_SIMPLE": "1"},    # plain per-tile pass + selection kernel
     "fused": {"AUTX_FUSE": "1"},                 # last-CTA fusions (select into scan, finalize into rank)
     "dma_out": {"AUTX_DMA_OUT": "1"},            # host lists by one copy instead of zero-copy stores
+    "scan_pre1": {"AUTX_SCAN_PRE": "1"},         # scan reads prog + prefetches before the PDL wait
+    "scan_pre2": {"AUTX_SCAN_PRE": "2"},         # ... prog, base, mtime before the wait
 }
 
 SUBSET = "fig2 or atlas_dag or mcts or chatbot or compaction or react or (random_tiny and 7)"
