@@ -725,12 +725,32 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   }
   // rows registered in this step start here (the scan reads older rows before the prologue ends)
   const uint32_t first_new = ctx->n_arr_staged ? ctx->arr_first_slot : ctx->tail;
-  s = flush_staged(ctx, t);
-  if (s) return s;
+  // the step prologue rides in the dense pass (k_scan_fused) when its records fit the kernel
+  // parameters, one engine, no KV allocator, a scalar policy and the default pipeline
+  const bool fuse = ctx->cfg.nranks <= 1 && !ctx->radix && !ctx->kv_on && !ctx->eq2 &&
+                    ctx->n_comp_staged <= (uint32_t)PRO_INLINE && ctx->n_arr_staged <= (uint32_t)PRO_INLINE &&
+                    step_can_fuse_prologue();
+  PrologueArgs fa;
+  if (fuse) {
+    memset(&fa, 0, offsetof(PrologueArgs, comp));
+    fa.n_comp = ctx->n_comp_staged;
+    fa.n_arr = ctx->n_arr_staged;
+    fa.first_slot = ctx->arr_first_slot;
+    fa.t = t;
+    fa.n_prog_rows = ctx->prog_next;
+    memcpy(fa.comp, ctx->h_cslots, fa.n_comp * sizeof(uint32_t));
+    memcpy(fa.arr, ctx->h_arr, fa.n_arr * sizeof(ArrivalRec));
+    ctx->n_comp_staged = ctx->n_arr_staged = ctx->n_par_staged = 0;
+    ctx->staged_new_progs.clear();
+  } else {
+    s = flush_staged(ctx, t);
+    if (s) return s;
+  }
   ++ctx->seqno;
   CK(launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv, ctx->kv_on, t,
                  ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr, ctx->radix ? &ctx->rx : nullptr,
-                 arr_base, &ctx->radix_passes, first_new));
+                 arr_base, &ctx->radix_passes, first_new, fuse ? &fa : nullptr,
+                 reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr)), ctx->d_cslots, ctx->d_arr));
   if (!ctx->out.zero_copy)
     CK(cudaMemcpyAsync(ctx->h_outblk, ctx->d_outblk, ctx->outblk_bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->done, ctx->stream));

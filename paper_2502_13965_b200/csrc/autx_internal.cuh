@@ -266,13 +266,22 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
 constexpr int PRO_INLINE = 96;
 struct PrologueArgs {
   uint32_t n_comp, n_arr, first_slot, t;
-  uint32_t n_prog_rows, _pad[3];  // process-table rows in use (prefetched into L2 for the scan)
+  uint32_t n_prog_rows, _pad[3];  // process-table rows in use
   const uint32_t* comp_ptr;
   const ArrivalRec* arr_ptr;
   const uint32_t* comp_lin;  // AUTX_ATLAS_EQ2: lineage index of each completion (mapped pinned)
   const uint32_t* par;       // AUTX_ATLAS_EQ2: parents' lineage indices (mapped pinned)
   uint32_t comp[PRO_INLINE];
   ArrivalRec arr[PRO_INLINE];
+};
+
+// A step prologue fused into the dense pass (k_scan_fused): its records, and where the pass leaves
+// them for the process-table commit in k_gather_ss.
+struct FusedCommit {
+  uint32_t on, n_comp, n_arr, _pad;
+  const CompRec* rec;
+  const uint32_t* cslots;
+  const ArrivalRec* arr;
 };
 
 // ---- kernel launchers (sched_kernels.cu / swap_kernels.cu) ----------------------------------
@@ -289,11 +298,15 @@ cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint
 cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt,
                             const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t,
                             const uint32_t* par = nullptr);
+bool step_can_fuse_prologue();
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev /* 5 events or null */,
                         const RadixState* rx /* non-null: AUTX_ORDER_RADIX */, uint32_t arr_base,
-                        uint32_t* radix_passes, uint32_t first_new /* first row registered this step */);
+                        uint32_t* radix_passes, uint32_t first_new /* first row registered this step */,
+                        const PrologueArgs* fused = nullptr /* non-null: fuse the prologue into the scan */,
+                        CompRec* fused_rec = nullptr, uint32_t* fused_cslots = nullptr,
+                        ArrivalRec* fused_arr = nullptr);
 cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                Outputs out, RadixState rx, uint32_t t, uint32_t n_rows,
                                uint32_t arr_base, int sms, uint32_t* passes_out);

@@ -208,18 +208,11 @@ __global__ void k_route(const char* base, uint64_t stride, uint32_t G, const Rou
 // ---------------------------------------------------------------------------------------------
 // a2: arrivals (Alg. 1 l.9-14).  Rows are appended in canonical order; row index = seq.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void register_one(const Policy& pol, CallTable& ct, ProgTable& pt, const ArrivalRec& r,
-                                             uint32_t s, uint32_t t, bool have_inh = false, uint32_t inh_given = 0) {
-  uint32_t p = r.prog;
-  if (r.flags & 2u) {  // first record of a program new in this batch: create its entry
-    pt.info[p] = PInfo{0, 0, 0ull};
-    pt.last_comp[p] = NONE;
-  }
-  // Alg. 1 l.11: the service after this step's completions (given by the caller, or read from L2
-  // after the caller's fence: see k_prologue)
-  uint32_t inh = have_inh ? inh_given : (r.flags & 1u) ? 0u : __ldcg(&pt.info[p].svc);
-  pt.last_arr[p] = t;
-  uint32_t q = place_queue(pol, inh);             // Alg. 1 l.12
+// The call-table row of an arrival that inherits `inh` (Alg. 1 l.11-13); returns its queue.
+__device__ __forceinline__ uint32_t register_row(const Policy& pol, CallTable& ct, const ArrivalRec& r, uint32_t s,
+                                                 uint32_t t, uint32_t inh) {
+  const uint32_t p = r.prog;
+  const uint32_t q = place_queue(pol, inh);       // Alg. 1 l.12
   ct.cid[s] = r.cid;
   ct.prog[s] = p;
   ct.arr[s] = t;
@@ -232,6 +225,21 @@ __device__ __forceinline__ void register_one(const Policy& pol, CallTable& ct, P
   ct.tok[s] = r.tok;
   ct.loc[s] = NONE;
   ct.hcls[s] = 0;
+  return q;
+}
+
+__device__ __forceinline__ void register_one(const Policy& pol, CallTable& ct, ProgTable& pt, const ArrivalRec& r,
+                                             uint32_t s, uint32_t t, bool have_inh = false, uint32_t inh_given = 0) {
+  uint32_t p = r.prog;
+  if (r.flags & 2u) {  // first record of a program new in this batch: create its entry
+    pt.info[p] = PInfo{0, 0, 0ull};
+    pt.last_comp[p] = NONE;
+  }
+  // Alg. 1 l.11: the service after this step's completions (given by the caller, or read from L2
+  // after the caller's fence: see k_prologue)
+  uint32_t inh = have_inh ? inh_given : (r.flags & 1u) ? 0u : __ldcg(&pt.info[p].svc);
+  pt.last_arr[p] = t;
+  register_row(pol, ct, r, s, t, inh);
 }
 
 // Eq. 2: p(c_j) = 0 for a root, else max over the parents c_k of p(c_k) + t_k; the
@@ -476,6 +484,145 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// Per-row core of the dense pass over one thread's 8 rows (Alg. 1 l.24-30): program-row gather
+// (adj may correct it, see k_scan_fused), anti-starvation, promotion writes, queue histogram.
+struct NoAdj {
+  __device__ __forceinline__ void operator()(int, uint32_t, uint32_t&, unsigned long long&) const {}
+};
+template <typename Adj, int R>
+__device__ __forceinline__ void dense_rows(const Policy& pol, CallTable& ct, const ProgTable& pt, uint32_t t,
+                                           uint32_t row0, uint32_t (&qfs)[R], const uint32_t (&prog)[R],
+                                           uint32_t (&base)[R], uint32_t (&mtim)[R], bool wq0, const Adj& adj,
+                                           uint64_t& hq, uint32_t& npromo, uint32_t& nlive) {
+  static_assert(R == 4 || R == 8, "rows per thread");
+  const bool anti = pol.beta_den != 0;
+  const uint32_t bnum = pol.beta_num, bden = pol.beta_den, quanta0 = pol.quanta[0];
+  // the program rows of all 8 rows in one round (svc and pwait only: 12 of the 16 bytes)
+  uint32_t svc[R], pwl[R];
+  uint32_t big = t & 0x80000000u;  // any operand >= 2^31: this thread needs the exact path
+  if (anti) {
+    uint32_t pwh[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {  // all gathers first (one round trip), then the corrections
+      const bool live = !(qfs[j] & QF_DEAD);
+      const uint2 pw = live ? __ldg(reinterpret_cast<const uint2*>(&pt.info[prog[j]].pwait)) : make_uint2(0u, 0u);
+      svc[j] = live ? __ldg(&pt.info[prog[j]].svc) : 0u;
+      pwl[j] = pw.x;
+      pwh[j] = pw.y;
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      unsigned long long pwj = (unsigned long long)pwh[j] << 32 | pwl[j];
+      adj(j, prog[j], svc[j], pwj);
+      pwl[j] = (uint32_t)pwj;
+      big |= (uint32_t)(pwj >> 32) | (((uint32_t)pwj | svc[j]) & 0x80000000u);
+    }
+  }
+  // Alg. 1 l.24-26 (R3, R4).  With t, svc and pwait below 2^31 (wait, mtime <= t), W and T
+  // are below 2^32, so W * beta_den >= beta_num * T is exact as two 32x32->64 products.  A
+  // warp holding any larger operand takes the 128-bit comparison (starving()) for all its rows.
+  uint32_t stv = 0;  // bit j: row j starving (not 0/0 and the ratio test holds)
+  if (anti) {
+    // (lanes past n_rows skip this block: vote among the lanes present; each lane still sees
+    // its own operand, so the choice is exact whichever lanes take part)
+    if (__any_sync(__activemask(), big != 0)) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const bool live = !(qfs[j] & QF_DEAD);
+        PInfo pi = live ? pt.info[prog[j]] : PInfo{0, 0, 0ull};
+        if (live) adj(j, prog[j], pi.svc, pi.pwait);
+        stv |= starving(pol, pi, t - base[j] - mtim[j], mtim[j]) ? 1u << j : 0u;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const uint32_t W = pwl[j] + (t - base[j] - mtim[j]), T = svc[j] + mtim[j];
+        const bool st = (W | T) != 0 && (uint64_t)W * bden >= (uint64_t)T * bnum;
+        stv |= st ? 1u << j : 0u;
+      }
+    }
+  }
+  bool wq = wq0, wb = false, wm = false;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const uint32_t qf = qfs[j];
+    const bool live = !(qf & QF_DEAD);
+    uint32_t q = qf & QF_QMASK;
+    const bool pr = live && ((stv >> j) & 1u);  // Alg. 1 l.26
+    if (pr && (q | mtim[j])) ct.quanta[row0 + j] = quanta0;
+    wq |= pr && q != 0;
+    wm |= pr && mtim[j] != 0;
+    wb |= pr;
+    qfs[j] = pr ? (qf & ~(uint32_t)QF_QMASK) : qf;
+    mtim[j] = pr ? 0u : mtim[j];
+    base[j] = pr ? t : base[j];
+    q = pr ? 0u : q;
+    npromo += pr ? 1u : 0u;
+    nlive += live ? 1u : 0u;
+    hq += live ? (1ull << (4 * q)) : 0ull;
+  }
+  if (wq) {
+#pragma unroll
+    for (int h = 0; h < R / 4; ++h)
+      reinterpret_cast<uint32_t*>(ct.qf + row0)[h] =
+          qfs[4 * h] | (qfs[4 * h + 1] << 8) | (qfs[4 * h + 2] << 16) | (qfs[4 * h + 3] << 24);
+  }
+  if (wb) {
+#pragma unroll
+    for (int h = 0; h < R / 4; ++h)
+      reinterpret_cast<uint4*>(ct.base + row0)[h] = make_uint4(base[4 * h], base[4 * h + 1], base[4 * h + 2], base[4 * h + 3]);
+  }
+  if (wm) {
+#pragma unroll
+    for (int h = 0; h < R / 4; ++h)
+      reinterpret_cast<uint4*>(ct.mtime + row0)[h] = make_uint4(mtim[4 * h], mtim[4 * h + 1], mtim[4 * h + 2], mtim[4 * h + 3]);
+  }
+}
+
+// Per-tile and per-super-tile queue counts + promotion / live totals of one CTA.
+template <int sel_mode, int NT = SCAN_THREADS>
+__device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t tile, uint64_t hq,
+                                            uint32_t npromo, uint32_t nlive) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t wq16[NW][MAX_K / 2];  // per warp: 16-bit counts of queues 2w, 2w + 1
+  __shared__ uint32_t wn[NW];
+  const uint32_t tid = threadIdx.x;
+  // per-queue counts: the 4-bit per-thread fields widened to 16 bits (<= 256 per warp), two
+  // queues per word, one redux.sync per word of the K queues in use
+  const uint32_t K = pol.K;
+#pragma unroll
+  for (int w = 0; w < MAX_K / 2; ++w) {
+    if ((uint32_t)(2 * w) < K) {
+      const uint32_t f = (uint32_t)(hq >> (8 * w));
+      const uint32_t v = __reduce_add_sync(0xffffffffu, (f & 0xFu) | ((f & 0xF0u) << 12));
+      if (lane_id() == 0) wq16[warp_id()][w] = v;
+    }
+  }
+  const uint32_t pl = __reduce_add_sync(0xffffffffu, (npromo << 16) | nlive);  // <= 256 each per warp
+  if (lane_id() == 0) wn[warp_id()] = pl;
+  __syncthreads();
+  if (tid < MAX_K) {
+    uint32_t c = 0;
+    if (tid < K) {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) c += (wq16[w][tid >> 1] >> (16 * (tid & 1))) & 0xFFFFu;
+    }
+    out.tile_cnt[(size_t)tile * MAX_K + tid] = c;
+    if (sel_mode == SEL_GATHER && c) atomicAdd(out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, c);
+  } else if (tid == 32) {
+    uint32_t a = 0, b = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) { a += wn[w] >> 16; b += wn[w] & 0xFFFFu; }
+    if (sel_mode == SEL_GATHER) {
+      uint32_t* qp = ctl->qpart[blockIdx.x % QP_LINES];
+      if (a) atomicAdd(qp + MAX_K, a);
+      if (b) atomicAdd(qp + MAX_K + 1, b);
+    } else {
+      out.tile_stat[tile] = make_uint2(a, b);
+    }
+  }
+}
+
 // pre (A/B switch AUTX_SCAN_PRE): what a CTA does while it waits for the prologue (PDL).  Rows
 // below first_new (this step's first arrival slot) keep prog/base/mtime through the prologue
 // (it writes only new rows and the qf/loc of completed ones; everything earlier in the stream
@@ -487,9 +634,6 @@ template <int sel_mode>
 __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                                Outputs out, uint32_t t, uint32_t n_rows,
                                                                uint32_t first_new, uint32_t pre) {
-  constexpr int NW = SCAN_THREADS / 32;
-  __shared__ uint32_t wq16[NW][MAX_K / 2];  // per warp: 16-bit counts of queues 2w, 2w + 1
-  __shared__ uint32_t wn[NW];
   const uint32_t tid = threadIdx.x, tile = blockIdx.x;
   const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
   const bool early = pre != 0 && row0 + ROWS_PER_THREAD <= first_new;
@@ -541,113 +685,160 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallT
     uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
 #pragma unroll
     for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
-    const bool anti = pol.beta_den != 0;
-    const uint32_t bnum = pol.beta_num, bden = pol.beta_den, quanta0 = pol.quanta[0];
-    // the program rows of all 8 rows in one round (svc and pwait only: 12 of the 16 bytes)
-    uint32_t svc[8], pwl[8];
-    uint32_t big = t & 0x80000000u;  // any operand >= 2^31: this thread needs the exact path
-    if (anti) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const bool live = !(qfs[j] & QF_DEAD);
-        const uint2 pw = live ? __ldg(reinterpret_cast<const uint2*>(&pt.info[prog[j]].pwait)) : make_uint2(0u, 0u);
-        svc[j] = live ? __ldg(&pt.info[prog[j]].svc) : 0u;
-        pwl[j] = pw.x;
-        big |= pw.y | ((pw.x | svc[j]) & 0x80000000u);
-      }
-    }
-    // Alg. 1 l.24-26 (R3, R4).  With t, svc and pwait below 2^31 (wait, mtime <= t), W and T
-    // are below 2^32, so W * beta_den >= beta_num * T is exact as two 32x32->64 products.  A
-    // warp holding any larger operand takes the 128-bit comparison (starving()) for all its rows.
-    uint32_t stv = 0;  // bit j: row j starving (not 0/0 and the ratio test holds)
-    if (anti) {
-      // (lanes past n_rows skip this block: vote among the lanes present; each lane still sees
-      // its own operand, so the choice is exact whichever lanes take part)
-      if (__any_sync(__activemask(), big != 0)) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const bool live = !(qfs[j] & QF_DEAD);
-          const PInfo pi = live ? pt.info[ct.prog[row0 + j]] : PInfo{0, 0, 0ull};  // rare: reload
-          stv |= starving(pol, pi, t - base[j] - mtim[j], mtim[j]) ? 1u << j : 0u;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t W = pwl[j] + (t - base[j] - mtim[j]), T = svc[j] + mtim[j];
-          const bool st = (W | T) != 0 && (uint64_t)W * bden >= (uint64_t)T * bnum;
-          stv |= st ? 1u << j : 0u;
-        }
-      }
-    }
-    bool wq = false, wb = false, wm = false;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t qf = qfs[j];
-      const bool live = !(qf & QF_DEAD);
-      uint32_t q = qf & QF_QMASK;
-      const bool pr = live && ((stv >> j) & 1u);  // Alg. 1 l.26
-      if (pr && (q | mtim[j])) ct.quanta[row0 + j] = quanta0;
-      wq |= pr && q != 0;
-      wm |= pr && mtim[j] != 0;
-      wb |= pr;
-      qfs[j] = pr ? (qf & ~(uint32_t)QF_QMASK) : qf;
-      mtim[j] = pr ? 0u : mtim[j];
-      base[j] = pr ? t : base[j];
-      q = pr ? 0u : q;
-      npromo += pr ? 1u : 0u;
-      nlive += live ? 1u : 0u;
-      hq += live ? (1ull << (4 * q)) : 0ull;
-    }
-    if (wq) {
-      uint2 qn;
-      qn.x = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
-      qn.y = qfs[4] | (qfs[5] << 8) | (qfs[6] << 16) | (qfs[7] << 24);
-      *reinterpret_cast<uint2*>(ct.qf + row0) = qn;
-    }
-    if (wb) {
-      *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
-      *reinterpret_cast<uint4*>(ct.base + row0 + 4) = make_uint4(base[4], base[5], base[6], base[7]);
-    }
-    if (wm) {
-      *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
-      *reinterpret_cast<uint4*>(ct.mtime + row0 + 4) = make_uint4(mtim[4], mtim[5], mtim[6], mtim[7]);
-    }
+    dense_rows<NoAdj, 8>(pol, ct, pt, t, row0, qfs, prog, base, mtim, false, NoAdj{}, hq, npromo, nlive);
   }
-  // per-queue counts: the 4-bit per-thread fields widened to 16 bits (<= 256 per warp), two
-  // queues per word, one redux.sync per word of the K queues in use
-  const uint32_t K = pol.K;
-#pragma unroll
-  for (int w = 0; w < MAX_K / 2; ++w) {
-    if ((uint32_t)(2 * w) < K) {
-      const uint32_t f = (uint32_t)(hq >> (8 * w));
-      const uint32_t v = __reduce_add_sync(0xffffffffu, (f & 0xFu) | ((f & 0xF0u) << 12));
-      if (lane_id() == 0) wq16[warp_id()][w] = v;
-    }
-  }
-  const uint32_t pl = __reduce_add_sync(0xffffffffu, (npromo << 16) | nlive);  // <= 256 each per warp
-  if (lane_id() == 0) wn[warp_id()] = pl;
-  __syncthreads();
-  if (tid < MAX_K) {
-    uint32_t c = 0;
-    if (tid < K) {
-#pragma unroll
-      for (int w = 0; w < NW; ++w) c += (wq16[w][tid >> 1] >> (16 * (tid & 1))) & 0xFFFFu;
-    }
-    out.tile_cnt[(size_t)tile * MAX_K + tid] = c;
-    if (sel_mode == SEL_GATHER && c) atomicAdd(out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, c);
-  } else if (tid == 32) {
-    uint32_t a = 0, b = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) { a += wn[w] >> 16; b += wn[w] & 0xFFFFu; }
-    if (sel_mode == SEL_GATHER) {
-      uint32_t* qp = ctl->qpart[blockIdx.x % QP_LINES];
-      if (a) atomicAdd(qp + MAX_K, a);
-      if (b) atomicAdd(qp + MAX_K + 1, b);
-    } else {
-      out.tile_stat[tile] = make_uint2(a, b);
-    }
-  }
+  tile_counts<sel_mode>(pol, ctl, out, tile, hq, npromo, nlive);
   CHAIN_END(1);
+}
+
+// Fused step prologue + dense pass (the default for a single engine whose step records ride
+// inline in the parameters, without the KV allocator, scalar policies).  The a1 / a2 effects
+// the dense pass depends on are derived where they are needed instead of by a kernel before it:
+//  - completed rows (Alg. 1 l.16-18) are marked dead by the thread that owns them;
+//  - every CTA folds this step's completion records into the program rows it reads (PLAS / FCFS /
+//    MLFQ sum, ATLAS max, pwait sum: exactly what the table update leaves before arrivals, R10);
+//  - arrivals (Alg. 1 l.9-14) are registered by the threads owning their rows, inheriting that
+//    post-completion service (a program first seen in this step inherits 0);
+//  - the process-table writes of a1 / a2 (reductions, last completion / arrival, new entries)
+//    are committed by k_gather_ss's last CTA, once every CTA here has read the old rows.
+// Results are identical to k_prologue + k_scan_tile (test_variants_gpu.py: fused_prologue).  Opt-in:
+// see step_can_fuse_prologue for the measured cost.
+// this step's completion records of program p folded into its row (rare: out of line)
+struct SvcPw { unsigned long long pw; uint32_t svc; };
+__device__ __noinline__ SvcPw fold_records(const CompRec* rec, uint32_t n, bool atlas, uint32_t p, uint32_t sv,
+                                           unsigned long long w) {
+  for (uint32_t i = 0; i < n; ++i)
+    if (rec[i].prog == p) {
+      sv = atlas ? max(sv, rec[i].cp) : sv + rec[i].exec;  // Alg. 1 l.4 / Eq. 1
+      w += rec[i].tw;                                      // Alg. 1 l.5-6 (R5)
+    }
+  return SvcPw{w, sv};
+}
+
+struct FusedAdj {
+  const CompRec* rec;    // shared: this step's completion records
+  const uint32_t* filt;  // shared: 1024-bit filter over their program rows
+  uint32_t n;
+  uint32_t newmask;      // bit j: row j is an arrival of a program first seen in this step
+  bool atlas;
+  __device__ __forceinline__ void operator()(int j, uint32_t p, uint32_t& svc, unsigned long long& pw) const {
+    if ((newmask >> j) & 1u) { svc = 0; pw = 0; return; }
+    if ((filt[(p >> 5) & 31] >> (p & 31)) & 1u) {
+      const SvcPw r = fold_records(rec, n, atlas, p, svc, pw);
+      svc = r.svc;
+      pw = r.pw;
+    }
+  }
+};
+
+constexpr int FUSED_THREADS = 512, FUSED_ROWS = TILE / FUSED_THREADS;  // 4 rows per thread: no spills
+template <int sel_mode>
+__global__ void __launch_bounds__(FUSED_THREADS, 2) k_scan_fused(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                                                                 Outputs out, uint32_t n_rows, CompRec* rec_out,
+                                                                 uint32_t* comp_out, ArrivalRec* arr_out,
+                                                                 const PrologueArgs a) {
+  constexpr int R = FUSED_ROWS;
+  __shared__ CompRec s_rec[PRO_INLINE];
+  __shared__ uint32_t s_filt[32];
+  __shared__ uint32_t s_dead[TILE / 32];
+  const uint32_t tid = threadIdx.x, tile = blockIdx.x, t = a.t;
+  const uint32_t row0 = tile * TILE + tid * R;
+  if (tid < 32) s_filt[tid] = 0;
+  if (tid < TILE / 32) s_dead[tid] = 0;
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(1);
+  // (1) one round of loads: this thread's rows and, for thread i < n_comp, completion record i
+  const bool rows = row0 < n_rows;
+  uint32_t qv = 0;
+  uint4 p0{}, b0{}, m0{};
+  if (rows) {
+    qv = __ldcs(reinterpret_cast<const uint32_t*>(ct.qf + row0));
+    p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+    b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+    m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+  }
+  if (tid < a.n_comp) {
+    const uint32_t cs = a.comp[tid];
+    const uint32_t e = ct.exec[cs];
+    CompRec r;
+    r.prog = ct.prog[cs];
+    r.exec = e;
+    r.cp = ct.inh[cs] + e;           // ATLAS critical-path candidate (Alg. 1 l.4)
+    r.tw = (t - ct.arr[cs]) - e;     // totwait (R5, R29)
+    s_rec[tid] = r;
+    atomicOr(&s_filt[(r.prog >> 5) & 31], 1u << (r.prog & 31));
+    if (cs / TILE == tile) atomicOr(&s_dead[(cs % TILE) >> 5], 1u << (cs & 31));
+    if (tile == 0) { rec_out[tid] = r; comp_out[tid] = cs; }  // for the commit
+  }
+  if (tile == 0) {
+    for (uint32_t i = tid; i < a.n_arr; i += FUSED_THREADS) arr_out[i] = a.arr[i];
+    if (tid == 0) ctl->t = t;
+  }
+  __syncthreads();
+  uint64_t hq = 0;
+  uint32_t npromo = 0, nlive = 0;
+  if (rows) {
+    uint32_t qfs[R], prog[R] = {p0.x, p0.y, p0.z, p0.w};
+    uint32_t base[R] = {b0.x, b0.y, b0.z, b0.w};
+    uint32_t mtim[R] = {m0.x, m0.y, m0.z, m0.w};
+    const uint32_t deadm = (s_dead[(row0 % TILE) >> 5] >> (row0 & 31)) & ((1u << R) - 1);
+#pragma unroll
+    for (int j = 0; j < R; ++j) qfs[j] = ((deadm >> j) & 1u) ? (uint32_t)QF_DEAD : (qv >> (8 * j)) & 0xffu;
+    FusedAdj adj{s_rec, s_filt, a.n_comp, 0u, pol.policy == AUTX_ATLAS};
+    bool wq0 = deadm != 0;
+    // this step's arrivals among this thread's rows (Alg. 1 l.9-14)
+    const uint32_t fs = a.first_slot, fe = a.first_slot + a.n_arr;
+    if (row0 + R > fs && row0 < fe) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const uint32_t row = row0 + j;
+        if (row < fs || row >= fe) continue;
+        const ArrivalRec ar = a.arr[row - fs];
+        uint32_t inh = 0;
+        if (ar.flags & 1u) {
+          adj.newmask |= 1u << j;
+        } else {
+          unsigned long long pw = 0;
+          inh = __ldg(&pt.info[ar.prog].svc);
+          adj(j, ar.prog, inh, pw);  // Alg. 1 l.11: the service after this step's completions
+        }
+        qfs[j] = register_row(pol, ct, ar, row, t, inh);
+        prog[j] = ar.prog;
+        base[j] = t;
+        mtim[j] = 0;
+        wq0 = true;
+      }
+    }
+    dense_rows<FusedAdj, R>(pol, ct, pt, t, row0, qfs, prog, base, mtim, wq0, adj, hq, npromo, nlive);
+  }
+  tile_counts<sel_mode, FUSED_THREADS>(pol, ctl, out, tile, hq, npromo, nlive);
+  CHAIN_END(1);
+}
+
+// The process-table writes of a fused step prologue (see k_scan_fused), after the dense pass:
+// new entries, last arrival / completion, the completion reductions (R10: sums and maxima
+// commute), released rows.
+__device__ void commit_prologue(const Policy& pol, CallTable& ct, ProgTable& pt, uint32_t t, uint32_t nc,
+                                uint32_t na, const CompRec* rec, const uint32_t* cs, const ArrivalRec* arr) {
+  // completions first: a program that ended after them may hand its row to a program first
+  // seen in this step, whose entry must start from zero (the order of k_prologue)
+  for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+    apply_record(pol, pt, rec[i], t);
+    ct.loc[cs[i]] = NONE;
+  }
+  __threadfence();
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) {
+    const ArrivalRec r = arr[i];
+    if (r.flags & 2u) {
+      pt.info[r.prog] = PInfo{0, 0, 0ull};
+      pt.last_comp[r.prog] = NONE;
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) pt.last_arr[arr[i].prog] = t;
 }
 
 // Persistent, TMA-staged variant of the dense pass (the default): each CTA walks tiles
@@ -1306,9 +1497,14 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS, 4) k_gather_ss(Policy pol, CallTable ct, Ctl* ctl, Outputs out,
-                                                               uint32_t n_rows, uint32_t ntiles, uint32_t t) {
+                                                               uint32_t n_rows, uint32_t ntiles, uint32_t t,
+                                                               ProgTable pt, FusedCommit fc) {
   pdl_wait();
   pdl_trigger();
+  if (fc.on && blockIdx.x == gridDim.x - 1) {  // the fused prologue's table writes (k_scan_fused)
+    commit_prologue(pol, ct, pt, t, fc.n_comp, fc.n_arr, fc.rec, fc.cslots, fc.arr);
+    return;
+  }
   CHAIN_BEGIN(3);
   gather_ss_body(pol, ct, ctl, out, n_rows, ntiles, t);
   CHAIN_END(3);
@@ -1887,10 +2083,22 @@ static uint32_t pow2_at_least(uint32_t x) {
   return p;
 }
 
+// Whether launch_step fuses the step prologue into the dense pass (k_scan_fused): opt-in with
+// AUTX_FUSED_PROLOGUE=1 on the default pipeline.  Measured slower than the PDL-chained
+// k_prologue + k_scan_tile (38.2 vs 35.8 us per step at 1M calls): with 8 rows per thread the
+// record folding pushes the pass past 64 registers (spills), and at 4 rows per thread a 1M-row
+// table no longer fits one wave (2 x 512-thread CTAs per SM).
+bool step_can_fuse_prologue() {
+  static const bool ok = getenv("AUTX_FUSED_PROLOGUE") && !getenv("AUTX_SCAN_SIMPLE") && !getenv("AUTX_FUSE") &&
+                         !getenv("AUTX_SELECT_KERNEL") && !getenv("AUTX_SCAN_BULK");
+  return ok;
+}
+
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev, const RadixState* rx, uint32_t arr_base,
-                        uint32_t* radix_passes, uint32_t first_new) {
+                        uint32_t* radix_passes, uint32_t first_new, const PrologueArgs* fused,
+                        CompRec* fused_rec, uint32_t* fused_cslots, ArrivalRec* fused_arr) {
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
   out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
@@ -1925,9 +2133,13 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
       if (ev) cudaEventRecord(ev[1], s);
       launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
     } else if (!bulk && !fuse) {
-      static const uint32_t pre = getenv("AUTX_SCAN_PRE") ? (uint32_t)atoi(getenv("AUTX_SCAN_PRE")) : 0u;
+      // default 1: prog + L2 prefetches while the prologue runs (measured ~0.4 us per step)
+      static const uint32_t pre = getenv("AUTX_SCAN_PRE") ? (uint32_t)atoi(getenv("AUTX_SCAN_PRE")) : 1u;
       if (sel_kernel)
         launch_pdl(k_scan_tile<SEL_KERNEL>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, first_new, pre);
+      else if (fused)
+        launch_pdl(k_scan_fused<SEL_GATHER>, ntiles, FUSED_THREADS, 0, s, pol, ct, pt, ctl, out, n_rows, fused_rec,
+                   fused_cslots, fused_arr, *fused);
       else
         launch_pdl(k_scan_tile<SEL_GATHER>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, first_new, pre);
       if (ev) cudaEventRecord(ev[1], s);
@@ -1945,8 +2157,11 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
     if (simple || fuse || sel_kernel)
       launch_pdl(k_gather, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t);
+    else if (fused)  // one more CTA commits the fused prologue's process-table writes
+      launch_pdl(k_gather_ss, ggrid + 1, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t, pt,
+                 FusedCommit{1u, fused->n_comp, fused->n_arr, 0u, fused_rec, fused_cslots, fused_arr});
     else
-      launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t);
+      launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t, pt, FusedCommit{});
   }
   uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
   // sorted keys [np] + admit and preempt id staging [2 x even(BS)]

@@ -6,7 +6,7 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/d_build.log 2>&1
 timeout 600 python bench.py --steps 200 --no-swap --no-cpu-baseline $BENCH_ARGS > gpurun_out/d_bench.json 2> gpurun_out/d_bench.err
 python -c "import json;d=json.loads(open('gpurun_out/d_bench.json').read().splitlines()[-1]);print('bench', d['value'], round(d['ms_per_step']*1e3,2), d['breakdown_ms'], d['roofline']['frac'])" || tail -5 gpurun_out/d_bench.err
 for e in $AB; do
-  env $e timeout 600 python bench.py --steps 200 --no-swap --no-cpu-baseline $BENCH_ARGS > gpurun_out/d_bench_ab.json 2>> gpurun_out/d_bench.err
+  env ${e//+/ } timeout 600 python bench.py --steps 200 --no-swap --no-cpu-baseline $BENCH_ARGS > gpurun_out/d_bench_ab.json 2>> gpurun_out/d_bench.err
   python -c "import json;d=json.loads(open('gpurun_out/d_bench_ab.json').read().splitlines()[-1]);print('$e', d['value'], round(d['ms_per_step']*1e3,2), d['breakdown_ms'])"
 done
 if [ -n "$NCU" ]; then
@@ -16,7 +16,7 @@ fi
 if [ -n "$CHAIN" ]; then
   AUTX_NVCC_FLAGS=-DAUTX_CHAIN_STAMPS python -c "import __graft_entry__ as g; g.build()" > gpurun_out/chain_build.log 2>&1
   for e in AUTX_DEFAULT=1 $AB; do
-    env $e AUTX_BENCH_CHAIN=1 timeout 600 python bench.py --steps 100 --no-swap --no-cpu-baseline $BENCH_ARGS > gpurun_out/chain_$e.json 2>> gpurun_out/chain.err
+    env ${e//+/ } AUTX_BENCH_CHAIN=1 timeout 600 python bench.py --steps 100 --no-swap --no-cpu-baseline $BENCH_ARGS > gpurun_out/chain_$e.json 2>> gpurun_out/chain.err
     python -c "import json;d=json.loads(open('gpurun_out/chain_$e.json').read().splitlines()[-1]);print('$e', round(d['ms_per_step']*1e3,2), d['chain_us'])"
   done
   python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1

@@ -18,7 +18,8 @@ VARIANTS = {
     "scan_simple": {"AUTX_SCAN_SIMPLE": "1"},    # plain per-tile pass + selection kernel
     "fused": {"AUTX_FUSE": "1"},                 # last-CTA fusions (select into scan, finalize into rank)
     "dma_out": {"AUTX_DMA_OUT": "1"},            # host lists by one copy instead of zero-copy stores
-    "scan_pre1": {"AUTX_SCAN_PRE": "1"},         # scan reads prog + prefetches before the PDL wait
+    "scan_pre0": {"AUTX_SCAN_PRE": "0"},         # scan reads nothing before the PDL wait
+    "fused_prologue": {"AUTX_FUSED_PROLOGUE": "1"},  # prologue folded into the dense pass (k_scan_fused)
     "scan_pre2": {"AUTX_SCAN_PRE": "2"},         # ... prog, base, mtime before the wait
 }
 
