@@ -285,8 +285,10 @@ class Scheduler:
         self._check(self.lib.autx_program_state(self.ctx, int(pid), C.byref(s), C.byref(w)))
         return s.value, w.value
 
-    def set_timing(self, on=True):
-        self._check(self.lib.autx_set_timing(self.ctx, 1 if on else 0))
+    def set_timing(self, on=True, stamps=False):
+        """on: CUDA events around the step's kernels; stamps: %globaltimer chain stamps instead
+        (no events, so the PDL chain runs as in untimed steps; read with phase_times())."""
+        self._check(self.lib.autx_set_timing(self.ctx, (1 if on else 0) | (2 if stamps else 0)))
 
     def last_step_timing(self):
         t = StepTiming()

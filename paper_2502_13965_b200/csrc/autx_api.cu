@@ -148,7 +148,7 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&t.cid, rows)); CK(dalloc(&t.prog, rows)); CK(dalloc(&t.arr, rows));
   CK(dalloc(&t.qf, rows)); CK(dalloc(&t.base, rows)); CK(dalloc(&t.mtime, rows));
   CK(dalloc(&t.exec, rows)); CK(dalloc(&t.quanta, rows)); CK(dalloc(&t.inh, rows));
-  CK(dalloc(&t.tok, rows)); CK(dalloc(&t.loc, rows)); CK(dalloc(&t.hcls, rows));
+  CK(dalloc(&t.tok, rows)); CK(dalloc(&t.loc, rows)); CK(dalloc(&t.hcls, rows)); CK(dalloc(&t.bidx, rows));
   CK(cudaMemsetAsync(t.qf, QF_DEAD, rows, ctx->stream));
   CK(cudaMemsetAsync(t.prog, 0, rows * 4, ctx->stream));
   CK(cudaMemsetAsync(t.base, 0, rows * 4, ctx->stream));
@@ -186,6 +186,8 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&o.skey, 2 * BS));
   CK(dalloc(&o.sidx, 2 * BS));
   CK(dalloc(&o.srec, 2 * BS));
+  CK(dalloc(&o.prev_pos, BS));
+  CK(cudaMemsetAsync(o.prev_pos, 0, (size_t)BS * 8, ctx->stream));  // seqno 0 never matches
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K)); CK(dalloc(&o.tile_off, ntiles + 1));
   CK(dalloc(&o.sup_cnt, (ntiles / SUP_TILES + 1) * MAX_K));
   CK(cudaMemset(o.sup_cnt, 0, (ntiles / SUP_TILES + 1) * MAX_K * sizeof(uint32_t)));
@@ -340,7 +342,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   CallTable& t = ctx->ct;
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
-                 t.loc, t.hcls, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
+                 t.loc, t.hcls, t.bidx, ctx->out.prev_pos, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
                  ctx->ctl, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
                  ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->out.tile_off,
                  ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
@@ -828,7 +830,7 @@ static autx_status compact(autx_ctx* ctx) {
   CK(dalloc(&tmp.cid, n)); CK(dalloc(&tmp.prog, n)); CK(dalloc(&tmp.arr, n)); CK(dalloc(&tmp.qf, n));
   CK(dalloc(&tmp.base, n)); CK(dalloc(&tmp.mtime, n)); CK(dalloc(&tmp.exec, n));
   CK(dalloc(&tmp.quanta, n)); CK(dalloc(&tmp.inh, n)); CK(dalloc(&tmp.tok, n)); CK(dalloc(&tmp.loc, n));
-  CK(dalloc(&tmp.hcls, n));
+  CK(dalloc(&tmp.hcls, n)); CK(dalloc(&tmp.bidx, n));
   uint32_t *d_live = nullptr, *d_map = nullptr;
   CK(dalloc(&d_live, n));
   CK(dalloc(&d_map, old2new.size()));
@@ -841,7 +843,7 @@ static autx_status compact(autx_ctx* ctx) {
   CK(cp(t.qf, tmp.qf, n)); CK(cp(t.base, tmp.base, (size_t)n * 4)); CK(cp(t.mtime, tmp.mtime, (size_t)n * 4));
   CK(cp(t.exec, tmp.exec, (size_t)n * 4)); CK(cp(t.quanta, tmp.quanta, (size_t)n * 4));
   CK(cp(t.inh, tmp.inh, (size_t)n * 4)); CK(cp(t.tok, tmp.tok, (size_t)n * 4)); CK(cp(t.loc, tmp.loc, (size_t)n * 4));
-  CK(cp(t.hcls, tmp.hcls, (size_t)n * 4));
+  CK(cp(t.hcls, tmp.hcls, (size_t)n * 4)); CK(cp(t.bidx, tmp.bidx, (size_t)n * 4));
   CK(cudaMemsetAsync(t.qf + n, QF_DEAD, rows - n, ctx->stream));
   // remap the previous batch (its completed rows were DEAD and are gone from the list: the
   // previous batch entries that are not live map to NONE and must be dropped)
@@ -853,6 +855,8 @@ static autx_status compact(autx_ctx* ctx) {
   for (uint32_t s : prev) if (s < old2new.size() && old2new[s] != NONE) np.push_back(old2new[s]);
   if (!np.empty()) CK(cudaMemcpy(ctx->out.prev_slots, np.data(), np.size() * 4, cudaMemcpyHostToDevice));
   uint32_t npv = (uint32_t)np.size();
+  // dropped entries shift the previous-batch indices the running rows carry
+  if (npv) CK(launch_set_bidx(ctx->stream, ctx->ct, ctx->out.prev_slots, npv));
   CK(cudaMemcpy(reinterpret_cast<char*>(ctx->ctl) + offsetof(Ctl, n_prev), &npv, 4, cudaMemcpyHostToDevice));
   for (auto& kv : ctx->call_slot) kv.second = old2new[kv.second];
   std::vector<uint32_t> sp(rows, 0), sa(rows, 0);
@@ -868,7 +872,7 @@ static autx_status compact(autx_ctx* ctx) {
   ctx->low = 0;
   ctx->tail = n;
   void* f[] = {tmp.cid, tmp.prog, tmp.arr, tmp.qf, tmp.base, tmp.mtime, tmp.exec, tmp.quanta, tmp.inh,
-               tmp.tok, tmp.loc, tmp.hcls, d_live, d_map};
+               tmp.tok, tmp.loc, tmp.hcls, tmp.bidx, d_live, d_map};
   for (void* p : f) cudaFree(p);
   return AUTX_OK;
 }
@@ -1065,7 +1069,8 @@ extern "C" autx_status autx_last_step_timing(autx_ctx* ctx, autx_step_timing* t)
 
 extern "C" autx_status autx_set_timing(autx_ctx* ctx, int32_t on) {
   if (!ctx) return AUTX_E_INVAL;
-  ctx->timing = on != 0;
+  ctx->timing = (on & 1) != 0;       // 1: CUDA events around the step's kernels
+  ctx->pol.stamps = (on & 2) ? 1 : 0;  // 2: %globaltimer chain stamps (no events: PDL undisturbed)
   return AUTX_OK;
 }
 

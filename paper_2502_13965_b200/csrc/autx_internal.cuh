@@ -37,6 +37,7 @@ struct CallTable {
   uint32_t* tok;     // input tokens (context)
   uint32_t* loc;     // resident slot (if RES) or host arena page offset (if swapped), else NONE
   uint32_t* hcls;    // host allocation size class (if swapped)
+  uint32_t* bidx;    // index in the last batch it joined (valid while QF_RUN: previous-batch index)
 };
 
 // Process-table fields the dense pass gathers for every call, packed so that one 16-byte load
@@ -68,6 +69,7 @@ struct Policy {
   uint32_t max_blocks_per_call;
   uint32_t host_pages_lo;  // host arena pages (capped to 2^32-1)
   uint32_t bt_shift;       // log2(block_tokens) if a power of two, else 0xFF
+  uint32_t stamps;         // record chain stamps (autx_set_timing mode 2)
 };
 
 // Step control block in device memory (written by the prologue kernels).
@@ -163,7 +165,7 @@ __device__ __forceinline__ void load_rec(const struct CallTable& ct, uint32_t s,
   x.mtime = ct.mtime[s];
   x.quanta = ct.quanta[s];
   x.qf = ct.qf[s];
-  x._pad = 0;
+  x._pad = (x.qf & QF_RUN) ? ct.bidx[s] : NONE;  // previous-batch index of a running call
   *r = x;
 }
 #endif
@@ -184,6 +186,9 @@ struct Outputs {
   uint64_t* skey;            // [2 BS] keys sorted by k_rank
   uint32_t* sidx;            // [2 BS] element index of each sorted key
   CandRec* srec;             // [2 BS] candidate records in sorted order
+  unsigned long long* prev_pos;  // [max_batch] seqno << 32 | sorted position of previous-batch entry j
+                                 // (k_rank; entries that are no candidate keep an older seqno)
+  uint32_t use_prev_pos;     // finalize tests batch membership of the previous batch by prev_pos
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* sup_cnt;         // [ceil(ntiles_cap / SUP_TILES) * MAX_K] per-queue counts of super-tiles
                              // (scan: atomics; gather: prefix; finalize: reset)
@@ -299,6 +304,7 @@ cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, Pro
                             const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t,
                             const uint32_t* par = nullptr);
 bool step_can_fuse_prologue();
+cudaError_t launch_set_bidx(cudaStream_t s, CallTable ct, const uint32_t* prev_slots, uint32_t n);
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev /* 5 events or null */,

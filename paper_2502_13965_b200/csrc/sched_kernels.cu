@@ -40,17 +40,18 @@ __device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc)
 #define STAMP(i) do { if (threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
 #endif
 
-// profiling build (-DAUTX_CHAIN_STAMPS): per kernel k of the step chain, %globaltimer when CTA 0
-// passes griddepcontrol.wait (dbg[32 + 3k]), the latest CTA end (33 + 3k) and the latest CTA
-// start past the wait (34 + 3k); finalize moves dbg[32, 64) to dbg[64, 96) at the step's end
+// Chain stamps (autx_set_timing mode 2, or always in a -DAUTX_CHAIN_STAMPS build): per kernel k
+// of the step chain, %globaltimer when CTA 0 passes griddepcontrol.wait (dbg[32 + 3k]), the
+// latest CTA end (33 + 3k) and the latest CTA start past the wait (34 + 3k); finalize moves
+// dbg[32, 64) to dbg[64, 96) at the step's end.  Off by default: one uniform parameter test.
 #ifdef AUTX_CHAIN_STAMPS
-#define CHAIN_BEGIN(k) do { if (threadIdx.x == 0) { const unsigned long long g_ = globaltimer(); \
-    if (blockIdx.x == 0) ctl->dbg[32 + 3 * (k)] = g_; atomicMax(&ctl->dbg[34 + 3 * (k)], g_); } } while (0)
-#define CHAIN_END(k) do { if (threadIdx.x == 0) atomicMax(&ctl->dbg[33 + 3 * (k)], globaltimer()); } while (0)
+#define STAMPS_ON true
 #else
-#define CHAIN_BEGIN(k) do { } while (0)
-#define CHAIN_END(k) do { } while (0)
+#define STAMPS_ON (pol.stamps != 0)
 #endif
+#define CHAIN_BEGIN(k) do { if (STAMPS_ON && threadIdx.x == 0) { const unsigned long long g_ = globaltimer(); \
+    if (blockIdx.x == 0) ctl->dbg[32 + 3 * (k)] = g_; atomicMax(&ctl->dbg[34 + 3 * (k)], g_); } } while (0)
+#define CHAIN_END(k) do { if (STAMPS_ON && threadIdx.x == 0) atomicMax(&ctl->dbg[33 + 3 * (k)], globaltimer()); } while (0)
 
 // ceil(tokens / block_tokens) (R14, R28): a shift when block_tokens is a power of two
 __device__ __forceinline__ uint32_t blocks_for(const Policy& pol, uint32_t tokens) {
@@ -1265,7 +1266,7 @@ __device__ __forceinline__ void gather_body(Policy& pol, CallTable& ct, Ctl* ctl
     uint4 c4[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) c4[v] = cidv[v];
-    uint4 ar[2], tk[2], ex[2], mt[2], qt[2];
+    uint4 ar[2], tk[2], ex[2], mt[2], qt[2], bd[2];
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
       ar[v] = reinterpret_cast<const uint4*>(ct.arr + row0)[v];
@@ -1273,6 +1274,7 @@ __device__ __forceinline__ void gather_body(Policy& pol, CallTable& ct, Ctl* ctl
       ex[v] = reinterpret_cast<const uint4*>(ct.exec + row0)[v];
       mt[v] = reinterpret_cast<const uint4*>(ct.mtime + row0)[v];
       qt[v] = reinterpret_cast<const uint4*>(ct.quanta + row0)[v];
+      bd[v] = reinterpret_cast<const uint4*>(ct.bidx + row0)[v];
     }
     auto lane4 = [](const uint4& a, int k) { return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : a.w; };
 #pragma unroll
@@ -1288,7 +1290,7 @@ __device__ __forceinline__ void gather_body(Policy& pol, CallTable& ct, Ctl* ctl
         r.mtime = lane4(mt[j >> 2], j & 3);
         r.quanta = lane4(qt[j >> 2], j & 3);
         r.qf = qfs[j];
-        r._pad = 0;
+        r._pad = (qfs[j] & QF_RUN) ? lane4(bd[j >> 2], j & 3) : NONE;  // previous-batch index
         out.cand[pos] = row0 + j;
         out.cand_rec[pos] = r;
         out.ckey[pos] = cand_key(r, t);
@@ -1464,7 +1466,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
     uint4 c4[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) c4[w] = cidv[w];
-    uint4 ar[2], tk[2], ex[2], mt[2], qt[2];
+    uint4 ar[2], tk[2], ex[2], mt[2], qt[2], bd[2];
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
       ar[w] = reinterpret_cast<const uint4*>(ct.arr + row0)[w];
@@ -1472,6 +1474,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
       ex[w] = reinterpret_cast<const uint4*>(ct.exec + row0)[w];
       mt[w] = reinterpret_cast<const uint4*>(ct.mtime + row0)[w];
       qt[w] = reinterpret_cast<const uint4*>(ct.quanta + row0)[w];
+      bd[w] = reinterpret_cast<const uint4*>(ct.bidx + row0)[w];
     }
     auto lane4 = [](const uint4& a, int k) { return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : a.w; };
 #pragma unroll
@@ -1487,7 +1490,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
         r.mtime = lane4(mt[j >> 2], j & 3);
         r.quanta = lane4(qt[j >> 2], j & 3);
         r.qf = qfs[j];
-        r._pad = 0;
+        r._pad = (qfs[j] & QF_RUN) ? lane4(bd[j >> 2], j & 3) : NONE;  // previous-batch index
         out.cand[pos] = row0 + j;
         out.cand_rec[pos] = r;
         out.ckey[pos] = cand_key(r, t);
@@ -1572,23 +1575,19 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   if (e0 < n) {
     // (2) compact the candidates (same deterministic order in every CTA): sentinels rank last and
     // nobody reads them, so only the n_valid candidates are ranked and compared against
-#ifdef AUTX_CHAIN_STAMPS
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[54] = globaltimer();
-#endif
+    if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[54] = globaltimer();
     uint32_t n_valid;
     uint32_t off = block_excl_scan<uint32_t, RANK_THREADS>(nv, red_r, &n_valid);
     for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS)
       if (rk[i] != ~0ull) { ck[off] = rk[i]; ci[off] = i; ++off; }
     __syncthreads();
-#ifdef AUTX_CHAIN_STAMPS
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[55] = globaltimer();
-#endif
+    if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[55] = globaltimer();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       ctl->n_cand_b = n_valid - na;
-#ifdef AUTX_CHAIN_STAMPS
-      ctl->dbg[52] = n_valid;
-      ctl->dbg[53] = n;
-#endif
+      if (STAMPS_ON) {
+        ctl->dbg[52] = n_valid;
+        ctl->dbg[53] = n;
+      }
     }
     // (3) rank = number of smaller keys (keys are unique), RANK_SUB threads per key; the record
     // load is issued before the count so that its latency hides behind it
@@ -1604,13 +1603,14 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     }
 #pragma unroll
     for (int d = 1; d < RANK_SUB; d <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-#ifdef AUTX_CHAIN_STAMPS
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[56] = globaltimer();
-#endif
+    if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[56] = globaltimer();
     if (sub == 0 && e < n_valid) {
       out.skey[cnt] = x;
       out.sidx[cnt] = eo;
       out.srec[cnt] = rec;
+      // a running call (previous-batch entry rec._pad) publishes its sorted position: finalize
+      // tests the previous batch's membership in the new one without searching
+      if (rec.qf & QF_RUN) out.prev_pos[rec._pad] = (unsigned long long)seqno << 32 | cnt;
     }
   }
   CHAIN_END(4);
@@ -1657,6 +1657,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   uint64_t c_cid[R];
   uint32_t p_s[R], p_qf[R], p_held[R];  // previous batch: slot, flags, held blocks, order key
   uint64_t p_cid[R], p_key[R];
+  unsigned long long p_pos[R];           // seqno << 32 | sorted position (k_rank), if use_prev_pos
   unsigned long long my_kv = 0;
   {
     // all loads of this phase first, through restrict-qualified locals, so that they overlap
@@ -1664,13 +1665,14 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     const uint64_t* __restrict__ skey = out.skey;
     const CandRec* __restrict__ srec = out.srec;
     const CandRec* __restrict__ prec = out.prev_rec;
+    const unsigned long long* __restrict__ ppos = out.prev_pos;
     uint64_t kk[R];
     CandRec rc[R], pr[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       // unconditional below BS (buffers hold >= BS entries): the loads do not wait for the counts
       const uint32_t i = tid * R + r;
-      if (i < BS) { kk[r] = skey[i]; rc[r] = srec[i]; pr[r] = prec[i]; }
+      if (i < BS) { kk[r] = skey[i]; rc[r] = srec[i]; pr[r] = prec[i]; p_pos[r] = ppos[i]; }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1770,18 +1772,27 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     uint32_t pos[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) pos[r] = 0;
-    for (uint32_t step = 1u << 12; step > 0; step >>= 1) {  // n_batch <= 4096
+    if (out.use_prev_pos) {
+      // k_rank's sorted position of each previous-batch entry that was a candidate (entries that
+      // were not, e.g. of a queue below q*, keep an older seqno and are not in the batch)
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const uint32_t probe = pos[r] + step;
-        if (probe <= n_batch && uk[probe - 1] < p_key[r]) pos[r] = probe;  // pos = #keys < key
+      for (int r = 0; r < R; ++r) pos[r] = (uint32_t)(p_pos[r] >> 32) == seqno ? (uint32_t)p_pos[r] : NONE;
+    } else {
+      for (uint32_t step = 1u << 12; step > 0; step >>= 1) {  // n_batch <= 4096
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t probe = pos[r] + step;
+          if (probe <= n_batch && uk[probe - 1] < p_key[r]) pos[r] = probe;  // pos = #keys < key
+        }
       }
+#pragma unroll
+      for (int r = 0; r < R; ++r) pos[r] = pos[r] < n_batch && uk[pos[r]] == p_key[r] ? pos[r] : NONE;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t i = tid * R + r;
       if (i < n_prev && !(p_qf[r] & QF_DEAD)) {
-        const bool in = pos[r] < n_batch && uk[pos[r]] == p_key[r];
+        const bool in = pos[r] < n_batch;
         if (!in) {
           is_pre |= 1u << r;
           my_pre += (1ull << 44) | p_held[r];
@@ -1961,6 +1972,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         ct.quanta[sl] = qt;
       }
       ct.qf[sl] = (uint8_t)(q | QF_RUN | QF_RES);
+      ct.bidx[sl] = i;
       out.prev_slots[i] = sl;
     }
   }
@@ -2029,13 +2041,13 @@ __global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* 
   pdl_trigger();
   CHAIN_BEGIN(5);
   finalize_body<NT, R>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
-#ifdef AUTX_CHAIN_STAMPS
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    ctl->dbg[33 + 3 * 5] = globaltimer();
-    for (int i = 0; i < 32; ++i) { ctl->dbg[64 + i] = ctl->dbg[32 + i]; ctl->dbg[32 + i] = 0; }
+  if (STAMPS_ON) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ctl->dbg[33 + 3 * 5] = globaltimer();
+      for (int i = 0; i < 32; ++i) { ctl->dbg[64 + i] = ctl->dbg[32 + i]; ctl->dbg[32 + i] = 0; }
+    }
   }
-#endif
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -2102,6 +2114,7 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
   out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
+  out.use_prev_pos = rx ? 0u : 1u;  // k_rank publishes previous-batch positions (select mode)
   if (ev) cudaEventRecord(ev[0], s);
   if (rx) {
     static int sms = 0;
@@ -2230,6 +2243,19 @@ __global__ void k_compact(CallTable src, CallTable dst, const uint32_t* live, ui
   dst.tok[i] = src.tok[s];
   dst.loc[i] = src.loc[s];
   dst.hcls[i] = src.hcls[s];
+  dst.bidx[i] = src.bidx[s];
+}
+
+__global__ void k_set_bidx(CallTable ct, const uint32_t* prev_slots, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) ct.bidx[prev_slots[i]] = i;
+}
+
+cudaError_t launch_set_bidx(cudaStream_t s, CallTable ct, const uint32_t* prev_slots, uint32_t n) {
+  if (n == 0) return cudaSuccess;
+  ++g_kernel_launches;
+  k_set_bidx<<<(n + 255) / 256, 256, 0, s>>>(ct, prev_slots, n);
+  return cudaGetLastError();
 }
 
 __global__ void k_remap(uint32_t* slots, uint32_t n, const uint32_t* old2new) {
