@@ -18,6 +18,7 @@
 using namespace autx;
 
 unsigned long long autx::g_kernel_launches = 0;
+thread_local std::vector<autx::LaunchRec>* autx::g_launch_rec = nullptr;
 
 extern "C" uint64_t autx_kernel_launches(void) {
   return __atomic_load_n(&g_kernel_launches, __ATOMIC_RELAXED);
@@ -109,6 +110,18 @@ struct autx_ctx {
   uint32_t* h_clin = nullptr;                      // [cslots_cap] lineage of each completion (pinned)
   uint32_t* h_par = nullptr;                       // parents' lineage indices of staged arrivals (pinned)
   uint32_t par_cap = 0, n_par_staged = 0;
+  // the step's kernels replayed as a CUDA graph: one executable per launch signature (kernels,
+  // block shapes, shared memory), whose kernel nodes receive each step's parameters
+  struct StepGraph {
+    std::vector<const void*> funcs;
+    std::vector<dim3> blocks;
+    std::vector<size_t> smem;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+    std::vector<cudaGraphNode_t> nodes;
+  };
+  std::vector<StepGraph> graphs;
+  cudaStream_t cap_stream = nullptr;  // capture only (the legacy stream cannot be captured)
   bool timed_complete = false, timed_register = false;   // events 4-5 / 6-7 recorded this step
   bool tc_step = false, tr_step = false;                  // ... for the step being waited on
   std::string err;
@@ -356,6 +369,11 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
                   ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr, ctx->h_clin, ctx->h_par,
                   ctx->rx.h_dig_hist};
   for (void* p : host) if (p) cudaFreeHost(p);
+  for (auto& g : ctx->graphs) {
+    if (g.x) cudaGraphExecDestroy(g.x);
+    if (g.g) cudaGraphDestroy(g.g);
+  }
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->done) cudaEventDestroy(ctx->done);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->sev) if (e) cudaEventDestroy(e);
@@ -706,6 +724,77 @@ static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uin
   return AUTX_OK;
 }
 
+// Replays the recorded launches of one step as a CUDA graph: the step is a launch-bound chain of
+// a few small kernels, and one graph launch plus per-node parameter updates costs the host a
+// fraction of the separate launches.  The graph of a new launch signature is captured once (with
+// the PDL attribute, so consecutive kernel nodes keep their programmatic edges).
+static autx_status step_graph_run(autx_ctx* ctx, std::vector<LaunchRec>& recs) {
+  autx_ctx::StepGraph* sg = nullptr;
+  for (auto& g : ctx->graphs) {
+    bool same = g.funcs.size() == recs.size();
+    for (size_t i = 0; same && i < recs.size(); ++i)
+      same = g.funcs[i] == recs[i].func && g.blocks[i].x == recs[i].block.x && g.smem[i] == recs[i].smem;
+    if (same) { sg = &g; break; }
+  }
+  if (sg) {
+    for (size_t i = 0; i < recs.size(); ++i) {
+      std::vector<void*> ptrs = recs[i].ptrs();
+      cudaKernelNodeParams kp = {};
+      kp.func = const_cast<void*>(recs[i].func);
+      kp.gridDim = recs[i].grid;
+      kp.blockDim = recs[i].block;
+      kp.sharedMemBytes = (unsigned)recs[i].smem;
+      kp.kernelParams = ptrs.data();
+      CK(cudaGraphExecKernelNodeSetParams(sg->x, sg->nodes[i], &kp));
+    }
+  } else {
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    if (ctx->graphs.size() >= 8) {  // bounded cache
+      for (auto& g : ctx->graphs) { cudaGraphExecDestroy(g.x); cudaGraphDestroy(g.g); }
+      ctx->graphs.clear();
+    }
+    autx_ctx::StepGraph g;
+    CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t err = cudaSuccess;
+    for (auto& r : recs) {
+      std::vector<void*> ptrs = r.ptrs();
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = r.grid;
+      cfg.blockDim = r.block;
+      cfg.dynamicSmemBytes = r.smem;
+      cfg.stream = ctx->cap_stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      err = cudaLaunchKernelExC(&cfg, r.func, ptrs.data());
+      if (err != cudaSuccess) break;
+      cudaStreamCaptureStatus st;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      err = cudaStreamGetCaptureInfo(ctx->cap_stream, &st, nullptr, nullptr, &deps, &nd);
+      if (err != cudaSuccess || nd != 1) { if (err == cudaSuccess) err = cudaErrorUnknown; break; }
+      g.nodes.push_back(deps[0]);
+      g.funcs.push_back(r.func);
+      g.blocks.push_back(r.block);
+      g.smem.push_back(r.smem);
+    }
+    cudaGraph_t graph = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    if (err != cudaSuccess || e2 != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      return fail(ctx, AUTX_E_CUDA, "step graph capture: %s", cudaGetErrorString(err != cudaSuccess ? err : e2));
+    }
+    g.g = graph;
+    CK(cudaGraphInstantiate(&g.x, graph, 0));
+    ctx->graphs.push_back(std::move(g));
+    sg = &ctx->graphs.back();
+  }
+  CK(cudaGraphLaunch(sg->x, ctx->stream));
+  return AUTX_OK;
+}
+
 extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out* out) {
   if (!ctx || !out) return AUTX_E_INVAL;
   autx_status s = sync_last(ctx);
@@ -727,6 +816,12 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   }
   // rows registered in this step start here (the scan reads older rows before the prologue ends)
   const uint32_t first_new = ctx->n_arr_staged ? ctx->arr_first_slot : ctx->tail;
+  // the step's kernels as one graph replay (AUTX_NO_GRAPH: separate launches); not with the
+  // per-kernel timing events, the radix pipeline (host-synchronised passes) or a bulk burst (DMA)
+  static const bool no_graph = getenv("AUTX_NO_GRAPH") != nullptr;
+  std::vector<LaunchRec> recs;
+  const bool graph = !no_graph && !ctx->timing && !ctx->radix && ctx->n_arr_staged <= 4096;
+  if (graph) g_launch_rec = &recs;
   // the step prologue rides in the dense pass (k_scan_fused) when its records fit the kernel
   // parameters, one engine, no KV allocator, a scalar policy and the default pipeline
   const bool fuse = ctx->cfg.nranks <= 1 && !ctx->radix && !ctx->kv_on && !ctx->eq2 &&
@@ -746,13 +841,21 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
     ctx->staged_new_progs.clear();
   } else {
     s = flush_staged(ctx, t);
-    if (s) return s;
+    if (s) { g_launch_rec = nullptr; return s; }
   }
   ++ctx->seqno;
-  CK(launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv, ctx->kv_on, t,
-                 ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr, ctx->radix ? &ctx->rx : nullptr,
-                 arr_base, &ctx->radix_passes, first_new, fuse ? &fa : nullptr,
-                 reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr)), ctx->d_cslots, ctx->d_arr));
+  const cudaError_t le = launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv,
+                                     ctx->kv_on, t, ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr,
+                                     ctx->radix ? &ctx->rx : nullptr, arr_base, &ctx->radix_passes, first_new,
+                                     fuse ? &fa : nullptr,
+                                     reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr)),
+                                     ctx->d_cslots, ctx->d_arr);
+  g_launch_rec = nullptr;
+  CK(le);
+  if (graph) {
+    s = step_graph_run(ctx, recs);
+    if (s) return s;
+  }
   if (!ctx->out.zero_copy)
     CK(cudaMemcpyAsync(ctx->h_outblk, ctx->d_outblk, ctx->outblk_bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->done, ctx->stream));

@@ -2,6 +2,8 @@
 // Nothing here is part of the C ABI (include/autx.h is).
 #pragma once
 #include <cstdint>
+#include <cstring>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace autx {
@@ -249,9 +251,43 @@ struct ArrivalRec {
 // predecessor in the stream still runs; it must call pdl_wait() before touching its inputs.
 extern unsigned long long g_kernel_launches;  // every library kernel launch (autx_kernel_launches)
 
+// A kernel launch recorded instead of issued (the step's launches are replayed as one CUDA graph
+// whose kernel nodes get this step's parameters: see autx_api.cu, step_graph_run).
+struct LaunchRec {
+  const void* func;
+  dim3 grid, block;
+  size_t smem;
+  std::vector<unsigned char> blob;  // argument values, 16-B aligned each
+  std::vector<size_t> off;
+  template <typename T>
+  void push(const T& v) {
+    const size_t o = (blob.size() + 15) & ~size_t(15);
+    blob.resize(o + sizeof(T));
+    memcpy(blob.data() + o, &v, sizeof(T));
+    off.push_back(o);
+  }
+  std::vector<void*> ptrs() {
+    std::vector<void*> p(off.size());
+    for (size_t i = 0; i < off.size(); ++i) p[i] = blob.data() + off[i];
+    return p;
+  }
+};
+extern thread_local std::vector<LaunchRec>* g_launch_rec;  // non-null: launch_pdl records
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args) {
+  if (g_launch_rec) {
+    LaunchRec r;
+    r.func = reinterpret_cast<const void*>(k);
+    r.grid = grid;
+    r.block = block;
+    r.smem = smem;
+    (r.push(static_cast<KArgs>(args)), ...);
+    g_launch_rec->push_back(std::move(r));
+    __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);  // runs in the graph replay
+    return cudaSuccess;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

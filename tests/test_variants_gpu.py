@@ -20,6 +20,7 @@ VARIANTS = {
     "dma_out": {"AUTX_DMA_OUT": "1"},            # host lists by one copy instead of zero-copy stores
     "scan_pre0": {"AUTX_SCAN_PRE": "0"},         # scan reads nothing before the PDL wait
     "fused_prologue": {"AUTX_FUSED_PROLOGUE": "1"},  # prologue folded into the dense pass (k_scan_fused)
+    "no_graph": {"AUTX_NO_GRAPH": "1"},          # the step's kernels as separate launches, not a graph replay
     "scan_pre2": {"AUTX_SCAN_PRE": "2"},         # ... prog, base, mtime before the wait
 }
 
