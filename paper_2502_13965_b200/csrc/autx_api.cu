@@ -196,6 +196,7 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&o.cand_rec, o.cand_cap));
   CK(dalloc(&o.prev_rec, BS));
   CK(dalloc(&o.ckey, 2 * BS));
+  CK(dalloc(&o.ckvb, 2 * BS));
   CK(dalloc(&o.skey, 2 * BS));
   CK(dalloc(&o.sidx, 2 * BS));
   CK(dalloc(&o.srec, 2 * BS));
@@ -357,7 +358,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
                  t.loc, t.hcls, t.bidx, ctx->out.prev_pos, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
                  ctx->ctl, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
-                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->out.tile_off,
+                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.ckvb, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->out.tile_off,
                  ctx->out.tile_pre, ctx->out.tile_stat, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,

@@ -99,6 +99,9 @@ struct Ctl {
   uint32_t rs_free_top;    // resident-slot free stack size
   uint32_t host_bump;      // host arena bump pointer (pages)
   uint32_t rank_done;      // last-CTA ticket of k_rank (fused finalize)
+  // batch totals reduced by k_rank's list writers (rank_lists), read and reset by finalize
+  uint32_t acc_nbatch, acc_nadmit;
+  unsigned long long acc_kv, acc_swap_in;
   uint32_t host_free_top[32];  // per size class free-stack size
   // self-selecting gather (default select path): slot + 1 of region A's last q* row (0 = none),
   // and the scan's partial totals, spread over QP_LINES 128-B lines (scan CTA b adds into line
@@ -191,6 +194,8 @@ struct Outputs {
   unsigned long long* prev_pos;  // [max_batch] seqno << 32 | sorted position of previous-batch entry j
                                  // (k_rank; entries that are no candidate keep an older seqno)
   uint32_t use_prev_pos;     // finalize tests batch membership of the previous batch by prev_pos
+  uint32_t rank_lists;       // k_rank writes batch / admit lists and accounting (no KV allocator)
+  uint32_t* ckvb;            // [2 BS] kvb of each key in ckey (R14)
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* sup_cnt;         // [ceil(ntiles_cap / SUP_TILES) * MAX_K] per-queue counts of super-tiles
                              // (scan: atomics; gather: prefix; finalize: reset)

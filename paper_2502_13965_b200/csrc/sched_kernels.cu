@@ -1230,6 +1230,7 @@ __device__ __forceinline__ void gather_body(Policy& pol, CallTable& ct, Ctl* ctl
       // region B: live calls of q* that region A (q* rows with slot <= boundary) does not hold
       bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == qs && (bnd == NONE || r.slot > bnd);
       out.ckey[na + j] = b ? cand_key(r, t) : ~0ull;
+      out.ckvb[na + j] = blocks_for(pol, r.tok + r.exec + 1);  // R14
     }
     return;
   }
@@ -1294,6 +1295,7 @@ __device__ __forceinline__ void gather_body(Policy& pol, CallTable& ct, Ctl* ctl
         out.cand[pos] = row0 + j;
         out.cand_rec[pos] = r;
         out.ckey[pos] = cand_key(r, t);
+        out.ckvb[pos] = blocks_for(pol, r.tok + r.exec + 1);  // R14
         ++pos;
       }
   }
@@ -1383,6 +1385,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
       out.prev_rec[j] = r;
       const bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == s_qs;
       out.ckey[s_m + j] = b ? cand_key(r, t) : ~0ull;
+      out.ckvb[s_m + j] = blocks_for(pol, r.tok + r.exec + 1);  // R14
     }
     return;
   }
@@ -1494,6 +1497,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
         out.cand[pos] = row0 + j;
         out.cand_rec[pos] = r;
         out.ckey[pos] = cand_key(r, t);
+        out.ckvb[pos] = blocks_for(pol, r.tok + r.exec + 1);  // R14
         ++pos;
       }
   }
@@ -1523,7 +1527,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_gather_ss(Policy pol, CallT
 // (Alg. 1 l.20-23), allocate KV blocks and build the swap plan.
 // ---------------------------------------------------------------------------------------------
 extern __shared__ unsigned char fin_smem[];
-template <int NT, int R>
+template <int NT, int R, bool LISTS = false>
 __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
                               uint32_t t, uint32_t np, uint32_t seqno);
 
@@ -1546,6 +1550,9 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   uint64_t* rk = reinterpret_cast<uint64_t*>(fin_smem);  // [n] keys, ~0 = no candidate
   uint64_t* ck = rk + n;                                 // [n_valid] the candidates' keys
   uint32_t* ci = reinterpret_cast<uint32_t*>(ck + n);    // [n_valid] their element index
+  uint32_t* rkv = ci + n;                                // [n] kvb of each element
+  uint32_t* ckv = rkv + n;                               // [n_valid] the candidates' kvb
+  const bool lists = out.rank_lists != 0;
   const uint32_t e0 = blockIdx.x * RANK_PER_CTA;
   const uint32_t bnd1 = ctl->qs_bnd1;
   // (1) keys into shared memory; previous-batch keys at or before region A's boundary are region
@@ -1556,10 +1563,12 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   uint32_t nv = 0;
   for (uint32_t c0 = 0; c0 < cap; c0 += RK * RANK_THREADS) {
     uint64_t kk[RK];
+    uint32_t kb[RK];
 #pragma unroll
     for (int r = 0; r < RK; ++r) {
       const uint32_t i = c0 + r * RANK_THREADS + threadIdx.x;
       kk[r] = i < cap ? __ldcg(out.ckey + i) : ~0ull;
+      kb[r] = lists && i < cap ? __ldcg(out.ckvb + i) : 0u;
     }
 #pragma unroll
     for (int r = 0; r < RK; ++r) {
@@ -1569,6 +1578,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
         if (i >= na && (uint32_t)(k & 0x7FFFFFFFu) < bnd1) k = ~0ull;
         nv += k != ~0ull ? 1u : 0u;
         rk[i] = k;
+        rkv[i] = kb[r];
       }
     }
   }
@@ -1579,7 +1589,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     uint32_t n_valid;
     uint32_t off = block_excl_scan<uint32_t, RANK_THREADS>(nv, red_r, &n_valid);
     for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS)
-      if (rk[i] != ~0ull) { ck[off] = rk[i]; ci[off] = i; ++off; }
+      if (rk[i] != ~0ull) { ck[off] = rk[i]; ci[off] = i; ckv[off] = rkv[i]; ++off; }
     __syncthreads();
     if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[55] = globaltimer();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1592,17 +1602,35 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     // (3) rank = number of smaller keys (keys are unique), RANK_SUB threads per key; the record
     // load is issued before the count so that its latency hides behind it
     const uint32_t e = e0 + threadIdx.x / RANK_SUB, sub = threadIdx.x % RANK_SUB;
-    uint32_t cnt = 0, eo = 0;
+    uint32_t cnt = 0, eo = 0, kvs = 0, nad = 0;
     uint64_t x = 0;
     CandRec rec;
     if (e < n_valid) {
       x = ck[e];
       eo = ci[e];
       if (sub == 0) rec = eo < na ? out.cand_rec[eo] : out.prev_rec[eo - na];
-      for (uint32_t j = sub; j < n_valid; j += RANK_SUB) cnt += ck[j] < x ? 1u : 0u;
+      if (lists) {
+        // with the rank, the kvb prefix (Alg. 1 l.34-37) and the admit rank (smaller keys of
+        // calls that did not run: not resident under eager eviction)
+        for (uint32_t j = sub; j < n_valid; j += RANK_SUB) {
+          const uint64_t y = ck[j];
+          const bool lt = y < x;
+          cnt += lt ? 1u : 0u;
+          kvs += lt ? ckv[j] : 0u;
+          nad += (lt && ((y >> 31) & 1u)) ? 1u : 0u;
+        }
+      } else {
+        for (uint32_t j = sub; j < n_valid; j += RANK_SUB) cnt += ck[j] < x ? 1u : 0u;
+      }
     }
 #pragma unroll
-    for (int d = 1; d < RANK_SUB; d <<= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    for (int d = 1; d < RANK_SUB; d <<= 1) {
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+      if (lists) {
+        kvs += __shfl_xor_sync(0xffffffffu, kvs, d);
+        nad += __shfl_xor_sync(0xffffffffu, nad, d);
+      }
+    }
     if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[56] = globaltimer();
     if (sub == 0 && e < n_valid) {
       out.skey[cnt] = x;
@@ -1611,6 +1639,44 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
       // a running call (previous-batch entry rec._pad) publishes its sorted position: finalize
       // tests the previous batch's membership in the new one without searching
       if (rec.qf & QF_RUN) out.prev_pos[rec._pad] = (unsigned long long)seqno << 32 | cnt;
+      if (lists) {
+        // Alg. 1 l.32-39 for this key alone: kvb >= 1 makes the inclusive prefix strictly
+        // increasing, so "count <= BS and sum kvb <= P" holds exactly on a prefix of the order
+        // (the first misfit stops, R13); the batch entries write their lists and accounting
+        const uint32_t incl = kvs + ckv[e];
+        const uint32_t BS = pol.max_batch;
+        if (cnt < BS && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) {
+          const uint32_t sl = rec.slot;
+          out.batch_slots[cnt] = sl;
+          out.batch_ids[cnt] = rec.cid;
+          if (out.zero_copy) { out.h_batch[cnt] = rec.cid; out.h_batch_slots[cnt] = sl; }
+          // step accounting + eager demotion (Alg. 1 l.20-23)
+          uint32_t q = rec.qf & QF_QMASK, qt = rec.quanta;
+          ct.exec[sl] = rec.exec + 1;
+          ct.mtime[sl] = rec.mtime + 1;
+          if (qt != AUTX_INF) {
+            qt -= 1;
+            if (qt == 0) {
+              q = min(q + 1, pol.K - 1);
+              qt = pol.quanta[q];
+            }
+            ct.quanta[sl] = qt;
+          }
+          ct.qf[sl] = (uint8_t)(q | QF_RUN | QF_RES);
+          ct.bidx[sl] = cnt;
+          out.prev_slots[cnt] = sl;
+          if ((x >> 31) & 1u) {  // admit: did not run in the previous step (not resident)
+            out.admit_ids[nad] = rec.cid;
+            out.admit_slots[nad] = sl;
+            if (out.zero_copy) out.h_admit[nad] = rec.cid;
+            const uint32_t held = rec.exec > 0 ? blocks_for(pol, rec.tok + rec.exec) : 0u;  // R28
+            if (held) atomicAdd(&ctl->acc_swap_in, (unsigned long long)held);
+            atomicMax(&ctl->acc_nadmit, nad + 1);
+          }
+          atomicMax(&ctl->acc_nbatch, cnt + 1);
+          atomicMax(&ctl->acc_kv, (unsigned long long)incl);
+        }
+      }
     }
   }
   CHAIN_END(4);
@@ -1624,10 +1690,11 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   if (!last) return;
   __threadfence();
   if (threadIdx.x == 0) ctl->rank_done = 0;
-  finalize_body<RANK_THREADS, 4>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  if (out.rank_lists) finalize_body<RANK_THREADS, 4, true>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  else finalize_body<RANK_THREADS, 4, false>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
 }
 
-template <int NT, int R>
+template <int NT, int R, bool LISTS>
 __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
                               uint32_t t, uint32_t np, uint32_t seqno) {
   uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] sorted keys of the first m candidates
@@ -1646,12 +1713,19 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   const uint32_t ncand = ctl->n_cand_a + ctl->n_cand_b;
   // host-record fields, loaded with everything else in the first round
   uint32_t c_live = 0, c_promo = 0, c_err = 0, c_einfo = 0;
-  if (tid == 0) { c_live = ctl->n_live; c_promo = ctl->n_promoted; c_err = ctl->err; c_einfo = ctl->err_info; }
+  // rank_lists: k_rank has written the batch and admit lists and the accounting; its totals
+  constexpr bool lists = LISTS;
+  uint32_t a_nb = 0, a_na = 0;
+  unsigned long long a_kv = 0, a_si = 0;
+  if (tid == 0) {
+    c_live = ctl->n_live; c_promo = ctl->n_promoted; c_err = ctl->err; c_einfo = ctl->err_info;
+    if (lists) { a_nb = ctl->acc_nbatch; a_na = ctl->acc_nadmit; a_kv = ctl->acc_kv; a_si = ctl->acc_swap_in; }
+  }
   STAMP(0);
   if (tid == 0) s_nbatch = 0;
   // ---- (1) the first m = min(BS, ncand) candidates in key order: key + record, plus the
   // previous batch's records (preempt), all in one round of independent loads --------------
-  const uint32_t m = min(BS, ncand);
+  const uint32_t m = lists ? 0u : min(BS, ncand);
   // R items per thread, blocked (i = tid * R + r): NT * R >= BS
   uint32_t c_s[R], c_qf[R], c_tok[R], c_ex[R], c_mt[R], c_qt[R], c_kvb[R];
   uint64_t c_cid[R];
@@ -1672,7 +1746,11 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     for (int r = 0; r < R; ++r) {
       // unconditional below BS (buffers hold >= BS entries): the loads do not wait for the counts
       const uint32_t i = tid * R + r;
-      if (i < BS) { kk[r] = skey[i]; rc[r] = srec[i]; pr[r] = prec[i]; p_pos[r] = ppos[i]; }
+      if (i < BS) {
+        if (!lists) { kk[r] = skey[i]; rc[r] = srec[i]; }
+        pr[r] = prec[i];
+        p_pos[r] = ppos[i];
+      }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1706,7 +1784,8 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   }
   STAMP(1);
   STAMP(2);
-  unsigned long long kv_pre = block_excl_scan<unsigned long long, NT>(my_kv, red64, nullptr);
+  unsigned long long kv_pre = lists ? 0ull : block_excl_scan<unsigned long long, NT>(my_kv, red64, nullptr);
+  if (lists && tid == 0) s_nbatch = a_nb;
   // Alg. 1 l.34-37: take while count <= BS and sum kvb <= P; kvb >= 1 makes the prefix sums
   // strictly increasing, so the fitting items are exactly a prefix: n_batch = max fitting i + 1
   unsigned long long c_incl[R];  // inclusive kvb prefix at each item
@@ -1727,14 +1806,17 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   const uint32_t n_batch = s_nbatch;
   STAMP(3);
   if (tid == 0 && ncand > 0 && n_batch == 0) {
-    if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u) ctl->err_info = (uint32_t)(uk[0] & 0x7FFFFFFF);
+    if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u)
+      ctl->err_info = (uint32_t)((lists ? out.skey[0] : uk[0]) & 0x7FFFFFFF);
   }
   // ---- (4) batch list and admit = batch calls not resident (batch order) -------------------
   unsigned long long my_ad = 0;
   if (n_batch == 0 && tid == 0) s_kvsum = 0;
+  if (lists && tid == 0) s_kvsum = a_kv;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t i = tid * R + r;
+    if (lists) break;  // (k_rank wrote the lists)
     if (i + 1 == n_batch) s_kvsum = c_incl[r];  // sum kvb over the batch (read after the scans below)
     if (i < n_batch) {
       out.batch_slots[i] = c_s[r];
@@ -1745,9 +1827,10 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       }
     }
   }
-  unsigned long long ad_tot;
-  unsigned long long ad_pre = block_excl_scan<unsigned long long, NT>(my_ad, red64, &ad_tot);
-  {
+  unsigned long long ad_tot = 0;
+  unsigned long long ad_pre = lists ? 0ull : block_excl_scan<unsigned long long, NT>(my_ad, red64, &ad_tot);
+  if (lists) ad_tot = (unsigned long long)a_na << 44 | a_si;  // (tid 0 only: the host record)
+  if (!lists) {
     uint32_t pos = (uint32_t)(ad_pre >> 44);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -1957,7 +2040,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t i = tid * R + r;
-    if (i < n_batch) {
+    if (!lists && i < n_batch) {
       uint32_t sl = c_s[r];
       uint32_t q = c_qf[r] & QF_QMASK;
       ct.exec[sl] = c_ex[r] + 1;
@@ -1995,6 +2078,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     ctl->n_live = 0;
     ctl->qs_bnd1 = 0;
     ctl->n_cand_b = 0;
+    if (lists) { ctl->acc_nbatch = 0; ctl->acc_nadmit = 0; ctl->acc_kv = 0; ctl->acc_swap_in = 0; }
     s_hout = h;
   }
   for (uint32_t i = tid; i < QP_LINES * 32; i += NT) (&ctl->qpart[0][0])[i] = 0;
@@ -2012,20 +2096,21 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
 #pragma unroll
     for (int k = 0; k < R / 2; ++k) {
       const uint32_t i = tid * (R / 2) + k;
-      if (i < (nb + 1) / 2)
+      if (!lists && i < (nb + 1) / 2)
         reinterpret_cast<uint4*>(out.h_batch)[i] =
             make_uint4((uint32_t)c_cid[2 * k], (uint32_t)(c_cid[2 * k] >> 32), (uint32_t)c_cid[2 * k + 1],
                        (uint32_t)(c_cid[2 * k + 1] >> 32));
     }
     // batch slots, R consecutive u32 per thread (8- or 16-byte stores)
-    if (tid * R < nb) {
+    if (!lists && tid * R < nb) {
       if constexpr (R == 2) reinterpret_cast<uint2*>(out.h_batch_slots)[tid] = make_uint2(c_s[0], c_s[1]);
       else if constexpr (R == 4) reinterpret_cast<uint4*>(out.h_batch_slots)[tid] = make_uint4(c_s[0], c_s[1], c_s[2], c_s[3]);
       else for (int r = 0; r < R; ++r) out.h_batch_slots[tid * R + r] = c_s[r];
     }
     const uint4* sa = reinterpret_cast<const uint4*>(s_ad);
     const uint4* sp = reinterpret_cast<const uint4*>(s_pr);
-    for (uint32_t i = tid; i < (na + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_admit)[i] = sa[i];
+    if (!lists)
+      for (uint32_t i = tid; i < (na + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_admit)[i] = sa[i];
     for (uint32_t i = tid; i < (np_ + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_preempt)[i] = sp[i];
     __syncthreads();
     // the host reads after the stream event that follows this kernel, which orders every store
@@ -2034,13 +2119,13 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   STAMP(8);
 }
 
-template <int NT, int R>
+template <int NT, int R, bool LISTS = false>
 __global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
                                                  bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
   pdl_wait();
   pdl_trigger();
   CHAIN_BEGIN(5);
-  finalize_body<NT, R>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  finalize_body<NT, R, LISTS>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
   if (STAMPS_ON) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -2180,7 +2265,14 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   // sorted keys [np] + admit and preempt id staging [2 x even(BS)]
   size_t fin_smem_bytes = ((size_t)np + 2 * ((pol.max_batch + 1) & ~1u)) * sizeof(uint64_t);
   // keys, compacted keys, element indices of <= 2 BS candidates (fused: finalize's layout after)
-  size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch * (2 * sizeof(uint64_t) + sizeof(uint32_t)), fin_smem_bytes);
+  // k_rank also decides the batch (lists, accounting) when there is no KV allocator and its keys
+  // + kvb fit shared memory
+  // (the 512-thread finalize and the fused rank+finalize have the matching variant)
+  out.rank_lists = (!kv_on && !rx && pol.max_batch <= 1024 && !getenv("AUTX_FIN256") &&
+                    !getenv("AUTX_FINALIZE_LISTS")) ? 1u : 0u;
+  size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch *
+                                          (2 * sizeof(uint64_t) + sizeof(uint32_t) + (out.rank_lists ? 8 : 0)),
+                                      fin_smem_bytes);
   // at most one rank CTA per SM: the CTAs are dispatched while the previous kernel still holds
   // most SMs, and two packed on one SM halve each other's issue rate (measured: the count loop
   // ran 2x slower behind the self-selecting gather's grid)
@@ -2190,6 +2282,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     cudaError_t e = cudaFuncSetAttribute(k_finalize<FIN_THREADS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_finalize<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_finalize<512, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_finalize<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
@@ -2213,7 +2307,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     if (fin256)
       launch_pdl(k_finalize<256, 4>, 1, 256, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
     else
-      launch_pdl(k_finalize<512, 2>, 1, 512, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+      launch_pdl(out.rank_lists ? k_finalize<512, 2, true> : k_finalize<512, 2>, 1, 512, fin_smem_bytes, s, pol, ct, ctl,
+                 out, kv, kv_on, t, np, seqno);
   } else {
     launch_pdl(k_rank<false>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
     launch_pdl(k_finalize<FIN_THREADS, 4>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np,

@@ -21,6 +21,7 @@ VARIANTS = {
     "scan_pre0": {"AUTX_SCAN_PRE": "0"},         # scan reads nothing before the PDL wait
     "fused_prologue": {"AUTX_FUSED_PROLOGUE": "1"},  # prologue folded into the dense pass (k_scan_fused)
     "no_graph": {"AUTX_NO_GRAPH": "1"},          # the step's kernels as separate launches, not a graph replay
+    "finalize_lists": {"AUTX_FINALIZE_LISTS": "1"},  # finalize cuts the batch and writes the lists (not k_rank)
     "scan_pre2": {"AUTX_SCAN_PRE": "2"},         # ... prog, base, mtime before the wait
 }
 
