@@ -1612,7 +1612,8 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
       if (lists) {
         // with the rank, the kvb prefix (Alg. 1 l.34-37) and the admit rank (smaller keys of
         // calls that did not run: not resident under eager eviction)
-        for (uint32_t j = sub; j < n_valid; j += RANK_SUB) {
+#pragma unroll 4
+        for (uint32_t j = sub; j < n_valid; j += RANK_SUB) {  // (4 independent smem chains in flight)
           const uint64_t y = ck[j];
           const bool lt = y < x;
           cnt += lt ? 1u : 0u;
@@ -1620,6 +1621,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
           nad += (lt && ((y >> 31) & 1u)) ? 1u : 0u;
         }
       } else {
+#pragma unroll 4
         for (uint32_t j = sub; j < n_valid; j += RANK_SUB) cnt += ck[j] < x ? 1u : 0u;
       }
     }
