@@ -72,8 +72,10 @@ def chain_spans(phase):
         rows[-1]["rank_keys"] = (c[20], c[21], 0)
         if c[22]:  # k_rank CTA 0: keys loaded, compacted, counted
             rows[-1]["rank_phases"] = tuple(c[22 + i] - t0 for i in range(3))
+        if c[25]:  # k_gather_ss tile 0: selection known, positions known, records emitted
+            rows[-1]["gather_phases"] = tuple(c[25 + i] - t0 for i in range(3))
     out = {}
-    for n in names + ["rank_keys", "rank_phases"]:
+    for n in names + ["rank_keys", "rank_phases", "gather_phases"]:
         v = [r[n] for r in rows if n in r]
         if v:
             div = 1 if n == "rank_keys" else 1e3

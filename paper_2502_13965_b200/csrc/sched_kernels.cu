@@ -656,6 +656,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallT
       const uint32_t sl = out.prev_slots[i];
       prefetch_l2(ct.cid + sl); prefetch_l2(ct.arr + sl); prefetch_l2(ct.tok + sl);
       prefetch_l2(ct.exec + sl); prefetch_l2(ct.mtime + sl); prefetch_l2(ct.quanta + sl);
+      prefetch_l2(ct.bidx + sl); prefetch_l2(ct.qf + sl);
     }
     if (early && pol.beta_den != 0) {
       const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
@@ -1332,7 +1333,11 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
   const uint32_t tid = threadIdx.x, tile = blockIdx.x;
   const uint32_t K = pol.K, BS = pol.max_batch;
   const bool is_tile = tile < ntiles;
-  // (1) one round of independent loads
+  // (1) one round of independent loads: this tile's queue bytes first (they do not depend on the
+  // selection), then the counts
+  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  const uint2 qv = is_tile && row0 < n_rows ? *reinterpret_cast<const uint2*>(ct.qf + row0)
+                                            : make_uint2(0x40404040u, 0x40404040u);
   {
     const uint32_t h = tid / MAX_K, k = tid % MAX_K;
     const uint32_t nsup = (ntiles + SUP_TILES - 1) / SUP_TILES, my_sup = tile / SUP_TILES;
@@ -1389,8 +1394,6 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
     }
     return;
   }
-  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
-  const uint2 qv = row0 < n_rows ? *reinterpret_cast<const uint2*>(ct.qf + row0) : make_uint2(0x40404040u, 0x40404040u);
   __syncthreads();
   // (2) q*, m', and this tile's prefix (warp 0, lane k = queue k)
   if (tid < 32) {
@@ -1427,6 +1430,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
   __syncthreads();
   // tiles without candidates leave now (their SM slots go to the next kernel's CTAs); the
   // boundary row is always in a tile with candidates
+  if (STAMPS_ON && tile == 0 && tid == 0) ctl->dbg[57] = globaltimer();
   if (!s_has) return;
   const uint32_t qs = s_qs, m = s_m;
   uint32_t qfs[8], na = 0, nq = 0;
@@ -1464,6 +1468,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
     }
     if (sel) flags |= 1u << j;
   }
+  if (STAMPS_ON && tile == 0 && tid == 0) ctl->dbg[58] = globaltimer();
   if (flags) {
     const uint4* cidv = reinterpret_cast<const uint4*>(ct.cid + row0);
     uint4 c4[4];
@@ -1500,6 +1505,10 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
         out.ckvb[pos] = blocks_for(pol, r.tok + r.exec + 1);  // R14
         ++pos;
       }
+  }
+  if (STAMPS_ON && tile == 0) {
+    __syncwarp();
+    if (tid == 0) ctl->dbg[59] = globaltimer();
   }
 }
 
