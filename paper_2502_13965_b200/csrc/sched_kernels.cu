@@ -1343,14 +1343,30 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
     const uint32_t nsup = (ntiles + SUP_TILES - 1) / SUP_TILES, my_sup = tile / SUP_TILES;
     uint32_t tot = 0, pre = 0;
     if (k < K) {
-      for (uint32_t S = h; S < nsup; S += NH) {
-        const uint32_t v = __ldcg(out.sup_cnt + S * MAX_K + k);
-        tot += v;
-        pre += (is_tile && S < my_sup) ? v : 0u;
-      }
+      // all loads issued before any is consumed (a rolled loop would chain one L2 round trip per
+      // iteration): the tile count, then up to 8 super-tile rows per half-warp (4.2M rows)
       const uint32_t tr = my_sup * SUP_TILES + h;  // earlier tile of the same super-tile, or this one
-      if (is_tile && tr <= tile) {
-        const uint32_t c = __ldcg(out.tile_cnt + (size_t)tr * MAX_K + k);
+      const bool has_tr = is_tile && tr <= tile;
+      const uint32_t c = has_tr ? __ldcg(out.tile_cnt + (size_t)tr * MAX_K + k) : 0u;
+      constexpr int SU = 8;
+      uint32_t v[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const uint32_t S = h + u * NH;
+        v[u] = S < nsup ? __ldcg(out.sup_cnt + S * MAX_K + k) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const uint32_t S = h + u * NH;
+        tot += v[u];
+        pre += (is_tile && S < my_sup) ? v[u] : 0u;
+      }
+      for (uint32_t S = h + SU * NH; S < nsup; S += NH) {  // larger tables
+        const uint32_t w = __ldcg(out.sup_cnt + S * MAX_K + k);
+        tot += w;
+        pre += (is_tile && S < my_sup) ? w : 0u;
+      }
+      if (has_tr) {
         if (tr < tile) pre += c;
         else s_own[k] = c;
       }
