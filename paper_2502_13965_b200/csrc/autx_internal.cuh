@@ -195,6 +195,7 @@ struct Outputs {
                                  // (k_rank; entries that are no candidate keep an older seqno)
   uint32_t use_prev_pos;     // finalize tests batch membership of the previous batch by prev_pos
   uint32_t rank_lists;       // k_rank writes batch / admit lists and accounting (no KV allocator)
+  uint32_t rank_wide;        // k_rank: a warp per key when the candidates fill <= half its grid
   uint32_t* ckvb;            // [2 BS] kvb of each key in ckey (R14)
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* sup_cnt;         // [ceil(ntiles_cap / SUP_TILES) * MAX_K] per-queue counts of super-tiles

@@ -1607,7 +1607,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
       }
     }
   }
-  if (e0 < n) {
+  if (blockIdx.x * (RANK_PER_CTA / 2) < n) {
     // (2) compact the candidates (same deterministic order in every CTA): sentinels rank last and
     // nobody reads them, so only the n_valid candidates are ranked and compared against
     if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[54] = globaltimer();
@@ -1626,7 +1626,11 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     }
     // (3) rank = number of smaller keys (keys are unique), RANK_SUB threads per key; the record
     // load is issued before the count so that its latency hides behind it
-    const uint32_t e = e0 + threadIdx.x / RANK_SUB, sub = threadIdx.x % RANK_SUB;
+    // when the candidates fill at most half the grid's capacity, a full warp per key (8 keys per
+    // CTA) keeps every CTA busy and halves each thread's compares; else half a warp per key
+    const bool wide = 2 * n_valid <= gridDim.x * RANK_PER_CTA && !FUSED && out.rank_wide;
+    const uint32_t subn = wide ? 32u : (uint32_t)RANK_SUB;
+    const uint32_t e = (wide ? blockIdx.x * (RANK_PER_CTA / 2) : e0) + threadIdx.x / subn, sub = threadIdx.x % subn;
     uint32_t cnt = 0, eo = 0, kvs = 0, nad = 0;
     uint64_t x = 0;
     CandRec rec;
@@ -1638,7 +1642,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
         // with the rank, the kvb prefix (Alg. 1 l.34-37) and the admit rank (smaller keys of
         // calls that did not run: not resident under eager eviction)
 #pragma unroll 4
-        for (uint32_t j = sub; j < n_valid; j += RANK_SUB) {  // (4 independent smem chains in flight)
+        for (uint32_t j = sub; j < n_valid; j += subn) {  // (4 independent smem chains in flight)
           const uint64_t y = ck[j];
           const bool lt = y < x;
           cnt += lt ? 1u : 0u;
@@ -1647,11 +1651,12 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
         }
       } else {
 #pragma unroll 4
-        for (uint32_t j = sub; j < n_valid; j += RANK_SUB) cnt += ck[j] < x ? 1u : 0u;
+        for (uint32_t j = sub; j < n_valid; j += subn) cnt += ck[j] < x ? 1u : 0u;
       }
     }
 #pragma unroll
-    for (int d = 1; d < RANK_SUB; d <<= 1) {
+    for (int d = 1; d < 32; d <<= 1) {
+      if ((uint32_t)d >= subn) break;
       cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
       if (lists) {
         kvs += __shfl_xor_sync(0xffffffffu, kvs, d);
@@ -2227,6 +2232,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   if (ntiles == 0) ntiles = 1;
   out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
   out.use_prev_pos = rx ? 0u : 1u;  // k_rank publishes previous-batch positions (select mode)
+  static const bool rank_narrow = getenv("AUTX_RANK_NARROW") != nullptr;
+  out.rank_wide = rank_narrow ? 0u : 1u;  // k_rank may use a warp per key when candidates are few
   if (ev) cudaEventRecord(ev[0], s);
   if (rx) {
     static int sms = 0;

@@ -22,6 +22,7 @@ VARIANTS = {
     "fused_prologue": {"AUTX_FUSED_PROLOGUE": "1"},  # prologue folded into the dense pass (k_scan_fused)
     "no_graph": {"AUTX_NO_GRAPH": "1"},          # the step's kernels as separate launches, not a graph replay
     "finalize_lists": {"AUTX_FINALIZE_LISTS": "1"},  # finalize cuts the batch and writes the lists (not k_rank)
+    "rank_narrow": {"AUTX_RANK_NARROW": "1"},    # half a warp per key in k_rank whatever the candidate count
     "scan_pre2": {"AUTX_SCAN_PRE": "2"},         # ... prog, base, mtime before the wait
 }
 
