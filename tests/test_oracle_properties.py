@@ -8,7 +8,7 @@ import pytest
 
 from autx_workload import random_tiny, fig2
 from oracle.autellix import (Engine, Config, simulate, simulate_multi, PLAS, ATLAS, MLFQ, FCFS,
-                             Workload, ceil_div)
+                             ATLAS_EQ2, Workload, ceil_div)
 
 LADDERS = [
     dict(K=1, q_hi=(), quanta=(None,)),
@@ -83,12 +83,13 @@ def run_checked(tr, cfg):
             break
         cids = [int(tr.call_id[c]) for c in completed]
         ended = wl.release(t, completed)
-        rec = eng.step(t, cids, wl.arrivals(t))
+        arr = wl.arrivals(t)
+        rec = eng.step(t, cids, arr, wl.parents_of(arr) if cfg.policy == ATLAS_EQ2 else None)
         for pid, s in eng.table.svc.items():
             assert s >= svc_hist.get(pid, 0)       # monotone table
             svc_hist[pid] = s
         for pid in ended:
-            eng.table.end_program(pid)
+            eng.end_program(pid)
         log.append(rec)
         completed = wl.ran(t, rec["batch"])
     assert wl.finished()
@@ -104,6 +105,16 @@ def test_random_tiny_invariants(seed):
             run_checked(tr, cfg)
         except ValueError as e:
             assert "exceeds the KV budget" in str(e)
+
+
+@pytest.mark.parametrize("seed", range(150))
+def test_random_tiny_invariants_eq2(seed):
+    """The step invariants under exact Eq. 2 inheritance (R31), DAG traces with forks and joins."""
+    tr = random_tiny(seed, max_calls=6)
+    try:
+        run_checked(tr, cfg_for(seed * 4 + 3, ATLAS_EQ2))
+    except ValueError as e:  # initial kvb > P (R13) or a call outgrowing P while it decodes (R14, R30)
+        assert "exceeds the KV budget" in str(e) or "exceeds the budget" in str(e)
 
 
 @pytest.mark.parametrize("seed", range(50))
