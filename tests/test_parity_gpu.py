@@ -244,6 +244,17 @@ def test_eq2_mcts_mapreduce_slice(frac):
                             max_calls=1 << 16), want)
 
 
+def test_eq2_with_kv_allocator():
+    """Exact Eq. 2 with the GPU block allocator on (the full finalize path: swap plan, block tables)
+    and a binding budget: decisions and swap blocks equal the oracle's."""
+    tr = mcts_mapreduce(30, seed=5, frac_mcts=0.5)
+    P = 6000
+    want, _ = oracle_records(tr, spec_ladder_config(ATLAS_EQ2, max_batch=64, kv_budget=P))
+    got = gpu_records(tr, spec_ladder_config(ATLAS_EQ2, max_batch=64, kv_budget=P), max_calls=1 << 16,
+                      n_gpu_blocks=P, max_blocks_per_call=4096, host_pages=1 << 16)
+    assert_same(got, want)
+
+
 def test_eq2_protocol_errors():
     from paper_2502_13965_b200 import Scheduler, AutxError, CALL_DESC
     with pytest.raises(AutxError):
