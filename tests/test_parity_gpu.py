@@ -446,3 +446,34 @@ def test_full_size_1m_burst_first_steps():
         assert rec["n_active"] == rec_o["n_active"] > 900_000
         assert (rec["batch"], rec["admit"], rec["preempt"]) == (rec_o["batch"], rec_o["admit"], rec_o["preempt"]), t
     s.close()
+
+
+@pytest.mark.parametrize("workload", ["chatbot", "react"])
+def test_full_size_chatbot_react_first_steps(workload):
+    """BASELINE configs[1] (10k ShareGPT-shaped programs, BS 256) and configs[2] (100k BFCL-shaped
+    programs, BS 256) at full size with the bench's PLAS configuration and KV budgets: 40 steps of
+    lists equal to the oracle's."""
+    from autx_workload import chatbot, react
+    from paper_2502_13965_b200 import TraceDriver
+    tr, P = (chatbot(10_000), 6000) if workload == "chatbot" else (react(100_000), 8000)
+    cfg = spec_ladder_config(PLAS, max_batch=256, kv_budget=P)
+    eng = Engine(cfg, check_formulations=False)
+    wl = Workload(tr)
+    s = make_sched(spec_ladder_config(PLAS, max_batch=256, kv_budget=P), max_calls=tr.n_programs + 4096,
+                   max_programs=tr.n_programs + 1024)
+    d = TraceDriver(tr, s)
+    completed = []
+    for t in range(40):
+        cids = [int(tr.call_id[c]) for c in completed]
+        ended = wl.release(t, completed)
+        rec_o = eng.step(t, cids, wl.arrivals(t))
+        for pid in ended:
+            eng.end_program(pid)
+        completed = wl.ran(t, rec_o["batch"])
+        if d.t != t:  # the driver skips steps with nothing active
+            assert not rec_o["batch"]
+            continue
+        rec = d.step()
+        assert rec["n_active"] == rec_o["n_active"]
+        assert (rec["batch"], rec["admit"], rec["preempt"]) == (rec_o["batch"], rec_o["admit"], rec_o["preempt"]), t
+    s.close()
