@@ -420,7 +420,8 @@ def test_radix_order_multi_tile(policy):
                             order_mode=ORDER_RADIX, max_calls=1 << 16), want)
 
 
-def test_full_size_1m_burst_first_steps():
+@pytest.mark.parametrize("policy,steps", [(ATLAS, 30), (ATLAS_EQ2, 12)])
+def test_full_size_1m_burst_first_steps(policy, steps):
     """BASELINE configs[3] at full size, in bench.py's launch configuration (select mode, graph
     replay, ATLAS, SPEC ladder, beta 2, BS 1024, P 32768): the first 30 steps of the 1M-call burst
     (registration of every call, then steady steps with completions and arrivals) decide exactly
@@ -428,17 +429,18 @@ def test_full_size_1m_burst_first_steps():
     from autx_workload import burst_mcts_mapreduce, BASE_SEED, CONFIG_INDEX
     from paper_2502_13965_b200 import TraceDriver
     tr = burst_mcts_mapreduce(1_000_000, seed=BASE_SEED + CONFIG_INDEX["mcts"])
-    cfg = spec_ladder_config(ATLAS, max_batch=1024, kv_budget=32768)
+    cfg = spec_ladder_config(policy, max_batch=1024, kv_budget=32768)
     eng = Engine(cfg, check_formulations=False)
     wl = Workload(tr)
-    s = make_sched(spec_ladder_config(ATLAS, max_batch=1024, kv_budget=32768),
+    s = make_sched(spec_ladder_config(policy, max_batch=1024, kv_budget=32768),
                    max_calls=1_300_000, max_programs=tr.n_programs + 1024)
     d = TraceDriver(tr, s)
     completed = []
-    for t in range(30):
+    for t in range(steps):
         cids = [int(tr.call_id[c]) for c in completed]
         ended = wl.release(t, completed)
-        rec_o = eng.step(t, cids, wl.arrivals(t))
+        arr = wl.arrivals(t)
+        rec_o = eng.step(t, cids, arr, wl.parents_of(arr) if policy == ATLAS_EQ2 else None)
         for pid in ended:
             eng.end_program(pid)
         completed = wl.ran(t, rec_o["batch"])
