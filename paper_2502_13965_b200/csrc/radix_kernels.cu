@@ -4,16 +4,16 @@
 // and the keys are sorted by a stable LSD radix sort, one byte per digit.  The table is kept in
 // seq (row) order, so sorting the high 32 bits stably already orders the low 32: only digits
 // 4..7 are sorted, and a digit whose 256-bin histogram is a single bin (all keys equal there)
-// is skipped.  The first min(BS, n_live) sorted keys become finalize's candidate list, and
-// finalize cuts the prefix exactly as in the selection path, so both modes give identical
-// decisions (tests/test_parity_gpu.py::test_radix_equals_select).
+// is skipped.  The first min(BS, n_live) sorted keys become the finalize's candidate list, and
+// the finalize cuts the prefix exactly as in the selection path, so both modes give identical
+// decisions (tests/test_parity_gpu.py::test_radix_order_*).
 //
 //   k_keys     dense pass: anti-starvation (same arithmetic as k_scan) + key pack + the four
 //              global 256-bin digit histograms (for skip detection)
 //   k_hist     per-tile 256-bin histogram of one digit        -> hist[digit value][tile]
 //   k_scan_h   exclusive scan of hist in (digit value, tile) order (one CTA)
 //   k_scatter  stable per-tile ranking (warp match + per-warp running counters) and scatter
-//   k_take     the first min(BS, n_live) keys -> candidate rows
+//   k_take     the first min(BS, n_live) keys -> region A of the finalize (k_fin)
 #include "autx_internal.cuh"
 #include "block_prims.cuh"
 #include "../../include/autx.h"
@@ -154,26 +154,22 @@ __global__ void __launch_bounds__(RX_THREADS) k_scatter(const uint64_t* in, uint
   }
 }
 
-__global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out, uint32_t BS, uint32_t K,
-                       uint32_t t) {
-  uint32_t n = min(BS, ctl->n_live);
+// The first min(BS, n_live) sorted keys -> region A (the finalize's candidates, already in key
+// order: q* = K, no region B).
+__global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out, uint32_t BS, uint32_t K) {
+  const uint32_t n = min(BS, ctl->n_live);
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    uint32_t sl = (uint32_t)keys[i];
-    CandRec r;
-    load_rec(ct, sl, &r);
-    out.cand[i] = sl;
-    out.cand_rec[i] = r;
-    out.ckey[i] = cand_key(r, t);
-  }
-  // previous batch: records for preempt; no region B (the full sort already ranked them)
-  for (uint32_t j = threadIdx.x; j < ctl->n_prev; j += blockDim.x) {
-    load_rec(ct, out.prev_slots[j], out.prev_rec + j);
-    out.ckey[n + j] = ~0ull;
+    const uint32_t s = (uint32_t)keys[i];
+    const uint32_t qf = ct.qf[s];
+    uint4* dst = reinterpret_cast<uint4*>(out.xrec + i);
+    const unsigned long long cid = ct.cid[s];
+    dst[0] = make_uint4((uint32_t)cid, (uint32_t)(cid >> 32), s, ct.arr[s]);
+    dst[1] = make_uint4(ct.tok[s], ct.exec[s], ct.mtime[s], ct.quanta[s]);
+    dst[2] = make_uint4(qf | ((qf & QF_RUN) ? ct.bidx[s] << 8 : 0u), 0u, 0u, 0u);
   }
   if (threadIdx.x == 0) {
-    ctl->n_cand_a = n;
-    ctl->n_cand_b = 0;
-    ctl->qstar = K;  // no extra running candidates: the sort already ordered them
+    ctl->n_x = n;
+    ctl->qstar = K;
   }
 }
 
@@ -210,7 +206,7 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
     ++passes;
   }
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_take<<<1, 1024, 0, s>>>(a, ct, ctl, out, pol.max_batch, pol.K, t);
+  k_take<<<1, 1024, 0, s>>>(a, ct, ctl, out, pol.max_batch, pol.K);
   if (passes_out) *passes_out = passes;
   return cudaGetLastError();
 }

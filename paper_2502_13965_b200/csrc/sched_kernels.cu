@@ -1,19 +1,19 @@
-// sm_100a kernels of one Autellix scheduling step.  Default chain,
-// PDL-linked on one stream:
+// sm_100a kernels of one Autellix scheduling step.  Select mode (the
+// default) runs the whole step as ONE cooperative kernel, k_step:
 //
-//   k_prologue   (a1, a2)  completion records -> process table (commutative reductions), rows
-//                          released; arrivals appended, inherit service, placed in a queue
-//   k_scan_bulk  (a4)      dense TMA-staged pass over every call: anti-starvation (integer
-//                          cross-multiply) + per-tile / per-super-tile queue counts
-//   k_gather_ss  (a5)      q*, m' and each tile's candidate offset from the counts; emits the
-//                          candidate set (<= BS rows of the lowest queues, table order) and the
-//                          previous batch's records and region-B keys
-//   k_rank       (a5)      multi-CTA rank counting of the <= 2 BS unique keys
-//   k_finalize   (a5, a6, a3, a7 plan)  prefix cutoff on BS and the KV budget, admit/preempt
-//                          lists, step accounting and eager demotion, GPU block allocation and
-//                          the swap plan, host mirrors
+//   prologue   (a1, a2)  completion records -> process table (commutative reductions), rows
+//                        released; arrivals appended, inherit service, placed in a queue
+//   dense pass (a3, a4)  every call: anti-starvation (integer cross-multiply) + per-tile /
+//                        per-super-tile queue counts; rows the prologue touches wait for it
+//   selection  (a5)      q*, m' and each tile's per-queue prefix; region A written in
+//                        (queue, seq) order (a stable counting sort by queue)
+//   finalize   (a5, a6, a3, a7 plan)  region B, the running-first partition inside each
+//                        (queue, arrival) group, the prefix cutoff on BS and the KV budget,
+//                        admit/preempt lists, step accounting and eager demotion, GPU block
+//                        allocation and the swap plan, host mirrors
 //
-// Every step of Alg. 1 runs here; the host only stages records.  Citations: see autx.h.
+// with two in-kernel grid barriers instead of kernel boundaries.  Every step of Alg. 1 runs here;
+// the host only stages records.  Citations: see autx.h.
 #include <algorithm>
 #include <cstdlib>
 
@@ -32,26 +32,14 @@ __device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc)
   return q;
 }
 
-#ifdef AUTX_PHASE_SYNC
-// profiling build: a barrier that must complete (its result is consumed) before the stamp, so
-// deferred-blocking barriers cannot shift time into the next phase
-#define STAMP(i) do { if (__syncthreads_count(1) && threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
-#else
-#define STAMP(i) do { if (threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
-#endif
-
-// Chain stamps (autx_set_timing mode 2, or always in a -DAUTX_CHAIN_STAMPS build): per kernel k
-// of the step chain, %globaltimer when CTA 0 passes griddepcontrol.wait (dbg[32 + 3k]), the
-// latest CTA end (33 + 3k) and the latest CTA start past the wait (34 + 3k); finalize moves
-// dbg[32, 64) to dbg[64, 96) at the step's end.  Off by default: one uniform parameter test.
+// Phase stamps (autx_set_timing mode 2, or always in a -DAUTX_CHAIN_STAMPS build): %globaltimer
+// at the step kernel's phase boundaries into ctl->dbg[40, 56) (see k_step); the finalize moves
+// them to dbg[64, 80) at the step's end.  Off by default: one uniform parameter test.
 #ifdef AUTX_CHAIN_STAMPS
-#define STAMPS_ON true
+#define STAMPS_ON(pol) true
 #else
-#define STAMPS_ON (pol.stamps != 0)
+#define STAMPS_ON(pol) ((pol).stamps != 0)
 #endif
-#define CHAIN_BEGIN(k) do { if (STAMPS_ON && threadIdx.x == 0) { const unsigned long long g_ = globaltimer(); \
-    if (blockIdx.x == 0) ctl->dbg[32 + 3 * (k)] = g_; atomicMax(&ctl->dbg[34 + 3 * (k)], g_); } } while (0)
-#define CHAIN_END(k) do { if (STAMPS_ON && threadIdx.x == 0) atomicMax(&ctl->dbg[33 + 3 * (k)], globaltimer()); } while (0)
 
 // ceil(tokens / block_tokens) (R14, R28): a shift when block_tokens is a power of two
 __device__ __forceinline__ uint32_t blocks_for(const Policy& pol, uint32_t tokens) {
@@ -96,7 +84,6 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
                               CompRec* s_rec = nullptr, const uint32_t* lin = nullptr) {
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
-  STAMP(16);
   for (uint32_t base = 0; base < n; base += NT) {
     uint32_t i = base + tid;
     bool valid = i < n;
@@ -114,9 +101,7 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       if (s_rec) s_rec[i] = r;  // the caller's shared-memory copy (n <= NT)
       if (lin) pt.crit[lin[i]] = r.cp;  // AUTX_ATLAS_EQ2: p(c) + t_c, an Eq. 2 operand
     }
-    STAMP(17);
     if (apply && valid) apply_record(pol, pt, r, t);
-    STAMP(18);
     // release the row and its KV (completed calls ran in step t-1, hence are resident)
     uint32_t nfree = 0, rslot = NONE;
     if (valid) {
@@ -149,7 +134,6 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
     __syncthreads();
   }
   if (tid == 0) ctl->t = t;
-  STAMP(19);
 }
 
 template <int NT>
@@ -164,13 +148,13 @@ __global__ void __launch_bounds__(NT) k_complete(Policy pol, CallTable ct, ProgT
 // Multi-engine: apply every engine's completion records (R22: sums and maxima commute, so the
 // replicated tables stay identical whatever the order).  recs of rank r start at
 // base + r * stride bytes, after a RouteHdr.
-__global__ void __launch_bounds__(FIN_THREADS) k_apply(Policy pol, ProgTable pt, const char* base,
+__global__ void __launch_bounds__(1024) k_apply(Policy pol, ProgTable pt, const char* base,
                                                        uint64_t stride, uint32_t G, uint32_t t) {
   for (uint32_t r = 0; r < G; ++r) {
     const RouteHdr* h = reinterpret_cast<const RouteHdr*>(base + r * stride);
     const CompRec* recs = reinterpret_cast<const CompRec*>(h + 1);
     const uint32_t n = h->n_comp;
-    for (uint32_t i = threadIdx.x; i < n; i += FIN_THREADS) apply_record(pol, pt, recs[i], t);
+    for (uint32_t i = threadIdx.x; i < n; i += 1024) apply_record(pol, pt, recs[i], t);
   }
 }
 
@@ -264,259 +248,148 @@ __global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const Arrival
   else register_one(pol, ct, pt, r, first_slot + i, t);
 }
 
-// Fused prologue of one step: completions (a1) then arrivals (a2), one CTA; a typical step's
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// ---------------------------------------------------------------------------------------------
+// Step prologue (a1 + a2) of one step: completions, then arrivals, by one CTA.  A typical step's
 // records travel inside the kernel parameters (no PCIe reads), larger batches through pointers.
-constexpr int PRO_THREADS = 256;
-__global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                          KvState kv, bool kv_on, CompRec* rec_out,
-                                                          const PrologueArgs a) {
-  __shared__ uint32_t s_comp[PRO_INLINE];
-  __shared__ ArrivalRec s_arr[PRO_INLINE];
+// Runs in the step kernel's finalize CTA (select mode) or as k_prologue (radix mode).  scratch:
+// shared memory for the records (the finalize's area, unused until the prologue is over).
+// ---------------------------------------------------------------------------------------------
+template <int NT>
+__device__ void prologue_body(const StepArgs& a, unsigned char* scratch) {
+  const PrologueArgs& p = a.pro;
+  const Policy& pol = a.pol;
+  CallTable ct = a.ct;
+  ProgTable pt = a.pt;
+  KvState kv = a.kv;
+  Ctl* ctl = a.ctl;
+  uint32_t* s_comp = reinterpret_cast<uint32_t*>(scratch);
+  ArrivalRec* s_arr = reinterpret_cast<ArrivalRec*>(scratch + PRO_INLINE * 4);
+  CompRec* s_rec = reinterpret_cast<CompRec*>(scratch + PRO_INLINE * (4 + sizeof(ArrivalRec)));
   const uint32_t tid = threadIdx.x;
-  const bool comp_inline = a.n_comp <= PRO_INLINE, arr_inline = a.n_arr <= PRO_INLINE;
+  const bool comp_inline = p.n_comp <= PRO_INLINE, arr_inline = p.n_arr <= PRO_INLINE;
+  const bool eq2 = pol.policy == AUTX_ATLAS_EQ2;
   if (comp_inline)
-    for (uint32_t i = tid; i < a.n_comp; i += PRO_THREADS) s_comp[i] = a.comp[i];
+    for (uint32_t i = tid; i < p.n_comp; i += NT) s_comp[i] = p.comp[i];
   if (arr_inline)
-    for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) s_arr[i] = a.arr[i];
-  pdl_wait();
-  pdl_trigger();
-  CHAIN_BEGIN(0);
+    for (uint32_t i = tid; i < p.n_arr; i += NT) s_arr[i] = p.arr[i];
   __syncthreads();
   if (comp_inline && arr_inline) {
-    // typical step: arrivals inherit the service after this step's completions (R10) computed
+    // typical step: arrivals inherit the service after this step's completions (R10), computed
     // here (old row value combined with the step's records of the same program, exactly what the
     // reductions leave in the row), so the row loads go out with the completion loads: one round
-    __shared__ CompRec s_rec[PRO_INLINE];
     uint32_t svc_old = 0;
-    const bool eq2 = pol.policy == AUTX_ATLAS_EQ2;
-    const bool my_arr = tid < a.n_arr;
+    const bool my_arr = tid < p.n_arr;
     if (my_arr && !eq2 && !(s_arr[tid].flags & 1u)) svc_old = __ldcg(&pt.info[s_arr[tid].prog].svc);
-    if (a.n_comp)
-      complete_body<PRO_THREADS>(pol, ct, pt, ctl, s_comp, a.n_comp, a.t, kv, kv_on, rec_out, true, s_rec,
-                                 eq2 ? a.comp_lin : nullptr);
+    if (p.n_comp)
+      complete_body<NT>(pol, ct, pt, ctl, s_comp, p.n_comp, p.t, kv, a.kv_on, a.rec_out, true, s_rec,
+                        eq2 ? p.comp_lin : nullptr);
     __syncthreads();
     if (my_arr) {
       const ArrivalRec r = s_arr[tid];
       uint32_t inh = 0;
       if (eq2) {
-        inh = eq2_priority(pt, a.par, r);  // parents completed this step are stored above the barrier
+        inh = eq2_priority(pt, p.par, r);  // parents completed this step are stored above the barrier
       } else if (!(r.flags & 1u)) {
         inh = svc_old;
-        for (uint32_t i = 0; i < a.n_comp; ++i)
+        for (uint32_t i = 0; i < p.n_comp; ++i)
           if (s_rec[i].prog == r.prog) inh = pol.policy == AUTX_ATLAS ? max(inh, s_rec[i].cp) : inh + s_rec[i].exec;
       }
-      register_one(pol, ct, pt, r, a.first_slot + tid, a.t, true, inh);
+      register_one(pol, ct, pt, r, p.first_slot + tid, p.t, true, inh);
     }
-    CHAIN_END(0);
-    return;
+  } else {
+    if (p.n_comp)
+      complete_body<NT>(pol, ct, pt, ctl, comp_inline ? s_comp : p.comp_ptr, p.n_comp, p.t, kv, a.kv_on,
+                        a.rec_out, true, nullptr, eq2 ? p.comp_lin : nullptr);
+    // arrivals inherit the service updated by this step's completions (R10): the reductions are
+    // performed at L2 before the barrier releases (fence), and register_one reads svc from L2
+    if (p.n_comp && p.n_arr) __threadfence();
+    __syncthreads();
+    const ArrivalRec* arr = arr_inline ? s_arr : p.arr_ptr;
+    for (uint32_t i = tid; i < p.n_arr; i += NT) {
+      if (eq2) register_one(pol, ct, pt, arr[i], p.first_slot + i, p.t, true, eq2_priority(pt, p.par, arr[i]));
+      else register_one(pol, ct, pt, arr[i], p.first_slot + i, p.t);
+    }
   }
-  const bool eq2 = pol.policy == AUTX_ATLAS_EQ2;
-  if (a.n_comp)
-    complete_body<PRO_THREADS>(pol, ct, pt, ctl, comp_inline ? s_comp : a.comp_ptr, a.n_comp, a.t, kv, kv_on,
-                               rec_out, true, nullptr, eq2 ? a.comp_lin : nullptr);
-  // arrivals inherit the service updated by this step's completions (R10): the reductions are
-  // performed at L2 before the barrier releases (fence), and register_one reads svc from L2
-  if (a.n_comp && a.n_arr) __threadfence();
-  __syncthreads();
-  const ArrivalRec* arr = arr_inline ? s_arr : a.arr_ptr;
-  for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) {
-    if (eq2) register_one(pol, ct, pt, arr[i], a.first_slot + i, a.t, true, eq2_priority(pt, a.par, arr[i]));
-    else register_one(pol, ct, pt, arr[i], a.first_slot + i, a.t);
-  }
-  CHAIN_END(0);
+  if (tid == 0) ctl->t = p.t;
 }
 
-cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl, KvState kv,
-                            bool kv_on, CompRec* rec_out, const PrologueArgs& a) {
-  return launch_pdl(k_prologue, 1, PRO_THREADS, 0, s, pol, ct, pt, ctl, kv, kv_on, rec_out, a);
+// Radix mode: the prologue as its own kernel, before the sort.
+__global__ void __launch_bounds__(ST_THREADS) k_prologue(const __grid_constant__ StepArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  prologue_body<ST_THREADS>(a, dsm);
 }
 
 // ---------------------------------------------------------------------------------------------
-// a4 + counting: the dense pass.  Every live call: wait = (t - base) - mtime (every active step
-// since the last reset either ran or waited), W = pwait[p] + wait, T = svc[p] + mtime; promote
-// to Q_1 iff W * beta_den >= beta_num * T and not 0/0 (Alg. 1 l.24-30, R3/R4/R7).  Demotion
-// (l.20-23) was applied eagerly by the previous step's finalize (only batch calls can exhaust a
-// quantum, and nothing in between reads q).  Bytes per call: qf 1 + prog 4 + base 4 + mtime 4
-// read; a promotion writes base (always: it becomes t) and only the fields that change: qf if
-// q != 0, mtime if != 0, quanta if q != 0 or mtime != 0 (a call in Q_1 that has not run since its
-// last reset already holds Q_1's quantum).
+// In-kernel synchronisation of the step kernel.  Its grid is launched cooperatively (every CTA is
+// co-resident), so CTAs may wait for each other: a CTA barrier orders the CTA's writes before
+// thread 0's gpu-scope fence + release increment; waiters poll with acquire loads.  Data written
+// by other CTAs in this kernel is read with ld.cg (L2), never through L1 or the read-only path.
 // ---------------------------------------------------------------------------------------------
-// Per-thread queue histogram: 16 queues x 4-bit fields in one u64 (<= 15 rows per thread), one
-// shift + add per row.  Warp reduction splits even/odd queues into 8-bit fields (<= 15 x 32 = 480
-// would overflow, so callers keep <= 8 rows per thread: <= 256 -> use 8-bit after summing <= 32
-// lanes of <= 8).
-__device__ __forceinline__ void hist_add(uint64_t& h, uint32_t q) { h += 1ull << (4 * q); }
-
-// Reduces the 4-bit histograms of a CTA into per-queue counts (written by the first 16 threads to
-// dst[0..16) and returned to thread k = queue k); wh: [NW][2] shared scratch.
-template <int NT>
-__device__ __forceinline__ uint32_t hist_reduce(uint64_t h, uint64_t (*wh)[2], uint32_t* dst) {
-  constexpr uint64_t M = 0x0F0F0F0F0F0F0F0Full;
-  // even / odd queues in 8-bit fields (<= 8 rows x 32 lanes = 256 would overflow: callers keep
-  // <= 7 rows per thread), each 32-bit half summed over the warp by one redux.sync
-  const uint64_t e = h & M, o = (h >> 4) & M;
-  const uint32_t e0 = __reduce_add_sync(0xffffffffu, (uint32_t)e), e1 = __reduce_add_sync(0xffffffffu, (uint32_t)(e >> 32));
-  const uint32_t o0 = __reduce_add_sync(0xffffffffu, (uint32_t)o), o1 = __reduce_add_sync(0xffffffffu, (uint32_t)(o >> 32));
-  if (lane_id() == 0) {
-    wh[warp_id()][0] = (uint64_t)e1 << 32 | e0;
-    wh[warp_id()][1] = (uint64_t)o1 << 32 | o0;
-  }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void grid_arrive(uint32_t* ctr) {
   __syncthreads();
-  if (threadIdx.x < MAX_K) {
-    const uint32_t k = threadIdx.x, sh = 8 * (k >> 1);
-    uint32_t sum = 0;
-#pragma unroll
-    for (int w = 0; w < NT / 32; ++w) sum += (uint32_t)(wh[w][k & 1] >> sh) & 0xffu;
-    dst[k] = sum;
-    return sum;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    red_release_add_u32(ctr, 1u);
   }
-  return 0;
 }
-
-__device__ __forceinline__ void count_q(uint64_t& c0, uint64_t& c1, uint64_t& c2, uint64_t& c3,
-                                        uint32_t q) {
-  uint64_t inc = 1ull << ((q & 3) * 16);
-  uint32_t g = q >> 2;
-  c0 += g == 0 ? inc : 0;
-  c1 += g == 1 ? inc : 0;
-  c2 += g == 2 ? inc : 0;
-  c3 += g == 3 ? inc : 0;
-}
-
-__global__ void __launch_bounds__(SCAN_THREADS, 3) k_scan(Policy pol, CallTable ct, ProgTable pt,
-                                                          Outputs out, uint32_t t, uint32_t n_rows) {
-  pdl_wait();
-  pdl_trigger();
-  const uint32_t tile = blockIdx.x;
-  const uint32_t row0 = tile * TILE + threadIdx.x * ROWS_PER_THREAD;
-  uint64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-  uint32_t npromo = 0, nlive = 0;
-  if (row0 < n_rows) {
-    const uint2 qv = __ldcs(reinterpret_cast<const uint2*>(ct.qf + row0));
-    const uint4 p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
-    const uint4 p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
-    uint4 b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
-    uint4 b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
-    uint4 m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
-    uint4 m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
-    uint32_t qfs[8], prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-    uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-    uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-#pragma unroll
-    for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
-    // independent gathers of the program rows first (memory-level parallelism)
-    uint32_t sv[8];
-    unsigned long long pw[8];
-    if (pol.beta_den != 0) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        bool live = !(qfs[j] & QF_DEAD);
-        PInfo pi = live ? pt.info[prog[j]] : PInfo{0, 0, 0ull};
-        sv[j] = pi.svc;
-        pw[j] = pi.pwait;
-      }
-    }
-    bool wq = false, wb = false, wm = false;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      uint32_t qf = qfs[j];
-      if (qf & QF_DEAD) continue;
-      ++nlive;
-      uint32_t q = qf & QF_QMASK;
-      if (pol.beta_den != 0) {
-        uint64_t W = pw[j] + (uint64_t)(t - base[j] - mtim[j]);
-        uint64_t T = (uint64_t)sv[j] + mtim[j];
-        if (!(W == 0 && T == 0) && mul_ge(W, pol.beta_den, T, pol.beta_num)) {
-          if (q != 0 || mtim[j] != 0) ct.quanta[row0 + j] = pol.quanta[0];
-          if (q != 0) { qfs[j] = qf & ~QF_QMASK; wq = true; }
-          if (mtim[j] != 0) { mtim[j] = 0; wm = true; }
-          base[j] = t;
-          wb = true;
-          q = 0;
-          ++npromo;
-        }
-      }
-      count_q(c0, c1, c2, c3, q);
-    }
-    if (wq) {
-      uint2 qn;
-      qn.x = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
-      qn.y = qfs[4] | (qfs[5] << 8) | (qfs[6] << 16) | (qfs[7] << 24);
-      *reinterpret_cast<uint2*>(ct.qf + row0) = qn;
-    }
-    if (wb) {
-      *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
-      *reinterpret_cast<uint4*>(ct.base + row0 + 4) = make_uint4(base[4], base[5], base[6], base[7]);
-    }
-    if (wm) {
-      *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
-      *reinterpret_cast<uint4*>(ct.mtime + row0 + 4) = make_uint4(mtim[4], mtim[5], mtim[6], mtim[7]);
-    }
-  }
-  // per-tile per-queue counts: warp reduce of packed 16-bit fields, then across warps
-  __shared__ uint64_t wc[SCAN_THREADS / 32][4];
-  __shared__ uint32_t wn[SCAN_THREADS / 32][2];
-  c0 = warp_sum(c0); c1 = warp_sum(c1); c2 = warp_sum(c2); c3 = warp_sum(c3);
-  npromo = warp_sum(npromo); nlive = warp_sum(nlive);
-  if (lane_id() == 0) {
-    wc[warp_id()][0] = c0; wc[warp_id()][1] = c1; wc[warp_id()][2] = c2; wc[warp_id()][3] = c3;
-    wn[warp_id()][0] = npromo; wn[warp_id()][1] = nlive;
-  }
+__device__ __forceinline__ void grid_wait(const uint32_t* ctr, uint32_t target) {
+  if (threadIdx.x == 0)
+    while (ld_acquire_u32(ctr) < target) __nanosleep(20);
   __syncthreads();
-  if (threadIdx.x < MAX_K) {
-    uint32_t k = threadIdx.x, sum = 0;
-#pragma unroll
-    for (int w = 0; w < SCAN_THREADS / 32; ++w) sum += (uint32_t)(wc[w][k >> 2] >> ((k & 3) * 16)) & 0xffffu;
-    out.tile_cnt[(size_t)tile * MAX_K + k] = sum;
-  } else if (threadIdx.x == 32) {
-    uint32_t a = 0, b = 0;
-#pragma unroll
-    for (int w = 0; w < SCAN_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
-    out.tile_stat[tile] = make_uint2(a, b);
-  }
+}
+__device__ __forceinline__ void wait_prologue(const Ctl* ctl, uint32_t seqno) {
+  if (threadIdx.x == 0)
+    while (ld_acquire_u32(&ctl->pro_seq) != seqno) __nanosleep(20);
+  __syncthreads();
 }
 
-enum { SEL_KERNEL = 0, SEL_FUSED = 1, SEL_GATHER = 2 };
-// One-tile-per-CTA variant of the dense pass sized for one wave: 256 threads x 8 rows, <= 64
-// registers so that 4 CTAs fit per SM (592 tiles = 1.2M rows resident at once).  Every row's
-// program-row gather is issued in one round (no per-tile serialisation as in the persistent
-// kernel), which is what bounds this latency-bound pass.  Per-row arithmetic is identical.
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
+// ---------------------------------------------------------------------------------------------
+// a3 + a4: the dense pass over one thread's 8 rows.  Every live call: wait = (t - base) - mtime
+// (every active step since the last reset either ran or waited), W = pwait[p] + wait,
+// T = svc[p] + mtime; promote to Q_1 iff W * beta_den >= beta_num * T and not 0/0 (Alg. 1
+// l.24-30, R3/R4/R7).  Demotion (l.20-23) was applied eagerly by the previous step's finalize
+// (only batch calls can exhaust a quantum, and nothing in between reads q).  Bytes per call:
+// qf 1 + prog 4 + base 4 + mtime 4 read; a promotion writes base (it becomes t) and only the
+// fields that change: qf if q != 0, mtime if != 0, quanta if q != 0 or mtime != 0 (a call in Q_1
+// that has not run since its last reset already holds Q_1's quantum).  CG: the program rows may
+// have been updated in this kernel (the prologue), so they are read from L2.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t qf_at(const uint32_t (&qw)[2], int j) { return (qw[j >> 2] >> (8 * (j & 3))) & 0xffu; }
+__device__ __forceinline__ uint32_t lane4(const uint4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
 
-// Per-row core of the dense pass over one thread's 8 rows (Alg. 1 l.24-30): program-row gather
-// (adj may correct it, see k_scan_fused), anti-starvation, promotion writes, queue histogram.
-struct NoAdj {
-  __device__ __forceinline__ void operator()(int, uint32_t, uint32_t&, unsigned long long&) const {}
-};
-template <typename Adj, int R>
-__device__ __forceinline__ void dense_rows(const Policy& pol, CallTable& ct, const ProgTable& pt, uint32_t t,
-                                           uint32_t row0, uint32_t (&qfs)[R], const uint32_t (&prog)[R],
-                                           uint32_t (&base)[R], uint32_t (&mtim)[R], bool wq0, const Adj& adj,
-                                           uint64_t& hq, uint32_t& npromo, uint32_t& nlive) {
-  static_assert(R == 4 || R == 8, "rows per thread");
+// qw: the 8 rows' flag bytes, packed 4 per word (updated in place).
+template <bool CG>
+__device__ __forceinline__ void dense_rows(const Policy& pol, const CallTable& ct, const ProgTable& pt, uint32_t t,
+                                           uint32_t row0, uint32_t (&qw)[2], const uint32_t (&prog)[8],
+                                           uint32_t (&base)[8], uint32_t (&mtim)[8], uint64_t& hq,
+                                           uint32_t& npromo, uint32_t& nlive) {
+  constexpr int R = 8;
   const bool anti = pol.beta_den != 0;
   const uint32_t bnum = pol.beta_num, bden = pol.beta_den, quanta0 = pol.quanta[0];
-  // the program rows of all 8 rows in one round (svc and pwait only: 12 of the 16 bytes)
   uint32_t svc[R], pwl[R];
   uint32_t big = t & 0x80000000u;  // any operand >= 2^31: this thread needs the exact path
   if (anti) {
-    uint32_t pwh[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) {  // all gathers first (one round trip), then the corrections
-      const bool live = !(qfs[j] & QF_DEAD);
-      const uint2 pw = live ? __ldg(reinterpret_cast<const uint2*>(&pt.info[prog[j]].pwait)) : make_uint2(0u, 0u);
-      svc[j] = live ? __ldg(&pt.info[prog[j]].svc) : 0u;
+    for (int j = 0; j < R; ++j) {  // the program rows of all 8 rows in one round
+      const bool live = !(qf_at(qw, j) & QF_DEAD);
+      const uint2* pp = reinterpret_cast<const uint2*>(&pt.info[prog[j]].pwait);
+      const uint2 pw = live ? (CG ? __ldcg(pp) : __ldg(pp)) : make_uint2(0u, 0u);
+      svc[j] = live ? (CG ? __ldcg(&pt.info[prog[j]].svc) : __ldg(&pt.info[prog[j]].svc)) : 0u;
       pwl[j] = pw.x;
-      pwh[j] = pw.y;
-    }
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      unsigned long long pwj = (unsigned long long)pwh[j] << 32 | pwl[j];
-      adj(j, prog[j], svc[j], pwj);
-      pwl[j] = (uint32_t)pwj;
-      big |= (uint32_t)(pwj >> 32) | (((uint32_t)pwj | svc[j]) & 0x80000000u);
+      big |= pw.y | ((pw.x | svc[j]) & 0x80000000u);
     }
   }
   // Alg. 1 l.24-26 (R3, R4).  With t, svc and pwait below 2^31 (wait, mtime <= t), W and T
@@ -524,14 +397,15 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, CallTable& ct, con
   // warp holding any larger operand takes the 128-bit comparison (starving()) for all its rows.
   uint32_t stv = 0;  // bit j: row j starving (not 0/0 and the ratio test holds)
   if (anti) {
-    // (lanes past n_rows skip this block: vote among the lanes present; each lane still sees
-    // its own operand, so the choice is exact whichever lanes take part)
     if (__any_sync(__activemask(), big != 0)) {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        const bool live = !(qfs[j] & QF_DEAD);
-        PInfo pi = live ? pt.info[prog[j]] : PInfo{0, 0, 0ull};
-        if (live) adj(j, prog[j], pi.svc, pi.pwait);
+        const bool live = !(qf_at(qw, j) & QF_DEAD);
+        PInfo pi{0, 0, 0ull};
+        if (live) {
+          pi.svc = __ldcg(&pt.info[prog[j]].svc);
+          pi.pwait = __ldcg(&pt.info[prog[j]].pwait);
+        }
         stv |= starving(pol, pi, t - base[j] - mtim[j], mtim[j]) ? 1u << j : 0u;
       }
     } else {
@@ -543,18 +417,18 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, CallTable& ct, con
       }
     }
   }
-  bool wq = wq0, wb = false, wm = false;
+  bool wb = false, wm = false;
+  const uint32_t qw0 = qw[0], qw1 = qw[1];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    const uint32_t qf = qfs[j];
+    const uint32_t qf = qf_at(qw, j);
     const bool live = !(qf & QF_DEAD);
     uint32_t q = qf & QF_QMASK;
     const bool pr = live && ((stv >> j) & 1u);  // Alg. 1 l.26
     if (pr && (q | mtim[j])) ct.quanta[row0 + j] = quanta0;
-    wq |= pr && q != 0;
     wm |= pr && mtim[j] != 0;
     wb |= pr;
-    qfs[j] = pr ? (qf & ~(uint32_t)QF_QMASK) : qf;
+    if (pr) qw[j >> 2] &= ~((uint32_t)QF_QMASK << (8 * (j & 3)));
     mtim[j] = pr ? 0u : mtim[j];
     base[j] = pr ? t : base[j];
     q = pr ? 0u : q;
@@ -562,12 +436,7 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, CallTable& ct, con
     nlive += live ? 1u : 0u;
     hq += live ? (1ull << (4 * q)) : 0ull;
   }
-  if (wq) {
-#pragma unroll
-    for (int h = 0; h < R / 4; ++h)
-      reinterpret_cast<uint32_t*>(ct.qf + row0)[h] =
-          qfs[4 * h] | (qfs[4 * h + 1] << 8) | (qfs[4 * h + 2] << 16) | (qfs[4 * h + 3] << 24);
-  }
+  if (qw[0] != qw0 || qw[1] != qw1) *reinterpret_cast<uint2*>(ct.qf + row0) = make_uint2(qw[0], qw[1]);
   if (wb) {
 #pragma unroll
     for (int h = 0; h < R / 4; ++h)
@@ -580,17 +449,73 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, CallTable& ct, con
   }
 }
 
-// Per-tile and per-super-tile queue counts + promotion / live totals of one CTA.
-template <int sel_mode, int NT = SCAN_THREADS>
-__device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t tile, uint64_t hq,
-                                            uint32_t npromo, uint32_t nlive) {
-  constexpr int NW = NT / 32;
-  __shared__ uint32_t wq16[NW][MAX_K / 2];  // per warp: 16-bit counts of queues 2w, 2w + 1
-  __shared__ uint32_t wn[NW];
+// The dense pass over one tile (thread: 8 consecutive rows).  Rows the prologue touches are
+// deferred until it has finished: this step's arrivals (rows >= first_new) and the rows of
+// programs with a completion in this step (s_filt: a 2048-bit filter of their process-table rows,
+// built from the parameters; a collision only defers more).  All other rows run at once, reading
+// nothing the prologue writes.  qw: the rows' flags after the pass.
+__device__ __forceinline__ void tile_pass(const StepArgs& a, uint32_t tile, const uint32_t* s_filt, bool filt_on,
+                                          uint32_t (&qw)[2], uint64_t& hq, uint32_t& npromo, uint32_t& nlive) {
   const uint32_t tid = threadIdx.x;
-  // per-queue counts: the 4-bit per-thread fields widened to 16 bits (<= 256 per warp), two
-  // queues per word, one redux.sync per word of the K queues in use
-  const uint32_t K = pol.K;
+  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  const bool have = row0 < a.n_rows;
+  const CallTable& ct = a.ct;
+  uint32_t prog[8], base[8], mtim[8];
+  bool defer = false;
+  qw[0] = qw[1] = 0x40404040u;  // QF_DEAD
+  if (have) {
+    const uint2 qv = *reinterpret_cast<const uint2*>(ct.qf + row0);
+    const uint4 p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+    const uint4 p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    const uint4 b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+    const uint4 b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+    const uint4 m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+    const uint4 m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+    qw[0] = qv.x;
+    qw[1] = qv.y;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      prog[j] = lane4(j < 4 ? p0 : p1, j & 3);
+      base[j] = lane4(j < 4 ? b0 : b1, j & 3);
+      mtim[j] = lane4(j < 4 ? m0 : m1, j & 3);
+    }
+    defer = a.defer_all || row0 + ROWS_PER_THREAD > a.first_new;
+    if (!defer && filt_on) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) defer |= ((s_filt[(prog[j] >> 5) & 63] >> (prog[j] & 31)) & 1u) != 0;
+    }
+    if (!defer) dense_rows<false>(a.pol, ct, a.pt, a.t, row0, qw, prog, base, mtim, hq, npromo, nlive);
+  }
+  if (__syncthreads_or(defer)) {
+    wait_prologue(a.ctl, a.seqno);
+    if (defer) {
+      const uint2 qv = __ldcg(reinterpret_cast<const uint2*>(ct.qf + row0));
+      const uint4 p0 = __ldcg(reinterpret_cast<const uint4*>(ct.prog + row0));
+      const uint4 p1 = __ldcg(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+      const uint4 b0 = __ldcg(reinterpret_cast<const uint4*>(ct.base + row0));
+      const uint4 b1 = __ldcg(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+      const uint4 m0 = __ldcg(reinterpret_cast<const uint4*>(ct.mtime + row0));
+      const uint4 m1 = __ldcg(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+      qw[0] = qv.x;
+      qw[1] = qv.y;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        prog[j] = lane4(j < 4 ? p0 : p1, j & 3);
+        base[j] = lane4(j < 4 ? b0 : b1, j & 3);
+        mtim[j] = lane4(j < 4 ? m0 : m1, j & 3);
+      }
+      dense_rows<true>(a.pol, ct, a.pt, a.t, row0, qw, prog, base, mtim, hq, npromo, nlive);
+    }
+  }
+}
+
+// Per-tile and per-super-tile queue counts, promotions and live rows of one tile.  The 4-bit
+// per-thread fields are widened to 16 bits (<= 256 per warp), two queues per word, one redux.sync
+// per word of the K queues in use.
+__device__ __forceinline__ void tile_publish(const StepArgs& a, uint32_t tile, uint64_t hq, uint32_t npromo,
+                                             uint32_t nlive, uint32_t (*wq16)[MAX_K / 2], uint32_t* wn) {
+  constexpr int NW = ST_THREADS / 32;
+  const uint32_t tid = threadIdx.x, K = a.pol.K;
 #pragma unroll
   for (int w = 0; w < MAX_K / 2; ++w) {
     if ((uint32_t)(2 * w) < K) {
@@ -608,1341 +533,482 @@ __device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs
 #pragma unroll
       for (int w = 0; w < NW; ++w) c += (wq16[w][tid >> 1] >> (16 * (tid & 1))) & 0xFFFFu;
     }
-    out.tile_cnt[(size_t)tile * MAX_K + tid] = c;
-    if (sel_mode == SEL_GATHER && c) atomicAdd(out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, c);
+    a.out.tile_cnt[(size_t)tile * MAX_K + tid] = c;
+    if (c) atomicAdd(a.out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, c);
   } else if (tid == 32) {
-    uint32_t a = 0, b = 0;
+    uint32_t pr = 0, lv = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) { a += wn[w] >> 16; b += wn[w] & 0xFFFFu; }
-    if (sel_mode == SEL_GATHER) {
-      uint32_t* qp = ctl->qpart[blockIdx.x % QP_LINES];
-      if (a) atomicAdd(qp + MAX_K, a);
-      if (b) atomicAdd(qp + MAX_K + 1, b);
-    } else {
-      out.tile_stat[tile] = make_uint2(a, b);
-    }
+    for (int w = 0; w < NW; ++w) { pr += wn[w] >> 16; lv += wn[w] & 0xFFFFu; }
+    uint32_t* qp = a.ctl->qpart[tile % QP_LINES];
+    if (pr) atomicAdd(qp + MAX_K, pr);
+    if (lv) atomicAdd(qp + MAX_K + 1, lv);
   }
+  __syncthreads();  // wq16 / wn reuse
 }
 
-// pre (A/B switch AUTX_SCAN_PRE): what a CTA does while it waits for the prologue (PDL).  Rows
-// below first_new (this step's first arrival slot) keep prog/base/mtime through the prologue
-// (it writes only new rows and the qf/loc of completed ones; everything earlier in the stream
-// is complete once this grid runs), so they may be read before the wait; qf, the program rows
-// and new rows are read after it.  0: nothing early; 1: prog early + L2 prefetch of the rows'
-// program entries and of the previous batch's records (the gather's cold reads); 2: prog, base
-// and mtime early + the same prefetches.
-template <int sel_mode>
-__global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                               Outputs out, uint32_t t, uint32_t n_rows,
-                                                               uint32_t first_new, uint32_t pre) {
-  const uint32_t tid = threadIdx.x, tile = blockIdx.x;
-  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
-  const bool early = pre != 0 && row0 + ROWS_PER_THREAD <= first_new;
-  uint4 p0, p1, b0, b1, m0, m1;
-  if (early) {
-    p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
-    p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
-    if (pre >= 2) {
-      b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
-      b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
-      m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
-      m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
-    }
-  }
-  if (pre != 0) {
-    // the previous batch's records: region B and most of region A in the gather
-    const uint32_t i = (gridDim.x - 1 - tile) * SCAN_THREADS + tid;
-    if (i < ctl->n_prev) {
-      const uint32_t sl = out.prev_slots[i];
-      prefetch_l2(ct.cid + sl); prefetch_l2(ct.arr + sl); prefetch_l2(ct.tok + sl);
-      prefetch_l2(ct.exec + sl); prefetch_l2(ct.mtime + sl); prefetch_l2(ct.quanta + sl);
-      prefetch_l2(ct.bidx + sl); prefetch_l2(ct.qf + sl);
-    }
-    if (early && pol.beta_den != 0) {
-      const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j == 0 || pr[j] != pr[j - 1]) prefetch_l2(pt.info + pr[j]);
-    }
-  }
-  pdl_wait();
-  pdl_trigger();
-  CHAIN_BEGIN(1);
-  uint64_t hq = 0;
-  uint32_t npromo = 0, nlive = 0;
-  if (row0 < n_rows) {
-    const uint2 qv = __ldcs(reinterpret_cast<const uint2*>(ct.qf + row0));
-    if (!early) {
-      p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
-      p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
-    }
-    if (!early || pre < 2) {
-      b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
-      b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
-      m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
-      m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
-    }
-    uint32_t qfs[8], prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-    uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-    uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-#pragma unroll
-    for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
-    dense_rows<NoAdj, 8>(pol, ct, pt, t, row0, qfs, prog, base, mtim, false, NoAdj{}, hq, npromo, nlive);
-  }
-  tile_counts<sel_mode>(pol, ctl, out, tile, hq, npromo, nlive);
-  CHAIN_END(1);
-}
-
-// Fused step prologue + dense pass (the default for a single engine whose step records ride
-// inline in the parameters, without the KV allocator, scalar policies).  The a1 / a2 effects
-// the dense pass depends on are derived where they are needed instead of by a kernel before it:
-//  - completed rows (Alg. 1 l.16-18) are marked dead by the thread that owns them;
-//  - every CTA folds this step's completion records into the program rows it reads (PLAS / FCFS /
-//    MLFQ sum, ATLAS max, pwait sum: exactly what the table update leaves before arrivals, R10);
-//  - arrivals (Alg. 1 l.9-14) are registered by the threads owning their rows, inheriting that
-//    post-completion service (a program first seen in this step inherits 0);
-//  - the process-table writes of a1 / a2 (reductions, last completion / arrival, new entries)
-//    are committed by k_gather_ss's last CTA, once every CTA here has read the old rows.
-// Results are identical to k_prologue + k_scan_tile (test_variants_gpu.py: fused_prologue).  Opt-in:
-// see step_can_fuse_prologue for the measured cost.
-// this step's completion records of program p folded into its row (rare: out of line)
-struct SvcPw { unsigned long long pw; uint32_t svc; };
-__device__ __noinline__ SvcPw fold_records(const CompRec* rec, uint32_t n, bool atlas, uint32_t p, uint32_t sv,
-                                           unsigned long long w) {
-  for (uint32_t i = 0; i < n; ++i)
-    if (rec[i].prog == p) {
-      sv = atlas ? max(sv, rec[i].cp) : sv + rec[i].exec;  // Alg. 1 l.4 / Eq. 1
-      w += rec[i].tw;                                      // Alg. 1 l.5-6 (R5)
-    }
-  return SvcPw{w, sv};
-}
-
-struct FusedAdj {
-  const CompRec* rec;    // shared: this step's completion records
-  const uint32_t* filt;  // shared: 1024-bit filter over their program rows
-  uint32_t n;
-  uint32_t newmask;      // bit j: row j is an arrival of a program first seen in this step
-  bool atlas;
-  __device__ __forceinline__ void operator()(int j, uint32_t p, uint32_t& svc, unsigned long long& pw) const {
-    if ((newmask >> j) & 1u) { svc = 0; pw = 0; return; }
-    if ((filt[(p >> 5) & 31] >> (p & 31)) & 1u) {
-      const SvcPw r = fold_records(rec, n, atlas, p, svc, pw);
-      svc = r.svc;
-      pw = r.pw;
-    }
-  }
+// ---------------------------------------------------------------------------------------------
+// a5 selection (after the first grid barrier).  q* = the smallest queue with
+// sum_{k<=q*} total_k >= BS (K if none), m' = BS - sum_{k<q*} total_k.  The BS smallest keys
+// (q, arrival, not-running, seq) are all among: every live row of a queue below q*, the first m'
+// rows of q* in table order (region A), and the running rows of q* that follow them inside the
+// same arrival group (region B: key order inside q* differs from table order only by moving
+// running calls forward within an arrival group).  Region A is written at its position in
+// (queue, seq) order: a stable counting sort by queue, base_q = sum_{k<q} total_k plus the rows
+// of queue q in earlier tiles (two-level prefix: super-tiles of SUP_TILES tiles, then the earlier
+// tiles of the own super-tile) plus the rank inside the tile.
+// ---------------------------------------------------------------------------------------------
+struct SelSmem {
+  uint32_t tot[ST_THREADS / MAX_K][MAX_K];  // per group of 16 threads: partial totals
+  uint32_t pre[ST_THREADS / MAX_K][MAX_K];  // ... partial prefix of the tile
+  uint32_t ownk[MAX_K];                     // the tile's own counts
+  uint32_t base[MAX_K], prek[MAX_K];        // sum_{k<q} total_k; rows of q in earlier tiles
+  uint32_t qs, m, nx, has, n_promo, n_live;
 };
 
-constexpr int FUSED_THREADS = 512, FUSED_ROWS = TILE / FUSED_THREADS;  // 4 rows per thread: no spills
-template <int sel_mode>
-__global__ void __launch_bounds__(FUSED_THREADS, 2) k_scan_fused(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                                 Outputs out, uint32_t n_rows, CompRec* rec_out,
-                                                                 uint32_t* comp_out, ArrivalRec* arr_out,
-                                                                 const PrologueArgs a) {
-  constexpr int R = FUSED_ROWS;
-  __shared__ CompRec s_rec[PRO_INLINE];
-  __shared__ uint32_t s_filt[32];
-  __shared__ uint32_t s_dead[TILE / 32];
-  const uint32_t tid = threadIdx.x, tile = blockIdx.x, t = a.t;
-  const uint32_t row0 = tile * TILE + tid * R;
-  if (tid < 32) s_filt[tid] = 0;
-  if (tid < TILE / 32) s_dead[tid] = 0;
-  __syncthreads();
-  pdl_wait();
-  pdl_trigger();
-  CHAIN_BEGIN(1);
-  // (1) one round of loads: this thread's rows and, for thread i < n_comp, completion record i
-  const bool rows = row0 < n_rows;
-  uint32_t qv = 0;
-  uint4 p0{}, b0{}, m0{};
-  if (rows) {
-    qv = __ldcs(reinterpret_cast<const uint32_t*>(ct.qf + row0));
-    p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
-    b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
-    m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+__device__ void select_for(const StepArgs& a, uint32_t tile, SelSmem& S) {
+  constexpr int NG = ST_THREADS / MAX_K;  // 32 groups
+  const uint32_t tid = threadIdx.x, h = tid / MAX_K, k = tid % MAX_K;
+  const uint32_t K = a.pol.K, BS = a.pol.max_batch;
+  const uint32_t nsup = (a.ntiles + SUP_TILES - 1) / SUP_TILES;
+  const bool is_tile = tile != NONE;
+  const uint32_t my_sup = is_tile ? tile / SUP_TILES : 0u, tr = my_sup * SUP_TILES + h;
+  uint32_t tot = 0, pre = 0;
+  if (k < K) {
+    // every load issued before any is consumed: the tile row, then up to 2 super-tile rows per
+    // group (8M rows), more in a loop
+    const bool has_tr = is_tile && h < SUP_TILES && tr <= tile;
+    const uint32_t c = has_tr ? __ldcg(a.out.tile_cnt + (size_t)tr * MAX_K + k) : 0u;
+    const uint32_t v0 = h < nsup ? __ldcg(a.out.sup_cnt + h * MAX_K + k) : 0u;
+    const uint32_t v1 = h + NG < nsup ? __ldcg(a.out.sup_cnt + (h + NG) * MAX_K + k) : 0u;
+    tot = v0 + v1;
+    pre = (is_tile && h < my_sup ? v0 : 0u) + (is_tile && h + NG < my_sup ? v1 : 0u);
+    for (uint32_t s = h + 2 * NG; s < nsup; s += NG) {
+      const uint32_t w = __ldcg(a.out.sup_cnt + s * MAX_K + k);
+      tot += w;
+      pre += (is_tile && s < my_sup) ? w : 0u;
+    }
+    if (has_tr) {
+      if (tr < tile) pre += c;
+      else S.ownk[k] = c;
+    }
+  } else if (is_tile && h == tile % SUP_TILES) {
+    S.ownk[k] = 0;
   }
-  if (tid < a.n_comp) {
-    const uint32_t cs = a.comp[tid];
-    const uint32_t e = ct.exec[cs];
-    CompRec r;
-    r.prog = ct.prog[cs];
-    r.exec = e;
-    r.cp = ct.inh[cs] + e;           // ATLAS critical-path candidate (Alg. 1 l.4)
-    r.tw = (t - ct.arr[cs]) - e;     // totwait (R5, R29)
-    s_rec[tid] = r;
-    atomicOr(&s_filt[(r.prog >> 5) & 31], 1u << (r.prog & 31));
-    if (cs / TILE == tile) atomicOr(&s_dead[(cs % TILE) >> 5], 1u << (cs & 31));
-    if (tile == 0) { rec_out[tid] = r; comp_out[tid] = cs; }  // for the commit
-  }
-  if (tile == 0) {
-    for (uint32_t i = tid; i < a.n_arr; i += FUSED_THREADS) arr_out[i] = a.arr[i];
-    if (tid == 0) ctl->t = t;
+  S.tot[h][k] = tot;
+  S.pre[h][k] = pre;
+  if (tid >= 256 && tid < 288) {
+    // promotions (even lanes) and live rows (odd lanes), for the host record
+    const uint32_t l = tid - 256;
+    uint32_t v = __ldcg(&a.ctl->qpart[l >> 1][MAX_K + (l & 1)]);
+#pragma unroll
+    for (int d = 2; d < 32; d <<= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (l == 0) S.n_promo = v;
+    if (l == 1) S.n_live = v;
   }
   __syncthreads();
-  uint64_t hq = 0;
-  uint32_t npromo = 0, nlive = 0;
-  if (rows) {
-    uint32_t qfs[R], prog[R] = {p0.x, p0.y, p0.z, p0.w};
-    uint32_t base[R] = {b0.x, b0.y, b0.z, b0.w};
-    uint32_t mtim[R] = {m0.x, m0.y, m0.z, m0.w};
-    const uint32_t deadm = (s_dead[(row0 % TILE) >> 5] >> (row0 & 31)) & ((1u << R) - 1);
-#pragma unroll
-    for (int j = 0; j < R; ++j) qfs[j] = ((deadm >> j) & 1u) ? (uint32_t)QF_DEAD : (qv >> (8 * j)) & 0xffu;
-    FusedAdj adj{s_rec, s_filt, a.n_comp, 0u, pol.policy == AUTX_ATLAS};
-    bool wq0 = deadm != 0;
-    // this step's arrivals among this thread's rows (Alg. 1 l.9-14)
-    const uint32_t fs = a.first_slot, fe = a.first_slot + a.n_arr;
-    if (row0 + R > fs && row0 < fe) {
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const uint32_t row = row0 + j;
-        if (row < fs || row >= fe) continue;
-        const ArrivalRec ar = a.arr[row - fs];
-        uint32_t inh = 0;
-        if (ar.flags & 1u) {
-          adj.newmask |= 1u << j;
-        } else {
-          unsigned long long pw = 0;
-          inh = __ldg(&pt.info[ar.prog].svc);
-          adj(j, ar.prog, inh, pw);  // Alg. 1 l.11: the service after this step's completions
-        }
-        qfs[j] = register_row(pol, ct, ar, row, t, inh);
-        prog[j] = ar.prog;
-        base[j] = t;
-        mtim[j] = 0;
-        wq0 = true;
-      }
-    }
-    dense_rows<FusedAdj, R>(pol, ct, pt, t, row0, qfs, prog, base, mtim, wq0, adj, hq, npromo, nlive);
-  }
-  tile_counts<sel_mode, FUSED_THREADS>(pol, ctl, out, tile, hq, npromo, nlive);
-  CHAIN_END(1);
-}
-
-// The process-table writes of a fused step prologue (see k_scan_fused), after the dense pass:
-// new entries, last arrival / completion, the completion reductions (R10: sums and maxima
-// commute), released rows.
-__device__ void commit_prologue(const Policy& pol, CallTable& ct, ProgTable& pt, uint32_t t, uint32_t nc,
-                                uint32_t na, const CompRec* rec, const uint32_t* cs, const ArrivalRec* arr) {
-  // completions first: a program that ended after them may hand its row to a program first
-  // seen in this step, whose entry must start from zero (the order of k_prologue)
-  for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
-    apply_record(pol, pt, rec[i], t);
-    ct.loc[cs[i]] = NONE;
-  }
-  __threadfence();
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) {
-    const ArrivalRec r = arr[i];
-    if (r.flags & 2u) {
-      pt.info[r.prog] = PInfo{0, 0, 0ull};
-      pt.last_comp[r.prog] = NONE;
-    }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) pt.last_arr[arr[i].prog] = t;
-}
-
-// Persistent, TMA-staged variant of the dense pass (the default): each CTA walks tiles
-// blockIdx.x, +gridDim.x, ...; one thread keeps SCAN_STAGES tiles in flight with
-// cp.async.bulk (global -> shared, completion counted on an mbarrier), so HBM keeps streaming
-// while the CTA gathers program rows and computes on the current tile.  Per-row arithmetic and
-// outputs are identical to k_scan.
-constexpr int SCAN_STAGES = 3;
-constexpr uint32_t STAGE_QF = TILE;             // bytes of qf per tile
-constexpr uint32_t STAGE_U32 = TILE * 4;        // bytes of one u32 field per tile
-constexpr uint32_t STAGE_BYTES = STAGE_QF + 3 * STAGE_U32;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void issue_tile(const CallTable& ct, uint32_t tile, unsigned char* st, uint64_t* bar) {
-  const size_t r0 = (size_t)tile * TILE;
-  mbar_expect_tx(bar, STAGE_BYTES);
-  bulk_g2s(st, ct.qf + r0, STAGE_QF, bar);
-  bulk_g2s(st + STAGE_QF, ct.prog + r0, STAGE_U32, bar);
-  bulk_g2s(st + STAGE_QF + STAGE_U32, ct.base + r0, STAGE_U32, bar);
-  bulk_g2s(st + STAGE_QF + 2 * STAGE_U32, ct.mtime + r0, STAGE_U32, bar);
-}
-
-extern __shared__ __align__(128) unsigned char scan_smem[];
-
-constexpr int BULK_THREADS = 512;                 // 16 warps per CTA, 4 rows per thread
-constexpr int BULK_ROWS = TILE / BULK_THREADS;
-
-template <int NT>
-__device__ void select_body(const Policy& pol, const CallTable& ct, Ctl* ctl, Outputs& out, uint32_t ntiles);
-
-template <int sel_mode>
-__global__ void __launch_bounds__(BULK_THREADS, 2) k_scan_bulk(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                               Outputs out, uint32_t t, uint32_t ntiles) {
-  // sel_mode: SEL_KERNEL = per-tile counts + stats for k_select; SEL_FUSED = the last CTA runs the
-  // selection; SEL_GATHER = per-tile counts + per-queue totals (global atomics) for k_gather_ss
-  pdl_wait();
-  CHAIN_BEGIN(1);
-  __shared__ __align__(8) uint64_t bars[SCAN_STAGES];
-  __shared__ uint64_t wh[BULK_THREADS / 32][2];
-  __shared__ uint32_t wn[BULK_THREADS / 32][2];
-  const uint32_t tid = threadIdx.x;
-  if (tid == 0) {
-    for (int i = 0; i < SCAN_STAGES; ++i) mbar_init(&bars[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int i = 0; i < SCAN_STAGES; ++i) {
-      uint32_t tl = blockIdx.x + i * gridDim.x;
-      if (tl < ntiles) issue_tile(ct, tl, scan_smem + i * STAGE_BYTES, &bars[i]);
-    }
-  pdl_trigger();
-  const bool anti = pol.beta_den != 0;
-  const uint32_t bnum = pol.beta_num, bden = pol.beta_den, quanta0 = pol.quanta[0];
-  uint32_t it = 0;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const uint32_t stage = it % SCAN_STAGES;
-    unsigned char* st = scan_smem + stage * STAGE_BYTES;
-    mbar_wait(&bars[stage], (it / SCAN_STAGES) & 1);
-    const uint32_t lr = tid * BULK_ROWS;
-    const uint32_t row0 = tile * TILE + lr;
-    const uint32_t qv = *reinterpret_cast<const uint32_t*>(st + lr);
-    const uint4 pg = *reinterpret_cast<const uint4*>(st + STAGE_QF + lr * 4);
-    const uint4 bs = *reinterpret_cast<const uint4*>(st + STAGE_QF + STAGE_U32 + lr * 4);
-    const uint4 mt = *reinterpret_cast<const uint4*>(st + STAGE_QF + 2 * STAGE_U32 + lr * 4);
-    __syncthreads();  // every thread has its rows in registers: the stage can be refilled
-    if (tid == 0) {
-      uint32_t nxt = tile + SCAN_STAGES * gridDim.x;
-      if (nxt < ntiles) issue_tile(ct, nxt, st, &bars[stage]);
-    }
-    uint32_t qfs[4], prog[4] = {pg.x, pg.y, pg.z, pg.w}, base[4] = {bs.x, bs.y, bs.z, bs.w},
-             mtim[4] = {mt.x, mt.y, mt.z, mt.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) qfs[j] = (qv >> (8 * j)) & 0xffu;
-    PInfo pi[4];
-    if (anti) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) pi[j] = !(qfs[j] & QF_DEAD) ? pt.info[prog[j]] : PInfo{0, 0, 0ull};
-    }
-    // per row, branch-free except the rare wide-arithmetic path of the starvation test
-    uint64_t hq = 0;
-    uint32_t npromo = 0, nlive = 0;
-    bool wq = false, wb = false, wm = false;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t qf = qfs[j];
-      const bool live = !(qf & QF_DEAD);
-      uint32_t q = qf & QF_QMASK;
-      bool pr = false;
-      if (anti) {
-        const uint32_t wait = t - base[j] - mtim[j];
-        const uint32_t W32 = (uint32_t)pi[j].pwait + wait, T32 = pi[j].svc + mtim[j];
-        const bool fast = (uint32_t)(pi[j].pwait >> 32) == 0 && W32 >= wait && T32 >= pi[j].svc;
-        bool st = (W32 | T32) != 0 && (uint64_t)W32 * bden >= (uint64_t)T32 * bnum;
-        if (!fast) st = starving(pol, pi[j], wait, mtim[j]);
-        pr = live && st;  // Alg. 1 l.26
-      }
-      if (pr && (q | mtim[j])) ct.quanta[row0 + j] = quanta0;
-      wq |= pr && q != 0;
-      wm |= pr && mtim[j] != 0;
-      wb |= pr;
-      qfs[j] = pr ? (qf & ~(uint32_t)QF_QMASK) : qf;
-      mtim[j] = pr ? 0u : mtim[j];
-      base[j] = pr ? t : base[j];
-      q = pr ? 0u : q;
-      npromo += pr ? 1u : 0u;
-      nlive += live ? 1u : 0u;
-      hq += live ? (1ull << (4 * q)) : 0ull;
-    }
-    if (wq) *reinterpret_cast<uint32_t*>(ct.qf + row0) = qfs[0] | (qfs[1] << 8) | (qfs[2] << 16) | (qfs[3] << 24);
-    if (wb) *reinterpret_cast<uint4*>(ct.base + row0) = make_uint4(base[0], base[1], base[2], base[3]);
-    if (wm) *reinterpret_cast<uint4*>(ct.mtime + row0) = make_uint4(mtim[0], mtim[1], mtim[2], mtim[3]);
-    const uint32_t pl = __reduce_add_sync(0xffffffffu, (npromo << 16) | nlive);  // <= 128 each per warp
-    if (lane_id() == 0) { wn[warp_id()][0] = pl >> 16; wn[warp_id()][1] = pl & 0xffffu; }
-    const uint32_t qc = hist_reduce<BULK_THREADS>(hq, wh, out.tile_cnt + (size_t)tile * MAX_K);
-    uint32_t* qp = ctl->qpart[blockIdx.x % QP_LINES];
-    if (sel_mode == SEL_GATHER && qc) atomicAdd(out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, qc);  // tid < MAX_K
-    if (tid == 32) {
-      uint32_t a = 0, b = 0;
-#pragma unroll
-      for (int w = 0; w < BULK_THREADS / 32; ++w) { a += wn[w][0]; b += wn[w][1]; }
-      if (sel_mode == SEL_GATHER) {
-        if (a) atomicAdd(qp + MAX_K, a);
-        if (b) atomicAdd(qp + MAX_K + 1, b);
-      } else {
-        out.tile_stat[tile] = make_uint2(a, b);
-      }
-    }
-    __syncthreads();  // wh/wn reuse
-  }
-  CHAIN_END(1);
-  // optionally, the last CTA to finish picks the boundary queue and the tile offsets
-  if constexpr (sel_mode != SEL_FUSED) return;
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) last = atomicAdd(&ctl->tiles_done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (tid == 0) ctl->tiles_done = 0;
-  select_body<BULK_THREADS>(pol, ct, ctl, out, ntiles);
-}
-
-// One CTA: q* = smallest q with sum_{k<=q} total_k >= BS (K if none), m' = BS - sum_{k<q*}
-// total_k.  Candidates: every live row with q < q*, plus the first m' rows of q* in table order.
-// Any call among the BS smallest keys is a candidate or a running call of q* (finalize adds
-// those): inside q* the key order (arr, not-running, seq) differs from table order (arr, seq)
-// only by moving running calls forward within an arrival group.  Per tile: the q* rows of
-// earlier tiles (tile_pre) and the candidate output offset
-//     off(tile) = sum_{k<q*} prefix_k(tile) + min(prefix_{q*}(tile), m').
-constexpr int SEL_THREADS = 512;  // one tile per thread up to 512 tiles (1M rows); fewer warps
-template <int NT>
-__device__ void find_boundary(const Policy& pol, const CallTable& ct, Ctl* ctl, uint32_t qs, uint32_t btile,
-                              uint32_t bk);
-
-template <int NT>
-__device__ void select_body(const Policy& pol, const CallTable& ct, Ctl* ctl, Outputs& out, uint32_t ntiles) {
-  __shared__ uint32_t tot[MAX_K + 2];
-  __shared__ unsigned long long red[33];
-  __shared__ uint32_t s_qstar, s_m, s_btile, s_bk;
-  const uint32_t tid = threadIdx.x;
-  if (tid < MAX_K + 2) tot[tid] = 0;
-  if (tid == 0) { s_btile = NONE; s_bk = 0; }
-  __syncthreads();
-  if (ntiles <= NT) {
-    // fast path: one tile per thread, its 16 counters stay in registers (one load round trip)
-    uint32_t x[MAX_K];
-    uint2 st = make_uint2(0, 0);
-    if (tid < ntiles) {
-      const uint4* c = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)tid * MAX_K);
-#pragma unroll
-      for (int v = 0; v < MAX_K / 4; ++v) {
-        uint4 y = __ldcg(c + v);
-        x[4 * v] = y.x; x[4 * v + 1] = y.y; x[4 * v + 2] = y.z; x[4 * v + 3] = y.w;
-      }
-      st = __ldcg(out.tile_stat + tid);
-    } else {
-#pragma unroll
-      for (int k = 0; k < MAX_K; ++k) x[k] = 0;
-    }
-#pragma unroll
-    for (int k = 0; k < MAX_K; ++k) {
-      uint32_t w = warp_sum(x[k]);
-      if (lane_id() == 0 && w) atomicAdd(&tot[k], w);
-    }
-    uint32_t ap = warp_sum(st.x), al = warp_sum(st.y);
-    if (lane_id() == 0) {
-      if (ap) atomicAdd(&tot[MAX_K], ap);
-      if (al) atomicAdd(&tot[MAX_K + 1], al);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t cum = 0, qs = pol.K, m = 0;
-      for (uint32_t k = 0; k < pol.K; ++k) {
-        if (cum + tot[k] >= pol.max_batch) { qs = k; m = pol.max_batch - cum; break; }
-        cum += tot[k];
-      }
-      s_qstar = qs;
-      s_m = m;
-      ctl->qstar = qs;
-      ctl->mprime = m;
-      ctl->n_promoted = tot[MAX_K];
-      ctl->n_live = tot[MAX_K + 1];
-    }
-    __syncthreads();
-    const uint32_t qs = s_qstar, m = s_m;
-    uint32_t a = 0, cq = 0;
-#pragma unroll
-    for (int k = 0; k < MAX_K; ++k) {
-      a += (uint32_t)k < qs ? x[k] : 0u;
-      cq += (uint32_t)k == qs ? x[k] : 0u;
-    }
-    unsigned long long total;
-    uint64_t pre = block_excl_scan<unsigned long long, NT>(((uint64_t)a << 32) | cq, red, &total);
-    if (tid < ntiles) {
-      uint32_t pre_a = (uint32_t)(pre >> 32), pre_q = (uint32_t)pre;
-      out.tile_pre[tid] = pre_q;
-      out.tile_off[tid] = pre_a + min(pre_q, m);
-      if (pre_q < m && m <= pre_q + cq) { s_btile = tid; s_bk = m - 1 - pre_q; }
-    }
-    if (tid == 0) {
-      uint32_t n = (uint32_t)(total >> 32) + min((uint32_t)total, m);
-      out.tile_off[ntiles] = n;
-      ctl->n_cand_a = n;
-      ctl->n_cand_b = 0;
-    }
-    __syncthreads();
-    find_boundary<NT>(pol, ct, ctl, qs, s_btile, s_bk);
-    return;
-  }
-  const uint32_t per = (ntiles + NT - 1) / NT;
-  const uint32_t t0 = min(ntiles, tid * per), t1 = min(ntiles, t0 + per);
-  uint32_t acc[MAX_K];
-#pragma unroll
-  for (int k = 0; k < MAX_K; ++k) acc[k] = 0;
-  uint32_t ap = 0, al = 0;
-  for (uint32_t tl = t0; tl < t1; ++tl) {
-    const uint4* c = reinterpret_cast<const uint4*>(out.tile_cnt + (size_t)tl * MAX_K);
-#pragma unroll
-    for (int v = 0; v < MAX_K / 4; ++v) {
-      uint4 x = __ldcg(c + v);
-      acc[4 * v] += x.x; acc[4 * v + 1] += x.y; acc[4 * v + 2] += x.z; acc[4 * v + 3] += x.w;
-    }
-    uint2 st = __ldcg(out.tile_stat + tl);
-    ap += st.x;
-    al += st.y;
-  }
-#pragma unroll
-  for (int k = 0; k < MAX_K; ++k) {
-    uint32_t w = warp_sum(acc[k]);
-    if (lane_id() == 0 && w) atomicAdd(&tot[k], w);
-  }
-  ap = warp_sum(ap);
-  al = warp_sum(al);
-  if (lane_id() == 0) {
-    if (ap) atomicAdd(&tot[MAX_K], ap);
-    if (al) atomicAdd(&tot[MAX_K + 1], al);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    uint32_t cum = 0, qs = pol.K, m = 0;
-    for (uint32_t k = 0; k < pol.K; ++k) {
-      if (cum + tot[k] >= pol.max_batch) { qs = k; m = pol.max_batch - cum; break; }
-      cum += tot[k];
-    }
-    s_qstar = qs;
-    s_m = m;
-    ctl->qstar = qs;
-    ctl->mprime = m;
-    ctl->n_promoted = tot[MAX_K];
-    ctl->n_live = tot[MAX_K + 1];
-  }
-  __syncthreads();
-  const uint32_t qs = s_qstar, m = s_m;
-  // per thread: (rows of queues < q*, rows of q*) over its tile range, packed in one u64 scan
-  uint64_t mine = 0;
-  for (uint32_t tl = t0; tl < t1; ++tl) {
-    const uint32_t* c = out.tile_cnt + (size_t)tl * MAX_K;
-    uint32_t a = 0;
-    for (uint32_t k = 0; k < qs && k < pol.K; ++k) a += c[k];
-    uint32_t cq = qs < pol.K ? c[qs] : 0;
-    mine += ((uint64_t)a << 32) | cq;
-  }
-  unsigned long long total;
-  uint64_t pre = block_excl_scan<unsigned long long, NT>(mine, red, &total);
-  uint32_t pre_a = (uint32_t)(pre >> 32), pre_q = (uint32_t)pre;
-  for (uint32_t tl = t0; tl < t1; ++tl) {
-    const uint32_t* c = out.tile_cnt + (size_t)tl * MAX_K;
-    uint32_t a = 0;
-    for (uint32_t k = 0; k < qs && k < pol.K; ++k) a += c[k];
-    uint32_t cq = qs < pol.K ? c[qs] : 0;
-    out.tile_pre[tl] = pre_q;
-    out.tile_off[tl] = pre_a + min(pre_q, m);
-    if (pre_q < m && m <= pre_q + cq) { s_btile = tl; s_bk = m - 1 - pre_q; }
-    pre_a += a;
-    pre_q += cq;
-  }
-  if (tid == 0) {
-    uint32_t ta = (uint32_t)(total >> 32), tq = (uint32_t)total;
-    uint32_t n = ta + min(tq, m);
-    out.tile_off[ntiles] = n;
-    ctl->n_cand_a = n;
-    ctl->n_cand_b = 0;
-  }
-  __syncthreads();
-  find_boundary<NT>(pol, ct, ctl, qs, s_btile, s_bk);
-}
-
-// Slot of region A's last row of q*: the bk-th (0-based) live row of q* inside tile btile.  Region
-// A's q* part is exactly the live q* rows with slot <= it (table order = slot order), which lets
-// the gather leave previous-batch rows already in A out of region B.
-template <int NT>
-__device__ void find_boundary(const Policy& pol, const CallTable& ct, Ctl* ctl, uint32_t qs, uint32_t btile,
-                              uint32_t bk) {
-  __shared__ uint32_t red_b[33];
-  if (btile == NONE) {  // q* = K (every live call is a candidate) or m' = 0
-    if (threadIdx.x == 0) ctl->qs_boundary = NONE;
-    return;
-  }
-  constexpr uint32_t CH = TILE / NT;  // qf bytes per thread
-  const uint32_t r0 = btile * TILE + threadIdx.x * CH;
-  uint32_t cnt = 0;
-  uint8_t b[CH];
-#pragma unroll
-  for (uint32_t j = 0; j < CH; ++j) {
-    b[j] = ct.qf[r0 + j];
-    cnt += (!(b[j] & QF_DEAD) && (b[j] & QF_QMASK) == qs) ? 1u : 0u;
-  }
-  uint32_t pre = block_excl_scan<uint32_t, NT>(cnt, red_b, nullptr);
-  if (pre <= bk && bk < pre + cnt) {
-    uint32_t k = pre;
-#pragma unroll
-    for (uint32_t j = 0; j < CH; ++j)
-      if (!(b[j] & QF_DEAD) && (b[j] & QF_QMASK) == qs) {
-        if (k == bk) ctl->qs_boundary = r0 + j;
-        ++k;
-      }
-  }
-}
-
-__global__ void __launch_bounds__(SEL_THREADS) k_select(Policy pol, CallTable ct, Ctl* ctl, Outputs out, uint32_t ntiles) {
-  pdl_wait();
-  pdl_trigger();
-  CHAIN_BEGIN(2);
-  select_body<SEL_THREADS>(pol, ct, ctl, out, ntiles);
-  CHAIN_END(2);
-}
-
-// ---------------------------------------------------------------------------------------------
-// a5 candidate gather: tiles with candidates re-read their 2 KB of qf and emit one CandRec per
-// candidate (q < q*, or among the first m' rows of q*) in table order.  CTAs past the last tile
-// write the records of the previous batch (the resident set) for preempt/region B.
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void gather_body(Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, uint32_t n_rows, uint32_t ntiles, uint32_t t) {
-  const uint32_t tile = blockIdx.x;
-  if (tile >= ntiles) {
-    // previous batch: records (for preempt) and, for its live calls of q*, keys (region B;
-    // duplicates of region A are removed after the sort); other entries get the ~0 sentinel
-    // (the slot load covers the buffer's capacity so that it does not wait for n_prev; k_rank
-    // counts the keys that remain)
-    const uint32_t j = (tile - ntiles) * SCAN_THREADS + threadIdx.x;
-    const uint32_t n_prev = ctl->n_prev, bnd = ctl->qs_boundary, qs = ctl->qstar, na = ctl->n_cand_a;
-    const uint32_t sl = j < pol.max_batch ? out.prev_slots[j] : 0u;
-    if (j < n_prev) {
-      CandRec r;
-      load_rec(ct, sl, &r);
-      out.prev_rec[j] = r;
-      // region B: live calls of q* that region A (q* rows with slot <= boundary) does not hold
-      bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == qs && (bnd == NONE || r.slot > bnd);
-      out.ckey[na + j] = b ? cand_key(r, t) : ~0ull;
-      out.ckvb[na + j] = blocks_for(pol, r.tok + r.exec + 1);  // R14
-    }
-    return;
-  }
-  // every load of this phase in one round, before the early exit of tiles without candidates
-  const uint32_t off = out.tile_off[tile];
-  const uint32_t cnt = out.tile_off[tile + 1] - off;
-  const uint32_t qs = ctl->qstar, m = ctl->mprime, pre_tile = out.tile_pre[tile];
-  const uint32_t row0 = tile * TILE + threadIdx.x * ROWS_PER_THREAD;
-  uint2 qv = row0 < n_rows ? *reinterpret_cast<const uint2*>(ct.qf + row0) : make_uint2(0x40404040u, 0x40404040u);
-  if (cnt == 0) return;
-  __shared__ uint32_t red[33];
-  uint32_t qfs[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
-  uint32_t nq = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) nq += (!(qfs[j] & QF_DEAD) && (qfs[j] & QF_QMASK) == qs) ? 1u : 0u;
-  uint32_t rq = pre_tile + block_excl_scan<uint32_t, SCAN_THREADS>(nq, red, nullptr);
-  uint32_t flags = 0, nsel = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint32_t qf = qfs[j];
-    if (qf & QF_DEAD) continue;
-    uint32_t q = qf & QF_QMASK;
-    bool sel = q < qs;
-    if (q == qs) { sel = rq < m; ++rq; }
-    if (sel) { flags |= 1u << j; ++nsel; }
-  }
-  uint32_t pos = off + block_excl_scan<uint32_t, SCAN_THREADS>(nsel, red, nullptr);
-  if (flags) {
-    // the thread's 8 consecutive rows: all fields with independent vector loads (one DRAM round
-    // trip), then one record + key per selected row
-    const uint4* cidv = reinterpret_cast<const uint4*>(ct.cid + row0);
-    uint4 c4[4];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) c4[v] = cidv[v];
-    uint4 ar[2], tk[2], ex[2], mt[2], qt[2], bd[2];
-#pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      ar[v] = reinterpret_cast<const uint4*>(ct.arr + row0)[v];
-      tk[v] = reinterpret_cast<const uint4*>(ct.tok + row0)[v];
-      ex[v] = reinterpret_cast<const uint4*>(ct.exec + row0)[v];
-      mt[v] = reinterpret_cast<const uint4*>(ct.mtime + row0)[v];
-      qt[v] = reinterpret_cast<const uint4*>(ct.quanta + row0)[v];
-      bd[v] = reinterpret_cast<const uint4*>(ct.bidx + row0)[v];
-    }
-    auto lane4 = [](const uint4& a, int k) { return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : a.w; };
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (flags & (1u << j)) {
-        CandRec r;
-        const uint4& cc = c4[j >> 1];
-        r.cid = (j & 1) ? ((uint64_t)cc.w << 32 | cc.z) : ((uint64_t)cc.y << 32 | cc.x);
-        r.slot = row0 + j;
-        r.arr = lane4(ar[j >> 2], j & 3);
-        r.tok = lane4(tk[j >> 2], j & 3);
-        r.exec = lane4(ex[j >> 2], j & 3);
-        r.mtime = lane4(mt[j >> 2], j & 3);
-        r.quanta = lane4(qt[j >> 2], j & 3);
-        r.qf = qfs[j];
-        r._pad = (qfs[j] & QF_RUN) ? lane4(bd[j >> 2], j & 3) : NONE;  // previous-batch index
-        out.cand[pos] = row0 + j;
-        out.cand_rec[pos] = r;
-        out.ckey[pos] = cand_key(r, t);
-        out.ckvb[pos] = blocks_for(pol, r.tok + r.exec + 1);  // R14
-        ++pos;
-      }
-  }
-}
-
-__global__ void __launch_bounds__(SCAN_THREADS) k_gather(Policy pol, CallTable ct, Ctl* ctl, Outputs out,
-                                                         uint32_t n_rows, uint32_t ntiles, uint32_t t) {
-  pdl_wait();
-  pdl_trigger();
-  CHAIN_BEGIN(3);
-  gather_body(pol, ct, ctl, out, n_rows, ntiles, t);
-  CHAIN_END(3);
-}
-
-// Self-selecting gather (default): no separate selection kernel.  Every CTA derives q* and m'
-// from the per-queue totals, and a tile CTA its candidate offset from the counts of the earlier
-// tiles, both from a two-level table the scan fills: per-tile counts (tile_cnt) and per-super-tile
-// counts (sup_cnt, SUP_TILES tiles each, accumulated with atomics).  The prefix of tile T is the
-// super-tiles before T's plus the <= SUP_TILES - 1 tiles of T's super-tile before T: one round of
-// a few loads per thread (half-warp h, lane k = queue k).
-//     off(T) = pre_a(T) + min(pre_q(T), m'),   pre_a = sum_{T'<T} sum_{k<q*} cnt,  pre_q = sum_{T'<T} cnt_q*.
-// Inside the tile, a thread's first candidate position follows from the exclusive counts of
-// earlier threads (A = live rows with q < q*, Q = live rows of q*) without a second scan, since
-// the q* rows are taken in table order:  pos = off + A + min(Q, m' - min(pre_q, m')).
-// The thread taking the m'-th q* row publishes its slot (region A's boundary); the previous-batch
-// CTAs emit keys for every live q* call of the previous batch and k_rank drops those with
-// slot <= boundary (they are in region A).
-__device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, uint32_t n_rows, uint32_t ntiles, uint32_t t) {
-  constexpr int NT = SCAN_THREADS, NW = NT / 32, NH = NT / MAX_K;  // NH half-warps of MAX_K lanes
-  __shared__ uint32_t s_tot[NH][MAX_K], s_pre[NH][MAX_K];
-  __shared__ uint32_t s_qs, s_m, s_prea, s_preq, s_has;
-  __shared__ uint32_t s_own[MAX_K];
-  __shared__ uint32_t s_cnt[NW];
-  const uint32_t tid = threadIdx.x, tile = blockIdx.x;
-  const uint32_t K = pol.K, BS = pol.max_batch;
-  const bool is_tile = tile < ntiles;
-  // (1) one round of independent loads: this tile's queue bytes first (they do not depend on the
-  // selection), then the counts
-  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
-  const uint2 qv = is_tile && row0 < n_rows ? *reinterpret_cast<const uint2*>(ct.qf + row0)
-                                            : make_uint2(0x40404040u, 0x40404040u);
-  {
-    const uint32_t h = tid / MAX_K, k = tid % MAX_K;
-    const uint32_t nsup = (ntiles + SUP_TILES - 1) / SUP_TILES, my_sup = tile / SUP_TILES;
-    uint32_t tot = 0, pre = 0;
-    if (k < K) {
-      // all loads issued before any is consumed (a rolled loop would chain one L2 round trip per
-      // iteration): the tile count, then up to 8 super-tile rows per half-warp (4.2M rows)
-      const uint32_t tr = my_sup * SUP_TILES + h;  // earlier tile of the same super-tile, or this one
-      const bool has_tr = is_tile && tr <= tile;
-      const uint32_t c = has_tr ? __ldcg(out.tile_cnt + (size_t)tr * MAX_K + k) : 0u;
-      constexpr int SU = 8;
-      uint32_t v[SU];
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        const uint32_t S = h + u * NH;
-        v[u] = S < nsup ? __ldcg(out.sup_cnt + S * MAX_K + k) : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < SU; ++u) {
-        const uint32_t S = h + u * NH;
-        tot += v[u];
-        pre += (is_tile && S < my_sup) ? v[u] : 0u;
-      }
-      for (uint32_t S = h + SU * NH; S < nsup; S += NH) {  // larger tables
-        const uint32_t w = __ldcg(out.sup_cnt + S * MAX_K + k);
-        tot += w;
-        pre += (is_tile && S < my_sup) ? w : 0u;
-      }
-      if (has_tr) {
-        if (tr < tile) pre += c;
-        else s_own[k] = c;
-      }
-    }
-    s_tot[h][k] = tot;
-    s_pre[h][k] = pre;
-    if (tile == 0 && tid < 32) {
-      // promotions (even lanes) and live rows (odd lanes) for finalize's host record
-      uint32_t stat = tid < 2 * QP_LINES ? __ldcg(&ctl->qpart[tid >> 1][MAX_K + (tid & 1)]) : 0u;
-#pragma unroll
-      for (int d = 2; d < 32; d <<= 1) stat += __shfl_xor_sync(0xffffffffu, stat, d);
-      if (tid == 0) ctl->n_promoted = stat;
-      if (tid == 1) ctl->n_live = stat;
-    }
-  }
-  if (!is_tile) {
-    // previous batch: records (for preempt) and region-B keys
-    const uint32_t j = (tile - ntiles) * NT + tid;
-    const uint32_t n_prev = ctl->n_prev;
-    CandRec r;
-    if (j < n_prev) load_rec(ct, out.prev_slots[j], &r);
-    __syncthreads();
-    if (tid < 32) {
-      uint32_t tq = 0;
-      if (tid < MAX_K) {
-#pragma unroll
-        for (int h = 0; h < NH; ++h) tq += s_tot[h][tid];
-      }
-      const uint32_t incl = warp_incl_scan(tq);
-      const uint32_t b = __ballot_sync(0xffffffffu, tid < K && incl >= BS);
-      const uint32_t qs = b ? __ffs(b) - 1 : K;
-      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-      if (tid == 0) { s_qs = qs; s_m = qs < K ? BS : tot; }  // s_m: n_cand_a here
-    }
-    __syncthreads();
-    if (j < n_prev) {
-      out.prev_rec[j] = r;
-      const bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == s_qs;
-      out.ckey[s_m + j] = b ? cand_key(r, t) : ~0ull;
-      out.ckvb[s_m + j] = blocks_for(pol, r.tok + r.exec + 1);  // R14
-    }
-    return;
-  }
-  __syncthreads();
-  // (2) q*, m', and this tile's prefix (warp 0, lane k = queue k)
   if (tid < 32) {
-    uint32_t tq = 0, pk = 0;
+    uint32_t T = 0, P = 0, O = 0;
     if (tid < MAX_K) {
-#pragma unroll
-      for (int h = 0; h < NH; ++h) { tq += s_tot[h][tid]; pk += s_pre[h][tid]; }
+#pragma unroll 8
+      for (int g = 0; g < NG; ++g) { T += S.tot[g][tid]; P += S.pre[g][tid]; }
+      O = is_tile ? S.ownk[tid] : 0u;
     }
-    const uint32_t incl = warp_incl_scan(tq);
+    const uint32_t incl = warp_incl_scan(T);
     const uint32_t b = __ballot_sync(0xffffffffu, tid < K && incl >= BS);
     const uint32_t qs = b ? __ffs(b) - 1 : K;
-    const uint32_t excl = __shfl_sync(0xffffffffu, incl - tq, qs & 31);
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t pa = warp_sum(tid < qs ? pk : 0u);
-    const uint32_t pq = __shfl_sync(0xffffffffu, pk, qs & 31);
-    // this tile's own live rows below q* and of q*: no candidate unless one of them is taken
-    const uint32_t own = tid < K ? s_own[tid] : 0u;
-    const uint32_t oa = warp_sum(tid < qs ? own : 0u);
-    const uint32_t oq = __shfl_sync(0xffffffffu, own, qs & 31);
+    const uint32_t base = incl - T;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t bq = __shfl_sync(0xffffffffu, base, qs & 31);
+    const uint32_t m = qs < K ? BS - bq : 0u;
+    const bool has = __ballot_sync(0xffffffffu, tid < K && O > 0 && (tid < qs || (tid == qs && P < m))) != 0;
+    if (tid < MAX_K) {
+      S.base[tid] = base;
+      S.prek[tid] = P;
+    }
     if (tid == 0) {
-      const uint32_t m = qs < K ? BS - excl : 0;
-      s_qs = qs;
-      s_m = m;
-      s_prea = pa;
-      s_preq = qs < K ? pq : 0;
-      s_has = oa > 0 || (qs < K && oq > 0 && pq < m);
-      if (tile == 0) {
-        ctl->qstar = qs;
-        ctl->mprime = m;
-        ctl->n_cand_a = qs < K ? BS : tot;
-      }
+      S.qs = qs;
+      S.m = m;
+      S.nx = qs < K ? BS : total;
+      S.has = has ? 1u : 0u;
     }
   }
   __syncthreads();
-  // tiles without candidates leave now (their SM slots go to the next kernel's CTAs); the
-  // boundary row is always in a tile with candidates
-  if (STAMPS_ON && tile == 0 && tid == 0) ctl->dbg[57] = globaltimer();
-  if (!s_has) return;
-  const uint32_t qs = s_qs, m = s_m;
-  uint32_t qfs[8], na = 0, nq = 0;
+}
+
+// Region A rows of one tile -> out.xrec at their (queue, seq) positions; the tile holding the
+// m'-th row of q* publishes it (region A's boundary).  Ranks inside the tile: one block scan per
+// word of 4 queues (16-bit fields), over the queues <= q*.
+__device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&qw)[2], const SelSmem& S,
+                             unsigned long long* red64) {
+  const uint32_t tid = threadIdx.x, K = a.pol.K;
+  const uint32_t qs = S.qs, m = S.m;
+  const uint32_t qmax = min(qs, K - 1);
+  const uint32_t nw = (qmax >> 2) + 1;
+  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  uint32_t pos2[4];  // positions of rows 2k, 2k+1 in 16-bit halves (BS <= 2048)
+  uint32_t sel = 0, bnd = 0;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
-    const bool live = !(qfs[j] & QF_DEAD);
-    const uint32_t q = qfs[j] & QF_QMASK;
-    na += (live && q < qs) ? 1u : 0u;
-    nq += (live && q == qs) ? 1u : 0u;
-  }
-  // (3) exclusive (A, Q) counts of the earlier threads of this tile
-  const uint32_t v = (na << 16) | nq;  // <= 2048 each
-  const uint32_t vin = warp_incl_scan(v);
-  if (lane_id() == 31) s_cnt[warp_id()] = vin;
-  __syncthreads();
-  uint32_t vex = vin - v;
+  for (int k = 0; k < 4; ++k) pos2[k] = 0;
+  for (uint32_t w = 0; w < nw; ++w) {
+    uint64_t c = 0;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) vex += (uint32_t)w < warp_id() ? s_cnt[w] : 0u;
-  const uint32_t pre_a = s_prea, pre_q = s_preq;
-  const uint32_t mq = m - min(pre_q, m);  // q* rows still to take at this tile's start
-  uint32_t rq = pre_q + (vex & 0xffffu);
-  uint32_t pos = pre_a + min(pre_q, m) + (vex >> 16) + min(vex & 0xffffu, mq);
-  uint32_t flags = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t qf = qfs[j];
-    if (qf & QF_DEAD) continue;
-    const uint32_t q = qf & QF_QMASK;
-    bool sel = q < qs;
-    if (q == qs) {
-      sel = rq < m;
-      if (rq + 1 == m) ctl->qs_bnd1 = row0 + j + 1;
-      ++rq;
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t qf = qf_at(qw, j), q = qf & QF_QMASK;
+      if (!(qf & QF_DEAD) && q <= qmax && (q >> 2) == w) c += 1ull << (16 * (q & 3));
     }
-    if (sel) flags |= 1u << j;
-  }
-  if (STAMPS_ON && tile == 0 && tid == 0) ctl->dbg[58] = globaltimer();
-  if (flags) {
-    const uint4* cidv = reinterpret_cast<const uint4*>(ct.cid + row0);
-    uint4 c4[4];
+    uint64_t ex = block_excl_scan<unsigned long long, ST_THREADS>(c, red64, nullptr);
 #pragma unroll
-    for (int w = 0; w < 4; ++w) c4[w] = cidv[w];
-    uint4 ar[2], tk[2], ex[2], mt[2], qt[2], bd[2];
-#pragma unroll
-    for (int w = 0; w < 2; ++w) {
-      ar[w] = reinterpret_cast<const uint4*>(ct.arr + row0)[w];
-      tk[w] = reinterpret_cast<const uint4*>(ct.tok + row0)[w];
-      ex[w] = reinterpret_cast<const uint4*>(ct.exec + row0)[w];
-      mt[w] = reinterpret_cast<const uint4*>(ct.mtime + row0)[w];
-      qt[w] = reinterpret_cast<const uint4*>(ct.quanta + row0)[w];
-      bd[w] = reinterpret_cast<const uint4*>(ct.bidx + row0)[w];
-    }
-    auto lane4 = [](const uint4& a, int k) { return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : a.w; };
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (flags & (1u << j)) {
-        CandRec r;
-        const uint4& cc = c4[j >> 1];
-        r.cid = (j & 1) ? ((uint64_t)cc.w << 32 | cc.z) : ((uint64_t)cc.y << 32 | cc.x);
-        r.slot = row0 + j;
-        r.arr = lane4(ar[j >> 2], j & 3);
-        r.tok = lane4(tk[j >> 2], j & 3);
-        r.exec = lane4(ex[j >> 2], j & 3);
-        r.mtime = lane4(mt[j >> 2], j & 3);
-        r.quanta = lane4(qt[j >> 2], j & 3);
-        r.qf = qfs[j];
-        r._pad = (qfs[j] & QF_RUN) ? lane4(bd[j >> 2], j & 3) : NONE;  // previous-batch index
-        out.cand[pos] = row0 + j;
-        out.cand_rec[pos] = r;
-        out.ckey[pos] = cand_key(r, t);
-        out.ckvb[pos] = blocks_for(pol, r.tok + r.exec + 1);  // R14
-        ++pos;
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t qf = qf_at(qw, j), q = qf & QF_QMASK;
+      if (!(qf & QF_DEAD) && q <= qmax && (q >> 2) == w) {
+        const uint32_t sh = 16 * (q & 3);
+        const uint32_t rank = S.prek[q] + (uint32_t)((ex >> sh) & 0xFFFFu);
+        ex += 1ull << sh;
+        if (q < qs || rank < m) {
+          sel |= 1u << j;
+          pos2[j >> 1] |= (S.base[q] + rank) << (16 * (j & 1));
+          if (q == qs && rank + 1 == m) bnd = 1u << j;
+        }
       }
+    }
   }
-  if (STAMPS_ON && tile == 0) {
-    __syncwarp();
-    if (tid == 0) ctl->dbg[59] = globaltimer();
+  if (!sel) return;
+  const CallTable& ct = a.ct;
+  CandRec* xrec = a.out.xrec;
+  // the thread's 8 rows: each field with vector loads, 4 rows at a time
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    if (!((sel >> (4 * half)) & 0xFu)) continue;
+    const uint32_t r4 = row0 + 4 * half;
+    const uint4 c0 = reinterpret_cast<const uint4*>(ct.cid + r4)[0];
+    const uint4 c1 = reinterpret_cast<const uint4*>(ct.cid + r4)[1];
+    const uint4 ar = *reinterpret_cast<const uint4*>(ct.arr + r4);
+    const uint4 tk = *reinterpret_cast<const uint4*>(ct.tok + r4);
+    const uint4 ex = *reinterpret_cast<const uint4*>(ct.exec + r4);
+    const uint4 mt = __ldcg(reinterpret_cast<const uint4*>(ct.mtime + r4));   // (promotions of this kernel)
+    const uint4 qt = __ldcg(reinterpret_cast<const uint4*>(ct.quanta + r4));
+    const uint4 bd = *reinterpret_cast<const uint4*>(ct.bidx + r4);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = 4 * half + k;
+      if (!((sel >> j) & 1u)) continue;
+      const uint4& cc = k < 2 ? c0 : c1;
+      const uint32_t qf = qf_at(qw, j);
+      const uint32_t arr = lane4(ar, k);
+      const uint32_t pos = (pos2[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+      uint4* dst = reinterpret_cast<uint4*>(xrec + pos);
+      dst[0] = make_uint4(k & 1 ? cc.z : cc.x, k & 1 ? cc.w : cc.y, r4 + k, arr);
+      dst[1] = make_uint4(lane4(tk, k), lane4(ex, k), lane4(mt, k), lane4(qt, k));
+      dst[2] = make_uint4(qf | ((qf & QF_RUN) ? lane4(bd, k) << 8 : 0u), 0u, 0u, 0u);
+      if ((bnd >> j) & 1u) {
+        a.ctl->bnd_slot = r4 + k;
+        a.ctl->bnd_arr = arr;
+      }
+    }
   }
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS, 4) k_gather_ss(Policy pol, CallTable ct, Ctl* ctl, Outputs out,
-                                                               uint32_t n_rows, uint32_t ntiles, uint32_t t,
-                                                               ProgTable pt, FusedCommit fc) {
-  pdl_wait();
-  pdl_trigger();
-  if (fc.on && blockIdx.x == gridDim.x - 1) {  // the fused prologue's table writes (k_scan_fused)
-    commit_prologue(pol, ct, pt, t, fc.n_comp, fc.n_arr, fc.rec, fc.cslots, fc.arr);
-    return;
-  }
-  CHAIN_BEGIN(3);
-  gather_ss_body(pol, ct, ctl, out, n_rows, ntiles, t);
-  CHAIN_END(3);
-}
-
 // ---------------------------------------------------------------------------------------------
-// a5/a6/a3/a7-plan: one CTA.  Sort <= 2 BS candidate keys
-//     q:4 | arrival (relative to t):27 | not-running:1 | seq (row):31       (R11, R12)
-// (region A from the gather, plus the previous batch's calls of q*, de-duplicated), cut the
-// longest prefix with count <= BS and sum kvb <= P (Alg. 1 l.32-39, first misfit stops, R13),
-// emit batch/admit/preempt, account (batch: exec++, mtime++, quanta--, running; everyone else
-// waits implicitly via the closed-form counters), demote batch calls whose quantum is exhausted
-// (Alg. 1 l.20-23), allocate KV blocks and build the swap plan.
+// a5 order + a6 cutoff + a3 demotion + a7 plan: one CTA of ST_THREADS, I candidates per thread
+// (C = ST_THREADS * I >= 2 BS).  Y = region A ++ region B (sorted by seq) is in (queue, arrival,
+// seq) order, so the key order (queue, arrival, not-running, seq) (R11, R12) is a stable
+// partition of Y inside each (queue, arrival) group with the running calls first.  The batch is
+// the longest prefix of that order with count <= BS and sum kvb <= P (Alg. 1 l.32-39, first
+// misfit stops, R13); admit = batch calls not resident, preempt = resident calls not in the
+// batch; batch calls are accounted (exec++, mtime++, quanta--; waiting calls implicitly through
+// the closed-form counters) and demoted when their quantum runs out (Alg. 1 l.20-23).
 // ---------------------------------------------------------------------------------------------
-extern __shared__ unsigned char fin_smem[];
-template <int NT, int R, bool LISTS = false>
-__device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
-                              uint32_t t, uint32_t np, uint32_t seqno);
-
 __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
-// k_rank: the candidates' sort.  A single SM needs ~35k cycles to sort 2048 64-bit keys with
-// any block sort (measured: scripts/micro/sort_bench.cu), so the order is computed across many
-// SMs instead: every CTA holds all n <= 2 BS keys in shared memory and each key's output index is
-// the number of keys before it (the keys are unique), RANK_SUB threads per key.
-constexpr int RANK_THREADS = 256, RANK_SUB = 16, RANK_PER_CTA = RANK_THREADS / RANK_SUB;
-template <bool FUSED>
-__global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
-                                                       bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
-  pdl_wait();
-  pdl_trigger();
-  CHAIN_BEGIN(4);
-  __shared__ uint32_t red_r[33];
-  const uint32_t na = ctl->n_cand_a;
-  const uint32_t n = na + ctl->n_prev;
-  uint64_t* rk = reinterpret_cast<uint64_t*>(fin_smem);  // [n] keys, ~0 = no candidate
-  uint64_t* ck = rk + n;                                 // [n_valid] the candidates' keys
-  uint32_t* ci = reinterpret_cast<uint32_t*>(ck + n);    // [n_valid] their element index
-  uint32_t* rkv = ci + n;                                // [n] kvb of each element
-  uint32_t* ckv = rkv + n;                               // [n_valid] the candidates' kvb
-  const bool lists = out.rank_lists != 0;
-  const uint32_t e0 = blockIdx.x * RANK_PER_CTA;
-  const uint32_t bnd1 = ctl->qs_bnd1;
-  // (1) keys into shared memory; previous-batch keys at or before region A's boundary are region
-  // A's already (self-selecting gather; bnd1 = 0 otherwise) and become sentinels.  The key loads
-  // cover the buffer's capacity, so they need not wait for the counts above (one round trip).
-  constexpr int RK = 8;
-  const uint32_t cap = 2 * pol.max_batch;
-  uint32_t nv = 0;
-  for (uint32_t c0 = 0; c0 < cap; c0 += RK * RANK_THREADS) {
-    uint64_t kk[RK];
-    uint32_t kb[RK];
+// exclusive max-scan over the block in thread order (0 for thread 0); smem: >= 33 words
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* smem) {
+  constexpr int NW = NT / 32;
+  uint32_t x = v;
 #pragma unroll
-    for (int r = 0; r < RK; ++r) {
-      const uint32_t i = c0 + r * RANK_THREADS + threadIdx.x;
-      kk[r] = i < cap ? __ldcg(out.ckey + i) : ~0ull;
-      kb[r] = lists && i < cap ? __ldcg(out.ckvb + i) : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < RK; ++r) {
-      const uint32_t i = c0 + r * RANK_THREADS + threadIdx.x;
-      if (i < n) {
-        uint64_t k = kk[r];
-        if (i >= na && (uint32_t)(k & 0x7FFFFFFFu) < bnd1) k = ~0ull;
-        nv += k != ~0ull ? 1u : 0u;
-        rk[i] = k;
-        rkv[i] = kb[r];
-      }
-    }
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane_id() >= (uint32_t)d) x = max(x, y);
   }
-  if (blockIdx.x * (RANK_PER_CTA / 2) < n) {
-    // (2) compact the candidates (same deterministic order in every CTA): sentinels rank last and
-    // nobody reads them, so only the n_valid candidates are ranked and compared against
-    if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[54] = globaltimer();
-    uint32_t n_valid;
-    uint32_t off = block_excl_scan<uint32_t, RANK_THREADS>(nv, red_r, &n_valid);
-    for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS)
-      if (rk[i] != ~0ull) { ck[off] = rk[i]; ci[off] = i; ckv[off] = rkv[i]; ++off; }
-    __syncthreads();
-    if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[55] = globaltimer();
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      ctl->n_cand_b = n_valid - na;
-      if (STAMPS_ON) {
-        ctl->dbg[52] = n_valid;
-        ctl->dbg[53] = n;
-      }
-    }
-    // (3) rank = number of smaller keys (keys are unique), RANK_SUB threads per key; the record
-    // load is issued before the count so that its latency hides behind it
-    // when the candidates fill at most half the grid's capacity, a full warp per key (8 keys per
-    // CTA) keeps every CTA busy and halves each thread's compares; else half a warp per key
-    const bool wide = 2 * n_valid <= gridDim.x * RANK_PER_CTA && !FUSED && out.rank_wide;
-    const uint32_t subn = wide ? 32u : (uint32_t)RANK_SUB;
-    const uint32_t e = (wide ? blockIdx.x * (RANK_PER_CTA / 2) : e0) + threadIdx.x / subn, sub = threadIdx.x % subn;
-    uint32_t cnt = 0, eo = 0, kvs = 0, nad = 0;
-    uint64_t x = 0;
-    CandRec rec;
-    if (e < n_valid) {
-      x = ck[e];
-      eo = ci[e];
-      if (sub == 0) rec = eo < na ? out.cand_rec[eo] : out.prev_rec[eo - na];
-      if (lists) {
-        // with the rank, the kvb prefix (Alg. 1 l.34-37) and the admit rank (smaller keys of
-        // calls that did not run: not resident under eager eviction)
-#pragma unroll 4
-        for (uint32_t j = sub; j < n_valid; j += subn) {  // (4 independent smem chains in flight)
-          const uint64_t y = ck[j];
-          const bool lt = y < x;
-          cnt += lt ? 1u : 0u;
-          kvs += lt ? ckv[j] : 0u;
-          nad += (lt && ((y >> 31) & 1u)) ? 1u : 0u;
-        }
-      } else {
-#pragma unroll 4
-        for (uint32_t j = sub; j < n_valid; j += subn) cnt += ck[j] < x ? 1u : 0u;
-      }
-    }
+  uint32_t ex = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane_id() == 0) ex = 0;
+  if (lane_id() == 31) smem[warp_id()] = x;
+  __syncthreads();
+  if (warp_id() == 0) {
+    uint32_t w = lane_id() < NW ? smem[lane_id()] : 0u;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      if ((uint32_t)d >= subn) break;
-      cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-      if (lists) {
-        kvs += __shfl_xor_sync(0xffffffffu, kvs, d);
-        nad += __shfl_xor_sync(0xffffffffu, nad, d);
-      }
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane_id() >= (uint32_t)d) w = max(w, y);
     }
-    if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[56] = globaltimer();
-    if (sub == 0 && e < n_valid) {
-      out.skey[cnt] = x;
-      out.sidx[cnt] = eo;
-      out.srec[cnt] = rec;
-      // a running call (previous-batch entry rec._pad) publishes its sorted position: finalize
-      // tests the previous batch's membership in the new one without searching
-      if (rec.qf & QF_RUN) out.prev_pos[rec._pad] = (unsigned long long)seqno << 32 | cnt;
-      if (lists) {
-        // Alg. 1 l.32-39 for this key alone: kvb >= 1 makes the inclusive prefix strictly
-        // increasing, so "count <= BS and sum kvb <= P" holds exactly on a prefix of the order
-        // (the first misfit stops, R13); the batch entries write their lists and accounting
-        const uint32_t incl = kvs + ckv[e];
-        const uint32_t BS = pol.max_batch;
-        if (cnt < BS && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) {
-          const uint32_t sl = rec.slot;
-          out.batch_slots[cnt] = sl;
-          out.batch_ids[cnt] = rec.cid;
-          if (out.zero_copy) { out.h_batch[cnt] = rec.cid; out.h_batch_slots[cnt] = sl; }
-          // step accounting + eager demotion (Alg. 1 l.20-23)
-          uint32_t q = rec.qf & QF_QMASK, qt = rec.quanta;
-          ct.exec[sl] = rec.exec + 1;
-          ct.mtime[sl] = rec.mtime + 1;
-          if (qt != AUTX_INF) {
-            qt -= 1;
-            if (qt == 0) {
-              q = min(q + 1, pol.K - 1);
-              qt = pol.quanta[q];
-            }
-            ct.quanta[sl] = qt;
-          }
-          ct.qf[sl] = (uint8_t)(q | QF_RUN | QF_RES);
-          ct.bidx[sl] = cnt;
-          out.prev_slots[cnt] = sl;
-          if ((x >> 31) & 1u) {  // admit: did not run in the previous step (not resident)
-            out.admit_ids[nad] = rec.cid;
-            out.admit_slots[nad] = sl;
-            if (out.zero_copy) out.h_admit[nad] = rec.cid;
-            const uint32_t held = rec.exec > 0 ? blocks_for(pol, rec.tok + rec.exec) : 0u;  // R28
-            if (held) atomicAdd(&ctl->acc_swap_in, (unsigned long long)held);
-            atomicMax(&ctl->acc_nadmit, nad + 1);
-          }
-          atomicMax(&ctl->acc_nbatch, cnt + 1);
-          atomicMax(&ctl->acc_kv, (unsigned long long)incl);
-        }
-      }
-    }
+    uint32_t we = __shfl_up_sync(0xffffffffu, w, 1);
+    if (lane_id() == 0) we = 0;
+    if (lane_id() < NW) smem[lane_id()] = we;
   }
-  CHAIN_END(4);
-  if (!FUSED) return;
-  // the last CTA to finish runs finalize on the sorted keys (saves a dependent launch)
-  __shared__ bool last;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&ctl->rank_done, 1u) == gridDim.x - 1;
+  const uint32_t r = max(smem[warp_id()], ex);
   __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (threadIdx.x == 0) ctl->rank_done = 0;
-  if (out.rank_lists) finalize_body<RANK_THREADS, 4, true>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
-  else finalize_body<RANK_THREADS, 4, false>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  return r;
 }
 
-template <int NT, int R, bool LISTS>
-__device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
-                              uint32_t t, uint32_t np, uint32_t seqno) {
-  uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] sorted keys of the first m candidates
-  // admit / preempt id lists staged in shared memory for the host mirrors (16-B aligned)
-  uint64_t* s_ad = uk + np;
-  uint64_t* s_pr = s_ad + ((pol.max_batch + 1) & ~1u);
-  __shared__ unsigned long long red64[33];
-  __shared__ uint32_t red[33];
+template <int I>
+constexpr size_t fin_smem_bytes() {
+  return (size_t)ST_THREADS * I * 48 + (size_t)ST_THREADS * I / 2;
+}
+
+template <int I>
+__device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs, uint32_t nx, uint32_t n_live,
+                              uint32_t n_promo, const uint32_t (&p_slot)[I / 2], uint32_t n_prev, bool wait2,
+                              unsigned long long* red64, uint32_t* red32) {
+  constexpr int NT = ST_THREADS, IP = I / 2, C = NT * I;
+  const Policy& pol = a.pol;
+  const CallTable& ct = a.ct;
+  const Outputs& out = a.out;
+  const KvState& kv = a.kv;
+  Ctl* ctl = a.ctl;
+  uint64_t* y_cid = reinterpret_cast<uint64_t*>(dsm);
+  uint32_t* y_slot = reinterpret_cast<uint32_t*>(dsm + 8 * (size_t)C);
+  uint32_t* y_arr = y_slot + C;
+  uint32_t* y_tok = y_arr + C;
+  uint32_t* y_exec = y_tok + C;
+  uint32_t* y_mt = y_exec + C;
+  uint32_t* y_qt = y_mt + C;
+  uint32_t* y_qfb = y_qt + C;
+  uint32_t* z = y_qfb + C;    // sorted position -> index in Y
+  uint32_t* hb = z + C;       // running calls before each group head; region B's slots first
+  uint32_t* grun = hb + C;    // running calls per group (at the head's index)
+  uint8_t* inb = reinterpret_cast<uint8_t*>(grun + C);  // previous-batch entry is in the new batch
+  uint64_t* s_ad = reinterpret_cast<uint64_t*>(hb);     // admit / preempt ids for the host mirrors
+  uint64_t* s_pr = reinterpret_cast<uint64_t*>(grun);   // (hb, grun are free once z is known)
   __shared__ uint32_t s_nbatch;
   __shared__ unsigned long long s_kvsum;
   __shared__ HostOut s_hout;
-  const uint32_t tid = threadIdx.x;
-  const uint32_t BS = pol.max_batch;
-  const uint32_t n_prev = ctl->n_prev;
-  // region A + region B (previous-batch calls of q* not in A): no duplicates, ~0 sentinels last
-  const uint32_t ncand = ctl->n_cand_a + ctl->n_cand_b;
-  // host-record fields, loaded with everything else in the first round
-  uint32_t c_live = 0, c_promo = 0, c_err = 0, c_einfo = 0;
-  // rank_lists: k_rank has written the batch and admit lists and the accounting; its totals
-  constexpr bool lists = LISTS;
-  uint32_t a_nb = 0, a_na = 0;
-  unsigned long long a_kv = 0, a_si = 0;
-  if (tid == 0) {
-    c_live = ctl->n_live; c_promo = ctl->n_promoted; c_err = ctl->err; c_einfo = ctl->err_info;
-    if (lists) { a_nb = ctl->acc_nbatch; a_na = ctl->acc_nadmit; a_kv = ctl->acc_kv; a_si = ctl->acc_swap_in; }
-  }
-  STAMP(0);
-  if (tid == 0) s_nbatch = 0;
-  // ---- (1) the first m = min(BS, ncand) candidates in key order: key + record, plus the
-  // previous batch's records (preempt), all in one round of independent loads --------------
-  const uint32_t m = lists ? 0u : min(BS, ncand);
-  // R items per thread, blocked (i = tid * R + r): NT * R >= BS
-  uint32_t c_s[R], c_qf[R], c_tok[R], c_ex[R], c_mt[R], c_qt[R], c_kvb[R];
-  uint64_t c_cid[R];
-  uint32_t p_s[R], p_qf[R], p_held[R];  // previous batch: slot, flags, held blocks, order key
-  uint64_t p_cid[R], p_key[R];
-  unsigned long long p_pos[R];           // seqno << 32 | sorted position (k_rank), if use_prev_pos
-  unsigned long long my_kv = 0;
-  {
-    // all loads of this phase first, through restrict-qualified locals, so that they overlap
-    // (one L2 round trip instead of a chain of them)
-    const uint64_t* __restrict__ skey = out.skey;
-    const CandRec* __restrict__ srec = out.srec;
-    const CandRec* __restrict__ prec = out.prev_rec;
-    const unsigned long long* __restrict__ ppos = out.prev_pos;
-    uint64_t kk[R];
-    CandRec rc[R], pr[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      // unconditional below BS (buffers hold >= BS entries): the loads do not wait for the counts
-      const uint32_t i = tid * R + r;
-      if (i < BS) {
-        if (!lists) { kk[r] = skey[i]; rc[r] = srec[i]; }
-        pr[r] = prec[i];
-        p_pos[r] = ppos[i];
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const uint32_t i = tid * R + r;
-      if (i < m) {
-        uk[i] = kk[r];
-        c_s[r] = rc[r].slot;
-        c_qf[r] = rc[r].qf;
-        c_tok[r] = rc[r].tok;
-        c_ex[r] = rc[r].exec;
-        c_mt[r] = rc[r].mtime;
-        c_qt[r] = rc[r].quanta;
-        c_cid[r] = rc[r].cid;
-      }
-      if (i < n_prev) {
-        p_s[r] = pr[r].slot;
-        p_qf[r] = pr[r].qf;
-        p_cid[r] = pr[r].cid;
-        p_key[r] = cand_key(pr[r], t);
-        p_held[r] = blocks_for(pol, pr[r].tok + pr[r].exec);  // R28
-      }
-    }
+  const uint32_t tid = threadIdx.x, BS = pol.max_batch, K = pol.K;
+  const bool stamps = STAMPS_ON(pol);
+  if (wait2) grid_wait(&ctl->bar2, a.n_tile_ctas);
+  if (stamps && tid == 0) ctl->dbg[44] = globaltimer();
+  // ---- (1) one round of loads: region A records, the previous batch's rows, the boundary -----
+  uint32_t bnd_slot = 0, bnd_arr = 0;
+  if (qs < K) {
+    bnd_slot = __ldcg(&ctl->bnd_slot);
+    bnd_arr = __ldcg(&ctl->bnd_arr);
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    c_kvb[r] = 0;
-    if (tid * R + r < m) {
-      c_kvb[r] = blocks_for(pol, c_tok[r] + c_ex[r] + 1);  // R14
-      my_kv += c_kvb[r];
+  for (int r = 0; r < I; ++r) {
+    const uint32_t i = r * NT + tid;
+    if (i < nx) {
+      const uint4* src = reinterpret_cast<const uint4*>(out.xrec + i);
+      const uint4 x0 = __ldcg(src), x1 = __ldcg(src + 1), x2 = __ldcg(src + 2);
+      y_cid[i] = (uint64_t)x0.y << 32 | x0.x;
+      y_slot[i] = x0.z;
+      y_arr[i] = x0.w;
+      y_tok[i] = x1.x;
+      y_exec[i] = x1.y;
+      y_mt[i] = x1.z;
+      y_qt[i] = x1.w;
+      y_qfb[i] = x2.x;
+    }
+    grun[i] = 0;
+  }
+  uint32_t p_qf[IP], p_arr[IP], p_tok[IP], p_exec[IP], p_mt[IP], p_qt[IP];
+  uint64_t p_cid[IP];
+#pragma unroll
+  for (int r = 0; r < IP; ++r) {
+    const uint32_t s = p_slot[r];
+    p_qf[r] = QF_DEAD;
+    if (s != NONE) {
+      p_qf[r] = __ldcg(ct.qf + s);
+      p_arr[r] = __ldcg(ct.arr + s);
+      p_tok[r] = __ldcg(ct.tok + s);
+      p_exec[r] = __ldcg(ct.exec + s);
+      p_mt[r] = __ldcg(ct.mtime + s);
+      p_qt[r] = __ldcg(ct.quanta + s);
+      p_cid[r] = __ldcg(reinterpret_cast<const unsigned long long*>(ct.cid + s));
+    }
+    if (tid * IP + r < n_prev) inb[tid * IP + r] = 0;
+  }
+  // ---- (2) region B: running calls of q* in the boundary's arrival group, past the boundary ---
+  uint32_t isb = 0, nbm = 0;
+#pragma unroll
+  for (int r = 0; r < IP; ++r) {
+    const bool b = qs < K && p_slot[r] != NONE && !(p_qf[r] & QF_DEAD) && (p_qf[r] & QF_QMASK) == qs &&
+                   p_arr[r] == bnd_arr && p_slot[r] > bnd_slot;
+    isb |= b ? 1u << r : 0u;
+    nbm += b ? 1u : 0u;
+  }
+  uint32_t n_b;
+  uint32_t ob = block_excl_scan<uint32_t, NT>(nbm, red32, &n_b);
+#pragma unroll
+  for (int r = 0; r < IP; ++r)
+    if ((isb >> r) & 1u) hb[ob++] = p_slot[r];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < IP; ++r)
+    if ((isb >> r) & 1u) {
+      uint32_t rank = 0;
+      for (uint32_t k = 0; k < n_b; ++k) rank += hb[k] < p_slot[r] ? 1u : 0u;
+      const uint32_t i = nx + rank;
+      y_cid[i] = p_cid[r];
+      y_slot[i] = p_slot[r];
+      y_arr[i] = p_arr[r];
+      y_tok[i] = p_tok[r];
+      y_exec[i] = p_exec[r];
+      y_mt[i] = p_mt[r];
+      y_qt[i] = p_qt[r];
+      y_qfb[i] = p_qf[r] | ((tid * IP + r) << 8);
+    }
+  const uint32_t n = nx + n_b;
+  __syncthreads();
+  if (stamps && tid == 0) ctl->dbg[45] = globaltimer();
+  // ---- (3) key order: stable partition, running calls first, inside each (queue, arrival) group
+  uint32_t gs[I], rex[I], runm = 0, headm = 0, my_runs = 0, my_head = 0;
+#pragma unroll
+  for (int r = 0; r < I; ++r) {
+    const uint32_t i = tid * I + r;
+    if (i < n) {
+      const uint32_t qfb = y_qfb[i];
+      const bool head = i == 0 || ((qfb ^ y_qfb[i - 1]) & QF_QMASK) != 0 || y_arr[i] != y_arr[i - 1];
+      const bool run = (qfb & QF_RUN) != 0;
+      runm |= run ? 1u << r : 0u;
+      headm |= head ? 1u << r : 0u;
+      my_runs += run ? 1u : 0u;
+      if (head) my_head = i;
     }
   }
-  STAMP(1);
-  STAMP(2);
-  unsigned long long kv_pre = lists ? 0ull : block_excl_scan<unsigned long long, NT>(my_kv, red64, nullptr);
-  if (lists && tid == 0) s_nbatch = a_nb;
-  // Alg. 1 l.34-37: take while count <= BS and sum kvb <= P; kvb >= 1 makes the prefix sums
-  // strictly increasing, so the fitting items are exactly a prefix: n_batch = max fitting i + 1
-  unsigned long long c_incl[R];  // inclusive kvb prefix at each item
-  {
-    unsigned long long incl = kv_pre;
+  const uint32_t rbase = block_excl_scan<uint32_t, NT>(my_runs, red32, nullptr);
+  uint32_t cur_gs = block_excl_max<NT>(my_head, red32), cur_r = rbase;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      uint32_t i = tid * R + r;
-      c_incl[r] = 0;
-      if (i < m) {
-        incl += c_kvb[r];
-        c_incl[r] = incl;
-        if (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget) atomicMax(&s_nbatch, i + 1);
+  for (int r = 0; r < I; ++r) {
+    const uint32_t i = tid * I + r;
+    if (i < n) {
+      if ((headm >> r) & 1u) {
+        cur_gs = i;
+        hb[i] = cur_r;
+      }
+      gs[r] = cur_gs;
+      rex[r] = cur_r;
+      if ((runm >> r) & 1u) {
+        atomicAdd(&grun[cur_gs], 1u);
+        ++cur_r;
       }
     }
   }
   __syncthreads();
-  const uint32_t n_batch = s_nbatch;
-  STAMP(3);
-  if (tid == 0 && ncand > 0 && n_batch == 0) {
-    if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u)
-      ctl->err_info = (uint32_t)((lists ? out.skey[0] : uk[0]) & 0x7FFFFFFF);
+#pragma unroll
+  for (int r = 0; r < I; ++r) {
+    const uint32_t i = tid * I + r;
+    if (i < n) {
+      const uint32_t rb = rex[r] - hb[gs[r]];
+      const uint32_t pos = (runm >> r) & 1u ? gs[r] + rb : gs[r] + grun[gs[r]] + (i - gs[r] - rb);
+      z[pos] = i;
+    }
   }
-  // ---- (4) batch list and admit = batch calls not resident (batch order) -------------------
+  __syncthreads();
+  // ---- (4) cutoff (Alg. 1 l.34-37): kvb >= 1 makes the inclusive prefix strictly increasing,
+  // so "count <= BS and sum kvb <= P" holds exactly on a prefix (n_batch = last fitting + 1) ----
+  const uint32_t nc = min(n, BS);
+  uint32_t kvb[I];
+  unsigned long long my_kv = 0;
+#pragma unroll
+  for (int r = 0; r < I; ++r) {
+    const uint32_t p = tid * I + r;
+    kvb[r] = 0;
+    if (p < nc) {
+      const uint32_t i = z[p];
+      kvb[r] = blocks_for(pol, y_tok[i] + y_exec[i] + 1);  // R14
+      my_kv += kvb[r];
+    }
+  }
+  if (tid == 0) s_nbatch = 0;
+  unsigned long long incl = block_excl_scan<unsigned long long, NT>(my_kv, red64, nullptr);
+  unsigned long long inc[I];
+#pragma unroll
+  for (int r = 0; r < I; ++r) {
+    const uint32_t p = tid * I + r;
+    incl += kvb[r];
+    inc[r] = incl;
+    if (p < nc && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) atomicMax(&s_nbatch, p + 1);
+  }
+  __syncthreads();
+  const uint32_t n_batch = s_nbatch;
+  if (tid == 0 && nc > 0 && n_batch == 0) set_err(ctl, AUTX_E_NOMEM, y_slot[z[0]]);
+  if (stamps && tid == 0) ctl->dbg[46] = globaltimer();
+  // ---- (5) batch list, admit = batch calls not resident (batch order), previous-batch marks ---
   unsigned long long my_ad = 0;
   if (n_batch == 0 && tid == 0) s_kvsum = 0;
-  if (lists && tid == 0) s_kvsum = a_kv;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    uint32_t i = tid * R + r;
-    if (lists) break;  // (k_rank wrote the lists)
-    if (i + 1 == n_batch) s_kvsum = c_incl[r];  // sum kvb over the batch (read after the scans below)
-    if (i < n_batch) {
-      out.batch_slots[i] = c_s[r];
-      out.batch_ids[i] = c_cid[r];
-      if (!(c_qf[r] & QF_RES)) {
-        uint64_t held = c_ex[r] > 0 ? blocks_for(pol, c_tok[r] + c_ex[r]) : 0;  // R28
+  for (int r = 0; r < I; ++r) {
+    const uint32_t p = tid * I + r;
+    if (p < n_batch) {
+      const uint32_t i = z[p];
+      const uint32_t qfb = y_qfb[i];
+      if (p + 1 == n_batch) s_kvsum = inc[r];
+      out.batch_slots[p] = y_slot[i];
+      out.batch_ids[p] = y_cid[i];
+      if (qfb & QF_RUN) inb[qfb >> 8] = 1;
+      if (!(qfb & QF_RES)) {
+        const uint32_t e = y_exec[i];
+        const uint64_t held = e > 0 ? blocks_for(pol, y_tok[i] + e) : 0u;  // R28
         my_ad += (1ull << 44) | held;
       }
     }
   }
-  unsigned long long ad_tot = 0;
-  unsigned long long ad_pre = lists ? 0ull : block_excl_scan<unsigned long long, NT>(my_ad, red64, &ad_tot);
-  if (lists) ad_tot = (unsigned long long)a_na << 44 | a_si;  // (tid 0 only: the host record)
-  if (!lists) {
+  unsigned long long ad_tot;
+  const unsigned long long ad_pre = block_excl_scan<unsigned long long, NT>(my_ad, red64, &ad_tot);
+  {
     uint32_t pos = (uint32_t)(ad_pre >> 44);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      uint32_t i = tid * R + r;
-      if (i < n_batch && !(c_qf[r] & QF_RES)) {
-        out.admit_ids[pos] = c_cid[r];
-        s_ad[pos] = c_cid[r];
-        out.admit_slots[pos] = c_s[r];
-        ++pos;
+    for (int r = 0; r < I; ++r) {
+      const uint32_t p = tid * I + r;
+      if (p < n_batch) {
+        const uint32_t i = z[p];
+        if (!(y_qfb[i] & QF_RES)) {
+          out.admit_ids[pos] = y_cid[i];
+          out.admit_slots[pos] = y_slot[i];
+          s_ad[pos] = y_cid[i];
+          ++pos;
+        }
       }
     }
   }
   const uint32_t n_admit = (uint32_t)(ad_tot >> 44);
   const unsigned long long swap_in = ad_tot & ((1ull << 44) - 1);
-  STAMP(4);
-  // ---- (5) preempt = previous batch, still active, not in the batch (previous-batch order) ---
+  // ---- (6) preempt = previous batch, still active, not in the batch (previous-batch order) ---
   unsigned long long my_pre = 0;
   uint32_t is_pre = 0;
-  {
-    // membership of each previous-batch row in the sorted batch prefix: fixed-length branchless
-    // binary searches, the R of a thread interleaved (independent smem chains)
-    uint32_t pos[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) pos[r] = 0;
-    if (out.use_prev_pos) {
-      // k_rank's sorted position of each previous-batch entry that was a candidate (entries that
-      // were not, e.g. of a queue below q*, keep an older seqno and are not in the batch)
-#pragma unroll
-      for (int r = 0; r < R; ++r) pos[r] = (uint32_t)(p_pos[r] >> 32) == seqno ? (uint32_t)p_pos[r] : NONE;
-    } else {
-      for (uint32_t step = 1u << 12; step > 0; step >>= 1) {  // n_batch <= 4096
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const uint32_t probe = pos[r] + step;
-          if (probe <= n_batch && uk[probe - 1] < p_key[r]) pos[r] = probe;  // pos = #keys < key
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) pos[r] = pos[r] < n_batch && uk[pos[r]] == p_key[r] ? pos[r] : NONE;
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const uint32_t i = tid * R + r;
-      if (i < n_prev && !(p_qf[r] & QF_DEAD)) {
-        const bool in = pos[r] < n_batch;
-        if (!in) {
-          is_pre |= 1u << r;
-          my_pre += (1ull << 44) | p_held[r];
-        }
-      }
+  for (int r = 0; r < IP; ++r) {
+    const uint32_t j = tid * IP + r;
+    if (p_slot[r] != NONE && !(p_qf[r] & QF_DEAD) && !inb[j]) {
+      is_pre |= 1u << r;
+      my_pre += (1ull << 44) | blocks_for(pol, p_tok[r] + p_exec[r]);  // R28
     }
   }
   unsigned long long pre_tot;
-  unsigned long long pre_pre = block_excl_scan<unsigned long long, NT>(my_pre, red64, &pre_tot);
+  const unsigned long long pre_pre = block_excl_scan<unsigned long long, NT>(my_pre, red64, &pre_tot);
   {
     uint32_t pos = (uint32_t)(pre_pre >> 44);
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (is_pre & (1u << r)) {
+    for (int r = 0; r < IP; ++r)
+      if ((is_pre >> r) & 1u) {
         out.preempt_ids[pos] = p_cid[r];
         s_pr[pos] = p_cid[r];
-        out.preempt_slots[pos] = p_s[r];
-        ct.qf[p_s[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
+        out.preempt_slots[pos] = p_slot[r];
+        ct.qf[p_slot[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
         ++pos;
       }
   }
   const uint32_t n_preempt = (uint32_t)(pre_tot >> 44);
   const unsigned long long swap_out = pre_tot & ((1ull << 44) - 1);
-  const unsigned long long kv_sum = s_kvsum;
-  STAMP(5);
-  STAMP(6);
-
-  // ---- KV blocks: swap plan + allocation (a7) --------------------------------------------------
-  if (kv_on) {
+  // ---- (7) KV blocks: swap plan + allocation (a7) ---------------------------------------------
+  if (a.kv_on) {
+    __syncthreads();  // preempt_slots
     const uint32_t W = pol.max_blocks_per_call;
-    // (1) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots
+    // (7a) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots
     uint32_t base_blk = 0, base_free = 0;
     const uint32_t top0 = ctl->free_top, rtop0 = ctl->rs_free_top;
     for (uint32_t c0 = 0; c0 < n_preempt; c0 += NT) {
-      uint32_t i = c0 + tid;
+      const uint32_t i = c0 + tid;
       uint32_t s = 0, rslot = 0, nb = 0;
       if (i < n_preempt) {
         s = out.preempt_slots[i];
@@ -1950,12 +1016,12 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         nb = kv.rs_nblk[rslot];
       }
       uint32_t tot;
-      uint32_t boff = base_blk + block_excl_scan<uint32_t, NT>(nb, red, &tot);
+      uint32_t boff = base_blk + block_excl_scan<uint32_t, NT>(nb, red32, &tot);
       if (i < n_preempt) {
-        uint32_t cls = ceil_log2(nb);
+        const uint32_t cls = ceil_log2(nb);
         // pop a page range of 2^cls pages from the class stack, else bump-allocate
         uint32_t page;
-        uint32_t k = atomicSub(&ctl->host_free_top[cls], 1u);
+        const uint32_t k = atomicSub(&ctl->host_free_top[cls], 1u);
         if ((int32_t)k > 0) {
           page = kv.host_free[(size_t)cls * kv.host_free_cap + k - 1];
         } else {
@@ -1968,28 +1034,28 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         kv.plan_out[i] = PlanItem{page, nb, boff};
         const uint32_t* src = kv.rs_blocks + (size_t)rslot * W;
         for (uint32_t j = 0; j < nb; ++j) {
-          uint32_t b = src[j];
+          const uint32_t b = src[j];
           kv.plan_out_blocks[boff + j] = b;
           kv.free_stack[top0 + boff + j] = b;
         }
         kv.rs_nblk[rslot] = 0;
       }
       uint32_t rt;
-      uint32_t roff = base_free + block_excl_scan<uint32_t, NT>(i < n_preempt ? 1u : 0u, red, &rt);
+      const uint32_t roff = base_free + block_excl_scan<uint32_t, NT>(i < n_preempt ? 1u : 0u, red32, &rt);
       if (i < n_preempt) kv.rs_free[rtop0 + roff] = rslot;
       base_blk += tot;
       base_free += rt;
     }
     __syncthreads();
-    uint32_t top = top0 + base_blk, rtop = rtop0 + base_free;
-    // (2) batch calls: grow/allocate to kvb; admitted calls take a resident slot
+    const uint32_t top = top0 + base_blk, rtop = rtop0 + base_free;
+    // (7b) batch calls: grow/allocate to kvb; admitted calls take a resident slot
     uint32_t pop_base = 0, rs_pop = 0, in_blk = 0, in_items = 0;
     for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
-      uint32_t i = c0 + tid;
+      const uint32_t i = c0 + tid;
       uint32_t s = 0, need = 0, have = 0, rslot = NONE, admit = 0, held = 0;
       if (i < n_batch) {
-        s = (uint32_t)(uk[i] & 0x7FFFFFFFu);
-        uint32_t qf = ct.qf[s];
+        s = y_slot[z[i]];
+        const uint32_t qf = ct.qf[s];
         need = ceil_div_u32(ct.tok[s] + ct.exec[s] + 1, pol.block_tokens);
         if (need > W) set_err(ctl, AUTX_E_NOMEM, 2);
         if (qf & QF_RES) {
@@ -2000,12 +1066,12 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
           if (ct.exec[s] > 0) held = ceil_div_u32(ct.tok[s] + ct.exec[s], pol.block_tokens);
         }
       }
-      uint32_t alloc = need > have ? need - have : 0;
+      const uint32_t alloc = need > have ? need - have : 0;
       uint32_t tot, rt, ht, it;
-      uint32_t aoff = pop_base + block_excl_scan<uint32_t, NT>(alloc, red, &tot);
-      uint32_t roff = rs_pop + block_excl_scan<uint32_t, NT>(admit, red, &rt);
-      uint32_t hoff = in_blk + block_excl_scan<uint32_t, NT>(held, red, &ht);
-      uint32_t ioff = in_items + block_excl_scan<uint32_t, NT>(held ? 1u : 0u, red, &it);
+      const uint32_t aoff = pop_base + block_excl_scan<uint32_t, NT>(alloc, red32, &tot);
+      const uint32_t roff = rs_pop + block_excl_scan<uint32_t, NT>(admit, red32, &rt);
+      const uint32_t hoff = in_blk + block_excl_scan<uint32_t, NT>(held, red32, &ht);
+      const uint32_t ioff = in_items + block_excl_scan<uint32_t, NT>(held ? 1u : 0u, red32, &it);
       if (i < n_batch) {
         if (admit) {
           if (roff >= rtop) set_err(ctl, AUTX_E_NOMEM, 3);
@@ -2018,7 +1084,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         kv.rs_nblk[rslot] = need;
         if (held) {
           // swap-in: host copy -> the first `held` blocks of the new list; free host pages after
-          uint32_t page = ct.loc[s];
+          const uint32_t page = ct.loc[s];
           kv.plan_in[ioff] = PlanItem{page, held, hoff};
           for (uint32_t j = 0; j < held; ++j) kv.plan_in_blocks[hoff + j] = dst[j];
         }
@@ -2030,24 +1096,27 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       in_items += it;
     }
     __syncthreads();
-    // (3) free the host ranges of swapped-in calls (after this step's swap-out allocations)
+    // (7c) free the host ranges of swapped-in calls (after this step's swap-out allocations)
     for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
-      uint32_t i = c0 + tid;
+      const uint32_t i = c0 + tid;
       if (i < in_items) {
-        PlanItem it = kv.plan_in[i];
-        uint32_t cls = ceil_log2(it.nblk);
-        uint32_t k = atomicAdd(&ctl->host_free_top[cls], 1u);
-        kv.host_free[(size_t)cls * kv.host_free_cap + k] = (uint32_t)it.host_page;
+        const PlanItem itm = kv.plan_in[i];
+        const uint32_t cls = ceil_log2(itm.nblk);
+        const uint32_t k = atomicAdd(&ctl->host_free_top[cls], 1u);
+        kv.host_free[(size_t)cls * kv.host_free_cap + k] = (uint32_t)itm.host_page;
       }
     }
-    // (4) block table CSR of the batch
+    // (7d) block table CSR of the batch
     uint32_t b0 = 0;
     for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
-      uint32_t i = c0 + tid;
+      const uint32_t i = c0 + tid;
       uint32_t need = 0, rslot = 0;
-      if (i < n_batch) { rslot = ct.loc[(uint32_t)(uk[i] & 0x7FFFFFFFu)]; need = kv.rs_nblk[rslot]; }
+      if (i < n_batch) {
+        rslot = ct.loc[y_slot[z[i]]];
+        need = kv.rs_nblk[rslot];
+      }
       uint32_t tot;
-      uint32_t o = b0 + block_excl_scan<uint32_t, NT>(need, red, &tot);
+      const uint32_t o = b0 + block_excl_scan<uint32_t, NT>(need, red32, &tot);
       if (i < n_batch) {
         kv.bt_offsets[i] = o;
         const uint32_t* src = kv.rs_blocks + (size_t)rslot * W;
@@ -2066,105 +1135,206 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     }
     __syncthreads();
   }
-
-  STAMP(7);
-  // ---- step accounting + eager demotion (Alg. 1 l.20-23) for the batch, from registers ------
+  // ---- (8) step accounting + eager demotion (Alg. 1 l.20-23) for the batch --------------------
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    uint32_t i = tid * R + r;
-    if (!lists && i < n_batch) {
-      uint32_t sl = c_s[r];
-      uint32_t q = c_qf[r] & QF_QMASK;
-      ct.exec[sl] = c_ex[r] + 1;
-      ct.mtime[sl] = c_mt[r] + 1;
-      uint32_t qt = c_qt[r];
+  for (int r = 0; r < I; ++r) {
+    const uint32_t p = tid * I + r;
+    if (p < n_batch) {
+      const uint32_t i = z[p];
+      const uint32_t sl = y_slot[i];
+      uint32_t q = y_qfb[i] & QF_QMASK, qt = y_qt[i];
+      ct.exec[sl] = y_exec[i] + 1;
+      ct.mtime[sl] = y_mt[i] + 1;
       if (qt != AUTX_INF) {
         qt -= 1;
         if (qt == 0) {
-          q = min(q + 1, pol.K - 1);
+          q = min(q + 1, K - 1);
           qt = pol.quanta[q];
         }
         ct.quanta[sl] = qt;
       }
       ct.qf[sl] = (uint8_t)(q | QF_RUN | QF_RES);
-      ct.bidx[sl] = i;
-      out.prev_slots[i] = sl;
+      ct.bidx[sl] = p;
+      out.prev_slots[p] = sl;
     }
   }
+  // ---- (9) host record, host mirrors, counters reset for the next step ------------------------
   if (tid == 0) {
     ctl->n_prev = n_batch;
     HostOut h;
     h.n_batch = n_batch;
     h.n_admit = n_admit;
     h.n_preempt = n_preempt;
-    h.n_active = c_live;
+    h.n_active = n_live;
     h.swap_out_blocks = swap_out;
     h.swap_in_blocks = swap_in;
-    h.kv_blocks = kv_sum;
-    h.n_promoted = c_promo;
-    const bool may_err = kv_on || n_batch == 0;  // the only places this kernel sets an error
-    h.err = may_err ? ctl->err : c_err;
-    h.seqno = seqno;
-    h.err_info = may_err ? ctl->err_info : c_einfo;
+    h.kv_blocks = n_batch ? s_kvsum : 0ull;
+    h.n_promoted = n_promo;
+    h.err = ctl->err;
+    h.seqno = a.seqno;
+    h.err_info = ctl->err_info;
     ctl->n_promoted = 0;
     ctl->n_live = 0;
-    ctl->qs_bnd1 = 0;
-    ctl->n_cand_b = 0;
-    if (lists) { ctl->acc_nbatch = 0; ctl->acc_nadmit = 0; ctl->acc_kv = 0; ctl->acc_swap_in = 0; }
+    ctl->bar1 = 0;
+    ctl->bar2 = 0;
     s_hout = h;
   }
   for (uint32_t i = tid; i < QP_LINES * 32; i += NT) (&ctl->qpart[0][0])[i] = 0;
   for (uint32_t i = tid; i < out.n_sup * MAX_K; i += NT) out.sup_cnt[i] = 0;
-  // host-visible results: by default the device block (counts + lists) is copied out by one
-  // cudaMemcpyAsync after the kernel; the zero-copy variant stores the mirrors over PCIe here
   __syncthreads();
   if (!out.zero_copy) {
     if (tid == 0) *out.d_hout = s_hout;
   } else {
-    const uint32_t nb = s_hout.n_batch, na = s_hout.n_admit, np_ = s_hout.n_preempt;
-    // 16-B posted stores over PCIe: batch ids straight from registers (a thread's R blocked
-    // items are R/2 consecutive words), admit/preempt ids from their shared-memory copies
-    static_assert(R % 2 == 0, "blocked items pair into 16-B words");
-#pragma unroll
-    for (int k = 0; k < R / 2; ++k) {
-      const uint32_t i = tid * (R / 2) + k;
-      if (!lists && i < (nb + 1) / 2)
-        reinterpret_cast<uint4*>(out.h_batch)[i] =
-            make_uint4((uint32_t)c_cid[2 * k], (uint32_t)(c_cid[2 * k] >> 32), (uint32_t)c_cid[2 * k + 1],
-                       (uint32_t)(c_cid[2 * k + 1] >> 32));
+    // 16-B posted stores over PCIe: pairs of batch ids, groups of 4 slots, admit/preempt ids from
+    // their shared-memory copies
+    const uint32_t nb = n_batch;
+    for (uint32_t k = tid; k < (nb + 1) / 2; k += NT) {
+      const uint64_t c0 = y_cid[z[2 * k]], c1 = 2 * k + 1 < nb ? y_cid[z[2 * k + 1]] : 0ull;
+      reinterpret_cast<uint4*>(out.h_batch)[k] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)c1, (uint32_t)(c1 >> 32));
     }
-    // batch slots, R consecutive u32 per thread (8- or 16-byte stores)
-    if (!lists && tid * R < nb) {
-      if constexpr (R == 2) reinterpret_cast<uint2*>(out.h_batch_slots)[tid] = make_uint2(c_s[0], c_s[1]);
-      else if constexpr (R == 4) reinterpret_cast<uint4*>(out.h_batch_slots)[tid] = make_uint4(c_s[0], c_s[1], c_s[2], c_s[3]);
-      else for (int r = 0; r < R; ++r) out.h_batch_slots[tid * R + r] = c_s[r];
+    for (uint32_t k = tid; k < (nb + 3) / 4; k += NT) {
+      uint32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = 4 * k + u < nb ? y_slot[z[4 * k + u]] : 0u;
+      reinterpret_cast<uint4*>(out.h_batch_slots)[k] = make_uint4(v[0], v[1], v[2], v[3]);
     }
     const uint4* sa = reinterpret_cast<const uint4*>(s_ad);
     const uint4* sp = reinterpret_cast<const uint4*>(s_pr);
-    if (!lists)
-      for (uint32_t i = tid; i < (na + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_admit)[i] = sa[i];
-    for (uint32_t i = tid; i < (np_ + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_preempt)[i] = sp[i];
+    for (uint32_t i = tid; i < (n_admit + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_admit)[i] = sa[i];
+    for (uint32_t i = tid; i < (n_preempt + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_preempt)[i] = sp[i];
     __syncthreads();
     // the host reads after the stream event that follows this kernel, which orders every store
     if (tid == 0) *out.hout = s_hout;
   }
-  STAMP(8);
+  if (stamps && tid == 0) {
+    ctl->dbg[47] = globaltimer();
+    for (int i = 0; i < 16; ++i) {
+      ctl->dbg[64 + i] = ctl->dbg[40 + i];
+      ctl->dbg[40 + i] = 0;
+    }
+    ctl->dbg[40] = ~0ull;
+  }
 }
 
-template <int NT, int R, bool LISTS = false>
-__global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
-                                                 bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
-  pdl_wait();
-  pdl_trigger();
-  CHAIN_BEGIN(5);
-  finalize_body<NT, R, LISTS>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
-  if (STAMPS_ON) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      ctl->dbg[33 + 3 * 5] = globaltimer();
-      for (int i = 0; i < 32; ++i) { ctl->dbg[64 + i] = ctl->dbg[32 + i]; ctl->dbg[32 + i] = 0; }
-    }
+// ---------------------------------------------------------------------------------------------
+// The step kernel (select mode): one cooperative launch per step.
+//   CTAs 0 .. n_tile_ctas-1: the dense pass over their tiles (a3, a4) with per-queue counts;
+//     grid barrier 1; selection and region-A extraction (a5); arrive at barrier 2.
+//   CTA n_tile_ctas: the prologue (a1, a2: completions and arrivals), the "prologue done" flag
+//     the deferred rows wait for; barrier 1; selection; the previous batch's slots; barrier 2;
+//     order, cutoff, lists, accounting, KV plan (a5, a6, a3, a7).
+// Stamps (dbg): 40 first CTA start, 41 last CTA start, 42 prologue done, 43 barrier 1 passed,
+// 44 barrier 2 passed, 45 finalize loads, 46 order + cutoff, 47 end, 48 last tile CTA at
+// barrier 1 (all but 40/41/48 by the finalize CTA).
+// ---------------------------------------------------------------------------------------------
+template <int I>
+__global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ StepArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ SelSmem S;
+  __shared__ unsigned long long red64[33];
+  __shared__ uint32_t red32[33];
+  __shared__ uint32_t wq16[ST_THREADS / 32][MAX_K / 2];
+  __shared__ uint32_t wn[ST_THREADS / 32];
+  const uint32_t tid = threadIdx.x;
+  Ctl* ctl = a.ctl;
+  const bool stamps = STAMPS_ON(a.pol);
+  if (stamps && tid == 0) {
+    const unsigned long long g = globaltimer();
+    atomicMin(&ctl->dbg[40], g);
+    atomicMax(&ctl->dbg[41], g);
   }
+  if (blockIdx.x == a.n_tile_ctas) {
+    // ---- prologue + finalize CTA ----
+    if (a.do_pro) prologue_body<ST_THREADS>(a, dsm);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(&ctl->pro_seq, a.seqno);
+      if (stamps) ctl->dbg[42] = globaltimer();
+    }
+    // the previous batch's slots now; their rows into L2 while the tiles run
+    constexpr int IP = I / 2;
+    const uint32_t n_prev = ctl->n_prev;
+    uint32_t p_slot[IP];
+#pragma unroll
+    for (int r = 0; r < IP; ++r) {
+      const uint32_t j = tid * IP + r;
+      p_slot[r] = j < n_prev ? a.out.prev_slots[j] : NONE;
+      if (p_slot[r] != NONE) {
+        const uint32_t s = p_slot[r];
+        prefetch_l2(a.ct.cid + s); prefetch_l2(a.ct.arr + s); prefetch_l2(a.ct.tok + s);
+        prefetch_l2(a.ct.exec + s); prefetch_l2(a.ct.mtime + s); prefetch_l2(a.ct.quanta + s);
+      }
+    }
+    grid_arrive(&ctl->bar1);
+    grid_wait(&ctl->bar1, gridDim.x);
+    if (stamps && tid == 0) ctl->dbg[43] = globaltimer();
+    select_for(a, NONE, S);
+    const uint32_t qs = S.qs, nx = S.nx, n_live = S.n_live, n_promo = S.n_promo;
+    finalize_core<I>(a, dsm, qs, nx, n_live, n_promo, p_slot, n_prev, true, red64, red32);
+    return;
+  }
+  // ---- tile CTA ----
+  uint32_t* s_filt = reinterpret_cast<uint32_t*>(dsm);  // 2048-bit filter of completed programs
+  const bool filt_on = !a.defer_all && a.pro.n_comp > 0;
+  if (filt_on) {
+    if (tid < 64) s_filt[tid] = 0;
+    __syncthreads();
+    if (tid < a.pro.n_comp) {
+      const uint32_t p = a.pro.comp_prog[tid];
+      atomicOr(&s_filt[(p >> 5) & 63], 1u << (p & 31));
+    }
+    __syncthreads();
+  }
+  uint32_t qw[2];
+  uint32_t last = NONE;
+  for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
+    uint64_t hq = 0;
+    uint32_t np = 0, nl = 0;
+    tile_pass(a, tile, s_filt, filt_on, qw, hq, np, nl);
+    tile_publish(a, tile, hq, np, nl, wq16, wn);
+    last = tile;
+  }
+  grid_arrive(&ctl->bar1);
+  if (stamps && tid == 0) atomicMax(&ctl->dbg[48], globaltimer());
+  grid_wait(&ctl->bar1, gridDim.x);
+  for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
+    select_for(a, tile, S);
+    if (S.has) {
+      if (tile != last) {
+        // an earlier tile of this CTA: its flags after the pass, from L2
+        const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+        const uint2 qv = row0 < a.n_rows ? __ldcg(reinterpret_cast<const uint2*>(a.ct.qf + row0))
+                                         : make_uint2(0x40404040u, 0x40404040u);
+        qw[0] = qv.x;
+        qw[1] = qv.y;
+        last = tile;
+      }
+      extract_tile(a, tile, qw, S, red64);
+    }
+    __syncthreads();  // S reuse
+  }
+  grid_arrive(&ctl->bar2);
+}
+
+// Radix mode: the finalize alone (one CTA) on the sorted candidates k_take wrote (q* = K: no
+// region B; the partition leaves an already key-ordered Y unchanged).
+template <int I>
+__global__ void __launch_bounds__(ST_THREADS) k_fin(const __grid_constant__ StepArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ unsigned long long red64[33];
+  __shared__ uint32_t red32[33];
+  constexpr int IP = I / 2;
+  const uint32_t tid = threadIdx.x;
+  Ctl* ctl = a.ctl;
+  const uint32_t n_prev = ctl->n_prev;
+  uint32_t p_slot[IP];
+#pragma unroll
+  for (int r = 0; r < IP; ++r) {
+    const uint32_t j = tid * IP + r;
+    p_slot[r] = j < n_prev ? a.out.prev_slots[j] : NONE;
+  }
+  finalize_core<I>(a, dsm, a.pol.K, ctl->n_x, ctl->n_live, ctl->n_promoted, p_slot, n_prev, false, red64, red32);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -2178,23 +1348,22 @@ cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, Pro
     return launch_pdl(k_complete<32>, 1, 32, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
   else if (n <= 256)
     return launch_pdl(k_complete<256>, 1, 256, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
-  else
-    return launch_pdl(k_complete<FIN_THREADS>, 1, FIN_THREADS, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
-  return cudaGetLastError();
+  return launch_pdl(k_complete<1024>, 1, 1024, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
 }
 
 cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,
                          uint64_t stride, uint32_t G, uint32_t t) {
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_apply<<<1, FIN_THREADS, 0, s>>>(pol, pt, (const char*)base, stride, G, t);
+  k_apply<<<1, 1024, 0, s>>>(pol, pt, (const char*)base, stride, G, t);
   return cudaGetLastError();
 }
 
 cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,
                          const RouteArr* arr, uint32_t n, int8_t* pin, uint32_t threshold,
                          int32_t* out) {
+  if (!n) return cudaSuccess;
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  if (n) k_route<<<1, 32, 0, s>>>((const char*)base, stride, G, arr, n, pin, threshold, out);
+  k_route<<<1, 32, 0, s>>>((const char*)base, stride, G, arr, n, pin, threshold, out);
   return cudaGetLastError();
 }
 
@@ -2203,152 +1372,90 @@ cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, Pro
                             const uint32_t* par) {
   if (n == 0) return cudaSuccess;
   return launch_pdl(k_register, (n + 255) / 256, 256, 0, s, pol, ct, pt, recs, n, first_slot, t, par);
+}
+
+// Candidates per finalize thread for a batch size (C = ST_THREADS * I >= 2 BS).
+static int fin_items(uint32_t bs) { return bs <= 512 ? 2 : bs <= 1024 ? 4 : 8; }
+
+template <int I>
+static cudaError_t setup_one(int* occ) {
+  const size_t sm = fin_smem_bytes<I>();
+  cudaError_t e = cudaFuncSetAttribute(k_step<I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_fin<I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_step<I>, ST_THREADS, sm);
+}
+
+// Called by autx_create with the context's device current (the attributes are per device).
+cudaError_t step_kernel_setup(uint32_t max_batch, uint32_t* capacity_out) {
+  int dev = 0, sms = 0, occ = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  const int I = fin_items(max_batch);
+  e = I == 2 ? setup_one<2>(&occ) : I == 4 ? setup_one<4>(&occ) : setup_one<8>(&occ);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  *capacity_out = (uint32_t)(occ * sms);
+  return cudaSuccess;
+}
+
+cudaError_t launch_prologue(cudaStream_t s, const StepArgs& a) {
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
+  k_prologue<<<1, ST_THREADS, PRO_INLINE * (4 + sizeof(ArrivalRec) + sizeof(CompRec)), s>>>(a);
   return cudaGetLastError();
 }
 
-static uint32_t pow2_at_least(uint32_t x) {
-  uint32_t p = 1;
-  while (p < x) p <<= 1;
-  return p;
+template <int I>
+static cudaError_t launch_step_kernel(cudaStream_t s, const StepArgs& a, uint32_t grid) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(ST_THREADS);
+  cfg.dynamicSmemBytes = fin_smem_bytes<I>();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // CTAs wait for each other: all must be resident
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
+  return cudaLaunchKernelEx(&cfg, k_step<I>, a);
 }
 
-// Whether launch_step fuses the step prologue into the dense pass (k_scan_fused): opt-in with
-// AUTX_FUSED_PROLOGUE=1 on the default pipeline.  Measured slower than the PDL-chained
-// k_prologue + k_scan_tile (38.2 vs 35.8 us per step at 1M calls): with 8 rows per thread the
-// record folding pushes the pass past 64 registers (spills), and at 4 rows per thread a 1M-row
-// table no longer fits one wave (2 x 512-thread CTAs per SM).
-bool step_can_fuse_prologue() {
-  static const bool ok = getenv("AUTX_FUSED_PROLOGUE") && !getenv("AUTX_SCAN_SIMPLE") && !getenv("AUTX_FUSE") &&
-                         !getenv("AUTX_SELECT_KERNEL") && !getenv("AUTX_SCAN_BULK");
-  return ok;
+template <int I>
+static cudaError_t launch_fin_kernel(cudaStream_t s, const StepArgs& a) {
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
+  k_fin<I><<<1, ST_THREADS, fin_smem_bytes<I>(), s>>>(a);
+  return cudaGetLastError();
 }
 
-cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                        Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
-                        uint32_t seqno, cudaEvent_t* ev, const RadixState* rx, uint32_t arr_base,
-                        uint32_t* radix_passes, uint32_t first_new, const PrologueArgs* fused,
-                        CompRec* fused_rec, uint32_t* fused_cslots, ArrivalRec* fused_arr) {
-  uint32_t ntiles = (n_rows + TILE - 1) / TILE;
-  if (ntiles == 0) ntiles = 1;
-  out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
-  out.use_prev_pos = rx ? 0u : 1u;  // k_rank publishes previous-batch positions (select mode)
-  static const bool rank_narrow = getenv("AUTX_RANK_NARROW") != nullptr;
-  out.rank_wide = rank_narrow ? 0u : 1u;  // k_rank may use a warp per key when candidates are few
+cudaError_t launch_step(cudaStream_t s, StepArgs& a, uint32_t capacity, cudaEvent_t* ev, const RadixState* rx,
+                        uint32_t arr_base, uint32_t* radix_passes) {
+  a.ntiles = std::max<uint32_t>(1, (a.n_rows + TILE - 1) / TILE);
+  a.out.n_sup = (a.ntiles + SUP_TILES - 1) / SUP_TILES;
+  a.n_tile_ctas = std::min<uint32_t>(a.ntiles, capacity - 1);
+  const int I = fin_items(a.pol.max_batch);
   if (ev) cudaEventRecord(ev[0], s);
+  cudaError_t e;
   if (rx) {
+    if (a.do_pro) {
+      e = launch_prologue(s, a);
+      if (e != cudaSuccess) return e;
+    }
     static int sms = 0;
     if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    cudaError_t e = launch_radix_order(s, pol, ct, pt, ctl, out, *rx, t, n_rows, arr_base, sms, radix_passes);
+    e = launch_radix_order(s, a.pol, a.ct, a.pt, a.ctl, a.out, *rx, a.t, a.n_rows, arr_base, sms, radix_passes);
     if (e != cudaSuccess) return e;
-    if (ev) cudaEventRecord(ev[1], s);
+    e = I == 2 ? launch_fin_kernel<2>(s, a) : I == 4 ? launch_fin_kernel<4>(s, a) : launch_fin_kernel<8>(s, a);
   } else {
-    static int scan_ctas = 0;
-    static bool simple = getenv("AUTX_SCAN_SIMPLE") != nullptr;  // A/B switch for profiling
-    // last-CTA fusion of select into the scan and finalize into the rank kernel: measured slower
-    // than the PDL-chained separate kernels (fences vs hidden launch gaps), kept as an option
-    static bool fuse = getenv("AUTX_FUSE") != nullptr;
-    // selection: derived by every gather CTA from two-level counts (default), or a one-CTA
-    // kernel between the scan and the gather (AUTX_SELECT_KERNEL; one more kernel in the chain,
-    // measured ~4 us slower per step)
-    static bool sel_kernel = getenv("AUTX_SELECT_KERNEL") != nullptr;
-    if (!scan_ctas) {
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-      scan_ctas = 2 * sms;
-      cudaFuncSetAttribute(k_scan_bulk<SEL_KERNEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
-      cudaFuncSetAttribute(k_scan_bulk<SEL_FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
-      cudaFuncSetAttribute(k_scan_bulk<SEL_GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCAN_STAGES * STAGE_BYTES);
-    }
-    static bool bulk = getenv("AUTX_SCAN_BULK") != nullptr;  // the persistent TMA-staged pass
-    if (simple) {
-      launch_pdl(k_scan, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, out, t, n_rows);
-      if (ev) cudaEventRecord(ev[1], s);
-      launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
-    } else if (!bulk && !fuse) {
-      // default 1: prog + L2 prefetches while the prologue runs (measured ~0.4 us per step)
-      static const uint32_t pre = getenv("AUTX_SCAN_PRE") ? (uint32_t)atoi(getenv("AUTX_SCAN_PRE")) : 1u;
-      if (sel_kernel)
-        launch_pdl(k_scan_tile<SEL_KERNEL>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, first_new, pre);
-      else if (fused)
-        launch_pdl(k_scan_fused<SEL_GATHER>, ntiles, FUSED_THREADS, 0, s, pol, ct, pt, ctl, out, n_rows, fused_rec,
-                   fused_cslots, fused_arr, *fused);
-      else
-        launch_pdl(k_scan_tile<SEL_GATHER>, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, first_new, pre);
-      if (ev) cudaEventRecord(ev[1], s);
-      if (sel_kernel) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
-    } else {
-      const int mode = fuse ? SEL_FUSED : sel_kernel ? SEL_KERNEL : SEL_GATHER;
-      const uint32_t sgrid = std::min<uint32_t>(ntiles, scan_ctas);
-      const size_t ssmem = (size_t)SCAN_STAGES * STAGE_BYTES;
-      if (mode == SEL_GATHER) launch_pdl(k_scan_bulk<SEL_GATHER>, sgrid, BULK_THREADS, ssmem, s, pol, ct, pt, ctl, out, t, ntiles);
-      else if (mode == SEL_FUSED) launch_pdl(k_scan_bulk<SEL_FUSED>, sgrid, BULK_THREADS, ssmem, s, pol, ct, pt, ctl, out, t, ntiles);
-      else launch_pdl(k_scan_bulk<SEL_KERNEL>, sgrid, BULK_THREADS, ssmem, s, pol, ct, pt, ctl, out, t, ntiles);
-      if (ev) cudaEventRecord(ev[1], s);
-      if (mode == SEL_KERNEL) launch_pdl(k_select, 1, SEL_THREADS, 0, s, pol, ct, ctl, out, ntiles);
-    }
-    const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
-    if (simple || fuse || sel_kernel)
-      launch_pdl(k_gather, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t);
-    else if (fused)  // one more CTA commits the fused prologue's process-table writes
-      launch_pdl(k_gather_ss, ggrid + 1, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t, pt,
-                 FusedCommit{1u, fused->n_comp, fused->n_arr, 0u, fused_rec, fused_cslots, fused_arr});
-    else
-      launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t, pt, FusedCommit{});
+    const uint32_t grid = a.n_tile_ctas + 1;
+    e = I == 2 ? launch_step_kernel<2>(s, a, grid) : I == 4 ? launch_step_kernel<4>(s, a, grid)
+                                                          : launch_step_kernel<8>(s, a, grid);
   }
-  uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
-  // sorted keys [np] + admit and preempt id staging [2 x even(BS)]
-  size_t fin_smem_bytes = ((size_t)np + 2 * ((pol.max_batch + 1) & ~1u)) * sizeof(uint64_t);
-  // keys, compacted keys, element indices of <= 2 BS candidates (fused: finalize's layout after)
-  // k_rank also decides the batch (lists, accounting) when there is no KV allocator and its keys
-  // + kvb fit shared memory
-  // (the 512-thread finalize and the fused rank+finalize have the matching variant)
-  out.rank_lists = (!kv_on && !rx && pol.max_batch <= 1024 && !getenv("AUTX_FIN256") &&
-                    !getenv("AUTX_FINALIZE_LISTS")) ? 1u : 0u;
-  size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch *
-                                          (2 * sizeof(uint64_t) + sizeof(uint32_t) + (out.rank_lists ? 8 : 0)),
-                                      fin_smem_bytes);
-  // at most one rank CTA per SM: the CTAs are dispatched while the previous kernel still holds
-  // most SMs, and two packed on one SM halve each other's issue rate (measured: the count loop
-  // ran 2x slower behind the self-selecting gather's grid)
-  rank_smem = std::max<size_t>(rank_smem, 120 * 1024);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_finalize<FIN_THREADS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_finalize<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_finalize<512, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_finalize<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_rank<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_rank<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const uint32_t rank_grid = (2 * pol.max_batch + RANK_PER_CTA - 1) / RANK_PER_CTA;
-  if (ev) cudaEventRecord(ev[2], s);
-  static bool fuse_fin = getenv("AUTX_FUSE") != nullptr;
-  if (pol.max_batch <= 1024 && fuse_fin) {
-    // rank + finalize in one launch: the last rank CTA (256 threads = 4 candidates each) finalizes
-    launch_pdl(k_rank<true>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
-  } else if (pol.max_batch <= 1024) {
-    // 512 threads x 2 candidates: 4 warps per scheduler to hide the phase's latency chains
-    // (1024 threads hit the 64-register cap and spill; 256 threads leave 2 warps per scheduler)
-    static bool fin256 = getenv("AUTX_FIN256") != nullptr;
-    launch_pdl(k_rank<false>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
-    if (fin256)
-      launch_pdl(k_finalize<256, 4>, 1, 256, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
-    else
-      launch_pdl(out.rank_lists ? k_finalize<512, 2, true> : k_finalize<512, 2>, 1, 512, fin_smem_bytes, s, pol, ct, ctl,
-                 out, kv, kv_on, t, np, seqno);
-  } else {
-    launch_pdl(k_rank<false>, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
-    launch_pdl(k_finalize<FIN_THREADS, 4>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np,
-               seqno);
-  }
-  if (ev) cudaEventRecord(ev[3], s);
+  if (e != cudaSuccess) return e;
+  if (ev) cudaEventRecord(ev[1], s);
   return cudaGetLastError();
 }
 

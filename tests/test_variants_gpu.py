@@ -12,18 +12,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 VARIANTS = {
-    "select_kernel": {"AUTX_SELECT_KERNEL": "1"},  # one-CTA selection kernel before the gather
-    "scan_bulk": {"AUTX_SCAN_BULK": "1"},        # persistent TMA-staged dense pass
-    "scan_bulk_select": {"AUTX_SCAN_BULK": "1", "AUTX_SELECT_KERNEL": "1"},
-    "scan_simple": {"AUTX_SCAN_SIMPLE": "1"},    # plain per-tile pass + selection kernel
-    "fused": {"AUTX_FUSE": "1"},                 # last-CTA fusions (select into scan, finalize into rank)
-    "dma_out": {"AUTX_DMA_OUT": "1"},            # host lists by one copy instead of zero-copy stores
-    "scan_pre0": {"AUTX_SCAN_PRE": "0"},         # scan reads nothing before the PDL wait
-    "fused_prologue": {"AUTX_FUSED_PROLOGUE": "1"},  # prologue folded into the dense pass (k_scan_fused)
-    "no_graph": {"AUTX_NO_GRAPH": "1"},          # the step's kernels as separate launches, not a graph replay
-    "finalize_lists": {"AUTX_FINALIZE_LISTS": "1"},  # finalize cuts the batch and writes the lists (not k_rank)
-    "rank_narrow": {"AUTX_RANK_NARROW": "1"},    # half a warp per key in k_rank whatever the candidate count
-    "scan_pre2": {"AUTX_SCAN_PRE": "2"},         # ... prog, base, mtime before the wait
+    "dma_out": {"AUTX_DMA_OUT": "1"},      # host lists by one copy instead of zero-copy stores
+    "defer_all": {"AUTX_DEFER_ALL": "1"},  # every row of the dense pass waits for the prologue
 }
 
 SUBSET = "fig2 or atlas_dag or mcts or chatbot or compaction or react or (random_tiny and 7)"
