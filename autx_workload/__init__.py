@@ -8,5 +8,6 @@ without sharing any method code (task rule ③).
 """
 from .gen import (  # noqa: F401
     Trace, fig2, atlas_dag_fixture, random_tiny, chatbot, react, mcts_mapreduce,
-    mixed, burst_mcts_mapreduce, lognormal_clipped, dag_trace, BASE_SEED, CONFIG_INDEX,
+    mixed, burst_mcts_mapreduce, burst_mixed, churn, concat, lognormal_clipped, dag_trace, BASE_SEED,
+    CONFIG_INDEX,
 )

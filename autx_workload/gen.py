@@ -402,6 +402,30 @@ def burst_mcts_mapreduce(target_active=1_000_000, seed=None) -> Trace:
     return mcts_mapreduce(n_programs=n_prog, seed=seed)
 
 
+def burst_mixed(target_active=4_000_000, seed=None) -> Trace:
+    """BASELINE configs[4] on one engine: an offline burst of an equal draw of
+    ShareGPT chat, BFCL ReAct and LATS MCTS / map-reduce programs.  n programs of each
+    kind put about n + n + 36.5 n calls in the ready set at step 0 (a chain's first call; an MCTS
+    program's w=5 roots, a map-reduce program's F ~ U{8..128} maps)."""
+    rng = rng_for(BASE_SEED + CONFIG_INDEX["multi"] if seed is None else seed)
+    n = int(round(target_active / (2 + 0.5 * MCTS_WIDTH + 0.5 * 68)))
+    s = [int(x) for x in rng.integers(0, 1 << 30, 3)]
+    return concat([chatbot(n, seed=s[0]), react(n, seed=s[1]), mcts_mapreduce(n, seed=s[2])], name="mixed_burst")
+
+
+def churn(n_programs=1_000_000, calls_per_program=4, seed=None) -> Trace:
+    """Stress shape for the step's prologue (SURVEY §8(d) timing protocol step 2): chains of
+    one-token calls with no interrupts, all submitted at step 0, so every call in a batch
+    completes after one step and its successor arrives in the next: about BS completions and BS
+    arrivals per step.  Prefills follow BFCL."""
+    rng = rng_for(BASE_SEED + 100 if seed is None else seed)
+    ncalls = np.full(n_programs, calls_per_program, np.int64)
+    C = int(ncalls.sum())
+    dec = np.ones(C, np.int64)
+    pre = lognormal_clipped(rng, *BFCL_PREFILL, C)
+    return _chains_trace("churn", ncalls, dec, pre, np.zeros(C, np.int64), np.zeros(n_programs, np.int64), 0)
+
+
 def mixed(n_programs=30_000, seed=None, rate=None) -> Trace:
     """Equal draw from ShareGPT / BFCL / LATS-style programs."""
     rng = rng_for(BASE_SEED + CONFIG_INDEX["multi"] if seed is None else seed)

@@ -4,18 +4,21 @@
 
 A step = one pass of SURVEY §8(a) rows a1-a6 (+ a8 when N > 1) through the C ABI over the
 whole active set: completions of the previous step, arrivals, demotion, anti-starvation,
-ordering, cutoff, admit/preempt lists and accounting.  Workload (BASELINE configs[3]): an
-offline burst of 50/50 LATS-MCTS and map-reduce DAG programs with ~1M calls ready at
-step 0, ATLAS, SPEC ladder (K=8), beta=2, BS=1024, KV budget 32768 blocks of 16 tokens;
-decisions/s = active calls ranked per step / device step time.  The KV swap (row a7) is timed
-in a second phase on the ReAct-shaped config with 8B-geometry pools (32 layers x 32 KiB
-chunks) and reported under "swap".
+ordering, cutoff, admit/preempt lists and accounting.  In select mode the device work of a step
+is ONE cooperative kernel (k_step).  Workload (BASELINE configs[3], the default): an offline
+burst of 50/50 LATS-MCTS and map-reduce DAG programs with ~1M calls ready at step 0,
+ATLAS, SPEC ladder (K=8), beta=2, BS=1024, KV budget 32768 blocks of 16 tokens, fast-forwarded
+10,000 steps so that queues, waits and promotions are diverse; decisions/s = active calls ranked
+per step / device step time.  Other workloads: --workload mixed4m (configs[4] on one engine: 4M
+calls, beyond L2), chatbot / react (configs[1] / [2]), churn (about BS completions and BS
+arrivals per step).  The KV swap (row a7) is timed in a second phase on the ReAct-shaped config
+with 8B-geometry pools (32 layers x 32 KiB chunks) and reported under "swap".
 
 Timing: W warm-up steps, then K steps; before each step L2 is flushed (a 512 MiB write) and a
 spin kernel gates the stream while the host enqueues the step, so CUDA events around the step
 measure device time only.  Multi-GPU: one rank per GPU (torchrun), each rank runs its own
-1M-call shard (weak scaling); every step includes the routing epoch (completion records + load
-all-gathered over NCCL, Alg. 2 over the replicated arrivals).
+shard; every step includes the routing epoch (completion records + load all-gathered over NCCL,
+Alg. 2 over the replicated arrivals).
 """
 import argparse
 import json
@@ -32,9 +35,15 @@ sys.path.insert(0, ROOT)
 
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
-SCAN_BYTES_PER_CALL = 13      # qf 1 + prog 4 + base 4 + mtime 4
-PROMOTE_BYTES = 4             # base written per promotion (other fields only if they change)
-PROG_BYTES = 12               # svc 4 + pwait 8 gathered per program
+# SURVEY §8(d) algorithmic bytes of one step: per active call 34 B read (prog, arr, seq, q,
+# flags, quanta, wait, mtime, exec, kvb) + 18 B written (q, flags, quanta, wait, mtime, exec);
+# per program 16 B (svc, pwait, parr, pin).  The roofline fraction uses these.
+ALGO_BYTES_PER_CALL = 52
+ALGO_BYTES_PER_PROGRAM = 16
+# What this design actually has to stream per step: the dense pass reads qf 1 +
+# prog 4 + base 4 + mtime 4 per row and the program rows it gathers (svc 4 + pwait 8).
+DESIGN_BYTES_PER_ROW = 13
+DESIGN_BYTES_PER_PROGRAM = 12
 
 
 def parse():
@@ -43,51 +52,76 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="autx", choices=["autx", "reference"])
-    ap.add_argument("--active", type=int, default=1_000_000)
-    ap.add_argument("--ff", type=int, default=100, help="fast-forward steps before warm-up")
+    ap.add_argument("--active", type=int, default=None, help="active calls of the burst (workload default)")
+    ap.add_argument("--ff", type=int, default=10_000, help="fast-forward steps before warm-up")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-swap", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--swap-steps", type=int, default=60)
     ap.add_argument("--order", default="select", choices=["select", "radix"])
+    ap.add_argument("--beta", default="2", choices=["2", "inf"], help="anti-starvation threshold")
     ap.add_argument("--policy", default=None, choices=["atlas", "atlas_eq2", "plas"],
                     help="override the workload's policy (atlas_eq2: exact Eq. 2, SURVEY 8(f) item 2)")
-    ap.add_argument("--workload", default="mcts", choices=["mcts", "chatbot", "react"],
-                    help="mcts: BASELINE configs[3] (default, the headline); chatbot/react: configs[1]/[2]")
+    ap.add_argument("--workload", default="mcts", choices=list(WORKLOADS),
+                    help="mcts: BASELINE configs[3] (default, the headline); mixed4m: configs[4] on one "
+                         "engine; chatbot/react: configs[1]/[2]; churn: ~BS completions + arrivals per step")
+    ap.add_argument("--json-out", default=None, help="also write the JSON line to this file")
     return ap.parse_args()
 
 
-def chain_spans(phase):
-    """Median (start, end) in us of each step-chain kernel relative to the first one's start, from
-    a -DAUTX_CHAIN_STAMPS build's stamps (None in a normal build)."""
-    names = ["prologue", "scan", "select", "gather", "rank", "finalize"]
+WORKLOADS = {
+    "mcts": dict(policy="atlas", max_batch=1024, kv_budget=32768, active=1_000_000,
+                 desc="mcts_mapreduce_burst (BASELINE configs[3])"),
+    "mixed4m": dict(policy="atlas", max_batch=1024, kv_budget=32768, active=4_000_000,
+                    desc="mixed burst, equal draw chat / ReAct / MCTS+map-reduce (BASELINE configs[4] on one engine)"),
+    "chatbot": dict(policy="plas", max_batch=256, kv_budget=6000, active=10_000,
+                    desc="chatbot 10k ShareGPT-shaped programs (BASELINE configs[1])"),
+    "react": dict(policy="plas", max_batch=256, kv_budget=8000, active=100_000,
+                  desc="ReAct 100k BFCL-shaped programs (BASELINE configs[2])"),
+    "churn": dict(policy="atlas", max_batch=1024, kv_budget=None, active=1_000_000,
+                  desc="churn stress: 1M one-token chains, ~BS completions and BS arrivals per step"),
+}
+
+
+def make_trace(name, active, seed_off=0):
+    from autx_workload import (burst_mcts_mapreduce, burst_mixed, chatbot, react, churn, BASE_SEED,
+                               CONFIG_INDEX)
+    if name == "mcts":
+        return burst_mcts_mapreduce(active, seed=BASE_SEED + CONFIG_INDEX["mcts"] + seed_off)
+    if name == "mixed4m":
+        return burst_mixed(active, seed=BASE_SEED + CONFIG_INDEX["multi"] + seed_off)
+    if name == "chatbot":
+        return chatbot(active, seed=BASE_SEED + CONFIG_INDEX["chatbot"] + seed_off)
+    if name == "react":
+        return react(active, seed=BASE_SEED + CONFIG_INDEX["react"] + seed_off)
+    return churn(active, seed=BASE_SEED + 100 + seed_off)
+
+
+PHASES = [("first_cta_start", 40), ("last_cta_start", 41), ("prologue_done", 42), ("last_tile_at_barrier1", 48),
+          ("barrier1_passed", 43), ("barrier2_passed", 44), ("finalize_loads", 45), ("order_cutoff", 46),
+          ("end", 47)]
+
+
+def phase_spans(phase):
+    """Median times in us of the step kernel's phases relative to its first CTA's start, from the
+    %globaltimer stamps of the last step (autx_phase_times [64, 80))."""
     rows = []
     for p in phase:
-        c = [int(x) for x in p[64:96]]
-        starts = [c[3 * k] for k in range(6) if c[3 * k]]
-        if not starts:
-            return None
-        t0 = min(starts)
-        rows.append({n: (c[3 * k] - t0, c[3 * k + 1] - t0, c[3 * k + 2] - t0) for k, n in enumerate(names) if c[3 * k]})
-        rows[-1]["rank_keys"] = (c[20], c[21], 0)
-        if c[22]:  # k_rank CTA 0: keys loaded, compacted, counted
-            rows[-1]["rank_phases"] = tuple(c[22 + i] - t0 for i in range(3))
-        if c[25]:  # k_gather_ss tile 0: selection known, positions known, records emitted
-            rows[-1]["gather_phases"] = tuple(c[25 + i] - t0 for i in range(3))
-    out = {}
-    for n in names + ["rank_keys", "rank_phases", "gather_phases"]:
-        v = [r[n] for r in rows if n in r]
-        if v:
-            div = 1 if n == "rank_keys" else 1e3
-            out[n] = [round(float(np.median([x[i] for x in v])) / div, 2) for i in range(2 if n == "rank_keys" else 3)]
-    return out
+        c = [int(x) for x in p[64:80]]
+        if not c[0] or c[0] == (1 << 64) - 1 or not c[7]:
+            continue
+        rows.append({n: (c[i - 40] - c[0]) / 1e3 for n, i in PHASES if c[i - 40]})
+    if not rows:
+        return None
+    return {n: round(float(np.median([r[n] for r in rows if n in r])), 2) for n, _ in PHASES
+            if any(n in r for r in rows)}
 
 
 def ncu_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per k_scan_tile launch from the committed
-    `ncu --set full` capture summary (profiles/scan_traffic.json), or None."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per k_step launch from the committed
+    `ncu --set full` capture summary (profiles/step_traffic.json), or None."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "scan_traffic.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "step_traffic.json")))
         return d["dram_bytes_per_launch"], d.get("source")
     except Exception:
         return None, None
@@ -202,7 +236,7 @@ def oracle_decisions_per_s(active, steps, warmup, seed_off=0):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    active = max(10_000, args.active // 10)
+    active = max(10_000, (args.active or 1_000_000) // 10)
     steps = max(1, min(args.steps, 10))
     v, per_step, wall, _ = oracle_decisions_per_s(active, steps, min(args.warmup, 3))
     line = {"metric": "sched decisions/s at 1M active calls", "value": v, "unit": "decisions/s",
@@ -293,39 +327,31 @@ def main():
         run_reference(args, rank, world)
         return
     import torch.distributed as dist
-    from autx_workload import burst_mcts_mapreduce, BASE_SEED, CONFIG_INDEX
     from paper_2502_13965_b200 import Scheduler, TraceDriver, ORDER_SELECT, ORDER_RADIX
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)   # one explicit stream for the library and the events
     torch.cuda.set_stream(stream)
     hbm_peak, peak_src = peaks()
+    wl = dict(WORKLOADS[args.workload])
+    active = args.active or wl["active"]
+    if args.policy:
+        wl["policy"] = args.policy
 
     t_gen = time.time()
     if world == 1:
-        if args.workload == "chatbot":
-            from autx_workload import chatbot
-            tr = chatbot(10_000)          # configs[1]: 10k ShareGPT-shaped programs, all active
-        elif args.workload == "react":
-            from autx_workload import react
-            tr = react(100_000)           # configs[2]: 100k BFCL-shaped programs, all active
-        else:
-            tr = burst_mcts_mapreduce(args.active, seed=BASE_SEED + CONFIG_INDEX["mcts"])
+        tr = make_trace(args.workload, active)
     else:
-        # weak scaling: one 1M-call shard per engine; every rank holds the whole (replicated)
-        # workload because Alg. 2 routes each arrival to any engine
+        # weak scaling: one shard per engine; every rank holds the whole (replicated) workload
+        # because Alg. 2 routes each arrival to any engine
         from autx_workload.gen import concat
-        tr = concat([burst_mcts_mapreduce(args.active, seed=BASE_SEED + CONFIG_INDEX["mcts"] + 1000 * r)
-                     for r in range(world)], name="mcts_mapreduce_burst_x%d" % world)
+        tr = concat([make_trace(args.workload, active, 1000 * r) for r in range(world)],
+                    name="%s_x%d" % (args.workload, world))
     t_gen = time.time() - t_gen
     lad = spec_ladder()
-    wl = {"mcts": dict(policy="atlas", max_batch=1024, kv_budget=32768),
-          "chatbot": dict(policy="plas", max_batch=256, kv_budget=6000),
-          "react": dict(policy="plas", max_batch=256, kv_budget=8000)}[args.workload]
-    if args.policy:
-        wl["policy"] = args.policy
-    s = Scheduler(policy=wl["policy"], beta=(1, 0) if os.environ.get("AUTX_BENCH_BETA_INF") else (2, 1), max_batch=wl["max_batch"], kv_budget=wl["kv_budget"], block_tokens=16,
-                  max_calls=int(args.active * 1.25) + 4096, max_programs=tr.n_programs + 1024,
+    beta = (1, 0) if args.beta == "inf" else (2, 1)
+    s = Scheduler(policy=wl["policy"], beta=beta, max_batch=wl["max_batch"], kv_budget=wl["kv_budget"],
+                  block_tokens=16, max_calls=int(active * 1.25) + 4096, max_programs=tr.n_programs + 1024,
                   order_mode=ORDER_RADIX if args.order == "radix" else ORDER_SELECT,
                   device=local, stream=stream.cuda_stream, rank=rank, nranks=world, **lad)
     if world == 1:
@@ -374,7 +400,7 @@ def main():
         b.synchronize()
         return a.elapsed_time(b), rec, nc, na
 
-    s.set_timing(False)                      # no per-kernel events inside the timed steps
+    s.set_timing(False)
     for _ in range(args.warmup):
         timed_step()
     if world > 1:
@@ -384,42 +410,30 @@ def main():
         os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_r{rank}.csv")
     clocks.start()
     from paper_2502_13965_b200.autx import kernel_launches
-    ms, decisions = [], 0
+    ms, decisions, comps, arrs, promoted = [], 0, [], [], []
     launches0 = kernel_launches()
-    chain_phase = []
-    want_chain = bool(os.environ.get("AUTX_BENCH_CHAIN"))  # with a -DAUTX_CHAIN_STAMPS build
     for _ in range(args.steps):
         dt, rec, nc, na = timed_step()
         ms.append(dt)
         decisions += rec["n_active"]
-        if want_chain:
-            chain_phase.append(s.phase_times().astype(np.int64))
+        comps.append(nc)
+        arrs.append(na)
+        promoted.append(rec["n_promoted"])
     launches = kernel_launches() - launches0  # counted by the library at every launch
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ck = clocks.stop(local)
-    # per-kernel breakdown: a separate run of steps with the library's CUDA events on
-    s.set_timing(True)
-    scan_ms, fin_ms, sel_ms, comp_ms, reg_ms = [], [], [], [], []
-    scan_bytes, promoted, phase = [], [], []
-    for _ in range(30):
-        _, rec, nc, na = timed_step()
-        tm = s.last_step_timing()
-        scan_ms.append(tm.scan_ms); sel_ms.append(tm.select_ms); fin_ms.append(tm.finalize_ms)
-        comp_ms.append(tm.complete_ms); reg_ms.append(tm.register_ms)
-        promoted.append(rec["n_promoted"])
-        phase.append(s.phase_times().astype(np.int64))
-        scan_bytes.append(SCAN_BYTES_PER_CALL * rec["n_active"] + PROMOTE_BYTES * rec["n_promoted"]
-                          + PROG_BYTES * tr.n_programs)
-    # device-side kernel spans of the undisturbed PDL chain: %globaltimer stamps (no events)
+    st = s.step_stats()                       # selection shape of the last timed step
+    # phase stamps inside the step kernel, a separate pass (the stamps add a few global stores)
     s.set_timing(False, stamps=True)
-    stamp_phase = []
+    stamp_phase, stats = [], []
     for _ in range(30):
         timed_step()
         stamp_phase.append(s.phase_times().astype(np.int64))
+        stats.append(s.step_stats())
     s.set_timing(False)
-    spans = chain_spans(stamp_phase)
+    spans = phase_spans(stamp_phase)
     total_ms = sum(ms)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -432,10 +446,10 @@ def main():
     ms_per_step = total_ms / args.steps
 
     # e2e: the same steps through the public API from the host, wall clock, no gate/flush
-    s.set_timing(False)
     e2e_dec, e2e_s, h2d, d2h, wall_s = 0, 0.0, 0, 0, 0.0
     split0 = dict(d.api_split)
-    for _ in range(min(args.steps, 100)):
+    e2e_steps = min(args.steps, 200)
+    for _ in range(e2e_steps):
         nc = len(d.pending)
         api0 = d.api_s
         t0 = time.perf_counter()
@@ -444,59 +458,57 @@ def main():
         wall_s += time.perf_counter() - t0
         e2e_s += d.api_s - api0
         e2e_dec += rec["n_active"]
-        h2d += 4 * nc + 24 * na
-        d2h += 8 * (rec["n_batch"] + rec["n_admit"] + rec["n_preempt"]) + 48
-    e2e_steps = min(args.steps, 100)
+        h2d += 8 * nc + 24 * na               # completion (slot, program row) + arrival records
+        d2h += 8 * (rec["n_batch"] + rec["n_admit"] + rec["n_preempt"]) + 4 * rec["n_batch"] + 48
     s.close()
 
-    scan_avg_ms = statistics.mean(scan_ms)
+    n_active = decisions / args.steps / world
+    n_programs = st["n_programs"]
+    algo_bytes = ALGO_BYTES_PER_CALL * n_active + ALGO_BYTES_PER_PROGRAM * n_programs
+    design_bytes = DESIGN_BYTES_PER_ROW * st["n_rows"] + DESIGN_BYTES_PER_PROGRAM * n_programs
+    achieved = algo_bytes / (ms_per_step * 1e-3) / 1e9
     traffic_bytes, traffic_src = ncu_traffic()
-    if args.workload != "mcts" or args.order != "select" or wl["policy"] != "atlas":
-        # the committed capture is of the default configuration's scan kernel only
+    if args.workload != "mcts" or args.order != "select" or wl["policy"] != "atlas" or args.beta != "2":
         traffic_bytes, traffic_src = None, "no ncu capture of this configuration"
-    achieved = statistics.mean(scan_bytes) / (scan_avg_ms * 1e-3) / 1e9
-    scan_span_us = (spans["scan"][1] - spans["scan"][0]) if spans and "scan" in spans else None
+    span_us = spans["end"] if spans else None
     result = {
         "metric": "sched decisions/s at 1M active calls", "value": value, "unit": "decisions/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
-        "config": {"workload": {"chatbot": "chatbot 10k ShareGPT-shaped programs (BASELINE configs[1])",
-                                "react": "ReAct 100k BFCL-shaped programs (BASELINE configs[2])"}.get(
-                       args.workload, "mcts_mapreduce_burst (BASELINE configs[3])") if world == 1 else
-                   "mcts_mapreduce_burst x%d engines with Alg. 2 routing (BASELINE configs[4], weak)" % world,
-                   "mean_active_calls_per_gpu": int(decisions / args.steps / world),
-                   "programs": tr.n_programs, "policy": wl["policy"], "ladder": "SPEC K=8", "beta": "2",
+        "config": {"workload": wl["desc"] if world == 1 else
+                   "%s x%d engines with Alg. 2 routing (BASELINE configs[4], weak)" % (args.workload, world),
+                   "mean_active_calls_per_gpu": int(n_active), "table_rows": st["n_rows"],
+                   "programs": n_programs, "policy": wl["policy"], "ladder": "SPEC K=8",
+                   "beta": "inf" if args.beta == "inf" else "2",
                    "max_batch": wl["max_batch"], "kv_budget_blocks": wl["kv_budget"], "fast_forward_steps": args.ff,
                    "order": args.order, "l2": "flushed before every step (512 MiB write)" if not args.no_flush else "hot",
                    "parallelism": f"engines{world} (one scheduler per GPU)"},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "k_scan_tile (dense anti-starvation + queue counts)"
-                     if args.order == "select" else "radix order (k_keys + LSD passes + k_take)",
+        "kernels_per_step": launches / args.steps,
+        "roofline": {"bound": "hbm", "kernel": "k_step (the whole step: one cooperative kernel)"
+                     if args.order == "select" else "radix order (prologue + k_keys + LSD passes + k_take + k_fin)",
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic_bytes, "traffic_source": traffic_src,
                      "peak_source": peak_src,
-                     "timing": "CUDA events around the kernel in a separate pass of 30 steps (events between "
-                               "PDL-chained kernels serialise them and add the launch latency)",
-                     "span_us": scan_span_us,
-                     "achieved_span": round(statistics.mean(scan_bytes) / (scan_span_us * 1e-6) / 1e9, 1)
-                     if scan_span_us else None,
-                     "frac_span": round(statistics.mean(scan_bytes) / (scan_span_us * 1e-6) / 1e9 / hbm_peak, 4)
-                     if scan_span_us else None,
-                     "span_source": "%globaltimer: first CTA past griddepcontrol.wait to the last CTA's end, "
-                                    "inside the undisturbed chain (30 steps, median)",
-                     "algorithmic_bytes_per_launch": int(statistics.mean(scan_bytes))},
-        "breakdown_ms": {"complete": statistics.mean(comp_ms), "register": statistics.mean(reg_ms),
-                         "scan": scan_avg_ms, "select+gather": statistics.mean(sel_ms),
-                         "finalize": statistics.mean(fin_ms),
-                         "step_p10": float(np.percentile(ms, 10)), "step_p50": float(np.percentile(ms, 50)),
-                         "step_p90": float(np.percentile(ms, 90))},
-        "promotions_per_step": statistics.mean(promoted),
-        "chain_us": chain_spans(chain_phase) if chain_phase else spans,
-        "finalize_phases_us": {n: round(float(np.median([p[b] - p[a] for p in phase])) / 1e3, 2) for n, a, b in (
-            ("loads", 0, 1), ("cutoff", 2, 3), ("batch_admit", 3, 4), ("preempt", 4, 5), ("kv", 6, 7),
-            ("account_mirror", 7, 8))},
-        "complete_phases_us": [round(float(np.median([p[i + 1] - p[i] for p in phase])) / 1e3, 2) for i in range(16, 19)],
+                     "algorithmic_bytes_per_launch": int(algo_bytes),
+                     "algorithmic_bytes": "SURVEY 8(d): 52 B per active call + 16 B per program",
+                     "timing": "CUDA events around each step's launch, L2 flushed before it (= ms_per_step)",
+                     "dominant_kernel_share": 1.0 if args.order == "select" else None,
+                     "design_bytes_per_launch": int(design_bytes),
+                     "design_bytes": "13 B per table row (qf, prog, base, mtime) + 12 B per program row",
+                     "span_us": span_us,
+                     "frac_span": round(algo_bytes / (span_us * 1e-6) / 1e9 / hbm_peak, 4) if span_us else None,
+                     "span_source": "%globaltimer: first CTA start to the end of the finalize (30 steps, median)"},
+        "step_ms": {"p10": float(np.percentile(ms, 10)), "p50": float(np.percentile(ms, 50)),
+                    "p90": float(np.percentile(ms, 90)), "mean": statistics.mean(ms)},
+        "phases_us": spans,
+        "state": {"promotions_per_step": statistics.mean(promoted),
+                  "completions_per_step": statistics.mean(comps), "arrivals_per_step": statistics.mean(arrs),
+                  "qstar": st["qstar"], "mprime": st["mprime"], "region_a": st["n_x"],
+                  "region_b_mean": statistics.mean(x["n_b"] for x in stats),
+                  "region_b_max": max(x["n_b"] for x in stats),
+                  "queue_occupancy": st["queue_counts"][:lad["K"]]},
         "e2e": {"value": e2e_dec / e2e_s, "unit": "decisions/s", "h2d_bytes_per_step": h2d // e2e_steps,
                 "d2h_bytes_per_step": d2h // e2e_steps, "ms_per_step": e2e_s * 1e3 / e2e_steps,
                 "timed": "wall clock inside the C-ABI calls (complete, end_program, register, sched_step, "
@@ -520,13 +532,17 @@ def main():
                           "config": "react (BFCL-shaped) 1000 programs, PLAS, BS=64, P=2560 blocks, 8B geometry "
                                     "(32 layers x K|V x 32 KiB chunks = 2 MiB/block)", **sw}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, per_step, wall, _ = oracle_decisions_per_s(args.active, 2, 0)
+        v, per_step, wall, _ = oracle_decisions_per_s(1_000_000, 2, 0)
         result["cpu_baseline"] = {"value": v, "unit": "decisions/s", "cores": 1, "kind": "oracle",
-                                  "sample": f"the same {args.active}-call burst, 2 steps after the setup step, "
+                                  "sample": f"the 1M-call burst of configs[3], 2 steps after the setup step, "
                                             f"{per_step:.2f} s/step single-threaded Python",
                                   "host_cores_available": os.cpu_count()}
     if rank == 0:
-        print(json.dumps(result), flush=True)
+        line = json.dumps(result)
+        print(line, flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                f.write(line + "\n")
     if world > 1:
         dist.destroy_process_group()
 

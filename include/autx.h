@@ -208,6 +208,17 @@ typedef struct {
  * sched_step, to a host array of capacity `cap`; *n receives the count. */
 autx_status autx_dump_calls(autx_ctx* ctx, autx_call_state* out, uint32_t cap, uint32_t* n);
 autx_status autx_program_state(autx_ctx* ctx, uint64_t program_id, uint32_t* svc, uint64_t* pwait);
+/* Shape of the last step's selection (select mode; radix mode reports q* = K, region B = 0):
+ * q* = the smallest queue with sum_{k<=q*} live_k >= BS (K if none), m' = rows of q* taken in
+ * table order, region A = the rows below q* plus those m' rows, region B = running calls of q*
+ * past them in the same arrival group, the table rows scanned, the live
+ * programs and the live calls per queue after anti-starvation.  Synchronises the stream. */
+typedef struct {
+  uint32_t qstar, mprime, n_x, n_b;
+  uint32_t n_rows, n_programs;
+  uint32_t queue_counts[16];
+} autx_step_stats;
+autx_status autx_step_stats(autx_ctx* ctx, autx_step_stats* out);
 /* Device-time of the kernels of the last sched_step (CUDA events around each phase). */
 typedef struct { float complete_ms, register_ms, scan_ms, select_ms, finalize_ms, total_ms; } autx_step_timing;
 autx_status autx_last_step_timing(autx_ctx* ctx, autx_step_timing* t);

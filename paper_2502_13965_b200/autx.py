@@ -65,6 +65,11 @@ class StepTiming(C.Structure):
                                            "finalize_ms", "total_ms")]
 
 
+class StepStats(C.Structure):
+    _fields_ = [(n, C.c_uint32) for n in ("qstar", "mprime", "n_x", "n_b", "n_rows", "n_programs")] + \
+               [("queue_counts", C.c_uint32 * 16)]
+
+
 CALL_DESC = np.dtype([("call_id", "<u8"), ("program_id", "<u8"), ("arrival_step", "<u4"),
                       ("program_arrival_step", "<u4"), ("input_tokens", "<u4"), ("_pad", "<u4")])
 CALL_STATE = np.dtype([("call_id", "<u8"), ("q", "<u4"), ("quanta", "<u4"), ("wait", "<u4"),
@@ -105,6 +110,7 @@ def load_library(path=LIB_PATH):
         "autx_dump_calls": ([P, P, u32, C.POINTER(u32)], i32),
         "autx_program_state": ([P, u64, C.POINTER(u32), C.POINTER(u64)], i32),
         "autx_last_step_timing": ([P, C.POINTER(StepTiming)], i32),
+        "autx_step_stats": ([P, C.POINTER(StepStats)], i32),
         "autx_set_timing": ([P, i32], i32),
         "autx_num_active": ([P], u32),
         "autx_phase_times": ([P, P, u32], i32),
@@ -124,7 +130,7 @@ def exported_symbols():
         "autx_end_program", "autx_complete", "autx_register_call", "autx_register_call_dag", "autx_sched_step",
         "autx_step_wait", "autx_kv_swap", "autx_block_table", "autx_block_table_host", "autx_route_record_bytes",
         "autx_route_pack", "autx_route_apply", "autx_dump_calls", "autx_program_state",
-        "autx_last_step_timing", "autx_set_timing", "autx_num_active", "autx_phase_times", "autx_kernel_launches"]
+        "autx_last_step_timing", "autx_step_stats", "autx_set_timing", "autx_num_active", "autx_phase_times", "autx_kernel_launches"]
 
 
 def kernel_launches():
@@ -285,9 +291,17 @@ class Scheduler:
         self._check(self.lib.autx_program_state(self.ctx, int(pid), C.byref(s), C.byref(w)))
         return s.value, w.value
 
+    def step_stats(self):
+        """Selection shape of the last step: q*, m', region A / B sizes, rows, programs, queues."""
+        st = StepStats()
+        self._check(self.lib.autx_step_stats(self.ctx, C.byref(st)))
+        d = {n: int(getattr(st, n)) for n, _ in StepStats._fields_[:6]}
+        d["queue_counts"] = [int(x) for x in st.queue_counts]
+        return d
+
     def set_timing(self, on=True, stamps=False):
-        """on: CUDA events around the step's kernels; stamps: %globaltimer chain stamps instead
-        (no events, so the PDL chain runs as in untimed steps; read with phase_times())."""
+        """on: CUDA events around the step's kernels; stamps: %globaltimer phase stamps inside
+        the step kernel instead (read with phase_times())."""
         self._check(self.lib.autx_set_timing(self.ctx, (1 if on else 0) | (2 if stamps else 0)))
 
     def last_step_timing(self):

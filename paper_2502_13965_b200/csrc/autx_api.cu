@@ -1071,6 +1071,30 @@ extern "C" autx_status autx_program_state(autx_ctx* ctx, uint64_t pid, uint32_t*
   return AUTX_OK;
 }
 
+extern "C" autx_status autx_step_stats(autx_ctx* ctx, autx_step_stats* o) {
+  if (!ctx || !o) return AUTX_E_INVAL;
+  autx_status s = sync_last(ctx);
+  if (s) return s;
+  CK(cudaStreamSynchronize(ctx->stream));
+  Ctl c;
+  CK(cudaMemcpy(&c, ctx->ctl, sizeof c, cudaMemcpyDeviceToHost));
+  memset(o, 0, sizeof *o);
+  o->qstar = c.qstar;
+  o->mprime = c.mprime;
+  o->n_x = c.n_x;
+  o->n_b = c.n_b;
+  o->n_rows = ctx->tail;
+  o->n_programs = (uint32_t)ctx->prog_row.size();
+  if (!ctx->radix && ctx->stepped) {
+    const uint32_t ntiles = std::max<uint32_t>(1, (ctx->tail + TILE - 1) / TILE);
+    std::vector<uint32_t> cnt((size_t)ntiles * MAX_K);
+    CK(cudaMemcpy(cnt.data(), ctx->out.tile_cnt, cnt.size() * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t t = 0; t < ntiles; ++t)
+      for (int k = 0; k < MAX_K; ++k) o->queue_counts[k] += cnt[(size_t)t * MAX_K + k];
+  }
+  return AUTX_OK;
+}
+
 extern "C" autx_status autx_last_step_timing(autx_ctx* ctx, autx_step_timing* t) {
   if (!ctx || !t) return AUTX_E_INVAL;
   *t = ctx->last_timing;

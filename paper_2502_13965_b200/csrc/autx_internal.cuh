@@ -91,6 +91,7 @@ struct Ctl {
   uint32_t rs_free_top;    // resident-slot free stack size
   uint32_t host_bump;      // host arena bump pointer (pages)
   uint32_t bnd_slot, bnd_arr;  // region A's last row of q* (slot, arrival): published by its tile
+  uint32_t n_b;                // region B size of the last step (finalize; autx_step_stats)
   uint32_t host_free_top[32];  // per size class free-stack size
   // step-kernel synchronisation, one 128-B line each: the prologue's completion (step seqno) and
   // the two grid barriers (arrival counts, reset by the finalize CTA at the end of the step)

@@ -757,7 +757,7 @@ constexpr size_t fin_smem_bytes() {
 }
 
 template <int I>
-__device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs, uint32_t nx, uint32_t n_live,
+__device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs, uint32_t mp, uint32_t nx, uint32_t n_live,
                               uint32_t n_promo, const uint32_t (&p_slot)[I / 2], uint32_t n_prev, bool wait2,
                               unsigned long long* red64, uint32_t* red32) {
   constexpr int NT = ST_THREADS, IP = I / 2, C = NT * I;
@@ -1161,6 +1161,10 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   // ---- (9) host record, host mirrors, counters reset for the next step ------------------------
   if (tid == 0) {
     ctl->n_prev = n_batch;
+    ctl->qstar = qs;
+    ctl->mprime = mp;
+    ctl->n_x = nx;
+    ctl->n_b = n_b;
     HostOut h;
     h.n_batch = n_batch;
     h.n_admit = n_admit;
@@ -1270,8 +1274,8 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
     grid_wait(&ctl->bar1, gridDim.x);
     if (stamps && tid == 0) ctl->dbg[43] = globaltimer();
     select_for(a, NONE, S);
-    const uint32_t qs = S.qs, nx = S.nx, n_live = S.n_live, n_promo = S.n_promo;
-    finalize_core<I>(a, dsm, qs, nx, n_live, n_promo, p_slot, n_prev, true, red64, red32);
+    const uint32_t qs = S.qs, mp = S.m, nx = S.nx, n_live = S.n_live, n_promo = S.n_promo;
+    finalize_core<I>(a, dsm, qs, mp, nx, n_live, n_promo, p_slot, n_prev, true, red64, red32);
     return;
   }
   // ---- tile CTA ----
@@ -1334,7 +1338,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_fin(const __grid_constant__ Step
     const uint32_t j = tid * IP + r;
     p_slot[r] = j < n_prev ? a.out.prev_slots[j] : NONE;
   }
-  finalize_core<I>(a, dsm, a.pol.K, ctl->n_x, ctl->n_live, ctl->n_promoted, p_slot, n_prev, false, red64, red32);
+  finalize_core<I>(a, dsm, a.pol.K, 0u, ctl->n_x, ctl->n_live, ctl->n_promoted, p_slot, n_prev, false, red64, red32);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -1,0 +1,26 @@
+#!/bin/bash
+# Bench runs on one B200.  BENCHES: space-separated list of name=args (args with + for spaces);
+# default: the headline only.  Results: gpurun_out/r02/<name>.json (+ .err).
+mkdir -p gpurun_out/r02
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r02/build.log 2>&1 || { tail -20 gpurun_out/r02/build.log; exit 1; }
+BENCHES=${BENCHES:-"headline=--no-swap+--no-cpu-baseline"}
+for b in $BENCHES; do
+  name=${b%%=*}; a=${b#*=}; a=${a//+/ }
+  timeout ${BENCH_TIMEOUT:-900} python bench.py $a --json-out gpurun_out/r02/$name.json > gpurun_out/r02/$name.out 2> gpurun_out/r02/$name.err
+  echo "== $name rc=$?"
+  python - "$name" <<'PY'
+import json, sys
+n = sys.argv[1]
+try:
+    d = json.loads(open(f"gpurun_out/r02/{n}.json").read())
+except Exception as e:
+    print("no json:", e); print(open(f"gpurun_out/r02/{n}.err").read()[-3000:]); sys.exit(0)
+r = d.get("roofline", {})
+print(n, "value %.3e" % d["value"], "ms/step %.2f us" % (d["ms_per_step"] * 1e3), "frac", r.get("frac"),
+      "e2e %.3e" % d["e2e"]["value"], "e2e us %.1f" % (d["e2e"]["ms_per_step"] * 1e3), "launches/step", d.get("kernels_per_step"))
+print("  step_ms", d.get("step_ms"))
+print("  phases", d.get("phases_us"))
+print("  state", d.get("state"))
+print("  api", d["e2e"].get("api_us_per_step"), "clocks", d.get("clocks"))
+PY
+done
