@@ -217,8 +217,8 @@ typedef struct {
   uint32_t qstar, mprime, n_x, n_b;
   uint32_t n_rows, n_programs;
   uint32_t queue_counts[16];
-} autx_step_stats;
-autx_status autx_step_stats(autx_ctx* ctx, autx_step_stats* out);
+} autx_selection_stats;
+autx_status autx_step_stats(autx_ctx* ctx, autx_selection_stats* out);
 /* Device-time of the kernels of the last sched_step (CUDA events around each phase). */
 typedef struct { float complete_ms, register_ms, scan_ms, select_ms, finalize_ms, total_ms; } autx_step_timing;
 autx_status autx_last_step_timing(autx_ctx* ctx, autx_step_timing* t);

@@ -1071,7 +1071,7 @@ extern "C" autx_status autx_program_state(autx_ctx* ctx, uint64_t pid, uint32_t*
   return AUTX_OK;
 }
 
-extern "C" autx_status autx_step_stats(autx_ctx* ctx, autx_step_stats* o) {
+extern "C" autx_status autx_step_stats(autx_ctx* ctx, autx_selection_stats* o) {
   if (!ctx || !o) return AUTX_E_INVAL;
   autx_status s = sync_last(ctx);
   if (s) return s;

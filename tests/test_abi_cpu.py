@@ -46,7 +46,7 @@ def test_struct_layout_matches_header(tmp_path, lib):
     c = tmp_path / "sz.c"
     c.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "autx.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\\n",'
                  'sizeof(autx_config), sizeof(autx_call_desc), sizeof(autx_step_out), sizeof(autx_kv_layout),'
-                 'sizeof(autx_swap_stats), sizeof(autx_call_state), sizeof(autx_step_timing), offsetof(autx_config, stream), sizeof(autx_step_stats));return 0;}\n')
+                 'sizeof(autx_swap_stats), sizeof(autx_call_state), sizeof(autx_step_timing), offsetof(autx_config, stream), sizeof(autx_selection_stats));return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.dirname(HEADER), str(c), "-o", str(exe)])
     got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
