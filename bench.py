@@ -97,8 +97,10 @@ def make_trace(name, active, seed_off=0):
     return churn(active, seed=BASE_SEED + 100 + seed_off)
 
 
-PHASES = [("first_cta_start", 40), ("last_cta_start", 41), ("prologue_done", 42), ("last_tile_at_barrier1", 48),
-          ("barrier1_passed", 43), ("barrier2_passed", 44), ("finalize_loads", 45), ("order_cutoff", 46),
+PHASES = [("first_cta_start", 40), ("last_cta_start", 41), ("prologue_completions", 57), ("prologue_done", 42),
+          ("last_tile_at_barrier1", 48), ("barrier1_passed", 43), ("tile0_selection", 54), ("tile0_extraction", 55),
+          ("last_tile_at_barrier2", 56), ("barrier2_passed", 44), ("finalize_loads", 49), ("region_b", 45),
+          ("key_order", 50), ("cutoff", 46), ("batch_admit", 51), ("preempt", 52), ("accounting_kv", 53),
           ("end", 47)]
 
 
@@ -107,7 +109,7 @@ def phase_spans(phase):
     %globaltimer stamps of the last step (autx_phase_times [64, 80))."""
     rows = []
     for p in phase:
-        c = [int(x) for x in p[64:80]]
+        c = [int(x) for x in p[64:88]]
         if not c[0] or c[0] == (1 << 64) - 1 or not c[7]:
             continue
         rows.append({n: (c[i - 40] - c[0]) / 1e3 for n, i in PHASES if c[i - 40]})

@@ -257,7 +257,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 // shared memory for the records (the finalize's area, unused until the prologue is over).
 // ---------------------------------------------------------------------------------------------
 template <int NT>
-__device__ void prologue_body(const StepArgs& a, unsigned char* scratch) {
+__device__ void prologue_body(const StepArgs& a, unsigned char* scratch, bool stamps = false) {
   const PrologueArgs& p = a.pro;
   const Policy& pol = a.pol;
   CallTable ct = a.ct;
@@ -286,6 +286,7 @@ __device__ void prologue_body(const StepArgs& a, unsigned char* scratch) {
       complete_body<NT>(pol, ct, pt, ctl, s_comp, p.n_comp, p.t, kv, a.kv_on, a.rec_out, true, s_rec,
                         eq2 ? p.comp_lin : nullptr);
     __syncthreads();
+    if (stamps && tid == 0) ctl->dbg[57] = globaltimer();
     if (my_arr) {
       const ArrivalRec r = s_arr[tid];
       uint32_t inh = 0;
@@ -838,6 +839,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   }
   uint32_t n_b;
   uint32_t ob = block_excl_scan<uint32_t, NT>(nbm, red32, &n_b);
+  if (stamps && tid == 0) ctl->dbg[49] = globaltimer();
 #pragma unroll
   for (int r = 0; r < IP; ++r)
     if ((isb >> r) & 1u) hb[ob++] = p_slot[r];
@@ -904,6 +906,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
     }
   }
   __syncthreads();
+  if (stamps && tid == 0) ctl->dbg[50] = globaltimer();
   // ---- (4) cutoff (Alg. 1 l.34-37): kvb >= 1 makes the inclusive prefix strictly increasing,
   // so "count <= BS and sum kvb <= P" holds exactly on a prefix (n_batch = last fitting + 1) ----
   const uint32_t nc = min(n, BS);
@@ -971,6 +974,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
       }
     }
   }
+  if (stamps && tid == 0) ctl->dbg[51] = globaltimer();
   const uint32_t n_admit = (uint32_t)(ad_tot >> 44);
   const unsigned long long swap_in = ad_tot & ((1ull << 44) - 1);
   // ---- (6) preempt = previous batch, still active, not in the batch (previous-batch order) ---
@@ -998,6 +1002,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
         ++pos;
       }
   }
+  if (stamps && tid == 0) ctl->dbg[52] = globaltimer();
   const uint32_t n_preempt = (uint32_t)(pre_tot >> 44);
   const unsigned long long swap_out = pre_tot & ((1ull << 44) - 1);
   // ---- (7) KV blocks: swap plan + allocation (a7) ---------------------------------------------
@@ -1158,6 +1163,10 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
       out.prev_slots[p] = sl;
     }
   }
+  if (stamps) {
+    __syncthreads();
+    if (tid == 0) ctl->dbg[53] = globaltimer();
+  }
   // ---- (9) host record, host mirrors, counters reset for the next step ------------------------
   if (tid == 0) {
     ctl->n_prev = n_batch;
@@ -1212,7 +1221,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   }
   if (stamps && tid == 0) {
     ctl->dbg[47] = globaltimer();
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 24; ++i) {
       ctl->dbg[64 + i] = ctl->dbg[40 + i];
       ctl->dbg[40 + i] = 0;
     }
@@ -1228,8 +1237,10 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
 //     the deferred rows wait for; barrier 1; selection; the previous batch's slots; barrier 2;
 //     order, cutoff, lists, accounting, KV plan (a5, a6, a3, a7).
 // Stamps (dbg): 40 first CTA start, 41 last CTA start, 42 prologue done, 43 barrier 1 passed,
-// 44 barrier 2 passed, 45 finalize loads, 46 order + cutoff, 47 end, 48 last tile CTA at
-// barrier 1 (all but 40/41/48 by the finalize CTA).
+// 44 barrier 2 passed, 45 region B placed, 46 cutoff, 47 end, 48 last tile CTA at barrier 1,
+// 49 finalize loads consumed, 50 key order, 51 batch + admit lists, 52 preempt list,
+// 53 accounting (+ KV plan), 54 / 55 tile 0 selection / extraction done, 56 last tile CTA at
+// barrier 2, 57 prologue completions applied.
 // ---------------------------------------------------------------------------------------------
 template <int I>
 __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ StepArgs a) {
@@ -1249,7 +1260,7 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
   }
   if (blockIdx.x == a.n_tile_ctas) {
     // ---- prologue + finalize CTA ----
-    if (a.do_pro) prologue_body<ST_THREADS>(a, dsm);
+    if (a.do_pro) prologue_body<ST_THREADS>(a, dsm, stamps);
     __syncthreads();
     if (tid == 0) {
       __threadfence();
@@ -1304,6 +1315,7 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
   grid_wait(&ctl->bar1, gridDim.x);
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
     select_for(a, tile, S);
+    if (stamps && tid == 0 && tile == 0) ctl->dbg[54] = globaltimer();
     if (S.has) {
       if (tile != last) {
         // an earlier tile of this CTA: its flags after the pass, from L2
@@ -1317,8 +1329,10 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
       extract_tile(a, tile, qw, S, red64);
     }
     __syncthreads();  // S reuse
+    if (stamps && tid == 0 && tile == 0) ctl->dbg[55] = globaltimer();
   }
   grid_arrive(&ctl->bar2);
+  if (stamps && tid == 0) atomicMax(&ctl->dbg[56], globaltimer());
 }
 
 // Radix mode: the finalize alone (one CTA) on the sorted candidates k_take wrote (q* = K: no
