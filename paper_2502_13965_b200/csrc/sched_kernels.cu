@@ -566,7 +566,7 @@ struct SelSmem {
   uint32_t qs, m, nx, has, n_promo, n_live;
 };
 
-__device__ __noinline__ void select_for(const StepArgs& a, uint32_t tile, SelSmem& S) {
+__device__ void select_for(const StepArgs& a, uint32_t tile, SelSmem& S) {
   constexpr int NG = ST_THREADS / MAX_K;  // 32 groups
   const uint32_t tid = threadIdx.x, h = tid / MAX_K, k = tid % MAX_K;
   const uint32_t K = a.pol.K, BS = a.pol.max_batch;
@@ -639,8 +639,8 @@ __device__ __noinline__ void select_for(const StepArgs& a, uint32_t tile, SelSme
 // Region A rows of one tile -> out.xrec at their (queue, seq) positions; the tile holding the
 // m'-th row of q* publishes it (region A's boundary).  Ranks inside the tile: one block scan per
 // word of 4 queues (16-bit fields), over the queues <= q*.
-__device__ __noinline__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&qw)[2], const SelSmem& S,
-                             unsigned long long* red64, bool dry = false) {
+__device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&qw)[2], const SelSmem& S,
+                             unsigned long long* red64) {
   const uint32_t tid = threadIdx.x, K = a.pol.K;
   const uint32_t qs = S.qs, m = S.m;
   const uint32_t qmax = min(qs, K - 1);
@@ -673,7 +673,6 @@ __device__ __noinline__ void extract_tile(const StepArgs& a, uint32_t tile, cons
       }
     }
   }
-  if (dry) sel = row0 < a.n_rows ? 0xFFu : 0u;  // every row's code path, nothing stored
   if (!sel) return;
   const CallTable& ct = a.ct;
   CandRec* xrec = a.out.xrec;
@@ -699,13 +698,9 @@ __device__ __noinline__ void extract_tile(const StepArgs& a, uint32_t tile, cons
       const uint32_t arr = lane4(ar, k);
       const uint32_t pos = (pos2[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
       uint4* dst = reinterpret_cast<uint4*>(xrec + pos);
-      const uint4 v0 = make_uint4(k & 1 ? cc.z : cc.x, k & 1 ? cc.w : cc.y, r4 + k, arr);
-      const uint4 v1 = make_uint4(lane4(tk, k), lane4(ex, k), lane4(mt, k), lane4(qt, k));
-      const uint4 v2 = make_uint4(qf | ((qf & QF_RUN) ? lane4(bd, k) << 8 : 0u), 0u, 0u, 0u);
-      if (dry) continue;
-      dst[0] = v0;
-      dst[1] = v1;
-      dst[2] = v2;
+      dst[0] = make_uint4(k & 1 ? cc.z : cc.x, k & 1 ? cc.w : cc.y, r4 + k, arr);
+      dst[1] = make_uint4(lane4(tk, k), lane4(ex, k), lane4(mt, k), lane4(qt, k));
+      dst[2] = make_uint4(qf | ((qf & QF_RUN) ? lane4(bd, k) << 8 : 0u), 0u, 0u, 0u);
       if ((bnd >> j) & 1u) {
         a.ctl->bnd_slot = r4 + k;
         a.ctl->bnd_arr = arr;
@@ -762,11 +757,10 @@ constexpr size_t fin_smem_bytes() {
   return (size_t)ST_THREADS * I * 48 + (size_t)ST_THREADS * I / 2;
 }
 
-// (__noinline__: one copy of the code serves the dry and the real pass)
 template <int I>
-__device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs, uint32_t mp, uint32_t nx, uint32_t n_live,
+__device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs, uint32_t mp, uint32_t nx, uint32_t n_live,
                               uint32_t n_promo, const uint32_t (&p_slot)[I / 2], uint32_t n_prev, bool wait2,
-                              unsigned long long* red64, uint32_t* red32, bool dry = false) {
+                              unsigned long long* red64, uint32_t* red32) {
   constexpr int NT = ST_THREADS, IP = I / 2, C = NT * I;
   const Policy& pol = a.pol;
   const CallTable& ct = a.ct;
@@ -791,9 +785,7 @@ __device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm
   __shared__ unsigned long long s_kvsum;
   __shared__ HostOut s_hout;
   const uint32_t tid = threadIdx.x, BS = pol.max_batch, K = pol.K;
-  // dry: the same code path with every global store, atomic and the KV plan skipped, so that the
-  // finalize CTA can pull its instructions into the caches while it waits (k_step)
-  const bool stamps = STAMPS_ON(pol) && !dry;
+  const bool stamps = STAMPS_ON(pol);
   if (wait2) grid_wait(&ctl->bar2, a.n_tile_ctas);
   if (stamps && tid == 0) ctl->dbg[44] = globaltimer();
   // ---- (1) one round of loads: region A records, the previous batch's rows, the boundary -----
@@ -938,11 +930,11 @@ __device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm
     const uint32_t p = tid * I + r;
     incl += kvb[r];
     inc[r] = incl;
-    if (p < nc && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) atomicMax(&s_nbatch, p + 1);  // (smem)
+    if (p < nc && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) atomicMax(&s_nbatch, p + 1);
   }
   __syncthreads();
   const uint32_t n_batch = s_nbatch;
-  if (!dry && tid == 0 && nc > 0 && n_batch == 0) set_err(ctl, AUTX_E_NOMEM, y_slot[z[0]]);
+  if (tid == 0 && nc > 0 && n_batch == 0) set_err(ctl, AUTX_E_NOMEM, y_slot[z[0]]);
   if (stamps && tid == 0) ctl->dbg[46] = globaltimer();
   // ---- (5) batch list, admit = batch calls not resident (batch order), previous-batch marks ---
   unsigned long long my_ad = 0;
@@ -954,11 +946,9 @@ __device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm
       const uint32_t i = z[p];
       const uint32_t qfb = y_qfb[i];
       if (p + 1 == n_batch) s_kvsum = inc[r];
-      if (!dry) {
-        out.batch_slots[p] = y_slot[i];
-        out.batch_ids[p] = y_cid[i];
-      }
-      if (qfb & QF_RUN) inb[min(qfb >> 8, (uint32_t)C / 2 - 1)] = 1;
+      out.batch_slots[p] = y_slot[i];
+      out.batch_ids[p] = y_cid[i];
+      if (qfb & QF_RUN) inb[qfb >> 8] = 1;
       if (!(qfb & QF_RES)) {
         const uint32_t e = y_exec[i];
         const uint64_t held = e > 0 ? blocks_for(pol, y_tok[i] + e) : 0u;  // R28
@@ -976,10 +966,8 @@ __device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm
       if (p < n_batch) {
         const uint32_t i = z[p];
         if (!(y_qfb[i] & QF_RES)) {
-          if (!dry) {
-            out.admit_ids[pos] = y_cid[i];
-            out.admit_slots[pos] = y_slot[i];
-          }
+          out.admit_ids[pos] = y_cid[i];
+          out.admit_slots[pos] = y_slot[i];
           s_ad[pos] = y_cid[i];
           ++pos;
         }
@@ -1007,12 +995,10 @@ __device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm
 #pragma unroll
     for (int r = 0; r < IP; ++r)
       if ((is_pre >> r) & 1u) {
+        out.preempt_ids[pos] = p_cid[r];
         s_pr[pos] = p_cid[r];
-        if (!dry) {
-          out.preempt_ids[pos] = p_cid[r];
-          out.preempt_slots[pos] = p_slot[r];
-          ct.qf[p_slot[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
-        }
+        out.preempt_slots[pos] = p_slot[r];
+        ct.qf[p_slot[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
         ++pos;
       }
   }
@@ -1020,7 +1006,7 @@ __device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm
   const uint32_t n_preempt = (uint32_t)(pre_tot >> 44);
   const unsigned long long swap_out = pre_tot & ((1ull << 44) - 1);
   // ---- (7) KV blocks: swap plan + allocation (a7) ---------------------------------------------
-  if (a.kv_on && !dry) {
+  if (a.kv_on) {
     __syncthreads();  // preempt_slots
     const uint32_t W = pol.max_blocks_per_call;
     // (7a) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots
@@ -1158,7 +1144,7 @@ __device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm
 #pragma unroll
   for (int r = 0; r < I; ++r) {
     const uint32_t p = tid * I + r;
-    if (p < n_batch && !dry) {
+    if (p < n_batch) {
       const uint32_t i = z[p];
       const uint32_t sl = y_slot[i];
       uint32_t q = y_qfb[i] & QF_QMASK, qt = y_qt[i];
@@ -1182,7 +1168,7 @@ __device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm
     if (tid == 0) ctl->dbg[53] = globaltimer();
   }
   // ---- (9) host record, host mirrors, counters reset for the next step ------------------------
-  if (tid == 0 && !dry) {
+  if (tid == 0) {
     ctl->n_prev = n_batch;
     ctl->qstar = qs;
     ctl->mprime = mp;
@@ -1206,41 +1192,32 @@ __device__ __noinline__ void finalize_core(const StepArgs& a, unsigned char* dsm
     ctl->bar2 = 0;
     s_hout = h;
   }
-  if (!dry) {
-    for (uint32_t i = tid; i < QP_LINES * 32; i += NT) (&ctl->qpart[0][0])[i] = 0;
-    for (uint32_t i = tid; i < out.n_sup * MAX_K; i += NT) out.sup_cnt[i] = 0;
-  }
+  for (uint32_t i = tid; i < QP_LINES * 32; i += NT) (&ctl->qpart[0][0])[i] = 0;
+  for (uint32_t i = tid; i < out.n_sup * MAX_K; i += NT) out.sup_cnt[i] = 0;
   __syncthreads();
   if (!out.zero_copy) {
-    if (tid == 0 && !dry) *out.d_hout = s_hout;
+    if (tid == 0) *out.d_hout = s_hout;
   } else {
     // 16-B posted stores over PCIe: pairs of batch ids, groups of 4 slots, admit/preempt ids from
     // their shared-memory copies
     const uint32_t nb = n_batch;
     for (uint32_t k = tid; k < (nb + 1) / 2; k += NT) {
       const uint64_t c0 = y_cid[z[2 * k]], c1 = 2 * k + 1 < nb ? y_cid[z[2 * k + 1]] : 0ull;
-      const uint4 v = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)c1, (uint32_t)(c1 >> 32));
-      if (!dry) reinterpret_cast<uint4*>(out.h_batch)[k] = v;
+      reinterpret_cast<uint4*>(out.h_batch)[k] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)c1, (uint32_t)(c1 >> 32));
     }
     for (uint32_t k = tid; k < (nb + 3) / 4; k += NT) {
       uint32_t v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) v[u] = 4 * k + u < nb ? y_slot[z[4 * k + u]] : 0u;
-      if (!dry) reinterpret_cast<uint4*>(out.h_batch_slots)[k] = make_uint4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<uint4*>(out.h_batch_slots)[k] = make_uint4(v[0], v[1], v[2], v[3]);
     }
     const uint4* sa = reinterpret_cast<const uint4*>(s_ad);
     const uint4* sp = reinterpret_cast<const uint4*>(s_pr);
-    for (uint32_t i = tid; i < (n_admit + 1) / 2; i += NT) {
-      const uint4 v = sa[i];
-      if (!dry) reinterpret_cast<uint4*>(out.h_admit)[i] = v;
-    }
-    for (uint32_t i = tid; i < (n_preempt + 1) / 2; i += NT) {
-      const uint4 v = sp[i];
-      if (!dry) reinterpret_cast<uint4*>(out.h_preempt)[i] = v;
-    }
+    for (uint32_t i = tid; i < (n_admit + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_admit)[i] = sa[i];
+    for (uint32_t i = tid; i < (n_preempt + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_preempt)[i] = sp[i];
     __syncthreads();
     // the host reads after the stream event that follows this kernel, which orders every store
-    if (tid == 0 && !dry) *out.hout = s_hout;
+    if (tid == 0) *out.hout = s_hout;
   }
   if (stamps && tid == 0) {
     ctl->dbg[47] = globaltimer();
@@ -1305,16 +1282,6 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
       }
     }
     grid_arrive(&ctl->bar1);
-    {
-      // while the tiles run: the selection and the whole finalize once without side effects, so
-      // that their code is in the instruction caches (and L2) when the real pass runs; the step's
-      // single-CTA phases are otherwise dominated by instruction fetch (ncu: no_instruction)
-      select_for(a, NONE, S);
-      uint32_t z_slot[IP];
-#pragma unroll
-      for (int r = 0; r < IP; ++r) z_slot[r] = 0;
-      finalize_core<I>(a, dsm, 0u, 1u, a.pol.max_batch, 0u, 0u, z_slot, a.pol.max_batch, false, red64, red32, true);
-    }
     grid_wait(&ctl->bar1, gridDim.x);
     if (stamps && tid == 0) ctl->dbg[43] = globaltimer();
     select_for(a, NONE, S);
@@ -1345,13 +1312,6 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
   }
   grid_arrive(&ctl->bar1);
   if (stamps && tid == 0) atomicMax(&ctl->dbg[48], globaltimer());
-  // while the other tiles finish: the selection and the extraction once without side effects
-  // (instruction caches, see the finalize CTA)
-  if (last != NONE) {
-    select_for(a, last, S);
-    extract_tile(a, last, qw, S, red64, true);
-    __syncthreads();
-  }
   grid_wait(&ctl->bar1, gridDim.x);
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
     select_for(a, tile, S);
