@@ -190,6 +190,7 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   o.batch_slots = reinterpret_cast<uint32_t*>(o.preempt_ids + BSp);
   CK(dalloc(&o.admit_slots, BS));
   CK(dalloc(&o.xrec, BS));
+  CK(dalloc(&o.prev_rec, BS));
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K));
   CK(dalloc(&o.sup_cnt, (ntiles / SUP_TILES + 1) * MAX_K));
   CK(cudaMemsetAsync(o.sup_cnt, 0, (ntiles / SUP_TILES + 1) * MAX_K * sizeof(uint32_t), ctx->stream));
@@ -347,7 +348,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
                  t.loc, t.hcls, t.bidx, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
                  ctx->ctl, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
-                 ctx->out.admit_slots, ctx->out.xrec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
+                 ctx->out.admit_slots, ctx->out.xrec, ctx->out.prev_rec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
                  ctx->kv.bt_offsets, ctx->kv.bt_blocks, ctx->d_pools, ctx->staging,
@@ -474,7 +475,7 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
     if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
     CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
     CK(launch_complete(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->h_cslots, n, t, ctx->kv,
-                       ctx->kv_on, recs, false));
+                       ctx->kv_on, recs, false, ctx->out.prev_rec));
     if (ctx->timing) {
       cudaEventRecord(ctx->ev[5], ctx->stream);
       ctx->timed_complete = true;
@@ -529,6 +530,8 @@ static void stage_prologue(autx_ctx* ctx, StepArgs& a, uint32_t t, bool with_arr
   static const bool force_defer = getenv("AUTX_DEFER_ALL") != nullptr;
   a.defer_all = (p.n_comp > (uint32_t)PRO_INLINE || force_defer) ? 1u : 0u;
   a.first_new = p.n_arr ? p.first_slot : NONE;
+  static const bool pro_first = getenv("AUTX_PRO_FIRST") != nullptr;  // A/B switch
+  a.pro_first = (pro_first && a.do_pro && !a.defer_all) ? 1u : 0u;
 }
 
 static void clear_staged(autx_ctx* ctx) {

@@ -96,6 +96,7 @@ struct Ctl {
   // step-kernel synchronisation, one 128-B line each: the prologue's completion (step seqno) and
   // the two grid barriers (arrival counts, reset by the finalize CTA at the end of the step)
   alignas(128) uint32_t pro_seq;
+  alignas(128) uint32_t go_seq;   // AUTX_PRO_FIRST: the prologue's loads are issued (tiles may stream)
   alignas(128) uint32_t bar1;
   alignas(128) uint32_t bar2;
   // scan partial totals over QP_LINES 128-B lines (CTA b adds into line b % QP_LINES: same-address
@@ -154,6 +155,9 @@ struct Outputs {
   uint32_t* preempt_slots;   // [max_batch]
   uint32_t* admit_slots;     // [max_batch]
   CandRec* xrec;             // [max_batch] region A in (queue, seq) order
+  CandRec* prev_rec;         // [max_batch] the previous batch's rows by previous-batch index: written by
+                             // the tiles owning them (live rows, after the dense pass) and by the
+                             // prologue (completed rows: qfb = QF_DEAD)
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K] live rows per (tile, queue) after anti-starvation
   uint32_t* sup_cnt;         // [ceil(ntiles_cap / SUP_TILES) * MAX_K] per-queue counts of super-tiles
                              // (scan: atomics; selection: prefix; finalize: reset)
@@ -262,13 +266,14 @@ struct StepArgs {
   uint32_t first_new;   // first row registered by this step's prologue (rows below are older)
   uint32_t defer_all;   // the prologue's records are not inline: every row waits for it
   uint32_t do_pro;      // the step has a prologue (completions or arrivals)
+  uint32_t pro_first;   // the tiles start streaming only once the prologue's loads are issued
   PrologueArgs pro;
 };
 
 // ---- kernel launchers (sched_kernels.cu / swap_kernels.cu / radix_kernels.cu) ---------------
 cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                             const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
-                            CompRec* rec_out, bool apply);
+                            CompRec* rec_out, bool apply, CandRec* prev_rec);
 // The step prologue (a1, a2) as its own kernel (radix mode, bulk bursts, before a compaction).
 cudaError_t launch_prologue(cudaStream_t s, const StepArgs& a);
 cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,

@@ -27,7 +27,7 @@ constexpr int RX_WARP_KEYS = 32 * RX_ITEMS;      // 512 keys per warp, contiguou
 
 __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                      RadixState rx, uint32_t t, uint32_t n_rows,
-                                                     uint32_t arr_base) {
+                                                     uint32_t arr_base, CandRec* prev_rec) {
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += RX_THREADS) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -40,8 +40,9 @@ __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, P
       if (!(qf & QF_DEAD)) {
         ++nlive;
         uint32_t q = qf & QF_QMASK;
+        uint32_t mt_now = ct.mtime[r], qt_now = ct.quanta[r];
         if (pol.beta_den != 0) {
-          uint32_t p = ct.prog[r], b = ct.base[r], m = ct.mtime[r];
+          uint32_t p = ct.prog[r], b = ct.base[r], m = mt_now;
           const PInfo pi = pt.info[p];
           uint64_t W = pi.pwait + (uint64_t)(t - b - m);
           uint64_t T = (uint64_t)pi.svc + m;
@@ -51,8 +52,19 @@ __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, P
             ct.base[r] = t;
             ct.mtime[r] = 0;
             ct.quanta[r] = pol.quanta[0];
+            mt_now = 0;
+            qt_now = pol.quanta[0];
+            qf &= ~QF_QMASK;
             ++npromo;
           }
+        }
+        if (qf & QF_RUN) {  // ran in the previous step: its record for the finalize (prev_rec)
+          const uint32_t bx = ct.bidx[r];
+          const unsigned long long cid = ct.cid[r];
+          uint4* dst = reinterpret_cast<uint4*>(prev_rec + bx);
+          dst[0] = make_uint4((uint32_t)cid, (uint32_t)(cid >> 32), r, ct.arr[r]);
+          dst[1] = make_uint4(ct.tok[r], ct.exec[r], mt_now, qt_now);
+          dst[2] = make_uint4(qf | (bx << 8), 0u, 0u, 0u);
         }
         uint64_t arel = (uint64_t)(ct.arr[r] - arr_base) & ((1u << 27) - 1);
         key = ((uint64_t)q << 60) | (arel << 33) | ((uint64_t)((qf & QF_RUN) ? 0u : 1u) << 32) | r;
@@ -181,7 +193,7 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
   cudaMemsetAsync(rx.dig_hist, 0, 4 * 256 * sizeof(uint32_t), s);
   uint32_t grid = std::min<uint32_t>(ntiles * RX_ITEMS, (uint32_t)sms * 8);
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_keys<<<grid, RX_THREADS, 0, s>>>(pol, ct, pt, ctl, rx, t, n_rows, arr_base);
+  k_keys<<<grid, RX_THREADS, 0, s>>>(pol, ct, pt, ctl, rx, t, n_rows, arr_base, out.prev_rec);
   // skip detection needs the digit histograms on the host (a 4 KB read; this mode is the
   // contract path, the selection path is the fast path)
   cudaMemcpyAsync(rx.h_dig_hist, rx.dig_hist, 4 * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);

@@ -81,7 +81,7 @@ __device__ __forceinline__ void apply_record(const Policy& pol, ProgTable pt, co
 template <int NT>
 __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, Ctl* ctl, const uint32_t* slots,
                               uint32_t n, uint32_t t, KvState& kv, bool kv_on, CompRec* rec_out, bool apply,
-                              CompRec* s_rec = nullptr, const uint32_t* lin = nullptr) {
+                              CompRec* s_rec = nullptr, const uint32_t* lin = nullptr, CandRec* prev_rec = nullptr) {
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
   for (uint32_t base = 0; base < n; base += NT) {
@@ -90,9 +90,11 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
     uint32_t s = valid ? slots[i] : 0;
     CompRec r{};
     uint8_t qf0 = QF_DEAD;
+    uint32_t bix = NONE;
     if (valid) {
       uint32_t e = ct.exec[s];
       qf0 = ct.qf[s];  // loaded with the record fields: one round trip
+      if (prev_rec) bix = ct.bidx[s];
       r.prog = ct.prog[s];
       r.exec = e;
       r.cp = ct.inh[s] + e;
@@ -112,6 +114,8 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       }
       ct.qf[s] = QF_DEAD;
       ct.loc[s] = NONE;
+      // a completed call ran in the previous step: its previous-batch record says it is gone
+      if (prev_rec && (qf0 & QF_RUN)) reinterpret_cast<uint4*>(prev_rec + bix)[2] = make_uint4(QF_DEAD, 0u, 0u, 0u);
     }
     if (kv_on) {
       uint32_t tot;
@@ -139,10 +143,10 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
 template <int NT>
 __global__ void __launch_bounds__(NT) k_complete(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                  const uint32_t* slots, uint32_t n, uint32_t t, KvState kv,
-                                                 bool kv_on, CompRec* rec_out, bool apply) {
+                                                 bool kv_on, CompRec* rec_out, bool apply, CandRec* prev_rec) {
   pdl_wait();
   pdl_trigger();
-  complete_body<NT>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+  complete_body<NT>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, nullptr, nullptr, prev_rec);
 }
 
 // Multi-engine: apply every engine's completion records (R22: sums and maxima commute, so the
@@ -284,7 +288,7 @@ __device__ void prologue_body(const StepArgs& a, unsigned char* scratch, bool st
     if (my_arr && !eq2 && !(s_arr[tid].flags & 1u)) svc_old = __ldcg(&pt.info[s_arr[tid].prog].svc);
     if (p.n_comp)
       complete_body<NT>(pol, ct, pt, ctl, s_comp, p.n_comp, p.t, kv, a.kv_on, a.rec_out, true, s_rec,
-                        eq2 ? p.comp_lin : nullptr);
+                        eq2 ? p.comp_lin : nullptr, a.out.prev_rec);
     __syncthreads();
     if (stamps && tid == 0) ctl->dbg[57] = globaltimer();
     if (my_arr) {
@@ -302,7 +306,7 @@ __device__ void prologue_body(const StepArgs& a, unsigned char* scratch, bool st
   } else {
     if (p.n_comp)
       complete_body<NT>(pol, ct, pt, ctl, comp_inline ? s_comp : p.comp_ptr, p.n_comp, p.t, kv, a.kv_on,
-                        a.rec_out, true, nullptr, eq2 ? p.comp_lin : nullptr);
+                        a.rec_out, true, nullptr, eq2 ? p.comp_lin : nullptr, a.out.prev_rec);
     // arrivals inherit the service updated by this step's completions (R10): the reductions are
     // performed at L2 before the barrier releases (fence), and register_one reads svc from L2
     if (p.n_comp && p.n_arr) __threadfence();
@@ -638,18 +642,25 @@ __device__ void select_for(const StepArgs& a, uint32_t tile, SelSmem& S) {
 
 // Region A rows of one tile -> out.xrec at their (queue, seq) positions; the tile holding the
 // m'-th row of q* publishes it (region A's boundary).  Ranks inside the tile: one block scan per
-// word of 4 queues (16-bit fields), over the queues <= q*.
+// word of 4 queues (16-bit fields), over the queues <= q* (ranks: the tile has candidates).  The
+// tile also writes the records of its rows that ran in the previous step to out.prev_rec (at
+// their previous-batch index), so that the finalize reads the previous batch contiguously.
 __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&qw)[2], const SelSmem& S,
-                             unsigned long long* red64) {
+                             unsigned long long* red64, bool ranks) {
   const uint32_t tid = threadIdx.x, K = a.pol.K;
   const uint32_t qs = S.qs, m = S.m;
   const uint32_t qmax = min(qs, K - 1);
-  const uint32_t nw = (qmax >> 2) + 1;
+  const uint32_t nw = ranks ? (qmax >> 2) + 1 : 0u;
   const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
   uint32_t pos2[4];  // positions of rows 2k, 2k+1 in 16-bit halves (BS <= 2048)
-  uint32_t sel = 0, bnd = 0;
+  uint32_t sel = 0, bnd = 0, runm = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) pos2[k] = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t qf = qf_at(qw, j);
+    runm |= (!(qf & QF_DEAD) && (qf & QF_RUN)) ? 1u << j : 0u;
+  }
   for (uint32_t w = 0; w < nw; ++w) {
     uint64_t c = 0;
 #pragma unroll
@@ -673,13 +684,15 @@ __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&
       }
     }
   }
-  if (!sel) return;
+  const uint32_t need = sel | runm;
+  if (!need) return;
   const CallTable& ct = a.ct;
   CandRec* xrec = a.out.xrec;
+  CandRec* prec = a.out.prev_rec;
   // the thread's 8 rows: each field with vector loads, 4 rows at a time
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
-    if (!((sel >> (4 * half)) & 0xFu)) continue;
+    if (!((need >> (4 * half)) & 0xFu)) continue;
     const uint32_t r4 = row0 + 4 * half;
     const uint4 c0 = reinterpret_cast<const uint4*>(ct.cid + r4)[0];
     const uint4 c1 = reinterpret_cast<const uint4*>(ct.cid + r4)[1];
@@ -692,18 +705,28 @@ __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int j = 4 * half + k;
-      if (!((sel >> j) & 1u)) continue;
+      if (!((need >> j) & 1u)) continue;
       const uint4& cc = k < 2 ? c0 : c1;
       const uint32_t qf = qf_at(qw, j);
-      const uint32_t arr = lane4(ar, k);
-      const uint32_t pos = (pos2[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
-      uint4* dst = reinterpret_cast<uint4*>(xrec + pos);
-      dst[0] = make_uint4(k & 1 ? cc.z : cc.x, k & 1 ? cc.w : cc.y, r4 + k, arr);
-      dst[1] = make_uint4(lane4(tk, k), lane4(ex, k), lane4(mt, k), lane4(qt, k));
-      dst[2] = make_uint4(qf | ((qf & QF_RUN) ? lane4(bd, k) << 8 : 0u), 0u, 0u, 0u);
-      if ((bnd >> j) & 1u) {
-        a.ctl->bnd_slot = r4 + k;
-        a.ctl->bnd_arr = arr;
+      const uint32_t arr = lane4(ar, k), bx = lane4(bd, k);
+      const uint4 v0 = make_uint4(k & 1 ? cc.z : cc.x, k & 1 ? cc.w : cc.y, r4 + k, arr);
+      const uint4 v1 = make_uint4(lane4(tk, k), lane4(ex, k), lane4(mt, k), lane4(qt, k));
+      const uint4 v2 = make_uint4(qf | ((qf & QF_RUN) ? bx << 8 : 0u), 0u, 0u, 0u);
+      if ((sel >> j) & 1u) {
+        uint4* dst = reinterpret_cast<uint4*>(xrec + ((pos2[j >> 1] >> (16 * (j & 1))) & 0xFFFFu));
+        dst[0] = v0;
+        dst[1] = v1;
+        dst[2] = v2;
+        if ((bnd >> j) & 1u) {
+          a.ctl->bnd_slot = r4 + k;
+          a.ctl->bnd_arr = arr;
+        }
+      }
+      if ((runm >> j) & 1u) {
+        uint4* dst = reinterpret_cast<uint4*>(prec + bx);
+        dst[0] = v0;
+        dst[1] = v1;
+        dst[2] = v2;
       }
     }
   }
@@ -758,8 +781,8 @@ constexpr size_t fin_smem_bytes() {
 }
 
 template <int I>
-__device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs, uint32_t mp, uint32_t nx, uint32_t n_live,
-                              uint32_t n_promo, const uint32_t (&p_slot)[I / 2], uint32_t n_prev, bool wait2,
+__device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs, uint32_t mp, uint32_t nx,
+                              uint32_t n_live, uint32_t n_promo, uint32_t n_prev, bool wait2,
                               unsigned long long* red64, uint32_t* red32) {
   constexpr int NT = ST_THREADS, IP = I / 2, C = NT * I;
   const Policy& pol = a.pol;
@@ -777,7 +800,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   uint32_t* y_qfb = y_qt + C;
   uint32_t* z = y_qfb + C;    // sorted position -> index in Y
   uint32_t* hb = z + C;       // running calls before each group head; region B's slots first
-  uint32_t* grun = hb + C;    // running calls per group (at the head's index)
+  uint32_t* grun = hb + C;    // running calls up to each group's end (at the head's index)
   uint8_t* inb = reinterpret_cast<uint8_t*>(grun + C);  // previous-batch entry is in the new batch
   uint64_t* s_ad = reinterpret_cast<uint64_t*>(hb);     // admit / preempt ids for the host mirrors
   uint64_t* s_pr = reinterpret_cast<uint64_t*>(grun);   // (hb, grun are free once z is known)
@@ -788,7 +811,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   const bool stamps = STAMPS_ON(pol);
   if (wait2) grid_wait(&ctl->bar2, a.n_tile_ctas);
   if (stamps && tid == 0) ctl->dbg[44] = globaltimer();
-  // ---- (1) one round of loads: region A records, the previous batch's rows, the boundary -----
+  // ---- (1) one round of coalesced loads: region A, the previous batch, the boundary ------------
   uint32_t bnd_slot = 0, bnd_arr = 0;
   if (qs < K) {
     bnd_slot = __ldcg(&ctl->bnd_slot);
@@ -809,31 +832,28 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
       y_qt[i] = x1.w;
       y_qfb[i] = x2.x;
     }
-    grun[i] = 0;
   }
-  uint32_t p_qf[IP], p_arr[IP], p_tok[IP], p_exec[IP], p_mt[IP], p_qt[IP];
-  uint64_t p_cid[IP];
+  // previous batch, blocked (preempt keeps previous-batch order): entry j = tid * IP + r
+  uint4 pr0[IP], pr1[IP];
+  uint32_t p_qf[IP];
 #pragma unroll
   for (int r = 0; r < IP; ++r) {
-    const uint32_t s = p_slot[r];
+    const uint32_t j = tid * IP + r;
     p_qf[r] = QF_DEAD;
-    if (s != NONE) {
-      p_qf[r] = __ldcg(ct.qf + s);
-      p_arr[r] = __ldcg(ct.arr + s);
-      p_tok[r] = __ldcg(ct.tok + s);
-      p_exec[r] = __ldcg(ct.exec + s);
-      p_mt[r] = __ldcg(ct.mtime + s);
-      p_qt[r] = __ldcg(ct.quanta + s);
-      p_cid[r] = __ldcg(reinterpret_cast<const unsigned long long*>(ct.cid + s));
+    if (j < n_prev) {
+      const uint4* src = reinterpret_cast<const uint4*>(out.prev_rec + j);
+      pr0[r] = __ldcg(src);
+      pr1[r] = __ldcg(src + 1);
+      p_qf[r] = __ldcg(src + 2).x & 0xFFu;
+      inb[j] = 0;
     }
-    if (tid * IP + r < n_prev) inb[tid * IP + r] = 0;
   }
   // ---- (2) region B: running calls of q* in the boundary's arrival group, past the boundary ---
   uint32_t isb = 0, nbm = 0;
 #pragma unroll
   for (int r = 0; r < IP; ++r) {
-    const bool b = qs < K && p_slot[r] != NONE && !(p_qf[r] & QF_DEAD) && (p_qf[r] & QF_QMASK) == qs &&
-                   p_arr[r] == bnd_arr && p_slot[r] > bnd_slot;
+    const bool b = qs < K && !(p_qf[r] & QF_DEAD) && (p_qf[r] & QF_QMASK) == qs && pr0[r].w == bnd_arr &&
+                   pr0[r].z > bnd_slot;
     isb |= b ? 1u << r : 0u;
     nbm += b ? 1u : 0u;
   }
@@ -842,27 +862,29 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   if (stamps && tid == 0) ctl->dbg[49] = globaltimer();
 #pragma unroll
   for (int r = 0; r < IP; ++r)
-    if ((isb >> r) & 1u) hb[ob++] = p_slot[r];
+    if ((isb >> r) & 1u) hb[ob++] = pr0[r].z;
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < IP; ++r)
     if ((isb >> r) & 1u) {
       uint32_t rank = 0;
-      for (uint32_t k = 0; k < n_b; ++k) rank += hb[k] < p_slot[r] ? 1u : 0u;
+      for (uint32_t k = 0; k < n_b; ++k) rank += hb[k] < pr0[r].z ? 1u : 0u;
       const uint32_t i = nx + rank;
-      y_cid[i] = p_cid[r];
-      y_slot[i] = p_slot[r];
-      y_arr[i] = p_arr[r];
-      y_tok[i] = p_tok[r];
-      y_exec[i] = p_exec[r];
-      y_mt[i] = p_mt[r];
-      y_qt[i] = p_qt[r];
+      y_cid[i] = (uint64_t)pr0[r].y << 32 | pr0[r].x;
+      y_slot[i] = pr0[r].z;
+      y_arr[i] = pr0[r].w;
+      y_tok[i] = pr1[r].x;
+      y_exec[i] = pr1[r].y;
+      y_mt[i] = pr1[r].z;
+      y_qt[i] = pr1[r].w;
       y_qfb[i] = p_qf[r] | ((tid * IP + r) << 8);
     }
   const uint32_t n = nx + n_b;
   __syncthreads();
   if (stamps && tid == 0) ctl->dbg[45] = globaltimer();
-  // ---- (3) key order: stable partition, running calls first, inside each (queue, arrival) group
+  // ---- (3) key order: stable partition, running calls first, inside each (queue, arrival) group.
+  // Blocked items (i = tid * I + r).  For item i of the group headed at gs: rb = running items of
+  // the group before i, rt = running items of the whole group (written by its last item).
   uint32_t gs[I], rex[I], runm = 0, headm = 0, my_runs = 0, my_head = 0;
 #pragma unroll
   for (int r = 0; r < I; ++r) {
@@ -889,10 +911,10 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
       }
       gs[r] = cur_gs;
       rex[r] = cur_r;
-      if ((runm >> r) & 1u) {
-        atomicAdd(&grun[cur_gs], 1u);
-        ++cur_r;
-      }
+      cur_r += (runm >> r) & 1u;
+      // the group's last item: the running count at its end
+      const bool last = i + 1 == n || ((y_qfb[i + 1] ^ y_qfb[i]) & QF_QMASK) != 0 || y_arr[i + 1] != y_arr[i];
+      if (last) grun[cur_gs] = cur_r;
     }
   }
   __syncthreads();
@@ -900,8 +922,9 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   for (int r = 0; r < I; ++r) {
     const uint32_t i = tid * I + r;
     if (i < n) {
-      const uint32_t rb = rex[r] - hb[gs[r]];
-      const uint32_t pos = (runm >> r) & 1u ? gs[r] + rb : gs[r] + grun[gs[r]] + (i - gs[r] - rb);
+      const uint32_t h0 = hb[gs[r]];
+      const uint32_t rb = rex[r] - h0;
+      const uint32_t pos = (runm >> r) & 1u ? gs[r] + rb : gs[r] + (grun[gs[r]] - h0) + (i - gs[r] - rb);
       z[pos] = i;
     }
   }
@@ -936,7 +959,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   const uint32_t n_batch = s_nbatch;
   if (tid == 0 && nc > 0 && n_batch == 0) set_err(ctl, AUTX_E_NOMEM, y_slot[z[0]]);
   if (stamps && tid == 0) ctl->dbg[46] = globaltimer();
-  // ---- (5) batch list, admit = batch calls not resident (batch order), previous-batch marks ---
+  // ---- (5) admit = batch calls not resident (batch order; blocked for the scan) -----------------
   unsigned long long my_ad = 0;
   if (n_batch == 0 && tid == 0) s_kvsum = 0;
 #pragma unroll
@@ -944,12 +967,8 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
     const uint32_t p = tid * I + r;
     if (p < n_batch) {
       const uint32_t i = z[p];
-      const uint32_t qfb = y_qfb[i];
       if (p + 1 == n_batch) s_kvsum = inc[r];
-      out.batch_slots[p] = y_slot[i];
-      out.batch_ids[p] = y_cid[i];
-      if (qfb & QF_RUN) inb[qfb >> 8] = 1;
-      if (!(qfb & QF_RES)) {
+      if (!(y_qfb[i] & QF_RES)) {
         const uint32_t e = y_exec[i];
         const uint64_t held = e > 0 ? blocks_for(pol, y_tok[i] + e) : 0u;  // R28
         my_ad += (1ull << 44) | held;
@@ -974,18 +993,31 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
       }
     }
   }
-  if (stamps && tid == 0) ctl->dbg[51] = globaltimer();
   const uint32_t n_admit = (uint32_t)(ad_tot >> 44);
   const unsigned long long swap_in = ad_tot & ((1ull << 44) - 1);
+  // batch list (strided: coalesced stores) and the previous batch's membership marks
+#pragma unroll
+  for (int r = 0; r < I; ++r) {
+    const uint32_t p = r * NT + tid;
+    if (p < n_batch) {
+      const uint32_t i = z[p];
+      const uint32_t qfb = y_qfb[i];
+      out.batch_slots[p] = y_slot[i];
+      out.batch_ids[p] = y_cid[i];
+      if (qfb & QF_RUN) inb[qfb >> 8] = 1;
+    }
+  }
+  __syncthreads();
+  if (stamps && tid == 0) ctl->dbg[51] = globaltimer();
   // ---- (6) preempt = previous batch, still active, not in the batch (previous-batch order) ---
   unsigned long long my_pre = 0;
   uint32_t is_pre = 0;
 #pragma unroll
   for (int r = 0; r < IP; ++r) {
     const uint32_t j = tid * IP + r;
-    if (p_slot[r] != NONE && !(p_qf[r] & QF_DEAD) && !inb[j]) {
+    if (j < n_prev && !(p_qf[r] & QF_DEAD) && !inb[j]) {
       is_pre |= 1u << r;
-      my_pre += (1ull << 44) | blocks_for(pol, p_tok[r] + p_exec[r]);  // R28
+      my_pre += (1ull << 44) | blocks_for(pol, pr1[r].x + pr1[r].y);  // R28: held = ceil((tok + exec) / bt)
     }
   }
   unsigned long long pre_tot;
@@ -995,16 +1027,17 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
 #pragma unroll
     for (int r = 0; r < IP; ++r)
       if ((is_pre >> r) & 1u) {
-        out.preempt_ids[pos] = p_cid[r];
-        s_pr[pos] = p_cid[r];
-        out.preempt_slots[pos] = p_slot[r];
-        ct.qf[p_slot[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
+        const uint64_t cid = (uint64_t)pr0[r].y << 32 | pr0[r].x;
+        out.preempt_ids[pos] = cid;
+        s_pr[pos] = cid;
+        out.preempt_slots[pos] = pr0[r].z;
+        ct.qf[pr0[r].z] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
         ++pos;
       }
   }
-  if (stamps && tid == 0) ctl->dbg[52] = globaltimer();
   const uint32_t n_preempt = (uint32_t)(pre_tot >> 44);
   const unsigned long long swap_out = pre_tot & ((1ull << 44) - 1);
+  if (stamps && tid == 0) ctl->dbg[52] = globaltimer();
   // ---- (7) KV blocks: swap plan + allocation (a7) ---------------------------------------------
   if (a.kv_on) {
     __syncthreads();  // preempt_slots
@@ -1140,10 +1173,11 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
     }
     __syncthreads();
   }
-  // ---- (8) step accounting + eager demotion (Alg. 1 l.20-23) for the batch --------------------
+  // ---- (8) step accounting + eager demotion (Alg. 1 l.20-23) for the batch (strided: the
+  // batch is nearly in table order, so neighbouring threads write neighbouring rows) ------------
 #pragma unroll
   for (int r = 0; r < I; ++r) {
-    const uint32_t p = tid * I + r;
+    const uint32_t p = r * NT + tid;
     if (p < n_batch) {
       const uint32_t i = z[p];
       const uint32_t sl = y_slot[i];
@@ -1260,6 +1294,20 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
   }
   if (blockIdx.x == a.n_tile_ctas) {
     // ---- prologue + finalize CTA ----
+    if (a.pro_first) {
+      // the prologue's rows into L2 ahead of the tiles' stream (it is on the critical path: the
+      // deferred rows wait for it), then let the tiles go
+      const PrologueArgs& p = a.pro;
+      if (tid < p.n_comp && p.n_comp <= PRO_INLINE) {
+        const uint32_t sl = p.comp[tid];
+        prefetch_l2(a.ct.exec + sl); prefetch_l2(a.ct.qf + sl); prefetch_l2(a.ct.prog + sl);
+        prefetch_l2(a.ct.inh + sl); prefetch_l2(a.ct.arr + sl); prefetch_l2(a.ct.bidx + sl);
+        prefetch_l2(a.ct.loc + sl); prefetch_l2(a.pt.info + p.comp_prog[tid]);
+      }
+      if (tid < p.n_arr && p.n_arr <= PRO_INLINE) prefetch_l2(a.pt.info + p.arr[tid].prog);
+      __syncthreads();
+      if (tid == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(&ctl->go_seq), "r"(a.seqno) : "memory");
+    }
     if (a.do_pro) prologue_body<ST_THREADS>(a, dsm, stamps);
     __syncthreads();
     if (tid == 0) {
@@ -1267,26 +1315,13 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
       st_release_u32(&ctl->pro_seq, a.seqno);
       if (stamps) ctl->dbg[42] = globaltimer();
     }
-    // the previous batch's slots now; their rows into L2 while the tiles run
-    constexpr int IP = I / 2;
     const uint32_t n_prev = ctl->n_prev;
-    uint32_t p_slot[IP];
-#pragma unroll
-    for (int r = 0; r < IP; ++r) {
-      const uint32_t j = tid * IP + r;
-      p_slot[r] = j < n_prev ? a.out.prev_slots[j] : NONE;
-      if (p_slot[r] != NONE) {
-        const uint32_t s = p_slot[r];
-        prefetch_l2(a.ct.cid + s); prefetch_l2(a.ct.arr + s); prefetch_l2(a.ct.tok + s);
-        prefetch_l2(a.ct.exec + s); prefetch_l2(a.ct.mtime + s); prefetch_l2(a.ct.quanta + s);
-      }
-    }
     grid_arrive(&ctl->bar1);
     grid_wait(&ctl->bar1, gridDim.x);
     if (stamps && tid == 0) ctl->dbg[43] = globaltimer();
     select_for(a, NONE, S);
     const uint32_t qs = S.qs, mp = S.m, nx = S.nx, n_live = S.n_live, n_promo = S.n_promo;
-    finalize_core<I>(a, dsm, qs, mp, nx, n_live, n_promo, p_slot, n_prev, true, red64, red32);
+    finalize_core<I>(a, dsm, qs, mp, nx, n_live, n_promo, n_prev, true, red64, red32);
     return;
   }
   // ---- tile CTA ----
@@ -1303,6 +1338,11 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
   }
   uint32_t qw[2];
   uint32_t last = NONE;
+  if (a.pro_first) {
+    if (tid == 0)
+      while (ld_acquire_u32(&ctl->go_seq) != a.seqno) __nanosleep(20);
+    __syncthreads();
+  }
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
     uint64_t hq = 0;
     uint32_t np = 0, nl = 0;
@@ -1316,18 +1356,18 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
     select_for(a, tile, S);
     if (stamps && tid == 0 && tile == 0) ctl->dbg[54] = globaltimer();
-    if (S.has) {
-      if (tile != last) {
-        // an earlier tile of this CTA: its flags after the pass, from L2
-        const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
-        const uint2 qv = row0 < a.n_rows ? __ldcg(reinterpret_cast<const uint2*>(a.ct.qf + row0))
-                                         : make_uint2(0x40404040u, 0x40404040u);
-        qw[0] = qv.x;
-        qw[1] = qv.y;
-        last = tile;
-      }
-      extract_tile(a, tile, qw, S, red64);
+    if (tile != last) {
+      // an earlier tile of this CTA: its flags after the pass, from L2
+      const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+      const uint2 qv = row0 < a.n_rows ? __ldcg(reinterpret_cast<const uint2*>(a.ct.qf + row0))
+                                       : make_uint2(0x40404040u, 0x40404040u);
+      qw[0] = qv.x;
+      qw[1] = qv.y;
+      last = tile;
     }
+    // rows that ran in the previous step: their records go to prev_rec
+    const bool run = ((qw[0] | qw[1]) & 0x10101010u) != 0;
+    if (__syncthreads_or(run) || S.has) extract_tile(a, tile, qw, S, red64, S.has != 0);
     __syncthreads();  // S reuse
     if (stamps && tid == 0 && tile == 0) ctl->dbg[55] = globaltimer();
   }
@@ -1342,17 +1382,8 @@ __global__ void __launch_bounds__(ST_THREADS) k_fin(const __grid_constant__ Step
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ unsigned long long red64[33];
   __shared__ uint32_t red32[33];
-  constexpr int IP = I / 2;
-  const uint32_t tid = threadIdx.x;
   Ctl* ctl = a.ctl;
-  const uint32_t n_prev = ctl->n_prev;
-  uint32_t p_slot[IP];
-#pragma unroll
-  for (int r = 0; r < IP; ++r) {
-    const uint32_t j = tid * IP + r;
-    p_slot[r] = j < n_prev ? a.out.prev_slots[j] : NONE;
-  }
-  finalize_core<I>(a, dsm, a.pol.K, 0u, ctl->n_x, ctl->n_live, ctl->n_promoted, p_slot, n_prev, false, red64, red32);
+  finalize_core<I>(a, dsm, a.pol.K, 0u, ctl->n_x, ctl->n_live, ctl->n_promoted, ctl->n_prev, false, red64, red32);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1360,13 +1391,13 @@ __global__ void __launch_bounds__(ST_THREADS) k_fin(const __grid_constant__ Step
 // ---------------------------------------------------------------------------------------------
 cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                             const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
-                            CompRec* rec_out, bool apply) {
+                            CompRec* rec_out, bool apply, CandRec* prev_rec) {
   // size the CTA to the record count: a typical step completes ~BS/mean-decode calls
   if (n <= 32)
-    return launch_pdl(k_complete<32>, 1, 32, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+    return launch_pdl(k_complete<32>, 1, 32, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, prev_rec);
   else if (n <= 256)
-    return launch_pdl(k_complete<256>, 1, 256, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
-  return launch_pdl(k_complete<1024>, 1, 1024, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+    return launch_pdl(k_complete<256>, 1, 256, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, prev_rec);
+  return launch_pdl(k_complete<1024>, 1, 1024, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, prev_rec);
 }
 
 cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,

@@ -6,7 +6,9 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r02/build.log 2>
 BENCHES=${BENCHES:-"headline=--no-swap+--no-cpu-baseline"}
 for b in $BENCHES; do
   name=${b%%=*}; a=${b#*=}; a=${a//+/ }
-  timeout ${BENCH_TIMEOUT:-900} python bench.py $a --json-out gpurun_out/r02/$name.json > gpurun_out/r02/$name.out 2> gpurun_out/r02/$name.err
+  envs=""; args=""
+  for tok in $a; do if [[ "$tok" =~ ^[A-Z_]+=.*$ ]]; then envs="$envs $tok"; else args="$args $tok"; fi; done
+  timeout ${BENCH_TIMEOUT:-900} env $envs python bench.py $args --json-out gpurun_out/r02/$name.json > gpurun_out/r02/$name.out 2> gpurun_out/r02/$name.err
   echo "== $name rc=$?"
   python - "$name" <<'PY'
 import json, sys

@@ -14,6 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "dma_out": {"AUTX_DMA_OUT": "1"},      # host lists by one copy instead of zero-copy stores
     "defer_all": {"AUTX_DEFER_ALL": "1"},  # every row of the dense pass waits for the prologue
+    "pro_first": {"AUTX_PRO_FIRST": "1"},  # the tiles stream only once the prologue's loads are issued
 }
 
 SUBSET = "fig2 or atlas_dag or mcts or chatbot or compaction or react or (random_tiny and 7)"
