@@ -532,6 +532,8 @@ static void stage_prologue(autx_ctx* ctx, StepArgs& a, uint32_t t, bool with_arr
   a.first_new = p.n_arr ? p.first_slot : NONE;
   static const bool pro_first = getenv("AUTX_PRO_FIRST") != nullptr;  // A/B switch
   a.pro_first = (pro_first && a.do_pro && !a.defer_all) ? 1u : 0u;
+  static const bool warm = getenv("AUTX_WARM_PARAMS") != nullptr;
+  a.warm_params = warm ? 1u : 0u;
 }
 
 static void clear_staged(autx_ctx* ctx) {

@@ -267,6 +267,7 @@ struct StepArgs {
   uint32_t defer_all;   // the prologue's records are not inline: every row waits for it
   uint32_t do_pro;      // the step has a prologue (completions or arrivals)
   uint32_t pro_first;   // the tiles start streaming only once the prologue's loads are issued
+  uint32_t warm_params; // the finalize CTA touches its parameter fields while it waits
   PrologueArgs pro;
 };
 

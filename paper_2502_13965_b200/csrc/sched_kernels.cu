@@ -685,6 +685,8 @@ __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&
     }
   }
   const uint32_t need = sel | runm;
+  const long long ec0 = clock64();
+  if (STAMPS_ON(a.pol) && tid == 0) atomicMax(&a.ctl->dbg[36], (unsigned long long)__popc(sel));
   if (!need) return;
   const CallTable& ct = a.ct;
   CandRec* xrec = a.out.xrec;
@@ -730,6 +732,7 @@ __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&
       }
     }
   }
+  if (STAMPS_ON(a.pol)) atomicMax(&a.ctl->dbg[37], (unsigned long long)(clock64() - ec0));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -811,6 +814,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   const bool stamps = STAMPS_ON(pol);
   if (wait2) grid_wait(&ctl->bar2, a.n_tile_ctas);
   if (stamps && tid == 0) ctl->dbg[44] = globaltimer();
+  long long dc0 = clock64(), dc1 = 0, dc2 = 0, dc3 = 0;
   // ---- (1) one round of coalesced loads: region A, the previous batch, the boundary ------------
   uint32_t bnd_slot = 0, bnd_arr = 0;
   if (qs < K) {
@@ -833,6 +837,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
       y_qfb[i] = x2.x;
     }
   }
+  if (stamps) { __syncthreads(); dc1 = clock64(); }
   // previous batch, blocked (preempt keeps previous-batch order): entry j = tid * IP + r
   uint4 pr0[IP], pr1[IP];
   uint32_t p_qf[IP];
@@ -848,6 +853,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
       inb[j] = 0;
     }
   }
+  if (stamps) { __syncthreads(); dc2 = clock64(); }
   // ---- (2) region B: running calls of q* in the boundary's arrival group, past the boundary ---
   uint32_t isb = 0, nbm = 0;
 #pragma unroll
@@ -859,7 +865,13 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   }
   uint32_t n_b;
   uint32_t ob = block_excl_scan<uint32_t, NT>(nbm, red32, &n_b);
-  if (stamps && tid == 0) ctl->dbg[49] = globaltimer();
+  if (stamps && tid == 0) {
+    dc3 = clock64();
+    ctl->dbg[49] = globaltimer();
+    ctl->dbg[58] = dc1 - dc0;  // clock64 cycles: region A loads
+    ctl->dbg[59] = dc2 - dc1;  // previous-batch loads
+    ctl->dbg[60] = dc3 - dc2;  // region-B count (block scan)
+  }
 #pragma unroll
   for (int r = 0; r < IP; ++r)
     if ((isb >> r) & 1u) hb[ob++] = pr0[r].z;
@@ -1259,6 +1271,10 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
       ctl->dbg[64 + i] = ctl->dbg[40 + i];
       ctl->dbg[40 + i] = 0;
     }
+    ctl->dbg[88] = ctl->dbg[39];
+    ctl->dbg[89] = ctl->dbg[36];
+    ctl->dbg[90] = ctl->dbg[37];
+    ctl->dbg[39] = ctl->dbg[36] = ctl->dbg[37] = 0;
     ctl->dbg[40] = ~0ull;
   }
 }
@@ -1317,6 +1333,15 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
     }
     const uint32_t n_prev = ctl->n_prev;
     grid_arrive(&ctl->bar1);
+    if (a.warm_params) {
+      // the parameter fields the finalize reads, once, so that its phases do not each start with
+      // a constant-cache miss (A/B switch AUTX_WARM_PARAMS)
+      const unsigned char* pa = reinterpret_cast<const unsigned char*>(&a);
+      uint32_t acc = 0;
+      for (uint32_t off = tid * 4; off < (uint32_t)offsetof(StepArgs, pro) + 64; off += ST_THREADS * 4)
+        acc ^= *reinterpret_cast<const uint32_t*>(pa + off);
+      if (acc == 0x9E3779B9u) red32[32] = acc;
+    }
     grid_wait(&ctl->bar1, gridDim.x);
     if (stamps && tid == 0) ctl->dbg[43] = globaltimer();
     select_for(a, NONE, S);
@@ -1354,7 +1379,9 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
   if (stamps && tid == 0) atomicMax(&ctl->dbg[48], globaltimer());
   grid_wait(&ctl->bar1, gridDim.x);
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
+    const long long xc0 = clock64();
     select_for(a, tile, S);
+    const long long xc1 = clock64();
     if (stamps && tid == 0 && tile == 0) ctl->dbg[54] = globaltimer();
     if (tile != last) {
       // an earlier tile of this CTA: its flags after the pass, from L2
@@ -1367,8 +1394,15 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
     }
     // rows that ran in the previous step: their records go to prev_rec
     const bool run = ((qw[0] | qw[1]) & 0x10101010u) != 0;
-    if (__syncthreads_or(run) || S.has) extract_tile(a, tile, qw, S, red64, S.has != 0);
+    const bool any_run = __syncthreads_or(run);
+    if (any_run || S.has) extract_tile(a, tile, qw, S, red64, S.has != 0);
     __syncthreads();  // S reuse
+    if (stamps && tid == 0) {
+      atomicMax(&ctl->dbg[61], (unsigned long long)(xc1 - xc0));            // selection, cycles
+      atomicMax(&ctl->dbg[62], (unsigned long long)(clock64() - xc1));      // extraction, cycles
+      if (S.has) atomicAdd(&ctl->dbg[63], 1ull);                             // tiles with candidates
+      if (any_run) atomicAdd(&ctl->dbg[39], 1ull);                           // tiles with running rows
+    }
     if (stamps && tid == 0 && tile == 0) ctl->dbg[55] = globaltimer();
   }
   grid_arrive(&ctl->bar2);
