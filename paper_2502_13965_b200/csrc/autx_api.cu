@@ -189,8 +189,10 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   o.preempt_ids = o.admit_ids + BSp; CK(dalloc(&o.prev_slots, BS)); CK(dalloc(&o.preempt_slots, BS));
   o.batch_slots = reinterpret_cast<uint32_t*>(o.preempt_ids + BSp);
   CK(dalloc(&o.admit_slots, BS));
-  CK(dalloc(&o.xrec, BS));
-  CK(dalloc(&o.prev_rec, BS));
+  for (RecSoA* r : {&o.xs, &o.ps}) {
+    CK(dalloc(&r->cid, BS)); CK(dalloc(&r->slot, BS)); CK(dalloc(&r->arr, BS)); CK(dalloc(&r->tok, BS));
+    CK(dalloc(&r->exec, BS)); CK(dalloc(&r->mt, BS)); CK(dalloc(&r->qt, BS)); CK(dalloc(&r->qfb, BS));
+  }
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K));
   CK(dalloc(&o.sup_cnt, (ntiles / SUP_TILES + 1) * MAX_K));
   CK(cudaMemsetAsync(o.sup_cnt, 0, (ntiles / SUP_TILES + 1) * MAX_K * sizeof(uint32_t), ctx->stream));
@@ -348,13 +350,17 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
                  t.loc, t.hcls, t.bidx, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
                  ctx->ctl, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
-                 ctx->out.admit_slots, ctx->out.xrec, ctx->out.prev_rec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
+                 ctx->out.admit_slots, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
                  ctx->kv.bt_offsets, ctx->kv.bt_blocks, ctx->d_pools, ctx->staging,
                  ctx->d_route_local, ctx->d_pin, ctx->d_rarr, ctx->d_rout,
                  ctx->rx.keys, ctx->rx.keys_alt, ctx->rx.dig_hist, ctx->rx.tile_hist};
   for (void* p : dev) if (p) cudaFree(p);
+  for (RecSoA* r : {&ctx->out.xs, &ctx->out.ps}) {
+    void* f[] = {r->cid, r->slot, r->arr, r->tok, r->exec, r->mt, r->qt, r->qfb};
+    for (void* p : f) if (p) cudaFree(p);
+  }
   void* host[] = {ctx->h_outblk,
                   ctx->h_cslots, ctx->h_cprog, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr, ctx->h_clin, ctx->h_par,
                   ctx->rx.h_dig_hist};
@@ -475,7 +481,7 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
     if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
     CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
     CK(launch_complete(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->h_cslots, n, t, ctx->kv,
-                       ctx->kv_on, recs, false, ctx->out.prev_rec));
+                       ctx->kv_on, recs, false, ctx->out.ps.qfb));
     if (ctx->timing) {
       cudaEventRecord(ctx->ev[5], ctx->stream);
       ctx->timed_complete = true;

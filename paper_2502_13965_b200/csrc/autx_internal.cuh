@@ -137,13 +137,18 @@ struct KvState {
   uint32_t plan_cap;        // capacity of the plan block lists
 };
 
-// Candidate record: a row among the step's <= BS smallest keys (region A), written by its tile
-// CTA at its position in (queue, seq) order; the finalize reads it from L2.
-struct __align__(16) CandRec {
-  unsigned long long cid;
-  uint32_t slot, arr, tok, exec, mtime, quanta;
-  uint32_t qfb;  // qf | previous-batch index << 8 (valid while QF_RUN)
-  uint32_t _pad[3];
+// Candidate records, struct-of-arrays: a row among the step's <= BS smallest keys (region A) at
+// its position in (queue, seq) order, or a row of the previous batch at its previous-batch index.
+// Written by the tile CTAs with coalesced stores, read by the finalize with coalesced loads.
+struct RecSoA {
+  unsigned long long* cid;
+  uint32_t* slot;
+  uint32_t* arr;
+  uint32_t* tok;
+  uint32_t* exec;
+  uint32_t* mt;    // mtime after this step's anti-starvation
+  uint32_t* qt;    // quanta after this step's anti-starvation
+  uint32_t* qfb;   // qf | previous-batch index << 8 (valid while QF_RUN); QF_DEAD: completed
 };
 
 struct Outputs {
@@ -154,8 +159,8 @@ struct Outputs {
   uint32_t* prev_slots;      // [max_batch] previous batch (slots), ctl->n_prev entries
   uint32_t* preempt_slots;   // [max_batch]
   uint32_t* admit_slots;     // [max_batch]
-  CandRec* xrec;             // [max_batch] region A in (queue, seq) order
-  CandRec* prev_rec;         // [max_batch] the previous batch's rows by previous-batch index: written by
+  RecSoA xs;                 // [max_batch] region A in (queue, seq) order
+  RecSoA ps;                 // [max_batch] the previous batch's rows by previous-batch index: written by
                              // the tiles owning them (live rows, after the dense pass) and by the
                              // prologue (completed rows: qfb = QF_DEAD)
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K] live rows per (tile, queue) after anti-starvation
@@ -274,7 +279,7 @@ struct StepArgs {
 // ---- kernel launchers (sched_kernels.cu / swap_kernels.cu / radix_kernels.cu) ---------------
 cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                             const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
-                            CompRec* rec_out, bool apply, CandRec* prev_rec);
+                            CompRec* rec_out, bool apply, uint32_t* prev_qfb);
 // The step prologue (a1, a2) as its own kernel (radix mode, bulk bursts, before a compaction).
 cudaError_t launch_prologue(cudaStream_t s, const StepArgs& a);
 cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,

@@ -27,7 +27,7 @@ constexpr int RX_WARP_KEYS = 32 * RX_ITEMS;      // 512 keys per warp, contiguou
 
 __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                      RadixState rx, uint32_t t, uint32_t n_rows,
-                                                     uint32_t arr_base, CandRec* prev_rec) {
+                                                     uint32_t arr_base, RecSoA ps) {
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += RX_THREADS) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -60,11 +60,14 @@ __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, P
         }
         if (qf & QF_RUN) {  // ran in the previous step: its record for the finalize (prev_rec)
           const uint32_t bx = ct.bidx[r];
-          const unsigned long long cid = ct.cid[r];
-          uint4* dst = reinterpret_cast<uint4*>(prev_rec + bx);
-          dst[0] = make_uint4((uint32_t)cid, (uint32_t)(cid >> 32), r, ct.arr[r]);
-          dst[1] = make_uint4(ct.tok[r], ct.exec[r], mt_now, qt_now);
-          dst[2] = make_uint4(qf | (bx << 8), 0u, 0u, 0u);
+          ps.cid[bx] = ct.cid[r];
+          ps.slot[bx] = r;
+          ps.arr[bx] = ct.arr[r];
+          ps.tok[bx] = ct.tok[r];
+          ps.exec[bx] = ct.exec[r];
+          ps.mt[bx] = mt_now;
+          ps.qt[bx] = qt_now;
+          ps.qfb[bx] = qf | (bx << 8);
         }
         uint64_t arel = (uint64_t)(ct.arr[r] - arr_base) & ((1u << 27) - 1);
         key = ((uint64_t)q << 60) | (arel << 33) | ((uint64_t)((qf & QF_RUN) ? 0u : 1u) << 32) | r;
@@ -173,11 +176,15 @@ __global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     const uint32_t s = (uint32_t)keys[i];
     const uint32_t qf = ct.qf[s];
-    uint4* dst = reinterpret_cast<uint4*>(out.xrec + i);
-    const unsigned long long cid = ct.cid[s];
-    dst[0] = make_uint4((uint32_t)cid, (uint32_t)(cid >> 32), s, ct.arr[s]);
-    dst[1] = make_uint4(ct.tok[s], ct.exec[s], ct.mtime[s], ct.quanta[s]);
-    dst[2] = make_uint4(qf | ((qf & QF_RUN) ? ct.bidx[s] << 8 : 0u), 0u, 0u, 0u);
+    const RecSoA& x = out.xs;
+    x.cid[i] = ct.cid[s];
+    x.slot[i] = s;
+    x.arr[i] = ct.arr[s];
+    x.tok[i] = ct.tok[s];
+    x.exec[i] = ct.exec[s];
+    x.mt[i] = ct.mtime[s];
+    x.qt[i] = ct.quanta[s];
+    x.qfb[i] = qf | ((qf & QF_RUN) ? ct.bidx[s] << 8 : 0u);
   }
   if (threadIdx.x == 0) {
     ctl->n_x = n;
@@ -193,7 +200,7 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
   cudaMemsetAsync(rx.dig_hist, 0, 4 * 256 * sizeof(uint32_t), s);
   uint32_t grid = std::min<uint32_t>(ntiles * RX_ITEMS, (uint32_t)sms * 8);
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_keys<<<grid, RX_THREADS, 0, s>>>(pol, ct, pt, ctl, rx, t, n_rows, arr_base, out.prev_rec);
+  k_keys<<<grid, RX_THREADS, 0, s>>>(pol, ct, pt, ctl, rx, t, n_rows, arr_base, out.ps);
   // skip detection needs the digit histograms on the host (a 4 KB read; this mode is the
   // contract path, the selection path is the fast path)
   cudaMemcpyAsync(rx.h_dig_hist, rx.dig_hist, 4 * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);

@@ -81,7 +81,7 @@ __device__ __forceinline__ void apply_record(const Policy& pol, ProgTable pt, co
 template <int NT>
 __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, Ctl* ctl, const uint32_t* slots,
                               uint32_t n, uint32_t t, KvState& kv, bool kv_on, CompRec* rec_out, bool apply,
-                              CompRec* s_rec = nullptr, const uint32_t* lin = nullptr, CandRec* prev_rec = nullptr) {
+                              CompRec* s_rec = nullptr, const uint32_t* lin = nullptr, uint32_t* prev_qfb = nullptr) {
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
   for (uint32_t base = 0; base < n; base += NT) {
@@ -94,7 +94,7 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
     if (valid) {
       uint32_t e = ct.exec[s];
       qf0 = ct.qf[s];  // loaded with the record fields: one round trip
-      if (prev_rec) bix = ct.bidx[s];
+      if (prev_qfb) bix = ct.bidx[s];
       r.prog = ct.prog[s];
       r.exec = e;
       r.cp = ct.inh[s] + e;
@@ -115,7 +115,7 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       ct.qf[s] = QF_DEAD;
       ct.loc[s] = NONE;
       // a completed call ran in the previous step: its previous-batch record says it is gone
-      if (prev_rec && (qf0 & QF_RUN)) reinterpret_cast<uint4*>(prev_rec + bix)[2] = make_uint4(QF_DEAD, 0u, 0u, 0u);
+      if (prev_qfb && (qf0 & QF_RUN)) prev_qfb[bix] = QF_DEAD;
     }
     if (kv_on) {
       uint32_t tot;
@@ -143,10 +143,10 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
 template <int NT>
 __global__ void __launch_bounds__(NT) k_complete(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                  const uint32_t* slots, uint32_t n, uint32_t t, KvState kv,
-                                                 bool kv_on, CompRec* rec_out, bool apply, CandRec* prev_rec) {
+                                                 bool kv_on, CompRec* rec_out, bool apply, uint32_t* prev_qfb) {
   pdl_wait();
   pdl_trigger();
-  complete_body<NT>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, nullptr, nullptr, prev_rec);
+  complete_body<NT>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, nullptr, nullptr, prev_qfb);
 }
 
 // Multi-engine: apply every engine's completion records (R22: sums and maxima commute, so the
@@ -288,7 +288,7 @@ __device__ void prologue_body(const StepArgs& a, unsigned char* scratch, bool st
     if (my_arr && !eq2 && !(s_arr[tid].flags & 1u)) svc_old = __ldcg(&pt.info[s_arr[tid].prog].svc);
     if (p.n_comp)
       complete_body<NT>(pol, ct, pt, ctl, s_comp, p.n_comp, p.t, kv, a.kv_on, a.rec_out, true, s_rec,
-                        eq2 ? p.comp_lin : nullptr, a.out.prev_rec);
+                        eq2 ? p.comp_lin : nullptr, a.out.ps.qfb);
     __syncthreads();
     if (stamps && tid == 0) ctl->dbg[57] = globaltimer();
     if (my_arr) {
@@ -306,7 +306,7 @@ __device__ void prologue_body(const StepArgs& a, unsigned char* scratch, bool st
   } else {
     if (p.n_comp)
       complete_body<NT>(pol, ct, pt, ctl, comp_inline ? s_comp : p.comp_ptr, p.n_comp, p.t, kv, a.kv_on,
-                        a.rec_out, true, nullptr, eq2 ? p.comp_lin : nullptr, a.out.prev_rec);
+                        a.rec_out, true, nullptr, eq2 ? p.comp_lin : nullptr, a.out.ps.qfb);
     // arrivals inherit the service updated by this step's completions (R10): the reductions are
     // performed at L2 before the barrier releases (fence), and register_one reads svc from L2
     if (p.n_comp && p.n_arr) __threadfence();
@@ -454,19 +454,22 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, const CallTable& c
   }
 }
 
-// The dense pass over one tile (thread: 8 consecutive rows).  Rows the prologue touches are
-// deferred until it has finished: this step's arrivals (rows >= first_new) and the rows of
-// programs with a completion in this step (s_filt: a 2048-bit filter of their process-table rows,
-// built from the parameters; a collision only defers more).  All other rows run at once, reading
-// nothing the prologue writes.  qw: the rows' flags after the pass.
+// The dense pass over one tile (thread: 8 consecutive rows).  Rows the prologue touches wait for
+// it: this step's arrivals (rows >= first_new: written by the prologue, loaded again afterwards)
+// and the rows of programs with a completion in this step (s_filt: a 2048-bit filter of their
+// process-table rows, built from the parameters; a collision only defers more).  Those keep the
+// row fields of the first load (the prologue does not change them) and only gather their program
+// rows again; the completed rows among them are known from the parameters (s_dead).  All other
+// rows run at once, reading nothing the prologue writes.  qw: the rows' flags after the pass.
 __device__ __forceinline__ void tile_pass(const StepArgs& a, uint32_t tile, const uint32_t* s_filt, bool filt_on,
-                                          uint32_t (&qw)[2], uint64_t& hq, uint32_t& npromo, uint32_t& nlive) {
+                                          uint32_t* s_dead, uint32_t (&qw)[2], uint64_t& hq, uint32_t& npromo,
+                                          uint32_t& nlive) {
   const uint32_t tid = threadIdx.x;
   const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
   const bool have = row0 < a.n_rows;
   const CallTable& ct = a.ct;
   uint32_t prog[8], base[8], mtim[8];
-  bool defer = false;
+  bool full = false, prog_only = false;
   qw[0] = qw[1] = 0x40404040u;  // QF_DEAD
   if (have) {
     const uint2 qv = *reinterpret_cast<const uint2*>(ct.qf + row0);
@@ -484,16 +487,25 @@ __device__ __forceinline__ void tile_pass(const StepArgs& a, uint32_t tile, cons
       base[j] = lane4(j < 4 ? b0 : b1, j & 3);
       mtim[j] = lane4(j < 4 ? m0 : m1, j & 3);
     }
-    defer = a.defer_all || row0 + ROWS_PER_THREAD > a.first_new;
-    if (!defer && filt_on) {
+    full = a.defer_all || row0 + ROWS_PER_THREAD > a.first_new;
+    if (!full && filt_on) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) defer |= ((s_filt[(prog[j] >> 5) & 63] >> (prog[j] & 31)) & 1u) != 0;
+      for (int j = 0; j < 8; ++j) prog_only |= ((s_filt[(prog[j] >> 5) & 63] >> (prog[j] & 31)) & 1u) != 0;
     }
-    if (!defer) dense_rows<false>(a.pol, ct, a.pt, a.t, row0, qw, prog, base, mtim, hq, npromo, nlive);
+    if (!full && !prog_only) dense_rows<false>(a.pol, ct, a.pt, a.t, row0, qw, prog, base, mtim, hq, npromo, nlive);
   }
-  if (__syncthreads_or(defer)) {
+  if (__syncthreads_or(full || prog_only)) {
+    if (filt_on) {
+      // this step's completed rows in this tile (marked dead by the prologue)
+      if (tid < TILE / 32) s_dead[tid] = 0;
+      __syncthreads();
+      if (tid < a.pro.n_comp) {
+        const uint32_t sl = a.pro.comp[tid];
+        if (sl / TILE == tile) atomicOr(&s_dead[(sl % TILE) >> 5], 1u << (sl & 31));
+      }
+    }
     wait_prologue(a.ctl, a.seqno);
-    if (defer) {
+    if (full) {
       const uint2 qv = __ldcg(reinterpret_cast<const uint2*>(ct.qf + row0));
       const uint4 p0 = __ldcg(reinterpret_cast<const uint4*>(ct.prog + row0));
       const uint4 p1 = __ldcg(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
@@ -509,6 +521,12 @@ __device__ __forceinline__ void tile_pass(const StepArgs& a, uint32_t tile, cons
         base[j] = lane4(j < 4 ? b0 : b1, j & 3);
         mtim[j] = lane4(j < 4 ? m0 : m1, j & 3);
       }
+      dense_rows<true>(a.pol, ct, a.pt, a.t, row0, qw, prog, base, mtim, hq, npromo, nlive);
+    } else if (prog_only) {
+      const uint32_t dead = (s_dead[(tid * ROWS_PER_THREAD) >> 5] >> ((tid * ROWS_PER_THREAD) & 31)) & 0xFFu;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if ((dead >> j) & 1u) qw[j >> 2] = (qw[j >> 2] & ~(0xFFu << (8 * (j & 3)))) | ((uint32_t)QF_DEAD << (8 * (j & 3)));
       dense_rows<true>(a.pol, ct, a.pt, a.t, row0, qw, prog, base, mtim, hq, npromo, nlive);
     }
   }
@@ -640,22 +658,30 @@ __device__ void select_for(const StepArgs& a, uint32_t tile, SelSmem& S) {
   __syncthreads();
 }
 
-// Region A rows of one tile -> out.xrec at their (queue, seq) positions; the tile holding the
+// Region A rows of one tile -> out.xs at their (queue, seq) positions; the tile holding the
 // m'-th row of q* publishes it (region A's boundary).  Ranks inside the tile: one block scan per
 // word of 4 queues (16-bit fields), over the queues <= q* (ranks: the tile has candidates).  The
-// tile also writes the records of its rows that ran in the previous step to out.prev_rec (at
-// their previous-batch index), so that the finalize reads the previous batch contiguously.
+// tile also writes the records of its rows that ran in the previous step to out.ps (at their
+// previous-batch index), so that the finalize reads the previous batch contiguously.  The copy is
+// cooperative: the owning threads only publish each row's position in shared memory, then all
+// threads copy the rows in [lo, hi] with consecutive rows on consecutive lanes (coalesced loads
+// from the table, coalesced stores into the struct-of-arrays records), whichever threads own them.
+// sm: >= TILE * 3 + 64 bytes of shared scratch.
 __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&qw)[2], const SelSmem& S,
-                             unsigned long long* red64, bool ranks) {
+                             unsigned long long* red64, bool ranks, unsigned char* sm) {
+  constexpr int NT = ST_THREADS;
   const uint32_t tid = threadIdx.x, K = a.pol.K;
   const uint32_t qs = S.qs, m = S.m;
   const uint32_t qmax = min(qs, K - 1);
   const uint32_t nw = ranks ? (qmax >> 2) + 1 : 0u;
-  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  const uint32_t l0 = tid * ROWS_PER_THREAD, tile0 = tile * TILE;
+  uint16_t* s_px = reinterpret_cast<uint16_t*>(sm);           // [TILE] position in region A or 0xFFFF
+  uint32_t* s_qf = reinterpret_cast<uint32_t*>(sm + 2 * TILE);  // [TILE / 4] flags after the pass
+  uint32_t* s_rng = reinterpret_cast<uint32_t*>(sm + 3 * TILE); // [2 * NW] per-warp lo / hi
   uint32_t pos2[4];  // positions of rows 2k, 2k+1 in 16-bit halves (BS <= 2048)
-  uint32_t sel = 0, bnd = 0, runm = 0;
+  uint32_t sel = 0, runm = 0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) pos2[k] = 0;
+  for (int k = 0; k < 4; ++k) pos2[k] = 0xFFFFFFFFu;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const uint32_t qf = qf_at(qw, j);
@@ -668,7 +694,7 @@ __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&
       const uint32_t qf = qf_at(qw, j), q = qf & QF_QMASK;
       if (!(qf & QF_DEAD) && q <= qmax && (q >> 2) == w) c += 1ull << (16 * (q & 3));
     }
-    uint64_t ex = block_excl_scan<unsigned long long, ST_THREADS>(c, red64, nullptr);
+    uint64_t ex = block_excl_scan<unsigned long long, NT>(c, red64, nullptr);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t qf = qf_at(qw, j), q = qf & QF_QMASK;
@@ -678,61 +704,59 @@ __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&
         ex += 1ull << sh;
         if (q < qs || rank < m) {
           sel |= 1u << j;
-          pos2[j >> 1] |= (S.base[q] + rank) << (16 * (j & 1));
-          if (q == qs && rank + 1 == m) bnd = 1u << j;
+          const uint32_t pos = S.base[q] + rank;
+          pos2[j >> 1] = (pos2[j >> 1] & ~(0xFFFFu << (16 * (j & 1)))) | (pos << (16 * (j & 1)));
+          if (q == qs && rank + 1 == m) {  // region A's boundary row
+            a.ctl->bnd_slot = tile0 + l0 + j;
+            a.ctl->bnd_arr = __ldcg(a.ct.arr + tile0 + l0 + j);
+          }
         }
       }
     }
   }
+  // publish positions and flags; the tile's range of rows to copy
   const uint32_t need = sel | runm;
-  const long long ec0 = clock64();
-  if (STAMPS_ON(a.pol) && tid == 0) atomicMax(&a.ctl->dbg[36], (unsigned long long)__popc(sel));
-  if (!need) return;
+  reinterpret_cast<uint4*>(s_px)[tid] = make_uint4(pos2[0], pos2[1], pos2[2], pos2[3]);
+  reinterpret_cast<uint2*>(s_qf)[tid] = make_uint2(qw[0], qw[1]);
+  uint32_t lo = need ? l0 + __ffs(need) - 1 : 0xFFFFFFFFu;
+  uint32_t hi = need ? l0 + 31 - __clz(need) : 0u;
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if (lane_id() == 0) {
+    s_rng[warp_id()] = lo;
+    s_rng[NT / 32 + warp_id()] = hi;
+  }
+  __syncthreads();
+  lo = 0xFFFFFFFFu;
+  hi = 0;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    lo = min(lo, s_rng[w]);
+    hi = max(hi, s_rng[NT / 32 + w]);
+  }
   const CallTable& ct = a.ct;
-  CandRec* xrec = a.out.xrec;
-  CandRec* prec = a.out.prev_rec;
-  // the thread's 8 rows: each field with vector loads, 4 rows at a time
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    if (!((need >> (4 * half)) & 0xFu)) continue;
-    const uint32_t r4 = row0 + 4 * half;
-    const uint4 c0 = reinterpret_cast<const uint4*>(ct.cid + r4)[0];
-    const uint4 c1 = reinterpret_cast<const uint4*>(ct.cid + r4)[1];
-    const uint4 ar = *reinterpret_cast<const uint4*>(ct.arr + r4);
-    const uint4 tk = *reinterpret_cast<const uint4*>(ct.tok + r4);
-    const uint4 ex = *reinterpret_cast<const uint4*>(ct.exec + r4);
-    const uint4 mt = __ldcg(reinterpret_cast<const uint4*>(ct.mtime + r4));   // (promotions of this kernel)
-    const uint4 qt = __ldcg(reinterpret_cast<const uint4*>(ct.quanta + r4));
-    const uint4 bd = *reinterpret_cast<const uint4*>(ct.bidx + r4);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int j = 4 * half + k;
-      if (!((need >> j) & 1u)) continue;
-      const uint4& cc = k < 2 ? c0 : c1;
-      const uint32_t qf = qf_at(qw, j);
-      const uint32_t arr = lane4(ar, k), bx = lane4(bd, k);
-      const uint4 v0 = make_uint4(k & 1 ? cc.z : cc.x, k & 1 ? cc.w : cc.y, r4 + k, arr);
-      const uint4 v1 = make_uint4(lane4(tk, k), lane4(ex, k), lane4(mt, k), lane4(qt, k));
-      const uint4 v2 = make_uint4(qf | ((qf & QF_RUN) ? bx << 8 : 0u), 0u, 0u, 0u);
-      if ((sel >> j) & 1u) {
-        uint4* dst = reinterpret_cast<uint4*>(xrec + ((pos2[j >> 1] >> (16 * (j & 1))) & 0xFFFFu));
-        dst[0] = v0;
-        dst[1] = v1;
-        dst[2] = v2;
-        if ((bnd >> j) & 1u) {
-          a.ctl->bnd_slot = r4 + k;
-          a.ctl->bnd_arr = arr;
-        }
-      }
-      if ((runm >> j) & 1u) {
-        uint4* dst = reinterpret_cast<uint4*>(prec + bx);
-        dst[0] = v0;
-        dst[1] = v1;
-        dst[2] = v2;
-      }
+  const RecSoA& xs = a.out.xs;
+  const RecSoA& ps = a.out.ps;
+  for (uint32_t l = lo + tid; l <= hi && lo != 0xFFFFFFFFu; l += NT) {
+    const uint32_t px = s_px[l];
+    const uint32_t qf = (s_qf[l >> 2] >> (8 * (l & 3))) & 0xFFu;
+    const bool run = !(qf & QF_DEAD) && (qf & QF_RUN);
+    if (px == 0xFFFFu && !run) continue;
+    const uint32_t r = tile0 + l;
+    const unsigned long long cid = ct.cid[r];
+    const uint32_t arr = ct.arr[r], tok = ct.tok[r], ex = ct.exec[r];
+    const uint32_t mt = __ldcg(ct.mtime + r), qt = __ldcg(ct.quanta + r);  // (promotions of this kernel)
+    const uint32_t bx = run ? ct.bidx[r] : 0u;
+    const uint32_t qfb = qf | (run ? bx << 8 : 0u);
+    if (px != 0xFFFFu) {
+      xs.cid[px] = cid; xs.slot[px] = r; xs.arr[px] = arr; xs.tok[px] = tok;
+      xs.exec[px] = ex; xs.mt[px] = mt; xs.qt[px] = qt; xs.qfb[px] = qfb;
+    }
+    if (run) {
+      ps.cid[bx] = cid; ps.slot[bx] = r; ps.arr[bx] = arr; ps.tok[bx] = tok;
+      ps.exec[bx] = ex; ps.mt[bx] = mt; ps.qt[bx] = qt; ps.qfb[bx] = qfb;
     }
   }
-  if (STAMPS_ON(a.pol)) atomicMax(&a.ctl->dbg[37], (unsigned long long)(clock64() - ec0));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -821,36 +845,47 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
     bnd_slot = __ldcg(&ctl->bnd_slot);
     bnd_arr = __ldcg(&ctl->bnd_arr);
   }
+  // region A: strided (coalesced), straight into the shared-memory arrays (nx <= BS <= NT * I / 2)
+  {
+    const RecSoA& xs = out.xs;
+    unsigned long long c[IP];
+    uint32_t f[IP][7];
 #pragma unroll
-  for (int r = 0; r < I; ++r) {
-    const uint32_t i = r * NT + tid;
-    if (i < nx) {
-      const uint4* src = reinterpret_cast<const uint4*>(out.xrec + i);
-      const uint4 x0 = __ldcg(src), x1 = __ldcg(src + 1), x2 = __ldcg(src + 2);
-      y_cid[i] = (uint64_t)x0.y << 32 | x0.x;
-      y_slot[i] = x0.z;
-      y_arr[i] = x0.w;
-      y_tok[i] = x1.x;
-      y_exec[i] = x1.y;
-      y_mt[i] = x1.z;
-      y_qt[i] = x1.w;
-      y_qfb[i] = x2.x;
+    for (int r = 0; r < IP; ++r) {  // every load of the round first
+      const uint32_t i = min(r * NT + tid, BS - 1);
+      c[r] = __ldcg(xs.cid + i);
+      f[r][0] = __ldcg(xs.slot + i); f[r][1] = __ldcg(xs.arr + i); f[r][2] = __ldcg(xs.tok + i);
+      f[r][3] = __ldcg(xs.exec + i); f[r][4] = __ldcg(xs.mt + i); f[r][5] = __ldcg(xs.qt + i);
+      f[r][6] = __ldcg(xs.qfb + i);
+    }
+#pragma unroll
+    for (int r = 0; r < IP; ++r) {
+      const uint32_t i = r * NT + tid;
+      if (i < nx) {
+        y_cid[i] = c[r]; y_slot[i] = f[r][0]; y_arr[i] = f[r][1]; y_tok[i] = f[r][2];
+        y_exec[i] = f[r][3]; y_mt[i] = f[r][4]; y_qt[i] = f[r][5]; y_qfb[i] = f[r][6];
+      }
     }
   }
   if (stamps) { __syncthreads(); dc1 = clock64(); }
   // previous batch, blocked (preempt keeps previous-batch order): entry j = tid * IP + r
-  uint4 pr0[IP], pr1[IP];
-  uint32_t p_qf[IP];
+  uint32_t p_slot[IP], p_arr[IP], p_tok[IP], p_exec[IP], p_mt[IP], p_qt[IP], p_qf[IP];
+  uint64_t p_cid[IP];
+  {
+    const RecSoA& ps = out.ps;
 #pragma unroll
-  for (int r = 0; r < IP; ++r) {
-    const uint32_t j = tid * IP + r;
-    p_qf[r] = QF_DEAD;
-    if (j < n_prev) {
-      const uint4* src = reinterpret_cast<const uint4*>(out.prev_rec + j);
-      pr0[r] = __ldcg(src);
-      pr1[r] = __ldcg(src + 1);
-      p_qf[r] = __ldcg(src + 2).x & 0xFFu;
-      inb[j] = 0;
+    for (int r = 0; r < IP; ++r) {
+      const uint32_t j = min(tid * IP + r, BS - 1);
+      p_cid[r] = __ldcg(ps.cid + j);
+      p_slot[r] = __ldcg(ps.slot + j); p_arr[r] = __ldcg(ps.arr + j); p_tok[r] = __ldcg(ps.tok + j);
+      p_exec[r] = __ldcg(ps.exec + j); p_mt[r] = __ldcg(ps.mt + j); p_qt[r] = __ldcg(ps.qt + j);
+      p_qf[r] = __ldcg(ps.qfb + j) & 0xFFu;
+    }
+#pragma unroll
+    for (int r = 0; r < IP; ++r) {
+      const uint32_t j = tid * IP + r;
+      if (j < n_prev) inb[j] = 0;
+      else p_qf[r] = QF_DEAD;
     }
   }
   if (stamps) { __syncthreads(); dc2 = clock64(); }
@@ -858,8 +893,8 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   uint32_t isb = 0, nbm = 0;
 #pragma unroll
   for (int r = 0; r < IP; ++r) {
-    const bool b = qs < K && !(p_qf[r] & QF_DEAD) && (p_qf[r] & QF_QMASK) == qs && pr0[r].w == bnd_arr &&
-                   pr0[r].z > bnd_slot;
+    const bool b = qs < K && !(p_qf[r] & QF_DEAD) && (p_qf[r] & QF_QMASK) == qs && p_arr[r] == bnd_arr &&
+                   p_slot[r] > bnd_slot;
     isb |= b ? 1u << r : 0u;
     nbm += b ? 1u : 0u;
   }
@@ -874,21 +909,21 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
   }
 #pragma unroll
   for (int r = 0; r < IP; ++r)
-    if ((isb >> r) & 1u) hb[ob++] = pr0[r].z;
+    if ((isb >> r) & 1u) hb[ob++] = p_slot[r];
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < IP; ++r)
     if ((isb >> r) & 1u) {
       uint32_t rank = 0;
-      for (uint32_t k = 0; k < n_b; ++k) rank += hb[k] < pr0[r].z ? 1u : 0u;
+      for (uint32_t k = 0; k < n_b; ++k) rank += hb[k] < p_slot[r] ? 1u : 0u;
       const uint32_t i = nx + rank;
-      y_cid[i] = (uint64_t)pr0[r].y << 32 | pr0[r].x;
-      y_slot[i] = pr0[r].z;
-      y_arr[i] = pr0[r].w;
-      y_tok[i] = pr1[r].x;
-      y_exec[i] = pr1[r].y;
-      y_mt[i] = pr1[r].z;
-      y_qt[i] = pr1[r].w;
+      y_cid[i] = p_cid[r];
+      y_slot[i] = p_slot[r];
+      y_arr[i] = p_arr[r];
+      y_tok[i] = p_tok[r];
+      y_exec[i] = p_exec[r];
+      y_mt[i] = p_mt[r];
+      y_qt[i] = p_qt[r];
       y_qfb[i] = p_qf[r] | ((tid * IP + r) << 8);
     }
   const uint32_t n = nx + n_b;
@@ -1029,7 +1064,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
     const uint32_t j = tid * IP + r;
     if (j < n_prev && !(p_qf[r] & QF_DEAD) && !inb[j]) {
       is_pre |= 1u << r;
-      my_pre += (1ull << 44) | blocks_for(pol, pr1[r].x + pr1[r].y);  // R28: held = ceil((tok + exec) / bt)
+      my_pre += (1ull << 44) | blocks_for(pol, p_tok[r] + p_exec[r]);  // R28: held = ceil((tok + exec) / bt)
     }
   }
   unsigned long long pre_tot;
@@ -1039,11 +1074,10 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
 #pragma unroll
     for (int r = 0; r < IP; ++r)
       if ((is_pre >> r) & 1u) {
-        const uint64_t cid = (uint64_t)pr0[r].y << 32 | pr0[r].x;
-        out.preempt_ids[pos] = cid;
-        s_pr[pos] = cid;
-        out.preempt_slots[pos] = pr0[r].z;
-        ct.qf[pr0[r].z] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
+        out.preempt_ids[pos] = p_cid[r];
+        s_pr[pos] = p_cid[r];
+        out.preempt_slots[pos] = p_slot[r];
+        ct.qf[p_slot[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
         ++pos;
       }
   }
@@ -1371,7 +1405,7 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
     uint64_t hq = 0;
     uint32_t np = 0, nl = 0;
-    tile_pass(a, tile, s_filt, filt_on, qw, hq, np, nl);
+    tile_pass(a, tile, s_filt, filt_on, s_filt + 64, qw, hq, np, nl);
     tile_publish(a, tile, hq, np, nl, wq16, wn);
     last = tile;
   }
@@ -1395,7 +1429,7 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
     // rows that ran in the previous step: their records go to prev_rec
     const bool run = ((qw[0] | qw[1]) & 0x10101010u) != 0;
     const bool any_run = __syncthreads_or(run);
-    if (any_run || S.has) extract_tile(a, tile, qw, S, red64, S.has != 0);
+    if (any_run || S.has) extract_tile(a, tile, qw, S, red64, S.has != 0, dsm + 1024);
     __syncthreads();  // S reuse
     if (stamps && tid == 0) {
       atomicMax(&ctl->dbg[61], (unsigned long long)(xc1 - xc0));            // selection, cycles
@@ -1425,7 +1459,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_fin(const __grid_constant__ Step
 // ---------------------------------------------------------------------------------------------
 cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                             const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
-                            CompRec* rec_out, bool apply, CandRec* prev_rec) {
+                            CompRec* rec_out, bool apply, uint32_t* prev_rec) {
   // size the CTA to the record count: a typical step completes ~BS/mean-decode calls
   if (n <= 32)
     return launch_pdl(k_complete<32>, 1, 32, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, prev_rec);

@@ -20,8 +20,19 @@ __global__ void __launch_bounds__(512, 2) k(const uint4* in, uint4* wr, uint4* x
       wr[(size_t)blockIdx.x * 1024 + tid] = acc;
       wr[(size_t)blockIdx.x * 1024 + 512 + tid] = acc;
     }
-    if (blockIdx.x == 0)
-      for (int r = 0; r < 6; ++r) xrec[r * 512 + tid] = make_uint4(tid, r, 1, 2);
+    if (blockIdx.x == 0) {
+      if (burst < 2) {
+        for (int r = 0; r < 6; ++r) xrec[r * 512 + tid] = make_uint4(tid, r, 1, 2);
+      } else {
+        // like the extraction: 48-B records, thread t writes records 8t' .. (rows of one thread),
+        // 3 x 16 B each, lanes 8 records apart (scattered partial sectors)
+        for (int k = 0; k < 2; ++k) {
+          const uint32_t rec = (tid % 128) * 8 + (tid / 128) * 2 + k;  // 1024 records
+          uint4* d = xrec + rec * 3;
+          d[0] = make_uint4(rec, 1, 2, 3); d[1] = make_uint4(4, 5, 6, 7); d[2] = make_uint4(8, 0, 0, 0);
+        }
+      }
+    }
     __syncthreads();
     if (tid == 0) { __threadfence(); atomicAdd(bar, 1u); }
     return;
@@ -44,7 +55,7 @@ int main() {
   cudaMalloc(&in, 246ull * 3584 * 16); cudaMalloc(&wr, 246ull * 1024 * 16); cudaMalloc(&xrec, 6 * 512 * 16);
   cudaMalloc(&bar, 4); cudaMemset(bar, 0, 4); cudaMallocManaged(&out, 64);
   void* fl; cudaMalloc(&fl, 512u << 20);
-  for (int burst = 0; burst < 2; ++burst)
+  for (int burst = 0; burst < 3; ++burst)
     for (int flush = 0; flush < 2; ++flush)
       for (int rep = 0; rep < 3; ++rep) {
         if (flush) cudaMemset(fl, rep, 512u << 20);
