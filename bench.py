@@ -115,13 +115,13 @@ def phase_spans(phase):
         rows.append({n: (c[i - 40] - c[0]) / 1e3 for n, i in PHASES if c[i - 40]})
         rows[-1].update({"cyc_xrec_loads": c[18], "cyc_prev_loads": c[19], "cyc_scan": c[20],
                          "cyc_select_max": c[21], "cyc_extract_max": c[22], "tiles_with_candidates": c[23],
-                         "tiles_with_running": int(p[88]), "max_selected_per_thread": int(p[89]),
-                         "cyc_extract_store_thread_max": int(p[90])})
+                         "tiles_with_running": int(p[88]), "cyc_x_rank": int(p[89]),
+                         "cyc_x_compact": int(p[90]), "cyc_x_copy": int(p[91]), "x_rows_copied_max": int(p[92])})
     if not rows:
         return None
     names = [n for n, _ in PHASES] + ["cyc_xrec_loads", "cyc_prev_loads", "cyc_scan", "cyc_select_max",
                                       "cyc_extract_max", "tiles_with_candidates", "tiles_with_running",
-                                      "max_selected_per_thread", "cyc_extract_store_thread_max"]
+                                      "cyc_x_rank", "cyc_x_compact", "cyc_x_copy", "x_rows_copied_max"]
     return {n: round(float(np.median([r[n] for r in rows if n in r])), 2) for n in names
             if any(n in r for r in rows)}
 

@@ -329,35 +329,48 @@ __global__ void __launch_bounds__(ST_THREADS) k_prologue(const __grid_constant__
 // ---------------------------------------------------------------------------------------------
 // In-kernel synchronisation of the step kernel.  Its grid is launched cooperatively (every CTA is
 // co-resident), so CTAs may wait for each other: a CTA barrier orders the CTA's writes before
-// thread 0's gpu-scope fence + release increment; waiters poll with acquire loads.  Data written
-// by other CTAs in this kernel is read with ld.cg (L2), never through L1 or the read-only path.
+// thread 0's gpu-scope fence and relaxed increment (a release pattern); a waiter polls with
+// relaxed loads and fences once when the condition holds (an acquire pattern).  Polling with
+// ld.acquire would invalidate the SM's whole L1 (CCTL.IVALL) at every poll, under the feet of the
+// other CTA on the SM (measured: every phase of the step 3-5x slower).  Data written by other
+// CTAs in this kernel is read with ld.cg (L2), never through L1 or the read-only path.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  const uint32_t v = ld_relaxed_u32(p);
+  fence_acq_rel();
   return v;
 }
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void red_release_add_u32(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void red_relaxed_add_u32(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void grid_arrive(uint32_t* ctr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    red_release_add_u32(ctr, 1u);
+    red_relaxed_add_u32(ctr, 1u);
   }
 }
 __device__ __forceinline__ void grid_wait(const uint32_t* ctr, uint32_t target) {
-  if (threadIdx.x == 0)
-    while (ld_acquire_u32(ctr) < target) __nanosleep(20);
+  if (threadIdx.x == 0) {
+    while (ld_relaxed_u32(ctr) < target) __nanosleep(20);
+    fence_acq_rel();
+  }
   __syncthreads();
 }
 __device__ __forceinline__ void wait_prologue(const Ctl* ctl, uint32_t seqno) {
-  if (threadIdx.x == 0)
-    while (ld_acquire_u32(&ctl->pro_seq) != seqno) __nanosleep(20);
+  if (threadIdx.x == 0) {
+    while (ld_relaxed_u32(&ctl->pro_seq) != seqno) __nanosleep(20);
+    fence_acq_rel();
+  }
   __syncthreads();
 }
 
@@ -666,7 +679,7 @@ __device__ void select_for(const StepArgs& a, uint32_t tile, SelSmem& S) {
 // cooperative: the owning threads only publish each row's position in shared memory, then all
 // threads copy the rows in [lo, hi] with consecutive rows on consecutive lanes (coalesced loads
 // from the table, coalesced stores into the struct-of-arrays records), whichever threads own them.
-// sm: >= TILE * 3 + 64 bytes of shared scratch.
+// sm: >= TILE * 5 + 64 bytes of shared scratch.
 __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&qw)[2], const SelSmem& S,
                              unsigned long long* red64, bool ranks, unsigned char* sm) {
   constexpr int NT = ST_THREADS;
@@ -680,6 +693,7 @@ __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&
   uint32_t* s_rng = reinterpret_cast<uint32_t*>(sm + 3 * TILE); // [2 * NW] per-warp lo / hi
   uint32_t pos2[4];  // positions of rows 2k, 2k+1 in 16-bit halves (BS <= 2048)
   uint32_t sel = 0, runm = 0;
+  const long long et0 = clock64();
 #pragma unroll
   for (int k = 0; k < 4; ++k) pos2[k] = 0xFFFFFFFFu;
 #pragma unroll
@@ -714,47 +728,77 @@ __device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&
       }
     }
   }
-  // publish positions and flags; the tile's range of rows to copy
+  const long long et1 = clock64();
+  // publish positions and flags, and compact the rows to copy into a list (warp-aggregated
+  // reservations: rows stay in order inside a warp's chunk)
   const uint32_t need = sel | runm;
   reinterpret_cast<uint4*>(s_px)[tid] = make_uint4(pos2[0], pos2[1], pos2[2], pos2[3]);
   reinterpret_cast<uint2*>(s_qf)[tid] = make_uint2(qw[0], qw[1]);
-  uint32_t lo = need ? l0 + __ffs(need) - 1 : 0xFFFFFFFFu;
-  uint32_t hi = need ? l0 + 31 - __clz(need) : 0u;
-  lo = __reduce_min_sync(0xffffffffu, lo);
-  hi = __reduce_max_sync(0xffffffffu, hi);
-  if (lane_id() == 0) {
-    s_rng[warp_id()] = lo;
-    s_rng[NT / 32 + warp_id()] = hi;
+  uint16_t* s_list = reinterpret_cast<uint16_t*>(sm + 3 * TILE + 64);  // [TILE] local rows to copy
+  uint32_t* s_n = s_rng;
+  if (tid == 0) *s_n = 0;
+  __syncthreads();
+  {
+    const uint32_t cnt = __popc(need);
+    const uint32_t incl = warp_incl_scan(cnt);
+    const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t wbase = 0;
+    if (lane_id() == 31 && wtot) wbase = atomicAdd(s_n, wtot);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    uint32_t o = wbase + incl - cnt;
+    for (uint32_t nd = need; nd; nd &= nd - 1) s_list[o++] = (uint16_t)(l0 + __ffs(nd) - 1);
   }
   __syncthreads();
-  lo = 0xFFFFFFFFu;
-  hi = 0;
-#pragma unroll
-  for (int w = 0; w < NT / 32; ++w) {
-    lo = min(lo, s_rng[w]);
-    hi = max(hi, s_rng[NT / 32 + w]);
-  }
+  const uint32_t n_copy = *s_n;
+  const long long et2 = clock64();
   const CallTable& ct = a.ct;
   const RecSoA& xs = a.out.xs;
   const RecSoA& ps = a.out.ps;
-  for (uint32_t l = lo + tid; l <= hi && lo != 0xFFFFFFFFu; l += NT) {
-    const uint32_t px = s_px[l];
-    const uint32_t qf = (s_qf[l >> 2] >> (8 * (l & 3))) & 0xFFu;
-    const bool run = !(qf & QF_DEAD) && (qf & QF_RUN);
-    if (px == 0xFFFFu && !run) continue;
-    const uint32_t r = tile0 + l;
-    const unsigned long long cid = ct.cid[r];
-    const uint32_t arr = ct.arr[r], tok = ct.tok[r], ex = ct.exec[r];
-    const uint32_t mt = __ldcg(ct.mtime + r), qt = __ldcg(ct.quanta + r);  // (promotions of this kernel)
-    const uint32_t bx = run ? ct.bidx[r] : 0u;
-    const uint32_t qfb = qf | (run ? bx << 8 : 0u);
-    if (px != 0xFFFFu) {
-      xs.cid[px] = cid; xs.slot[px] = r; xs.arr[px] = arr; xs.tok[px] = tok;
-      xs.exec[px] = ex; xs.mt[px] = mt; xs.qt[px] = qt; xs.qfb[px] = qfb;
+  // two rows per thread per round, all loads of a round issued before any store
+  for (uint32_t i0 = tid; i0 < n_copy; i0 += 2 * NT) {
+    uint32_t lr[2], r[2], arr[2], tok[2], ex[2], mt[2], qt[2], bx[2];
+    unsigned long long cid[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t i = i0 + u * NT;
+      ok[u] = i < n_copy;
+      lr[u] = ok[u] ? s_list[i] : 0u;
+      r[u] = tile0 + lr[u];
+      cid[u] = ok[u] ? ct.cid[r[u]] : 0ull;
+      arr[u] = ok[u] ? ct.arr[r[u]] : 0u;
+      tok[u] = ok[u] ? ct.tok[r[u]] : 0u;
+      ex[u] = ok[u] ? ct.exec[r[u]] : 0u;
+      mt[u] = ok[u] ? __ldcg(ct.mtime + r[u]) : 0u;  // (promotions of this kernel)
+      qt[u] = ok[u] ? __ldcg(ct.quanta + r[u]) : 0u;
+      bx[u] = ok[u] ? ct.bidx[r[u]] : 0u;
     }
-    if (run) {
-      ps.cid[bx] = cid; ps.slot[bx] = r; ps.arr[bx] = arr; ps.tok[bx] = tok;
-      ps.exec[bx] = ex; ps.mt[bx] = mt; ps.qt[bx] = qt; ps.qfb[bx] = qfb;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      const uint32_t l = lr[u];
+      const uint32_t px = s_px[l];
+      const uint32_t qf = (s_qf[l >> 2] >> (8 * (l & 3))) & 0xFFu;
+      const bool run = !(qf & QF_DEAD) && (qf & QF_RUN);
+      const uint32_t qfb = qf | (run ? bx[u] << 8 : 0u);
+      if (px != 0xFFFFu) {
+        xs.cid[px] = cid[u]; xs.slot[px] = r[u]; xs.arr[px] = arr[u]; xs.tok[px] = tok[u];
+        xs.exec[px] = ex[u]; xs.mt[px] = mt[u]; xs.qt[px] = qt[u]; xs.qfb[px] = qfb;
+      }
+      if (run) {
+        const uint32_t b = bx[u];
+        ps.cid[b] = cid[u]; ps.slot[b] = r[u]; ps.arr[b] = arr[u]; ps.tok[b] = tok[u];
+        ps.exec[b] = ex[u]; ps.mt[b] = mt[u]; ps.qt[b] = qt[u]; ps.qfb[b] = qfb;
+      }
+    }
+  }
+  if (STAMPS_ON(a.pol)) {
+    __syncthreads();
+    if (tid == 0) {
+      atomicMax(&a.ctl->dbg[36], (unsigned long long)(et1 - et0));
+      atomicMax(&a.ctl->dbg[37], (unsigned long long)(et2 - et1));
+      atomicMax(&a.ctl->dbg[38], (unsigned long long)(clock64() - et2));
+      atomicMax(&a.ctl->dbg[35], (unsigned long long)n_copy);
     }
   }
 }
@@ -1308,7 +1352,9 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
     ctl->dbg[88] = ctl->dbg[39];
     ctl->dbg[89] = ctl->dbg[36];
     ctl->dbg[90] = ctl->dbg[37];
-    ctl->dbg[39] = ctl->dbg[36] = ctl->dbg[37] = 0;
+    ctl->dbg[91] = ctl->dbg[38];
+    ctl->dbg[92] = ctl->dbg[35];
+    ctl->dbg[39] = ctl->dbg[36] = ctl->dbg[37] = ctl->dbg[38] = ctl->dbg[35] = 0;
     ctl->dbg[40] = ~0ull;
   }
 }
@@ -1398,8 +1444,10 @@ __global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ 
   uint32_t qw[2];
   uint32_t last = NONE;
   if (a.pro_first) {
-    if (tid == 0)
-      while (ld_acquire_u32(&ctl->go_seq) != a.seqno) __nanosleep(20);
+    if (tid == 0) {
+      while (ld_relaxed_u32(&ctl->go_seq) != a.seqno) __nanosleep(20);
+      fence_acq_rel();
+    }
     __syncthreads();
   }
   for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
