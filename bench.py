@@ -97,38 +97,33 @@ def make_trace(name, active, seed_off=0):
     return churn(active, seed=BASE_SEED + 100 + seed_off)
 
 
-PHASES = [("first_cta_start", 40), ("last_cta_start", 41), ("prologue_completions", 57), ("prologue_done", 42),
-          ("last_tile_at_barrier1", 48), ("barrier1_passed", 43), ("tile0_selection", 54), ("tile0_extraction", 55),
-          ("last_tile_at_barrier2", 56), ("barrier2_passed", 44), ("finalize_loads", 49), ("region_b", 45),
-          ("key_order", 50), ("cutoff", 46), ("batch_admit", 51), ("preempt", 52), ("accounting_kv", 53),
-          ("end", 47)]
+CHAIN = ["prologue", "scan", "select", "gather", "rank", "finalize"]
 
 
-def phase_spans(phase):
-    """Median times in us of the step kernel's phases relative to its first CTA's start, from the
-    %globaltimer stamps of the last step (autx_phase_times [64, 80))."""
+def chain_spans(phase):
+    """Median (CTA 0 past griddepcontrol.wait, latest CTA end, latest CTA past the wait) in us of
+    each kernel of the step chain, relative to the first kernel's CTA 0, from the library's
+    %globaltimer chain stamps (autx_set_timing mode 2: autx_phase_times [64, 96))."""
     rows = []
     for p in phase:
-        c = [int(x) for x in p[64:89]]
-        if not c[0] or c[0] == (1 << 64) - 1 or not c[7]:
+        c = [int(x) for x in p[64:96]]
+        starts = [c[3 * k] for k in range(6) if c[3 * k]]
+        if not starts:
             continue
-        rows.append({n: (c[i - 40] - c[0]) / 1e3 for n, i in PHASES if c[i - 40]})
-        rows[-1].update({"cyc_xrec_loads": c[18], "cyc_prev_loads": c[19], "cyc_scan": c[20],
-                         "cyc_select_max": c[21], "cyc_extract_max": c[22], "tiles_with_candidates": c[23],
-                         "tiles_with_running": int(p[88]), "cyc_x_rank": int(p[89]),
-                         "cyc_x_compact": int(p[90]), "cyc_x_copy": int(p[91]), "x_rows_copied_max": int(p[92])})
-    if not rows:
-        return None
-    names = [n for n, _ in PHASES] + ["cyc_xrec_loads", "cyc_prev_loads", "cyc_scan", "cyc_select_max",
-                                      "cyc_extract_max", "tiles_with_candidates", "tiles_with_running",
-                                      "cyc_x_rank", "cyc_x_compact", "cyc_x_copy", "x_rows_copied_max"]
-    return {n: round(float(np.median([r[n] for r in rows if n in r])), 2) for n in names
-            if any(n in r for r in rows)}
+        t0 = min(starts)
+        rows.append({n: (c[3 * k] - t0, c[3 * k + 1] - t0, c[3 * k + 2] - t0) for k, n in enumerate(CHAIN)
+                     if c[3 * k]})
+    out = {}
+    for n in CHAIN:
+        v = [r[n] for r in rows if n in r]
+        if v:
+            out[n] = [round(float(np.median([x[i] for x in v])) / 1e3, 2) for i in range(3)]
+    return out or None
 
 
 def ncu_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per k_step launch from the committed
-    `ncu --set full` capture summary (profiles/step_traffic.json), or None."""
+    """dram__bytes_read.sum + dram__bytes_write.sum of one step's kernels (summed over the chain)
+    from the committed `ncu --set full` capture summary (profiles/step_traffic.json), or None."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "step_traffic.json")))
         return d["dram_bytes_per_launch"], d.get("source")
@@ -434,7 +429,17 @@ def main():
         dist.barrier()
     ck = clocks.stop(local)
     st = s.step_stats()                       # selection shape of the last timed step
-    # phase stamps inside the step kernel, a separate pass (the stamps add a few global stores)
+    # per-kernel device time: a separate pass with the library's CUDA events between the chain's
+    # kernels (events serialise the PDL chain, so the parts add up to more than a step)
+    s.set_timing(True)
+    ev_ms = {"scan": [], "select+gather": [], "rank+finalize": []}
+    for _ in range(30):
+        timed_step()
+        tm = s.last_step_timing()
+        ev_ms["scan"].append(tm.scan_ms)
+        ev_ms["select+gather"].append(tm.select_ms)
+        ev_ms["rank+finalize"].append(tm.finalize_ms)
+    # the undisturbed chain: %globaltimer stamps inside the kernels (no events), another pass
     s.set_timing(False, stamps=True)
     stamp_phase, stats = [], []
     for _ in range(30):
@@ -442,7 +447,7 @@ def main():
         stamp_phase.append(s.phase_times().astype(np.int64))
         stats.append(s.step_stats())
     s.set_timing(False)
-    spans = phase_spans(stamp_phase)
+    spans = chain_spans(stamp_phase)
     total_ms = sum(ms)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -476,10 +481,13 @@ def main():
     algo_bytes = ALGO_BYTES_PER_CALL * n_active + ALGO_BYTES_PER_PROGRAM * n_programs
     design_bytes = DESIGN_BYTES_PER_ROW * st["n_rows"] + DESIGN_BYTES_PER_PROGRAM * n_programs
     achieved = algo_bytes / (ms_per_step * 1e-3) / 1e9
+    ev_mean = {k: statistics.mean(v) for k, v in ev_ms.items()}
+    span_k = {k: round(v[1] - v[0], 2) for k, v in (spans or {}).items()}
+    dominant = max(span_k, key=span_k.get) if span_k else None
     traffic_bytes, traffic_src = ncu_traffic()
     if args.workload != "mcts" or args.order != "select" or wl["policy"] != "atlas" or args.beta != "2":
         traffic_bytes, traffic_src = None, "no ncu capture of this configuration"
-    span_us = spans["end"] if spans else None
+    span_us = spans["finalize"][1] if spans and "finalize" in spans else None
     result = {
         "metric": "sched decisions/s at 1M active calls", "value": value, "unit": "decisions/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -495,23 +503,28 @@ def main():
                    "parallelism": f"engines{world} (one scheduler per GPU)"},
         "gpu_launches": launches,
         "kernels_per_step": launches / args.steps,
-        "roofline": {"bound": "hbm", "kernel": "k_step (the whole step: one cooperative kernel)"
-                     if args.order == "select" else "radix order (prologue + k_keys + LSD passes + k_take + k_fin)",
+        "roofline": {"bound": "hbm", "kernel": "the step (one graph launch of the PDL chain k_prologue -> "
+                     "k_scan_tile -> k_gather_ss -> k_rank -> k_finalize)" if args.order == "select" else
+                     "the step (prologue + k_keys + LSD passes + k_take + k_rank + k_finalize)",
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": traffic_bytes, "traffic_source": traffic_src,
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": int(algo_bytes),
                      "algorithmic_bytes": "SURVEY 8(d): 52 B per active call + 16 B per program",
                      "timing": "CUDA events around each step's launch, L2 flushed before it (= ms_per_step)",
-                     "dominant_kernel_share": 1.0 if args.order == "select" else None,
+                     "dominant_kernel": dominant,
+                     "dominant_by": "longest span inside the undisturbed chain (%globaltimer, CTA 0 past the PDL "
+                                    "wait to the latest CTA end); see chain_us, kernel_event_ms and profiles/",
                      "design_bytes_per_launch": int(design_bytes),
                      "design_bytes": "13 B per table row (qf, prog, base, mtime) + 12 B per program row",
-                     "span_us": span_us,
-                     "frac_span": round(algo_bytes / (span_us * 1e-6) / 1e9 / hbm_peak, 4) if span_us else None,
-                     "span_source": "%globaltimer: first CTA start to the end of the finalize (30 steps, median)"},
+                     "chain_span_us": span_us,
+                     "chain_span_source": "%globaltimer: the first kernel's CTA 0 to the finalize's end (30 steps, "
+                                          "median); the rest of ms_per_step is launch and event overhead"},
         "step_ms": {"p10": float(np.percentile(ms, 10)), "p50": float(np.percentile(ms, 50)),
                     "p90": float(np.percentile(ms, 90)), "mean": statistics.mean(ms)},
-        "phases_us": spans,
+        "chain_us": spans,
+        "kernel_span_us": span_k,
+        "kernel_event_ms": ev_mean,
         "state": {"promotions_per_step": statistics.mean(promoted),
                   "completions_per_step": statistics.mean(comps), "arrivals_per_step": statistics.mean(arrs),
                   "qstar": st["qstar"], "mprime": st["mprime"], "region_a": st["n_x"],

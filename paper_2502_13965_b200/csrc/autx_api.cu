@@ -5,7 +5,6 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstddef>
-#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -19,6 +18,7 @@
 using namespace autx;
 
 unsigned long long autx::g_kernel_launches = 0;
+thread_local std::vector<autx::LaunchRec>* autx::g_launch_rec = nullptr;
 
 extern "C" uint64_t autx_kernel_launches(void) {
   return __atomic_load_n(&g_kernel_launches, __ATOMIC_RELAXED);
@@ -38,8 +38,6 @@ struct autx_ctx {
   bool kv_on = false;
   // pinned staging (device reads it through UVA)
   uint32_t* h_cslots = nullptr;  // [max_batch * 4] completion slots
-  uint32_t* h_cprog = nullptr;   // [max_batch * 4] their process-table rows (the scan's filter)
-  uint32_t capacity = 0;         // co-resident CTAs of the step kernel on this device
   uint32_t cslots_cap = 0;
   ArrivalRec* h_arr = nullptr;
   uint32_t arr_cap = 0;
@@ -112,8 +110,20 @@ struct autx_ctx {
   uint32_t* h_clin = nullptr;                      // [cslots_cap] lineage of each completion (pinned)
   uint32_t* h_par = nullptr;                       // parents' lineage indices of staged arrivals (pinned)
   uint32_t par_cap = 0, n_par_staged = 0;
-  bool timed_complete = false;  // events 4-5 (multi-engine k_complete) recorded this step
-  bool tc_step = false;         // ... for the step being waited on
+  // the step's kernels replayed as a CUDA graph: one executable per launch signature (kernels,
+  // block shapes, shared memory), whose kernel nodes receive each step's parameters
+  struct StepGraph {
+    std::vector<const void*> funcs;
+    std::vector<dim3> blocks;
+    std::vector<size_t> smem;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+    std::vector<cudaGraphNode_t> nodes;
+  };
+  std::vector<StepGraph> graphs;
+  cudaStream_t cap_stream = nullptr;  // capture only (the legacy stream cannot be captured)
+  bool timed_complete = false, timed_register = false;   // events 4-5 / 6-7 recorded this step
+  bool tc_step = false, tr_step = false;                  // ... for the step being waited on
   std::string err;
 };
 
@@ -161,15 +171,7 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&p.info, P)); CK(dalloc(&p.last_arr, P)); CK(dalloc(&p.last_comp, P));
   CK(cudaMemsetAsync(p.info, 0, P * sizeof(PInfo), ctx->stream));
   CK(dalloc(&ctx->ctl, 1));
-  {
-    static Ctl init;  // pinned copy not needed: synchronised below, before autx_create returns
-    memset(&init, 0, sizeof init);
-    init.dbg[40] = ~0ull;  // first-CTA-start stamp (a minimum)
-    init.free_top = c.n_gpu_blocks;
-    init.rs_free_top = c.n_gpu_blocks > 0 ? c.max_batch : 0;
-    CK(cudaMemcpyAsync(ctx->ctl, &init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-  }
+  CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
   Outputs& o = ctx->out;
   uint32_t BS = c.max_batch;
   size_t ntiles = rows / TILE + 1;
@@ -189,10 +191,17 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   o.preempt_ids = o.admit_ids + BSp; CK(dalloc(&o.prev_slots, BS)); CK(dalloc(&o.preempt_slots, BS));
   o.batch_slots = reinterpret_cast<uint32_t*>(o.preempt_ids + BSp);
   CK(dalloc(&o.admit_slots, BS));
-  for (RecSoA* r : {&o.xs, &o.ps}) {
-    CK(dalloc(&r->cid, BS)); CK(dalloc(&r->slot, BS)); CK(dalloc(&r->arr, BS)); CK(dalloc(&r->tok, BS));
-    CK(dalloc(&r->exec, BS)); CK(dalloc(&r->mt, BS)); CK(dalloc(&r->qt, BS)); CK(dalloc(&r->qfb, BS));
-  }
+  o.cand_cap = 2 * BS;
+  CK(dalloc(&o.cand, o.cand_cap));
+  CK(dalloc(&o.cand_rec, o.cand_cap));
+  CK(dalloc(&o.prev_rec, BS));
+  CK(dalloc(&o.ckey, 2 * BS));
+  CK(dalloc(&o.ckvb, 2 * BS));
+  CK(dalloc(&o.skey, 2 * BS));
+  CK(dalloc(&o.sidx, 2 * BS));
+  CK(dalloc(&o.srec, 2 * BS));
+  CK(dalloc(&o.prev_pos, BS));
+  CK(cudaMemsetAsync(o.prev_pos, 0, (size_t)BS * 8, ctx->stream));  // seqno 0 never matches
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K));
   CK(dalloc(&o.sup_cnt, (ntiles / SUP_TILES + 1) * MAX_K));
   CK(cudaMemsetAsync(o.sup_cnt, 0, (ntiles / SUP_TILES + 1) * MAX_K * sizeof(uint32_t), ctx->stream));
@@ -204,7 +213,6 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   ctx->ran_seq.assign(rows, 0);
   ctx->cslots_cap = 4 * BS;
   CK(cudaHostAlloc((void**)&ctx->h_cslots, ctx->cslots_cap * 4, cudaHostAllocMapped));
-  CK(cudaHostAlloc((void**)&ctx->h_cprog, ctx->cslots_cap * 4, 0));
   ctx->arr_cap = 4 * BS;
   CK(cudaHostAlloc((void**)&ctx->h_arr, ctx->arr_cap * sizeof(ArrivalRec), cudaHostAllocMapped));
   CK(dalloc(&ctx->d_cslots, ctx->cslots_cap));
@@ -260,7 +268,12 @@ static autx_status alloc_tables(autx_ctx* ctx) {
     kv.plan_cap = c.n_gpu_blocks;
     CK(dalloc(&kv.plan_out_blocks, kv.plan_cap)); CK(dalloc(&kv.plan_in_blocks, kv.plan_cap));
     CK(dalloc(&kv.bt_offsets, BS + 1)); CK(dalloc(&kv.bt_blocks, kv.plan_cap));
-    CK(cudaStreamSynchronize(ctx->stream));  // the host vectors above go out of scope
+    Ctl init{};
+    memset(&init, 0, sizeof init);
+    init.free_top = c.n_gpu_blocks;
+    init.rs_free_top = BS;
+    CK(cudaMemcpyAsync(ctx->ctl, &init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // fs, rs, init go out of scope
   }
   return AUTX_OK;
 }
@@ -312,20 +325,21 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
   p.max_blocks_per_call = c.max_blocks_per_call;
   p.host_pages_lo = (uint32_t)std::min<uint64_t>(c.host_pages, 0xFFFFFFF0ull);
   ctx->device = c.device;
+  p.device = c.device;
   if (cudaSetDevice(c.device) != cudaSuccess) {
     autx_status s = fail(ctx, AUTX_E_CUDA, "cudaSetDevice(%d) failed", c.device);
+    delete ctx;
+    return s;
+  }
+  if (cudaError_t e = step_kernels_setup(); e != cudaSuccess) {
+    autx_status s = fail(ctx, AUTX_E_CUDA, "step kernel setup: %s", cudaGetErrorString(e));
+    fprintf(stderr, "autx_create: %s\n", ctx->err.c_str());
     delete ctx;
     return s;
   }
   // NULL = the legacy default stream (what torch.cuda.current_stream() is by default), so
   // library work orders with the caller's default-stream work
   ctx->stream = (cudaStream_t)c.stream;
-  if (cudaError_t e = step_kernel_setup(c.max_batch, &ctx->capacity); e != cudaSuccess) {
-    autx_status s = fail(ctx, AUTX_E_CUDA, "step kernel setup: %s", cudaGetErrorString(e));
-    fprintf(stderr, "autx_create: %s\n", ctx->err.c_str());
-    delete ctx;
-    return s;
-  }
   autx_status s = alloc_tables(ctx);
   if (s == AUTX_OK) {
     if (cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming) != cudaSuccess) s = AUTX_E_CUDA;
@@ -348,23 +362,24 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   CallTable& t = ctx->ct;
   void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
-                 t.loc, t.hcls, t.bidx, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
+                 t.loc, t.hcls, t.bidx, ctx->out.prev_pos, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
                  ctx->ctl, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
-                 ctx->out.admit_slots, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
+                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.ckvb, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
                  ctx->kv.bt_offsets, ctx->kv.bt_blocks, ctx->d_pools, ctx->staging,
                  ctx->d_route_local, ctx->d_pin, ctx->d_rarr, ctx->d_rout,
                  ctx->rx.keys, ctx->rx.keys_alt, ctx->rx.dig_hist, ctx->rx.tile_hist};
   for (void* p : dev) if (p) cudaFree(p);
-  for (RecSoA* r : {&ctx->out.xs, &ctx->out.ps}) {
-    void* f[] = {r->cid, r->slot, r->arr, r->tok, r->exec, r->mt, r->qt, r->qfb};
-    for (void* p : f) if (p) cudaFree(p);
-  }
   void* host[] = {ctx->h_outblk,
-                  ctx->h_cslots, ctx->h_cprog, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr, ctx->h_clin, ctx->h_par,
+                  ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr, ctx->h_clin, ctx->h_par,
                   ctx->rx.h_dig_hist};
   for (void* p : host) if (p) cudaFreeHost(p);
+  for (auto& g : ctx->graphs) {
+    if (g.x) cudaGraphExecDestroy(g.x);
+    if (g.g) cudaGraphDestroy(g.g);
+  }
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   if (ctx->done) cudaEventDestroy(ctx->done);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->sev) if (e) cudaEventDestroy(e);
@@ -466,7 +481,6 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
   for (uint32_t i = 0; i < n; ++i) {
     const uint32_t slot = sl[i];
     ctx->h_cslots[i] = slot;
-    ctx->h_cprog[i] = ctx->slot_prog[slot];
     if (ctx->eq2) ctx->h_clin[i] = ctx->lin_of.at(ids[i]);
     ctx->slot_live[slot] = 0;
     ctx->prog_active[ctx->slot_prog[slot]] -= 1;
@@ -481,7 +495,7 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
     if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
     CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
     CK(launch_complete(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->h_cslots, n, t, ctx->kv,
-                       ctx->kv_on, recs, false, ctx->out.ps.qfb));
+                       ctx->kv_on, recs, false));
     if (ctx->timing) {
       cudaEventRecord(ctx->ev[5], ctx->stream);
       ctx->timed_complete = true;
@@ -494,77 +508,47 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
 
 static autx_status compact(autx_ctx* ctx);
 
-// The parameter block of step t's kernels, without the prologue's records.
-static void step_args(autx_ctx* ctx, StepArgs& a, uint32_t t) {
-  memset(&a, 0, offsetof(StepArgs, pro) + offsetof(PrologueArgs, comp));
-  a.pol = ctx->pol;
-  a.ct = ctx->ct;
-  a.pt = ctx->pt;
-  a.ctl = ctx->ctl;
-  a.out = ctx->out;
-  a.kv = ctx->kv;
-  a.rec_out = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
-  a.kv_on = ctx->kv_on ? 1u : 0u;
-  a.t = t;
-  a.n_rows = ctx->tail;
-  a.seqno = ctx->seqno;
-  a.first_new = NONE;
-}
-
-// Moves the staged completions (and arrivals) of step t into the prologue's parameters: inline
-// when they fit, else through the pinned staging buffers (read through UVA).
-static void stage_prologue(autx_ctx* ctx, StepArgs& a, uint32_t t, bool with_arrivals) {
-  PrologueArgs& p = a.pro;
-  p.n_comp = ctx->n_comp_staged;
-  p.n_arr = with_arrivals ? ctx->n_arr_staged : 0;
-  p.first_slot = ctx->arr_first_slot;
-  p.t = t;
-  p.n_prog_rows = ctx->prog_next;
-  if (p.n_comp <= (uint32_t)PRO_INLINE) {
-    memcpy(p.comp, ctx->h_cslots, p.n_comp * sizeof(uint32_t));
-    memcpy(p.comp_prog, ctx->h_cprog, p.n_comp * sizeof(uint32_t));
-  } else {
-    p.comp_ptr = ctx->h_cslots;
-  }
-  if (p.n_arr <= (uint32_t)PRO_INLINE) memcpy(p.arr, ctx->h_arr, p.n_arr * sizeof(ArrivalRec));
-  else p.arr_ptr = ctx->h_arr;
-  p.comp_lin = ctx->h_clin;  // AUTX_ATLAS_EQ2 only (read through UVA)
-  p.par = ctx->h_par;
-  a.do_pro = (p.n_comp || p.n_arr) ? 1u : 0u;
-  // AUTX_DEFER_ALL=1 (test switch): every row waits for the prologue, as with records that do
-  // not fit the parameters
-  static const bool force_defer = getenv("AUTX_DEFER_ALL") != nullptr;
-  a.defer_all = (p.n_comp > (uint32_t)PRO_INLINE || force_defer) ? 1u : 0u;
-  a.first_new = p.n_arr ? p.first_slot : NONE;
-  static const bool pro_first = getenv("AUTX_PRO_FIRST") != nullptr;  // A/B switch
-  a.pro_first = (pro_first && a.do_pro && !a.defer_all) ? 1u : 0u;
-  static const bool warm = getenv("AUTX_WARM_PARAMS") != nullptr;
-  a.warm_params = warm ? 1u : 0u;
-}
-
-static void clear_staged(autx_ctx* ctx) {
-  ctx->n_comp_staged = ctx->n_arr_staged = 0;
-  ctx->n_par_staged = 0;
-  ctx->staged_new_progs.clear();
-}
-
-// Runs the staged completions and arrivals of step t now, ahead of the step kernel: before a
-// compaction, and for a bulk burst (> 4096 arrivals: one DMA and the multi-CTA registration
-// kernel, after a prologue kernel for the completions, R10).
+// Launches the staged completions and arrivals of step t: one prologue kernel whose inputs ride
+// in the kernel parameters when small; bulk arrivals (an offline burst) go through one DMA and
+// the multi-CTA registration kernel.
 static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
   if (ctx->n_comp_staged == 0 && ctx->n_arr_staged == 0) return AUTX_OK;
   const bool bulk = ctx->n_arr_staged > 4096;
-  StepArgs a;
-  step_args(ctx, a, t);
-  stage_prologue(ctx, a, t, !bulk);
-  if (a.do_pro) CK(launch_prologue(ctx->stream, a));
+  PrologueArgs a;
+  memset(&a, 0, offsetof(PrologueArgs, comp));
+  a.n_comp = ctx->n_comp_staged;
+  a.n_arr = bulk ? 0 : ctx->n_arr_staged;
+  a.first_slot = ctx->arr_first_slot;
+  a.t = t;
+  a.n_prog_rows = ctx->prog_next;
+  if (a.n_comp <= (uint32_t)PRO_INLINE) memcpy(a.comp, ctx->h_cslots, a.n_comp * sizeof(uint32_t));
+  else a.comp_ptr = ctx->h_cslots;
+  if (a.n_arr <= (uint32_t)PRO_INLINE) memcpy(a.arr, ctx->h_arr, a.n_arr * sizeof(ArrivalRec));
+  else a.arr_ptr = ctx->h_arr;
+  a.comp_lin = ctx->h_clin;  // AUTX_ATLAS_EQ2 only (read through UVA)
+  a.par = ctx->h_par;
+  CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
+  if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
+  if (a.n_comp || a.n_arr)
+    CK(launch_prologue(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->kv, ctx->kv_on, recs, a));
+  if (ctx->timing) {
+    cudaEventRecord(ctx->ev[5], ctx->stream);
+    ctx->timed_complete = true;
+  }
   if (bulk) {
+    if (ctx->timing) cudaEventRecord(ctx->ev[6], ctx->stream);
     CK(cudaMemcpyAsync(ctx->d_arr, ctx->h_arr, (size_t)ctx->n_arr_staged * sizeof(ArrivalRec),
                        cudaMemcpyHostToDevice, ctx->stream));
     CK(launch_register(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->d_arr, ctx->n_arr_staged,
                        ctx->arr_first_slot, t, ctx->h_par));
+    if (ctx->timing) {
+      cudaEventRecord(ctx->ev[7], ctx->stream);
+      ctx->timed_register = true;
+    }
   }
-  clear_staged(ctx);
+  ctx->n_comp_staged = ctx->n_arr_staged = 0;
+  ctx->n_par_staged = 0;
+  ctx->staged_new_progs.clear();
   return AUTX_OK;
 }
 
@@ -746,6 +730,77 @@ static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uin
   return AUTX_OK;
 }
 
+// Replays the recorded launches of one step as a CUDA graph: the step is a launch-bound chain of
+// a few small kernels, and one graph launch plus per-node parameter updates costs the host a
+// fraction of the separate launches.  The graph of a new launch signature is captured once (with
+// the PDL attribute, so consecutive kernel nodes keep their programmatic edges).
+static autx_status step_graph_run(autx_ctx* ctx, std::vector<LaunchRec>& recs) {
+  autx_ctx::StepGraph* sg = nullptr;
+  for (auto& g : ctx->graphs) {
+    bool same = g.funcs.size() == recs.size();
+    for (size_t i = 0; same && i < recs.size(); ++i)
+      same = g.funcs[i] == recs[i].func && g.blocks[i].x == recs[i].block.x && g.smem[i] == recs[i].smem;
+    if (same) { sg = &g; break; }
+  }
+  if (sg) {
+    for (size_t i = 0; i < recs.size(); ++i) {
+      std::vector<void*> ptrs = recs[i].ptrs();
+      cudaKernelNodeParams kp = {};
+      kp.func = const_cast<void*>(recs[i].func);
+      kp.gridDim = recs[i].grid;
+      kp.blockDim = recs[i].block;
+      kp.sharedMemBytes = (unsigned)recs[i].smem;
+      kp.kernelParams = ptrs.data();
+      CK(cudaGraphExecKernelNodeSetParams(sg->x, sg->nodes[i], &kp));
+    }
+  } else {
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    if (ctx->graphs.size() >= 8) {  // bounded cache
+      for (auto& g : ctx->graphs) { cudaGraphExecDestroy(g.x); cudaGraphDestroy(g.g); }
+      ctx->graphs.clear();
+    }
+    autx_ctx::StepGraph g;
+    CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t err = cudaSuccess;
+    for (auto& r : recs) {
+      std::vector<void*> ptrs = r.ptrs();
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = r.grid;
+      cfg.blockDim = r.block;
+      cfg.dynamicSmemBytes = r.smem;
+      cfg.stream = ctx->cap_stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      err = cudaLaunchKernelExC(&cfg, r.func, ptrs.data());
+      if (err != cudaSuccess) break;
+      cudaStreamCaptureStatus st;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      err = cudaStreamGetCaptureInfo(ctx->cap_stream, &st, nullptr, nullptr, &deps, &nd);
+      if (err != cudaSuccess || nd != 1) { if (err == cudaSuccess) err = cudaErrorUnknown; break; }
+      g.nodes.push_back(deps[0]);
+      g.funcs.push_back(r.func);
+      g.blocks.push_back(r.block);
+      g.smem.push_back(r.smem);
+    }
+    cudaGraph_t graph = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    if (err != cudaSuccess || e2 != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      return fail(ctx, AUTX_E_CUDA, "step graph capture: %s", cudaGetErrorString(err != cudaSuccess ? err : e2));
+    }
+    g.g = graph;
+    CK(cudaGraphInstantiate(&g.x, graph, 0));
+    ctx->graphs.push_back(std::move(g));
+    sg = &ctx->graphs.back();
+  }
+  CK(cudaGraphLaunch(sg->x, ctx->stream));
+  return AUTX_OK;
+}
+
 extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out* out) {
   if (!ctx || !out) return AUTX_E_INVAL;
   autx_status s = sync_last(ctx);
@@ -759,25 +814,31 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
     return fail(ctx, AUTX_E_STATE, "cannot skip steps while calls are active");
   if (ctx->cfg.nranks > 1 && !ctx->routed_this)
     return fail(ctx, AUTX_E_STATE, "multi-engine: autx_route_apply must run every step");
-  uint32_t arr_base = 0;
-  if (ctx->radix) {
-    while (ctx->low < ctx->tail && !ctx->slot_live[ctx->low]) ++ctx->low;
-    arr_base = ctx->low < ctx->tail ? ctx->slot_arr[ctx->low] : t;
-    if (t - arr_base >= (1u << 27)) return fail(ctx, AUTX_E_NOMEM, "arrival span exceeds the 27-bit key field");
-  }
-  // a bulk burst is registered by its own kernels first; a typical step's records ride in the
-  // step kernel's parameters
-  if (ctx->n_arr_staged > 4096) {
-    s = flush_staged(ctx, t);
+  // both orderings pack t - arrival (select: k_gather_ss / k_rank keys) or arrival - base (radix)
+  // into a 27-bit key field
+  while (ctx->low < ctx->tail && !ctx->slot_live[ctx->low]) ++ctx->low;
+  const uint32_t arr_base = ctx->low < ctx->tail ? ctx->slot_arr[ctx->low] : t;
+  if (t - arr_base >= (1u << 27)) return fail(ctx, AUTX_E_NOMEM, "arrival span exceeds the 27-bit key field");
+  // rows registered in this step start here (the scan reads older rows before the prologue ends)
+  const uint32_t first_new = ctx->n_arr_staged ? ctx->arr_first_slot : ctx->tail;
+  // the step's kernels as one graph replay (AUTX_NO_GRAPH: separate launches); not with the
+  // per-kernel timing events, the radix pipeline (host-synchronised passes) or a bulk burst (DMA)
+  static const bool no_graph = getenv("AUTX_NO_GRAPH") != nullptr;
+  std::vector<LaunchRec> recs;
+  const bool graph = !no_graph && !ctx->timing && !ctx->radix && ctx->n_arr_staged <= 4096;
+  if (graph) g_launch_rec = &recs;
+  s = flush_staged(ctx, t);
+  if (s) { g_launch_rec = nullptr; return s; }
+  ++ctx->seqno;
+  const cudaError_t le = launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv,
+                                     ctx->kv_on, t, ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr,
+                                     ctx->radix ? &ctx->rx : nullptr, arr_base, &ctx->radix_passes, first_new);
+  g_launch_rec = nullptr;
+  CK(le);
+  if (graph) {
+    s = step_graph_run(ctx, recs);
     if (s) return s;
   }
-  ++ctx->seqno;
-  StepArgs a;
-  step_args(ctx, a, t);
-  stage_prologue(ctx, a, t, true);
-  clear_staged(ctx);
-  CK(launch_step(ctx->stream, a, ctx->capacity, ctx->timing ? ctx->ev : nullptr, ctx->radix ? &ctx->rx : nullptr,
-                 arr_base, &ctx->radix_passes));
   if (!ctx->out.zero_copy)
     CK(cudaMemcpyAsync(ctx->h_outblk, ctx->d_outblk, ctx->outblk_bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->done, ctx->stream));
@@ -790,7 +851,8 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   ctx->routed_this = false;
   ctx->n_reg_this = 0;
   ctx->tc_step = ctx->timed_complete;
-  ctx->timed_complete = false;
+  ctx->tr_step = ctx->timed_register;
+  ctx->timed_complete = ctx->timed_register = false;
   ctx->n_completed_pending = 0;
   ctx->have_last_key = false;
   memset(out, 0, sizeof *out);
@@ -819,15 +881,19 @@ extern "C" autx_status autx_step_wait(autx_ctx* ctx, autx_step_out* out) {
   out->kv_blocks = h.kv_blocks;
   out->n_promoted = h.n_promoted;
   if (ctx->timing) {
-    float st = 0, d = 0;
-    cudaEventElapsedTime(&st, ctx->ev[0], ctx->ev[1]);
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+    float d = 0, e = 0;
     if (ctx->tc_step) cudaEventElapsedTime(&d, ctx->ev[4], ctx->ev[5]);
-    ctx->last_timing.scan_ms = st;  // the whole step kernel (select mode) / prologue + sort + finalize (radix)
-    ctx->last_timing.select_ms = 0;
-    ctx->last_timing.finalize_ms = 0;
+    if (ctx->tr_step) cudaEventElapsedTime(&e, ctx->ev[6], ctx->ev[7]);
+    ctx->last_timing.scan_ms = a;
+    ctx->last_timing.select_ms = b;
+    ctx->last_timing.finalize_ms = c;
     ctx->last_timing.complete_ms = d;
-    ctx->last_timing.register_ms = 0;
-    ctx->last_timing.total_ms = st + d;
+    ctx->last_timing.register_ms = e;
+    ctx->last_timing.total_ms = a + b + c + d + e;
   }
   return AUTX_OK;
 }
@@ -877,8 +943,9 @@ static autx_status compact(autx_ctx* ctx) {
   if (npv) CK(cudaMemcpyAsync(ctx->out.prev_slots, np.data(), np.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
   // dropped entries shift the previous-batch indices the running rows carry
   if (npv) CK(launch_set_bidx(ctx->stream, ctx->ct, ctx->out.prev_slots, npv));
-  CK(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->ctl) + offsetof(Ctl, n_prev), &npv, 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));  // np, npv, lv, old2new go out of scope
+  CK(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->ctl) + offsetof(Ctl, n_prev), &npv, 4, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // lv, old2new, np, npv go out of scope
   for (auto& kv : ctx->call_slot) kv.second = old2new[kv.second];
   std::vector<uint32_t> sp(rows, 0), sa(rows, 0);
   std::vector<uint8_t> sl(rows, 0);
@@ -1092,8 +1159,8 @@ extern "C" autx_status autx_step_stats(autx_ctx* ctx, autx_selection_stats* o) {
   memset(o, 0, sizeof *o);
   o->qstar = c.qstar;
   o->mprime = c.mprime;
-  o->n_x = c.n_x;
-  o->n_b = c.n_b;
+  o->n_x = c.n_cand_a;
+  o->n_b = c.last_n_b;
   o->n_rows = ctx->tail;
   o->n_programs = (uint32_t)ctx->prog_row.size();
   if (!ctx->radix && ctx->stepped) {

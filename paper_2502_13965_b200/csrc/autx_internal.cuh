@@ -18,11 +18,12 @@ constexpr uint8_t QF_INB = 0x80;    // scratch: member of the batch being formed
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr int MAX_K = 16;
 constexpr int QP_LINES = 16;
-constexpr int SUP_TILES = 16;  // tiles per super-tile (the two-level queue-count prefix)
-constexpr int ST_THREADS = 512;  // threads per CTA of the step kernel
+constexpr int SUP_TILES = 16;  // tiles per super-tile (the gather's two-level prefix)
+constexpr int SCAN_THREADS = 256;
 constexpr int ROWS_PER_THREAD = 8;
-constexpr int TILE = ST_THREADS * ROWS_PER_THREAD;  // rows per tile (4096)
-constexpr int MAX_BATCH = 2048;  // BS limit: the finalize keeps 2 BS candidate records in shared memory
+constexpr int TILE = SCAN_THREADS * ROWS_PER_THREAD;  // rows per scan tile (2048)
+constexpr int FIN_THREADS = 1024;
+constexpr int MAX_BATCH = 2048;  // BS limit: k_rank keeps 2 BS keys (+ kvb, indices) in shared memory
 
 // Device-resident call table, struct-of-arrays, rows in (arrival, seq) order.  Row index ==
 // registration order, so the paper's FCFS tie `seq` is the row index.
@@ -72,15 +73,24 @@ struct Policy {
   uint32_t host_pages_lo;  // host arena pages (capped to 2^32-1)
   uint32_t bt_shift;       // log2(block_tokens) if a power of two, else 0xFF
   uint32_t stamps;         // record chain stamps (autx_set_timing mode 2)
+  int32_t device;          // CUDA device of the context
 };
 
-// Step control block in device memory.
+// Step control block in device memory (written by the prologue kernels).
 struct Ctl {
   uint32_t t;          // current step
-  uint32_t n_x;        // candidates of region A (radix path: set by k_take)
-  uint32_t qstar;      // boundary queue q* of the last step (K: every live call is a candidate)
-  uint32_t mprime;     // rows of q* taken in table order
-  uint32_t n_promoted, n_live;  // radix path: reduced by k_keys (the step kernel uses qpart)
+  uint32_t n_rows;     // rows in use (tail)
+  uint32_t ntiles;
+  uint32_t tiles_done; // last-CTA ticket for the scan kernel
+  // selection result (scan kernel's last CTA)
+  uint32_t qstar;      // boundary queue (K if all live calls are candidates)
+  uint32_t mprime;     // rows of q* to take in table order
+  uint32_t n_cand_a;   // candidates from the table scan
+  uint32_t n_cand_b;   // extra running candidates of queue q* (previous batch, not in region A)
+  uint32_t qs_boundary;  // slot of the m'-th live row of q* (region A's last q* row)
+  uint32_t n_promoted;
+  uint32_t n_live;
+  // finalize results
   uint32_t n_prev;     // previous batch size (slots in prev_slots)
   uint32_t err;        // sticky device error code (autx_status)
   uint32_t err_info;
@@ -90,19 +100,19 @@ struct Ctl {
   uint32_t free_top;       // GPU block free stack size
   uint32_t rs_free_top;    // resident-slot free stack size
   uint32_t host_bump;      // host arena bump pointer (pages)
-  uint32_t bnd_slot, bnd_arr;  // region A's last row of q* (slot, arrival): published by its tile
-  uint32_t n_b;                // region B size of the last step (finalize; autx_step_stats)
+  uint32_t rank_done;      // last-CTA ticket of k_rank (fused finalize)
+  // batch totals reduced by k_rank's list writers (rank_lists), read and reset by finalize
+  uint32_t acc_nbatch, acc_nadmit;
+  unsigned long long acc_kv, acc_swap_in;
   uint32_t host_free_top[32];  // per size class free-stack size
-  // step-kernel synchronisation, one 128-B line each: the prologue's completion (step seqno) and
-  // the two grid barriers (arrival counts, reset by the finalize CTA at the end of the step)
-  alignas(128) uint32_t pro_seq;
-  alignas(128) uint32_t go_seq;   // AUTX_PRO_FIRST: the prologue's loads are issued (tiles may stream)
-  alignas(128) uint32_t bar1;
-  alignas(128) uint32_t bar2;
-  // scan partial totals over QP_LINES 128-B lines (CTA b adds into line b % QP_LINES: same-address
-  // reductions serialise at L2): [MAX_K] promotions, [MAX_K + 1] live rows.  Reset by finalize.
+  // self-selecting gather (default select path): slot + 1 of region A's last q* row (0 = none),
+  // and the scan's partial totals, spread over QP_LINES 128-B lines (scan CTA b adds into line
+  // b % QP_LINES: same-address reductions serialise at L2): [0, MAX_K) live rows per queue after
+  // anti-starvation, [MAX_K] promotions, [MAX_K + 1] live rows.  Reset by finalize.
+  uint32_t qs_bnd1;
+  uint32_t last_n_b;   // region B size of the last step (autx_step_stats; n_cand_b is reset by finalize)
   alignas(128) uint32_t qpart[QP_LINES][32];
-  unsigned long long dbg[96];  // %globaltimer stamps (autx_phase_times): [40, 56) this step, [64, 80) last step
+  unsigned long long dbg[96];  // [32, 64) live chain stamps, [64, 96) last step's (AUTX_CHAIN_STAMPS)  // %globaltimer stamps of kernel phases (autx_phase_times)
 };
 
 // Host-visible step output written by the finalize kernel into mapped pinned memory.
@@ -137,19 +147,36 @@ struct KvState {
   uint32_t plan_cap;        // capacity of the plan block lists
 };
 
-// Candidate records, struct-of-arrays: a row among the step's <= BS smallest keys (region A) at
-// its position in (queue, seq) order, or a row of the previous batch at its previous-batch index.
-// Written by the tile CTAs with coalesced stores, read by the finalize with coalesced loads.
-struct RecSoA {
-  unsigned long long* cid;
-  uint32_t* slot;
-  uint32_t* arr;
-  uint32_t* tok;
-  uint32_t* exec;
-  uint32_t* mt;    // mtime after this step's anti-starvation
-  uint32_t* qt;    // quanta after this step's anti-starvation
-  uint32_t* qfb;   // qf | previous-batch index << 8 (valid while QF_RUN); QF_DEAD: completed
+// Candidate record written by the multi-CTA gather so that the single-CTA finalize reads
+// contiguous, L2-resident data instead of chasing random rows of the call table.
+struct CandRec {
+  unsigned long long cid;
+  uint32_t slot, arr, tok, exec, mtime, quanta, qf, _pad;
 };
+
+#ifdef __CUDACC__
+// Unique 64-bit order key (R11, R12): q:4 | arrival relative to step t:27 | not-running:1 |
+// seq (row):31.  Requires t - arrival < 2^27 and rows < 2^31.
+__device__ __forceinline__ uint64_t cand_key(const CandRec& r, uint32_t t) {
+  uint64_t arel = (uint64_t)((1u << 27) - 1 - (t - r.arr)) & ((1u << 27) - 1);  // later arrival: larger
+  return ((uint64_t)(r.qf & QF_QMASK) << 59) | (arel << 32) | ((uint64_t)((r.qf & QF_RUN) ? 0u : 1u) << 31) |
+         (r.slot & 0x7FFFFFFFu);
+}
+
+__device__ __forceinline__ void load_rec(const struct CallTable& ct, uint32_t s, CandRec* r) {
+  CandRec x;
+  x.cid = ct.cid[s];
+  x.slot = s;
+  x.arr = ct.arr[s];
+  x.tok = ct.tok[s];
+  x.exec = ct.exec[s];
+  x.mtime = ct.mtime[s];
+  x.quanta = ct.quanta[s];
+  x.qf = ct.qf[s];
+  x._pad = (x.qf & QF_RUN) ? ct.bidx[s] : NONE;  // previous-batch index of a running call
+  *r = x;
+}
+#endif
 
 struct Outputs {
   uint32_t* batch_slots;     // [max_batch]
@@ -159,13 +186,23 @@ struct Outputs {
   uint32_t* prev_slots;      // [max_batch] previous batch (slots), ctl->n_prev entries
   uint32_t* preempt_slots;   // [max_batch]
   uint32_t* admit_slots;     // [max_batch]
-  RecSoA xs;                 // [max_batch] region A in (queue, seq) order
-  RecSoA ps;                 // [max_batch] the previous batch's rows by previous-batch index: written by
-                             // the tiles owning them (live rows, after the dense pass) and by the
-                             // prologue (completed rows: qfb = QF_DEAD)
-  uint32_t* tile_cnt;        // [ntiles_cap * MAX_K] live rows per (tile, queue) after anti-starvation
+  uint32_t* cand;            // [cand_cap] candidate slots (radix path)
+  uint32_t cand_cap;
+  CandRec* cand_rec;         // [cand_cap] region-A candidate records
+  CandRec* prev_rec;         // [max_batch] records of the previous batch
+  uint64_t* ckey;            // [2 BS] keys: region A at [0, nA), previous batch at [nA, nA + n_prev)
+  uint64_t* skey;            // [2 BS] keys sorted by k_rank
+  uint32_t* sidx;            // [2 BS] element index of each sorted key
+  CandRec* srec;             // [2 BS] candidate records in sorted order
+  unsigned long long* prev_pos;  // [max_batch] seqno << 32 | sorted position of previous-batch entry j
+                                 // (k_rank; entries that are no candidate keep an older seqno)
+  uint32_t use_prev_pos;     // finalize tests batch membership of the previous batch by prev_pos
+  uint32_t rank_lists;       // k_rank writes batch / admit lists and accounting (no KV allocator)
+  uint32_t rank_wide;        // k_rank: a warp per key when the candidates fill <= half its grid
+  uint32_t* ckvb;            // [2 BS] kvb of each key in ckey (R14)
+  uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* sup_cnt;         // [ceil(ntiles_cap / SUP_TILES) * MAX_K] per-queue counts of super-tiles
-                             // (scan: atomics; selection: prefix; finalize: reset)
+                             // (scan: atomics; gather: prefix; finalize: reset)
   uint32_t n_sup;            // super-tiles in use this step (set per launch; finalize resets them)
   HostOut* hout;             // host-visible counts (pinned)
   HostOut* d_hout;           // device copy of the counts (copied out with the lists by one DMA)
@@ -216,13 +253,47 @@ struct ArrivalRec {
   uint32_t par;    // AUTX_ATLAS_EQ2: offset of the parents' lineage indices in PrologueArgs::par
 };
 
-extern unsigned long long g_kernel_launches;  // every library kernel launch (autx_kernel_launches)
-
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
 // predecessor in the stream still runs; it must call pdl_wait() before touching its inputs.
+extern unsigned long long g_kernel_launches;  // every library kernel launch (autx_kernel_launches)
+
+// A kernel launch recorded instead of issued (the step's launches are replayed as one CUDA graph
+// whose kernel nodes get this step's parameters: see autx_api.cu, step_graph_run).
+struct LaunchRec {
+  const void* func;
+  dim3 grid, block;
+  size_t smem;
+  std::vector<unsigned char> blob;  // argument values, 16-B aligned each
+  std::vector<size_t> off;
+  template <typename T>
+  void push(const T& v) {
+    const size_t o = (blob.size() + 15) & ~size_t(15);
+    blob.resize(o + sizeof(T));
+    memcpy(blob.data() + o, &v, sizeof(T));
+    off.push_back(o);
+  }
+  std::vector<void*> ptrs() {
+    std::vector<void*> p(off.size());
+    for (size_t i = 0; i < off.size(); ++i) p[i] = blob.data() + off[i];
+    return p;
+  }
+};
+extern thread_local std::vector<LaunchRec>* g_launch_rec;  // non-null: launch_pdl records
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args) {
+  if (g_launch_rec) {
+    LaunchRec r;
+    r.func = reinterpret_cast<const void*>(k);
+    r.grid = grid;
+    r.block = block;
+    r.smem = smem;
+    (r.push(static_cast<KArgs>(args)), ...);
+    g_launch_rec->push_back(std::move(r));
+    __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);  // runs in the graph replay
+    return cudaSuccess;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -237,11 +308,9 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
-// Inputs of the step prologue (completions + arrivals), passed by value as kernel parameters
-// when they fit (PRO_INLINE each), else through the pointers.  comp_prog[i] is the process-table
-// row of completion i (a host-side id map, no arithmetic): the scan CTAs defer exactly the rows
-// of those programs until the prologue has updated their service.
-constexpr int PRO_INLINE = 128;
+// Inputs of the fused step prologue (completions + arrivals), passed by value as kernel
+// parameters when they fit (PRO_INLINE each), else through the pointers.
+constexpr int PRO_INLINE = 96;
 struct PrologueArgs {
   uint32_t n_comp, n_arr, first_slot, t;
   uint32_t n_prog_rows, _pad[3];  // process-table rows in use
@@ -250,38 +319,15 @@ struct PrologueArgs {
   const uint32_t* comp_lin;  // AUTX_ATLAS_EQ2: lineage index of each completion (mapped pinned)
   const uint32_t* par;       // AUTX_ATLAS_EQ2: parents' lineage indices (mapped pinned)
   uint32_t comp[PRO_INLINE];
-  uint32_t comp_prog[PRO_INLINE];
   ArrivalRec arr[PRO_INLINE];
 };
 
-// Everything one scheduling step reads, passed to the step kernel as one __grid_constant__
-// parameter block.
-struct StepArgs {
-  Policy pol;
-  CallTable ct;
-  ProgTable pt;
-  Ctl* ctl;
-  Outputs out;
-  KvState kv;
-  CompRec* rec_out;     // this step's completion records (routing epoch)
-  uint32_t kv_on;
-  uint32_t t, n_rows, ntiles;
-  uint32_t n_tile_ctas;  // CTAs 0 .. n_tile_ctas-1 scan tiles; CTA n_tile_ctas runs prologue + finalize
-  uint32_t seqno;
-  uint32_t first_new;   // first row registered by this step's prologue (rows below are older)
-  uint32_t defer_all;   // the prologue's records are not inline: every row waits for it
-  uint32_t do_pro;      // the step has a prologue (completions or arrivals)
-  uint32_t pro_first;   // the tiles start streaming only once the prologue's loads are issued
-  uint32_t warm_params; // the finalize CTA touches its parameter fields while it waits
-  PrologueArgs pro;
-};
-
-// ---- kernel launchers (sched_kernels.cu / swap_kernels.cu / radix_kernels.cu) ---------------
+// ---- kernel launchers (sched_kernels.cu / swap_kernels.cu) ----------------------------------
 cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                             const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
-                            CompRec* rec_out, bool apply, uint32_t* prev_qfb);
-// The step prologue (a1, a2) as its own kernel (radix mode, bulk bursts, before a compaction).
-cudaError_t launch_prologue(cudaStream_t s, const StepArgs& a);
+                            CompRec* rec_out, bool apply);
+cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl, KvState kv,
+                            bool kv_on, CompRec* rec_out, const PrologueArgs& a);
 cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,
                          uint64_t stride, uint32_t G, uint32_t t);
 cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,
@@ -290,14 +336,15 @@ cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint
 cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt,
                             const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t,
                             const uint32_t* par = nullptr);
+// Per-device setup of the step kernels (shared-memory attributes); called by autx_create after
+// cudaSetDevice.
+cudaError_t step_kernels_setup();
 cudaError_t launch_set_bidx(cudaStream_t s, CallTable ct, const uint32_t* prev_slots, uint32_t n);
-// Per-device launch setup of the step kernels (shared-memory attribute, co-resident CTA
-// capacity); called by autx_create after cudaSetDevice.
-cudaError_t step_kernel_setup(uint32_t max_batch, uint32_t* capacity_out);
-// One scheduling step (a1-a6): the cooperative step kernel (select mode), or the prologue, the
-// radix sort and the finalize kernel (radix mode).  ev: 2 events around the step, or null.
-cudaError_t launch_step(cudaStream_t s, StepArgs& a, uint32_t capacity, cudaEvent_t* ev,
-                        const RadixState* rx, uint32_t arr_base, uint32_t* radix_passes);
+cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                        Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
+                        uint32_t seqno, cudaEvent_t* ev /* 4 events or null */,
+                        const RadixState* rx /* non-null: AUTX_ORDER_RADIX */, uint32_t arr_base,
+                        uint32_t* radix_passes, uint32_t first_new /* first row registered this step */);
 cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                Outputs out, RadixState rx, uint32_t t, uint32_t n_rows,
                                uint32_t arr_base, int sms, uint32_t* passes_out);

@@ -4,16 +4,16 @@
 // and the keys are sorted by a stable LSD radix sort, one byte per digit.  The table is kept in
 // seq (row) order, so sorting the high 32 bits stably already orders the low 32: only digits
 // 4..7 are sorted, and a digit whose 256-bin histogram is a single bin (all keys equal there)
-// is skipped.  The first min(BS, n_live) sorted keys become the finalize's candidate list, and
-// the finalize cuts the prefix exactly as in the selection path, so both modes give identical
-// decisions (tests/test_parity_gpu.py::test_radix_order_*).
+// is skipped.  The first min(BS, n_live) sorted keys become finalize's candidate list, and
+// finalize cuts the prefix exactly as in the selection path, so both modes give identical
+// decisions (tests/test_parity_gpu.py::test_radix_equals_select).
 //
 //   k_keys     dense pass: anti-starvation (same arithmetic as k_scan) + key pack + the four
 //              global 256-bin digit histograms (for skip detection)
 //   k_hist     per-tile 256-bin histogram of one digit        -> hist[digit value][tile]
 //   k_scan_h   exclusive scan of hist in (digit value, tile) order (one CTA)
 //   k_scatter  stable per-tile ranking (warp match + per-warp running counters) and scatter
-//   k_take     the first min(BS, n_live) keys -> region A of the finalize (k_fin)
+//   k_take     the first min(BS, n_live) keys -> candidate rows
 #include "autx_internal.cuh"
 #include "block_prims.cuh"
 #include "../../include/autx.h"
@@ -27,7 +27,7 @@ constexpr int RX_WARP_KEYS = 32 * RX_ITEMS;      // 512 keys per warp, contiguou
 
 __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                      RadixState rx, uint32_t t, uint32_t n_rows,
-                                                     uint32_t arr_base, RecSoA ps) {
+                                                     uint32_t arr_base) {
   __shared__ uint32_t h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += RX_THREADS) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -40,9 +40,8 @@ __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, P
       if (!(qf & QF_DEAD)) {
         ++nlive;
         uint32_t q = qf & QF_QMASK;
-        uint32_t mt_now = ct.mtime[r], qt_now = ct.quanta[r];
         if (pol.beta_den != 0) {
-          uint32_t p = ct.prog[r], b = ct.base[r], m = mt_now;
+          uint32_t p = ct.prog[r], b = ct.base[r], m = ct.mtime[r];
           const PInfo pi = pt.info[p];
           uint64_t W = pi.pwait + (uint64_t)(t - b - m);
           uint64_t T = (uint64_t)pi.svc + m;
@@ -52,22 +51,8 @@ __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, P
             ct.base[r] = t;
             ct.mtime[r] = 0;
             ct.quanta[r] = pol.quanta[0];
-            mt_now = 0;
-            qt_now = pol.quanta[0];
-            qf &= ~QF_QMASK;
             ++npromo;
           }
-        }
-        if (qf & QF_RUN) {  // ran in the previous step: its record for the finalize (prev_rec)
-          const uint32_t bx = ct.bidx[r];
-          ps.cid[bx] = ct.cid[r];
-          ps.slot[bx] = r;
-          ps.arr[bx] = ct.arr[r];
-          ps.tok[bx] = ct.tok[r];
-          ps.exec[bx] = ct.exec[r];
-          ps.mt[bx] = mt_now;
-          ps.qt[bx] = qt_now;
-          ps.qfb[bx] = qf | (bx << 8);
         }
         uint64_t arel = (uint64_t)(ct.arr[r] - arr_base) & ((1u << 27) - 1);
         key = ((uint64_t)q << 60) | (arel << 33) | ((uint64_t)((qf & QF_RUN) ? 0u : 1u) << 32) | r;
@@ -169,26 +154,26 @@ __global__ void __launch_bounds__(RX_THREADS) k_scatter(const uint64_t* in, uint
   }
 }
 
-// The first min(BS, n_live) sorted keys -> region A (the finalize's candidates, already in key
-// order: q* = K, no region B).
-__global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out, uint32_t BS, uint32_t K) {
-  const uint32_t n = min(BS, ctl->n_live);
+__global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out, uint32_t BS, uint32_t K,
+                       uint32_t t) {
+  uint32_t n = min(BS, ctl->n_live);
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint32_t s = (uint32_t)keys[i];
-    const uint32_t qf = ct.qf[s];
-    const RecSoA& x = out.xs;
-    x.cid[i] = ct.cid[s];
-    x.slot[i] = s;
-    x.arr[i] = ct.arr[s];
-    x.tok[i] = ct.tok[s];
-    x.exec[i] = ct.exec[s];
-    x.mt[i] = ct.mtime[s];
-    x.qt[i] = ct.quanta[s];
-    x.qfb[i] = qf | ((qf & QF_RUN) ? ct.bidx[s] << 8 : 0u);
+    uint32_t sl = (uint32_t)keys[i];
+    CandRec r;
+    load_rec(ct, sl, &r);
+    out.cand[i] = sl;
+    out.cand_rec[i] = r;
+    out.ckey[i] = cand_key(r, t);
+  }
+  // previous batch: records for preempt; no region B (the full sort already ranked them)
+  for (uint32_t j = threadIdx.x; j < ctl->n_prev; j += blockDim.x) {
+    load_rec(ct, out.prev_slots[j], out.prev_rec + j);
+    out.ckey[n + j] = ~0ull;
   }
   if (threadIdx.x == 0) {
-    ctl->n_x = n;
-    ctl->qstar = K;
+    ctl->n_cand_a = n;
+    ctl->n_cand_b = 0;
+    ctl->qstar = K;  // no extra running candidates: the sort already ordered them
   }
 }
 
@@ -200,7 +185,7 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
   cudaMemsetAsync(rx.dig_hist, 0, 4 * 256 * sizeof(uint32_t), s);
   uint32_t grid = std::min<uint32_t>(ntiles * RX_ITEMS, (uint32_t)sms * 8);
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_keys<<<grid, RX_THREADS, 0, s>>>(pol, ct, pt, ctl, rx, t, n_rows, arr_base, out.ps);
+  k_keys<<<grid, RX_THREADS, 0, s>>>(pol, ct, pt, ctl, rx, t, n_rows, arr_base);
   // skip detection needs the digit histograms on the host (a 4 KB read; this mode is the
   // contract path, the selection path is the fast path)
   cudaMemcpyAsync(rx.h_dig_hist, rx.dig_hist, 4 * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
@@ -225,7 +210,7 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
     ++passes;
   }
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_take<<<1, 1024, 0, s>>>(a, ct, ctl, out, pol.max_batch, pol.K);
+  k_take<<<1, 1024, 0, s>>>(a, ct, ctl, out, pol.max_batch, pol.K, t);
   if (passes_out) *passes_out = passes;
   return cudaGetLastError();
 }

@@ -1,19 +1,19 @@
-// sm_100a kernels of one Autellix scheduling step.  Select mode (the
-// default) runs the whole step as ONE cooperative kernel, k_step:
+// sm_100a kernels of one Autellix scheduling step.  Default chain,
+// PDL-linked on one stream:
 //
-//   prologue   (a1, a2)  completion records -> process table (commutative reductions), rows
-//                        released; arrivals appended, inherit service, placed in a queue
-//   dense pass (a3, a4)  every call: anti-starvation (integer cross-multiply) + per-tile /
-//                        per-super-tile queue counts; rows the prologue touches wait for it
-//   selection  (a5)      q*, m' and each tile's per-queue prefix; region A written in
-//                        (queue, seq) order (a stable counting sort by queue)
-//   finalize   (a5, a6, a3, a7 plan)  region B, the running-first partition inside each
-//                        (queue, arrival) group, the prefix cutoff on BS and the KV budget,
-//                        admit/preempt lists, step accounting and eager demotion, GPU block
-//                        allocation and the swap plan, host mirrors
+//   k_prologue   (a1, a2)  completion records -> process table (commutative reductions), rows
+//                          released; arrivals appended, inherit service, placed in a queue
+//   k_scan_bulk  (a4)      dense TMA-staged pass over every call: anti-starvation (integer
+//                          cross-multiply) + per-tile / per-super-tile queue counts
+//   k_gather_ss  (a5)      q*, m' and each tile's candidate offset from the counts; emits the
+//                          candidate set (<= BS rows of the lowest queues, table order) and the
+//                          previous batch's records and region-B keys
+//   k_rank       (a5)      multi-CTA rank counting of the <= 2 BS unique keys
+//   k_finalize   (a5, a6, a3, a7 plan)  prefix cutoff on BS and the KV budget, admit/preempt
+//                          lists, step accounting and eager demotion, GPU block allocation and
+//                          the swap plan, host mirrors
 //
-// with two in-kernel grid barriers instead of kernel boundaries.  Every step of Alg. 1 runs here;
-// the host only stages records.  Citations: see autx.h.
+// Every step of Alg. 1 runs here; the host only stages records.  Citations: see autx.h.
 #include <algorithm>
 #include <cstdlib>
 
@@ -32,14 +32,26 @@ __device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc)
   return q;
 }
 
-// Phase stamps (autx_set_timing mode 2, or always in a -DAUTX_CHAIN_STAMPS build): %globaltimer
-// at the step kernel's phase boundaries into ctl->dbg[40, 56) (see k_step); the finalize moves
-// them to dbg[64, 80) at the step's end.  Off by default: one uniform parameter test.
-#ifdef AUTX_CHAIN_STAMPS
-#define STAMPS_ON(pol) true
+#ifdef AUTX_PHASE_SYNC
+// profiling build: a barrier that must complete (its result is consumed) before the stamp, so
+// deferred-blocking barriers cannot shift time into the next phase
+#define STAMP(i) do { if (__syncthreads_count(1) && threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
 #else
-#define STAMPS_ON(pol) ((pol).stamps != 0)
+#define STAMP(i) do { if (threadIdx.x == 0) ctl->dbg[i] = globaltimer(); } while (0)
 #endif
+
+// Chain stamps (autx_set_timing mode 2, or always in a -DAUTX_CHAIN_STAMPS build): per kernel k
+// of the step chain, %globaltimer when CTA 0 passes griddepcontrol.wait (dbg[32 + 3k]), the
+// latest CTA end (33 + 3k) and the latest CTA start past the wait (34 + 3k); finalize moves
+// dbg[32, 64) to dbg[64, 96) at the step's end.  Off by default: one uniform parameter test.
+#ifdef AUTX_CHAIN_STAMPS
+#define STAMPS_ON true
+#else
+#define STAMPS_ON (pol.stamps != 0)
+#endif
+#define CHAIN_BEGIN(k) do { if (STAMPS_ON && threadIdx.x == 0) { const unsigned long long g_ = globaltimer(); \
+    if (blockIdx.x == 0) ctl->dbg[32 + 3 * (k)] = g_; atomicMax(&ctl->dbg[34 + 3 * (k)], g_); } } while (0)
+#define CHAIN_END(k) do { if (STAMPS_ON && threadIdx.x == 0) atomicMax(&ctl->dbg[33 + 3 * (k)], globaltimer()); } while (0)
 
 // ceil(tokens / block_tokens) (R14, R28): a shift when block_tokens is a power of two
 __device__ __forceinline__ uint32_t blocks_for(const Policy& pol, uint32_t tokens) {
@@ -81,20 +93,19 @@ __device__ __forceinline__ void apply_record(const Policy& pol, ProgTable pt, co
 template <int NT>
 __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, Ctl* ctl, const uint32_t* slots,
                               uint32_t n, uint32_t t, KvState& kv, bool kv_on, CompRec* rec_out, bool apply,
-                              CompRec* s_rec = nullptr, const uint32_t* lin = nullptr, uint32_t* prev_qfb = nullptr) {
+                              CompRec* s_rec = nullptr, const uint32_t* lin = nullptr) {
   __shared__ uint32_t red_u[33];
   const uint32_t tid = threadIdx.x;
+  STAMP(16);
   for (uint32_t base = 0; base < n; base += NT) {
     uint32_t i = base + tid;
     bool valid = i < n;
     uint32_t s = valid ? slots[i] : 0;
     CompRec r{};
     uint8_t qf0 = QF_DEAD;
-    uint32_t bix = NONE;
     if (valid) {
       uint32_t e = ct.exec[s];
       qf0 = ct.qf[s];  // loaded with the record fields: one round trip
-      if (prev_qfb) bix = ct.bidx[s];
       r.prog = ct.prog[s];
       r.exec = e;
       r.cp = ct.inh[s] + e;
@@ -103,7 +114,9 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       if (s_rec) s_rec[i] = r;  // the caller's shared-memory copy (n <= NT)
       if (lin) pt.crit[lin[i]] = r.cp;  // AUTX_ATLAS_EQ2: p(c) + t_c, an Eq. 2 operand
     }
+    STAMP(17);
     if (apply && valid) apply_record(pol, pt, r, t);
+    STAMP(18);
     // release the row and its KV (completed calls ran in step t-1, hence are resident)
     uint32_t nfree = 0, rslot = NONE;
     if (valid) {
@@ -114,8 +127,6 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       }
       ct.qf[s] = QF_DEAD;
       ct.loc[s] = NONE;
-      // a completed call ran in the previous step: its previous-batch record says it is gone
-      if (prev_qfb && (qf0 & QF_RUN)) prev_qfb[bix] = QF_DEAD;
     }
     if (kv_on) {
       uint32_t tot;
@@ -138,27 +149,28 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
     __syncthreads();
   }
   if (tid == 0) ctl->t = t;
+  STAMP(19);
 }
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_complete(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                  const uint32_t* slots, uint32_t n, uint32_t t, KvState kv,
-                                                 bool kv_on, CompRec* rec_out, bool apply, uint32_t* prev_qfb) {
+                                                 bool kv_on, CompRec* rec_out, bool apply) {
   pdl_wait();
   pdl_trigger();
-  complete_body<NT>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, nullptr, nullptr, prev_qfb);
+  complete_body<NT>(pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
 }
 
 // Multi-engine: apply every engine's completion records (R22: sums and maxima commute, so the
 // replicated tables stay identical whatever the order).  recs of rank r start at
 // base + r * stride bytes, after a RouteHdr.
-__global__ void __launch_bounds__(1024) k_apply(Policy pol, ProgTable pt, const char* base,
+__global__ void __launch_bounds__(FIN_THREADS) k_apply(Policy pol, ProgTable pt, const char* base,
                                                        uint64_t stride, uint32_t G, uint32_t t) {
   for (uint32_t r = 0; r < G; ++r) {
     const RouteHdr* h = reinterpret_cast<const RouteHdr*>(base + r * stride);
     const CompRec* recs = reinterpret_cast<const CompRec*>(h + 1);
     const uint32_t n = h->n_comp;
-    for (uint32_t i = threadIdx.x; i < n; i += 1024) apply_record(pol, pt, recs[i], t);
+    for (uint32_t i = threadIdx.x; i < n; i += FIN_THREADS) apply_record(pol, pt, recs[i], t);
   }
 }
 
@@ -252,178 +264,128 @@ __global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const Arrival
   else register_one(pol, ct, pt, r, first_slot + i, t);
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-
-// ---------------------------------------------------------------------------------------------
-// Step prologue (a1 + a2) of one step: completions, then arrivals, by one CTA.  A typical step's
+// Fused prologue of one step: completions (a1) then arrivals (a2), one CTA; a typical step's
 // records travel inside the kernel parameters (no PCIe reads), larger batches through pointers.
-// Runs in the step kernel's finalize CTA (select mode) or as k_prologue (radix mode).  scratch:
-// shared memory for the records (the finalize's area, unused until the prologue is over).
-// ---------------------------------------------------------------------------------------------
-template <int NT>
-__device__ void prologue_body(const StepArgs& a, unsigned char* scratch, bool stamps = false) {
-  const PrologueArgs& p = a.pro;
-  const Policy& pol = a.pol;
-  CallTable ct = a.ct;
-  ProgTable pt = a.pt;
-  KvState kv = a.kv;
-  Ctl* ctl = a.ctl;
-  uint32_t* s_comp = reinterpret_cast<uint32_t*>(scratch);
-  ArrivalRec* s_arr = reinterpret_cast<ArrivalRec*>(scratch + PRO_INLINE * 4);
-  CompRec* s_rec = reinterpret_cast<CompRec*>(scratch + PRO_INLINE * (4 + sizeof(ArrivalRec)));
+constexpr int PRO_THREADS = 256;
+__global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                                                          KvState kv, bool kv_on, CompRec* rec_out,
+                                                          const PrologueArgs a) {
+  __shared__ uint32_t s_comp[PRO_INLINE];
+  __shared__ ArrivalRec s_arr[PRO_INLINE];
   const uint32_t tid = threadIdx.x;
-  const bool comp_inline = p.n_comp <= PRO_INLINE, arr_inline = p.n_arr <= PRO_INLINE;
-  const bool eq2 = pol.policy == AUTX_ATLAS_EQ2;
+  const bool comp_inline = a.n_comp <= PRO_INLINE, arr_inline = a.n_arr <= PRO_INLINE;
   if (comp_inline)
-    for (uint32_t i = tid; i < p.n_comp; i += NT) s_comp[i] = p.comp[i];
+    for (uint32_t i = tid; i < a.n_comp; i += PRO_THREADS) s_comp[i] = a.comp[i];
   if (arr_inline)
-    for (uint32_t i = tid; i < p.n_arr; i += NT) s_arr[i] = p.arr[i];
+    for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) s_arr[i] = a.arr[i];
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(0);
   __syncthreads();
   if (comp_inline && arr_inline) {
-    // typical step: arrivals inherit the service after this step's completions (R10), computed
+    // typical step: arrivals inherit the service after this step's completions (R10) computed
     // here (old row value combined with the step's records of the same program, exactly what the
     // reductions leave in the row), so the row loads go out with the completion loads: one round
+    __shared__ CompRec s_rec[PRO_INLINE];
     uint32_t svc_old = 0;
-    const bool my_arr = tid < p.n_arr;
+    const bool eq2 = pol.policy == AUTX_ATLAS_EQ2;
+    const bool my_arr = tid < a.n_arr;
     if (my_arr && !eq2 && !(s_arr[tid].flags & 1u)) svc_old = __ldcg(&pt.info[s_arr[tid].prog].svc);
-    if (p.n_comp)
-      complete_body<NT>(pol, ct, pt, ctl, s_comp, p.n_comp, p.t, kv, a.kv_on, a.rec_out, true, s_rec,
-                        eq2 ? p.comp_lin : nullptr, a.out.ps.qfb);
+    if (a.n_comp)
+      complete_body<PRO_THREADS>(pol, ct, pt, ctl, s_comp, a.n_comp, a.t, kv, kv_on, rec_out, true, s_rec,
+                                 eq2 ? a.comp_lin : nullptr);
     __syncthreads();
-    if (stamps && tid == 0) ctl->dbg[57] = globaltimer();
     if (my_arr) {
       const ArrivalRec r = s_arr[tid];
       uint32_t inh = 0;
       if (eq2) {
-        inh = eq2_priority(pt, p.par, r);  // parents completed this step are stored above the barrier
+        inh = eq2_priority(pt, a.par, r);  // parents completed this step are stored above the barrier
       } else if (!(r.flags & 1u)) {
         inh = svc_old;
-        for (uint32_t i = 0; i < p.n_comp; ++i)
+        for (uint32_t i = 0; i < a.n_comp; ++i)
           if (s_rec[i].prog == r.prog) inh = pol.policy == AUTX_ATLAS ? max(inh, s_rec[i].cp) : inh + s_rec[i].exec;
       }
-      register_one(pol, ct, pt, r, p.first_slot + tid, p.t, true, inh);
+      register_one(pol, ct, pt, r, a.first_slot + tid, a.t, true, inh);
     }
-  } else {
-    if (p.n_comp)
-      complete_body<NT>(pol, ct, pt, ctl, comp_inline ? s_comp : p.comp_ptr, p.n_comp, p.t, kv, a.kv_on,
-                        a.rec_out, true, nullptr, eq2 ? p.comp_lin : nullptr, a.out.ps.qfb);
-    // arrivals inherit the service updated by this step's completions (R10): the reductions are
-    // performed at L2 before the barrier releases (fence), and register_one reads svc from L2
-    if (p.n_comp && p.n_arr) __threadfence();
-    __syncthreads();
-    const ArrivalRec* arr = arr_inline ? s_arr : p.arr_ptr;
-    for (uint32_t i = tid; i < p.n_arr; i += NT) {
-      if (eq2) register_one(pol, ct, pt, arr[i], p.first_slot + i, p.t, true, eq2_priority(pt, p.par, arr[i]));
-      else register_one(pol, ct, pt, arr[i], p.first_slot + i, p.t);
-    }
+    CHAIN_END(0);
+    return;
   }
-  if (tid == 0) ctl->t = p.t;
-}
-
-// Radix mode: the prologue as its own kernel, before the sort.
-__global__ void __launch_bounds__(ST_THREADS) k_prologue(const __grid_constant__ StepArgs a) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  prologue_body<ST_THREADS>(a, dsm);
-}
-
-// ---------------------------------------------------------------------------------------------
-// In-kernel synchronisation of the step kernel.  Its grid is launched cooperatively (every CTA is
-// co-resident), so CTAs may wait for each other: a CTA barrier orders the CTA's writes before
-// thread 0's gpu-scope fence and relaxed increment (a release pattern); a waiter polls with
-// relaxed loads and fences once when the condition holds (an acquire pattern).  Polling with
-// ld.acquire would invalidate the SM's whole L1 (CCTL.IVALL) at every poll, under the feet of the
-// other CTA on the SM (measured: every phase of the step 3-5x slower).  Data written by other
-// CTAs in this kernel is read with ld.cg (L2), never through L1 or the read-only path.
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  const uint32_t v = ld_relaxed_u32(p);
-  fence_acq_rel();
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_relaxed_add_u32(uint32_t* p, uint32_t v) {
-  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void grid_arrive(uint32_t* ctr) {
+  const bool eq2 = pol.policy == AUTX_ATLAS_EQ2;
+  if (a.n_comp)
+    complete_body<PRO_THREADS>(pol, ct, pt, ctl, comp_inline ? s_comp : a.comp_ptr, a.n_comp, a.t, kv, kv_on,
+                               rec_out, true, nullptr, eq2 ? a.comp_lin : nullptr);
+  // arrivals inherit the service updated by this step's completions (R10): the reductions are
+  // performed at L2 before the barrier releases (fence), and register_one reads svc from L2
+  if (a.n_comp && a.n_arr) __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    red_relaxed_add_u32(ctr, 1u);
+  const ArrivalRec* arr = arr_inline ? s_arr : a.arr_ptr;
+  for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) {
+    if (eq2) register_one(pol, ct, pt, arr[i], a.first_slot + i, a.t, true, eq2_priority(pt, a.par, arr[i]));
+    else register_one(pol, ct, pt, arr[i], a.first_slot + i, a.t);
   }
+  CHAIN_END(0);
 }
-__device__ __forceinline__ void grid_wait(const uint32_t* ctr, uint32_t target) {
-  if (threadIdx.x == 0) {
-    while (ld_relaxed_u32(ctr) < target) __nanosleep(20);
-    fence_acq_rel();
-  }
-  __syncthreads();
-}
-__device__ __forceinline__ void wait_prologue(const Ctl* ctl, uint32_t seqno) {
-  if (threadIdx.x == 0) {
-    while (ld_relaxed_u32(&ctl->pro_seq) != seqno) __nanosleep(20);
-    fence_acq_rel();
-  }
-  __syncthreads();
+
+cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl, KvState kv,
+                            bool kv_on, CompRec* rec_out, const PrologueArgs& a) {
+  return launch_pdl(k_prologue, 1, PRO_THREADS, 0, s, pol, ct, pt, ctl, kv, kv_on, rec_out, a);
 }
 
 // ---------------------------------------------------------------------------------------------
-// a3 + a4: the dense pass over one thread's 8 rows.  Every live call: wait = (t - base) - mtime
-// (every active step since the last reset either ran or waited), W = pwait[p] + wait,
-// T = svc[p] + mtime; promote to Q_1 iff W * beta_den >= beta_num * T and not 0/0 (Alg. 1
-// l.24-30, R3/R4/R7).  Demotion (l.20-23) was applied eagerly by the previous step's finalize
-// (only batch calls can exhaust a quantum, and nothing in between reads q).  Bytes per call:
-// qf 1 + prog 4 + base 4 + mtime 4 read; a promotion writes base (it becomes t) and only the
-// fields that change: qf if q != 0, mtime if != 0, quanta if q != 0 or mtime != 0 (a call in Q_1
-// that has not run since its last reset already holds Q_1's quantum).  CG: the program rows may
-// have been updated in this kernel (the prologue), so they are read from L2.
+// a4 + counting: the dense pass.  Every live call: wait = (t - base) - mtime (every active step
+// since the last reset either ran or waited), W = pwait[p] + wait, T = svc[p] + mtime; promote
+// to Q_1 iff W * beta_den >= beta_num * T and not 0/0 (Alg. 1 l.24-30, R3/R4/R7).  Demotion
+// (l.20-23) was applied eagerly by the previous step's finalize (only batch calls can exhaust a
+// quantum, and nothing in between reads q).  Bytes per call: qf 1 + prog 4 + base 4 + mtime 4
+// read; a promotion writes base (always: it becomes t) and only the fields that change: qf if
+// q != 0, mtime if != 0, quanta if q != 0 or mtime != 0 (a call in Q_1 that has not run since its
+// last reset already holds Q_1's quantum).
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t qf_at(const uint32_t (&qw)[2], int j) { return (qw[j >> 2] >> (8 * (j & 3))) & 0xffu; }
-__device__ __forceinline__ uint32_t lane4(const uint4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+// The dense pass runs one tile per CTA, sized for one wave: 256 threads x 8 rows, <= 64
+// registers so that 4 CTAs fit per SM (592 tiles = 1.2M rows resident at once).  Every row's
+// program-row gather is issued in one round, which is what bounds this latency-bound pass.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
-// qw: the 8 rows' flag bytes, packed 4 per word (updated in place).
-template <bool CG>
-__device__ __forceinline__ void dense_rows(const Policy& pol, const CallTable& ct, const ProgTable& pt, uint32_t t,
-                                           uint32_t row0, uint32_t (&qw)[2], const uint32_t (&prog)[8],
-                                           uint32_t (&base)[8], uint32_t (&mtim)[8], uint64_t& hq,
+// Per-row core of the dense pass over one thread's 8 rows (Alg. 1 l.24-30): program-row gather,
+// anti-starvation, promotion writes, queue histogram.
+template <int R>
+__device__ __forceinline__ void dense_rows(const Policy& pol, CallTable& ct, const ProgTable& pt, uint32_t t,
+                                           uint32_t row0, uint32_t (&qfs)[R], const uint32_t (&prog)[R],
+                                           uint32_t (&base)[R], uint32_t (&mtim)[R], uint64_t& hq,
                                            uint32_t& npromo, uint32_t& nlive) {
-  constexpr int R = 8;
+  static_assert(R == 4 || R == 8, "rows per thread");
   const bool anti = pol.beta_den != 0;
   const uint32_t bnum = pol.beta_num, bden = pol.beta_den, quanta0 = pol.quanta[0];
+  // the program rows of all 8 rows in one round (svc and pwait only: 12 of the 16 bytes)
   uint32_t svc[R], pwl[R];
   uint32_t big = t & 0x80000000u;  // any operand >= 2^31: this thread needs the exact path
   if (anti) {
+    uint32_t pwh[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) {  // the program rows of all 8 rows in one round
-      const bool live = !(qf_at(qw, j) & QF_DEAD);
-      const uint2* pp = reinterpret_cast<const uint2*>(&pt.info[prog[j]].pwait);
-      const uint2 pw = live ? (CG ? __ldcg(pp) : __ldg(pp)) : make_uint2(0u, 0u);
-      svc[j] = live ? (CG ? __ldcg(&pt.info[prog[j]].svc) : __ldg(&pt.info[prog[j]].svc)) : 0u;
+    for (int j = 0; j < R; ++j) {  // all gathers first (one round trip), then the corrections
+      const bool live = !(qfs[j] & QF_DEAD);
+      const uint2 pw = live ? __ldg(reinterpret_cast<const uint2*>(&pt.info[prog[j]].pwait)) : make_uint2(0u, 0u);
+      svc[j] = live ? __ldg(&pt.info[prog[j]].svc) : 0u;
       pwl[j] = pw.x;
-      big |= pw.y | ((pw.x | svc[j]) & 0x80000000u);
+      pwh[j] = pw.y;
     }
+#pragma unroll
+    for (int j = 0; j < R; ++j) big |= pwh[j] | ((pwl[j] | svc[j]) & 0x80000000u);
   }
   // Alg. 1 l.24-26 (R3, R4).  With t, svc and pwait below 2^31 (wait, mtime <= t), W and T
   // are below 2^32, so W * beta_den >= beta_num * T is exact as two 32x32->64 products.  A
   // warp holding any larger operand takes the 128-bit comparison (starving()) for all its rows.
   uint32_t stv = 0;  // bit j: row j starving (not 0/0 and the ratio test holds)
   if (anti) {
+    // (lanes past n_rows skip this block: vote among the lanes present; each lane still sees
+    // its own operand, so the choice is exact whichever lanes take part)
     if (__any_sync(__activemask(), big != 0)) {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        const bool live = !(qf_at(qw, j) & QF_DEAD);
-        PInfo pi{0, 0, 0ull};
-        if (live) {
-          pi.svc = __ldcg(&pt.info[prog[j]].svc);
-          pi.pwait = __ldcg(&pt.info[prog[j]].pwait);
-        }
+        const bool live = !(qfs[j] & QF_DEAD);
+        const PInfo pi = live ? pt.info[prog[j]] : PInfo{0, 0, 0ull};
         stv |= starving(pol, pi, t - base[j] - mtim[j], mtim[j]) ? 1u << j : 0u;
       }
     } else {
@@ -435,18 +397,18 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, const CallTable& c
       }
     }
   }
-  bool wb = false, wm = false;
-  const uint32_t qw0 = qw[0], qw1 = qw[1];
+  bool wq = false, wb = false, wm = false;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    const uint32_t qf = qf_at(qw, j);
+    const uint32_t qf = qfs[j];
     const bool live = !(qf & QF_DEAD);
     uint32_t q = qf & QF_QMASK;
     const bool pr = live && ((stv >> j) & 1u);  // Alg. 1 l.26
     if (pr && (q | mtim[j])) ct.quanta[row0 + j] = quanta0;
+    wq |= pr && q != 0;
     wm |= pr && mtim[j] != 0;
     wb |= pr;
-    if (pr) qw[j >> 2] &= ~((uint32_t)QF_QMASK << (8 * (j & 3)));
+    qfs[j] = pr ? (qf & ~(uint32_t)QF_QMASK) : qf;
     mtim[j] = pr ? 0u : mtim[j];
     base[j] = pr ? t : base[j];
     q = pr ? 0u : q;
@@ -454,7 +416,12 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, const CallTable& c
     nlive += live ? 1u : 0u;
     hq += live ? (1ull << (4 * q)) : 0ull;
   }
-  if (qw[0] != qw0 || qw[1] != qw1) *reinterpret_cast<uint2*>(ct.qf + row0) = make_uint2(qw[0], qw[1]);
+  if (wq) {
+#pragma unroll
+    for (int h = 0; h < R / 4; ++h)
+      reinterpret_cast<uint32_t*>(ct.qf + row0)[h] =
+          qfs[4 * h] | (qfs[4 * h + 1] << 8) | (qfs[4 * h + 2] << 16) | (qfs[4 * h + 3] << 24);
+  }
   if (wb) {
 #pragma unroll
     for (int h = 0; h < R / 4; ++h)
@@ -467,91 +434,17 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, const CallTable& c
   }
 }
 
-// The dense pass over one tile (thread: 8 consecutive rows).  Rows the prologue touches wait for
-// it: this step's arrivals (rows >= first_new: written by the prologue, loaded again afterwards)
-// and the rows of programs with a completion in this step (s_filt: a 2048-bit filter of their
-// process-table rows, built from the parameters; a collision only defers more).  Those keep the
-// row fields of the first load (the prologue does not change them) and only gather their program
-// rows again; the completed rows among them are known from the parameters (s_dead).  All other
-// rows run at once, reading nothing the prologue writes.  qw: the rows' flags after the pass.
-__device__ __forceinline__ void tile_pass(const StepArgs& a, uint32_t tile, const uint32_t* s_filt, bool filt_on,
-                                          uint32_t* s_dead, uint32_t (&qw)[2], uint64_t& hq, uint32_t& npromo,
-                                          uint32_t& nlive) {
+// Per-tile and per-super-tile queue counts + promotion / live totals of one CTA.
+template <int NT = SCAN_THREADS>
+__device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t tile, uint64_t hq,
+                                            uint32_t npromo, uint32_t nlive) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t wq16[NW][MAX_K / 2];  // per warp: 16-bit counts of queues 2w, 2w + 1
+  __shared__ uint32_t wn[NW];
   const uint32_t tid = threadIdx.x;
-  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
-  const bool have = row0 < a.n_rows;
-  const CallTable& ct = a.ct;
-  uint32_t prog[8], base[8], mtim[8];
-  bool full = false, prog_only = false;
-  qw[0] = qw[1] = 0x40404040u;  // QF_DEAD
-  if (have) {
-    const uint2 qv = *reinterpret_cast<const uint2*>(ct.qf + row0);
-    const uint4 p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
-    const uint4 p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
-    const uint4 b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
-    const uint4 b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
-    const uint4 m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
-    const uint4 m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
-    qw[0] = qv.x;
-    qw[1] = qv.y;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      prog[j] = lane4(j < 4 ? p0 : p1, j & 3);
-      base[j] = lane4(j < 4 ? b0 : b1, j & 3);
-      mtim[j] = lane4(j < 4 ? m0 : m1, j & 3);
-    }
-    full = a.defer_all || row0 + ROWS_PER_THREAD > a.first_new;
-    if (!full && filt_on) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) prog_only |= ((s_filt[(prog[j] >> 5) & 63] >> (prog[j] & 31)) & 1u) != 0;
-    }
-    if (!full && !prog_only) dense_rows<false>(a.pol, ct, a.pt, a.t, row0, qw, prog, base, mtim, hq, npromo, nlive);
-  }
-  if (__syncthreads_or(full || prog_only)) {
-    if (filt_on) {
-      // this step's completed rows in this tile (marked dead by the prologue)
-      if (tid < TILE / 32) s_dead[tid] = 0;
-      __syncthreads();
-      if (tid < a.pro.n_comp) {
-        const uint32_t sl = a.pro.comp[tid];
-        if (sl / TILE == tile) atomicOr(&s_dead[(sl % TILE) >> 5], 1u << (sl & 31));
-      }
-    }
-    wait_prologue(a.ctl, a.seqno);
-    if (full) {
-      const uint2 qv = __ldcg(reinterpret_cast<const uint2*>(ct.qf + row0));
-      const uint4 p0 = __ldcg(reinterpret_cast<const uint4*>(ct.prog + row0));
-      const uint4 p1 = __ldcg(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
-      const uint4 b0 = __ldcg(reinterpret_cast<const uint4*>(ct.base + row0));
-      const uint4 b1 = __ldcg(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
-      const uint4 m0 = __ldcg(reinterpret_cast<const uint4*>(ct.mtime + row0));
-      const uint4 m1 = __ldcg(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
-      qw[0] = qv.x;
-      qw[1] = qv.y;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        prog[j] = lane4(j < 4 ? p0 : p1, j & 3);
-        base[j] = lane4(j < 4 ? b0 : b1, j & 3);
-        mtim[j] = lane4(j < 4 ? m0 : m1, j & 3);
-      }
-      dense_rows<true>(a.pol, ct, a.pt, a.t, row0, qw, prog, base, mtim, hq, npromo, nlive);
-    } else if (prog_only) {
-      const uint32_t dead = (s_dead[(tid * ROWS_PER_THREAD) >> 5] >> ((tid * ROWS_PER_THREAD) & 31)) & 0xFFu;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if ((dead >> j) & 1u) qw[j >> 2] = (qw[j >> 2] & ~(0xFFu << (8 * (j & 3)))) | ((uint32_t)QF_DEAD << (8 * (j & 3)));
-      dense_rows<true>(a.pol, ct, a.pt, a.t, row0, qw, prog, base, mtim, hq, npromo, nlive);
-    }
-  }
-}
-
-// Per-tile and per-super-tile queue counts, promotions and live rows of one tile.  The 4-bit
-// per-thread fields are widened to 16 bits (<= 256 per warp), two queues per word, one redux.sync
-// per word of the K queues in use.
-__device__ __forceinline__ void tile_publish(const StepArgs& a, uint32_t tile, uint64_t hq, uint32_t npromo,
-                                             uint32_t nlive, uint32_t (*wq16)[MAX_K / 2], uint32_t* wn) {
-  constexpr int NW = ST_THREADS / 32;
-  const uint32_t tid = threadIdx.x, K = a.pol.K;
+  // per-queue counts: the 4-bit per-thread fields widened to 16 bits (<= 256 per warp), two
+  // queues per word, one redux.sync per word of the K queues in use
+  const uint32_t K = pol.K;
 #pragma unroll
   for (int w = 0; w < MAX_K / 2; ++w) {
     if ((uint32_t)(2 * w) < K) {
@@ -569,574 +462,700 @@ __device__ __forceinline__ void tile_publish(const StepArgs& a, uint32_t tile, u
 #pragma unroll
       for (int w = 0; w < NW; ++w) c += (wq16[w][tid >> 1] >> (16 * (tid & 1))) & 0xFFFFu;
     }
-    a.out.tile_cnt[(size_t)tile * MAX_K + tid] = c;
-    if (c) atomicAdd(a.out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, c);
+    out.tile_cnt[(size_t)tile * MAX_K + tid] = c;
+    if (c) atomicAdd(out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, c);
   } else if (tid == 32) {
-    uint32_t pr = 0, lv = 0;
+    uint32_t a = 0, b = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) { pr += wn[w] >> 16; lv += wn[w] & 0xFFFFu; }
-    uint32_t* qp = a.ctl->qpart[tile % QP_LINES];
-    if (pr) atomicAdd(qp + MAX_K, pr);
-    if (lv) atomicAdd(qp + MAX_K + 1, lv);
+    for (int w = 0; w < NW; ++w) { a += wn[w] >> 16; b += wn[w] & 0xFFFFu; }
+    uint32_t* qp = ctl->qpart[blockIdx.x % QP_LINES];
+    if (a) atomicAdd(qp + MAX_K, a);
+    if (b) atomicAdd(qp + MAX_K + 1, b);
   }
-  __syncthreads();  // wq16 / wn reuse
 }
 
-// ---------------------------------------------------------------------------------------------
-// a5 selection (after the first grid barrier).  q* = the smallest queue with
-// sum_{k<=q*} total_k >= BS (K if none), m' = BS - sum_{k<q*} total_k.  The BS smallest keys
-// (q, arrival, not-running, seq) are all among: every live row of a queue below q*, the first m'
-// rows of q* in table order (region A), and the running rows of q* that follow them inside the
-// same arrival group (region B: key order inside q* differs from table order only by moving
-// running calls forward within an arrival group).  Region A is written at its position in
-// (queue, seq) order: a stable counting sort by queue, base_q = sum_{k<q} total_k plus the rows
-// of queue q in earlier tiles (two-level prefix: super-tiles of SUP_TILES tiles, then the earlier
-// tiles of the own super-tile) plus the rank inside the tile.
-// ---------------------------------------------------------------------------------------------
-struct SelSmem {
-  uint32_t tot[ST_THREADS / MAX_K][MAX_K];  // per group of 16 threads: partial totals
-  uint32_t pre[ST_THREADS / MAX_K][MAX_K];  // ... partial prefix of the tile
-  uint32_t ownk[MAX_K];                     // the tile's own counts
-  uint32_t base[MAX_K], prek[MAX_K];        // sum_{k<q} total_k; rows of q in earlier tiles
-  uint32_t qs, m, nx, has, n_promo, n_live;
-};
-
-__device__ void select_for(const StepArgs& a, uint32_t tile, SelSmem& S) {
-  constexpr int NG = ST_THREADS / MAX_K;  // 32 groups
-  const uint32_t tid = threadIdx.x, h = tid / MAX_K, k = tid % MAX_K;
-  const uint32_t K = a.pol.K, BS = a.pol.max_batch;
-  const uint32_t nsup = (a.ntiles + SUP_TILES - 1) / SUP_TILES;
-  const bool is_tile = tile != NONE;
-  const uint32_t my_sup = is_tile ? tile / SUP_TILES : 0u, tr = my_sup * SUP_TILES + h;
-  uint32_t tot = 0, pre = 0;
-  if (k < K) {
-    // every load issued before any is consumed: the tile row, then up to 2 super-tile rows per
-    // group (8M rows), more in a loop
-    const bool has_tr = is_tile && h < SUP_TILES && tr <= tile;
-    const uint32_t c = has_tr ? __ldcg(a.out.tile_cnt + (size_t)tr * MAX_K + k) : 0u;
-    const uint32_t v0 = h < nsup ? __ldcg(a.out.sup_cnt + h * MAX_K + k) : 0u;
-    const uint32_t v1 = h + NG < nsup ? __ldcg(a.out.sup_cnt + (h + NG) * MAX_K + k) : 0u;
-    tot = v0 + v1;
-    pre = (is_tile && h < my_sup ? v0 : 0u) + (is_tile && h + NG < my_sup ? v1 : 0u);
-    for (uint32_t s = h + 2 * NG; s < nsup; s += NG) {
-      const uint32_t w = __ldcg(a.out.sup_cnt + s * MAX_K + k);
-      tot += w;
-      pre += (is_tile && s < my_sup) ? w : 0u;
+// pre (A/B switch AUTX_SCAN_PRE): what a CTA does while it waits for the prologue (PDL).  Rows
+// below first_new (this step's first arrival slot) keep prog/base/mtime through the prologue
+// (it writes only new rows and the qf/loc of completed ones; everything earlier in the stream
+// is complete once this grid runs), so they may be read before the wait; qf, the program rows
+// and new rows are read after it.  0: nothing early; 1: prog early + L2 prefetch of the rows'
+// program entries and of the previous batch's records (the gather's cold reads); 2: prog, base
+// and mtime early + the same prefetches.
+__global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                                                               Outputs out, uint32_t t, uint32_t n_rows,
+                                                               uint32_t first_new, uint32_t pre) {
+  const uint32_t tid = threadIdx.x, tile = blockIdx.x;
+  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  const bool early = pre != 0 && row0 + ROWS_PER_THREAD <= first_new;
+  uint4 p0, p1, b0, b1, m0, m1;
+  if (early) {
+    p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+    p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    if (pre >= 2) {
+      b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+      b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+      m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+      m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
     }
-    if (has_tr) {
-      if (tr < tile) pre += c;
-      else S.ownk[k] = c;
-    }
-  } else if (is_tile && h == tile % SUP_TILES) {
-    S.ownk[k] = 0;
   }
-  S.tot[h][k] = tot;
-  S.pre[h][k] = pre;
-  if (tid >= 256 && tid < 288) {
-    // promotions (even lanes) and live rows (odd lanes), for the host record
-    const uint32_t l = tid - 256;
-    uint32_t v = __ldcg(&a.ctl->qpart[l >> 1][MAX_K + (l & 1)]);
+  if (pre != 0) {
+    // the previous batch's records: region B and most of region A in the gather
+    const uint32_t i = (gridDim.x - 1 - tile) * SCAN_THREADS + tid;
+    if (i < ctl->n_prev) {
+      const uint32_t sl = out.prev_slots[i];
+      prefetch_l2(ct.cid + sl); prefetch_l2(ct.arr + sl); prefetch_l2(ct.tok + sl);
+      prefetch_l2(ct.exec + sl); prefetch_l2(ct.mtime + sl); prefetch_l2(ct.quanta + sl);
+      prefetch_l2(ct.bidx + sl); prefetch_l2(ct.qf + sl);
+    }
+    if (early && pol.beta_den != 0) {
+      const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
-    for (int d = 2; d < 32; d <<= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    if (l == 0) S.n_promo = v;
-    if (l == 1) S.n_live = v;
+      for (int j = 0; j < 8; ++j)
+        if (j == 0 || pr[j] != pr[j - 1]) prefetch_l2(pt.info + pr[j]);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(1);
+  uint64_t hq = 0;
+  uint32_t npromo = 0, nlive = 0;
+  if (row0 < n_rows) {
+    const uint2 qv = __ldcs(reinterpret_cast<const uint2*>(ct.qf + row0));
+    if (!early) {
+      p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+      p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    }
+    if (!early || pre < 2) {
+      b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+      b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+      m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+      m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+    }
+    uint32_t qfs[8], prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
+    dense_rows<8>(pol, ct, pt, t, row0, qfs, prog, base, mtim, hq, npromo, nlive);
+  }
+  tile_counts(pol, ctl, out, tile, hq, npromo, nlive);
+  CHAIN_END(1);
+}
+
+// Self-selecting gather (default): no separate selection kernel.  Every CTA derives q* and m'
+// from the per-queue totals, and a tile CTA its candidate offset from the counts of the earlier
+// tiles, both from a two-level table the scan fills: per-tile counts (tile_cnt) and per-super-tile
+// counts (sup_cnt, SUP_TILES tiles each, accumulated with atomics).  The prefix of tile T is the
+// super-tiles before T's plus the <= SUP_TILES - 1 tiles of T's super-tile before T: one round of
+// a few loads per thread (half-warp h, lane k = queue k).
+//     off(T) = pre_a(T) + min(pre_q(T), m'),   pre_a = sum_{T'<T} sum_{k<q*} cnt,  pre_q = sum_{T'<T} cnt_q*.
+// Inside the tile, a thread's first candidate position follows from the exclusive counts of
+// earlier threads (A = live rows with q < q*, Q = live rows of q*) without a second scan, since
+// the q* rows are taken in table order:  pos = off + A + min(Q, m' - min(pre_q, m')).
+// The thread taking the m'-th q* row publishes its slot (region A's boundary); the previous-batch
+// CTAs emit keys for every live q* call of the previous batch and k_rank drops those with
+// slot <= boundary (they are in region A).
+__device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, uint32_t n_rows, uint32_t ntiles, uint32_t t) {
+  constexpr int NT = SCAN_THREADS, NW = NT / 32, NH = NT / MAX_K;  // NH half-warps of MAX_K lanes
+  __shared__ uint32_t s_tot[NH][MAX_K], s_pre[NH][MAX_K];
+  __shared__ uint32_t s_qs, s_m, s_prea, s_preq, s_has;
+  __shared__ uint32_t s_own[MAX_K];
+  __shared__ uint32_t s_cnt[NW];
+  const uint32_t tid = threadIdx.x, tile = blockIdx.x;
+  const uint32_t K = pol.K, BS = pol.max_batch;
+  const bool is_tile = tile < ntiles;
+  // (1) one round of independent loads: this tile's queue bytes first (they do not depend on the
+  // selection), then the counts
+  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  const uint2 qv = is_tile && row0 < n_rows ? *reinterpret_cast<const uint2*>(ct.qf + row0)
+                                            : make_uint2(0x40404040u, 0x40404040u);
+  {
+    const uint32_t h = tid / MAX_K, k = tid % MAX_K;
+    const uint32_t nsup = (ntiles + SUP_TILES - 1) / SUP_TILES, my_sup = tile / SUP_TILES;
+    uint32_t tot = 0, pre = 0;
+    if (k < K) {
+      // all loads issued before any is consumed (a rolled loop would chain one L2 round trip per
+      // iteration): the tile count, then up to 8 super-tile rows per half-warp (4.2M rows)
+      const uint32_t tr = my_sup * SUP_TILES + h;  // earlier tile of the same super-tile, or this one
+      const bool has_tr = is_tile && tr <= tile;
+      const uint32_t c = has_tr ? __ldcg(out.tile_cnt + (size_t)tr * MAX_K + k) : 0u;
+      constexpr int SU = 8;
+      uint32_t v[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const uint32_t S = h + u * NH;
+        v[u] = S < nsup ? __ldcg(out.sup_cnt + S * MAX_K + k) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const uint32_t S = h + u * NH;
+        tot += v[u];
+        pre += (is_tile && S < my_sup) ? v[u] : 0u;
+      }
+      for (uint32_t S = h + SU * NH; S < nsup; S += NH) {  // larger tables
+        const uint32_t w = __ldcg(out.sup_cnt + S * MAX_K + k);
+        tot += w;
+        pre += (is_tile && S < my_sup) ? w : 0u;
+      }
+      if (has_tr) {
+        if (tr < tile) pre += c;
+        else s_own[k] = c;
+      }
+    }
+    s_tot[h][k] = tot;
+    s_pre[h][k] = pre;
+    if (tile == 0 && tid < 32) {
+      // promotions (even lanes) and live rows (odd lanes) for finalize's host record
+      uint32_t stat = tid < 2 * QP_LINES ? __ldcg(&ctl->qpart[tid >> 1][MAX_K + (tid & 1)]) : 0u;
+#pragma unroll
+      for (int d = 2; d < 32; d <<= 1) stat += __shfl_xor_sync(0xffffffffu, stat, d);
+      if (tid == 0) ctl->n_promoted = stat;
+      if (tid == 1) ctl->n_live = stat;
+    }
+  }
+  if (!is_tile) {
+    // previous batch: records (for preempt) and region-B keys
+    const uint32_t j = (tile - ntiles) * NT + tid;
+    const uint32_t n_prev = ctl->n_prev;
+    CandRec r;
+    if (j < n_prev) load_rec(ct, out.prev_slots[j], &r);
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t tq = 0;
+      if (tid < MAX_K) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) tq += s_tot[h][tid];
+      }
+      const uint32_t incl = warp_incl_scan(tq);
+      const uint32_t b = __ballot_sync(0xffffffffu, tid < K && incl >= BS);
+      const uint32_t qs = b ? __ffs(b) - 1 : K;
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (tid == 0) { s_qs = qs; s_m = qs < K ? BS : tot; }  // s_m: n_cand_a here
+    }
+    __syncthreads();
+    if (j < n_prev) {
+      out.prev_rec[j] = r;
+      const bool b = !(r.qf & QF_DEAD) && (r.qf & QF_QMASK) == s_qs;
+      out.ckey[s_m + j] = b ? cand_key(r, t) : ~0ull;
+      out.ckvb[s_m + j] = blocks_for(pol, r.tok + r.exec + 1);  // R14
+    }
+    return;
   }
   __syncthreads();
+  // (2) q*, m', and this tile's prefix (warp 0, lane k = queue k)
   if (tid < 32) {
-    uint32_t T = 0, P = 0, O = 0;
+    uint32_t tq = 0, pk = 0;
     if (tid < MAX_K) {
-#pragma unroll 8
-      for (int g = 0; g < NG; ++g) { T += S.tot[g][tid]; P += S.pre[g][tid]; }
-      O = is_tile ? S.ownk[tid] : 0u;
+#pragma unroll
+      for (int h = 0; h < NH; ++h) { tq += s_tot[h][tid]; pk += s_pre[h][tid]; }
     }
-    const uint32_t incl = warp_incl_scan(T);
+    const uint32_t incl = warp_incl_scan(tq);
     const uint32_t b = __ballot_sync(0xffffffffu, tid < K && incl >= BS);
     const uint32_t qs = b ? __ffs(b) - 1 : K;
-    const uint32_t base = incl - T;
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t bq = __shfl_sync(0xffffffffu, base, qs & 31);
-    const uint32_t m = qs < K ? BS - bq : 0u;
-    const bool has = __ballot_sync(0xffffffffu, tid < K && O > 0 && (tid < qs || (tid == qs && P < m))) != 0;
-    if (tid < MAX_K) {
-      S.base[tid] = base;
-      S.prek[tid] = P;
-    }
+    const uint32_t excl = __shfl_sync(0xffffffffu, incl - tq, qs & 31);
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t pa = warp_sum(tid < qs ? pk : 0u);
+    const uint32_t pq = __shfl_sync(0xffffffffu, pk, qs & 31);
+    // this tile's own live rows below q* and of q*: no candidate unless one of them is taken
+    const uint32_t own = tid < K ? s_own[tid] : 0u;
+    const uint32_t oa = warp_sum(tid < qs ? own : 0u);
+    const uint32_t oq = __shfl_sync(0xffffffffu, own, qs & 31);
     if (tid == 0) {
-      S.qs = qs;
-      S.m = m;
-      S.nx = qs < K ? BS : total;
-      S.has = has ? 1u : 0u;
+      const uint32_t m = qs < K ? BS - excl : 0;
+      s_qs = qs;
+      s_m = m;
+      s_prea = pa;
+      s_preq = qs < K ? pq : 0;
+      s_has = oa > 0 || (qs < K && oq > 0 && pq < m);
+      if (tile == 0) {
+        ctl->qstar = qs;
+        ctl->mprime = m;
+        ctl->n_cand_a = qs < K ? BS : tot;
+      }
     }
   }
   __syncthreads();
-}
-
-// Region A rows of one tile -> out.xs at their (queue, seq) positions; the tile holding the
-// m'-th row of q* publishes it (region A's boundary).  Ranks inside the tile: one block scan per
-// word of 4 queues (16-bit fields), over the queues <= q* (ranks: the tile has candidates).  The
-// tile also writes the records of its rows that ran in the previous step to out.ps (at their
-// previous-batch index), so that the finalize reads the previous batch contiguously.  The copy is
-// cooperative: the owning threads only publish each row's position in shared memory, then all
-// threads copy the rows in [lo, hi] with consecutive rows on consecutive lanes (coalesced loads
-// from the table, coalesced stores into the struct-of-arrays records), whichever threads own them.
-// sm: >= TILE * 5 + 64 bytes of shared scratch.
-__device__ void extract_tile(const StepArgs& a, uint32_t tile, const uint32_t (&qw)[2], const SelSmem& S,
-                             unsigned long long* red64, bool ranks, unsigned char* sm) {
-  constexpr int NT = ST_THREADS;
-  const uint32_t tid = threadIdx.x, K = a.pol.K;
-  const uint32_t qs = S.qs, m = S.m;
-  const uint32_t qmax = min(qs, K - 1);
-  const uint32_t nw = ranks ? (qmax >> 2) + 1 : 0u;
-  const uint32_t l0 = tid * ROWS_PER_THREAD, tile0 = tile * TILE;
-  uint16_t* s_px = reinterpret_cast<uint16_t*>(sm);           // [TILE] position in region A or 0xFFFF
-  uint32_t* s_qf = reinterpret_cast<uint32_t*>(sm + 2 * TILE);  // [TILE / 4] flags after the pass
-  uint32_t* s_rng = reinterpret_cast<uint32_t*>(sm + 3 * TILE); // [2 * NW] per-warp lo / hi
-  uint32_t pos2[4];  // positions of rows 2k, 2k+1 in 16-bit halves (BS <= 2048)
-  uint32_t sel = 0, runm = 0;
-  const long long et0 = clock64();
-#pragma unroll
-  for (int k = 0; k < 4; ++k) pos2[k] = 0xFFFFFFFFu;
+  // tiles without candidates leave now (their SM slots go to the next kernel's CTAs); the
+  // boundary row is always in a tile with candidates
+  if (STAMPS_ON && tile == 0 && tid == 0) ctl->dbg[57] = globaltimer();
+  if (!s_has) return;
+  const uint32_t qs = s_qs, m = s_m;
+  uint32_t qfs[8], na = 0, nq = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const uint32_t qf = qf_at(qw, j);
-    runm |= (!(qf & QF_DEAD) && (qf & QF_RUN)) ? 1u << j : 0u;
+    qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
+    const bool live = !(qfs[j] & QF_DEAD);
+    const uint32_t q = qfs[j] & QF_QMASK;
+    na += (live && q < qs) ? 1u : 0u;
+    nq += (live && q == qs) ? 1u : 0u;
   }
-  for (uint32_t w = 0; w < nw; ++w) {
-    uint64_t c = 0;
+  // (3) exclusive (A, Q) counts of the earlier threads of this tile
+  const uint32_t v = (na << 16) | nq;  // <= 2048 each
+  const uint32_t vin = warp_incl_scan(v);
+  if (lane_id() == 31) s_cnt[warp_id()] = vin;
+  __syncthreads();
+  uint32_t vex = vin - v;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t qf = qf_at(qw, j), q = qf & QF_QMASK;
-      if (!(qf & QF_DEAD) && q <= qmax && (q >> 2) == w) c += 1ull << (16 * (q & 3));
+  for (int w = 0; w < NW; ++w) vex += (uint32_t)w < warp_id() ? s_cnt[w] : 0u;
+  const uint32_t pre_a = s_prea, pre_q = s_preq;
+  const uint32_t mq = m - min(pre_q, m);  // q* rows still to take at this tile's start
+  uint32_t rq = pre_q + (vex & 0xffffu);
+  uint32_t pos = pre_a + min(pre_q, m) + (vex >> 16) + min(vex & 0xffffu, mq);
+  uint32_t flags = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t qf = qfs[j];
+    if (qf & QF_DEAD) continue;
+    const uint32_t q = qf & QF_QMASK;
+    bool sel = q < qs;
+    if (q == qs) {
+      sel = rq < m;
+      if (rq + 1 == m) ctl->qs_bnd1 = row0 + j + 1;
+      ++rq;
     }
-    uint64_t ex = block_excl_scan<unsigned long long, NT>(c, red64, nullptr);
+    if (sel) flags |= 1u << j;
+  }
+  if (STAMPS_ON && tile == 0 && tid == 0) ctl->dbg[58] = globaltimer();
+  if (flags) {
+    const uint4* cidv = reinterpret_cast<const uint4*>(ct.cid + row0);
+    uint4 c4[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t qf = qf_at(qw, j), q = qf & QF_QMASK;
-      if (!(qf & QF_DEAD) && q <= qmax && (q >> 2) == w) {
-        const uint32_t sh = 16 * (q & 3);
-        const uint32_t rank = S.prek[q] + (uint32_t)((ex >> sh) & 0xFFFFu);
-        ex += 1ull << sh;
-        if (q < qs || rank < m) {
-          sel |= 1u << j;
-          const uint32_t pos = S.base[q] + rank;
-          pos2[j >> 1] = (pos2[j >> 1] & ~(0xFFFFu << (16 * (j & 1)))) | (pos << (16 * (j & 1)));
-          if (q == qs && rank + 1 == m) {  // region A's boundary row
-            a.ctl->bnd_slot = tile0 + l0 + j;
-            a.ctl->bnd_arr = __ldcg(a.ct.arr + tile0 + l0 + j);
+    for (int w = 0; w < 4; ++w) c4[w] = cidv[w];
+    uint4 ar[2], tk[2], ex[2], mt[2], qt[2], bd[2];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      ar[w] = reinterpret_cast<const uint4*>(ct.arr + row0)[w];
+      tk[w] = reinterpret_cast<const uint4*>(ct.tok + row0)[w];
+      ex[w] = reinterpret_cast<const uint4*>(ct.exec + row0)[w];
+      mt[w] = reinterpret_cast<const uint4*>(ct.mtime + row0)[w];
+      qt[w] = reinterpret_cast<const uint4*>(ct.quanta + row0)[w];
+      bd[w] = reinterpret_cast<const uint4*>(ct.bidx + row0)[w];
+    }
+    auto lane4 = [](const uint4& a, int k) { return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : a.w; };
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (flags & (1u << j)) {
+        CandRec r;
+        const uint4& cc = c4[j >> 1];
+        r.cid = (j & 1) ? ((uint64_t)cc.w << 32 | cc.z) : ((uint64_t)cc.y << 32 | cc.x);
+        r.slot = row0 + j;
+        r.arr = lane4(ar[j >> 2], j & 3);
+        r.tok = lane4(tk[j >> 2], j & 3);
+        r.exec = lane4(ex[j >> 2], j & 3);
+        r.mtime = lane4(mt[j >> 2], j & 3);
+        r.quanta = lane4(qt[j >> 2], j & 3);
+        r.qf = qfs[j];
+        r._pad = (qfs[j] & QF_RUN) ? lane4(bd[j >> 2], j & 3) : NONE;  // previous-batch index
+        out.cand[pos] = row0 + j;
+        out.cand_rec[pos] = r;
+        out.ckey[pos] = cand_key(r, t);
+        out.ckvb[pos] = blocks_for(pol, r.tok + r.exec + 1);  // R14
+        ++pos;
+      }
+  }
+  if (STAMPS_ON && tile == 0) {
+    __syncwarp();
+    if (tid == 0) ctl->dbg[59] = globaltimer();
+  }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS, 4) k_gather_ss(Policy pol, CallTable ct, Ctl* ctl, Outputs out,
+                                                               uint32_t n_rows, uint32_t ntiles, uint32_t t) {
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(3);
+  gather_ss_body(pol, ct, ctl, out, n_rows, ntiles, t);
+  CHAIN_END(3);
+}
+
+// ---------------------------------------------------------------------------------------------
+// a5/a6/a3/a7-plan: one CTA.  Sort <= 2 BS candidate keys
+//     q:4 | arrival (relative to t):27 | not-running:1 | seq (row):31       (R11, R12)
+// (region A from the gather, plus the previous batch's calls of q*, de-duplicated), cut the
+// longest prefix with count <= BS and sum kvb <= P (Alg. 1 l.32-39, first misfit stops, R13),
+// emit batch/admit/preempt, account (batch: exec++, mtime++, quanta--, running; everyone else
+// waits implicitly via the closed-form counters), demote batch calls whose quantum is exhausted
+// (Alg. 1 l.20-23), allocate KV blocks and build the swap plan.
+// ---------------------------------------------------------------------------------------------
+extern __shared__ unsigned char fin_smem[];
+template <int NT, int R, bool LISTS = false>
+__device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
+                              uint32_t t, uint32_t np, uint32_t seqno);
+
+__device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
+
+// k_rank: the candidates' sort.  A single SM needs ~35k cycles to sort 2048 64-bit keys with
+// any block sort (measured: scripts/micro/sort_bench.cu), so the order is computed across many
+// SMs instead: every CTA holds all n <= 2 BS keys in shared memory and each key's output index is
+// the number of keys before it (the keys are unique), RANK_SUB threads per key.
+constexpr int RANK_THREADS = 256, RANK_SUB = 16, RANK_PER_CTA = RANK_THREADS / RANK_SUB;
+__global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
+                                                       bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(4);
+  __shared__ uint32_t red_r[33];
+  const uint32_t na = ctl->n_cand_a;
+  const uint32_t n = na + ctl->n_prev;
+  uint64_t* rk = reinterpret_cast<uint64_t*>(fin_smem);  // [n] keys, ~0 = no candidate
+  uint64_t* ck = rk + n;                                 // [n_valid] the candidates' keys
+  uint32_t* ci = reinterpret_cast<uint32_t*>(ck + n);    // [n_valid] their element index
+  uint32_t* rkv = ci + n;                                // [n] kvb of each element
+  uint32_t* ckv = rkv + n;                               // [n_valid] the candidates' kvb
+  const bool lists = out.rank_lists != 0;
+  const uint32_t e0 = blockIdx.x * RANK_PER_CTA;
+  const uint32_t bnd1 = ctl->qs_bnd1;
+  // (1) keys into shared memory; previous-batch keys at or before region A's boundary are region
+  // A's already (self-selecting gather; bnd1 = 0 otherwise) and become sentinels.  The key loads
+  // cover the buffer's capacity, so they need not wait for the counts above (one round trip).
+  constexpr int RK = 8;
+  const uint32_t cap = 2 * pol.max_batch;
+  uint32_t nv = 0;
+  for (uint32_t c0 = 0; c0 < cap; c0 += RK * RANK_THREADS) {
+    uint64_t kk[RK];
+    uint32_t kb[RK];
+#pragma unroll
+    for (int r = 0; r < RK; ++r) {
+      const uint32_t i = c0 + r * RANK_THREADS + threadIdx.x;
+      kk[r] = i < cap ? __ldcg(out.ckey + i) : ~0ull;
+      kb[r] = lists && i < cap ? __ldcg(out.ckvb + i) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < RK; ++r) {
+      const uint32_t i = c0 + r * RANK_THREADS + threadIdx.x;
+      if (i < n) {
+        uint64_t k = kk[r];
+        if (i >= na && (uint32_t)(k & 0x7FFFFFFFu) < bnd1) k = ~0ull;
+        nv += k != ~0ull ? 1u : 0u;
+        rk[i] = k;
+        rkv[i] = kb[r];
+      }
+    }
+  }
+  if (blockIdx.x * (RANK_PER_CTA / 2) < n) {
+    // (2) compact the candidates (same deterministic order in every CTA): sentinels rank last and
+    // nobody reads them, so only the n_valid candidates are ranked and compared against
+    if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[54] = globaltimer();
+    uint32_t n_valid;
+    uint32_t off = block_excl_scan<uint32_t, RANK_THREADS>(nv, red_r, &n_valid);
+    for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS)
+      if (rk[i] != ~0ull) { ck[off] = rk[i]; ci[off] = i; ckv[off] = rkv[i]; ++off; }
+    __syncthreads();
+    if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[55] = globaltimer();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctl->n_cand_b = n_valid - na;
+      if (STAMPS_ON) {
+        ctl->dbg[52] = n_valid;
+        ctl->dbg[53] = n;
+      }
+    }
+    // (3) rank = number of smaller keys (keys are unique), RANK_SUB threads per key; the record
+    // load is issued before the count so that its latency hides behind it
+    // when the candidates fill at most half the grid's capacity, a full warp per key (8 keys per
+    // CTA) keeps every CTA busy and halves each thread's compares; else half a warp per key
+    const bool wide = 2 * n_valid <= gridDim.x * RANK_PER_CTA && out.rank_wide;
+    const uint32_t subn = wide ? 32u : (uint32_t)RANK_SUB;
+    const uint32_t e = (wide ? blockIdx.x * (RANK_PER_CTA / 2) : e0) + threadIdx.x / subn, sub = threadIdx.x % subn;
+    uint32_t cnt = 0, eo = 0, kvs = 0, nad = 0;
+    uint64_t x = 0;
+    CandRec rec;
+    if (e < n_valid) {
+      x = ck[e];
+      eo = ci[e];
+      if (sub == 0) rec = eo < na ? out.cand_rec[eo] : out.prev_rec[eo - na];
+      if (lists) {
+        // with the rank, the kvb prefix (Alg. 1 l.34-37) and the admit rank (smaller keys of
+        // calls that did not run: not resident under eager eviction)
+#pragma unroll 4
+        for (uint32_t j = sub; j < n_valid; j += subn) {  // (4 independent smem chains in flight)
+          const uint64_t y = ck[j];
+          const bool lt = y < x;
+          cnt += lt ? 1u : 0u;
+          kvs += lt ? ckv[j] : 0u;
+          nad += (lt && ((y >> 31) & 1u)) ? 1u : 0u;
+        }
+      } else {
+#pragma unroll 4
+        for (uint32_t j = sub; j < n_valid; j += subn) cnt += ck[j] < x ? 1u : 0u;
+      }
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      if ((uint32_t)d >= subn) break;
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+      if (lists) {
+        kvs += __shfl_xor_sync(0xffffffffu, kvs, d);
+        nad += __shfl_xor_sync(0xffffffffu, nad, d);
+      }
+    }
+    if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[56] = globaltimer();
+    if (sub == 0 && e < n_valid) {
+      out.skey[cnt] = x;
+      out.sidx[cnt] = eo;
+      out.srec[cnt] = rec;
+      // a running call (previous-batch entry rec._pad) publishes its sorted position: finalize
+      // tests the previous batch's membership in the new one without searching
+      if (rec.qf & QF_RUN) out.prev_pos[rec._pad] = (unsigned long long)seqno << 32 | cnt;
+      if (lists) {
+        // Alg. 1 l.32-39 for this key alone: kvb >= 1 makes the inclusive prefix strictly
+        // increasing, so "count <= BS and sum kvb <= P" holds exactly on a prefix of the order
+        // (the first misfit stops, R13); the batch entries write their lists and accounting
+        const uint32_t incl = kvs + ckv[e];
+        const uint32_t BS = pol.max_batch;
+        if (cnt < BS && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) {
+          const uint32_t sl = rec.slot;
+          out.batch_slots[cnt] = sl;
+          out.batch_ids[cnt] = rec.cid;
+          if (out.zero_copy) { out.h_batch[cnt] = rec.cid; out.h_batch_slots[cnt] = sl; }
+          // step accounting + eager demotion (Alg. 1 l.20-23)
+          uint32_t q = rec.qf & QF_QMASK, qt = rec.quanta;
+          ct.exec[sl] = rec.exec + 1;
+          ct.mtime[sl] = rec.mtime + 1;
+          if (qt != AUTX_INF) {
+            qt -= 1;
+            if (qt == 0) {
+              q = min(q + 1, pol.K - 1);
+              qt = pol.quanta[q];
+            }
+            ct.quanta[sl] = qt;
           }
+          ct.qf[sl] = (uint8_t)(q | QF_RUN | QF_RES);
+          ct.bidx[sl] = cnt;
+          out.prev_slots[cnt] = sl;
+          if ((x >> 31) & 1u) {  // admit: did not run in the previous step (not resident)
+            out.admit_ids[nad] = rec.cid;
+            out.admit_slots[nad] = sl;
+            if (out.zero_copy) out.h_admit[nad] = rec.cid;
+            const uint32_t held = rec.exec > 0 ? blocks_for(pol, rec.tok + rec.exec) : 0u;  // R28
+            if (held) atomicAdd(&ctl->acc_swap_in, (unsigned long long)held);
+            atomicMax(&ctl->acc_nadmit, nad + 1);
+          }
+          atomicMax(&ctl->acc_nbatch, cnt + 1);
+          atomicMax(&ctl->acc_kv, (unsigned long long)incl);
         }
       }
     }
   }
-  const long long et1 = clock64();
-  // publish positions and flags, and compact the rows to copy into a list (warp-aggregated
-  // reservations: rows stay in order inside a warp's chunk)
-  const uint32_t need = sel | runm;
-  reinterpret_cast<uint4*>(s_px)[tid] = make_uint4(pos2[0], pos2[1], pos2[2], pos2[3]);
-  reinterpret_cast<uint2*>(s_qf)[tid] = make_uint2(qw[0], qw[1]);
-  uint16_t* s_list = reinterpret_cast<uint16_t*>(sm + 3 * TILE + 64);  // [TILE] local rows to copy
-  uint32_t* s_n = s_rng;
-  if (tid == 0) *s_n = 0;
-  __syncthreads();
-  {
-    const uint32_t cnt = __popc(need);
-    const uint32_t incl = warp_incl_scan(cnt);
-    const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-    uint32_t wbase = 0;
-    if (lane_id() == 31 && wtot) wbase = atomicAdd(s_n, wtot);
-    wbase = __shfl_sync(0xffffffffu, wbase, 31);
-    uint32_t o = wbase + incl - cnt;
-    for (uint32_t nd = need; nd; nd &= nd - 1) s_list[o++] = (uint16_t)(l0 + __ffs(nd) - 1);
-  }
-  __syncthreads();
-  const uint32_t n_copy = *s_n;
-  const long long et2 = clock64();
-  const CallTable& ct = a.ct;
-  const RecSoA& xs = a.out.xs;
-  const RecSoA& ps = a.out.ps;
-  // two rows per thread per round, all loads of a round issued before any store
-  for (uint32_t i0 = tid; i0 < n_copy; i0 += 2 * NT) {
-    uint32_t lr[2], r[2], arr[2], tok[2], ex[2], mt[2], qt[2], bx[2];
-    unsigned long long cid[2];
-    bool ok[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const uint32_t i = i0 + u * NT;
-      ok[u] = i < n_copy;
-      lr[u] = ok[u] ? s_list[i] : 0u;
-      r[u] = tile0 + lr[u];
-      cid[u] = ok[u] ? ct.cid[r[u]] : 0ull;
-      arr[u] = ok[u] ? ct.arr[r[u]] : 0u;
-      tok[u] = ok[u] ? ct.tok[r[u]] : 0u;
-      ex[u] = ok[u] ? ct.exec[r[u]] : 0u;
-      mt[u] = ok[u] ? __ldcg(ct.mtime + r[u]) : 0u;  // (promotions of this kernel)
-      qt[u] = ok[u] ? __ldcg(ct.quanta + r[u]) : 0u;
-      bx[u] = ok[u] ? ct.bidx[r[u]] : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      if (!ok[u]) continue;
-      const uint32_t l = lr[u];
-      const uint32_t px = s_px[l];
-      const uint32_t qf = (s_qf[l >> 2] >> (8 * (l & 3))) & 0xFFu;
-      const bool run = !(qf & QF_DEAD) && (qf & QF_RUN);
-      const uint32_t qfb = qf | (run ? bx[u] << 8 : 0u);
-      if (px != 0xFFFFu) {
-        xs.cid[px] = cid[u]; xs.slot[px] = r[u]; xs.arr[px] = arr[u]; xs.tok[px] = tok[u];
-        xs.exec[px] = ex[u]; xs.mt[px] = mt[u]; xs.qt[px] = qt[u]; xs.qfb[px] = qfb;
-      }
-      if (run) {
-        const uint32_t b = bx[u];
-        ps.cid[b] = cid[u]; ps.slot[b] = r[u]; ps.arr[b] = arr[u]; ps.tok[b] = tok[u];
-        ps.exec[b] = ex[u]; ps.mt[b] = mt[u]; ps.qt[b] = qt[u]; ps.qfb[b] = qfb;
-      }
-    }
-  }
-  if (STAMPS_ON(a.pol)) {
-    __syncthreads();
-    if (tid == 0) {
-      atomicMax(&a.ctl->dbg[36], (unsigned long long)(et1 - et0));
-      atomicMax(&a.ctl->dbg[37], (unsigned long long)(et2 - et1));
-      atomicMax(&a.ctl->dbg[38], (unsigned long long)(clock64() - et2));
-      atomicMax(&a.ctl->dbg[35], (unsigned long long)n_copy);
-    }
-  }
+  CHAIN_END(4);
 }
 
-// ---------------------------------------------------------------------------------------------
-// a5 order + a6 cutoff + a3 demotion + a7 plan: one CTA of ST_THREADS, I candidates per thread
-// (C = ST_THREADS * I >= 2 BS).  Y = region A ++ region B (sorted by seq) is in (queue, arrival,
-// seq) order, so the key order (queue, arrival, not-running, seq) (R11, R12) is a stable
-// partition of Y inside each (queue, arrival) group with the running calls first.  The batch is
-// the longest prefix of that order with count <= BS and sum kvb <= P (Alg. 1 l.32-39, first
-// misfit stops, R13); admit = batch calls not resident, preempt = resident calls not in the
-// batch; batch calls are accounted (exec++, mtime++, quanta--; waiting calls implicitly through
-// the closed-form counters) and demoted when their quantum runs out (Alg. 1 l.20-23).
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
-
-// exclusive max-scan over the block in thread order (0 for thread 0); smem: >= 33 words
-template <int NT>
-__device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* smem) {
-  constexpr int NW = NT / 32;
-  uint32_t x = v;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-    if (lane_id() >= (uint32_t)d) x = max(x, y);
-  }
-  uint32_t ex = __shfl_up_sync(0xffffffffu, x, 1);
-  if (lane_id() == 0) ex = 0;
-  if (lane_id() == 31) smem[warp_id()] = x;
-  __syncthreads();
-  if (warp_id() == 0) {
-    uint32_t w = lane_id() < NW ? smem[lane_id()] : 0u;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
-      if (lane_id() >= (uint32_t)d) w = max(w, y);
-    }
-    uint32_t we = __shfl_up_sync(0xffffffffu, w, 1);
-    if (lane_id() == 0) we = 0;
-    if (lane_id() < NW) smem[lane_id()] = we;
-  }
-  __syncthreads();
-  const uint32_t r = max(smem[warp_id()], ex);
-  __syncthreads();
-  return r;
-}
-
-template <int I>
-constexpr size_t fin_smem_bytes() {
-  return (size_t)ST_THREADS * I * 48 + (size_t)ST_THREADS * I / 2;
-}
-
-template <int I>
-__device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs, uint32_t mp, uint32_t nx,
-                              uint32_t n_live, uint32_t n_promo, uint32_t n_prev, bool wait2,
-                              unsigned long long* red64, uint32_t* red32) {
-  constexpr int NT = ST_THREADS, IP = I / 2, C = NT * I;
-  const Policy& pol = a.pol;
-  const CallTable& ct = a.ct;
-  const Outputs& out = a.out;
-  const KvState& kv = a.kv;
-  Ctl* ctl = a.ctl;
-  uint64_t* y_cid = reinterpret_cast<uint64_t*>(dsm);
-  uint32_t* y_slot = reinterpret_cast<uint32_t*>(dsm + 8 * (size_t)C);
-  uint32_t* y_arr = y_slot + C;
-  uint32_t* y_tok = y_arr + C;
-  uint32_t* y_exec = y_tok + C;
-  uint32_t* y_mt = y_exec + C;
-  uint32_t* y_qt = y_mt + C;
-  uint32_t* y_qfb = y_qt + C;
-  uint32_t* z = y_qfb + C;    // sorted position -> index in Y
-  uint32_t* hb = z + C;       // running calls before each group head; region B's slots first
-  uint32_t* grun = hb + C;    // running calls up to each group's end (at the head's index)
-  uint8_t* inb = reinterpret_cast<uint8_t*>(grun + C);  // previous-batch entry is in the new batch
-  uint64_t* s_ad = reinterpret_cast<uint64_t*>(hb);     // admit / preempt ids for the host mirrors
-  uint64_t* s_pr = reinterpret_cast<uint64_t*>(grun);   // (hb, grun are free once z is known)
+template <int NT, int R, bool LISTS>
+__device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
+                              uint32_t t, uint32_t np, uint32_t seqno) {
+  uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] sorted keys of the first m candidates
+  // admit / preempt id lists staged in shared memory for the host mirrors (16-B aligned)
+  uint64_t* s_ad = uk + np;
+  uint64_t* s_pr = s_ad + ((pol.max_batch + 1) & ~1u);
+  __shared__ unsigned long long red64[33];
+  __shared__ uint32_t red[33];
   __shared__ uint32_t s_nbatch;
   __shared__ unsigned long long s_kvsum;
   __shared__ HostOut s_hout;
-  const uint32_t tid = threadIdx.x, BS = pol.max_batch, K = pol.K;
-  const bool stamps = STAMPS_ON(pol);
-  if (wait2) grid_wait(&ctl->bar2, a.n_tile_ctas);
-  if (stamps && tid == 0) ctl->dbg[44] = globaltimer();
-  long long dc0 = clock64(), dc1 = 0, dc2 = 0, dc3 = 0;
-  // ---- (1) one round of coalesced loads: region A, the previous batch, the boundary ------------
-  uint32_t bnd_slot = 0, bnd_arr = 0;
-  if (qs < K) {
-    bnd_slot = __ldcg(&ctl->bnd_slot);
-    bnd_arr = __ldcg(&ctl->bnd_arr);
+  const uint32_t tid = threadIdx.x;
+  const uint32_t BS = pol.max_batch;
+  const uint32_t n_prev = ctl->n_prev;
+  // region A + region B (previous-batch calls of q* not in A): no duplicates, ~0 sentinels last
+  const uint32_t ncand = ctl->n_cand_a + ctl->n_cand_b;
+  // host-record fields, loaded with everything else in the first round
+  uint32_t c_live = 0, c_promo = 0, c_err = 0, c_einfo = 0;
+  // rank_lists: k_rank has written the batch and admit lists and the accounting; its totals
+  constexpr bool lists = LISTS;
+  uint32_t a_nb = 0, a_na = 0;
+  unsigned long long a_kv = 0, a_si = 0;
+  if (tid == 0) {
+    c_live = ctl->n_live; c_promo = ctl->n_promoted; c_err = ctl->err; c_einfo = ctl->err_info;
+    if (lists) { a_nb = ctl->acc_nbatch; a_na = ctl->acc_nadmit; a_kv = ctl->acc_kv; a_si = ctl->acc_swap_in; }
   }
-  // region A: strided (coalesced), straight into the shared-memory arrays (nx <= BS <= NT * I / 2)
-  {
-    const RecSoA& xs = out.xs;
-    unsigned long long c[IP];
-    uint32_t f[IP][7];
-#pragma unroll
-    for (int r = 0; r < IP; ++r) {  // every load of the round first
-      const uint32_t i = min(r * NT + tid, BS - 1);
-      c[r] = __ldcg(xs.cid + i);
-      f[r][0] = __ldcg(xs.slot + i); f[r][1] = __ldcg(xs.arr + i); f[r][2] = __ldcg(xs.tok + i);
-      f[r][3] = __ldcg(xs.exec + i); f[r][4] = __ldcg(xs.mt + i); f[r][5] = __ldcg(xs.qt + i);
-      f[r][6] = __ldcg(xs.qfb + i);
-    }
-#pragma unroll
-    for (int r = 0; r < IP; ++r) {
-      const uint32_t i = r * NT + tid;
-      if (i < nx) {
-        y_cid[i] = c[r]; y_slot[i] = f[r][0]; y_arr[i] = f[r][1]; y_tok[i] = f[r][2];
-        y_exec[i] = f[r][3]; y_mt[i] = f[r][4]; y_qt[i] = f[r][5]; y_qfb[i] = f[r][6];
-      }
-    }
-  }
-  if (stamps) { __syncthreads(); dc1 = clock64(); }
-  // previous batch, blocked (preempt keeps previous-batch order): entry j = tid * IP + r
-  uint32_t p_slot[IP], p_arr[IP], p_tok[IP], p_exec[IP], p_mt[IP], p_qt[IP], p_qf[IP];
-  uint64_t p_cid[IP];
-  {
-    const RecSoA& ps = out.ps;
-#pragma unroll
-    for (int r = 0; r < IP; ++r) {
-      const uint32_t j = min(tid * IP + r, BS - 1);
-      p_cid[r] = __ldcg(ps.cid + j);
-      p_slot[r] = __ldcg(ps.slot + j); p_arr[r] = __ldcg(ps.arr + j); p_tok[r] = __ldcg(ps.tok + j);
-      p_exec[r] = __ldcg(ps.exec + j); p_mt[r] = __ldcg(ps.mt + j); p_qt[r] = __ldcg(ps.qt + j);
-      p_qf[r] = __ldcg(ps.qfb + j) & 0xFFu;
-    }
-#pragma unroll
-    for (int r = 0; r < IP; ++r) {
-      const uint32_t j = tid * IP + r;
-      if (j < n_prev) inb[j] = 0;
-      else p_qf[r] = QF_DEAD;
-    }
-  }
-  if (stamps) { __syncthreads(); dc2 = clock64(); }
-  // ---- (2) region B: running calls of q* in the boundary's arrival group, past the boundary ---
-  uint32_t isb = 0, nbm = 0;
-#pragma unroll
-  for (int r = 0; r < IP; ++r) {
-    const bool b = qs < K && !(p_qf[r] & QF_DEAD) && (p_qf[r] & QF_QMASK) == qs && p_arr[r] == bnd_arr &&
-                   p_slot[r] > bnd_slot;
-    isb |= b ? 1u << r : 0u;
-    nbm += b ? 1u : 0u;
-  }
-  uint32_t n_b;
-  uint32_t ob = block_excl_scan<uint32_t, NT>(nbm, red32, &n_b);
-  if (stamps && tid == 0) {
-    dc3 = clock64();
-    ctl->dbg[49] = globaltimer();
-    ctl->dbg[58] = dc1 - dc0;  // clock64 cycles: region A loads
-    ctl->dbg[59] = dc2 - dc1;  // previous-batch loads
-    ctl->dbg[60] = dc3 - dc2;  // region-B count (block scan)
-  }
-#pragma unroll
-  for (int r = 0; r < IP; ++r)
-    if ((isb >> r) & 1u) hb[ob++] = p_slot[r];
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < IP; ++r)
-    if ((isb >> r) & 1u) {
-      uint32_t rank = 0;
-      for (uint32_t k = 0; k < n_b; ++k) rank += hb[k] < p_slot[r] ? 1u : 0u;
-      const uint32_t i = nx + rank;
-      y_cid[i] = p_cid[r];
-      y_slot[i] = p_slot[r];
-      y_arr[i] = p_arr[r];
-      y_tok[i] = p_tok[r];
-      y_exec[i] = p_exec[r];
-      y_mt[i] = p_mt[r];
-      y_qt[i] = p_qt[r];
-      y_qfb[i] = p_qf[r] | ((tid * IP + r) << 8);
-    }
-  const uint32_t n = nx + n_b;
-  __syncthreads();
-  if (stamps && tid == 0) ctl->dbg[45] = globaltimer();
-  // ---- (3) key order: stable partition, running calls first, inside each (queue, arrival) group.
-  // Blocked items (i = tid * I + r).  For item i of the group headed at gs: rb = running items of
-  // the group before i, rt = running items of the whole group (written by its last item).
-  uint32_t gs[I], rex[I], runm = 0, headm = 0, my_runs = 0, my_head = 0;
-#pragma unroll
-  for (int r = 0; r < I; ++r) {
-    const uint32_t i = tid * I + r;
-    if (i < n) {
-      const uint32_t qfb = y_qfb[i];
-      const bool head = i == 0 || ((qfb ^ y_qfb[i - 1]) & QF_QMASK) != 0 || y_arr[i] != y_arr[i - 1];
-      const bool run = (qfb & QF_RUN) != 0;
-      runm |= run ? 1u << r : 0u;
-      headm |= head ? 1u << r : 0u;
-      my_runs += run ? 1u : 0u;
-      if (head) my_head = i;
-    }
-  }
-  const uint32_t rbase = block_excl_scan<uint32_t, NT>(my_runs, red32, nullptr);
-  uint32_t cur_gs = block_excl_max<NT>(my_head, red32), cur_r = rbase;
-#pragma unroll
-  for (int r = 0; r < I; ++r) {
-    const uint32_t i = tid * I + r;
-    if (i < n) {
-      if ((headm >> r) & 1u) {
-        cur_gs = i;
-        hb[i] = cur_r;
-      }
-      gs[r] = cur_gs;
-      rex[r] = cur_r;
-      cur_r += (runm >> r) & 1u;
-      // the group's last item: the running count at its end
-      const bool last = i + 1 == n || ((y_qfb[i + 1] ^ y_qfb[i]) & QF_QMASK) != 0 || y_arr[i + 1] != y_arr[i];
-      if (last) grun[cur_gs] = cur_r;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < I; ++r) {
-    const uint32_t i = tid * I + r;
-    if (i < n) {
-      const uint32_t h0 = hb[gs[r]];
-      const uint32_t rb = rex[r] - h0;
-      const uint32_t pos = (runm >> r) & 1u ? gs[r] + rb : gs[r] + (grun[gs[r]] - h0) + (i - gs[r] - rb);
-      z[pos] = i;
-    }
-  }
-  __syncthreads();
-  if (stamps && tid == 0) ctl->dbg[50] = globaltimer();
-  // ---- (4) cutoff (Alg. 1 l.34-37): kvb >= 1 makes the inclusive prefix strictly increasing,
-  // so "count <= BS and sum kvb <= P" holds exactly on a prefix (n_batch = last fitting + 1) ----
-  const uint32_t nc = min(n, BS);
-  uint32_t kvb[I];
-  unsigned long long my_kv = 0;
-#pragma unroll
-  for (int r = 0; r < I; ++r) {
-    const uint32_t p = tid * I + r;
-    kvb[r] = 0;
-    if (p < nc) {
-      const uint32_t i = z[p];
-      kvb[r] = blocks_for(pol, y_tok[i] + y_exec[i] + 1);  // R14
-      my_kv += kvb[r];
-    }
-  }
+  STAMP(0);
   if (tid == 0) s_nbatch = 0;
-  unsigned long long incl = block_excl_scan<unsigned long long, NT>(my_kv, red64, nullptr);
-  unsigned long long inc[I];
+  // ---- (1) the first m = min(BS, ncand) candidates in key order: key + record, plus the
+  // previous batch's records (preempt), all in one round of independent loads --------------
+  const uint32_t m = lists ? 0u : min(BS, ncand);
+  // R items per thread, blocked (i = tid * R + r): NT * R >= BS
+  uint32_t c_s[R], c_qf[R], c_tok[R], c_ex[R], c_mt[R], c_qt[R], c_kvb[R];
+  uint64_t c_cid[R];
+  uint32_t p_s[R], p_qf[R], p_held[R];  // previous batch: slot, flags, held blocks, order key
+  uint64_t p_cid[R], p_key[R];
+  unsigned long long p_pos[R];           // seqno << 32 | sorted position (k_rank), if use_prev_pos
+  unsigned long long my_kv = 0;
+  {
+    // all loads of this phase first, through restrict-qualified locals, so that they overlap
+    // (one L2 round trip instead of a chain of them)
+    const uint64_t* __restrict__ skey = out.skey;
+    const CandRec* __restrict__ srec = out.srec;
+    const CandRec* __restrict__ prec = out.prev_rec;
+    const unsigned long long* __restrict__ ppos = out.prev_pos;
+    uint64_t kk[R];
+    CandRec rc[R], pr[R];
 #pragma unroll
-  for (int r = 0; r < I; ++r) {
-    const uint32_t p = tid * I + r;
-    incl += kvb[r];
-    inc[r] = incl;
-    if (p < nc && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) atomicMax(&s_nbatch, p + 1);
+    for (int r = 0; r < R; ++r) {
+      // unconditional below BS (buffers hold >= BS entries): the loads do not wait for the counts
+      const uint32_t i = tid * R + r;
+      if (i < BS) {
+        if (!lists) { kk[r] = skey[i]; rc[r] = srec[i]; }
+        pr[r] = prec[i];
+        p_pos[r] = ppos[i];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t i = tid * R + r;
+      if (i < m) {
+        uk[i] = kk[r];
+        c_s[r] = rc[r].slot;
+        c_qf[r] = rc[r].qf;
+        c_tok[r] = rc[r].tok;
+        c_ex[r] = rc[r].exec;
+        c_mt[r] = rc[r].mtime;
+        c_qt[r] = rc[r].quanta;
+        c_cid[r] = rc[r].cid;
+      }
+      if (i < n_prev) {
+        p_s[r] = pr[r].slot;
+        p_qf[r] = pr[r].qf;
+        p_cid[r] = pr[r].cid;
+        p_key[r] = cand_key(pr[r], t);
+        p_held[r] = blocks_for(pol, pr[r].tok + pr[r].exec);  // R28
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    c_kvb[r] = 0;
+    if (tid * R + r < m) {
+      c_kvb[r] = blocks_for(pol, c_tok[r] + c_ex[r] + 1);  // R14
+      my_kv += c_kvb[r];
+    }
+  }
+  STAMP(1);
+  STAMP(2);
+  unsigned long long kv_pre = lists ? 0ull : block_excl_scan<unsigned long long, NT>(my_kv, red64, nullptr);
+  if (lists && tid == 0) s_nbatch = a_nb;
+  // Alg. 1 l.34-37: take while count <= BS and sum kvb <= P; kvb >= 1 makes the prefix sums
+  // strictly increasing, so the fitting items are exactly a prefix: n_batch = max fitting i + 1
+  unsigned long long c_incl[R];  // inclusive kvb prefix at each item
+  {
+    unsigned long long incl = kv_pre;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      uint32_t i = tid * R + r;
+      c_incl[r] = 0;
+      if (i < m) {
+        incl += c_kvb[r];
+        c_incl[r] = incl;
+        if (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget) atomicMax(&s_nbatch, i + 1);
+      }
+    }
   }
   __syncthreads();
   const uint32_t n_batch = s_nbatch;
-  if (tid == 0 && nc > 0 && n_batch == 0) set_err(ctl, AUTX_E_NOMEM, y_slot[z[0]]);
-  if (stamps && tid == 0) ctl->dbg[46] = globaltimer();
-  // ---- (5) admit = batch calls not resident (batch order; blocked for the scan) -----------------
+  STAMP(3);
+  if (tid == 0 && ncand > 0 && n_batch == 0) {
+    if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u)
+      ctl->err_info = (uint32_t)((lists ? out.skey[0] : uk[0]) & 0x7FFFFFFF);
+  }
+  // ---- (4) batch list and admit = batch calls not resident (batch order) -------------------
   unsigned long long my_ad = 0;
   if (n_batch == 0 && tid == 0) s_kvsum = 0;
+  if (lists && tid == 0) s_kvsum = a_kv;
 #pragma unroll
-  for (int r = 0; r < I; ++r) {
-    const uint32_t p = tid * I + r;
-    if (p < n_batch) {
-      const uint32_t i = z[p];
-      if (p + 1 == n_batch) s_kvsum = inc[r];
-      if (!(y_qfb[i] & QF_RES)) {
-        const uint32_t e = y_exec[i];
-        const uint64_t held = e > 0 ? blocks_for(pol, y_tok[i] + e) : 0u;  // R28
+  for (int r = 0; r < R; ++r) {
+    uint32_t i = tid * R + r;
+    if (lists) break;  // (k_rank wrote the lists)
+    if (i + 1 == n_batch) s_kvsum = c_incl[r];  // sum kvb over the batch (read after the scans below)
+    if (i < n_batch) {
+      out.batch_slots[i] = c_s[r];
+      out.batch_ids[i] = c_cid[r];
+      if (!(c_qf[r] & QF_RES)) {
+        uint64_t held = c_ex[r] > 0 ? blocks_for(pol, c_tok[r] + c_ex[r]) : 0;  // R28
         my_ad += (1ull << 44) | held;
       }
     }
   }
-  unsigned long long ad_tot;
-  const unsigned long long ad_pre = block_excl_scan<unsigned long long, NT>(my_ad, red64, &ad_tot);
-  {
+  unsigned long long ad_tot = 0;
+  unsigned long long ad_pre = lists ? 0ull : block_excl_scan<unsigned long long, NT>(my_ad, red64, &ad_tot);
+  if (lists) ad_tot = (unsigned long long)a_na << 44 | a_si;  // (tid 0 only: the host record)
+  if (!lists) {
     uint32_t pos = (uint32_t)(ad_pre >> 44);
 #pragma unroll
-    for (int r = 0; r < I; ++r) {
-      const uint32_t p = tid * I + r;
-      if (p < n_batch) {
-        const uint32_t i = z[p];
-        if (!(y_qfb[i] & QF_RES)) {
-          out.admit_ids[pos] = y_cid[i];
-          out.admit_slots[pos] = y_slot[i];
-          s_ad[pos] = y_cid[i];
-          ++pos;
-        }
+    for (int r = 0; r < R; ++r) {
+      uint32_t i = tid * R + r;
+      if (i < n_batch && !(c_qf[r] & QF_RES)) {
+        out.admit_ids[pos] = c_cid[r];
+        s_ad[pos] = c_cid[r];
+        out.admit_slots[pos] = c_s[r];
+        ++pos;
       }
     }
   }
   const uint32_t n_admit = (uint32_t)(ad_tot >> 44);
   const unsigned long long swap_in = ad_tot & ((1ull << 44) - 1);
-  // batch list (strided: coalesced stores) and the previous batch's membership marks
-#pragma unroll
-  for (int r = 0; r < I; ++r) {
-    const uint32_t p = r * NT + tid;
-    if (p < n_batch) {
-      const uint32_t i = z[p];
-      const uint32_t qfb = y_qfb[i];
-      out.batch_slots[p] = y_slot[i];
-      out.batch_ids[p] = y_cid[i];
-      if (qfb & QF_RUN) inb[qfb >> 8] = 1;
-    }
-  }
-  __syncthreads();
-  if (stamps && tid == 0) ctl->dbg[51] = globaltimer();
-  // ---- (6) preempt = previous batch, still active, not in the batch (previous-batch order) ---
+  STAMP(4);
+  // ---- (5) preempt = previous batch, still active, not in the batch (previous-batch order) ---
   unsigned long long my_pre = 0;
   uint32_t is_pre = 0;
+  {
+    // membership of each previous-batch row in the sorted batch prefix: fixed-length branchless
+    // binary searches, the R of a thread interleaved (independent smem chains)
+    uint32_t pos[R];
 #pragma unroll
-  for (int r = 0; r < IP; ++r) {
-    const uint32_t j = tid * IP + r;
-    if (j < n_prev && !(p_qf[r] & QF_DEAD) && !inb[j]) {
-      is_pre |= 1u << r;
-      my_pre += (1ull << 44) | blocks_for(pol, p_tok[r] + p_exec[r]);  // R28: held = ceil((tok + exec) / bt)
+    for (int r = 0; r < R; ++r) pos[r] = 0;
+    if (out.use_prev_pos) {
+      // k_rank's sorted position of each previous-batch entry that was a candidate (entries that
+      // were not, e.g. of a queue below q*, keep an older seqno and are not in the batch)
+#pragma unroll
+      for (int r = 0; r < R; ++r) pos[r] = (uint32_t)(p_pos[r] >> 32) == seqno ? (uint32_t)p_pos[r] : NONE;
+    } else {
+      for (uint32_t step = 1u << 12; step > 0; step >>= 1) {  // n_batch <= 4096
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const uint32_t probe = pos[r] + step;
+          if (probe <= n_batch && uk[probe - 1] < p_key[r]) pos[r] = probe;  // pos = #keys < key
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) pos[r] = pos[r] < n_batch && uk[pos[r]] == p_key[r] ? pos[r] : NONE;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t i = tid * R + r;
+      if (i < n_prev && !(p_qf[r] & QF_DEAD)) {
+        const bool in = pos[r] < n_batch;
+        if (!in) {
+          is_pre |= 1u << r;
+          my_pre += (1ull << 44) | p_held[r];
+        }
+      }
     }
   }
   unsigned long long pre_tot;
-  const unsigned long long pre_pre = block_excl_scan<unsigned long long, NT>(my_pre, red64, &pre_tot);
+  unsigned long long pre_pre = block_excl_scan<unsigned long long, NT>(my_pre, red64, &pre_tot);
   {
     uint32_t pos = (uint32_t)(pre_pre >> 44);
 #pragma unroll
-    for (int r = 0; r < IP; ++r)
-      if ((is_pre >> r) & 1u) {
+    for (int r = 0; r < R; ++r)
+      if (is_pre & (1u << r)) {
         out.preempt_ids[pos] = p_cid[r];
         s_pr[pos] = p_cid[r];
-        out.preempt_slots[pos] = p_slot[r];
-        ct.qf[p_slot[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
+        out.preempt_slots[pos] = p_s[r];
+        ct.qf[p_s[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
         ++pos;
       }
   }
   const uint32_t n_preempt = (uint32_t)(pre_tot >> 44);
   const unsigned long long swap_out = pre_tot & ((1ull << 44) - 1);
-  if (stamps && tid == 0) ctl->dbg[52] = globaltimer();
-  // ---- (7) KV blocks: swap plan + allocation (a7) ---------------------------------------------
-  if (a.kv_on) {
-    __syncthreads();  // preempt_slots
+  const unsigned long long kv_sum = s_kvsum;
+  STAMP(5);
+  STAMP(6);
+
+  // ---- KV blocks: swap plan + allocation (a7) --------------------------------------------------
+  if (kv_on) {
     const uint32_t W = pol.max_blocks_per_call;
-    // (7a) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots
+    // (1) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots
     uint32_t base_blk = 0, base_free = 0;
     const uint32_t top0 = ctl->free_top, rtop0 = ctl->rs_free_top;
     for (uint32_t c0 = 0; c0 < n_preempt; c0 += NT) {
-      const uint32_t i = c0 + tid;
+      uint32_t i = c0 + tid;
       uint32_t s = 0, rslot = 0, nb = 0;
       if (i < n_preempt) {
         s = out.preempt_slots[i];
@@ -1144,12 +1163,12 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
         nb = kv.rs_nblk[rslot];
       }
       uint32_t tot;
-      uint32_t boff = base_blk + block_excl_scan<uint32_t, NT>(nb, red32, &tot);
+      uint32_t boff = base_blk + block_excl_scan<uint32_t, NT>(nb, red, &tot);
       if (i < n_preempt) {
-        const uint32_t cls = ceil_log2(nb);
+        uint32_t cls = ceil_log2(nb);
         // pop a page range of 2^cls pages from the class stack, else bump-allocate
         uint32_t page;
-        const uint32_t k = atomicSub(&ctl->host_free_top[cls], 1u);
+        uint32_t k = atomicSub(&ctl->host_free_top[cls], 1u);
         if ((int32_t)k > 0) {
           page = kv.host_free[(size_t)cls * kv.host_free_cap + k - 1];
         } else {
@@ -1162,28 +1181,28 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
         kv.plan_out[i] = PlanItem{page, nb, boff};
         const uint32_t* src = kv.rs_blocks + (size_t)rslot * W;
         for (uint32_t j = 0; j < nb; ++j) {
-          const uint32_t b = src[j];
+          uint32_t b = src[j];
           kv.plan_out_blocks[boff + j] = b;
           kv.free_stack[top0 + boff + j] = b;
         }
         kv.rs_nblk[rslot] = 0;
       }
       uint32_t rt;
-      const uint32_t roff = base_free + block_excl_scan<uint32_t, NT>(i < n_preempt ? 1u : 0u, red32, &rt);
+      uint32_t roff = base_free + block_excl_scan<uint32_t, NT>(i < n_preempt ? 1u : 0u, red, &rt);
       if (i < n_preempt) kv.rs_free[rtop0 + roff] = rslot;
       base_blk += tot;
       base_free += rt;
     }
     __syncthreads();
-    const uint32_t top = top0 + base_blk, rtop = rtop0 + base_free;
-    // (7b) batch calls: grow/allocate to kvb; admitted calls take a resident slot
+    uint32_t top = top0 + base_blk, rtop = rtop0 + base_free;
+    // (2) batch calls: grow/allocate to kvb; admitted calls take a resident slot
     uint32_t pop_base = 0, rs_pop = 0, in_blk = 0, in_items = 0;
     for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
-      const uint32_t i = c0 + tid;
+      uint32_t i = c0 + tid;
       uint32_t s = 0, need = 0, have = 0, rslot = NONE, admit = 0, held = 0;
       if (i < n_batch) {
-        s = y_slot[z[i]];
-        const uint32_t qf = ct.qf[s];
+        s = (uint32_t)(uk[i] & 0x7FFFFFFFu);
+        uint32_t qf = ct.qf[s];
         need = ceil_div_u32(ct.tok[s] + ct.exec[s] + 1, pol.block_tokens);
         if (need > W) set_err(ctl, AUTX_E_NOMEM, 2);
         if (qf & QF_RES) {
@@ -1194,12 +1213,12 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
           if (ct.exec[s] > 0) held = ceil_div_u32(ct.tok[s] + ct.exec[s], pol.block_tokens);
         }
       }
-      const uint32_t alloc = need > have ? need - have : 0;
+      uint32_t alloc = need > have ? need - have : 0;
       uint32_t tot, rt, ht, it;
-      const uint32_t aoff = pop_base + block_excl_scan<uint32_t, NT>(alloc, red32, &tot);
-      const uint32_t roff = rs_pop + block_excl_scan<uint32_t, NT>(admit, red32, &rt);
-      const uint32_t hoff = in_blk + block_excl_scan<uint32_t, NT>(held, red32, &ht);
-      const uint32_t ioff = in_items + block_excl_scan<uint32_t, NT>(held ? 1u : 0u, red32, &it);
+      uint32_t aoff = pop_base + block_excl_scan<uint32_t, NT>(alloc, red, &tot);
+      uint32_t roff = rs_pop + block_excl_scan<uint32_t, NT>(admit, red, &rt);
+      uint32_t hoff = in_blk + block_excl_scan<uint32_t, NT>(held, red, &ht);
+      uint32_t ioff = in_items + block_excl_scan<uint32_t, NT>(held ? 1u : 0u, red, &it);
       if (i < n_batch) {
         if (admit) {
           if (roff >= rtop) set_err(ctl, AUTX_E_NOMEM, 3);
@@ -1212,7 +1231,7 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
         kv.rs_nblk[rslot] = need;
         if (held) {
           // swap-in: host copy -> the first `held` blocks of the new list; free host pages after
-          const uint32_t page = ct.loc[s];
+          uint32_t page = ct.loc[s];
           kv.plan_in[ioff] = PlanItem{page, held, hoff};
           for (uint32_t j = 0; j < held; ++j) kv.plan_in_blocks[hoff + j] = dst[j];
         }
@@ -1224,27 +1243,24 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
       in_items += it;
     }
     __syncthreads();
-    // (7c) free the host ranges of swapped-in calls (after this step's swap-out allocations)
+    // (3) free the host ranges of swapped-in calls (after this step's swap-out allocations)
     for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
-      const uint32_t i = c0 + tid;
+      uint32_t i = c0 + tid;
       if (i < in_items) {
-        const PlanItem itm = kv.plan_in[i];
-        const uint32_t cls = ceil_log2(itm.nblk);
-        const uint32_t k = atomicAdd(&ctl->host_free_top[cls], 1u);
-        kv.host_free[(size_t)cls * kv.host_free_cap + k] = (uint32_t)itm.host_page;
+        PlanItem it = kv.plan_in[i];
+        uint32_t cls = ceil_log2(it.nblk);
+        uint32_t k = atomicAdd(&ctl->host_free_top[cls], 1u);
+        kv.host_free[(size_t)cls * kv.host_free_cap + k] = (uint32_t)it.host_page;
       }
     }
-    // (7d) block table CSR of the batch
+    // (4) block table CSR of the batch
     uint32_t b0 = 0;
     for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
-      const uint32_t i = c0 + tid;
+      uint32_t i = c0 + tid;
       uint32_t need = 0, rslot = 0;
-      if (i < n_batch) {
-        rslot = ct.loc[y_slot[z[i]]];
-        need = kv.rs_nblk[rslot];
-      }
+      if (i < n_batch) { rslot = ct.loc[(uint32_t)(uk[i] & 0x7FFFFFFFu)]; need = kv.rs_nblk[rslot]; }
       uint32_t tot;
-      const uint32_t o = b0 + block_excl_scan<uint32_t, NT>(need, red32, &tot);
+      uint32_t o = b0 + block_excl_scan<uint32_t, NT>(need, red, &tot);
       if (i < n_batch) {
         kv.bt_offsets[i] = o;
         const uint32_t* src = kv.rs_blocks + (size_t)rslot * W;
@@ -1263,243 +1279,106 @@ __device__ void finalize_core(const StepArgs& a, unsigned char* dsm, uint32_t qs
     }
     __syncthreads();
   }
-  // ---- (8) step accounting + eager demotion (Alg. 1 l.20-23) for the batch (strided: the
-  // batch is nearly in table order, so neighbouring threads write neighbouring rows) ------------
+
+  STAMP(7);
+  // ---- step accounting + eager demotion (Alg. 1 l.20-23) for the batch, from registers ------
 #pragma unroll
-  for (int r = 0; r < I; ++r) {
-    const uint32_t p = r * NT + tid;
-    if (p < n_batch) {
-      const uint32_t i = z[p];
-      const uint32_t sl = y_slot[i];
-      uint32_t q = y_qfb[i] & QF_QMASK, qt = y_qt[i];
-      ct.exec[sl] = y_exec[i] + 1;
-      ct.mtime[sl] = y_mt[i] + 1;
+  for (int r = 0; r < R; ++r) {
+    uint32_t i = tid * R + r;
+    if (!lists && i < n_batch) {
+      uint32_t sl = c_s[r];
+      uint32_t q = c_qf[r] & QF_QMASK;
+      ct.exec[sl] = c_ex[r] + 1;
+      ct.mtime[sl] = c_mt[r] + 1;
+      uint32_t qt = c_qt[r];
       if (qt != AUTX_INF) {
         qt -= 1;
         if (qt == 0) {
-          q = min(q + 1, K - 1);
+          q = min(q + 1, pol.K - 1);
           qt = pol.quanta[q];
         }
         ct.quanta[sl] = qt;
       }
       ct.qf[sl] = (uint8_t)(q | QF_RUN | QF_RES);
-      ct.bidx[sl] = p;
-      out.prev_slots[p] = sl;
+      ct.bidx[sl] = i;
+      out.prev_slots[i] = sl;
     }
   }
-  if (stamps) {
-    __syncthreads();
-    if (tid == 0) ctl->dbg[53] = globaltimer();
-  }
-  // ---- (9) host record, host mirrors, counters reset for the next step ------------------------
   if (tid == 0) {
     ctl->n_prev = n_batch;
-    ctl->qstar = qs;
-    ctl->mprime = mp;
-    ctl->n_x = nx;
-    ctl->n_b = n_b;
     HostOut h;
     h.n_batch = n_batch;
     h.n_admit = n_admit;
     h.n_preempt = n_preempt;
-    h.n_active = n_live;
+    h.n_active = c_live;
     h.swap_out_blocks = swap_out;
     h.swap_in_blocks = swap_in;
-    h.kv_blocks = n_batch ? s_kvsum : 0ull;
-    h.n_promoted = n_promo;
-    h.err = ctl->err;
-    h.seqno = a.seqno;
-    h.err_info = ctl->err_info;
+    h.kv_blocks = kv_sum;
+    h.n_promoted = c_promo;
+    const bool may_err = kv_on || n_batch == 0;  // the only places this kernel sets an error
+    h.err = may_err ? ctl->err : c_err;
+    h.seqno = seqno;
+    h.err_info = may_err ? ctl->err_info : c_einfo;
     ctl->n_promoted = 0;
     ctl->n_live = 0;
-    ctl->bar1 = 0;
-    ctl->bar2 = 0;
+    ctl->qs_bnd1 = 0;
+    ctl->last_n_b = ctl->n_cand_b;
+    ctl->n_cand_b = 0;
+    if (lists) { ctl->acc_nbatch = 0; ctl->acc_nadmit = 0; ctl->acc_kv = 0; ctl->acc_swap_in = 0; }
     s_hout = h;
   }
   for (uint32_t i = tid; i < QP_LINES * 32; i += NT) (&ctl->qpart[0][0])[i] = 0;
   for (uint32_t i = tid; i < out.n_sup * MAX_K; i += NT) out.sup_cnt[i] = 0;
+  // host-visible results: by default the device block (counts + lists) is copied out by one
+  // cudaMemcpyAsync after the kernel; the zero-copy variant stores the mirrors over PCIe here
   __syncthreads();
   if (!out.zero_copy) {
     if (tid == 0) *out.d_hout = s_hout;
   } else {
-    // 16-B posted stores over PCIe: pairs of batch ids, groups of 4 slots, admit/preempt ids from
-    // their shared-memory copies
-    const uint32_t nb = n_batch;
-    for (uint32_t k = tid; k < (nb + 1) / 2; k += NT) {
-      const uint64_t c0 = y_cid[z[2 * k]], c1 = 2 * k + 1 < nb ? y_cid[z[2 * k + 1]] : 0ull;
-      reinterpret_cast<uint4*>(out.h_batch)[k] = make_uint4((uint32_t)c0, (uint32_t)(c0 >> 32), (uint32_t)c1, (uint32_t)(c1 >> 32));
-    }
-    for (uint32_t k = tid; k < (nb + 3) / 4; k += NT) {
-      uint32_t v[4];
+    const uint32_t nb = s_hout.n_batch, na = s_hout.n_admit, np_ = s_hout.n_preempt;
+    // 16-B posted stores over PCIe: batch ids straight from registers (a thread's R blocked
+    // items are R/2 consecutive words), admit/preempt ids from their shared-memory copies
+    static_assert(R % 2 == 0, "blocked items pair into 16-B words");
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = 4 * k + u < nb ? y_slot[z[4 * k + u]] : 0u;
-      reinterpret_cast<uint4*>(out.h_batch_slots)[k] = make_uint4(v[0], v[1], v[2], v[3]);
+    for (int k = 0; k < R / 2; ++k) {
+      const uint32_t i = tid * (R / 2) + k;
+      if (!lists && i < (nb + 1) / 2)
+        reinterpret_cast<uint4*>(out.h_batch)[i] =
+            make_uint4((uint32_t)c_cid[2 * k], (uint32_t)(c_cid[2 * k] >> 32), (uint32_t)c_cid[2 * k + 1],
+                       (uint32_t)(c_cid[2 * k + 1] >> 32));
+    }
+    // batch slots, R consecutive u32 per thread (8- or 16-byte stores)
+    if (!lists && tid * R < nb) {
+      if constexpr (R == 2) reinterpret_cast<uint2*>(out.h_batch_slots)[tid] = make_uint2(c_s[0], c_s[1]);
+      else if constexpr (R == 4) reinterpret_cast<uint4*>(out.h_batch_slots)[tid] = make_uint4(c_s[0], c_s[1], c_s[2], c_s[3]);
+      else for (int r = 0; r < R; ++r) out.h_batch_slots[tid * R + r] = c_s[r];
     }
     const uint4* sa = reinterpret_cast<const uint4*>(s_ad);
     const uint4* sp = reinterpret_cast<const uint4*>(s_pr);
-    for (uint32_t i = tid; i < (n_admit + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_admit)[i] = sa[i];
-    for (uint32_t i = tid; i < (n_preempt + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_preempt)[i] = sp[i];
+    if (!lists)
+      for (uint32_t i = tid; i < (na + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_admit)[i] = sa[i];
+    for (uint32_t i = tid; i < (np_ + 1) / 2; i += NT) reinterpret_cast<uint4*>(out.h_preempt)[i] = sp[i];
     __syncthreads();
     // the host reads after the stream event that follows this kernel, which orders every store
     if (tid == 0) *out.hout = s_hout;
   }
-  if (stamps && tid == 0) {
-    ctl->dbg[47] = globaltimer();
-    for (int i = 0; i < 24; ++i) {
-      ctl->dbg[64 + i] = ctl->dbg[40 + i];
-      ctl->dbg[40 + i] = 0;
-    }
-    ctl->dbg[88] = ctl->dbg[39];
-    ctl->dbg[89] = ctl->dbg[36];
-    ctl->dbg[90] = ctl->dbg[37];
-    ctl->dbg[91] = ctl->dbg[38];
-    ctl->dbg[92] = ctl->dbg[35];
-    ctl->dbg[39] = ctl->dbg[36] = ctl->dbg[37] = ctl->dbg[38] = ctl->dbg[35] = 0;
-    ctl->dbg[40] = ~0ull;
-  }
+  STAMP(8);
 }
 
-// ---------------------------------------------------------------------------------------------
-// The step kernel (select mode): one cooperative launch per step.
-//   CTAs 0 .. n_tile_ctas-1: the dense pass over their tiles (a3, a4) with per-queue counts;
-//     grid barrier 1; selection and region-A extraction (a5); arrive at barrier 2.
-//   CTA n_tile_ctas: the prologue (a1, a2: completions and arrivals), the "prologue done" flag
-//     the deferred rows wait for; barrier 1; selection; the previous batch's slots; barrier 2;
-//     order, cutoff, lists, accounting, KV plan (a5, a6, a3, a7).
-// Stamps (dbg): 40 first CTA start, 41 last CTA start, 42 prologue done, 43 barrier 1 passed,
-// 44 barrier 2 passed, 45 region B placed, 46 cutoff, 47 end, 48 last tile CTA at barrier 1,
-// 49 finalize loads consumed, 50 key order, 51 batch + admit lists, 52 preempt list,
-// 53 accounting (+ KV plan), 54 / 55 tile 0 selection / extraction done, 56 last tile CTA at
-// barrier 2, 57 prologue completions applied.
-// ---------------------------------------------------------------------------------------------
-template <int I>
-__global__ void __launch_bounds__(ST_THREADS, 2) k_step(const __grid_constant__ StepArgs a) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ SelSmem S;
-  __shared__ unsigned long long red64[33];
-  __shared__ uint32_t red32[33];
-  __shared__ uint32_t wq16[ST_THREADS / 32][MAX_K / 2];
-  __shared__ uint32_t wn[ST_THREADS / 32];
-  const uint32_t tid = threadIdx.x;
-  Ctl* ctl = a.ctl;
-  const bool stamps = STAMPS_ON(a.pol);
-  if (stamps && tid == 0) {
-    const unsigned long long g = globaltimer();
-    atomicMin(&ctl->dbg[40], g);
-    atomicMax(&ctl->dbg[41], g);
-  }
-  if (blockIdx.x == a.n_tile_ctas) {
-    // ---- prologue + finalize CTA ----
-    if (a.pro_first) {
-      // the prologue's rows into L2 ahead of the tiles' stream (it is on the critical path: the
-      // deferred rows wait for it), then let the tiles go
-      const PrologueArgs& p = a.pro;
-      if (tid < p.n_comp && p.n_comp <= PRO_INLINE) {
-        const uint32_t sl = p.comp[tid];
-        prefetch_l2(a.ct.exec + sl); prefetch_l2(a.ct.qf + sl); prefetch_l2(a.ct.prog + sl);
-        prefetch_l2(a.ct.inh + sl); prefetch_l2(a.ct.arr + sl); prefetch_l2(a.ct.bidx + sl);
-        prefetch_l2(a.ct.loc + sl); prefetch_l2(a.pt.info + p.comp_prog[tid]);
-      }
-      if (tid < p.n_arr && p.n_arr <= PRO_INLINE) prefetch_l2(a.pt.info + p.arr[tid].prog);
-      __syncthreads();
-      if (tid == 0) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(&ctl->go_seq), "r"(a.seqno) : "memory");
-    }
-    if (a.do_pro) prologue_body<ST_THREADS>(a, dsm, stamps);
+template <int NT, int R, bool LISTS = false>
+__global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
+                                                 bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(5);
+  finalize_body<NT, R, LISTS>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  if (STAMPS_ON) {
     __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_u32(&ctl->pro_seq, a.seqno);
-      if (stamps) ctl->dbg[42] = globaltimer();
+    if (threadIdx.x == 0) {
+      ctl->dbg[33 + 3 * 5] = globaltimer();
+      for (int i = 0; i < 32; ++i) { ctl->dbg[64 + i] = ctl->dbg[32 + i]; ctl->dbg[32 + i] = 0; }
     }
-    const uint32_t n_prev = ctl->n_prev;
-    grid_arrive(&ctl->bar1);
-    if (a.warm_params) {
-      // the parameter fields the finalize reads, once, so that its phases do not each start with
-      // a constant-cache miss (A/B switch AUTX_WARM_PARAMS)
-      const unsigned char* pa = reinterpret_cast<const unsigned char*>(&a);
-      uint32_t acc = 0;
-      for (uint32_t off = tid * 4; off < (uint32_t)offsetof(StepArgs, pro) + 64; off += ST_THREADS * 4)
-        acc ^= *reinterpret_cast<const uint32_t*>(pa + off);
-      if (acc == 0x9E3779B9u) red32[32] = acc;
-    }
-    grid_wait(&ctl->bar1, gridDim.x);
-    if (stamps && tid == 0) ctl->dbg[43] = globaltimer();
-    select_for(a, NONE, S);
-    const uint32_t qs = S.qs, mp = S.m, nx = S.nx, n_live = S.n_live, n_promo = S.n_promo;
-    finalize_core<I>(a, dsm, qs, mp, nx, n_live, n_promo, n_prev, true, red64, red32);
-    return;
   }
-  // ---- tile CTA ----
-  uint32_t* s_filt = reinterpret_cast<uint32_t*>(dsm);  // 2048-bit filter of completed programs
-  const bool filt_on = !a.defer_all && a.pro.n_comp > 0;
-  if (filt_on) {
-    if (tid < 64) s_filt[tid] = 0;
-    __syncthreads();
-    if (tid < a.pro.n_comp) {
-      const uint32_t p = a.pro.comp_prog[tid];
-      atomicOr(&s_filt[(p >> 5) & 63], 1u << (p & 31));
-    }
-    __syncthreads();
-  }
-  uint32_t qw[2];
-  uint32_t last = NONE;
-  if (a.pro_first) {
-    if (tid == 0) {
-      while (ld_relaxed_u32(&ctl->go_seq) != a.seqno) __nanosleep(20);
-      fence_acq_rel();
-    }
-    __syncthreads();
-  }
-  for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
-    uint64_t hq = 0;
-    uint32_t np = 0, nl = 0;
-    tile_pass(a, tile, s_filt, filt_on, s_filt + 64, qw, hq, np, nl);
-    tile_publish(a, tile, hq, np, nl, wq16, wn);
-    last = tile;
-  }
-  grid_arrive(&ctl->bar1);
-  if (stamps && tid == 0) atomicMax(&ctl->dbg[48], globaltimer());
-  grid_wait(&ctl->bar1, gridDim.x);
-  for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += a.n_tile_ctas) {
-    const long long xc0 = clock64();
-    select_for(a, tile, S);
-    const long long xc1 = clock64();
-    if (stamps && tid == 0 && tile == 0) ctl->dbg[54] = globaltimer();
-    if (tile != last) {
-      // an earlier tile of this CTA: its flags after the pass, from L2
-      const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
-      const uint2 qv = row0 < a.n_rows ? __ldcg(reinterpret_cast<const uint2*>(a.ct.qf + row0))
-                                       : make_uint2(0x40404040u, 0x40404040u);
-      qw[0] = qv.x;
-      qw[1] = qv.y;
-      last = tile;
-    }
-    // rows that ran in the previous step: their records go to prev_rec
-    const bool run = ((qw[0] | qw[1]) & 0x10101010u) != 0;
-    const bool any_run = __syncthreads_or(run);
-    if (any_run || S.has) extract_tile(a, tile, qw, S, red64, S.has != 0, dsm + 1024);
-    __syncthreads();  // S reuse
-    if (stamps && tid == 0) {
-      atomicMax(&ctl->dbg[61], (unsigned long long)(xc1 - xc0));            // selection, cycles
-      atomicMax(&ctl->dbg[62], (unsigned long long)(clock64() - xc1));      // extraction, cycles
-      if (S.has) atomicAdd(&ctl->dbg[63], 1ull);                             // tiles with candidates
-      if (any_run) atomicAdd(&ctl->dbg[39], 1ull);                           // tiles with running rows
-    }
-    if (stamps && tid == 0 && tile == 0) ctl->dbg[55] = globaltimer();
-  }
-  grid_arrive(&ctl->bar2);
-  if (stamps && tid == 0) atomicMax(&ctl->dbg[56], globaltimer());
-}
-
-// Radix mode: the finalize alone (one CTA) on the sorted candidates k_take wrote (q* = K: no
-// region B; the partition leaves an already key-ordered Y unchanged).
-template <int I>
-__global__ void __launch_bounds__(ST_THREADS) k_fin(const __grid_constant__ StepArgs a) {
-  extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ unsigned long long red64[33];
-  __shared__ uint32_t red32[33];
-  Ctl* ctl = a.ctl;
-  finalize_core<I>(a, dsm, a.pol.K, 0u, ctl->n_x, ctl->n_live, ctl->n_promoted, ctl->n_prev, false, red64, red32);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1507,28 +1386,29 @@ __global__ void __launch_bounds__(ST_THREADS) k_fin(const __grid_constant__ Step
 // ---------------------------------------------------------------------------------------------
 cudaError_t launch_complete(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                             const uint32_t* slots, uint32_t n, uint32_t t, KvState kv, bool kv_on,
-                            CompRec* rec_out, bool apply, uint32_t* prev_rec) {
+                            CompRec* rec_out, bool apply) {
   // size the CTA to the record count: a typical step completes ~BS/mean-decode calls
   if (n <= 32)
-    return launch_pdl(k_complete<32>, 1, 32, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, prev_rec);
+    return launch_pdl(k_complete<32>, 1, 32, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
   else if (n <= 256)
-    return launch_pdl(k_complete<256>, 1, 256, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, prev_rec);
-  return launch_pdl(k_complete<1024>, 1, 1024, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply, prev_rec);
+    return launch_pdl(k_complete<256>, 1, 256, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+  else
+    return launch_pdl(k_complete<FIN_THREADS>, 1, FIN_THREADS, 0, s, pol, ct, pt, ctl, slots, n, t, kv, kv_on, rec_out, apply);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,
                          uint64_t stride, uint32_t G, uint32_t t) {
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_apply<<<1, 1024, 0, s>>>(pol, pt, (const char*)base, stride, G, t);
+  k_apply<<<1, FIN_THREADS, 0, s>>>(pol, pt, (const char*)base, stride, G, t);
   return cudaGetLastError();
 }
 
 cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,
                          const RouteArr* arr, uint32_t n, int8_t* pin, uint32_t threshold,
                          int32_t* out) {
-  if (!n) return cudaSuccess;
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_route<<<1, 32, 0, s>>>((const char*)base, stride, G, arr, n, pin, threshold, out);
+  if (n) k_route<<<1, 32, 0, s>>>((const char*)base, stride, G, arr, n, pin, threshold, out);
   return cudaGetLastError();
 }
 
@@ -1537,90 +1417,80 @@ cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, Pro
                             const uint32_t* par) {
   if (n == 0) return cudaSuccess;
   return launch_pdl(k_register, (n + 255) / 256, 256, 0, s, pol, ct, pt, recs, n, first_slot, t, par);
-}
-
-// Candidates per finalize thread for a batch size (C = ST_THREADS * I >= 2 BS).
-static int fin_items(uint32_t bs) { return bs <= 512 ? 2 : bs <= 1024 ? 4 : 8; }
-
-template <int I>
-static cudaError_t setup_one(int* occ) {
-  const size_t sm = fin_smem_bytes<I>();
-  cudaError_t e = cudaFuncSetAttribute(k_step<I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_fin<I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_step<I>, ST_THREADS, sm);
-}
-
-// Called by autx_create with the context's device current (the attributes are per device).
-cudaError_t step_kernel_setup(uint32_t max_batch, uint32_t* capacity_out) {
-  int dev = 0, sms = 0, occ = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return e;
-  const int I = fin_items(max_batch);
-  e = I == 2 ? setup_one<2>(&occ) : I == 4 ? setup_one<4>(&occ) : setup_one<8>(&occ);
-  if (e != cudaSuccess) return e;
-  if (occ < 1) return cudaErrorInvalidConfiguration;
-  *capacity_out = (uint32_t)(occ * sms);
-  return cudaSuccess;
-}
-
-cudaError_t launch_prologue(cudaStream_t s, const StepArgs& a) {
-  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_prologue<<<1, ST_THREADS, PRO_INLINE * (4 + sizeof(ArrivalRec) + sizeof(CompRec)), s>>>(a);
   return cudaGetLastError();
 }
 
-template <int I>
-static cudaError_t launch_step_kernel(cudaStream_t s, const StepArgs& a, uint32_t grid) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(ST_THREADS);
-  cfg.dynamicSmemBytes = fin_smem_bytes<I>();
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;  // CTAs wait for each other: all must be resident
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  return cudaLaunchKernelEx(&cfg, k_step<I>, a);
+static uint32_t pow2_at_least(uint32_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
 }
 
-template <int I>
-static cudaError_t launch_fin_kernel(cudaStream_t s, const StepArgs& a) {
-  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_fin<I><<<1, ST_THREADS, fin_smem_bytes<I>(), s>>>(a);
-  return cudaGetLastError();
+// Dynamic shared memory above 48 KB is a per-device function attribute: set for the current device
+// (autx_create calls this after cudaSetDevice, once per context).
+cudaError_t step_kernels_setup() {
+  const int big = 200 * 1024;
+  cudaError_t e = cudaFuncSetAttribute(k_finalize<FIN_THREADS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_finalize<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_finalize<512, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  return e;
 }
 
-cudaError_t launch_step(cudaStream_t s, StepArgs& a, uint32_t capacity, cudaEvent_t* ev, const RadixState* rx,
-                        uint32_t arr_base, uint32_t* radix_passes) {
-  a.ntiles = std::max<uint32_t>(1, (a.n_rows + TILE - 1) / TILE);
-  a.out.n_sup = (a.ntiles + SUP_TILES - 1) / SUP_TILES;
-  a.n_tile_ctas = std::min<uint32_t>(a.ntiles, capacity - 1);
-  const int I = fin_items(a.pol.max_batch);
+// The step's chain on stream s, PDL-linked: [prologue (launched by the caller)] -> k_scan_tile ->
+// k_gather_ss -> k_rank -> k_finalize; radix mode replaces scan + gather by the sort.
+cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                        Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
+                        uint32_t seqno, cudaEvent_t* ev, const RadixState* rx, uint32_t arr_base,
+                        uint32_t* radix_passes, uint32_t first_new) {
+  uint32_t ntiles = (n_rows + TILE - 1) / TILE;
+  if (ntiles == 0) ntiles = 1;
+  out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
+  out.use_prev_pos = rx ? 0u : 1u;  // k_rank publishes previous-batch positions (select mode)
+  static const bool rank_narrow = getenv("AUTX_RANK_NARROW") != nullptr;
+  out.rank_wide = rank_narrow ? 0u : 1u;  // k_rank may use a warp per key when candidates are few
   if (ev) cudaEventRecord(ev[0], s);
-  cudaError_t e;
   if (rx) {
-    if (a.do_pro) {
-      e = launch_prologue(s, a);
-      if (e != cudaSuccess) return e;
-    }
-    static int sms = 0;
-    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    e = launch_radix_order(s, a.pol, a.ct, a.pt, a.ctl, a.out, *rx, a.t, a.n_rows, arr_base, sms, radix_passes);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pol.device);
+    cudaError_t e = launch_radix_order(s, pol, ct, pt, ctl, out, *rx, t, n_rows, arr_base, sms, radix_passes);
     if (e != cudaSuccess) return e;
-    e = I == 2 ? launch_fin_kernel<2>(s, a) : I == 4 ? launch_fin_kernel<4>(s, a) : launch_fin_kernel<8>(s, a);
+    if (ev) cudaEventRecord(ev[1], s);
   } else {
-    const uint32_t grid = a.n_tile_ctas + 1;
-    e = I == 2 ? launch_step_kernel<2>(s, a, grid) : I == 4 ? launch_step_kernel<4>(s, a, grid)
-                                                          : launch_step_kernel<8>(s, a, grid);
+    // prog + L2 prefetches while the prologue runs (AUTX_SCAN_PRE, default 1: measured ~0.4 us)
+    static const uint32_t pre = getenv("AUTX_SCAN_PRE") ? (uint32_t)atoi(getenv("AUTX_SCAN_PRE")) : 1u;
+    launch_pdl(k_scan_tile, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, first_new, pre);
+    if (ev) cudaEventRecord(ev[1], s);
+    const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
+    launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t);
   }
-  if (e != cudaSuccess) return e;
-  if (ev) cudaEventRecord(ev[1], s);
+  uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
+  // sorted keys [np] + admit and preempt id staging [2 x even(BS)]
+  const size_t fin_smem_bytes = ((size_t)np + 2 * ((pol.max_batch + 1) & ~1u)) * sizeof(uint64_t);
+  // k_rank also decides the batch (lists, accounting) when there is no KV allocator and its keys
+  // + kvb fit shared memory; else the finalize does (AUTX_FINALIZE_LISTS forces the latter)
+  static const bool fin_lists = getenv("AUTX_FINALIZE_LISTS") != nullptr;
+  out.rank_lists = (!kv_on && !rx && pol.max_batch <= 1024 && !fin_lists) ? 1u : 0u;
+  // k_rank's layout: rk, ck (u64) and ci, rkv, ckv (u32) per key, 2 BS keys (rkv / ckv are
+  // written even when rank_lists is off)
+  size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch * (2 * sizeof(uint64_t) + 3 * sizeof(uint32_t)),
+                                      fin_smem_bytes);
+  // at most one rank CTA per SM: the CTAs are dispatched while the previous kernel still holds
+  // most SMs, and two packed on one SM halve each other's issue rate (measured: the count loop
+  // ran 2x slower behind the self-selecting gather's grid)
+  rank_smem = std::max<size_t>(rank_smem, 120 * 1024);
+  const uint32_t rank_grid = (2 * pol.max_batch + RANK_PER_CTA - 1) / RANK_PER_CTA;
+  if (ev) cudaEventRecord(ev[2], s);
+  launch_pdl(k_rank, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  // 512 threads x 2 candidates: 4 warps per scheduler to hide the phase's latency chains (1024
+  // threads hit the 64-register cap and spill); BS > 1024 takes 1024 threads x 4
+  if (pol.max_batch <= 1024)
+    launch_pdl(out.rank_lists ? k_finalize<512, 2, true> : k_finalize<512, 2>, 1, 512, fin_smem_bytes, s, pol, ct,
+               ctl, out, kv, kv_on, t, np, seqno);
+  else
+    launch_pdl(k_finalize<FIN_THREADS, 4>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np,
+               seqno);
+  if (ev) cudaEventRecord(ev[3], s);
   return cudaGetLastError();
 }
 

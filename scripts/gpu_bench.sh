@@ -21,7 +21,7 @@ r = d.get("roofline", {})
 print(n, "value %.3e" % d["value"], "ms/step %.2f us" % (d["ms_per_step"] * 1e3), "frac", r.get("frac"),
       "e2e %.3e" % d["e2e"]["value"], "e2e us %.1f" % (d["e2e"]["ms_per_step"] * 1e3), "launches/step", d.get("kernels_per_step"))
 print("  step_ms", d.get("step_ms"))
-print("  phases", d.get("phases_us"))
+print("  chain", d.get("chain_us"), "kern_ev", d.get("kernel_event_ms"))
 print("  state", d.get("state"))
 print("  api", d["e2e"].get("api_us_per_step"), "clocks", d.get("clocks"))
 PY

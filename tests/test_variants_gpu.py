@@ -12,9 +12,12 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 VARIANTS = {
-    "dma_out": {"AUTX_DMA_OUT": "1"},      # host lists by one copy instead of zero-copy stores
-    "defer_all": {"AUTX_DEFER_ALL": "1"},  # every row of the dense pass waits for the prologue
-    "pro_first": {"AUTX_PRO_FIRST": "1"},  # the tiles stream only once the prologue's loads are issued
+    "dma_out": {"AUTX_DMA_OUT": "1"},            # host lists by one copy instead of zero-copy stores
+    "scan_pre0": {"AUTX_SCAN_PRE": "0"},         # scan reads nothing before the PDL wait
+    "scan_pre2": {"AUTX_SCAN_PRE": "2"},         # ... prog, base, mtime before the wait
+    "no_graph": {"AUTX_NO_GRAPH": "1"},          # the step's kernels as separate launches, not a graph replay
+    "finalize_lists": {"AUTX_FINALIZE_LISTS": "1"},  # finalize cuts the batch and writes the lists (not k_rank)
+    "rank_narrow": {"AUTX_RANK_NARROW": "1"},    # half a warp per key in k_rank whatever the candidate count
 }
 
 SUBSET = "fig2 or atlas_dag or mcts or chatbot or compaction or react or (random_tiny and 7)"
