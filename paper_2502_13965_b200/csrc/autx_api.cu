@@ -119,6 +119,8 @@ struct autx_ctx {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t x = nullptr;
     std::vector<cudaGraphNode_t> nodes;
+    std::vector<std::vector<unsigned char>> blobs;  // parameters last set on each node
+    std::vector<dim3> grids;
   };
   std::vector<StepGraph> graphs;
   cudaStream_t cap_stream = nullptr;  // capture only (the legacy stream cannot be captured)
@@ -511,8 +513,10 @@ static autx_status compact(autx_ctx* ctx);
 // Launches the staged completions and arrivals of step t: one prologue kernel whose inputs ride
 // in the kernel parameters when small; bulk arrivals (an offline burst) go through one DMA and
 // the multi-CTA registration kernel.
-static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
-  if (ctx->n_comp_staged == 0 && ctx->n_arr_staged == 0) return AUTX_OK;
+// always: launch the prologue even without records (sched_step: it also hands the step's scalars
+// to the rest of the chain).
+static autx_status flush_staged(autx_ctx* ctx, uint32_t t, bool always = false) {
+  if (ctx->n_comp_staged == 0 && ctx->n_arr_staged == 0 && !always) return AUTX_OK;
   const bool bulk = ctx->n_arr_staged > 4096;
   PrologueArgs a;
   memset(&a, 0, offsetof(PrologueArgs, comp));
@@ -521,6 +525,8 @@ static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
   a.first_slot = ctx->arr_first_slot;
   a.t = t;
   a.n_prog_rows = ctx->prog_next;
+  a.n_rows = ctx->tail;
+  a.seqno = ctx->seqno;
   if (a.n_comp <= (uint32_t)PRO_INLINE) memcpy(a.comp, ctx->h_cslots, a.n_comp * sizeof(uint32_t));
   else a.comp_ptr = ctx->h_cslots;
   if (a.n_arr <= (uint32_t)PRO_INLINE) memcpy(a.arr, ctx->h_arr, a.n_arr * sizeof(ArrivalRec));
@@ -529,8 +535,7 @@ static autx_status flush_staged(autx_ctx* ctx, uint32_t t) {
   a.par = ctx->h_par;
   CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
   if (ctx->timing) cudaEventRecord(ctx->ev[4], ctx->stream);
-  if (a.n_comp || a.n_arr)
-    CK(launch_prologue(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->kv, ctx->kv_on, recs, a));
+  CK(launch_prologue(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->kv, ctx->kv_on, recs, a));
   if (ctx->timing) {
     cudaEventRecord(ctx->ev[5], ctx->stream);
     ctx->timed_complete = true;
@@ -744,6 +749,11 @@ static autx_status step_graph_run(autx_ctx* ctx, std::vector<LaunchRec>& recs) {
   }
   if (sg) {
     for (size_t i = 0; i < recs.size(); ++i) {
+      // only nodes whose parameters or grid changed: the chain reads the step's scalars from
+      // the control block, so a typical step re-parameterises the prologue alone
+      const dim3& g = recs[i].grid;
+      if (sg->blobs[i] == recs[i].blob && sg->grids[i].x == g.x && sg->grids[i].y == g.y && sg->grids[i].z == g.z)
+        continue;
       std::vector<void*> ptrs = recs[i].ptrs();
       cudaKernelNodeParams kp = {};
       kp.func = const_cast<void*>(recs[i].func);
@@ -752,6 +762,8 @@ static autx_status step_graph_run(autx_ctx* ctx, std::vector<LaunchRec>& recs) {
       kp.sharedMemBytes = (unsigned)recs[i].smem;
       kp.kernelParams = ptrs.data();
       CK(cudaGraphExecKernelNodeSetParams(sg->x, sg->nodes[i], &kp));
+      sg->blobs[i] = recs[i].blob;
+      sg->grids[i] = g;
     }
   } else {
     if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
@@ -785,6 +797,8 @@ static autx_status step_graph_run(autx_ctx* ctx, std::vector<LaunchRec>& recs) {
       g.funcs.push_back(r.func);
       g.blocks.push_back(r.block);
       g.smem.push_back(r.smem);
+      g.blobs.push_back(r.blob);
+      g.grids.push_back(r.grid);
     }
     cudaGraph_t graph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(ctx->cap_stream, &graph);
@@ -819,20 +833,18 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   while (ctx->low < ctx->tail && !ctx->slot_live[ctx->low]) ++ctx->low;
   const uint32_t arr_base = ctx->low < ctx->tail ? ctx->slot_arr[ctx->low] : t;
   if (t - arr_base >= (1u << 27)) return fail(ctx, AUTX_E_NOMEM, "arrival span exceeds the 27-bit key field");
-  // rows registered in this step start here (the scan reads older rows before the prologue ends)
-  const uint32_t first_new = ctx->n_arr_staged ? ctx->arr_first_slot : ctx->tail;
   // the step's kernels as one graph replay (AUTX_NO_GRAPH: separate launches); not with the
   // per-kernel timing events, the radix pipeline (host-synchronised passes) or a bulk burst (DMA)
   static const bool no_graph = getenv("AUTX_NO_GRAPH") != nullptr;
   std::vector<LaunchRec> recs;
   const bool graph = !no_graph && !ctx->timing && !ctx->radix && ctx->n_arr_staged <= 4096;
   if (graph) g_launch_rec = &recs;
-  s = flush_staged(ctx, t);
-  if (s) { g_launch_rec = nullptr; return s; }
   ++ctx->seqno;
+  s = flush_staged(ctx, t, true);  // the prologue, always: it hands t, n_rows, seqno to the chain
+  if (s) { g_launch_rec = nullptr; return s; }
   const cudaError_t le = launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv,
                                      ctx->kv_on, t, ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr,
-                                     ctx->radix ? &ctx->rx : nullptr, arr_base, &ctx->radix_passes, first_new);
+                                     ctx->radix ? &ctx->rx : nullptr, arr_base, &ctx->radix_passes);
   g_launch_rec = nullptr;
   CK(le);
   if (graph) {
@@ -944,6 +956,8 @@ static autx_status compact(autx_ctx* ctx) {
   // dropped entries shift the previous-batch indices the running rows carry
   if (npv) CK(launch_set_bidx(ctx->stream, ctx->ct, ctx->out.prev_slots, npv));
   CK(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->ctl) + offsetof(Ctl, n_prev), &npv, 4, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->ctl) + offsetof(Ctl, s_tail_prev), &n, 4, cudaMemcpyHostToDevice,
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));  // lv, old2new, np, npv go out of scope
   for (auto& kv : ctx->call_slot) kv.second = old2new[kv.second];

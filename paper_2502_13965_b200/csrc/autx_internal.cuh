@@ -111,6 +111,11 @@ struct Ctl {
   // anti-starvation, [MAX_K] promotions, [MAX_K + 1] live rows.  Reset by finalize.
   uint32_t qs_bnd1;
   uint32_t last_n_b;   // region B size of the last step (autx_step_stats; n_cand_b is reset by finalize)
+  // this step's scalars, written by the prologue from its parameters, read by the rest of the
+  // chain after its PDL wait: a graph replay then only re-parameterises the prologue node
+  uint32_t s_t, s_n_rows, s_seqno;
+  uint32_t s_tail_prev;  // rows older than this step's arrivals (finalize / compaction): the scan
+                         // may read them before its PDL wait
   alignas(128) uint32_t qpart[QP_LINES][32];
   unsigned long long dbg[96];  // [32, 64) live chain stamps, [64, 96) last step's (AUTX_CHAIN_STAMPS)  // %globaltimer stamps of kernel phases (autx_phase_times)
 };
@@ -203,7 +208,6 @@ struct Outputs {
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* sup_cnt;         // [ceil(ntiles_cap / SUP_TILES) * MAX_K] per-queue counts of super-tiles
                              // (scan: atomics; gather: prefix; finalize: reset)
-  uint32_t n_sup;            // super-tiles in use this step (set per launch; finalize resets them)
   HostOut* hout;             // host-visible counts (pinned)
   HostOut* d_hout;           // device copy of the counts (copied out with the lists by one DMA)
   int zero_copy;             // 1: finalize stores the host mirrors itself over PCIe (A/B switch)
@@ -313,7 +317,7 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
 constexpr int PRO_INLINE = 96;
 struct PrologueArgs {
   uint32_t n_comp, n_arr, first_slot, t;
-  uint32_t n_prog_rows, _pad[3];  // process-table rows in use
+  uint32_t n_prog_rows, n_rows, seqno, _pad;  // process-table rows in use; table rows and step seqno
   const uint32_t* comp_ptr;
   const ArrivalRec* arr_ptr;
   const uint32_t* comp_lin;  // AUTX_ATLAS_EQ2: lineage index of each completion (mapped pinned)
@@ -344,7 +348,7 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev /* 4 events or null */,
                         const RadixState* rx /* non-null: AUTX_ORDER_RADIX */, uint32_t arr_base,
-                        uint32_t* radix_passes, uint32_t first_new /* first row registered this step */);
+                        uint32_t* radix_passes);
 cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                Outputs out, RadixState rx, uint32_t t, uint32_t n_rows,
                                uint32_t arr_base, int sms, uint32_t* passes_out);

@@ -281,6 +281,11 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
   pdl_wait();
   pdl_trigger();
   CHAIN_BEGIN(0);
+  if (tid == 0) {  // the step's scalars for the rest of the chain (read after their PDL wait)
+    ctl->s_t = a.t;
+    ctl->s_n_rows = a.n_rows;
+    ctl->s_seqno = a.seqno;
+  }
   __syncthreads();
   if (comp_inline && arr_inline) {
     // typical step: arrivals inherit the service after this step's completions (R10) computed
@@ -482,10 +487,10 @@ __device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs
 // program entries and of the previous batch's records (the gather's cold reads); 2: prog, base
 // and mtime early + the same prefetches.
 __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                               Outputs out, uint32_t t, uint32_t n_rows,
-                                                               uint32_t first_new, uint32_t pre) {
+                                                               Outputs out, uint32_t pre) {
   const uint32_t tid = threadIdx.x, tile = blockIdx.x;
   const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  const uint32_t first_new = ctl->s_tail_prev;  // written before this step's chain
   const bool early = pre != 0 && row0 + ROWS_PER_THREAD <= first_new;
   uint4 p0, p1, b0, b1, m0, m1;
   if (early) {
@@ -517,6 +522,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallT
   pdl_wait();
   pdl_trigger();
   CHAIN_BEGIN(1);
+  const uint32_t t = ctl->s_t, n_rows = ctl->s_n_rows;
   uint64_t hq = 0;
   uint32_t npromo = 0, nlive = 0;
   if (row0 < n_rows) {
@@ -759,10 +765,11 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
   }
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS, 4) k_gather_ss(Policy pol, CallTable ct, Ctl* ctl, Outputs out,
-                                                               uint32_t n_rows, uint32_t ntiles, uint32_t t) {
+__global__ void __launch_bounds__(SCAN_THREADS, 4) k_gather_ss(Policy pol, CallTable ct, Ctl* ctl, Outputs out) {
   pdl_wait();
   pdl_trigger();
+  const uint32_t t = ctl->s_t, n_rows = ctl->s_n_rows;
+  const uint32_t ntiles = n_rows ? (n_rows + TILE - 1) / TILE : 1u;
   CHAIN_BEGIN(3);
   gather_ss_body(pol, ct, ctl, out, n_rows, ntiles, t);
   CHAIN_END(3);
@@ -790,9 +797,10 @@ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 
 // the number of keys before it (the keys are unique), RANK_SUB threads per key.
 constexpr int RANK_THREADS = 256, RANK_SUB = 16, RANK_PER_CTA = RANK_THREADS / RANK_SUB;
 __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
-                                                       bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
+                                                       bool kv_on, uint32_t np) {
   pdl_wait();
   pdl_trigger();
+  const uint32_t t = ctl->s_t, seqno = ctl->s_seqno;
   CHAIN_BEGIN(4);
   __shared__ uint32_t red_r[33];
   const uint32_t na = ctl->n_cand_a;
@@ -1328,7 +1336,11 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     s_hout = h;
   }
   for (uint32_t i = tid; i < QP_LINES * 32; i += NT) (&ctl->qpart[0][0])[i] = 0;
-  for (uint32_t i = tid; i < out.n_sup * MAX_K; i += NT) out.sup_cnt[i] = 0;
+  {
+    const uint32_t n_rows = ctl->s_n_rows, ntiles = n_rows ? (n_rows + TILE - 1) / TILE : 1u;
+    for (uint32_t i = tid; i < (ntiles + SUP_TILES - 1) / SUP_TILES * MAX_K; i += NT) out.sup_cnt[i] = 0;
+    if (tid == 0) ctl->s_tail_prev = n_rows;  // the next step's scan may read these rows early
+  }
   // host-visible results: by default the device block (counts + lists) is copied out by one
   // cudaMemcpyAsync after the kernel; the zero-copy variant stores the mirrors over PCIe here
   __syncthreads();
@@ -1367,9 +1379,10 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
 
 template <int NT, int R, bool LISTS = false>
 __global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
-                                                 bool kv_on, uint32_t t, uint32_t np, uint32_t seqno) {
+                                                 bool kv_on, uint32_t np) {
   pdl_wait();
   pdl_trigger();
+  const uint32_t t = ctl->s_t, seqno = ctl->s_seqno;
   CHAIN_BEGIN(5);
   finalize_body<NT, R, LISTS>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
   if (STAMPS_ON) {
@@ -1442,10 +1455,9 @@ cudaError_t step_kernels_setup() {
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev, const RadixState* rx, uint32_t arr_base,
-                        uint32_t* radix_passes, uint32_t first_new) {
+                        uint32_t* radix_passes) {
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
-  out.n_sup = (ntiles + SUP_TILES - 1) / SUP_TILES;
   out.use_prev_pos = rx ? 0u : 1u;  // k_rank publishes previous-batch positions (select mode)
   static const bool rank_narrow = getenv("AUTX_RANK_NARROW") != nullptr;
   out.rank_wide = rank_narrow ? 0u : 1u;  // k_rank may use a warp per key when candidates are few
@@ -1459,10 +1471,10 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   } else {
     // prog + L2 prefetches while the prologue runs (AUTX_SCAN_PRE, default 1: measured ~0.4 us)
     static const uint32_t pre = getenv("AUTX_SCAN_PRE") ? (uint32_t)atoi(getenv("AUTX_SCAN_PRE")) : 1u;
-    launch_pdl(k_scan_tile, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, t, n_rows, first_new, pre);
+    launch_pdl(k_scan_tile, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, pre);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
-    launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out, n_rows, ntiles, t);
+    launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out);
   }
   uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
   // sorted keys [np] + admit and preempt id staging [2 x even(BS)]
@@ -1481,15 +1493,14 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   rank_smem = std::max<size_t>(rank_smem, 120 * 1024);
   const uint32_t rank_grid = (2 * pol.max_batch + RANK_PER_CTA - 1) / RANK_PER_CTA;
   if (ev) cudaEventRecord(ev[2], s);
-  launch_pdl(k_rank, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  launch_pdl(k_rank, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, np);
   // 512 threads x 2 candidates: 4 warps per scheduler to hide the phase's latency chains (1024
   // threads hit the 64-register cap and spill); BS > 1024 takes 1024 threads x 4
   if (pol.max_batch <= 1024)
     launch_pdl(out.rank_lists ? k_finalize<512, 2, true> : k_finalize<512, 2>, 1, 512, fin_smem_bytes, s, pol, ct,
-               ctl, out, kv, kv_on, t, np, seqno);
+               ctl, out, kv, kv_on, np);
   else
-    launch_pdl(k_finalize<FIN_THREADS, 4>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, t, np,
-               seqno);
+    launch_pdl(k_finalize<FIN_THREADS, 4>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, np);
   if (ev) cudaEventRecord(ev[3], s);
   return cudaGetLastError();
 }
