@@ -3,6 +3,7 @@
 // this file only validates, maps 64-bit ids to table rows, stages records in pinned memory
 // and launches.
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstddef>
 #include <cstdio>
@@ -128,6 +129,22 @@ struct autx_ctx {
   bool tc_step = false, tr_step = false;                  // ... for the step being waited on
   std::string err;
 };
+
+// AUTX_HOST_PROFILE=1: host time per section of autx_sched_step, printed by autx_destroy.
+struct HostProf {
+  const bool on = getenv("AUTX_HOST_PROFILE") != nullptr;
+  double acc[8] = {};
+  uint64_t n = 0;
+  std::chrono::steady_clock::time_point t0;
+  void start() { if (on) t0 = std::chrono::steady_clock::now(); }
+  void lap(int i) {
+    if (!on) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    acc[i] += std::chrono::duration<double, std::micro>(t1 - t0).count();
+    t0 = t1;
+  }
+};
+static HostProf g_hp;
 
 static autx_status fail(autx_ctx* c, autx_status s, const char* fmt, ...) {
   char buf[512];
@@ -360,6 +377,10 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
 
 extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   if (!ctx) return AUTX_E_INVAL;
+  if (g_hp.on && g_hp.n)
+    fprintf(stderr, "autx host us/step over %llu sched_steps: checks %.2f prologue %.2f record %.2f graph %.2f tail %.2f\n",
+            (unsigned long long)g_hp.n, g_hp.acc[0] / g_hp.n, g_hp.acc[1] / g_hp.n, g_hp.acc[2] / g_hp.n,
+            g_hp.acc[3] / g_hp.n, g_hp.acc[4] / g_hp.n);
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   CallTable& t = ctx->ct;
@@ -553,7 +574,10 @@ static autx_status flush_staged(autx_ctx* ctx, uint32_t t, bool always = false) 
   }
   ctx->n_comp_staged = ctx->n_arr_staged = 0;
   ctx->n_par_staged = 0;
-  ctx->staged_new_progs.clear();
+  // (clear() on an unordered_set memsets every bucket: after a burst of new programs that is
+  // ~30k buckets per step, so an empty set is left alone and a big one is released)
+  if (ctx->staged_new_progs.size() > 4096) std::unordered_set<uint64_t>().swap(ctx->staged_new_progs);
+  else if (!ctx->staged_new_progs.empty()) ctx->staged_new_progs.clear();
   return AUTX_OK;
 }
 
@@ -817,6 +841,7 @@ static autx_status step_graph_run(autx_ctx* ctx, std::vector<LaunchRec>& recs) {
 
 extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out* out) {
   if (!ctx || !out) return AUTX_E_INVAL;
+  g_hp.start();
   autx_status s = sync_last(ctx);
   if (s) return s;
   if (ctx->stepped && t <= ctx->t_last) return fail(ctx, AUTX_E_STATE, "step %u <= last step %u", t, ctx->t_last);
@@ -840,17 +865,21 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   const bool graph = !no_graph && !ctx->timing && !ctx->radix && ctx->n_arr_staged <= 4096;
   if (graph) g_launch_rec = &recs;
   ++ctx->seqno;
+  g_hp.lap(0);
   s = flush_staged(ctx, t, true);  // the prologue, always: it hands t, n_rows, seqno to the chain
   if (s) { g_launch_rec = nullptr; return s; }
+  g_hp.lap(1);
   const cudaError_t le = launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv,
                                      ctx->kv_on, t, ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr,
                                      ctx->radix ? &ctx->rx : nullptr, arr_base, &ctx->radix_passes);
   g_launch_rec = nullptr;
   CK(le);
+  g_hp.lap(2);
   if (graph) {
     s = step_graph_run(ctx, recs);
     if (s) return s;
   }
+  g_hp.lap(3);
   if (!ctx->out.zero_copy)
     CK(cudaMemcpyAsync(ctx->h_outblk, ctx->d_outblk, ctx->outblk_bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->done, ctx->stream));
@@ -875,6 +904,8 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   out->h_admit = ctx->out.h_admit;
   out->h_preempt = ctx->out.h_preempt;
   out->done = (void*)ctx->done;
+  g_hp.lap(4);
+  ++g_hp.n;
   return AUTX_OK;
 }
 

@@ -271,6 +271,7 @@ struct LaunchRec {
   std::vector<size_t> off;
   template <typename T>
   void push(const T& v) {
+    if (blob.capacity() < 8192) blob.reserve(8192);  // one allocation per record
     const size_t o = (blob.size() + 15) & ~size_t(15);
     blob.resize(o + sizeof(T));
     memcpy(blob.data() + o, &v, sizeof(T));
