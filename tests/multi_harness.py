@@ -96,11 +96,9 @@ def run_rank(rank, world, port, out_path, use_gpu, trace_name, seed, cfg_kw):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from autx_workload import random_tiny, chatbot, mcts_mapreduce
     from oracle.autellix import Config
     from paper_2502_13965_b200.multi import MultiEngineDriver
-    tr = {"tiny": lambda: random_tiny(seed, max_programs=6), "chatbot": lambda: chatbot(60),
-          "mcts": lambda: mcts_mapreduce(8)}[trace_name]()
+    tr = make_trace(trace_name, seed)
     cfg = Config(**cfg_kw)
     if use_gpu:
         from paper_2502_13965_b200 import Scheduler
@@ -162,11 +160,31 @@ def run_world(tmp_path, use_gpu, trace_name, seed, cfg_kw, world=2):
     return [pickle.load(open(o, "rb")) for o in outs]
 
 
-def oracle_multi(trace_name, seed, cfg_kw, world=2):
+def make_trace(trace_name, seed):
+    """The multi-engine tests' traces; "golden_route": tests/golden/route_2engine.json."""
     from autx_workload import random_tiny, chatbot, mcts_mapreduce
+    if trace_name == "golden_route":
+        from test_oracle_route_golden import golden_trace_and_config
+        return golden_trace_and_config()[1]
+    return {"tiny": lambda: random_tiny(seed, max_programs=6), "chatbot": lambda: chatbot(60),
+            "mcts": lambda: mcts_mapreduce(8)}[trace_name]()
+
+
+def golden_route():
+    """(config kwargs, expected routes, expected per-engine records) of the golden trace."""
+    import json
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "route_2engine.json")))
+    c = g["config"]
+    cfg = dict(policy=c["policy"], K=c["K"], q_hi=tuple(c["q_hi"]), quanta=tuple(c["quanta"]), beta=tuple(c["beta"]),
+               max_batch=c["max_batch"], token_threshold=c["token_threshold"])
+    routes = [(t, list(cids), list(dest)) for t, cids, dest in g["routes"]]
+    logs = [[(t, b, a, p) for t, b, a, p in eng] for eng in g["batches"]]
+    return cfg, routes, logs
+
+
+def oracle_multi(trace_name, seed, cfg_kw, world=2):
     from oracle.autellix import Config, simulate_multi
-    tr = {"tiny": lambda: random_tiny(seed, max_programs=6), "chatbot": lambda: chatbot(60),
-          "mcts": lambda: mcts_mapreduce(8)}[trace_name]()
+    tr = make_trace(trace_name, seed)
     logs, routes = simulate_multi(tr, Config(**cfg_kw), world)
     out = [[(r["t"], r["batch"], r["admit"], r["preempt"]) for r in lg if r["batch"] or r["preempt"]]
            for lg in logs]

@@ -20,3 +20,14 @@ def test_gloo_world2_matches_oracle_lockstep(tmp_path, seed, ci):
         assert res[r]["log"] == want[r]
         got_routes = [x for x in res[r]["routes"] if x[1]]
         assert got_routes == [x for x in routes if x[1]]
+
+
+def test_gloo_world2_golden_route(tmp_path):
+    """The hand-derived two-engine trace (tests/golden/route_2engine.json) through the driver's
+    host protocol: routes and per-engine decisions equal the golden, not only the oracle."""
+    from multi_harness import golden_route
+    cfg, routes, logs = golden_route()
+    res = run_world(tmp_path, False, "golden_route", 0, cfg)
+    for r in range(2):
+        assert res[r]["log"] == logs[r]
+        assert [x for x in res[r]["routes"] if x[1]] == routes

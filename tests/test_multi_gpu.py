@@ -24,3 +24,14 @@ def test_two_engines_match_oracle(tmp_path, trace, seed, ci):
     for r in range(2):
         assert res[r]["log"] == want[r], f"engine {r}"
         assert [x for x in res[r]["routes"] if x[1]] == [x for x in routes if x[1]]
+
+
+def test_two_engines_golden_route(tmp_path):
+    """Two CUDA engines on the hand-derived trace (tests/golden/route_2engine.json): Alg. 2
+    routes (load after completions, first-long-call pin) and decisions equal the golden."""
+    from multi_harness import golden_route
+    cfg, routes, logs = golden_route()
+    res = run_world(tmp_path, True, "golden_route", 0, cfg)
+    for r in range(2):
+        assert res[r]["log"] == logs[r], f"engine {r}"
+        assert [x for x in res[r]["routes"] if x[1]] == routes
