@@ -479,3 +479,73 @@ def test_full_size_chatbot_react_first_steps(workload):
         assert rec["n_active"] == rec_o["n_active"]
         assert (rec["batch"], rec["admit"], rec["preempt"]) == (rec_o["batch"], rec_o["admit"], rec_o["preempt"]), t
     s.close()
+
+
+def oracle_from_snapshot(s, tr, cfg, d):
+    """The oracle's engine state rebuilt from a GPU snapshot (SURVEY §8(d) timing protocol step
+    1): every active call's state from autx_dump_calls (table order = registration order), the
+    process table of every live program from autx_program_state, the previous batch in order."""
+    from oracle.autellix import Call
+    st = s.dump_calls()
+    eng = Engine(cfg, check_formulations=False)
+    for i, r in enumerate(st):
+        cid = int(r["call_id"])
+        p = cid >> 16
+        qt = int(r["quanta"])
+        tok, ex = int(r["input_tokens"]), int(r["exec"])
+        eng.calls[cid] = Call(cid=cid, pid=int(tr.prog_id[p]), arr=int(r["arrival_step"]),
+                              parr=int(tr.prog_arrival[p]), seq=i, input_tokens=tok, inh=int(r["inh"]),
+                              q=int(r["q"]), quanta=None if qt == 0xFFFFFFFF else qt, wait=int(r["wait"]),
+                              mtime=int(r["mtime"]), exec=ex, totwait=int(r["totwait"]),
+                              running=bool(r["flags"] & 1), resident=bool(r["flags"] & 2),
+                              held=-(-(tok + ex) // cfg.block_tokens) if ex else 0)
+    eng.next_seq = len(st)
+    for p in np.nonzero(d.calls_left > 0)[0]:
+        pid = int(tr.prog_id[p])
+        svc, pw = s.program_state(pid)
+        eng.table.svc[pid], eng.table.pwait[pid] = svc, pw
+        eng.table.last_arrival[pid], eng.table.last_completion[pid] = 0, None
+    eng.prev_batch = list(d.log[-1]["batch"])
+    return eng
+
+
+@pytest.mark.parametrize("policy", [ATLAS, PLAS])
+def test_full_size_1m_snapshot_after_10k_steps(policy):
+    """BASELINE configs[3] at full size in the bench's state: the GPU runs the 1M-call burst for
+    10,000 steps (the bench's fast-forward), the oracle is rebuilt from the GPU's snapshot, and
+    the two then run 10 steps side by side with the same completions and arrivals: lists equal
+    every step, and the full per-call state and the touched programs' table rows equal at the
+    end (the transition function at full scale)."""
+    from autx_workload import burst_mcts_mapreduce, BASE_SEED, CONFIG_INDEX
+    from paper_2502_13965_b200 import TraceDriver
+    tr = burst_mcts_mapreduce(1_000_000, seed=BASE_SEED + CONFIG_INDEX["mcts"])
+    cfg = spec_ladder_config(policy, max_batch=1024, kv_budget=32768)
+    s = make_sched(spec_ladder_config(policy, max_batch=1024, kv_budget=32768),
+                   max_calls=1_300_000, max_programs=tr.n_programs + 1024)
+    d = TraceDriver(tr, s, log_lists=False)
+    for _ in range(10_000):
+        d.step()
+    d.log_lists = True  # the previous batch, in order, for the snapshot
+    d.step()
+    eng = oracle_from_snapshot(s, tr, cfg, d)
+    assert len(eng.calls) > 800_000
+    touched = set()
+    for _ in range(10):
+        t = d.t
+        cids = [int(x) for x in tr.call_id[d.pending]]
+        touched.update(int(tr.prog_id[int(c) >> 16]) for c in cids)
+        left = d.calls_left.copy()
+        rec = d.step()
+        arr = [(int(tr.call_id[c]), int(tr.prog_id[tr.call_prog[c]]), t, int(tr.prog_arrival[tr.call_prog[c]]),
+                int(tr.input_tokens[c])) for c in d.arr_idx]
+        rec_o = eng.step(t, cids, arr)
+        for p in np.nonzero((left > 0) & (d.calls_left == 0))[0]:
+            eng.end_program(int(tr.prog_id[p]))
+        assert rec["n_active"] == rec_o["n_active"]
+        assert (rec["batch"], rec["admit"], rec["preempt"]) == (rec_o["batch"], rec_o["admit"], rec_o["preempt"]), t
+    got = [tuple(int(x) for x in r) for r in s.dump_calls()]
+    assert got == normalize_oracle_state(eng, cfg)
+    for pid in sorted(touched):
+        if pid in eng.table.svc:
+            assert s.program_state(pid) == (eng.table.svc[pid], eng.table.pwait[pid]), pid
+    s.close()
