@@ -278,6 +278,12 @@ def host_link_peak(torch, nbytes=1 << 30):
 
 
 def bench_swap(torch, args, link):
+    """Row a7 on the ReAct-shaped config with 8B-geometry pools, three modes.  Every run also
+    checks the swapped bytes (SURVEY §8(d) "pattern round trip on every benchmark run"): the
+    "engine" fills each newly allocated block of a call with a pattern of (call, block, layer,
+    K|V) in every layer, and every block a call gets back after a swap-out / swap-in round trip
+    (possibly another GPU block id) must hold its pattern, in all 32 layers x K|V.  The checks
+    run outside the timed kv_swap calls."""
     from autx_workload import react, BASE_SEED, CONFIG_INDEX
     from paper_2502_13965_b200 import Scheduler, TraceDriver, SWAP_SM, SWAP_STAGED_DMA, SWAP_PER_CHUNK_MEMCPY
     L, chunk = 32, 32 << 10                 # LLaMA-3.1-8B: 32 layers x 8 KV heads x 128 x bf16 x 16 tok
@@ -288,20 +294,26 @@ def bench_swap(torch, args, link):
     host = torch.empty(host_pages * page, dtype=torch.uint8).pin_memory()
     lad = spec_ladder()
     results = {}
+
+    def pat(cids, js, l, kv):  # one byte per (call, block, layer, K|V), the whole chunk
+        return ((cids * 31 + js * 7 + l * 3 + kv) & 0xFF).to(torch.uint8)
+
     for name, mode in (("sm", SWAP_SM), ("staged_dma", SWAP_STAGED_DMA), ("per_chunk_memcpy", SWAP_PER_CHUNK_MEMCPY)):
         tr = react(1000, seed=BASE_SEED + CONFIG_INDEX["react"])
         s = Scheduler(policy="plas", beta=(2, 1), max_batch=64, kv_budget=P, block_tokens=16,
                       max_calls=1 << 16, max_programs=1 << 14, n_gpu_blocks=P, max_blocks_per_call=P,
                       host_pages=host_pages, **lad)
-        d = TraceDriver(tr, s, log_lists=False)
+        d = TraceDriver(tr, s, log_lists=True)
         tot_b = tot_ms = 0.0
         b_d2h = b_h2d = 0
         n = 0
         t_at_peak = 0.0
+        written = {}          # call id -> leading blocks the engine has written
+        checked = mismatched = 0
         for i in range(args.swap_steps + 20):
             if not d.skip_idle():
                 break
-            d.step()
+            rec = d.step()
             st = s.kv_swap([x.data_ptr() for x in kp], [x.data_ptr() for x in vp], chunk,
                            host.data_ptr(), host.numel(), mode)
             if i >= 20 and (st.bytes_d2h + st.bytes_h2d) > 0:
@@ -311,11 +323,42 @@ def bench_swap(torch, args, link):
                 b_h2d += st.bytes_h2d
                 t_at_peak += st.bytes_d2h / (link["d2h"] * 1e9) + st.bytes_h2d / (link["h2d"] * 1e9)
                 n += 1
+            # content check of the blocks that came back, then the engine's writes to new blocks
+            offs, blks = s.block_table_host()
+            ci, cj, cb, ni, nj, nb = [], [], [], [], [], []
+            for k, cid in enumerate(rec["batch"]):
+                mine = blks[offs[k]:offs[k + 1]]
+                w = written.get(cid, 0)
+                for j in range(len(mine)):
+                    (ci if j < w else ni).append(cid)
+                    (cj if j < w else nj).append(j)
+                    (cb if j < w else nb).append(int(mine[j]))
+                written[cid] = len(mine)
+            admitted = set(rec["admit"])
+            keep = [k for k in range(len(ci)) if ci[k] in admitted]  # only round trips need checking
+            if keep:
+                cids = torch.tensor([ci[k] for k in keep], device="cuda", dtype=torch.int64)
+                js = torch.tensor([cj[k] for k in keep], device="cuda", dtype=torch.int64)
+                idx = torch.tensor([cb[k] for k in keep], device="cuda", dtype=torch.int64)
+                for l in range(L):
+                    for kv, pools in ((0, kp), (1, vp)):
+                        ok = (pools[l][idx] == pat(cids, js, l, kv)[:, None]).all(dim=1)
+                        mismatched += int((~ok).sum())
+                checked += len(keep) * L * 2
+            if ni:
+                cids = torch.tensor(ni, device="cuda", dtype=torch.int64)
+                js = torch.tensor(nj, device="cuda", dtype=torch.int64)
+                idx = torch.tensor(nb, device="cuda", dtype=torch.int64)
+                for l in range(L):
+                    for kv, pools in ((0, kp), (1, vp)):
+                        pools[l][idx] = pat(cids, js, l, kv)[:, None].expand(-1, chunk)
         s.close()
         if n:
             gbs = tot_b / (tot_ms * 1e-3) / 1e9
             results[name] = {"GB/s": round(gbs, 2), "steps": n, "bytes_d2h": b_d2h, "bytes_h2d": b_h2d,
-                             "ms_per_step": tot_ms / n, "frac_of_host_link": round(t_at_peak / (tot_ms * 1e-3), 4)}
+                             "ms_per_step": tot_ms / n, "frac_of_host_link": round(t_at_peak / (tot_ms * 1e-3), 4),
+                             "content_check": {"chunks_checked": checked, "chunks_mismatched": mismatched,
+                                               "ok": checked > 0 and mismatched == 0}}
     del kp, vp, host
     return results
 
