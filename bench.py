@@ -300,9 +300,11 @@ def bench_swap(torch, args, link):
 
     for name, mode in (("sm", SWAP_SM), ("staged_dma", SWAP_STAGED_DMA), ("per_chunk_memcpy", SWAP_PER_CHUNK_MEMCPY)):
         tr = react(1000, seed=BASE_SEED + CONFIG_INDEX["react"])
+        # the library and the engine's reads / writes of the pools on one stream (autx.h: all
+        # device work is ordered on the context's stream)
         s = Scheduler(policy="plas", beta=(2, 1), max_batch=64, kv_budget=P, block_tokens=16,
                       max_calls=1 << 16, max_programs=1 << 14, n_gpu_blocks=P, max_blocks_per_call=P,
-                      host_pages=host_pages, **lad)
+                      host_pages=host_pages, stream=torch.cuda.current_stream().cuda_stream, **lad)
         d = TraceDriver(tr, s, log_lists=True)
         tot_b = tot_ms = 0.0
         b_d2h = b_h2d = 0
