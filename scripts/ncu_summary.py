@@ -2,7 +2,8 @@
 """Summarise ncu output for profiles/: a launch list CSV (--metrics gpu__time_duration.sum) and
 optionally a `--set full` report, into markdown.
 
-usage: python scripts/ncu_summary.py launches.csv [prof.ncu-rep] > profiles/<name>.md
+usage: python scripts/ncu_summary.py launches.csv [prof.ncu-rep] [--traffic=profiles/step_traffic.json]
+       > profiles/<name>.md
 """
 import collections
 import csv
@@ -17,7 +18,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__grid_size", "launch__block_size"]
 
 
-def launches(path):
+def launches(path, traffic_out=None):
+    """Launch list with gpu__time_duration.sum (and optionally dram__bytes_read/write.sum) per
+    launch; traffic_out: write the per-step DRAM bytes of the chain (sum over its kernels, mean
+    over the listed steps) as JSON for bench.py's roofline.traffic."""
     rows = list(csv.reader(open(path)))
     hdr, data = None, []
     for r in rows:
@@ -26,19 +30,37 @@ def launches(path):
             continue
         if hdr and len(r) == len(hdr):
             data.append(dict(zip(hdr, r)))
-    by = collections.OrderedDict()
+    per = collections.OrderedDict()  # (launch id, kernel) -> {metric: value}
     for d in data:
-        by.setdefault(d["Kernel Name"].split("(")[0].split("<")[0], []).append(float(d["Metric Value"]))
-    unit = data[0]["Metric Unit"] if data else "ns"
+        k = (d["ID"], d["Kernel Name"].split("(")[0].split("<")[0])
+        per.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+    by = collections.OrderedDict()
+    for (_, name), m in per.items():
+        by.setdefault(name, []).append(m)
     print(f"## Launch list ({path.split('/')[-1]}: cold-cache, serialised; compare shares)\n")
-    print("| kernel | launches | mean | median | share of listed time |")
-    print("|---|---|---|---|---|")
-    total = sum(sum(v) for v in by.values()) or 1
-    for k, v in sorted(by.items(), key=lambda kv: -sum(kv[1])):
-        sv = sorted(v)
-        print(f"| {k} | {len(v)} | {sum(v)/len(v)/1e3:.2f} us | {sv[len(sv)//2]/1e3:.2f} us | "
-              f"{100*sum(v)/total:.1f}% |" if unit == "ns" else f"| {k} | {len(v)} | {sum(v)/len(v)} {unit} | | |")
+    print("| kernel | launches | mean time | median time | share of listed time | DRAM read / launch | DRAM write / launch |")
+    print("|---|---|---|---|---|---|---|")
+    tkey = "gpu__time_duration.sum"
+    total = sum(sum(x.get(tkey, 0) for x in v) for v in by.values()) or 1
+    for k, v in sorted(by.items(), key=lambda kv: -sum(x.get(tkey, 0) for x in kv[1])):
+        ts = sorted(x.get(tkey, 0) for x in v)
+        rd = sum(x.get("dram__bytes_read.sum", 0) for x in v) / len(v)
+        wr = sum(x.get("dram__bytes_write.sum", 0) for x in v) / len(v)
+        print(f"| {k} | {len(v)} | {sum(ts)/len(ts)/1e3:.2f} us | {ts[len(ts)//2]/1e3:.2f} us | "
+              f"{100*sum(ts)/total:.1f}% | {rd/1e6:.3f} MB | {wr/1e6:.3f} MB |")
     print()
+    if traffic_out:
+        import json
+        steps = min(len(v) for v in by.values())
+        b = sum(sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in v) / len(v)
+                for v in by.values())
+        json.dump({"dram_bytes_per_launch": int(b), "steps": steps,
+                   "per_kernel_bytes": {k: int(sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0)
+                                                   for x in v) / len(v)) for k, v in by.items()},
+                   "source": f"ncu launch list {path.split('/')[-1]}: dram__bytes_read.sum + dram__bytes_write.sum "
+                             "of the five chain kernels of one step (mean over the listed steps; ncu replays each "
+                             "kernel cold, so this is an upper bound of one step's DRAM traffic)"},
+                  open(traffic_out, "w"), indent=1)
 
 
 def full(path):
@@ -72,6 +94,11 @@ def full(path):
 
 
 if __name__ == "__main__":
-    launches(sys.argv[1])
-    if len(sys.argv) > 2:
-        full(sys.argv[2])
+    traffic = None
+    args = [a for a in sys.argv[1:] if not a.startswith("--traffic=")]
+    for a in sys.argv[1:]:
+        if a.startswith("--traffic="):
+            traffic = a.split("=", 1)[1]
+    launches(args[0], traffic)
+    if len(args) > 1:
+        full(args[1])
