@@ -438,6 +438,8 @@ def main():
     gate_cycles = 2_000_000                   # ~1 ms spin while the host enqueues the step
 
     def timed_step():
+        if world == 1:
+            d.prepare()                       # the workload model's host work, not the library's
         if not args.no_flush:
             flush.zero_()
         torch.cuda._sleep(gate_cycles)

@@ -90,15 +90,24 @@ class TraceDriver:
         pos = np.repeat(tr.par_ptr[idx] - off[:-1], cnt) + np.arange(int(off[-1]))
         return off.astype(np.uint32), tr.call_id[tr.par[pos]]
 
-    def issue(self):
-        """Host half of one engine step: completions, session ends, arrivals, sched_step.
-        Returns (n_completions, n_arrivals) without waiting for the device."""
+    def prepare(self):
+        """Workload side of the next step (no ABI call): the completed calls' ids, the programs
+        they end, this step's arrivals.  Kept apart so a benchmark can do it before timing."""
         t = self.t
-        s = self.s
-        nc = len(self.pending)
         ids = self.tr.call_id[self.pending]
         ended = self._release(t, self.pending)
         arr = self.arrivals(t)
+        self._prepared = (t, ids, ended, arr)
+
+    def issue(self):
+        """Host half of one engine step: completions, session ends, arrivals, sched_step.
+        Returns (n_completions, n_arrivals) without waiting for the device."""
+        if getattr(self, "_prepared", None) is None or self._prepared[0] != self.t:
+            self.prepare()
+        t, ids, ended, arr = self._prepared
+        self._prepared = None
+        s = self.s
+        nc = len(ids)
         pc = time.perf_counter
         t0 = pc()
         if nc:
