@@ -549,3 +549,18 @@ def test_full_size_1m_snapshot_after_10k_steps(policy):
         if pid in eng.table.svc:
             assert s.program_state(pid) == (eng.table.svc[pid], eng.table.pwait[pid]), pid
     s.close()
+
+
+def test_program_latency_of_gpu_schedules():
+    """SURVEY §8(f) item 4 on the CUDA path's decisions: the program-level token latency
+     and its tail computed from the GPU decision log equal the oracle's."""
+    from oracle.metrics import program_latency, latency_summary
+    from paper_2502_13965_b200 import TraceDriver
+    tr = chatbot(300)
+    cfg = spec_ladder_config(PLAS, max_batch=32, kv_budget=2400)
+    olog, _ = simulate(tr, cfg, check_formulations=False)
+    s = make_sched(spec_ladder_config(PLAS, max_batch=32, kv_budget=2400))
+    glog = TraceDriver(tr, s).run()
+    s.close()
+    assert program_latency(tr, glog) == program_latency(tr, olog)
+    assert latency_summary(program_latency(tr, glog))["p99"] > 0
