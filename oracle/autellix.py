@@ -381,6 +381,52 @@ def route(arrivals, loads, pins, threshold=2048):
     return out
 
 
+def route_least_used(arrivals, loads):
+    """The Least Used comparator of §6.4: every call to the engine with the fewest LLM
+    calls in the system (ties -> lowest id), no pinning; loads +1 per assignment (R23)."""
+    out = []
+    for _ in arrivals:
+        e = min(range(len(loads)), key=lambda i: (loads[i], i))
+        loads[e] += 1
+        out.append(e)
+    return out
+
+
+def route_round_robin(arrivals, n_engines, state):
+    """The Round Robin comparator of §6.4: engines in cyclic order, one per call in
+    canonical order; state = {"next": engine of the next call} persists across steps."""
+    out = []
+    for _ in arrivals:
+        out.append(state["next"])
+        state["next"] = (state["next"] + 1) % n_engines
+    return out
+
+
+ROUTERS = ("locality", "least_used", "round_robin")
+
+
+class PrefixCache:
+    """The program-prefix KV cache of the router's locality argument (§4.3; SPEC
+    S:L183-191, reading R34): engine e holds, per program, the longest context (input + decoded
+    tokens) of the program's calls it has served; a new call of the program there reuses at most
+    its inherited context (its input tokens minus its own new prompt).  Prefill work = input
+    tokens - reused tokens (a relative cost: the idealized engine's steps do not depend on it)."""
+
+    def __init__(self, n_engines):
+        self.ctx = [dict() for _ in range(n_engines)]
+        self.prefill = 0
+        self.hits = []   # (input tokens, reused tokens) per call
+
+    def admit(self, e, pid, input_tokens, own_prefill):
+        reused = min(self.ctx[e].get(pid, 0), input_tokens - own_prefill)
+        self.prefill += input_tokens - reused
+        self.hits.append((input_tokens, reused))
+        return reused
+
+    def done(self, e, pid, input_tokens, decode):
+        self.ctx[e][pid] = max(self.ctx[e].get(pid, 0), input_tokens + decode)
+
+
 # ---------------------------------------------------------------------------------
 # Discrete-event harness: DAG readiness, hidden decode lengths, program end.
 # ---------------------------------------------------------------------------------
@@ -504,15 +550,18 @@ def gantt_strings(trace, gantt):
 # ---------------------------------------------------------------------------------
 # Multi-engine lockstep with a replicated process table (reading R22)
 # ---------------------------------------------------------------------------------
-def simulate_multi(trace, cfg: Config, n_engines: int, max_steps=1_000_000):
+def simulate_multi(trace, cfg: Config, n_engines: int, max_steps=1_000_000, router="locality", cache=None):
     """G engines step together.  Per step: local completions -> all completion
-    records applied to the (replicated) table -> loads -> Alg. 2 routing of the
-    step's arrivals in canonical order -> each engine schedules."""
+    records applied to the (replicated) table -> loads -> routing of the step's arrivals
+    in canonical order (Alg. 2, or a §6.4 comparator) -> each engine schedules.
+    cache: a PrefixCache that records each routed call's prefix reuse."""
     assert cfg.policy != ATLAS_EQ2, "Eq. 2 mode is single-engine (parents may run on other engines)"
+    assert router in ROUTERS
     table = ProgramTable()
     engines = [Engine(cfg, table=table, check_formulations=False) for _ in range(n_engines)]
     wl = Workload(trace)
     pins = {}
+    rr = {"next": 0}
     logs = [[] for _ in range(n_engines)]
     routes = []
     completed = [[] for _ in range(n_engines)]
@@ -525,13 +574,26 @@ def simulate_multi(trace, cfg: Config, n_engines: int, max_steps=1_000_000):
             cids = [int(trace.call_id[c]) for c in completed[e]]
             recs.extend(eng.complete(t, cids))
             all_done.extend(completed[e])
+            if cache is not None:
+                for c in completed[e]:
+                    cache.done(e, int(trace.prog_id[trace.call_prog[c]]), int(trace.input_tokens[c]),
+                               int(trace.decode[c]))
         for pid, ex, inh, tw in recs:
             table.apply_completion(cfg.policy, pid, ex, inh, tw, t)
         ended = wl.release(t, sorted(all_done))
         arr = wl.arrivals(t)
         loads = [eng.load() for eng in engines]
-        dest = route([(a[0], a[1], a[4]) for a in arr], loads, pins, cfg.token_threshold)
+        if router == "locality":
+            dest = route([(a[0], a[1], a[4]) for a in arr], loads, pins, cfg.token_threshold)
+        elif router == "least_used":
+            dest = route_least_used(arr, loads)
+        else:
+            dest = route_round_robin(arr, n_engines, rr)
         routes.append((t, [a[0] for a in arr], dest))
+        if cache is not None:
+            for a, e in zip(arr, dest):
+                c = wl.index[a[0]]
+                cache.admit(e, a[1], a[4], int(trace.prefill[c]))
         for e, eng in enumerate(engines):
             eng.register(t, [a for a, d in zip(arr, dest) if d == e])
         for e, eng in enumerate(engines):
