@@ -57,6 +57,16 @@ typedef enum { AUTX_ORDER_SELECT = 0, AUTX_ORDER_RADIX = 1 } autx_order_mode;
 
 #define AUTX_INF 0xFFFFFFFFu /* infinite quantum / budget */
 
+/* Multi-engine routing (a8, f3).  LOCALITY is Alg. 2; the other two are the
+ * comparators of §6.4: LEAST_USED sends every call to the engine with the fewest
+ * calls in the system (ties -> lowest id, no pinning); ROUND_ROBIN cycles through the engines in
+ * canonical arrival order, the cursor persisting across steps (replicated on every rank). */
+typedef enum {
+  AUTX_ROUTE_LOCALITY = 0,
+  AUTX_ROUTE_LEAST_USED = 1,
+  AUTX_ROUTE_ROUND_ROBIN = 2
+} autx_route_policy;
+
 typedef struct {
   int32_t policy;            /* autx_policy                                                         */
   uint32_t K;                /* number of queues, 1..16                                     */
@@ -80,6 +90,8 @@ typedef struct {
                                 torch.cuda.current_stream().cuda_stream); NULL = the legacy default
                                 stream                                                               */
   int32_t rank, nranks;      /* engine id and engine count (routing)                                 */
+  uint32_t route_policy;     /* autx_route_policy: how autx_route_apply places arrivals  */
+  uint32_t _reserved;        /* must be 0                                                            */
 } autx_config;
 
 /* One arriving LLM call (Alg. 1 l.9).  Arrays of these must be in canonical order

@@ -15,6 +15,7 @@ FCFS, MLFQ, PLAS, ATLAS = 0, 1, 2, 3
 ATLAS_EQ2 = 4
 POLICY = {"fcfs": FCFS, "mlfq": MLFQ, "plas": PLAS, "atlas": ATLAS, "atlas_eq2": ATLAS_EQ2}
 ORDER_SELECT, ORDER_RADIX = 0, 1
+ROUTE = {"locality": 0, "least_used": 1, "round_robin": 2}   # autx_route_policy
 SWAP_SM, SWAP_PER_CHUNK_MEMCPY, SWAP_STAGED_DMA = 0, 1, 2
 INF = 0xFFFFFFFF
 STATUS = {0: "OK", 1: "E_INVAL", 2: "E_NOENT", 3: "E_EXIST", 4: "E_NOMEM", 5: "E_STATE",
@@ -36,7 +37,7 @@ class Config(C.Structure):
                 ("order_mode", C.c_uint32), ("n_gpu_blocks", C.c_uint32),
                 ("max_blocks_per_call", C.c_uint32), ("host_pages", C.c_uint64),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
-                ("nranks", C.c_int32)]
+                ("nranks", C.c_int32), ("route_policy", C.c_uint32), ("_reserved", C.c_uint32)]
 
 
 class StepOut(C.Structure):
@@ -148,7 +149,8 @@ class Scheduler:
     def __init__(self, policy="plas", K=1, q_hi=(), quanta=(None,), beta=(1, 0), max_batch=2,
                  kv_budget=None, block_tokens=16, max_calls=1 << 16, max_programs=1 << 16,
                  token_threshold=2048, order_mode=ORDER_SELECT, n_gpu_blocks=0,
-                 max_blocks_per_call=0, host_pages=0, device=0, stream=None, rank=0, nranks=1):
+                 max_blocks_per_call=0, host_pages=0, device=0, stream=None, rank=0, nranks=1,
+                 route_policy="locality"):
         self.lib = load_library()
         cfg = Config()
         cfg.policy = POLICY[policy] if isinstance(policy, str) else int(policy)
@@ -171,6 +173,7 @@ class Scheduler:
         cfg.device = device
         cfg.stream = stream
         cfg.rank, cfg.nranks = rank, nranks
+        cfg.route_policy = ROUTE[route_policy] if isinstance(route_policy, str) else int(route_policy)
         self.cfg = cfg
         self.eq2 = cfg.policy == ATLAS_EQ2
         self.ctx = C.c_void_p()

@@ -91,6 +91,7 @@ struct autx_ctx {
   char* d_route_local = nullptr;   // RouteHdr + max_batch CompRec: this step's completion records
   RouteHdr* h_hdr = nullptr;       // pinned staging for the header
   int8_t* d_pin = nullptr;         // [max_programs] Alg. 2 pin table (-1 = none)
+  uint32_t* d_rr = nullptr;        // Round Robin cursor (replicated: every rank routes the same batch)
   RouteArr* h_rarr = nullptr;
   RouteArr* d_rarr = nullptr;
   int32_t* d_rout = nullptr;
@@ -241,6 +242,8 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(cudaHostAlloc((void**)&ctx->h_hdr, sizeof(RouteHdr), 0));
   CK(dalloc(&ctx->d_pin, P));
   CK(cudaMemsetAsync(ctx->d_pin, 0xff, P, ctx->stream));
+  CK(dalloc(&ctx->d_rr, 1));
+  CK(cudaMemsetAsync(ctx->d_rr, 0, 4, ctx->stream));
   ctx->prog_active.assign(P, 0);
   ctx->slot_prog.assign(rows, 0);
   ctx->slot_arr.assign(rows, 0);
@@ -310,6 +313,8 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
   };
   if (c.policy < AUTX_FCFS || c.policy > AUTX_ATLAS_EQ2) return bad("policy");
   if (c.policy == AUTX_ATLAS_EQ2 && c.nranks > 1) return bad("AUTX_ATLAS_EQ2 is single-engine (nranks must be 1)");
+  if (c.route_policy > AUTX_ROUTE_ROUND_ROBIN) return bad("route_policy");
+  if (c._reserved) return bad("_reserved must be 0");
   if (c.K < 1 || c.K > 16) return bad("K must be 1..16");
   for (uint32_t i = 0; i + 1 < c.K; ++i) {
     if (i > 0 && c.q_hi[i] < c.q_hi[i - 1]) return bad("q_hi must be ascending");
@@ -391,7 +396,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
                  ctx->kv.bt_offsets, ctx->kv.bt_blocks, ctx->d_pools, ctx->staging,
-                 ctx->d_route_local, ctx->d_pin, ctx->d_rarr, ctx->d_rout,
+                 ctx->d_route_local, ctx->d_pin, ctx->d_rr, ctx->d_rarr, ctx->d_rout,
                  ctx->rx.keys, ctx->rx.keys_alt, ctx->rx.dig_hist, ctx->rx.tile_hist};
   for (void* p : dev) if (p) cudaFree(p);
   void* host[] = {ctx->h_outblk,
@@ -1299,7 +1304,7 @@ extern "C" autx_status autx_route_apply(autx_ctx* ctx, const void* d_records, co
   if (n) {
     CK(cudaMemcpyAsync(ctx->d_rarr, ctx->h_rarr, (size_t)n * sizeof(RouteArr), cudaMemcpyHostToDevice, ctx->stream));
     CK(launch_route(ctx->stream, d_records, stride, G, ctx->d_rarr, n, ctx->d_pin, ctx->cfg.token_threshold,
-                    ctx->d_rout));
+                    ctx->d_rout, ctx->cfg.route_policy, ctx->d_rr));
     CK(cudaMemcpyAsync(engine_out, ctx->d_rout, (size_t)n * 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
   }

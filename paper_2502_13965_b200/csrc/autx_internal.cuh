@@ -337,7 +337,7 @@ cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const 
                          uint64_t stride, uint32_t G, uint32_t t);
 cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,
                          const RouteArr* arr, uint32_t n, int8_t* pin, uint32_t threshold,
-                         int32_t* out);
+                         int32_t* out, uint32_t mode, uint32_t* rr);
 cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt,
                             const ArrivalRec* recs, uint32_t n, uint32_t first_slot, uint32_t t,
                             const uint32_t* par = nullptr);

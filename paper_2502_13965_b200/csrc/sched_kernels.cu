@@ -176,11 +176,23 @@ __global__ void __launch_bounds__(FIN_THREADS) k_apply(Policy pol, ProgTable pt,
 
 // Alg. 2 over the replicated arrival batch, canonical order: tokens <= threshold -> argmin load
 // (ties -> lowest engine id); else the program's pinned engine, or argmin + pin (l.5-10).  The
-// chosen engine's load is incremented after each assignment (R23).  One thread: the recurrence
-// through `load` is sequential by definition; G <= 8 loads stay in registers.
+// chosen engine's load is incremented after each assignment (R23).  mode 1 (Least Used):
+// argmin load for every call, no pins; mode 2 (Round Robin): the replicated cursor *rr.
+// One thread: the recurrence through `load` is sequential by definition; G <= 8 loads stay in
+// registers.
 __global__ void k_route(const char* base, uint64_t stride, uint32_t G, const RouteArr* arr,
-                        uint32_t n, int8_t* pin, uint32_t threshold, int32_t* out) {
+                        uint32_t n, int8_t* pin, uint32_t threshold, int32_t* out, uint32_t mode,
+                        uint32_t* rr) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (mode == 2) {
+    uint32_t e = *rr;
+    for (uint32_t i = 0; i < n; ++i) {
+      out[i] = (int32_t)e;
+      e = e + 1 == G ? 0 : e + 1;
+    }
+    *rr = e;
+    return;
+  }
   uint64_t load[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e)
@@ -188,8 +200,9 @@ __global__ void k_route(const char* base, uint64_t stride, uint32_t G, const Rou
   for (uint32_t i = 0; i < n; ++i) {
     RouteArr a = arr[i];
     int e;
-    int pinned = a.tok > threshold ? pin[a.prog] : -1;
-    if (a.tok > threshold && pinned >= 0) {
+    const bool lng = mode == 0 && a.tok > threshold;
+    int pinned = lng ? pin[a.prog] : -1;
+    if (lng && pinned >= 0) {
       e = pinned;
     } else {
       e = 0;
@@ -197,7 +210,7 @@ __global__ void k_route(const char* base, uint64_t stride, uint32_t G, const Rou
 #pragma unroll
       for (int k = 1; k < 8; ++k)
         if (load[k] < best) { best = load[k]; e = k; }
-      if (a.tok > threshold) pin[a.prog] = (int8_t)e;
+      if (lng) pin[a.prog] = (int8_t)e;
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k)
@@ -1419,9 +1432,9 @@ cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const 
 
 cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,
                          const RouteArr* arr, uint32_t n, int8_t* pin, uint32_t threshold,
-                         int32_t* out) {
+                         int32_t* out, uint32_t mode, uint32_t* rr) {
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  if (n) k_route<<<1, 32, 0, s>>>((const char*)base, stride, G, arr, n, pin, threshold, out);
+  if (n) k_route<<<1, 32, 0, s>>>((const char*)base, stride, G, arr, n, pin, threshold, out, mode, rr);
   return cudaGetLastError();
 }
 

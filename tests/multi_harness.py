@@ -17,8 +17,9 @@ REC_BYTES = 1 << 16
 
 
 class OracleSched:
-    def __init__(self, cfg, rank, world):
+    def __init__(self, cfg, rank, world, router="locality"):
         from oracle.autellix import Engine, ProgramTable
+        self.router, self.rr = router, {"next": 0}
         self.eng = Engine(cfg, table=ProgramTable(), check_formulations=False)
         self.cfg, self.rank, self.world = cfg, rank, world
         self.recs = []
@@ -43,7 +44,7 @@ class OracleSched:
         self.recs = []
 
     def route_apply(self, ptr, descs):
-        from oracle.autellix import route
+        from oracle.autellix import route, route_least_used, route_round_robin
         t = self.t + 1 if self.last else 0
         raw = ctypes.string_at(ptr, REC_BYTES * self.world)
         loads = []
@@ -60,6 +61,10 @@ class OracleSched:
         arr = [(int(d["call_id"]), int(d["program_id"]), int(d["input_tokens"])) for d in descs]
         for _, pid, _ in arr:       # replicated process table: every rank creates every entry
             self.eng.table.ensure(pid, t)
+        if self.router == "least_used":
+            return np.array(route_least_used(arr, loads), np.int32)
+        if self.router == "round_robin":
+            return np.array(route_round_robin(arr, self.world, self.rr), np.int32)
         return np.array(route(arr, loads, self.pins, self.cfg.token_threshold), np.int32)
 
     def register(self, descs):
@@ -90,7 +95,7 @@ class OracleSched:
         return len(self.eng.calls)
 
 
-def run_rank(rank, world, port, out_path, use_gpu, trace_name, seed, cfg_kw):
+def run_rank(rank, world, port, out_path, use_gpu, trace_name, seed, cfg_kw, router="locality"):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -106,7 +111,7 @@ def run_rank(rank, world, port, out_path, use_gpu, trace_name, seed, cfg_kw):
         s = Scheduler(policy=cfg.policy, K=cfg.K, q_hi=cfg.q_hi, quanta=cfg.quanta, beta=cfg.beta,
                       max_batch=cfg.max_batch, kv_budget=cfg.kv_budget, block_tokens=cfg.block_tokens,
                       max_calls=1 << 15, max_programs=1 << 12, token_threshold=cfg.token_threshold,
-                      rank=rank, nranks=world)
+                      rank=rank, nranks=world, route_policy=router)
 
         def new_record(nbytes):
             return torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
@@ -117,7 +122,7 @@ def run_rank(rank, world, port, out_path, use_gpu, trace_name, seed, cfg_kw):
             dist.all_gather(parts, rec.cpu())
             return torch.cat(parts).cuda()
     else:
-        s = OracleSched(cfg, rank, world)
+        s = OracleSched(cfg, rank, world, router)
 
         def new_record(nbytes):
             return torch.zeros(nbytes, dtype=torch.uint8)
@@ -141,7 +146,7 @@ def run_rank(rank, world, port, out_path, use_gpu, trace_name, seed, cfg_kw):
     dist.destroy_process_group()
 
 
-def run_world(tmp_path, use_gpu, trace_name, seed, cfg_kw, world=2):
+def run_world(tmp_path, use_gpu, trace_name, seed, cfg_kw, world=2, router="locality"):
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -150,7 +155,7 @@ def run_world(tmp_path, use_gpu, trace_name, seed, cfg_kw, world=2):
     s.close()
     outs = [str(tmp_path / f"rank{r}.pkl") for r in range(world)]
     ctx = mp.get_context("spawn")
-    ps = [ctx.Process(target=run_rank, args=(r, world, port, outs[r], use_gpu, trace_name, seed, cfg_kw))
+    ps = [ctx.Process(target=run_rank, args=(r, world, port, outs[r], use_gpu, trace_name, seed, cfg_kw, router))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -182,10 +187,10 @@ def golden_route():
     return cfg, routes, logs
 
 
-def oracle_multi(trace_name, seed, cfg_kw, world=2):
+def oracle_multi(trace_name, seed, cfg_kw, world=2, router="locality"):
     from oracle.autellix import Config, simulate_multi
     tr = make_trace(trace_name, seed)
-    logs, routes = simulate_multi(tr, Config(**cfg_kw), world)
+    logs, routes = simulate_multi(tr, Config(**cfg_kw), world, router=router)
     out = [[(r["t"], r["batch"], r["admit"], r["preempt"]) for r in lg if r["batch"] or r["preempt"]]
            for lg in logs]
     return out, [(t, c, d) for t, c, d in routes]

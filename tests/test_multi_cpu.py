@@ -31,3 +31,12 @@ def test_gloo_world2_golden_route(tmp_path):
     for r in range(2):
         assert res[r]["log"] == logs[r]
         assert [x for x in res[r]["routes"] if x[1]] == routes
+
+
+@pytest.mark.parametrize("router", ["least_used", "round_robin"])
+def test_gloo_world2_comparator_routers(tmp_path, router):
+    res = run_world(tmp_path, False, "tiny", 2, CFGS[1], router=router)
+    want, routes = oracle_multi("tiny", 2, CFGS[1], router=router)
+    for r in range(2):
+        assert res[r]["log"] == want[r]
+        assert [x for x in res[r]["routes"] if x[1]] == [x for x in routes if x[1]]

@@ -35,3 +35,15 @@ def test_two_engines_golden_route(tmp_path):
     for r in range(2):
         assert res[r]["log"] == logs[r], f"engine {r}"
         assert [x for x in res[r]["routes"] if x[1]] == routes
+
+
+@pytest.mark.parametrize("router", ["least_used", "round_robin"])
+@pytest.mark.parametrize("trace,seed,ci", [("tiny", 2, 1), ("chatbot", 0, 2)])
+def test_two_engines_comparator_routers(tmp_path, router, trace, seed, ci):
+    """The §6.4 comparators in k_route: routes and decisions equal the oracle's
+    simulate_multi(router=...)."""
+    res = run_world(tmp_path, True, trace, seed, CFGS[ci], router=router)
+    want, routes = oracle_multi(trace, seed, CFGS[ci], router=router)
+    for r in range(2):
+        assert res[r]["log"] == want[r], f"engine {r}"
+        assert [x for x in res[r]["routes"] if x[1]] == [x for x in routes if x[1]]
