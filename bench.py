@@ -399,27 +399,31 @@ def main():
     t_gen = time.time() - t_gen
     lad = spec_ladder()
     beta = (1, 0) if args.beta == "inf" else (2, 1)
+    gloo = os.environ.get("AUTX_DIST_BACKEND", "nccl") == "gloo"
+    comm = None
+    if world > 1 and not gloo:
+        # the library's own NCCL communicator for autx_route (torch only ships the 128-byte id)
+        from paper_2502_13965_b200.autx import comm_unique_id, comm_init
+        box = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        comm = comm_init(box[0], rank, world, local)
     s = Scheduler(policy=wl["policy"], beta=beta, max_batch=wl["max_batch"], kv_budget=wl["kv_budget"],
                   block_tokens=16, max_calls=int(active * 1.25) + 4096, max_programs=tr.n_programs + 1024,
                   order_mode=ORDER_RADIX if args.order == "radix" else ORDER_SELECT,
-                  device=local, stream=stream.cuda_stream, rank=rank, nranks=world, **lad)
+                  device=local, stream=stream.cuda_stream, rank=rank, nranks=world, nccl_comm=comm, **lad)
     if world == 1:
         d = TraceDriver(tr, s, log_lists=False)
     else:
         from paper_2502_13965_b200.multi import MultiEngineDriver
-        gloo = os.environ.get("AUTX_DIST_BACKEND", "nccl") == "gloo"
-        nrec = s.route_record_bytes()
-        gathered = torch.empty(world * nrec, dtype=torch.uint8, device=dev)
+        exchange = None                       # autx_route: record, ncclAllGather, apply, Alg. 2
+        if gloo:
+            nrec = s.route_record_bytes()
 
-        def exchange(rec):
-            if gloo:
+            def exchange(rec):
                 parts = [torch.empty(nrec, dtype=torch.uint8) for _ in range(world)]
                 torch.cuda.current_stream().synchronize()
                 dist.all_gather(parts, rec.cpu())
-                gathered.copy_(torch.cat(parts))
-            else:
-                dist.all_gather_into_tensor(gathered, rec)   # NCCL over NVLink, on the stream
-            return gathered
+                return torch.cat(parts).to(dev)
 
         def gather_ids(local_ids):
             out = [None] * world
@@ -435,14 +439,16 @@ def main():
     t_setup = time.time() - t_setup
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    gate_cycles = 2_000_000                   # ~1 ms spin while the host enqueues the step
+    # ~1 ms spin while the host enqueues the step.  N > 1: none, because autx_route returns the
+    # routes to the host (engine_out) mid-step, so the host waits on the device there anyway
+    gate_cycles = 2_000_000 if world == 1 else 0
 
     def timed_step():
-        if world == 1:
-            d.prepare()                       # the workload model's host work, not the library's
+        d.prepare()                           # the workload model's host work, not the library's
         if not args.no_flush:
             flush.zero_()
-        torch.cuda._sleep(gate_cycles)
+        if gate_cycles:
+            torch.cuda._sleep(gate_cycles)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         nc, na = d.issue()
@@ -613,6 +619,10 @@ def main():
             with open(args.json_out, "w") as f:
                 f.write(line + "\n")
     if world > 1:
+        s.close()
+        if comm:
+            from paper_2502_13965_b200.autx import comm_destroy
+            comm_destroy(comm)
         dist.destroy_process_group()
 
 

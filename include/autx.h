@@ -90,8 +90,11 @@ typedef struct {
                                 torch.cuda.current_stream().cuda_stream); NULL = the legacy default
                                 stream                                                               */
   int32_t rank, nranks;      /* engine id and engine count (routing)                                 */
-  uint32_t route_policy;     /* autx_route_policy: how autx_route_apply places arrivals  */
+  uint32_t route_policy;     /* autx_route_policy: how autx_route places arrivals        */
   uint32_t _reserved;        /* must be 0                                                            */
+  void* nccl_comm;           /* ncclComm_t of the nranks engines (autx_comm_init), caller-owned, or
+                                NULL: autx_route then needs nranks == 1 (the split
+                                autx_route_pack/apply path needs no communicator)                     */
 } autx_config;
 
 /* One arriving LLM call (Alg. 1 l.9).  Arrays of these must be in canonical order
@@ -200,7 +203,35 @@ autx_status autx_block_table_host(autx_ctx* ctx, uint32_t* h_offsets, uint32_t* 
                                   uint32_t* n_batch);
 
 /* ---- multi-engine routing (a8, Alg. 2) --------------------------------------------------- */
-/* Routing epoch, split around the caller's all-gather (torch.distributed / NCCL): pack this
+/* One routing epoch as ONE collective call (Alg. 2 "query engine workloads in
+ * parallel"; SURVEY §8(e) order).  Every rank calls it once per step, after autx_complete and
+ * before autx_register_call, with the identical replicated arrival batch `calls` (canonical
+ * order, host array, n may be 0).  On the ctx stream it
+ *   1. writes this engine's epoch record: load = queued + running calls after this step's
+ *      completions (R21) and the completion records of autx_complete (device resident),
+ *   2. all-gathers the nranks fixed-size records with ncclAllGather on cfg.nccl_comm (NVLink /
+ *      NVSwitch; with nranks == 1 and no communicator the record is used in place),
+ *   3. applies all nranks engines' completion records (its own included) to the replicated
+ *      process table (sums / maxima commute, so every rank's table stays identical, R22),
+ *   4. routes `calls` with the policy of cfg.route_policy (Alg. 2: LEN <= token_threshold ->
+ *      least-loaded engine, else the program's pinned engine, pinning on first sight; loads from
+ *      the epoch snapshot, incremented per assignment, R23); pins are replicated.
+ * engine_out[i] (host array, n entries) receives the engine of calls[i]; it is the call's only
+ * host round trip (the caller registers the calls routed to it).  Errors: E_INVAL (nranks > 1
+ * without nccl_comm, non-canonical batch, > 8 engines), E_STATE (after autx_register_call, or
+ * twice in one step), E_NCCL (the collective failed; message from ncclGetErrorString). */
+autx_status autx_route(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n, int32_t* engine_out);
+
+/* NCCL communicator helpers for autx_config.nccl_comm (the library links NCCL itself; torch is
+ * only the launcher).  Rank 0 calls autx_comm_unique_id (128 bytes), the caller broadcasts the
+ * bytes to every rank (any channel), then every rank calls autx_comm_init with its own rank and
+ * device (collective).  The communicator outlives every ctx that uses it: destroy it last. */
+autx_status autx_comm_unique_id(void* id_out /* 128 bytes */);
+autx_status autx_comm_init(const void* id /* 128 bytes */, int32_t rank, int32_t nranks, int32_t device,
+                           void** comm_out);
+autx_status autx_comm_destroy(void* comm);
+
+/* Routing epoch, split around the caller's own all-gather (e.g. gloo on a host): pack this
  * engine's epoch record (load = queued + running calls after this step's completions, R21, and
  * the completion records of this step) into a device buffer of autx_route_record_bytes(), then
  * after the all-gather of nranks records apply the peers' completion records to the

@@ -107,6 +107,13 @@ def simulate_srpt(trace, max_batch, max_steps=1_000_000):
     return log
 
 
+def makespan(trace, log):
+    """Offline makespan (§6.5.1, "makespan of all programs"; Fig. 9): steps from
+    the first program arrival to the last call completion (completion = the step after its last
+    decode step, reading R29)."""
+    return int(completion_steps(trace, log).max()) - int(np.min(trace.prog_arrival))
+
+
 def total_wait(trace, log):
     """Steps every call spent active but not running (the Fig. 2 metric, reading R16)."""
     done = completion_steps(trace, log)

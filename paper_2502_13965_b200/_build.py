@@ -9,6 +9,23 @@ LIB = os.path.join(HERE, "libautx.so")
 SOURCES = ["autx_api.cu", "sched_kernels.cu", "swap_kernels.cu", "radix_kernels.cu"]
 HEADERS = ["autx_internal.cuh", "block_prims.cuh", os.path.join("..", "..", "include", "autx.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dirs():
+    """NCCL headers and library: the wheel torch itself loads (one libnccl.so.2 per process),
+    else the system copy."""
+    try:
+        import nvidia.nccl as nn
+        root = list(nn.__path__)[0]
+        inc, lib = os.path.join(root, "include"), os.path.join(root, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+            return inc, lib
+    except ImportError:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+NCCL_INC, NCCL_LIB = _nccl_dirs()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v"]
 
@@ -34,7 +51,8 @@ def build(force=False, verbose=False):
     if not force and not stale():
         return LIB
     extra = _extra()
-    cmd = [NVCC, *FLAGS, *extra, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
+    cmd = [NVCC, *FLAGS, *extra, "-I", NCCL_INC, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES],
+           "-L", NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", "-rpath," + NCCL_LIB]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

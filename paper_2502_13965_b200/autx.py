@@ -37,7 +37,8 @@ class Config(C.Structure):
                 ("order_mode", C.c_uint32), ("n_gpu_blocks", C.c_uint32),
                 ("max_blocks_per_call", C.c_uint32), ("host_pages", C.c_uint64),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
-                ("nranks", C.c_int32), ("route_policy", C.c_uint32), ("_reserved", C.c_uint32)]
+                ("nranks", C.c_int32), ("route_policy", C.c_uint32), ("_reserved", C.c_uint32),
+                ("nccl_comm", C.c_void_p)]
 
 
 class StepOut(C.Structure):
@@ -108,6 +109,10 @@ def load_library(path=LIB_PATH):
         "autx_route_record_bytes": ([P], u64),
         "autx_route_pack": ([P, P], i32),
         "autx_route_apply": ([P, P, P, u32, P], i32),
+        "autx_route": ([P, P, u32, P], i32),
+        "autx_comm_unique_id": ([P], i32),
+        "autx_comm_init": ([P, i32, i32, i32, C.POINTER(P)], i32),
+        "autx_comm_destroy": ([P], i32),
         "autx_dump_calls": ([P, P, u32, C.POINTER(u32)], i32),
         "autx_program_state": ([P, u64, C.POINTER(u32), C.POINTER(u64)], i32),
         "autx_last_step_timing": ([P, C.POINTER(StepTiming)], i32),
@@ -130,13 +135,38 @@ def exported_symbols():
         "autx_create", "autx_destroy", "autx_last_error", "autx_version", "autx_start_program",
         "autx_end_program", "autx_complete", "autx_register_call", "autx_register_call_dag", "autx_sched_step",
         "autx_step_wait", "autx_kv_swap", "autx_block_table", "autx_block_table_host", "autx_route_record_bytes",
-        "autx_route_pack", "autx_route_apply", "autx_dump_calls", "autx_program_state",
+        "autx_route_pack", "autx_route_apply", "autx_route", "autx_comm_unique_id", "autx_comm_init",
+        "autx_comm_destroy", "autx_dump_calls", "autx_program_state",
         "autx_last_step_timing", "autx_step_stats", "autx_set_timing", "autx_num_active", "autx_phase_times", "autx_kernel_launches"]
 
 
 def kernel_launches():
     """Kernels launched by libautx.so so far in this process."""
     return int(load_library().autx_kernel_launches())
+
+
+def comm_unique_id():
+    """128-byte NCCL unique id (rank 0; broadcast it to the other ranks by any channel)."""
+    buf = C.create_string_buffer(128)
+    st = load_library().autx_comm_unique_id(buf)
+    if st != 0:
+        raise AutxError(st, "autx_comm_unique_id failed")
+    return buf.raw
+
+
+def comm_init(uid, rank, nranks, device):
+    """The library's own NCCL communicator for autx_config.nccl_comm (collective over ranks)."""
+    comm = C.c_void_p()
+    st = load_library().autx_comm_init(C.create_string_buffer(bytes(uid), 128), rank, nranks, device,
+                                       C.byref(comm))
+    if st != 0:
+        raise AutxError(st, "autx_comm_init failed")
+    return comm.value
+
+
+def comm_destroy(comm):
+    if comm:
+        load_library().autx_comm_destroy(C.c_void_p(comm))
 
 
 def _ptr(a):
@@ -150,7 +180,7 @@ class Scheduler:
                  kv_budget=None, block_tokens=16, max_calls=1 << 16, max_programs=1 << 16,
                  token_threshold=2048, order_mode=ORDER_SELECT, n_gpu_blocks=0,
                  max_blocks_per_call=0, host_pages=0, device=0, stream=None, rank=0, nranks=1,
-                 route_policy="locality"):
+                 route_policy="locality", nccl_comm=None):
         self.lib = load_library()
         cfg = Config()
         cfg.policy = POLICY[policy] if isinstance(policy, str) else int(policy)
@@ -174,6 +204,7 @@ class Scheduler:
         cfg.stream = stream
         cfg.rank, cfg.nranks = rank, nranks
         cfg.route_policy = ROUTE[route_policy] if isinstance(route_policy, str) else int(route_policy)
+        cfg.nccl_comm = nccl_comm
         self.cfg = cfg
         self.eq2 = cfg.policy == ATLAS_EQ2
         self.ctx = C.c_void_p()
@@ -279,6 +310,13 @@ class Scheduler:
         out = np.zeros(len(a), np.int32)
         self._check(self.lib.autx_route_apply(self.ctx, C.c_void_p(d_records_ptr), _ptr(a), len(a),
                                               _ptr(out)))
+        return out
+
+    def route(self, descs):
+        """One routing epoch as one collective (autx_route): record, NCCL all-gather, apply, Alg. 2."""
+        a = np.ascontiguousarray(descs, dtype=CALL_DESC)
+        out = np.zeros(len(a), np.int32)
+        self._check(self.lib.autx_route(self.ctx, _ptr(a), len(a), _ptr(out)))
         return out
 
     # ---- introspection ----------------------------------------------------------------------

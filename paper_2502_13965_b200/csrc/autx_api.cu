@@ -13,6 +13,8 @@
 #include <unordered_set>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/autx.h"
 #include "autx_internal.cuh"
 
@@ -89,7 +91,7 @@ struct autx_ctx {
   size_t outblk_bytes = 0;
   // routing epoch (a8)
   char* d_route_local = nullptr;   // RouteHdr + max_batch CompRec: this step's completion records
-  RouteHdr* h_hdr = nullptr;       // pinned staging for the header
+  char* d_route_all = nullptr;     // nranks gathered records (autx_route's all-gather destination)
   int8_t* d_pin = nullptr;         // [max_programs] Alg. 2 pin table (-1 = none)
   uint32_t* d_rr = nullptr;        // Round Robin cursor (replicated: every rank routes the same batch)
   RouteArr* h_rarr = nullptr;
@@ -239,7 +241,7 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&ctx->d_arr, ctx->arr_cap));
   CK(dalloc(&ctx->d_route_local, sizeof(RouteHdr) + (size_t)BS * sizeof(CompRec)));
   CK(cudaMemsetAsync(ctx->d_route_local, 0, sizeof(RouteHdr), ctx->stream));
-  CK(cudaHostAlloc((void**)&ctx->h_hdr, sizeof(RouteHdr), 0));
+  CK(dalloc(&ctx->d_route_all, (size_t)std::max(c.nranks, 1) * (sizeof(RouteHdr) + (size_t)BS * sizeof(CompRec))));
   CK(dalloc(&ctx->d_pin, P));
   CK(cudaMemsetAsync(ctx->d_pin, 0xff, P, ctx->stream));
   CK(dalloc(&ctx->d_rr, 1));
@@ -315,6 +317,7 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
   if (c.policy == AUTX_ATLAS_EQ2 && c.nranks > 1) return bad("AUTX_ATLAS_EQ2 is single-engine (nranks must be 1)");
   if (c.route_policy > AUTX_ROUTE_ROUND_ROBIN) return bad("route_policy");
   if (c._reserved) return bad("_reserved must be 0");
+  if (c.nranks < 1 || c.nranks > 8 || c.rank < 0 || c.rank >= c.nranks) return bad("rank / nranks (1..8 engines)");
   if (c.K < 1 || c.K > 16) return bad("K must be 1..16");
   for (uint32_t i = 0; i + 1 < c.K; ++i) {
     if (i > 0 && c.q_hi[i] < c.q_hi[i - 1]) return bad("q_hi must be ascending");
@@ -396,11 +399,11 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
                  ctx->kv.bt_offsets, ctx->kv.bt_blocks, ctx->d_pools, ctx->staging,
-                 ctx->d_route_local, ctx->d_pin, ctx->d_rr, ctx->d_rarr, ctx->d_rout,
+                 ctx->d_route_local, ctx->d_route_all, ctx->d_pin, ctx->d_rr, ctx->d_rarr, ctx->d_rout,
                  ctx->rx.keys, ctx->rx.keys_alt, ctx->rx.dig_hist, ctx->rx.tile_hist};
   for (void* p : dev) if (p) cudaFree(p);
   void* host[] = {ctx->h_outblk,
-                  ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_hdr, ctx->h_rarr, ctx->h_clin, ctx->h_par,
+                  ctx->h_cslots, ctx->h_arr, ctx->h_pools, ctx->h_rarr, ctx->h_clin, ctx->h_par,
                   ctx->rx.h_dig_hist};
   for (void* p : host) if (p) cudaFreeHost(p);
   for (auto& g : ctx->graphs) {
@@ -1248,26 +1251,22 @@ extern "C" autx_status autx_route_pack(autx_ctx* ctx, void* d_record) {
   autx_status s = sync_last(ctx);
   if (s) return s;
   if (ctx->registered_this) return fail(ctx, AUTX_E_STATE, "autx_route_pack after autx_register_call");
-  CK(cudaStreamSynchronize(ctx->stream));  // h_hdr reuse
-  ctx->h_hdr->load = ctx->call_slot.size();  // queued + running after this step's completions
-  ctx->h_hdr->n_comp = ctx->completed_this ? ctx->n_completed_pending : 0;
-  ctx->h_hdr->_pad = 0;
-  CK(cudaMemcpyAsync(d_record, ctx->h_hdr, sizeof(RouteHdr), cudaMemcpyHostToDevice, ctx->stream));
-  if (ctx->h_hdr->n_comp)
+  // header from the kernel parameters (queued + running after this step's completions, R21)
+  const uint32_t n_comp = ctx->completed_this ? ctx->n_completed_pending : 0;
+  CK(launch_route_hdr(ctx->stream, d_record, ctx->call_slot.size(), n_comp));
+  if (n_comp)
     CK(cudaMemcpyAsync((char*)d_record + sizeof(RouteHdr), ctx->d_route_local + sizeof(RouteHdr),
-                       (size_t)ctx->h_hdr->n_comp * sizeof(CompRec), cudaMemcpyDeviceToDevice, ctx->stream));
+                       (size_t)n_comp * sizeof(CompRec), cudaMemcpyDeviceToDevice, ctx->stream));
   return AUTX_OK;
 }
 
-extern "C" autx_status autx_route_apply(autx_ctx* ctx, const void* d_records, const autx_call_desc* calls,
-                                        uint32_t n, int32_t* engine_out) {
-  if (!ctx || !d_records || (n && (!calls || !engine_out))) return AUTX_E_INVAL;
-  uint32_t G = (uint32_t)std::max(ctx->cfg.nranks, 1);
-  if (G > 8) return fail(ctx, AUTX_E_INVAL, "at most 8 engines");
-  if (ctx->registered_this) return fail(ctx, AUTX_E_STATE, "autx_route_apply after autx_register_call");
-  if (ctx->routed_this) return fail(ctx, AUTX_E_STATE, "autx_route_apply twice in one step");
-  uint32_t t = next_step(ctx);
-  uint64_t stride = autx_route_record_bytes(ctx);
+// Steps 3-4 of a routing epoch over the gathered records (d_records: nranks records of
+// autx_route_record_bytes() each): apply every engine's completion records, then Alg. 2.
+static autx_status route_common(autx_ctx* ctx, const void* d_records, const autx_call_desc* calls, uint32_t n,
+                                int32_t* engine_out) {
+  const uint32_t G = (uint32_t)std::max(ctx->cfg.nranks, 1);
+  const uint32_t t = next_step(ctx);
+  const uint64_t stride = autx_route_record_bytes(ctx);
   if (ctx->cfg.nranks > 1) CK(launch_apply(ctx->stream, ctx->pol, ctx->pt, d_records, stride, G, t));
   if (n > ctx->rarr_cap) {
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1278,9 +1277,8 @@ extern "C" autx_status autx_route_apply(autx_ctx* ctx, const void* d_records, co
     CK(cudaHostAlloc((void**)&ctx->h_rarr, (size_t)n * sizeof(RouteArr), 0));
     CK(dalloc(&ctx->d_rarr, n));
     CK(dalloc(&ctx->d_rout, n));
-  } else {
-    CK(cudaStreamSynchronize(ctx->stream));
   }
+  // (h_rarr is free to refill: the last epoch that used it synchronised on its engine_out copy)
   // replicated process-table rows: created in canonical arrival order on every rank
   for (uint32_t i = 0; i < n; ++i) {
     const autx_call_desc& d = calls[i];
@@ -1310,6 +1308,80 @@ extern "C" autx_status autx_route_apply(autx_ctx* ctx, const void* d_records, co
   }
   ctx->routed_this = true;
   return AUTX_OK;
+}
+
+static autx_status route_checks(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n, int32_t* engine_out) {
+  if (n && (!calls || !engine_out)) return fail(ctx, AUTX_E_INVAL, "calls / engine_out");
+  if (ctx->registered_this) return fail(ctx, AUTX_E_STATE, "routing after autx_register_call");
+  if (ctx->routed_this) return fail(ctx, AUTX_E_STATE, "routing twice in one step");
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_route_apply(autx_ctx* ctx, const void* d_records, const autx_call_desc* calls,
+                                        uint32_t n, int32_t* engine_out) {
+  if (!ctx || !d_records) return AUTX_E_INVAL;
+  if (autx_status s = route_checks(ctx, calls, n, engine_out)) return s;
+  return route_common(ctx, d_records, calls, n, engine_out);
+}
+
+#define NCK(call)                                                                                  \
+  do {                                                                                             \
+    ncclResult_t r_ = (call);                                                                      \
+    if (r_ != ncclSuccess) return fail(ctx, AUTX_E_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+extern "C" autx_status autx_route(autx_ctx* ctx, const autx_call_desc* calls, uint32_t n, int32_t* engine_out) {
+  if (!ctx) return AUTX_E_INVAL;
+  if (autx_status s = route_checks(ctx, calls, n, engine_out)) return s;
+  const int G = std::max(ctx->cfg.nranks, 1);
+  ncclComm_t comm = reinterpret_cast<ncclComm_t>(ctx->cfg.nccl_comm);
+  if (G > 1 && !comm) return fail(ctx, AUTX_E_INVAL, "autx_route with nranks > 1 needs autx_config.nccl_comm");
+  autx_status s = sync_last(ctx);  // the previous step's host-visible state (no device wait otherwise)
+  if (s) return s;
+  // 1. this engine's epoch record: header from the host's counts, records already on the device
+  //    (written by autx_complete's kernel)
+  const uint32_t n_comp = ctx->completed_this ? ctx->n_completed_pending : 0;
+  CK(launch_route_hdr(ctx->stream, ctx->d_route_local, ctx->call_slot.size(), n_comp));
+  // 2. the all-gather of the fixed-size records, stream-ordered (NCCL over NVLink / NVSwitch)
+  const size_t stride = autx_route_record_bytes(ctx);
+  const void* recs = ctx->d_route_local;
+  if (comm) {
+    int cr = 0, cn = 0;
+    NCK(ncclCommCount(comm, &cn));
+    NCK(ncclCommUserRank(comm, &cr));
+    if (cn != G || cr != ctx->cfg.rank)
+      return fail(ctx, AUTX_E_INVAL, "nccl_comm is rank %d of %d, config says %d of %d", cr, cn, ctx->cfg.rank, G);
+    NCK(ncclAllGather(ctx->d_route_local, ctx->d_route_all, stride, ncclUint8, comm, ctx->stream));
+    recs = ctx->d_route_all;
+  }
+  // 3-4. apply every engine's records, route with Alg. 2
+  return route_common(ctx, recs, calls, n, engine_out);
+}
+
+extern "C" autx_status autx_comm_unique_id(void* id_out) {
+  if (!id_out) return AUTX_E_INVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return AUTX_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id_out, &id, sizeof id);
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_comm_init(const void* id, int32_t rank, int32_t nranks, int32_t device, void** comm_out) {
+  if (!id || !comm_out || nranks < 1 || rank < 0 || rank >= nranks) return AUTX_E_INVAL;
+  *comm_out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return AUTX_E_CUDA;
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof u);
+  ncclComm_t c = nullptr;
+  if (ncclCommInitRank(&c, nranks, u, rank) != ncclSuccess) return AUTX_E_NCCL;
+  *comm_out = c;
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_comm_destroy(void* comm) {
+  if (!comm) return AUTX_E_INVAL;
+  return ncclCommDestroy(reinterpret_cast<ncclComm_t>(comm)) == ncclSuccess ? AUTX_OK : AUTX_E_NCCL;
 }
 
 extern "C" autx_status autx_phase_times(autx_ctx* ctx, uint64_t* ns, uint32_t cap) {

@@ -335,6 +335,7 @@ cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, Pro
                             bool kv_on, CompRec* rec_out, const PrologueArgs& a);
 cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const void* base,
                          uint64_t stride, uint32_t G, uint32_t t);
+cudaError_t launch_route_hdr(cudaStream_t s, void* rec, uint64_t load, uint32_t n_comp);
 cudaError_t launch_route(cudaStream_t s, const void* base, uint64_t stride, uint32_t G,
                          const RouteArr* arr, uint32_t n, int8_t* pin, uint32_t threshold,
                          int32_t* out, uint32_t mode, uint32_t* rr);

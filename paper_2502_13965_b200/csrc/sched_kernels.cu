@@ -174,6 +174,12 @@ __global__ void __launch_bounds__(FIN_THREADS) k_apply(Policy pol, ProgTable pt,
   }
 }
 
+// The epoch record's header (autx_route): load and completion count from the kernel parameters,
+// so the host stages nothing that a later step could overwrite before the copy ran.
+__global__ void k_route_hdr(RouteHdr* h, unsigned long long load, uint32_t n_comp) {
+  if (threadIdx.x == 0) *h = RouteHdr{load, n_comp, 0u};
+}
+
 // Alg. 2 over the replicated arrival batch, canonical order: tokens <= threshold -> argmin load
 // (ties -> lowest engine id); else the program's pinned engine, or argmin + pin (l.5-10).  The
 // chosen engine's load is incremented after each assignment (R23).  mode 1 (Least Used):
@@ -1427,6 +1433,12 @@ cudaError_t launch_apply(cudaStream_t s, const Policy& pol, ProgTable pt, const 
                          uint64_t stride, uint32_t G, uint32_t t) {
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   k_apply<<<1, FIN_THREADS, 0, s>>>(pol, pt, (const char*)base, stride, G, t);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_route_hdr(cudaStream_t s, void* rec, uint64_t load, uint32_t n_comp) {
+  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
+  k_route_hdr<<<1, 32, 0, s>>>(reinterpret_cast<RouteHdr*>(rec), load, n_comp);
   return cudaGetLastError();
 }
 

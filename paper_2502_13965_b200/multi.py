@@ -3,13 +3,16 @@ one routing epoch per step.
 
 Per step t on every rank (order of SURVEY §8(e); the oracle's simulate_multi follows it too):
   1. local completions of step t-1            -> autx_complete (rows freed, records built)
-  2. epoch record (load after 1, records)      -> autx_route_pack into a device buffer
-  3. all-gather of the G records               -> `exchange` (NCCL all_gather on GPUs, gloo in tests)
-  4. every rank applies all G record sets to its replicated process table and routes the
-     replicated arrival batch with Alg. 2     -> autx_route_apply (R22, R23)
-  5. register the arrivals routed here, schedule -> autx_register_call, autx_sched_step
+  2. epoch record (load after 1, records), all-gather of the G records, apply all G record sets
+     to the replicated process table (R22), route the replicated arrival batch with Alg. 2 (R23)
+                                               -> autx_route: one collective (ncclAllGather on the
+                                                  library's communicator), or, with an
+                                                  `exchange` callable (gloo tests), the split
+                                                  autx_route_pack / exchange / autx_route_apply
+  3. register the arrivals routed here, schedule -> autx_register_call, autx_sched_step
 The workload side (DAG readiness) needs every rank's completed call ids, which `gather_ids`
-all-gathers; it is harness state, not scheduler state.
+all-gathers in `prepare()`; it is harness state (the meta-engine's), not scheduler state,
+so a benchmark does it before its timed region.
 """
 from __future__ import annotations
 
@@ -24,28 +27,39 @@ class MultiEngineDriver(TraceDriver):
     def __init__(self, trace, sched, rank, world, exchange, gather_ids, new_record, log_lists=True):
         super().__init__(trace, sched, log_lists=log_lists)
         self.rank, self.world = rank, world
-        self.exchange = exchange          # record tensor -> gathered tensor (world records)
+        self.exchange = exchange          # None: autx_route (in-library NCCL); else record -> gathered
         self.gather_ids = gather_ids      # local np.int64 array -> list of arrays (all ranks)
-        self.rec = new_record(sched.route_record_bytes())
+        self.rec = new_record(sched.route_record_bytes()) if exchange is not None else None
         self.routes = []
 
-    def issue(self):
+    def prepare(self):
+        """Harness side of step t (no ABI call): every engine's completed calls (for DAG
+        readiness), the programs they end, the replicated arrival batch."""
         t = self.t
-        s = self.s
         local = self.pending
-        t0 = time.perf_counter()
-        if len(local):
-            s.complete(self.tr.call_id[local])
-        s.route_pack(self.rec.data_ptr())
-        gathered = self.exchange(self.rec)
-        self.api_s += time.perf_counter() - t0
         all_done = np.sort(np.concatenate([np.asarray(x, np.int64) for x in self.gather_ids(local)]))
         ended = self._release(t, all_done)
-        arr = self.arrivals(t)
+        self._prepared = (t, self.tr.call_id[local], ended, self.arrivals(t))
+
+    def issue(self):
+        if getattr(self, "_prepared", None) is None or self._prepared[0] != self.t:
+            self.prepare()
+        t, ids, ended, arr = self._prepared
+        self._prepared = None
+        s = self.s
         t0 = time.perf_counter()
-        for pid in ended:
-            s.end_program(pid)
-        dest = s.route_apply(gathered.data_ptr(), arr)
+        if len(ids):
+            s.complete(ids)
+        if self.exchange is None:
+            for pid in ended:
+                s.end_program(pid)
+            dest = s.route(arr)
+        else:
+            s.route_pack(self.rec.data_ptr())
+            gathered = self.exchange(self.rec)
+            for pid in ended:
+                s.end_program(pid)
+            dest = s.route_apply(gathered.data_ptr(), arr)
         mine = arr[dest == self.rank]
         if len(mine):
             s.register(mine)
@@ -53,7 +67,7 @@ class MultiEngineDriver(TraceDriver):
         self.api_s += time.perf_counter() - t0
         if self.log_lists:
             self.routes.append((t, [int(x) for x in arr["call_id"]], [int(x) for x in dest]))
-        return len(local), len(mine)
+        return len(ids), len(mine)
 
     def run(self, max_steps=10 ** 9):
         # lockstep: every rank runs every step (no idle skipping: it needs global knowledge)

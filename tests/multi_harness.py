@@ -105,7 +105,20 @@ def run_rank(rank, world, port, out_path, use_gpu, trace_name, seed, cfg_kw, rou
     from paper_2502_13965_b200.multi import MultiEngineDriver
     tr = make_trace(trace_name, seed)
     cfg = Config(**cfg_kw)
-    if use_gpu:
+    if use_gpu == "nccl":
+        # autx_route: the library's own NCCL communicator, one GPU per rank
+        from paper_2502_13965_b200 import Scheduler
+        from paper_2502_13965_b200.autx import comm_unique_id, comm_init
+        torch.cuda.set_device(rank)
+        box = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        comm = comm_init(box[0], rank, world, rank)
+        s = Scheduler(policy=cfg.policy, K=cfg.K, q_hi=cfg.q_hi, quanta=cfg.quanta, beta=cfg.beta,
+                      max_batch=cfg.max_batch, kv_budget=cfg.kv_budget, block_tokens=cfg.block_tokens,
+                      max_calls=1 << 15, max_programs=1 << 12, token_threshold=cfg.token_threshold,
+                      device=rank, rank=rank, nranks=world, route_policy=router, nccl_comm=comm)
+        new_record, exchange = None, None
+    elif use_gpu:
         from paper_2502_13965_b200 import Scheduler
         torch.cuda.set_device(0)
         s = Scheduler(policy=cfg.policy, K=cfg.K, q_hi=cfg.q_hi, quanta=cfg.quanta, beta=cfg.beta,
@@ -139,6 +152,10 @@ def run_rank(rank, world, port, out_path, use_gpu, trace_name, seed, cfg_kw, rou
 
     d = MultiEngineDriver(tr, s, rank, world, exchange, gather_ids, new_record)
     log = d.run(max_steps=100000)
+    if use_gpu == "nccl":
+        from paper_2502_13965_b200.autx import comm_destroy
+        s.close()
+        comm_destroy(comm)
     recs = [(r["t"], r["batch"], r["admit"], r["preempt"]) for r in log if r["batch"] or r["preempt"]]
     with open(out_path, "wb") as f:
         pickle.dump({"log": recs, "routes": d.routes}, f)
