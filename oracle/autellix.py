@@ -29,6 +29,25 @@ engine step t (time unit = one decode iteration, reading R17):
         batch, admit = batch - resident, preempt = resident - batch, swap bytes
   7. account: batch exec++ mtime++ quanta-- running; others wait++ totwait++
 
+Multi-step scheduling with over-provisioning (reading R32),
+`Config.sched_every` = N, `Config.overprovision` = X (N = 1, X = 0 is the plain path above):
+  * a scheduling point is the first step, every N-th step after the last scheduling point, and
+    any step whose carried-over resident list is empty (idle engines do not wait for the window);
+  * at a scheduling point steps 3-6 run as above, but the cutoff takes the longest prefix with
+    count <= BS + X (and sum kvb <= P): the resident set R; the batch is its first BS calls and
+    the other <= X calls are "standby" — their KV is put on the GPU (admitted) so that they join
+    the batch at once when a batch call finishes before the next scheduling point;
+  * between scheduling points (window steps) demotion, anti-starvation and ordering do not run
+    (the scheduler runs "once every N decoding steps"): the carried resident list (batch, then
+    standby, minus completed calls) is walked in order while sum kvb <= P (stop at the first
+    misfit); its first BS calls run, the rest stay standby, and the calls after the misfit are
+    evicted (KV growth of running calls: lazy eviction, lowest priority first).  Arrivals wait
+    for the next scheduling point;
+  * admit = R - resident before (swap-in when the call has run, else a fresh allocation);
+    preempt = resident before - R, in the previous R order; a preempted call that never ran has
+    no KV content, so it is freed without a swap-out; quanta keep counting down in window steps
+    and the demotion they trigger waits for the next scheduling point.
+
 Two independent formulations of steps 5-6 are provided and cross-checked:
   * `order_sorted`:  sort every active call by the unique key and take the prefix;
   * `order_queues`:  Alg. 1's literal walk over Q_1..Q_K (each queue a list in
@@ -62,6 +81,8 @@ class Config:
     block_tokens: int = 16
     block_bytes: int = 0             # bytes of one logical KV block over all layers (swap ledger)
     token_threshold: int = 2048      # Alg. 2 line 2
+    sched_every: int = 1             # N: the scheduler runs once every N steps (R32)
+    overprovision: int = 0           # X: resident standby calls beyond BS (R32)
 
     def check(self):
         assert self.policy in (FCFS, MLFQ, PLAS, ATLAS, ATLAS_EQ2)
@@ -69,6 +90,7 @@ class Config:
         assert list(self.q_hi) == sorted(self.q_hi)
         assert all(q is None or q >= 1 for q in self.quanta)
         assert self.max_batch >= 1
+        assert self.sched_every >= 1 and self.overprovision >= 0
         return self
 
 
@@ -157,6 +179,8 @@ class Engine:
         self.calls = {}          # cid -> Call (active calls)
         self.next_seq = 0
         self.prev_batch = []     # cids of the previous step's batch, in batch order
+        self.standby = []        # R32: resident, not running (after the batch in R order)
+        self.since = None        # R32: steps since the last scheduling point (None: none yet)
         self.check = check_formulations
         self.last_arrival_key = None
         self.crit = {}           # ATLAS_EQ2: completed cid -> p(c) + t_c (Eq. 2 operand)
@@ -196,6 +220,7 @@ class Engine:
                 self.crit_of_prog.setdefault(c.pid, []).append(cid)
             del self.calls[cid]
         self.prev_batch = [x for x in self.prev_batch if x in self.calls]
+        self.standby = [x for x in self.standby if x in self.calls]
         return recs
 
     def apply_records(self, t, recs):
@@ -263,7 +288,7 @@ class Engine:
                 c.mtime = 0
 
     def fits(self, count, kv_sum, c):
-        if count + 1 > self.cfg.max_batch:
+        if count + 1 > self.cfg.max_batch + self.cfg.overprovision:   # R32: BS + X resident
             return False
         P = self.cfg.kv_budget
         return P is None or kv_sum + self.kvb(c) <= P
@@ -314,17 +339,39 @@ class Engine:
         if self.check:
             alt = self.order_queues()
             assert alt == batch, f"formulations disagree at t={t}: {batch} vs {alt}"
-        in_batch = set(batch)
-        prev = self.prev_batch
-        admit = [x for x in batch if not self.calls[x].resident]
-        preempt = [x for x in prev if x not in in_batch]
+        return self._commit(t, batch)
+
+    def window(self, t):
+        """R32 window step: the carried resident list, walked in order under the KV budget."""
+        res, n, kv = [], 0, 0
+        for x in self.prev_batch + self.standby:
+            c = self.calls[x]
+            if not self.fits(n, kv, c):
+                break                                                   # lazy eviction
+            res.append(x)
+            n += 1
+            kv += self.kvb(c)
+        if self.calls and not res:
+            raise CapacityError(f"t={t}: a call's KV need exceeds the budget (reading R14)")
+        return self._commit(t, res)
+
+    def _commit(self, t, res):
+        """Lists, swap ledger and step accounting (phases 6-7) for resident set `res` (in
+        order): the first BS calls run, the rest are standby (R32; none when X = 0)."""
+        BS = self.cfg.max_batch
+        batch, standby = res[:BS], res[BS:]
+        in_res, in_batch = set(res), set(batch)
+        prev = self.prev_batch + self.standby
+        admit = [x for x in res if not self.calls[x].resident]
+        preempt = [x for x in prev if x not in in_res]
         bb = self.cfg.block_bytes
-        swap_out = sum(self.calls[x].held for x in preempt) * bb
+        # a call that never ran has no KV content: no host copy either way (R28, R32)
+        swap_out = sum(self.calls[x].held for x in preempt if self.calls[x].exec > 0) * bb
         swap_in = sum(self.calls[x].held for x in admit if self.calls[x].exec > 0) * bb
-        blocks = sum(self.kvb(self.calls[x]) for x in batch)
+        blocks = sum(self.kvb(self.calls[x]) for x in res)
         for x in preempt:
             self.calls[x].resident = False
-        for x in batch:
+        for x in res:
             c = self.calls[x]
             c.resident = True
             c.held = self.kvb(c)
@@ -340,15 +387,30 @@ class Engine:
                 c.totwait += 1
                 c.running = False
         self.prev_batch = list(batch)
-        return dict(t=t, batch=batch, admit=admit, preempt=preempt, swap_out=swap_out,
-                    swap_in=swap_in, kv_blocks=blocks, n_active=len(self.calls))
+        self.standby = list(standby)
+        rec = dict(t=t, batch=batch, admit=admit, preempt=preempt, swap_out=swap_out,
+                   swap_in=swap_in, kv_blocks=blocks, n_active=len(self.calls))
+        if self.cfg.overprovision or self.cfg.sched_every > 1:
+            rec["standby"] = standby
+        return rec
+
+    def sched_point(self):
+        """R32: does this step run the scheduler (after completions and arrivals)?"""
+        carried = self.prev_batch + self.standby
+        return self.since is None or self.since >= self.cfg.sched_every or not carried
 
     def step(self, t, completed, arrivals, parents=None):
         recs = self.complete(t, completed)
         self.apply_records(t, recs)
         self.register(t, arrivals, parents)
-        self.demote_and_promote()
-        return self.schedule(t)
+        if self.sched_point():
+            self.demote_and_promote()
+            rec = self.schedule(t)
+            self.since = 1
+        else:
+            rec = self.window(t)
+            self.since += 1
+        return rec
 
     def load(self):
         """Alg. 2 QUERY_ENGINE_WORKLOADS: queued + running calls (reading R21)."""
