@@ -95,6 +95,14 @@ typedef struct {
   void* nccl_comm;           /* ncclComm_t of the nranks engines (autx_comm_init), caller-owned, or
                                 NULL: autx_route then needs nranks == 1 (the split
                                 autx_route_pack/apply path needs no communicator)                     */
+  /* Multi-step scheduling with over-provisioning ("running the scheduler once every N
+   * decoding steps ... overprovisions queued requests already on the GPU"; reading R32):     */
+  uint32_t sched_every;      /* N >= 1 (0 = 1): the ordering runs at the first step, every N-th step
+                                after the last one and whenever the carried resident list is empty;
+                                the steps between (window steps) keep the resident list, in order,
+                                under the KV budget.  N > 1: single engine, AUTX_ORDER_SELECT      */
+  uint32_t overprovision;    /* X >= 0: the resident set is the longest prefix with <= BS + X calls
+                                (BS + X <= 2048); its first BS calls run, the rest are standby    */
 } autx_config;
 
 /* One arriving LLM call (Alg. 1 l.9).  Arrays of these must be in canonical order
@@ -114,9 +122,12 @@ typedef struct {
  * the host mirrors (pinned, library-owned) and the counts are valid once `done` (a
  * cudaEvent_t) has completed — autx_step_wait() waits for it. */
 typedef struct {
-  const uint64_t* batch;       /* device: call ids of the batch, in key order (Alg. 1 l.32-39) */
-  const uint64_t* admit;       /* device: batch calls not resident before this step, batch order */
-  const uint64_t* preempt;     /* device: resident calls not in the batch, previous-batch order  */
+  const uint64_t* batch;       /* device: call ids of the batch, in key order (Alg. 1 l.32-39),
+                                  then the standby calls (n_standby, R32)                      */
+  const uint64_t* admit;       /* device: batch (and standby) calls not resident before this step,
+                                  batch order                                                    */
+  const uint64_t* preempt;     /* device: resident calls no longer resident, previous order; a
+                                  preempted call that never ran has no KV content to swap (R32)  */
   const uint64_t* h_batch;     /* host mirrors of the three lists                                */
   const uint64_t* h_admit;
   const uint64_t* h_preempt;
@@ -125,7 +136,8 @@ typedef struct {
   uint64_t swap_in_blocks;     /* sum over admit with a host copy of held blocks               */
   uint64_t kv_blocks;          /* sum over the batch of kvb                                    */
   uint32_t n_promoted;         /* anti-starvation promotions this step (diagnostic)            */
-  uint32_t _pad;
+  uint32_t n_standby;          /* R32: resident standby calls; batch[n_batch .. n_batch+n_standby)
+                                  (device and host lists) holds them in order; 0 when X = 0      */
   void* done;                  /* cudaEvent_t recorded after the step's device work            */
 } autx_step_out;
 

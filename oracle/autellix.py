@@ -372,9 +372,7 @@ class Engine:
         for x in preempt:
             self.calls[x].resident = False
         for x in res:
-            c = self.calls[x]
-            c.resident = True
-            c.held = self.kvb(c)
+            self.calls[x].resident = True
         for c in self.calls.values():                                   # phase 7
             if c.cid in in_batch:
                 c.exec += 1
@@ -386,6 +384,9 @@ class Engine:
                 c.wait += 1
                 c.totwait += 1
                 c.running = False
+        for x in res:   # R28: a resident call holds the blocks of its KV, ceil((input + exec) / bt)
+            c = self.calls[x]
+            c.held = ceil_div(c.input_tokens + c.exec, self.cfg.block_tokens)
         self.prev_batch = list(batch)
         self.standby = list(standby)
         rec = dict(t=t, batch=batch, admit=admit, preempt=preempt, swap_out=swap_out,

@@ -38,7 +38,7 @@ class Config(C.Structure):
                 ("max_blocks_per_call", C.c_uint32), ("host_pages", C.c_uint64),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("route_policy", C.c_uint32), ("_reserved", C.c_uint32),
-                ("nccl_comm", C.c_void_p)]
+                ("nccl_comm", C.c_void_p), ("sched_every", C.c_uint32), ("overprovision", C.c_uint32)]
 
 
 class StepOut(C.Structure):
@@ -47,7 +47,7 @@ class StepOut(C.Structure):
                 ("h_preempt", C.POINTER(C.c_uint64)), ("n_batch", C.c_uint32),
                 ("n_admit", C.c_uint32), ("n_preempt", C.c_uint32), ("n_active", C.c_uint32),
                 ("swap_out_blocks", C.c_uint64), ("swap_in_blocks", C.c_uint64),
-                ("kv_blocks", C.c_uint64), ("n_promoted", C.c_uint32), ("_pad", C.c_uint32),
+                ("kv_blocks", C.c_uint64), ("n_promoted", C.c_uint32), ("n_standby", C.c_uint32),
                 ("done", C.c_void_p)]
 
 
@@ -180,7 +180,7 @@ class Scheduler:
                  kv_budget=None, block_tokens=16, max_calls=1 << 16, max_programs=1 << 16,
                  token_threshold=2048, order_mode=ORDER_SELECT, n_gpu_blocks=0,
                  max_blocks_per_call=0, host_pages=0, device=0, stream=None, rank=0, nranks=1,
-                 route_policy="locality", nccl_comm=None):
+                 route_policy="locality", nccl_comm=None, sched_every=1, overprovision=0):
         self.lib = load_library()
         cfg = Config()
         cfg.policy = POLICY[policy] if isinstance(policy, str) else int(policy)
@@ -205,6 +205,7 @@ class Scheduler:
         cfg.rank, cfg.nranks = rank, nranks
         cfg.route_policy = ROUTE[route_policy] if isinstance(route_policy, str) else int(route_policy)
         cfg.nccl_comm = nccl_comm
+        cfg.sched_every, cfg.overprovision = sched_every, overprovision   # R32
         self.cfg = cfg
         self.eq2 = cfg.policy == ATLAS_EQ2
         self.ctx = C.c_void_p()
@@ -213,6 +214,7 @@ class Scheduler:
             raise AutxError(st, "autx_create failed (see stderr)")
         self.out = StepOut()
         self.max_batch = max_batch
+        self.list_cap = max_batch + overprovision
         self._views = None
 
     def _check(self, st):
@@ -269,10 +271,16 @@ class Scheduler:
         o = self.out
         if self._views is None:
             # the pinned mirrors live as long as the context: wrap them once
-            f = lambda p: np.ctypeslib.as_array(p, shape=(max(self.max_batch, 1),))
+            f = lambda p: np.ctypeslib.as_array(p, shape=(max(self.list_cap, 1),))
             self._views = (f(o.h_batch), f(o.h_admit), f(o.h_preempt))
         vb, va, vp = self._views
         return vb[:o.n_batch].copy(), va[:o.n_admit].copy(), vp[:o.n_preempt].copy()
+
+    def standby(self):
+        """R32: the resident standby calls of the last waited step, in order (after the batch)."""
+        self.lists()
+        o = self.out
+        return self._views[0][o.n_batch:o.n_batch + o.n_standby].copy()
 
     def kv_swap(self, k_ptrs, v_ptrs, chunk_bytes, host_ptr, host_bytes, mode=SWAP_SM):
         L = len(k_ptrs)

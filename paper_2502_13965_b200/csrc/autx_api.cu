@@ -99,6 +99,8 @@ struct autx_ctx {
   int32_t* d_rout = nullptr;
   uint32_t rarr_cap = 0;
   bool routed_this = false;
+  // R32 multi-step scheduling: steps since the last scheduling point (0: none yet)
+  uint32_t since = 0;
   uint32_t n_reg_this = 0;
   // work staged for the next sched_step's prologue kernel (single-engine mode)
   uint32_t n_comp_staged = 0, n_arr_staged = 0, arr_first_slot = 0;
@@ -195,7 +197,7 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&ctx->ctl, 1));
   CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
   Outputs& o = ctx->out;
-  uint32_t BS = c.max_batch;
+  uint32_t BS = ctx->pol.max_batch;  // list / resident-set capacity: BS + X (R32)
   size_t ntiles = rows / TILE + 1;
   // one device block [counts | batch | admit | preempt | batch slots] and its pinned mirror: one
   // D2H per step (the slots let the host check completions without an id set)
@@ -333,6 +335,11 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
   if (c.n_gpu_blocks > 0 && c.kv_budget_blocks != AUTX_INF && c.kv_budget_blocks > c.n_gpu_blocks)
     return bad("kv_budget_blocks exceeds n_gpu_blocks");
   if (c.order_mode != AUTX_ORDER_SELECT && c.order_mode != AUTX_ORDER_RADIX) return bad("order_mode");
+  const uint32_t N = c.sched_every ? c.sched_every : 1u;
+  if (c.overprovision > (uint32_t)MAX_BATCH || c.max_batch + c.overprovision > (uint32_t)MAX_BATCH)
+    return bad("max_batch + overprovision must be <= 2048");
+  if ((N > 1 || c.overprovision) && (c.order_mode != AUTX_ORDER_SELECT || c.nranks > 1))
+    return bad("multi-step scheduling / over-provisioning (R32) needs AUTX_ORDER_SELECT and one engine");
   ctx->cfg = c;
   Policy& p = ctx->pol;
   p.policy = c.policy;
@@ -341,7 +348,9 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
   memcpy(p.quanta, c.quanta, sizeof p.quanta);
   p.beta_num = c.beta_num;
   p.beta_den = c.beta_den;
-  p.max_batch = c.max_batch;
+  p.max_batch = c.max_batch + c.overprovision;  // resident set: BS + X (R32)
+  p.run_batch = c.max_batch;
+  p.multistep = N > 1 ? 1u : 0u;
   p.kv_budget = c.kv_budget_blocks;
   p.block_tokens = c.block_tokens;
   p.bt_shift = 0xFFu;
@@ -556,6 +565,7 @@ static autx_status flush_staged(autx_ctx* ctx, uint32_t t, bool always = false) 
   a.n_prog_rows = ctx->prog_next;
   a.n_rows = ctx->tail;
   a.seqno = ctx->seqno;
+  a.n_active = (uint32_t)ctx->call_slot.size();
   if (a.n_comp <= (uint32_t)PRO_INLINE) memcpy(a.comp, ctx->h_cslots, a.n_comp * sizeof(uint32_t));
   else a.comp_ptr = ctx->h_cslots;
   if (a.n_arr <= (uint32_t)PRO_INLINE) memcpy(a.arr, ctx->h_arr, a.n_arr * sizeof(ArrivalRec));
@@ -871,6 +881,17 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   static const bool no_graph = getenv("AUTX_NO_GRAPH") != nullptr;
   std::vector<LaunchRec> recs;
   const bool graph = !no_graph && !ctx->timing && !ctx->radix && ctx->n_arr_staged <= 4096;
+  // R32: a window step keeps the resident list; the ordering runs at the first step, every N-th
+  // step after the last scheduling point, and whenever the carried list is empty (the previous
+  // step's resident calls, which the host knows from its record, minus this step's completions)
+  bool window = false;
+  if (ctx->pol.multistep) {
+    const HostOut& h = *ctx->out.hout;
+    const uint32_t carried = ctx->stepped ? h.n_batch + h.n_standby - (ctx->completed_this ? ctx->n_completed_pending : 0)
+                                          : 0u;
+    window = ctx->since != 0 && ctx->since < ctx->cfg.sched_every && carried > 0;
+    ctx->since = window ? ctx->since + 1 : 1;
+  }
   if (graph) g_launch_rec = &recs;
   ++ctx->seqno;
   g_hp.lap(0);
@@ -879,7 +900,7 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   g_hp.lap(1);
   const cudaError_t le = launch_step(ctx->stream, ctx->pol, ctx->ct, ctx->pt, ctx->ctl, ctx->out, ctx->kv,
                                      ctx->kv_on, t, ctx->tail, ctx->seqno, ctx->timing ? ctx->ev : nullptr,
-                                     ctx->radix ? &ctx->rx : nullptr, arr_base, &ctx->radix_passes);
+                                     ctx->radix ? &ctx->rx : nullptr, arr_base, &ctx->radix_passes, window);
   g_launch_rec = nullptr;
   CK(le);
   g_hp.lap(2);
@@ -931,6 +952,7 @@ extern "C" autx_status autx_step_wait(autx_ctx* ctx, autx_step_out* out) {
   out->swap_in_blocks = h.swap_in_blocks;
   out->kv_blocks = h.kv_blocks;
   out->n_promoted = h.n_promoted;
+  out->n_standby = h.n_standby;
   if (ctx->timing) {
     float a = 0, b = 0, c = 0;
     cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
@@ -985,8 +1007,8 @@ static autx_status compact(autx_ctx* ctx) {
   // remap the previous batch (its completed rows were DEAD and are gone from the list: the
   // previous batch entries that are not live map to NONE and must be dropped)
   HostOut h = *ctx->out.hout;
-  std::vector<uint32_t> prev(h.n_batch);
-  CK(cudaMemcpyAsync(prev.data(), ctx->out.prev_slots, (size_t)h.n_batch * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<uint32_t> prev(h.n_batch + h.n_standby);  // the resident list (R32: batch, standby)
+  CK(cudaMemcpyAsync(prev.data(), ctx->out.prev_slots, prev.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   std::vector<uint32_t> np;
   for (uint32_t s : prev) if (s < old2new.size() && old2new[s] != NONE) np.push_back(old2new[s]);

@@ -13,7 +13,8 @@ constexpr uint8_t QF_QMASK = 0x0F;  // queue index q (0 = Q_1, highest priority)
 constexpr uint8_t QF_RUN = 0x10;    // in the previous step's batch ("running", key tie R12)
 constexpr uint8_t QF_RES = 0x20;    // KV resident on the GPU (eager eviction: == RUN after a step)
 constexpr uint8_t QF_DEAD = 0x40;   // empty row (completed call / never used)
-constexpr uint8_t QF_INB = 0x80;    // scratch: member of the batch being formed (finalize only)
+constexpr uint8_t QF_DEM = 0x80;    // multi-step (R32): quantum exhausted in a window step, demotion
+                                    // pending until the next scheduling point's dense pass
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr int MAX_K = 16;
@@ -65,7 +66,9 @@ struct Policy {
   uint32_t q_hi[15];
   uint32_t quanta[16];
   uint32_t beta_num, beta_den;
-  uint32_t max_batch;
+  uint32_t max_batch;      // resident-set capacity BS + X (R32; = BS when X = 0)
+  uint32_t run_batch;      // BS: the first run_batch resident calls run
+  uint32_t multistep;      // sched_every > 1: demotion deferred to scheduling points (QF_DEM)
   uint32_t kv_budget;
   uint32_t block_tokens;
   uint32_t n_gpu_blocks;
@@ -113,7 +116,7 @@ struct Ctl {
   uint32_t last_n_b;   // region B size of the last step (autx_step_stats; n_cand_b is reset by finalize)
   // this step's scalars, written by the prologue from its parameters, read by the rest of the
   // chain after its PDL wait: a graph replay then only re-parameterises the prologue node
-  uint32_t s_t, s_n_rows, s_seqno;
+  uint32_t s_t, s_n_rows, s_seqno, s_n_active;
   uint32_t s_tail_prev;  // rows older than this step's arrivals (finalize / compaction): the scan
                          // may read them before its PDL wait
   alignas(128) uint32_t qpart[QP_LINES][32];
@@ -127,7 +130,10 @@ struct HostOut {
   uint32_t n_promoted, err;
   uint32_t seqno;  // step sequence number, for sanity
   uint32_t err_info;
+  uint32_t n_standby;  // R32: resident standby calls after the batch in the batch list
+  uint32_t _pad;
 };
+static_assert(sizeof(HostOut) <= 64, "HostOut heads the 64-byte counts block of the output lists");
 
 // Swap plan (built by finalize, executed by autx_kv_swap).
 struct PlanItem {
@@ -178,7 +184,7 @@ __device__ __forceinline__ void load_rec(const struct CallTable& ct, uint32_t s,
   x.mtime = ct.mtime[s];
   x.quanta = ct.quanta[s];
   x.qf = ct.qf[s];
-  x._pad = (x.qf & QF_RUN) ? ct.bidx[s] : NONE;  // previous-batch index of a running call
+  x._pad = (x.qf & QF_RES) ? ct.bidx[s] : NONE;  // index in the previous resident list
   *r = x;
 }
 #endif
@@ -318,7 +324,7 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
 constexpr int PRO_INLINE = 96;
 struct PrologueArgs {
   uint32_t n_comp, n_arr, first_slot, t;
-  uint32_t n_prog_rows, n_rows, seqno, _pad;  // process-table rows in use; table rows and step seqno
+  uint32_t n_prog_rows, n_rows, seqno, n_active;  // process-table rows in use; table rows, step seqno, active calls
   const uint32_t* comp_ptr;
   const ArrivalRec* arr_ptr;
   const uint32_t* comp_lin;  // AUTX_ATLAS_EQ2: lineage index of each completion (mapped pinned)
@@ -350,7 +356,7 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev /* 4 events or null */,
                         const RadixState* rx /* non-null: AUTX_ORDER_RADIX */, uint32_t arr_base,
-                        uint32_t* radix_passes);
+                        uint32_t* radix_passes, bool window = false);
 cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                Outputs out, RadixState rx, uint32_t t, uint32_t n_rows,
                                uint32_t arr_base, int sms, uint32_t* passes_out);

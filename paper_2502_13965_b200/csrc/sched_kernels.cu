@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
     ctl->s_t = a.t;
     ctl->s_n_rows = a.n_rows;
     ctl->s_seqno = a.seqno;
+    ctl->s_n_active = a.n_active;
   }
   __syncthreads();
   if (comp_inline && arr_inline) {
@@ -422,6 +423,21 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, CallTable& ct, con
     }
   }
   bool wq = false, wb = false, wm = false;
+  if (pol.multistep) {
+    // R32: demotions deferred from window steps (quantum exhausted, QF_DEM) happen here, at the
+    // scheduling point, before anti-starvation (Alg. 1 l.20-23 before l.24-30, R9); the ratio
+    // above does not read q
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const uint32_t qf = qfs[j];
+      if ((qf & (QF_DEM | QF_DEAD)) == QF_DEM) {
+        const uint32_t q = min((qf & QF_QMASK) + 1u, pol.K - 1);
+        ct.quanta[row0 + j] = pol.quanta[q];
+        qfs[j] = (qf & ~(uint32_t)(QF_QMASK | QF_DEM)) | q;
+        wq = true;
+      }
+    }
+  }
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     const uint32_t qf = qfs[j];
@@ -770,7 +786,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
         r.mtime = lane4(mt[j >> 2], j & 3);
         r.quanta = lane4(qt[j >> 2], j & 3);
         r.qf = qfs[j];
-        r._pad = (qfs[j] & QF_RUN) ? lane4(bd[j >> 2], j & 3) : NONE;  // previous-batch index
+        r._pad = (qfs[j] & QF_RES) ? lane4(bd[j >> 2], j & 3) : NONE;  // previous resident index
         out.cand[pos] = row0 + j;
         out.cand_rec[pos] = r;
         out.ckey[pos] = cand_key(r, t);
@@ -920,9 +936,9 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
       out.skey[cnt] = x;
       out.sidx[cnt] = eo;
       out.srec[cnt] = rec;
-      // a running call (previous-batch entry rec._pad) publishes its sorted position: finalize
-      // tests the previous batch's membership in the new one without searching
-      if (rec.qf & QF_RUN) out.prev_pos[rec._pad] = (unsigned long long)seqno << 32 | cnt;
+      // a resident call (previous resident-list entry rec._pad) publishes its sorted position:
+      // finalize tests the previous list's membership in the new one without searching
+      if (rec.qf & QF_RES) out.prev_pos[rec._pad] = (unsigned long long)seqno << 32 | cnt;
       if (lists) {
         // Alg. 1 l.32-39 for this key alone: kvb >= 1 makes the inclusive prefix strictly
         // increasing, so "count <= BS and sum kvb <= P" holds exactly on a prefix of the order
@@ -1001,7 +1017,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   // R items per thread, blocked (i = tid * R + r): NT * R >= BS
   uint32_t c_s[R], c_qf[R], c_tok[R], c_ex[R], c_mt[R], c_qt[R], c_kvb[R];
   uint64_t c_cid[R];
-  uint32_t p_s[R], p_qf[R], p_held[R];  // previous batch: slot, flags, held blocks, order key
+  uint32_t p_s[R], p_qf[R], p_held[R];  // previous resident list: slot, flags, blocks to swap out, key
   uint64_t p_cid[R], p_key[R];
   unsigned long long p_pos[R];           // seqno << 32 | sorted position (k_rank), if use_prev_pos
   unsigned long long my_kv = 0;
@@ -1042,7 +1058,9 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         p_qf[r] = pr[r].qf;
         p_cid[r] = pr[r].cid;
         p_key[r] = cand_key(pr[r], t);
-        p_held[r] = blocks_for(pol, pr[r].tok + pr[r].exec);  // R28
+        // R28: a resident call holds ceil((input + exec) / bt) blocks; one that never ran has no
+        // KV content and nothing to swap out (R32: standby calls)
+        p_held[r] = pr[r].exec > 0 ? blocks_for(pol, pr[r].tok + pr[r].exec) : 0u;
       }
     }
   }
@@ -1075,22 +1093,24 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     }
   }
   __syncthreads();
-  const uint32_t n_batch = s_nbatch;
+  // the resident set (R32: <= BS + X calls) and the batch, its first BS calls (n_res when X = 0)
+  const uint32_t n_res = s_nbatch;
+  const uint32_t n_batch = min(n_res, pol.run_batch);
   STAMP(3);
-  if (tid == 0 && ncand > 0 && n_batch == 0) {
+  if (tid == 0 && ncand > 0 && n_res == 0) {
     if (atomicCAS(&ctl->err, 0u, (uint32_t)AUTX_E_NOMEM) == 0u)
       ctl->err_info = (uint32_t)((lists ? out.skey[0] : uk[0]) & 0x7FFFFFFF);
   }
   // ---- (4) batch list and admit = batch calls not resident (batch order) -------------------
   unsigned long long my_ad = 0;
-  if (n_batch == 0 && tid == 0) s_kvsum = 0;
+  if (n_res == 0 && tid == 0) s_kvsum = 0;
   if (lists && tid == 0) s_kvsum = a_kv;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     uint32_t i = tid * R + r;
     if (lists) break;  // (k_rank wrote the lists)
-    if (i + 1 == n_batch) s_kvsum = c_incl[r];  // sum kvb over the batch (read after the scans below)
-    if (i < n_batch) {
+    if (i + 1 == n_res) s_kvsum = c_incl[r];  // sum kvb over the resident set (read after the scans below)
+    if (i < n_res) {
       out.batch_slots[i] = c_s[r];
       out.batch_ids[i] = c_cid[r];
       if (!(c_qf[r] & QF_RES)) {
@@ -1107,7 +1127,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       uint32_t i = tid * R + r;
-      if (i < n_batch && !(c_qf[r] & QF_RES)) {
+      if (i < n_res && !(c_qf[r] & QF_RES)) {
         out.admit_ids[pos] = c_cid[r];
         s_ad[pos] = c_cid[r];
         out.admit_slots[pos] = c_s[r];
@@ -1133,21 +1153,21 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
 #pragma unroll
       for (int r = 0; r < R; ++r) pos[r] = (uint32_t)(p_pos[r] >> 32) == seqno ? (uint32_t)p_pos[r] : NONE;
     } else {
-      for (uint32_t step = 1u << 12; step > 0; step >>= 1) {  // n_batch <= 4096
+      for (uint32_t step = 1u << 12; step > 0; step >>= 1) {  // n_res <= 4096
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const uint32_t probe = pos[r] + step;
-          if (probe <= n_batch && uk[probe - 1] < p_key[r]) pos[r] = probe;  // pos = #keys < key
+          if (probe <= n_res && uk[probe - 1] < p_key[r]) pos[r] = probe;  // pos = #keys < key
         }
       }
 #pragma unroll
-      for (int r = 0; r < R; ++r) pos[r] = pos[r] < n_batch && uk[pos[r]] == p_key[r] ? pos[r] : NONE;
+      for (int r = 0; r < R; ++r) pos[r] = pos[r] < n_res && uk[pos[r]] == p_key[r] ? pos[r] : NONE;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t i = tid * R + r;
       if (i < n_prev && !(p_qf[r] & QF_DEAD)) {
-        const bool in = pos[r] < n_batch;
+        const bool in = pos[r] < n_res;
         if (!in) {
           is_pre |= 1u << r;
           my_pre += (1ull << 44) | p_held[r];
@@ -1165,7 +1185,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         out.preempt_ids[pos] = p_cid[r];
         s_pr[pos] = p_cid[r];
         out.preempt_slots[pos] = p_s[r];
-        ct.qf[p_s[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES | QF_INB));
+        ct.qf[p_s[r]] = (uint8_t)(p_qf[r] & ~(QF_RUN | QF_RES));
         ++pos;
       }
   }
@@ -1178,38 +1198,44 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   // ---- KV blocks: swap plan + allocation (a7) --------------------------------------------------
   if (kv_on) {
     const uint32_t W = pol.max_blocks_per_call;
-    // (1) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots
-    uint32_t base_blk = 0, base_free = 0;
+    // (1) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots.
+    // A call that never ran (R32 standby) has no KV content: its blocks are freed, not swapped.
+    uint32_t base_blk = 0, base_free = 0, base_plan = 0, base_items = 0;
     const uint32_t top0 = ctl->free_top, rtop0 = ctl->rs_free_top;
     for (uint32_t c0 = 0; c0 < n_preempt; c0 += NT) {
       uint32_t i = c0 + tid;
-      uint32_t s = 0, rslot = 0, nb = 0;
+      uint32_t s = 0, rslot = 0, nb = 0, ns = 0;
       if (i < n_preempt) {
         s = out.preempt_slots[i];
         rslot = ct.loc[s];
         nb = kv.rs_nblk[rslot];
+        ns = ct.exec[s] > 0 ? nb : 0u;
       }
-      uint32_t tot;
+      uint32_t tot, ptot, itot;
       uint32_t boff = base_blk + block_excl_scan<uint32_t, NT>(nb, red, &tot);
+      uint32_t poff = base_plan + block_excl_scan<uint32_t, NT>(ns, red, &ptot);
+      uint32_t ioff = base_items + block_excl_scan<uint32_t, NT>(ns ? 1u : 0u, red, &itot);
       if (i < n_preempt) {
-        uint32_t cls = ceil_log2(nb);
-        // pop a page range of 2^cls pages from the class stack, else bump-allocate
-        uint32_t page;
-        uint32_t k = atomicSub(&ctl->host_free_top[cls], 1u);
-        if ((int32_t)k > 0) {
-          page = kv.host_free[(size_t)cls * kv.host_free_cap + k - 1];
-        } else {
-          atomicAdd(&ctl->host_free_top[cls], 1u);
-          page = atomicAdd(&ctl->host_bump, 1u << cls);
-          if ((uint64_t)page + (1u << cls) > pol.host_pages_lo) set_err(ctl, AUTX_E_NOMEM, 1);
+        uint32_t page = NONE, cls = 0;
+        if (ns) {
+          cls = ceil_log2(ns);
+          // pop a page range of 2^cls pages from the class stack, else bump-allocate
+          uint32_t k = atomicSub(&ctl->host_free_top[cls], 1u);
+          if ((int32_t)k > 0) {
+            page = kv.host_free[(size_t)cls * kv.host_free_cap + k - 1];
+          } else {
+            atomicAdd(&ctl->host_free_top[cls], 1u);
+            page = atomicAdd(&ctl->host_bump, 1u << cls);
+            if ((uint64_t)page + (1u << cls) > pol.host_pages_lo) set_err(ctl, AUTX_E_NOMEM, 1);
+          }
+          kv.plan_out[ioff] = PlanItem{page, ns, poff};
         }
         ct.loc[s] = page;
         ct.hcls[s] = cls;
-        kv.plan_out[i] = PlanItem{page, nb, boff};
         const uint32_t* src = kv.rs_blocks + (size_t)rslot * W;
         for (uint32_t j = 0; j < nb; ++j) {
           uint32_t b = src[j];
-          kv.plan_out_blocks[boff + j] = b;
+          if (j < ns) kv.plan_out_blocks[poff + j] = b;
           kv.free_stack[top0 + boff + j] = b;
         }
         kv.rs_nblk[rslot] = 0;
@@ -1219,18 +1245,21 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       if (i < n_preempt) kv.rs_free[rtop0 + roff] = rslot;
       base_blk += tot;
       base_free += rt;
+      base_plan += ptot;
+      base_items += itot;
     }
     __syncthreads();
     uint32_t top = top0 + base_blk, rtop = rtop0 + base_free;
-    // (2) batch calls: grow/allocate to kvb; admitted calls take a resident slot
+    // (2) resident calls: the batch grows/allocates to kvb (the next token's block), standby
+    // calls (R32) to the blocks of their existing KV; admitted calls take a resident slot
     uint32_t pop_base = 0, rs_pop = 0, in_blk = 0, in_items = 0;
-    for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
+    for (uint32_t c0 = 0; c0 < n_res; c0 += NT) {
       uint32_t i = c0 + tid;
       uint32_t s = 0, need = 0, have = 0, rslot = NONE, admit = 0, held = 0;
-      if (i < n_batch) {
+      if (i < n_res) {
         s = (uint32_t)(uk[i] & 0x7FFFFFFFu);
         uint32_t qf = ct.qf[s];
-        need = ceil_div_u32(ct.tok[s] + ct.exec[s] + 1, pol.block_tokens);
+        need = ceil_div_u32(ct.tok[s] + ct.exec[s] + (i < n_batch ? 1u : 0u), pol.block_tokens);
         if (need > W) set_err(ctl, AUTX_E_NOMEM, 2);
         if (qf & QF_RES) {
           rslot = ct.loc[s];
@@ -1240,13 +1269,14 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
           if (ct.exec[s] > 0) held = ceil_div_u32(ct.tok[s] + ct.exec[s], pol.block_tokens);
         }
       }
-      uint32_t alloc = need > have ? need - have : 0;
+      need = max(need, have);
+      uint32_t alloc = need - have;
       uint32_t tot, rt, ht, it;
       uint32_t aoff = pop_base + block_excl_scan<uint32_t, NT>(alloc, red, &tot);
       uint32_t roff = rs_pop + block_excl_scan<uint32_t, NT>(admit, red, &rt);
       uint32_t hoff = in_blk + block_excl_scan<uint32_t, NT>(held, red, &ht);
       uint32_t ioff = in_items + block_excl_scan<uint32_t, NT>(held ? 1u : 0u, red, &it);
-      if (i < n_batch) {
+      if (i < n_res) {
         if (admit) {
           if (roff >= rtop) set_err(ctl, AUTX_E_NOMEM, 3);
           rslot = kv.rs_free[rtop - 1 - roff];
@@ -1271,7 +1301,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     }
     __syncthreads();
     // (3) free the host ranges of swapped-in calls (after this step's swap-out allocations)
-    for (uint32_t c0 = 0; c0 < n_batch; c0 += NT) {
+    for (uint32_t c0 = 0; c0 < n_res; c0 += NT) {
       uint32_t i = c0 + tid;
       if (i < in_items) {
         PlanItem it = kv.plan_in[i];
@@ -1299,9 +1329,9 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       kv.bt_offsets[n_batch] = b0;
       ctl->free_top = top - pop_base;
       ctl->rs_free_top = rtop - rs_pop;
-      ctl->n_plan_out = n_preempt;
+      ctl->n_plan_out = base_items;
       ctl->n_plan_in = in_items;
-      ctl->plan_out_chunks = base_blk;
+      ctl->plan_out_chunks = base_plan;
       ctl->plan_in_chunks = in_blk;
     }
     __syncthreads();
@@ -1314,27 +1344,39 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     uint32_t i = tid * R + r;
     if (!lists && i < n_batch) {
       uint32_t sl = c_s[r];
-      uint32_t q = c_qf[r] & QF_QMASK;
+      uint32_t q = c_qf[r] & QF_QMASK, dem = c_qf[r] & QF_DEM;
       ct.exec[sl] = c_ex[r] + 1;
       ct.mtime[sl] = c_mt[r] + 1;
       uint32_t qt = c_qt[r];
       if (qt != AUTX_INF) {
-        qt -= 1;
+        if (qt > 0) qt -= 1;
         if (qt == 0) {
-          q = min(q + 1, pol.K - 1);
-          qt = pol.quanta[q];
+          if (pol.multistep) {
+            dem = QF_DEM;  // R32: demoted at the next scheduling point
+          } else {
+            q = min(q + 1, pol.K - 1);
+            qt = pol.quanta[q];
+          }
         }
         ct.quanta[sl] = qt;
       }
-      ct.qf[sl] = (uint8_t)(q | QF_RUN | QF_RES);
+      ct.qf[sl] = (uint8_t)(q | dem | QF_RUN | QF_RES);
+      ct.bidx[sl] = i;
+      out.prev_slots[i] = sl;
+    } else if (!lists && i < n_res) {
+      // R32 standby: resident, not running (waits implicitly via the closed-form counters)
+      const uint32_t sl = c_s[r];
+      ct.qf[sl] = (uint8_t)((c_qf[r] & (QF_QMASK | QF_DEM)) | QF_RES);
       ct.bidx[sl] = i;
       out.prev_slots[i] = sl;
     }
   }
   if (tid == 0) {
-    ctl->n_prev = n_batch;
+    ctl->n_prev = n_res;
     HostOut h;
     h.n_batch = n_batch;
+    h.n_standby = n_res - n_batch;
+    h._pad = 0;
     h.n_admit = n_admit;
     h.n_preempt = n_preempt;
     h.n_active = c_live;
@@ -1366,7 +1408,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   if (!out.zero_copy) {
     if (tid == 0) *out.d_hout = s_hout;
   } else {
-    const uint32_t nb = s_hout.n_batch, na = s_hout.n_admit, np_ = s_hout.n_preempt;
+    const uint32_t nb = s_hout.n_batch + s_hout.n_standby, na = s_hout.n_admit, np_ = s_hout.n_preempt;
     // 16-B posted stores over PCIe: batch ids straight from registers (a thread's R blocked
     // items are R/2 consecutive words), admit/preempt ids from their shared-memory copies
     static_assert(R % 2 == 0, "blocked items pair into 16-B words");
@@ -1464,6 +1506,57 @@ static uint32_t pow2_at_least(uint32_t x) {
   return p;
 }
 
+// R32 window step (multi-step scheduling): no ordering.  The candidates are the previous
+// resident list (batch, then standby), in its order, without the calls that completed (the
+// prologue marked them DEAD); finalize then cuts it under the KV budget exactly as a scheduling
+// point's sorted candidates (the first misfit stops: lazy eviction of the tail), splits batch /
+// standby and accounts.  One CTA: the list holds <= BS + X <= 2048 calls.
+constexpr int WIN_THREADS = 1024;
+__global__ void __launch_bounds__(WIN_THREADS) k_window(Policy pol, CallTable ct, Ctl* ctl, Outputs out) {
+  __shared__ uint32_t red_w[33];
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t t = ctl->s_t, seqno = ctl->s_seqno, n_prev = ctl->n_prev;
+  CHAIN_BEGIN(3);
+  constexpr int R = 2;  // 2 x 1024 >= MAX_BATCH
+  CandRec rc[R];
+  uint32_t live[R], nl = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t j = threadIdx.x * R + r;  // blocked: the list order is kept by the scan below
+    live[r] = 0;
+    if (j < n_prev) {
+      load_rec(ct, out.prev_slots[j], &rc[r]);
+      live[r] = !(rc[r].qf & QF_DEAD);
+      nl += live[r];
+    }
+  }
+  uint32_t n_live;
+  uint32_t pos = block_excl_scan<uint32_t, WIN_THREADS>(nl, red_w, &n_live);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t j = threadIdx.x * R + r;
+    if (j < n_prev) {
+      out.prev_rec[j] = rc[r];
+      if (live[r]) {
+        out.srec[pos] = rc[r];
+        out.skey[pos] = cand_key(rc[r], t);  // finalize reads the slot from the low bits
+        out.prev_pos[j] = (unsigned long long)seqno << 32 | pos;
+        ++pos;
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    ctl->n_cand_a = n_live;
+    ctl->n_cand_b = 0;
+    ctl->n_live = ctl->s_n_active;
+    ctl->n_promoted = 0;
+    ctl->qstar = pol.K;
+    ctl->mprime = 0;
+  }
+  CHAIN_END(3);
+}
+
 // Dynamic shared memory above 48 KB is a per-device function attribute: set for the current device
 // (autx_create calls this after cudaSetDevice, once per context).
 cudaError_t step_kernels_setup() {
@@ -1480,13 +1573,32 @@ cudaError_t step_kernels_setup() {
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev, const RadixState* rx, uint32_t arr_base,
-                        uint32_t* radix_passes) {
+                        uint32_t* radix_passes, bool window) {
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
   out.use_prev_pos = rx ? 0u : 1u;  // k_rank publishes previous-batch positions (select mode)
   static const bool rank_narrow = getenv("AUTX_RANK_NARROW") != nullptr;
   out.rank_wide = rank_narrow ? 0u : 1u;  // k_rank may use a warp per key when candidates are few
   if (ev) cudaEventRecord(ev[0], s);
+  uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
+  // sorted keys [np] + admit and preempt id staging [2 x even(BS)]
+  const size_t fin_smem_bytes = ((size_t)np + 2 * ((pol.max_batch + 1) & ~1u)) * sizeof(uint64_t);
+  static const bool fin_lists = getenv("AUTX_FINALIZE_LISTS") != nullptr;
+  // R32 (standby calls, deferred demotion): the finalize decides the batch
+  const bool r32 = pol.run_batch != pol.max_batch || pol.multistep;
+  if (window) {
+    // R32 window step: the carried resident list instead of scan, selection and ordering
+    out.rank_lists = 0;
+    if (ev) cudaEventRecord(ev[1], s);
+    launch_pdl(k_window, 1, WIN_THREADS, 0, s, pol, ct, ctl, out);
+    if (ev) cudaEventRecord(ev[2], s);
+    if (pol.max_batch <= 1024)
+      launch_pdl(k_finalize<512, 2>, 1, 512, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, np);
+    else
+      launch_pdl(k_finalize<FIN_THREADS, 4>, 1, FIN_THREADS, fin_smem_bytes, s, pol, ct, ctl, out, kv, kv_on, np);
+    if (ev) cudaEventRecord(ev[3], s);
+    return cudaGetLastError();
+  }
   if (rx) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pol.device);
@@ -1501,13 +1613,9 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
     launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out);
   }
-  uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
-  // sorted keys [np] + admit and preempt id staging [2 x even(BS)]
-  const size_t fin_smem_bytes = ((size_t)np + 2 * ((pol.max_batch + 1) & ~1u)) * sizeof(uint64_t);
   // k_rank also decides the batch (lists, accounting) when there is no KV allocator and its keys
   // + kvb fit shared memory; else the finalize does (AUTX_FINALIZE_LISTS forces the latter)
-  static const bool fin_lists = getenv("AUTX_FINALIZE_LISTS") != nullptr;
-  out.rank_lists = (!kv_on && !rx && pol.max_batch <= 1024 && !fin_lists) ? 1u : 0u;
+  out.rank_lists = (!kv_on && !rx && pol.max_batch <= 1024 && !fin_lists && !r32) ? 1u : 0u;
   // k_rank's layout: rk, ck (u64) and ci, rkv, ckv (u32) per key, 2 BS keys (rkv / ckv are
   // written even when rank_lists is off)
   size_t rank_smem = std::max<size_t>((size_t)2 * pol.max_batch * (2 * sizeof(uint64_t) + 3 * sizeof(uint32_t)),

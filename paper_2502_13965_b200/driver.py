@@ -149,6 +149,8 @@ class TraceDriver:
         if self.log_lists:
             rec.update(batch=[int(x) for x in batch], admit=[int(x) for x in admit],
                        preempt=[int(x) for x in preempt])
+            if getattr(out, "n_standby", 0):   # R32 over-provisioned resident calls
+                rec["standby"] = [int(x) for x in s.standby()]
         self.log.append(rec)
         bi = self.idx_of(batch)
         self.remaining[bi] -= 1
