@@ -162,6 +162,7 @@ typedef struct {
   uint64_t bytes_d2h, bytes_h2d;  /* bytes moved over the host link by this call               */
   uint32_t chunks_d2h, chunks_h2d;
   float ms;                       /* device time of the swap (CUDA events), valid after return */
+  uint32_t duplex;                /* 1: swap-out and swap-in ran at the same time (full duplex)  */
 } autx_swap_stats;
 
 /* ---- lifecycle -------------------------------------------------------------------------- */
@@ -203,8 +204,12 @@ autx_status autx_step_wait(autx_ctx* ctx, autx_step_out* out);  /* waits for out
 
 /* ---- KV swap (a7) --------------------------------------------------------------------- */
 /* Executes the last step's swap plan: swap-out (GPU blocks -> host arena) of every preempted
- * call, then swap-in (host arena -> newly allocated GPU blocks) of every admitted call with a
- * host copy.  Requires n_gpu_blocks > 0. */
+ * call and swap-in (host arena -> newly allocated GPU blocks) of every admitted call with a
+ * host copy.  The two directions run at the same time (full duplex: both halves of the host
+ * link; SM mode one kernel, staged-DMA mode a second stream) unless a swap-in target block was
+ * freed by this step's swap-out — the allocator hands out blocks freed in earlier steps first,
+ * so that only happens when the pool runs short — then swap-out runs first.  Requires
+ * n_gpu_blocks > 0. */
 autx_status autx_kv_swap(autx_ctx* ctx, const autx_kv_layout* layout, int32_t mode,
                          autx_swap_stats* stats);
 /* Block table of the last batch as CSR: d_offsets[n_batch+1], d_blocks[...] (device pointers,

@@ -59,7 +59,7 @@ class KvLayout(C.Structure):
 
 class SwapStats(C.Structure):
     _fields_ = [("bytes_d2h", C.c_uint64), ("bytes_h2d", C.c_uint64), ("chunks_d2h", C.c_uint32),
-                ("chunks_h2d", C.c_uint32), ("ms", C.c_float)]
+                ("chunks_h2d", C.c_uint32), ("ms", C.c_float), ("duplex", C.c_uint32)]
 
 
 class StepTiming(C.Structure):
@@ -282,7 +282,7 @@ class Scheduler:
         o = self.out
         return self._views[0][o.n_batch:o.n_batch + o.n_standby].copy()
 
-    def kv_swap(self, k_ptrs, v_ptrs, chunk_bytes, host_ptr, host_bytes, mode=SWAP_SM):
+    def kv_swap(self, k_ptrs, v_ptrs, chunk_bytes, host_ptr, host_bytes, mode=SWAP_STAGED_DMA):
         L = len(k_ptrs)
         kp = (C.c_void_p * L)(*k_ptrs)
         vp = (C.c_void_p * L)(*v_ptrs)

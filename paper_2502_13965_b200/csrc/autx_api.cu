@@ -83,8 +83,13 @@ struct autx_ctx {
   void** d_pools = nullptr;  // [2 * n_layers]
   uint32_t pools_cap = 0;
   void** h_pools = nullptr;
-  char* staging = nullptr;
+  char* staging = nullptr;          // swap-out staging (staged DMA mode)
   size_t staging_bytes = 0;
+  char* staging_in = nullptr;       // swap-in staging: its own buffer, so the legs overlap
+  size_t staging_in_bytes = 0;
+  cudaStream_t stream_in = nullptr; // the swap-in leg's stream (full duplex, staged DMA mode)
+  cudaEvent_t sev_in[2] = {};
+  bool last_swap_duplex = false;
   cudaEvent_t sev[2] = {};
   char* d_outblk = nullptr;  // [counts | batch | admit | preempt] on the device
   char* h_outblk = nullptr;  // pinned mirror
@@ -423,6 +428,9 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   if (ctx->done) cudaEventDestroy(ctx->done);
   for (auto& e : ctx->ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->sev) if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->sev_in) if (e) cudaEventDestroy(e);
+  if (ctx->stream_in) cudaStreamDestroy(ctx->stream_in);
+  if (ctx->staging_in) cudaFree(ctx->staging_in);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return AUTX_OK;
@@ -1080,9 +1088,19 @@ extern "C" autx_status autx_kv_swap(autx_ctx* ctx, const autx_kv_layout* L, int3
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->device);
   CK(cudaEventRecord(ctx->sev[0], ctx->stream));
+  // full duplex: both directions at once unless a swap-in target block was freed by this step's
+  // swap-out (the allocator avoids that while older free blocks last; ctl->swap_serial)
+  // (the per-chunk comparator stays vLLM's: one stream, one copy at a time)
+  const bool duplex = c.plan_out_chunks && c.plan_in_chunks && !c.swap_serial && mode != AUTX_SWAP_PER_CHUNK_MEMCPY &&
+                      !getenv("AUTX_SWAP_HALF_DUPLEX");
+  ctx->last_swap_duplex = duplex;
   if (mode == AUTX_SWAP_SM) {
-    if (c.plan_out_chunks) CK(launch_swap(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, arena, 0, dev_sms * 4));
-    if (c.plan_in_chunks) CK(launch_swap(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, arena, 1, dev_sms * 4));
+    if (duplex) {
+      CK(launch_swap(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, arena, 2, dev_sms * 8));
+    } else {
+      if (c.plan_out_chunks) CK(launch_swap(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, arena, 0, dev_sms * 4));
+      if (c.plan_in_chunks) CK(launch_swap(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, arena, 1, dev_sms * 4));
+    }
   } else if (mode == AUTX_SWAP_PER_CHUNK_MEMCPY || mode == AUTX_SWAP_STAGED_DMA) {
     // both comparators need the plan on the host
     std::vector<PlanItem> po(c.n_plan_out), pi(c.n_plan_in);
@@ -1111,13 +1129,35 @@ extern "C" autx_status autx_kv_swap(autx_ctx* ctx, const autx_kv_layout* L, int3
     } else {
       // the paper's scheme: gather into a contiguous buffer, one bulk transfer
       // per call
-      size_t need = (size_t)std::max(c.plan_out_chunks, c.plan_in_chunks) * page;
-      if (need > ctx->staging_bytes) {
-        if (ctx->staging) cudaFree(ctx->staging);
-        ctx->staging = nullptr;
-        CK(cudaMalloc((void**)&ctx->staging, need));
-        ctx->staging_bytes = need;
-        CK(cudaEventRecord(ctx->sev[0], ctx->stream));
+      auto grow = [&](char** buf, size_t* have, size_t need) -> cudaError_t {
+        if (need <= *have) return cudaSuccess;
+        if (*buf) cudaFree(*buf);
+        *buf = nullptr;
+        *have = 0;
+        cudaError_t e = cudaMalloc((void**)buf, need);
+        if (e == cudaSuccess) *have = need;
+        return e;
+      };
+      const size_t need_out = (size_t)c.plan_out_chunks * page, need_in = (size_t)c.plan_in_chunks * page;
+      if (need_out > ctx->staging_bytes || need_in > (duplex ? ctx->staging_in_bytes : ctx->staging_bytes)) {
+        CK(grow(&ctx->staging, &ctx->staging_bytes, duplex ? need_out : std::max(need_out, need_in)));
+        if (duplex) CK(grow(&ctx->staging_in, &ctx->staging_in_bytes, need_in));
+        CK(cudaEventRecord(ctx->sev[0], ctx->stream));  // (allocations synchronise: time from here)
+      }
+      // swap-in leg: on its own stream when the directions may overlap (both copy engines and
+      // both link directions busy at once), after everything before this call on ctx->stream
+      cudaStream_t sin = ctx->stream;
+      char* st_in = ctx->staging;
+      if (duplex) {
+        if (!ctx->stream_in) {
+          CK(cudaStreamCreateWithFlags(&ctx->stream_in, cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&ctx->sev_in[0], cudaEventDisableTiming));
+          CK(cudaEventCreateWithFlags(&ctx->sev_in[1], cudaEventDisableTiming));
+        }
+        CK(cudaEventRecord(ctx->sev_in[0], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->stream_in, ctx->sev_in[0], 0));
+        sin = ctx->stream_in;
+        st_in = ctx->staging_in;
       }
       if (c.plan_out_chunks) {
         CK(launch_stage(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, ctx->staging, 0, dev_sms * 4));
@@ -1127,9 +1167,13 @@ extern "C" autx_status autx_kv_swap(autx_ctx* ctx, const autx_kv_layout* L, int3
       }
       if (c.plan_in_chunks) {
         for (auto& it : pi)
-          CK(cudaMemcpyAsync(ctx->staging + (uint64_t)it.blk_off * page, arena + it.host_page * page,
-                             (uint64_t)it.nblk * page, cudaMemcpyHostToDevice, ctx->stream));
-        CK(launch_stage(ctx->stream, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, ctx->staging, 1, dev_sms * 4));
+          CK(cudaMemcpyAsync(st_in + (uint64_t)it.blk_off * page, arena + it.host_page * page,
+                             (uint64_t)it.nblk * page, cudaMemcpyHostToDevice, sin));
+        CK(launch_stage(sin, ctx->ctl, ctx->kv, kp, vp, L->n_layers, L->chunk_bytes, st_in, 1, dev_sms * 4));
+      }
+      if (duplex) {
+        CK(cudaEventRecord(ctx->sev_in[1], sin));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->sev_in[1], 0));
       }
     }
   } else {
@@ -1138,6 +1182,7 @@ extern "C" autx_status autx_kv_swap(autx_ctx* ctx, const autx_kv_layout* L, int3
   CK(cudaEventRecord(ctx->sev[1], ctx->stream));
   CK(cudaEventSynchronize(ctx->sev[1]));
   CK(cudaEventElapsedTime(&stats->ms, ctx->sev[0], ctx->sev[1]));
+  stats->duplex = ctx->last_swap_duplex ? 1u : 0u;
   return AUTX_OK;
 }
 

@@ -98,6 +98,8 @@ struct Ctl {
   uint32_t err;        // sticky device error code (autx_status)
   uint32_t err_info;
   uint32_t n_plan_out, n_plan_in;   // swap plan items
+  uint32_t swap_serial;             // a swap-in target block was freed by this step's swap-out:
+                                    // the directions must run one after the other
   uint32_t plan_out_chunks, plan_in_chunks;
   // allocator state
   uint32_t free_top;       // GPU block free stack size

@@ -1283,8 +1283,13 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         }
         if (aoff + alloc > top) set_err(ctl, AUTX_E_NOMEM, 4);
         uint32_t* dst = kv.rs_blocks + (size_t)rslot * W;
-        for (uint32_t j = 0; j < alloc && have + j < W && aoff + j < top; ++j)
-          dst[have + j] = kv.free_stack[top - 1 - aoff - j];
+        // pops take the blocks freed by earlier steps first (stack [0, top0)), and this step's
+        // swap-outs' blocks [top0, top) only when those run out: a swap-in then never writes a
+        // block this step's swap-out still reads, so the two directions can run at once
+        for (uint32_t j = 0; j < alloc && have + j < W && aoff + j < top; ++j) {
+          const uint32_t k = aoff + j;
+          dst[have + j] = k < top0 ? kv.free_stack[top0 - 1 - k] : kv.free_stack[top - 1 - (k - top0)];
+        }
         kv.rs_nblk[rslot] = need;
         if (held) {
           // swap-in: host copy -> the first `held` blocks of the new list; free host pages after
@@ -1300,6 +1305,21 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       in_items += it;
     }
     __syncthreads();
+    {
+      // the stack after the pops: the older blocks left, then this step's freed blocks left
+      const uint32_t pops_old = min(pop_base, top0), pops_new = pop_base - pops_old;
+      const uint32_t nkeep = base_blk > pops_new ? base_blk - pops_new : 0u, dst0 = top0 - pops_old;
+      if (dst0 != top0) {
+        for (uint32_t c0 = 0; c0 < nkeep; c0 += NT) {  // downward move, chunk by chunk (reads first)
+          const uint32_t i = c0 + tid;
+          const uint32_t v = i < nkeep ? kv.free_stack[top0 + i] : 0u;
+          __syncthreads();
+          if (i < nkeep) kv.free_stack[dst0 + i] = v;
+          __syncthreads();
+        }
+      }
+      if (tid == 0) ctl->swap_serial = pops_new > 0 ? 1u : 0u;
+    }
     // (3) free the host ranges of swapped-in calls (after this step's swap-out allocations)
     for (uint32_t c0 = 0; c0 < n_res; c0 += NT) {
       uint32_t i = c0 + tid;

@@ -48,17 +48,24 @@ __device__ __forceinline__ void copy_chunk(uint4* __restrict__ dst, const uint4*
   }
 }
 
-// direction 0: swap-out (pool -> host arena); 1: swap-in (host arena -> pool)
+// direction 0: swap-out (pool -> host arena); 1: swap-in (host arena -> pool); 2: both at once
+// (full duplex over the host link): even CTAs swap out, odd CTAs swap in
 __global__ void __launch_bounds__(256) k_swap_sm(const Ctl* ctl, KvState kv, void* const* kpool,
                                                  void* const* vpool, SwapGeom g, char* arena,
                                                  int direction) {
+  uint32_t cta = blockIdx.x, ncta = gridDim.x;
+  if (direction == 2) {
+    direction = (int)(blockIdx.x & 1u);
+    cta = blockIdx.x >> 1;
+    ncta = (gridDim.x + 1 - (uint32_t)direction) >> 1;
+  }
   const uint32_t n_items = direction == 0 ? ctl->n_plan_out : ctl->n_plan_in;
   const uint32_t n_blocks = direction == 0 ? ctl->plan_out_chunks : ctl->plan_in_chunks;
   const PlanItem* items = direction == 0 ? kv.plan_out : kv.plan_in;
   const uint32_t* blocks = direction == 0 ? kv.plan_out_blocks : kv.plan_in_blocks;
   const uint64_t n_chunks = (uint64_t)n_blocks * g.n_layers * 2;
   const uint32_t n16 = g.chunk_bytes / 16;
-  for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+  for (uint64_t c = cta; c < n_chunks; c += ncta) {
     uint32_t b = (uint32_t)(c / (2 * g.n_layers));
     uint32_t rem = (uint32_t)(c % (2 * g.n_layers));
     uint32_t l = rem >> 1, kvsel = rem & 1;

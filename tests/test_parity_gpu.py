@@ -331,17 +331,19 @@ def test_protocol_errors():
     s.close()
 
 
-@pytest.mark.parametrize("mode", [0, 2, 1])
-def test_kv_swap_round_trip_bytes(mode):
+@pytest.mark.parametrize("mode,pool", [(0, 1), (2, 1), (1, 1), (0, 2), (2, 2)])
+def test_kv_swap_round_trip_bytes(mode, pool):
     """Swap-out then swap-in through the C ABI moves exactly the oracle's blocks and restores
     every preempted call's KV contents byte for byte, possibly into other GPU blocks.  Modes:
-    0 SM-driven copy, 2 staged DMA (the paper's scheme), 1 per-chunk cudaMemcpyAsync (vLLM)."""
+    0 SM-driven copy, 2 staged DMA (the paper's scheme), 1 per-chunk cudaMemcpyAsync (vLLM).
+    pool = 2: a block pool twice the budget, where swap-ins take blocks freed by earlier steps and
+    the two directions run at the same time (full duplex) on most steps."""
     import torch
     from paper_2502_13965_b200 import TraceDriver
     tr = chatbot(120)
     L, chunk = 2, 1024
     P = 2400
-    nblk = P
+    nblk = pool * P
     cfg = spec_ladder_config(PLAS, max_batch=16, kv_budget=P)
     want, _ = oracle_records(tr, cfg)
     s = make_sched(spec_ladder_config(PLAS, max_batch=16, kv_budget=P), n_gpu_blocks=nblk,
@@ -353,6 +355,7 @@ def test_kv_swap_round_trip_bytes(mode):
     written = {}   # call id -> number of leading blocks whose contents the "engine" wrote
     moved_out = moved_in = 0
     got = []
+    duplex = both = 0
 
     def pat(cid, j, l, kv):
         return (cid * 1000003 + j * 101 + l * 7 + kv) & 0x7FFFFFFF
@@ -367,6 +370,8 @@ def test_kv_swap_round_trip_bytes(mode):
         assert st.bytes_h2d == rec["swap_in_blocks"] * L * 2 * chunk
         moved_out += st.bytes_d2h
         moved_in += st.bytes_h2d
+        duplex += st.duplex
+        both += st.bytes_d2h > 0 and st.bytes_h2d > 0
         offs, blks = s.block_table_host()
         chk_idx, chk_val, new_idx, new_val = [], [], [], []
         for i, cid in enumerate(rec["batch"]):
@@ -392,6 +397,8 @@ def test_kv_swap_round_trip_bytes(mode):
     got = [g for g in got if g[1] or g[3]]
     assert_same(got, want)
     assert moved_out > 0 and moved_in > 0
+    if pool == 2 and mode != 1:
+        assert both > 0 and duplex >= both // 2, (duplex, both)
     s.close()
 
 
