@@ -555,7 +555,9 @@ def main():
         e2e_dec += rec["n_active"]
         h2d += 8 * nc + 24 * na               # completion (slot, program row) + arrival records
         d2h += 8 * (rec["n_batch"] + rec["n_admit"] + rec["n_preempt"]) + 4 * rec["n_batch"] + 48
-    s.close()
+    n_compact, compact_us = s.compaction_stats()
+    if world == 1:
+        s.close()
 
     n_active = decisions / args.steps / world
     n_programs = st["n_programs"]
@@ -611,7 +613,11 @@ def main():
                   "qstar": st["qstar"], "mprime": st["mprime"], "region_a": st["n_x"],
                   "region_b_mean": statistics.mean(x["n_b"] for x in stats),
                   "region_b_max": max(x["n_b"] for x in stats),
-                  "queue_occupancy": st["queue_counts"][:lad["K"]]},
+                  "queue_occupancy": st["queue_counts"][:lad["K"]],
+                  "compactions": dict(count=n_compact, host_us_total=round(compact_us, 1), steps=d.t,
+                                      note="G8 device compactions over the whole run (setup, fast-forward, "
+                                           "warm-up, timed and e2e steps); their kernels run inside "
+                                           "autx_register_call, so e2e includes them")},
         "e2e": {"value": e2e_dec / e2e_s, "unit": "decisions/s", "h2d_bytes_per_step": h2d // e2e_steps,
                 "d2h_bytes_per_step": d2h // e2e_steps, "ms_per_step": e2e_s * 1e3 / e2e_steps,
                 "timed": "wall clock inside the C-ABI calls (complete, end_program, register, sched_step, "

@@ -290,6 +290,10 @@ uint32_t autx_num_active(const autx_ctx* ctx);
  * wait) of chain kernel k (0 prologue, 1 scan, 2 select, 3 gather, 4 rank, 5 finalize; 0 = did
  * not run), [84, 85] = (ranked keys, key slots) of k_rank; copies min(cap, 96). */
 autx_status autx_phase_times(autx_ctx* ctx, uint64_t* ns, uint32_t cap);
+/* G8 stable compactions of the call table so far (device kernels into the other half of a double
+ * buffer; run inside autx_register_call when the table's tail reaches max_calls) and the host time
+ * they took (id-map remap), in microseconds. */
+autx_status autx_compaction_stats(const autx_ctx* ctx, uint64_t* n_compactions, double* host_us);
 /* Number of kernels this library has launched so far (all contexts of the process). */
 uint64_t autx_kernel_launches(void);
 

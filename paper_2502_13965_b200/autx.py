@@ -121,6 +121,7 @@ def load_library(path=LIB_PATH):
         "autx_num_active": ([P], u32),
         "autx_phase_times": ([P, P, u32], i32),
         "autx_kernel_launches": ([], u64),
+        "autx_compaction_stats": ([P, C.POINTER(u64), C.POINTER(C.c_double)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -137,7 +138,8 @@ def exported_symbols():
         "autx_step_wait", "autx_kv_swap", "autx_block_table", "autx_block_table_host", "autx_route_record_bytes",
         "autx_route_pack", "autx_route_apply", "autx_route", "autx_comm_unique_id", "autx_comm_init",
         "autx_comm_destroy", "autx_dump_calls", "autx_program_state",
-        "autx_last_step_timing", "autx_step_stats", "autx_set_timing", "autx_num_active", "autx_phase_times", "autx_kernel_launches"]
+        "autx_last_step_timing", "autx_step_stats", "autx_set_timing", "autx_num_active", "autx_phase_times", "autx_kernel_launches",
+        "autx_compaction_stats"]
 
 
 def kernel_launches():
@@ -275,6 +277,12 @@ class Scheduler:
             self._views = (f(o.h_batch), f(o.h_admit), f(o.h_preempt))
         vb, va, vp = self._views
         return vb[:o.n_batch].copy(), va[:o.n_admit].copy(), vp[:o.n_preempt].copy()
+
+    def compaction_stats(self):
+        """(number of G8 compactions so far, host microseconds they took)."""
+        n, us = C.c_uint64(), C.c_double()
+        self._check(self.lib.autx_compaction_stats(self.ctx, C.byref(n), C.byref(us)))
+        return int(n.value), float(us.value)
 
     def standby(self):
         """R32: the resident standby calls of the last waited step, in order (after the batch)."""

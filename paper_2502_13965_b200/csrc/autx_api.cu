@@ -34,6 +34,13 @@ struct autx_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   CallTable ct{};
+  CallTable ct2{};                 // the other half of the double-buffered call table (compaction)
+  size_t rows = 0;                 // call-table rows (max_calls padded to whole tiles)
+  uint32_t* d_tile_live = nullptr; // compaction: live rows per tile
+  uint32_t* d_old2new = nullptr;   // compaction: old row -> new row (NONE: dropped)
+  std::vector<uint32_t> h_old2new;
+  uint64_t n_compactions = 0;
+  double compact_host_us = 0;
   ProgTable pt{};
   Ctl* ctl = nullptr;
   Outputs out{};
@@ -186,15 +193,20 @@ extern "C" const char* autx_last_error(const autx_ctx* ctx) { return ctx ? ctx->
 static autx_status alloc_tables(autx_ctx* ctx) {
   const autx_config& c = ctx->cfg;
   size_t rows = ((size_t)c.max_calls + TILE - 1) / TILE * TILE;  // padded to whole tiles
-  CallTable& t = ctx->ct;
-  CK(dalloc(&t.cid, rows)); CK(dalloc(&t.prog, rows)); CK(dalloc(&t.arr, rows));
-  CK(dalloc(&t.qf, rows)); CK(dalloc(&t.base, rows)); CK(dalloc(&t.mtime, rows));
-  CK(dalloc(&t.exec, rows)); CK(dalloc(&t.quanta, rows)); CK(dalloc(&t.inh, rows));
-  CK(dalloc(&t.tok, rows)); CK(dalloc(&t.loc, rows)); CK(dalloc(&t.hcls, rows)); CK(dalloc(&t.bidx, rows));
-  CK(cudaMemsetAsync(t.qf, QF_DEAD, rows, ctx->stream));
-  CK(cudaMemsetAsync(t.prog, 0, rows * 4, ctx->stream));
-  CK(cudaMemsetAsync(t.base, 0, rows * 4, ctx->stream));
-  CK(cudaMemsetAsync(t.mtime, 0, rows * 4, ctx->stream));
+  ctx->rows = rows;
+  for (CallTable* tp : {&ctx->ct, &ctx->ct2}) {  // double buffer: compaction writes the other one
+    CallTable& t = *tp;
+    CK(dalloc(&t.cid, rows)); CK(dalloc(&t.prog, rows)); CK(dalloc(&t.arr, rows));
+    CK(dalloc(&t.qf, rows)); CK(dalloc(&t.base, rows)); CK(dalloc(&t.mtime, rows));
+    CK(dalloc(&t.exec, rows)); CK(dalloc(&t.quanta, rows)); CK(dalloc(&t.inh, rows));
+    CK(dalloc(&t.tok, rows)); CK(dalloc(&t.loc, rows)); CK(dalloc(&t.hcls, rows)); CK(dalloc(&t.bidx, rows));
+    CK(cudaMemsetAsync(t.qf, QF_DEAD, rows, ctx->stream));
+    CK(cudaMemsetAsync(t.prog, 0, rows * 4, ctx->stream));
+    CK(cudaMemsetAsync(t.base, 0, rows * 4, ctx->stream));
+    CK(cudaMemsetAsync(t.mtime, 0, rows * 4, ctx->stream));
+  }
+  CK(dalloc(&ctx->d_tile_live, rows / TILE + 1));
+  CK(dalloc(&ctx->d_old2new, rows));
   ProgTable& p = ctx->pt;
   size_t P = std::max<uint32_t>(c.max_programs, 1);
   CK(dalloc(&p.info, P)); CK(dalloc(&p.last_arr, P)); CK(dalloc(&p.last_comp, P));
@@ -405,9 +417,12 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
             g_hp.acc[3] / g_hp.n, g_hp.acc[4] / g_hp.n);
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  CallTable& t = ctx->ct;
-  void* dev[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok,
-                 t.loc, t.hcls, t.bidx, ctx->out.prev_pos, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
+  for (CallTable* tp : {&ctx->ct, &ctx->ct2}) {
+    CallTable& t = *tp;
+    void* cols[] = {t.cid, t.prog, t.arr, t.qf, t.base, t.mtime, t.exec, t.quanta, t.inh, t.tok, t.loc, t.hcls, t.bidx};
+    for (void* p : cols) if (p) cudaFree(p);
+  }
+  void* dev[] = {ctx->d_tile_live, ctx->d_old2new, ctx->out.prev_pos, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
                  ctx->ctl, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
                  ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.ckvb, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
@@ -979,72 +994,37 @@ extern "C" autx_status autx_step_wait(autx_ctx* ctx, autx_step_out* out) {
   return AUTX_OK;
 }
 
-// G8: stable compaction.  Live rows in table order are exactly the active calls sorted by row.
+// G8: stable compaction on the device into the other half of the double-buffered call table
+// (k_live_count, k_compact, k_remap_prev: no host sort, no allocation, no synchronisation).  The
+// host remaps its own id maps in parallel: a live row's new index is its rank among the live rows,
+// a prefix count over slot_live.
 static autx_status compact(autx_ctx* ctx) {
-  CK(cudaStreamSynchronize(ctx->stream));
-  std::vector<std::pair<uint32_t, uint64_t>> live;
-  live.reserve(ctx->call_slot.size());
-  for (auto& kv : ctx->call_slot) live.emplace_back(kv.second, kv.first);
-  std::sort(live.begin(), live.end());
-  uint32_t n = (uint32_t)live.size();
-  std::vector<uint32_t> lv(n), old2new(std::max<uint32_t>(ctx->tail, 1), NONE);
-  for (uint32_t i = 0; i < n; ++i) {
-    lv[i] = live[i].first;
-    old2new[lv[i]] = i;
+  const uint32_t n = (uint32_t)ctx->call_slot.size();
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(cudaMemsetAsync(ctx->ct2.qf, QF_DEAD, ctx->rows, ctx->stream));
+  CK(launch_compact(ctx->stream, ctx->ct, ctx->ct2, ctx->tail, n, ctx->d_tile_live, ctx->d_old2new, ctx->ctl,
+                    ctx->out.prev_slots));
+  std::swap(ctx->ct, ctx->ct2);
+  std::vector<uint32_t>& o2n = ctx->h_old2new;
+  o2n.resize(std::max<uint32_t>(ctx->tail, 1));
+  uint32_t k = 0;
+  for (uint32_t r = 0; r < ctx->tail; ++r) {
+    const bool live = ctx->slot_live[r];
+    o2n[r] = live ? k : NONE;
+    if (live) {
+      ctx->slot_prog[k] = ctx->slot_prog[r];
+      ctx->slot_arr[k] = ctx->slot_arr[r];
+      ctx->slot_live[k] = 1;
+      ++k;
+    }
   }
-  size_t rows = ((size_t)ctx->cfg.max_calls + TILE - 1) / TILE * TILE;
-  CallTable tmp{};
-  CK(dalloc(&tmp.cid, n)); CK(dalloc(&tmp.prog, n)); CK(dalloc(&tmp.arr, n)); CK(dalloc(&tmp.qf, n));
-  CK(dalloc(&tmp.base, n)); CK(dalloc(&tmp.mtime, n)); CK(dalloc(&tmp.exec, n));
-  CK(dalloc(&tmp.quanta, n)); CK(dalloc(&tmp.inh, n)); CK(dalloc(&tmp.tok, n)); CK(dalloc(&tmp.loc, n));
-  CK(dalloc(&tmp.hcls, n)); CK(dalloc(&tmp.bidx, n));
-  uint32_t *d_live = nullptr, *d_map = nullptr;
-  CK(dalloc(&d_live, n));
-  CK(dalloc(&d_map, old2new.size()));
-  CK(cudaMemcpyAsync(d_live, lv.data(), (size_t)n * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d_map, old2new.data(), old2new.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(launch_compact(ctx->stream, ctx->ct, tmp, d_live, n));
-  CallTable& t = ctx->ct;
-  auto cp = [&](void* dst, void* src, size_t bytes) { return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream); };
-  CK(cp(t.cid, tmp.cid, (size_t)n * 8)); CK(cp(t.prog, tmp.prog, (size_t)n * 4)); CK(cp(t.arr, tmp.arr, (size_t)n * 4));
-  CK(cp(t.qf, tmp.qf, n)); CK(cp(t.base, tmp.base, (size_t)n * 4)); CK(cp(t.mtime, tmp.mtime, (size_t)n * 4));
-  CK(cp(t.exec, tmp.exec, (size_t)n * 4)); CK(cp(t.quanta, tmp.quanta, (size_t)n * 4));
-  CK(cp(t.inh, tmp.inh, (size_t)n * 4)); CK(cp(t.tok, tmp.tok, (size_t)n * 4)); CK(cp(t.loc, tmp.loc, (size_t)n * 4));
-  CK(cp(t.hcls, tmp.hcls, (size_t)n * 4)); CK(cp(t.bidx, tmp.bidx, (size_t)n * 4));
-  CK(cudaMemsetAsync(t.qf + n, QF_DEAD, rows - n, ctx->stream));
-  // remap the previous batch (its completed rows were DEAD and are gone from the list: the
-  // previous batch entries that are not live map to NONE and must be dropped)
-  HostOut h = *ctx->out.hout;
-  std::vector<uint32_t> prev(h.n_batch + h.n_standby);  // the resident list (R32: batch, standby)
-  CK(cudaMemcpyAsync(prev.data(), ctx->out.prev_slots, prev.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  std::vector<uint32_t> np;
-  for (uint32_t s : prev) if (s < old2new.size() && old2new[s] != NONE) np.push_back(old2new[s]);
-  uint32_t npv = (uint32_t)np.size();
-  if (npv) CK(cudaMemcpyAsync(ctx->out.prev_slots, np.data(), np.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-  // dropped entries shift the previous-batch indices the running rows carry
-  if (npv) CK(launch_set_bidx(ctx->stream, ctx->ct, ctx->out.prev_slots, npv));
-  CK(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->ctl) + offsetof(Ctl, n_prev), &npv, 4, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->ctl) + offsetof(Ctl, s_tail_prev), &n, 4, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));  // lv, old2new, np, npv go out of scope
-  for (auto& kv : ctx->call_slot) kv.second = old2new[kv.second];
-  std::vector<uint32_t> sp(rows, 0), sa(rows, 0);
-  std::vector<uint8_t> sl(rows, 0);
-  for (uint32_t i = 0; i < n; ++i) {
-    sp[i] = ctx->slot_prog[lv[i]];
-    sa[i] = ctx->slot_arr[lv[i]];
-    sl[i] = 1;
-  }
-  ctx->slot_prog.swap(sp);
-  ctx->slot_arr.swap(sa);
-  ctx->slot_live.swap(sl);
+  if (k != n) return fail(ctx, AUTX_E_STATE, "compaction: %u live rows on the host, %u active calls", k, n);
+  std::fill(ctx->slot_live.begin() + k, ctx->slot_live.begin() + ctx->tail, 0);
+  for (auto& kv : ctx->call_slot) kv.second = o2n[kv.second];
   ctx->low = 0;
   ctx->tail = n;
-  void* f[] = {tmp.cid, tmp.prog, tmp.arr, tmp.qf, tmp.base, tmp.mtime, tmp.exec, tmp.quanta, tmp.inh,
-               tmp.tok, tmp.loc, tmp.hcls, tmp.bidx, d_live, d_map};
-  for (void* p : f) cudaFree(p);
+  ++ctx->n_compactions;
+  ctx->compact_host_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
   return AUTX_OK;
 }
 
@@ -1303,6 +1283,13 @@ extern "C" autx_status autx_set_timing(autx_ctx* ctx, int32_t on) {
   if (!ctx) return AUTX_E_INVAL;
   ctx->timing = (on & 1) != 0;       // 1: CUDA events around the step's kernels
   ctx->pol.stamps = (on & 2) ? 1 : 0;  // 2: %globaltimer chain stamps (no events: PDL undisturbed)
+  return AUTX_OK;
+}
+
+extern "C" autx_status autx_compaction_stats(const autx_ctx* ctx, uint64_t* n, double* host_us) {
+  if (!ctx || !n || !host_us) return AUTX_E_INVAL;
+  *n = ctx->n_compactions;
+  *host_us = ctx->compact_host_us;
   return AUTX_OK;
 }
 

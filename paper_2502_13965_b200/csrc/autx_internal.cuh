@@ -353,7 +353,6 @@ cudaError_t launch_register(cudaStream_t s, const Policy& pol, CallTable ct, Pro
 // Per-device setup of the step kernels (shared-memory attributes); called by autx_create after
 // cudaSetDevice.
 cudaError_t step_kernels_setup();
-cudaError_t launch_set_bidx(cudaStream_t s, CallTable ct, const uint32_t* prev_slots, uint32_t n);
 cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl,
                         Outputs out, KvState kv, bool kv_on, uint32_t t, uint32_t n_rows,
                         uint32_t seqno, cudaEvent_t* ev /* 4 events or null */,
@@ -368,8 +367,7 @@ cudaError_t launch_swap(cudaStream_t s, const Ctl* ctl, KvState kv, void* const*
 cudaError_t launch_stage(cudaStream_t s, const Ctl* ctl, KvState kv, void* const* d_kpool,
                          void* const* d_vpool, uint32_t n_layers, uint32_t chunk_bytes,
                          char* staging, int direction, int n_ctas);
-cudaError_t launch_compact(cudaStream_t s, CallTable src, CallTable dst, const uint32_t* live,
-                           uint32_t n_live);
-cudaError_t launch_remap(cudaStream_t s, uint32_t* slots, uint32_t n, const uint32_t* old2new);
+cudaError_t launch_compact(cudaStream_t s, CallTable src, CallTable dst, uint32_t n_rows, uint32_t n_live,
+                           uint32_t* tile_live, uint32_t* old2new, Ctl* ctl, uint32_t* prev_slots);
 
 }  // namespace autx

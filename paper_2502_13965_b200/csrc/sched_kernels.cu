@@ -1659,55 +1659,106 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
 }
 
 // ---------------------------------------------------------------------------------------------
-// G8: stable compaction of the call table (drop completed rows, keep (arrival, seq) order).
-// live[i] = old row of the i-th live row in table order; dst gets rows 0..n_live-1.
+// G8: stable compaction of the call table on the device (drop completed rows, keep (arrival, seq)
+// order): live counts per 2048-row tile, then every tile scatters its live rows to their rank
+// among the live rows into the other buffer of the double-buffered table and records old2new;
+// one CTA remaps (and compacts) the previous resident list.  No host sort, no allocation.
 // ---------------------------------------------------------------------------------------------
-__global__ void k_compact(CallTable src, CallTable dst, const uint32_t* live, uint32_t n_live) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_live) return;
-  uint32_t s = live[i];
-  dst.cid[i] = src.cid[s];
-  dst.prog[i] = src.prog[s];
-  dst.arr[i] = src.arr[s];
-  dst.qf[i] = src.qf[s];
-  dst.base[i] = src.base[s];
-  dst.mtime[i] = src.mtime[s];
-  dst.exec[i] = src.exec[s];
-  dst.quanta[i] = src.quanta[s];
-  dst.inh[i] = src.inh[s];
-  dst.tok[i] = src.tok[s];
-  dst.loc[i] = src.loc[s];
-  dst.hcls[i] = src.hcls[s];
-  dst.bidx[i] = src.bidx[s];
+__global__ void __launch_bounds__(SCAN_THREADS) k_live_count(CallTable src, uint32_t n_rows, uint32_t* tile_live) {
+  __shared__ uint32_t red_c[33];
+  const uint32_t row0 = blockIdx.x * TILE + threadIdx.x * ROWS_PER_THREAD;
+  uint32_t nl = 0;
+#pragma unroll
+  for (int j = 0; j < ROWS_PER_THREAD; ++j)
+    nl += (row0 + j < n_rows && !(src.qf[row0 + j] & QF_DEAD)) ? 1u : 0u;
+  uint32_t tot;
+  block_excl_scan<uint32_t, SCAN_THREADS>(nl, red_c, &tot);
+  if (threadIdx.x == 0) tile_live[blockIdx.x] = tot;
 }
 
-__global__ void k_set_bidx(CallTable ct, const uint32_t* prev_slots, uint32_t n) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) ct.bidx[prev_slots[i]] = i;
+__global__ void __launch_bounds__(SCAN_THREADS) k_compact(CallTable src, CallTable dst, uint32_t n_rows,
+                                                          const uint32_t* tile_live, uint32_t* old2new) {
+  __shared__ uint32_t red_c[33];
+  const uint32_t tile = blockIdx.x, tid = threadIdx.x;
+  // this tile's offset: the live rows of the tiles before it (<= a few hundred counts)
+  uint32_t pre = 0;
+  for (uint32_t k = tid; k < tile; k += SCAN_THREADS) pre += tile_live[k];
+  uint32_t base;
+  block_excl_scan<uint32_t, SCAN_THREADS>(pre, red_c, &base);
+  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  uint32_t live = 0, nl = 0;
+#pragma unroll
+  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
+    const bool l = row0 + j < n_rows && !(src.qf[row0 + j] & QF_DEAD);
+    live |= l ? 1u << j : 0u;
+    nl += l ? 1u : 0u;
+  }
+  uint32_t pos = base + block_excl_scan<uint32_t, SCAN_THREADS>(nl, red_c, nullptr);
+#pragma unroll
+  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
+    const uint32_t s = row0 + j;
+    if (s >= n_rows) break;
+    if (!((live >> j) & 1u)) {
+      old2new[s] = NONE;
+      continue;
+    }
+    const uint32_t i = pos++;
+    old2new[s] = i;
+    dst.cid[i] = src.cid[s];
+    dst.prog[i] = src.prog[s];
+    dst.arr[i] = src.arr[s];
+    dst.qf[i] = src.qf[s];
+    dst.base[i] = src.base[s];
+    dst.mtime[i] = src.mtime[s];
+    dst.exec[i] = src.exec[s];
+    dst.quanta[i] = src.quanta[s];
+    dst.inh[i] = src.inh[s];
+    dst.tok[i] = src.tok[s];
+    dst.loc[i] = src.loc[s];
+    dst.hcls[i] = src.hcls[s];
+    dst.bidx[i] = src.bidx[s];
+  }
 }
 
-cudaError_t launch_set_bidx(cudaStream_t s, CallTable ct, const uint32_t* prev_slots, uint32_t n) {
-  if (n == 0) return cudaSuccess;
-  ++g_kernel_launches;
-  k_set_bidx<<<(n + 255) / 256, 256, 0, s>>>(ct, prev_slots, n);
-  return cudaGetLastError();
+// The previous resident list through old2new, its completed (dropped) entries removed in order;
+// the surviving entries' list index (bidx) follows.  One CTA: <= 2048 entries.
+__global__ void __launch_bounds__(1024) k_remap_prev(CallTable ct, Ctl* ctl, uint32_t* prev_slots,
+                                                     const uint32_t* old2new, uint32_t n_live) {
+  __shared__ uint32_t red_c[33];
+  const uint32_t n = ctl->n_prev;
+  constexpr int R = 2;
+  uint32_t v[R], nl = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t j = threadIdx.x * R + r;
+    v[r] = j < n ? old2new[prev_slots[j]] : NONE;
+    nl += v[r] != NONE ? 1u : 0u;
+  }
+  uint32_t tot;
+  uint32_t pos = block_excl_scan<uint32_t, 1024>(nl, red_c, &tot);  // (reads complete before the barrier)
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (v[r] != NONE) {
+      prev_slots[pos] = v[r];
+      ct.bidx[v[r]] = pos;
+      ++pos;
+    }
+  if (threadIdx.x == 0) {
+    ctl->n_prev = tot;
+    ctl->s_tail_prev = n_live;  // every row below n_live predates the next step's arrivals
+  }
 }
 
-__global__ void k_remap(uint32_t* slots, uint32_t n, const uint32_t* old2new) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) slots[i] = old2new[slots[i]];
-}
-
-cudaError_t launch_compact(cudaStream_t s, CallTable src, CallTable dst, const uint32_t* live,
-                           uint32_t n_live) {
+cudaError_t launch_compact(cudaStream_t s, CallTable src, CallTable dst, uint32_t n_rows, uint32_t n_live,
+                           uint32_t* tile_live, uint32_t* old2new, Ctl* ctl, uint32_t* prev_slots) {
+  const uint32_t ntiles = (n_rows + TILE - 1) / TILE;
+  if (ntiles) {
+    __atomic_fetch_add(&g_kernel_launches, 2ull, __ATOMIC_RELAXED);
+    k_live_count<<<ntiles, SCAN_THREADS, 0, s>>>(src, n_rows, tile_live);
+    k_compact<<<ntiles, SCAN_THREADS, 0, s>>>(src, dst, n_rows, tile_live, old2new);
+  }
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  if (n_live) k_compact<<<(n_live + 255) / 256, 256, 0, s>>>(src, dst, live, n_live);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_remap(cudaStream_t s, uint32_t* slots, uint32_t n, const uint32_t* old2new) {
-  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  if (n) k_remap<<<(n + 255) / 256, 256, 0, s>>>(slots, n, old2new);
+  k_remap_prev<<<1, 1024, 0, s>>>(dst, ctl, prev_slots, old2new, n_live);
   return cudaGetLastError();
 }
 

@@ -169,6 +169,16 @@ def test_kv_round_trip_bytes_multistep():
     s.close()
 
 
+@pytest.mark.parametrize("N,X", [(3, 4), (1, 4)])
+def test_multistep_with_compaction(N, X):
+    """The resident list (batch + standby) survives device compaction (k_remap_prev)."""
+    cfg = lambda: Config(**{**spec_ladder_config(PLAS, max_batch=16, kv_budget=2400).__dict__,
+                            "sched_every": N, "overprovision": X})
+    tr = chatbot(200)
+    assert_same(gpu_records(tr, cfg(), max_calls=400, n_gpu_blocks=2400, max_blocks_per_call=4096,
+                            host_pages=1 << 14), oracle_records(tr, cfg()))
+
+
 def test_config_errors():
     from paper_2502_13965_b200 import AutxError
     base = spec_ladder_config(PLAS, max_batch=16)

@@ -294,6 +294,27 @@ def test_compaction_preserves_schedule():
     assert_same(gpu_records(tr, spec_ladder_config(PLAS, max_batch=16), max_calls=400), want)
 
 
+@pytest.mark.parametrize("policy,kv", [(PLAS, 2400), (ATLAS, None), (ATLAS_EQ2, 3000)])
+def test_device_compaction_with_kv_allocator(policy, kv):
+    """Device-side G8 compaction (double-buffered table, k_live_count / k_compact /
+    k_remap_prev) under the KV block allocator (resident slots and host pages move with their
+    rows) and exact Eq. 2 (lineage by call id): lists and ledgers equal the oracle's, and the
+    table really was compacted many times."""
+    from paper_2502_13965_b200 import TraceDriver
+    tr = mcts_mapreduce(12) if policy == ATLAS_EQ2 else chatbot(200)
+    mk = lambda: spec_ladder_config(policy, max_batch=16, kv_budget=kv)
+    want, _ = oracle_records(tr, mk())
+    extra = dict(n_gpu_blocks=kv, max_blocks_per_call=4096, host_pages=1 << 14) if kv else {}
+    s = make_sched(mk(), max_calls=650 if policy == ATLAS_EQ2 else 400, **extra)
+    log = TraceDriver(tr, s).run()
+    n, us = s.compaction_stats()
+    s.close()
+    got = [(r["t"], r["batch"], r["admit"], r["preempt"], r["swap_out_blocks"], r["swap_in_blocks"],
+            r["kv_blocks"]) for r in log if r["batch"] or r["preempt"]]
+    assert_same(got, want)
+    assert n >= (1 if policy == ATLAS_EQ2 else 3)
+
+
 def test_protocol_errors():
     from paper_2502_13965_b200 import Scheduler, AutxError, CALL_DESC
     s = Scheduler(policy="plas", K=2, q_hi=(1,), quanta=(1, None), max_batch=1, kv_budget=4,
