@@ -323,19 +323,25 @@ def bench_swap(torch, args, link):
     def pat(cids, js, l, kv):  # one byte per (call, block, layer, K|V), the whole chunk
         return ((cids * 31 + js * 7 + l * 3 + kv) & 0xFF).to(torch.uint8)
 
-    for name, mode in (("sm", SWAP_SM), ("staged_dma", SWAP_STAGED_DMA), ("per_chunk_memcpy", SWAP_PER_CHUNK_MEMCPY)):
+    runs = (("sm", SWAP_SM, 1, 0), ("staged_dma", SWAP_STAGED_DMA, 1, 0),
+            ("per_chunk_memcpy", SWAP_PER_CHUNK_MEMCPY, 1, 0),
+            # the scheduler every 4 steps, 16 standby calls
+            ("staged_dma_multistep_N4_X16", SWAP_STAGED_DMA, 4, 16))
+    for name, mode, N, X in runs:
         tr = react(1000, seed=BASE_SEED + CONFIG_INDEX["react"])
         # the library and the engine's reads / writes of the pools on one stream (autx.h: all
         # device work is ordered on the context's stream)
         s = Scheduler(policy="plas", beta=(2, 1), max_batch=64, kv_budget=P, block_tokens=16,
                       max_calls=1 << 16, max_programs=1 << 14, n_gpu_blocks=nblk, max_blocks_per_call=P,
-                      host_pages=host_pages, stream=torch.cuda.current_stream().cuda_stream, **lad)
+                      host_pages=host_pages, stream=torch.cuda.current_stream().cuda_stream,
+                      sched_every=N, overprovision=X, **lad)
         d = TraceDriver(tr, s, log_lists=True)
         tot_b = tot_ms = 0.0
         b_d2h = b_h2d = 0
         n = 0
         t_at_peak = 0.0
         n_duplex = 0
+        blocks_all = 0        # blocks swapped over every step of the run (both directions)
         written = {}          # call id -> leading blocks the engine has written
         checked = mismatched = 0
         for i in range(args.swap_steps + 20):
@@ -344,6 +350,7 @@ def bench_swap(torch, args, link):
             rec = d.step()
             st = s.kv_swap([x.data_ptr() for x in kp], [x.data_ptr() for x in vp], chunk,
                            host.data_ptr(), host.numel(), mode)
+            blocks_all += rec["swap_out_blocks"] + rec["swap_in_blocks"]
             if i >= 20 and (st.bytes_d2h + st.bytes_h2d) > 0:
                 tot_b += st.bytes_d2h + st.bytes_h2d
                 tot_ms += st.ms
@@ -387,6 +394,8 @@ def bench_swap(torch, args, link):
             results[name] = {"GB/s": round(gbs, 2), "steps": n, "bytes_d2h": b_d2h, "bytes_h2d": b_h2d,
                              "ms_per_step": tot_ms / n, "frac_of_host_link": round(t_at_peak / (tot_ms * 1e-3), 4),
                              "frac_of_duplex_peak": round(gbs / link["duplex"], 4), "duplex_steps": n_duplex,
+                             "sched_every": N, "overprovision": X,
+                             "swapped_blocks_per_step": round(blocks_all / (i + 1), 2),
                              "content_check": {"chunks_checked": checked, "chunks_mismatched": mismatched,
                                                "ok": checked > 0 and mismatched == 0}}
     del kp, vp, host

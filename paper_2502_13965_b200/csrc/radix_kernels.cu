@@ -4,14 +4,17 @@
 // and the keys are sorted by a stable LSD radix sort, one byte per digit.  The table is kept in
 // seq (row) order, so sorting the high 32 bits stably already orders the low 32: only digits
 // 4..7 are sorted, and a digit whose 256-bin histogram is a single bin (all keys equal there)
-// is skipped.  The first min(BS, n_live) sorted keys become finalize's candidate list, and
+// is skipped — decided on the device by every pass kernel from k_keys' global digit histograms,
+// so the step needs no host round trip; a pass reads the key buffer the earlier non-skipped
+// passes left (parity of their count).  The first min(BS, n_live) sorted keys become finalize's candidate list, and
 // finalize cuts the prefix exactly as in the selection path, so both modes give identical
 // decisions (tests/test_parity_gpu.py::test_radix_equals_select).
 //
 //   k_keys     dense pass: anti-starvation (same arithmetic as k_scan) + key pack + the four
 //              global 256-bin digit histograms (for skip detection)
 //   k_hist     per-tile 256-bin histogram of one digit        -> hist[digit value][tile]
-//   k_scan_h   exclusive scan of hist in (digit value, tile) order (one CTA)
+//   k_scan_h   exclusive scan of hist in (digit value, tile) order: a warp per digit value scans
+//              its tiles, the digit values' bases come from the global histogram
 //   k_scatter  stable per-tile ranking (warp match + per-warp running counters) and scatter
 //   k_take     the first min(BS, n_live) keys -> candidate rows
 #include "autx_internal.cuh"
@@ -75,9 +78,25 @@ __global__ void __launch_bounds__(RX_THREADS) k_keys(Policy pol, CallTable ct, P
   }
 }
 
-__global__ void __launch_bounds__(RX_THREADS) k_hist(const uint64_t* keys, uint32_t* hist, uint32_t ntiles,
-                                                     int shift) {
+// Is digit d (of digits 4..7) a single bin over all n_pad keys (the pass is the identity)?  And
+// which key buffer does pass d read (the number of earlier non-skipped passes, mod 2)?  Every
+// CTA of a pass kernel derives both from the global digit histograms (block of >= 256 threads).
+__device__ __forceinline__ bool digit_uniform(const uint32_t* dig_hist, int d, uint32_t n_pad) {
+  const uint32_t v = threadIdx.x < 256 ? dig_hist[d * 256 + threadIdx.x] : 0u;
+  return __syncthreads_or(v == n_pad) != 0;
+}
+__device__ __forceinline__ uint32_t pass_src(const uint32_t* dig_hist, int d, uint32_t n_pad) {
+  uint32_t src = 0;
+  for (int e = 0; e < d; ++e) src ^= digit_uniform(dig_hist, e, n_pad) ? 0u : 1u;
+  return src;
+}
+
+__global__ void __launch_bounds__(RX_THREADS) k_hist(RadixState rx, uint32_t* hist, uint32_t ntiles, int d) {
   __shared__ uint32_t h[256];
+  const uint32_t n_pad = ntiles * RX_TILE;
+  if (digit_uniform(rx.dig_hist, d, n_pad)) return;
+  const int shift = 32 + 8 * d;
+  const uint64_t* keys = pass_src(rx.dig_hist, d, n_pad) ? rx.keys_alt : rx.keys;
   h[threadIdx.x] = 0;
   __syncthreads();
   const uint64_t* k = keys + (size_t)blockIdx.x * RX_TILE;
@@ -90,29 +109,44 @@ __global__ void __launch_bounds__(RX_THREADS) k_hist(const uint64_t* keys, uint3
   hist[(size_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
-// exclusive scan over 256 * ntiles counters in (digit, tile) order, one CTA of 1024 threads
-__global__ void __launch_bounds__(1024) k_scan_h(uint32_t* hist, uint32_t n) {
-  __shared__ uint32_t red[33];
-  uint32_t per = (n + 1023) / 1024;
-  uint32_t a = threadIdx.x * per, b = min(n, a + per);
-  uint32_t s = 0;
-  for (uint32_t i = a; i < b; ++i) s += hist[i];
-  uint32_t off = block_excl_scan<uint32_t, 1024>(s, red, nullptr);
-  for (uint32_t i = a; i < b; ++i) {
-    uint32_t v = hist[i];
-    hist[i] = off;
-    off += v;
+// Exclusive scan of the (digit value, tile) counters: a warp per digit value walks its ntiles
+// counters 32 at a time with a carry; the value's base is the exclusive prefix of the global
+// digit histogram (k_keys) over the smaller values.  8 CTAs x 32 warps = the 256 values.
+__global__ void __launch_bounds__(1024) k_scan_h(RadixState rx, uint32_t* hist, uint32_t ntiles, int d) {
+  const uint32_t n_pad = ntiles * RX_TILE;
+  if (digit_uniform(rx.dig_hist, d, n_pad)) return;
+  const uint32_t v = blockIdx.x * 32 + warp_id(), lane = lane_id();
+  // base of value v: sum of the global histogram over values < v (8 per lane)
+  uint32_t b = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t u = lane * 8 + k;
+    b += u < v ? rx.dig_hist[d * 256 + u] : 0u;
+  }
+  uint32_t carry = warp_sum(b);
+  uint32_t* row = hist + (size_t)v * ntiles;
+  for (uint32_t c0 = 0; c0 < ntiles; c0 += 32) {
+    const uint32_t i = c0 + lane;
+    const uint32_t x = i < ntiles ? row[i] : 0u;
+    const uint32_t inc = warp_incl_scan(x);
+    if (i < ntiles) row[i] = carry + inc - x;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
   }
 }
 
 // Stable scatter of one digit.  Warp w of a tile owns keys [w*512, (w+1)*512) of the tile in
 // order; pass 1 counts its digits, a per-bin exclusive scan across warps gives each warp's base,
 // pass 2 walks the 512 keys in order (32 at a time) ranking equal digits with __match_any_sync.
-__global__ void __launch_bounds__(RX_THREADS) k_scatter(const uint64_t* in, uint64_t* out,
-                                                        const uint32_t* hist, uint32_t ntiles,
-                                                        int shift) {
+__global__ void __launch_bounds__(RX_THREADS) k_scatter(RadixState rx, const uint32_t* hist, uint32_t ntiles,
+                                                        int d) {
   __shared__ uint32_t wh[RX_THREADS / 32][256];
   __shared__ uint32_t gbase[256];
+  const uint32_t n_pad = ntiles * RX_TILE;
+  if (digit_uniform(rx.dig_hist, d, n_pad)) return;
+  const int shift = 32 + 8 * d;
+  const bool alt = pass_src(rx.dig_hist, d, n_pad) != 0;
+  const uint64_t* in = alt ? rx.keys_alt : rx.keys;
+  uint64_t* out = alt ? rx.keys : rx.keys_alt;
   const uint32_t w = warp_id(), lane = lane_id();
   for (int i = lane; i < 256; i += 32) wh[w][i] = 0;
   const uint64_t* k = in + (size_t)blockIdx.x * RX_TILE + w * RX_WARP_KEYS;
@@ -154,8 +188,9 @@ __global__ void __launch_bounds__(RX_THREADS) k_scatter(const uint64_t* in, uint
   }
 }
 
-__global__ void k_take(const uint64_t* keys, CallTable ct, Ctl* ctl, Outputs out, uint32_t BS, uint32_t K,
-                       uint32_t t) {
+__global__ void __launch_bounds__(1024) k_take(RadixState rx, uint32_t n_pad, CallTable ct, Ctl* ctl, Outputs out,
+                                               uint32_t BS, uint32_t K, uint32_t t) {
+  const uint64_t* keys = pass_src(rx.dig_hist, 4, n_pad) ? rx.keys_alt : rx.keys;  // after the 4 passes
   uint32_t n = min(BS, ctl->n_live);
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     uint32_t sl = (uint32_t)keys[i];
@@ -186,31 +221,17 @@ cudaError_t launch_radix_order(cudaStream_t s, const Policy& pol, CallTable ct, 
   uint32_t grid = std::min<uint32_t>(ntiles * RX_ITEMS, (uint32_t)sms * 8);
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
   k_keys<<<grid, RX_THREADS, 0, s>>>(pol, ct, pt, ctl, rx, t, n_rows, arr_base);
-  // skip detection needs the digit histograms on the host (a 4 KB read; this mode is the
-  // contract path, the selection path is the fast path)
-  cudaMemcpyAsync(rx.h_dig_hist, rx.dig_hist, 4 * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
-  cudaError_t e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return e;
-  uint64_t* a = rx.keys;
-  uint64_t* b = rx.keys_alt;
-  uint32_t passes = 0;
+  // the skip decisions are taken on the device (no host round trip mid-step); the host learns
+  // the pass count from the histograms afterwards (autx_step_stats), not needed here
+  uint32_t passes = 4;
   for (int d = 0; d < 4; ++d) {
-    bool uniform = false;
-    for (int v = 0; v < 256; ++v)
-      if (rx.h_dig_hist[d * 256 + v] == n_pad) uniform = true;
-    if (uniform) continue;
-    int shift = 32 + 8 * d;
-  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-    k_hist<<<ntiles, RX_THREADS, 0, s>>>(a, rx.tile_hist, ntiles, shift);
-  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-    k_scan_h<<<1, 1024, 0, s>>>(rx.tile_hist, 256 * ntiles);
-  __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-    k_scatter<<<ntiles, RX_THREADS, 0, s>>>(a, b, rx.tile_hist, ntiles, shift);
-    std::swap(a, b);
-    ++passes;
+    __atomic_fetch_add(&g_kernel_launches, 3ull, __ATOMIC_RELAXED);
+    k_hist<<<ntiles, RX_THREADS, 0, s>>>(rx, rx.tile_hist, ntiles, d);
+    k_scan_h<<<8, 1024, 0, s>>>(rx, rx.tile_hist, ntiles, d);
+    k_scatter<<<ntiles, RX_THREADS, 0, s>>>(rx, rx.tile_hist, ntiles, d);
   }
   __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);
-  k_take<<<1, 1024, 0, s>>>(a, ct, ctl, out, pol.max_batch, pol.K, t);
+  k_take<<<1, 1024, 0, s>>>(rx, n_pad, ct, ctl, out, pol.max_batch, pol.K, t);
   if (passes_out) *passes_out = passes;
   return cudaGetLastError();
 }
