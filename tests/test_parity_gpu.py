@@ -509,6 +509,39 @@ def test_full_size_chatbot_react_first_steps(workload):
     s.close()
 
 
+@pytest.mark.parametrize("bs,P,X,kv", [(2048, None, 0, False), (1536, 60000, 0, True), (1024, 60000, 1024, True),
+                                        (2000, None, 0, False)])
+def test_large_batch_saturated(bs, P, X, kv):
+    """Resident sets above 1024 (BS up to the 2048 cap, or BS + X over-provisioned): the finalize's
+    1024-thread variant and k_rank's shared memory at 2 x 2048 keys, with more active calls than the
+    resident set can take (saturated), 60 steps side by side with the oracle, lists and ledgers."""
+    from paper_2502_13965_b200 import TraceDriver
+    tr = chatbot(2600)
+    mk = lambda: Config(**{**spec_ladder_config(PLAS, max_batch=bs, kv_budget=P).__dict__, "overprovision": X,
+                           "block_bytes": 1})
+    eng = Engine(mk(), check_formulations=False)
+    wl = Workload(tr)
+    extra = dict(n_gpu_blocks=P, max_blocks_per_call=4096, host_pages=1 << 16) if kv else {}
+    s = make_sched(mk(), max_calls=tr.n_calls + 4096, max_programs=tr.n_programs + 1024, overprovision=X, **extra)
+    d = TraceDriver(tr, s)
+    completed, saturated = [], 0
+    for t in range(60):
+        cids = [int(tr.call_id[c]) for c in completed]
+        ended = wl.release(t, completed)
+        rec_o = eng.step(t, cids, wl.arrivals(t))
+        for pid in ended:
+            eng.end_program(pid)
+        completed = wl.ran(t, rec_o["batch"])
+        rec = d.step()
+        saturated += rec["n_active"] > bs + X
+        assert (rec["batch"], rec.get("standby", []), rec["admit"], rec["preempt"]) == \
+            (rec_o["batch"], rec_o.get("standby", []), rec_o["admit"], rec_o["preempt"]), t
+        assert (rec["swap_out_blocks"], rec["swap_in_blocks"], rec["kv_blocks"]) == \
+            (rec_o["swap_out"], rec_o["swap_in"], rec_o["kv_blocks"]), t
+    assert saturated >= 50
+    s.close()
+
+
 def oracle_from_snapshot(s, tr, cfg, d):
     """The oracle's engine state rebuilt from a GPU snapshot (SURVEY §8(d) timing protocol step
     1): every active call's state from autx_dump_calls (table order = registration order), the
