@@ -589,10 +589,22 @@ static autx_status flush_staged(autx_ctx* ctx, uint32_t t, bool always = false) 
   a.n_rows = ctx->tail;
   a.seqno = ctx->seqno;
   a.n_active = (uint32_t)ctx->call_slot.size();
-  if (a.n_comp <= (uint32_t)PRO_INLINE) memcpy(a.comp, ctx->h_cslots, a.n_comp * sizeof(uint32_t));
-  else a.comp_ptr = ctx->h_cslots;
-  if (a.n_arr <= (uint32_t)PRO_INLINE) memcpy(a.arr, ctx->h_arr, a.n_arr * sizeof(ArrivalRec));
-  else a.arr_ptr = ctx->h_arr;
+  // larger batches: one DMA each to device memory ahead of the step (stream-ordered before the
+  // prologue; the pinned staging is not reused before this step's `done`), read by the kernel from
+  // HBM instead of one PCIe round trip per record
+  if (a.n_comp <= (uint32_t)PRO_INLINE) {
+    memcpy(a.comp, ctx->h_cslots, a.n_comp * sizeof(uint32_t));
+  } else {
+    CK(cudaMemcpyAsync(ctx->d_cslots, ctx->h_cslots, (size_t)a.n_comp * 4, cudaMemcpyHostToDevice, ctx->stream));
+    a.comp_ptr = ctx->d_cslots;
+  }
+  if (a.n_arr <= (uint32_t)PRO_INLINE) {
+    memcpy(a.arr, ctx->h_arr, a.n_arr * sizeof(ArrivalRec));
+  } else {
+    CK(cudaMemcpyAsync(ctx->d_arr, ctx->h_arr, (size_t)a.n_arr * sizeof(ArrivalRec), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    a.arr_ptr = ctx->d_arr;
+  }
   a.comp_lin = ctx->h_clin;  // AUTX_ATLAS_EQ2 only (read through UVA)
   a.par = ctx->h_par;
   CompRec* recs = reinterpret_cast<CompRec*>(ctx->d_route_local + sizeof(RouteHdr));
@@ -724,6 +736,8 @@ static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uin
     if (s) return s;
     s = compact(ctx);
     if (s) return s;
+    // the flushed prologue (or its DMA) may still read the pinned staging this call refills
+    CK(cudaStreamSynchronize(ctx->stream));
   }
   // staging buffer growth, keeping records already staged for this step
   const uint32_t need = ctx->n_arr_staged + n;

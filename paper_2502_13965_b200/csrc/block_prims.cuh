@@ -1,6 +1,7 @@
 // Warp/block primitives (scans, reductions, 128-bit compare, PDL, timers) written for sm_100a.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace autx {
@@ -65,6 +66,21 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // pdl_trigger() lets the successor launch as soon as every CTA of this grid has started.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Bounds checks of a debug build (AUTX_NVCC_FLAGS=-DAUTX_BOUNDS): print the site and trap.  The
+// pool refuses compute-sanitizer, so out-of-bounds indices are caught by these instead.
+#ifdef AUTX_BOUNDS
+#define AUTX_CHECK(cond, what, v)                                                                        \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("AUTX_CHECK failed: %s (%s:%d) value %llu block %d thread %d\n", what, __FILE__, __LINE__, \
+             (unsigned long long)(v), (int)blockIdx.x, (int)threadIdx.x);                               \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define AUTX_CHECK(cond, what, v) do { } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t ceil_div_u32(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
 

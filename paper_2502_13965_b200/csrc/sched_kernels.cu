@@ -123,6 +123,7 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       uint8_t qf = qf0;
       if (kv_on && (qf & QF_RES)) {
         rslot = ct.loc[s];
+        AUTX_CHECK(rslot < pol.max_batch, "complete: resident slot", rslot);
         nfree = kv.rs_nblk[rslot];
       }
       ct.qf[s] = QF_DEAD;
@@ -135,9 +136,12 @@ __device__ void complete_body(const Policy& pol, CallTable& ct, ProgTable& pt, C
       uint32_t roff = block_excl_scan<uint32_t, NT>(has, red_u, &rtot);
       uint32_t top = ctl->free_top, rtop = ctl->rs_free_top;
       if (rslot != NONE) {
+        AUTX_CHECK(nfree == blocks_for(pol, ct.tok[s] + ct.exec[s]), "complete: held blocks", nfree);
         const uint32_t* src = kv.rs_blocks + (size_t)rslot * pol.max_blocks_per_call;
+        AUTX_CHECK(top + off + nfree <= pol.n_gpu_blocks, "complete: free stack push", top + off + nfree);
         for (uint32_t j = 0; j < nfree; ++j) kv.free_stack[top + off + j] = src[j];
         kv.rs_nblk[rslot] = 0;
+        AUTX_CHECK(rtop + roff < pol.max_batch, "complete: resident-slot push", rtop + roff);
         kv.rs_free[rtop + roff] = rslot;
       }
       __syncthreads();
@@ -284,8 +288,10 @@ __global__ void k_register(Policy pol, CallTable ct, ProgTable pt, const Arrival
 }
 
 // Fused prologue of one step: completions (a1) then arrivals (a2), one CTA; a typical step's
-// records travel inside the kernel parameters (no PCIe reads), larger batches through pointers.
-constexpr int PRO_THREADS = 256;
+// records travel inside the kernel parameters (no PCIe reads), larger batches through pointers to
+// device copies the host made before the step (one DMA each).  256 threads, or 1024 when a batch
+// exceeds 256 records (one pass instead of up to four dependent ones).
+template <int PRO_THREADS>
 __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
                                                           KvState kv, bool kv_on, CompRec* rec_out,
                                                           const PrologueArgs a) {
@@ -353,7 +359,9 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
 
 cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, ProgTable pt, Ctl* ctl, KvState kv,
                             bool kv_on, CompRec* rec_out, const PrologueArgs& a) {
-  return launch_pdl(k_prologue, 1, PRO_THREADS, 0, s, pol, ct, pt, ctl, kv, kv_on, rec_out, a);
+  if (std::max(a.n_comp, a.n_arr) > 256)
+    return launch_pdl(k_prologue<1024>, 1, 1024, 0, s, pol, ct, pt, ctl, kv, kv_on, rec_out, a);
+  return launch_pdl(k_prologue<256>, 1, 256, 0, s, pol, ct, pt, ctl, kv, kv_on, rec_out, a);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -514,6 +522,46 @@ __device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs
   }
 }
 
+// Region A decided by tile 0 alone (AUTX_SCAN_EMIT, default on): when the first tile holds at
+// least BS live calls of Q_1 after anti-starvation, q* = 0, m' = BS and region A is exactly its
+// first BS Q_1 rows in table order — no other tile's count can change that — so the dense pass's
+// tile 0 emits the candidates, the boundary and the selection itself and tags the step
+// (fast_seq); the gather's tile CTAs then leave at once and only its previous-list CTAs run.
+// Rows are re-read (this CTA's own writes, L1/L2 hits): the common path keeps its registers.
+__device__ __noinline__ void scan_emit_tile0(const Policy& pol, CallTable ct, Ctl* ctl, Outputs out, uint32_t t,
+                                             uint32_t n_rows, uint32_t seqno) {
+  __shared__ uint32_t red_e[33];
+  const uint32_t BS = pol.max_batch, tid = threadIdx.x;
+  const uint32_t row0 = tid * ROWS_PER_THREAD;
+  uint32_t qfs[ROWS_PER_THREAD], n0 = 0;
+  const uint2 qv = row0 < n_rows ? __ldcg(reinterpret_cast<const uint2*>(ct.qf + row0)) : make_uint2(0x40404040u, 0x40404040u);
+#pragma unroll
+  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
+    qfs[j] = row0 + j < n_rows ? ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu : (uint32_t)QF_DEAD;
+    n0 += (qfs[j] & (QF_DEAD | QF_QMASK)) == 0 ? 1u : 0u;
+  }
+  uint32_t pos = block_excl_scan<uint32_t, SCAN_THREADS>(n0, red_e, nullptr);
+#pragma unroll
+  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
+    if ((qfs[j] & (QF_DEAD | QF_QMASK)) != 0 || pos >= BS) continue;
+    const uint32_t s = row0 + j;
+    CandRec r;
+    load_rec(ct, s, &r);
+    out.cand[pos] = s;
+    out.cand_rec[pos] = r;
+    out.ckey[pos] = cand_key(r, t);
+    out.ckvb[pos] = blocks_for(pol, r.tok + r.exec + 1);  // R14
+    if (pos + 1 == BS) ctl->qs_bnd1 = s + 1;
+    ++pos;
+  }
+  if (tid == 0) {
+    ctl->qstar = 0;
+    ctl->mprime = BS;
+    ctl->n_cand_a = BS;
+    ctl->fast_seq = seqno;
+  }
+}
+
 // pre (A/B switch AUTX_SCAN_PRE): what a CTA does while it waits for the prologue (PDL).  Rows
 // below first_new (this step's first arrival slot) keep prog/base/mtime through the prologue
 // (it writes only new rows and the qf/loc of completed ones; everything earlier in the stream
@@ -522,7 +570,7 @@ __device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs
 // program entries and of the previous batch's records (the gather's cold reads); 2: prog, base
 // and mtime early + the same prefetches.
 __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                               Outputs out, uint32_t pre) {
+                                                               Outputs out, uint32_t pre, uint32_t emit) {
   const uint32_t tid = threadIdx.x, tile = blockIdx.x;
   const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
   const uint32_t first_new = ctl->s_tail_prev;  // written before this step's chain
@@ -580,6 +628,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallT
     dense_rows<8>(pol, ct, pt, t, row0, qfs, prog, base, mtim, hq, npromo, nlive);
   }
   tile_counts(pol, ctl, out, tile, hq, npromo, nlive);
+  if (emit && tile == 0) {
+    __syncthreads();  // tile 0's Q_1 count (tid 0's store) and its rows' writes are visible in the CTA
+    if (__ldcg(out.tile_cnt) >= pol.max_batch) scan_emit_tile0(pol, ct, ctl, out, t, n_rows, ctl->s_seqno);
+  }
   CHAIN_END(1);
 }
 
@@ -654,6 +706,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
       if (tid == 1) ctl->n_live = stat;
     }
   }
+  if (is_tile && __ldcg(&ctl->fast_seq) == ctl->s_seqno) return;  // region A emitted by the dense pass
   if (!is_tile) {
     // previous batch: records (for preempt) and region-B keys
     const uint32_t j = (tile - ntiles) * NT + tid;
@@ -1197,6 +1250,8 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
 
   // ---- KV blocks: swap plan + allocation (a7) --------------------------------------------------
   if (kv_on) {
+    // the preempt list (and its rows' flags) written above by other threads is read below
+    __syncthreads();
     const uint32_t W = pol.max_blocks_per_call;
     // (1) preempted calls: host pages (size-class stacks), plan items, free GPU blocks + slots.
     // A call that never ran (R32 standby) has no KV content: its blocks are freed, not swapped.
@@ -1207,8 +1262,11 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       uint32_t s = 0, rslot = 0, nb = 0, ns = 0;
       if (i < n_preempt) {
         s = out.preempt_slots[i];
+        AUTX_CHECK(!(ct.qf[s] & QF_RES), "preempt: still flagged resident", s);
         rslot = ct.loc[s];
+        AUTX_CHECK(rslot < pol.max_batch, "preempt: resident slot", rslot);
         nb = kv.rs_nblk[rslot];
+        AUTX_CHECK(nb == blocks_for(pol, ct.tok[s] + ct.exec[s]), "preempt: held blocks", nb * 100000 + blocks_for(pol, ct.tok[s] + ct.exec[s]));
         ns = ct.exec[s] > 0 ? nb : 0u;
       }
       uint32_t tot, ptot, itot;
@@ -1228,6 +1286,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
             page = atomicAdd(&ctl->host_bump, 1u << cls);
             if ((uint64_t)page + (1u << cls) > pol.host_pages_lo) set_err(ctl, AUTX_E_NOMEM, 1);
           }
+          AUTX_CHECK(ioff < pol.max_batch && poff + ns <= kv.plan_cap, "preempt: plan", poff + ns);
           kv.plan_out[ioff] = PlanItem{page, ns, poff};
         }
         ct.loc[s] = page;
@@ -1236,12 +1295,14 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         for (uint32_t j = 0; j < nb; ++j) {
           uint32_t b = src[j];
           if (j < ns) kv.plan_out_blocks[poff + j] = b;
+          AUTX_CHECK(top0 + boff + j < pol.n_gpu_blocks, "preempt: free stack push", top0 + boff + j);
           kv.free_stack[top0 + boff + j] = b;
         }
         kv.rs_nblk[rslot] = 0;
       }
       uint32_t rt;
       uint32_t roff = base_free + block_excl_scan<uint32_t, NT>(i < n_preempt ? 1u : 0u, red, &rt);
+      AUTX_CHECK(i >= n_preempt || rtop0 + roff < pol.max_batch, "preempt: resident-slot push", rtop0 + roff);
       if (i < n_preempt) kv.rs_free[rtop0 + roff] = rslot;
       base_blk += tot;
       base_free += rt;
@@ -1263,6 +1324,8 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         if (need > W) set_err(ctl, AUTX_E_NOMEM, 2);
         if (qf & QF_RES) {
           rslot = ct.loc[s];
+          AUTX_CHECK(rslot < pol.max_batch, "resident: slot", rslot);
+          AUTX_CHECK(kv.rs_nblk[rslot] == blocks_for(pol, ct.tok[s] + ct.exec[s]), "resident: held blocks", kv.rs_nblk[rslot]);
           have = kv.rs_nblk[rslot];
         } else {
           admit = 1;
@@ -1279,9 +1342,13 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       if (i < n_res) {
         if (admit) {
           if (roff >= rtop) set_err(ctl, AUTX_E_NOMEM, 3);
+          AUTX_CHECK(roff < rtop, "admit: resident-slot pop", roff);
           rslot = kv.rs_free[rtop - 1 - roff];
+          AUTX_CHECK(kv.rs_nblk[rslot] == 0, "admit: popped resident slot not empty", rslot * 100000 + kv.rs_nblk[rslot]);
         }
+        AUTX_CHECK(i >= n_res || aoff + alloc <= top, "alloc: pool exhausted", aoff + alloc);
         if (aoff + alloc > top) set_err(ctl, AUTX_E_NOMEM, 4);
+        AUTX_CHECK(rslot < pol.max_batch && have <= W, "alloc: slot / held", rslot);
         uint32_t* dst = kv.rs_blocks + (size_t)rslot * W;
         // pops take the blocks freed by earlier steps first (stack [0, top0)), and this step's
         // swap-outs' blocks [top0, top) only when those run out: a swap-in then never writes a
@@ -1294,6 +1361,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         if (held) {
           // swap-in: host copy -> the first `held` blocks of the new list; free host pages after
           uint32_t page = ct.loc[s];
+          AUTX_CHECK(ioff < pol.max_batch && hoff + held <= kv.plan_cap && held <= W, "swap-in: plan", hoff + held);
           kv.plan_in[ioff] = PlanItem{page, held, hoff};
           for (uint32_t j = 0; j < held; ++j) kv.plan_in_blocks[hoff + j] = dst[j];
         }
@@ -1314,6 +1382,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
           const uint32_t i = c0 + tid;
           const uint32_t v = i < nkeep ? kv.free_stack[top0 + i] : 0u;
           __syncthreads();
+          AUTX_CHECK(i >= nkeep || top0 + i < pol.n_gpu_blocks, "free stack move", top0 + i);
           if (i < nkeep) kv.free_stack[dst0 + i] = v;
           __syncthreads();
         }
@@ -1327,6 +1396,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         PlanItem it = kv.plan_in[i];
         uint32_t cls = ceil_log2(it.nblk);
         uint32_t k = atomicAdd(&ctl->host_free_top[cls], 1u);
+        AUTX_CHECK(k < kv.host_free_cap && cls < 32, "host range free", k);
         kv.host_free[(size_t)cls * kv.host_free_cap + k] = (uint32_t)it.host_page;
       }
     }
@@ -1628,7 +1698,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   } else {
     // prog + L2 prefetches while the prologue runs (AUTX_SCAN_PRE, default 1: measured ~0.4 us)
     static const uint32_t pre = getenv("AUTX_SCAN_PRE") ? (uint32_t)atoi(getenv("AUTX_SCAN_PRE")) : 1u;
-    launch_pdl(k_scan_tile, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, pre);
+    static const uint32_t emit = getenv("AUTX_SCAN_EMIT") ? (uint32_t)atoi(getenv("AUTX_SCAN_EMIT")) : 1u;
+    launch_pdl(k_scan_tile, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, pre, emit);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
     launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out);

@@ -169,6 +169,19 @@ def test_kv_round_trip_bytes_multistep():
     s.close()
 
 
+@pytest.mark.parametrize("kv", [None, 3000])
+def test_multistep_exact_eq2(kv):
+    """Exact Eq. 2 inheritance (R31) under multi-step scheduling: DAG arrivals registered in window
+    steps inherit from parents completed mid-window."""
+    from autx_workload import mcts_mapreduce
+    from oracle.autellix import ATLAS_EQ2
+    cfg = lambda: Config(**{**spec_ladder_config(ATLAS_EQ2, max_batch=16, kv_budget=kv).__dict__,
+                            "sched_every": 3, "overprovision": 4})
+    tr = mcts_mapreduce(12)
+    extra = dict(n_gpu_blocks=kv, max_blocks_per_call=4096, host_pages=1 << 14) if kv else {}
+    assert_same(gpu_records(tr, cfg(), **extra), oracle_records(tr, cfg()))
+
+
 @pytest.mark.parametrize("N,X", [(3, 4), (1, 4)])
 def test_multistep_with_compaction(N, X):
     """The resident list (batch + standby) survives device compaction (k_remap_prev)."""

@@ -521,7 +521,7 @@ def test_large_batch_saturated(bs, P, X, kv):
                            "block_bytes": 1})
     eng = Engine(mk(), check_formulations=False)
     wl = Workload(tr)
-    extra = dict(n_gpu_blocks=P, max_blocks_per_call=4096, host_pages=1 << 16) if kv else {}
+    extra = dict(n_gpu_blocks=P, max_blocks_per_call=4096, host_pages=1 << 18) if kv else {}
     s = make_sched(mk(), max_calls=tr.n_calls + 4096, max_programs=tr.n_programs + 1024, overprovision=X, **extra)
     d = TraceDriver(tr, s)
     completed, saturated = [], 0
