@@ -115,7 +115,6 @@ struct Ctl {
   // b % QP_LINES: same-address reductions serialise at L2): [0, MAX_K) live rows per queue after
   // anti-starvation, [MAX_K] promotions, [MAX_K + 1] live rows.  Reset by finalize.
   uint32_t qs_bnd1;
-  uint32_t fast_seq;   // seqno of a step whose region A the dense pass's tile 0 emitted itself
   uint32_t last_n_b;   // region B size of the last step (autx_step_stats; n_cand_b is reset by finalize)
   // this step's scalars, written by the prologue from its parameters, read by the rest of the
   // chain after its PDL wait: a graph replay then only re-parameterises the prologue node

@@ -522,46 +522,6 @@ __device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs
   }
 }
 
-// Region A decided by tile 0 alone (AUTX_SCAN_EMIT, default on): when the first tile holds at
-// least BS live calls of Q_1 after anti-starvation, q* = 0, m' = BS and region A is exactly its
-// first BS Q_1 rows in table order — no other tile's count can change that — so the dense pass's
-// tile 0 emits the candidates, the boundary and the selection itself and tags the step
-// (fast_seq); the gather's tile CTAs then leave at once and only its previous-list CTAs run.
-// Rows are re-read (this CTA's own writes, L1/L2 hits): the common path keeps its registers.
-__device__ __noinline__ void scan_emit_tile0(const Policy& pol, CallTable ct, Ctl* ctl, Outputs out, uint32_t t,
-                                             uint32_t n_rows, uint32_t seqno) {
-  __shared__ uint32_t red_e[33];
-  const uint32_t BS = pol.max_batch, tid = threadIdx.x;
-  const uint32_t row0 = tid * ROWS_PER_THREAD;
-  uint32_t qfs[ROWS_PER_THREAD], n0 = 0;
-  const uint2 qv = row0 < n_rows ? __ldcg(reinterpret_cast<const uint2*>(ct.qf + row0)) : make_uint2(0x40404040u, 0x40404040u);
-#pragma unroll
-  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
-    qfs[j] = row0 + j < n_rows ? ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu : (uint32_t)QF_DEAD;
-    n0 += (qfs[j] & (QF_DEAD | QF_QMASK)) == 0 ? 1u : 0u;
-  }
-  uint32_t pos = block_excl_scan<uint32_t, SCAN_THREADS>(n0, red_e, nullptr);
-#pragma unroll
-  for (int j = 0; j < ROWS_PER_THREAD; ++j) {
-    if ((qfs[j] & (QF_DEAD | QF_QMASK)) != 0 || pos >= BS) continue;
-    const uint32_t s = row0 + j;
-    CandRec r;
-    load_rec(ct, s, &r);
-    out.cand[pos] = s;
-    out.cand_rec[pos] = r;
-    out.ckey[pos] = cand_key(r, t);
-    out.ckvb[pos] = blocks_for(pol, r.tok + r.exec + 1);  // R14
-    if (pos + 1 == BS) ctl->qs_bnd1 = s + 1;
-    ++pos;
-  }
-  if (tid == 0) {
-    ctl->qstar = 0;
-    ctl->mprime = BS;
-    ctl->n_cand_a = BS;
-    ctl->fast_seq = seqno;
-  }
-}
-
 // pre (A/B switch AUTX_SCAN_PRE): what a CTA does while it waits for the prologue (PDL).  Rows
 // below first_new (this step's first arrival slot) keep prog/base/mtime through the prologue
 // (it writes only new rows and the qf/loc of completed ones; everything earlier in the stream
@@ -570,7 +530,7 @@ __device__ __noinline__ void scan_emit_tile0(const Policy& pol, CallTable ct, Ct
 // program entries and of the previous batch's records (the gather's cold reads); 2: prog, base
 // and mtime early + the same prefetches.
 __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
-                                                               Outputs out, uint32_t pre, uint32_t emit) {
+                                                               Outputs out, uint32_t pre) {
   const uint32_t tid = threadIdx.x, tile = blockIdx.x;
   const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
   const uint32_t first_new = ctl->s_tail_prev;  // written before this step's chain
@@ -628,10 +588,6 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallT
     dense_rows<8>(pol, ct, pt, t, row0, qfs, prog, base, mtim, hq, npromo, nlive);
   }
   tile_counts(pol, ctl, out, tile, hq, npromo, nlive);
-  if (emit && tile == 0) {
-    __syncthreads();  // tile 0's Q_1 count (tid 0's store) and its rows' writes are visible in the CTA
-    if (__ldcg(out.tile_cnt) >= pol.max_batch) scan_emit_tile0(pol, ct, ctl, out, t, n_rows, ctl->s_seqno);
-  }
   CHAIN_END(1);
 }
 
@@ -706,7 +662,6 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
       if (tid == 1) ctl->n_live = stat;
     }
   }
-  if (is_tile && __ldcg(&ctl->fast_seq) == ctl->s_seqno) return;  // region A emitted by the dense pass
   if (!is_tile) {
     // previous batch: records (for preempt) and region-B keys
     const uint32_t j = (tile - ntiles) * NT + tid;
@@ -1698,8 +1653,7 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   } else {
     // prog + L2 prefetches while the prologue runs (AUTX_SCAN_PRE, default 1: measured ~0.4 us)
     static const uint32_t pre = getenv("AUTX_SCAN_PRE") ? (uint32_t)atoi(getenv("AUTX_SCAN_PRE")) : 1u;
-    static const uint32_t emit = getenv("AUTX_SCAN_EMIT") ? (uint32_t)atoi(getenv("AUTX_SCAN_EMIT")) : 1u;
-    launch_pdl(k_scan_tile, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, pre, emit);
+    launch_pdl(k_scan_tile, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, pre);
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
     launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out);

@@ -18,7 +18,6 @@ VARIANTS = {
     "no_graph": {"AUTX_NO_GRAPH": "1"},          # the step's kernels as separate launches, not a graph replay
     "finalize_lists": {"AUTX_FINALIZE_LISTS": "1"},  # finalize cuts the batch and writes the lists (not k_rank)
     "rank_narrow": {"AUTX_RANK_NARROW": "1"},    # half a warp per key in k_rank whatever the candidate count
-    "scan_emit0": {"AUTX_SCAN_EMIT": "0"},       # the gather selects region A even when tile 0 decides it
 }
 
 SUBSET = "fig2 or atlas_dag or mcts or chatbot or compaction or react or (random_tiny and 7)"
