@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libautx.so")
 SOURCES = ["autx_api.cu", "sched_kernels.cu", "swap_kernels.cu", "radix_kernels.cu"]
-HEADERS = ["autx_internal.cuh", "block_prims.cuh", os.path.join("..", "..", "include", "autx.h")]
+HEADERS = ["autx_internal.cuh", "block_prims.cuh", "idmap.h", os.path.join("..", "..", "include", "autx.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

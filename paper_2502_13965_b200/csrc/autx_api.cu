@@ -17,6 +17,7 @@
 
 #include "../../include/autx.h"
 #include "autx_internal.cuh"
+#include "idmap.h"
 
 using namespace autx;
 
@@ -54,8 +55,8 @@ struct autx_ctx {
   uint32_t* d_cslots = nullptr;
   ArrivalRec* d_arr = nullptr;
   // host-side maps
-  std::unordered_map<uint64_t, uint32_t> call_slot;   // active call id -> row
-  std::unordered_map<uint64_t, uint32_t> prog_row;    // program id -> process-table row
+  IdMap call_slot;                                    // active call id -> row
+  IdMap prog_row;                                     // program id -> process-table row
   std::vector<uint32_t> prog_free;
   uint32_t prog_next = 0;
   std::vector<uint32_t> prog_active;                  // active calls per program row
@@ -393,6 +394,8 @@ extern "C" autx_status autx_create(const autx_config* cfg, autx_ctx** outp) {
   // NULL = the legacy default stream (what torch.cuda.current_stream() is by default), so
   // library work orders with the caller's default-stream work
   ctx->stream = (cudaStream_t)c.stream;
+  ctx->call_slot.reserve(c.max_calls);
+  ctx->prog_row.reserve(c.max_programs);
   autx_status s = alloc_tables(ctx);
   if (s == AUTX_OK) {
     if (cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming) != cudaSuccess) s = AUTX_E_CUDA;
@@ -497,21 +500,21 @@ extern "C" autx_status autx_start_program(autx_ctx* ctx, uint64_t pid) {
 
 extern "C" autx_status autx_end_program(autx_ctx* ctx, uint64_t pid) {
   if (!ctx) return AUTX_E_INVAL;
-  auto it = ctx->prog_row.find(pid);
-  if (it == ctx->prog_row.end()) return fail(ctx, AUTX_E_NOENT, "unknown program %llu", (unsigned long long)pid);
-  if (ctx->prog_active[it->second] != 0)
+  uint32_t* it = ctx->prog_row.find(pid);
+  if (!it) return fail(ctx, AUTX_E_NOENT, "unknown program %llu", (unsigned long long)pid);
+  if (ctx->prog_active[*it] != 0)
     return fail(ctx, AUTX_E_STATE, "program %llu still has %u active calls", (unsigned long long)pid,
-                ctx->prog_active[it->second]);
+                ctx->prog_active[*it]);
   if (ctx->eq2) {  // the program's Eq. 2 operands go with it
-    for (uint64_t cid : ctx->prog_calls[it->second]) {
+    for (uint64_t cid : ctx->prog_calls[*it]) {
       auto l = ctx->lin_of.find(cid);
       ctx->lin_free.push_back(l->second);
       ctx->lin_of.erase(l);
     }
-    ctx->prog_calls[it->second].clear();
+    ctx->prog_calls[*it].clear();
   }
-  ctx->prog_free.push_back(it->second);
-  ctx->prog_row.erase(it);
+  ctx->prog_free.push_back(*it);
+  ctx->prog_row.erase(pid);
   return AUTX_OK;
 }
 
@@ -530,11 +533,11 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
   std::vector<uint32_t>& sl = ctx->comp_scratch;
   sl.resize(n);
   for (uint32_t i = 0; i < n; ++i) {
-    auto it = ctx->call_slot.find(ids[i]);
-    if (it == ctx->call_slot.end()) return fail(ctx, AUTX_E_NOENT, "unknown call %llu", (unsigned long long)ids[i]);
-    if (!ctx->stepped || ctx->ran_seq[it->second] != ctx->seqno)
+    const uint32_t* it = ctx->call_slot.find(ids[i]);
+    if (!it) return fail(ctx, AUTX_E_NOENT, "unknown call %llu", (unsigned long long)ids[i]);
+    if (!ctx->stepped || ctx->ran_seq[*it] != ctx->seqno)
       return fail(ctx, AUTX_E_STATE, "call %llu did not run in step %u", (unsigned long long)ids[i], ctx->t_last);
-    sl[i] = it->second;
+    sl[i] = *it;
   }
   {
     std::vector<uint32_t> srt(sl);
@@ -702,7 +705,7 @@ static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uin
     for (uint32_t i = 0; i < n; ++i) {
       if (poff[i + 1] < poff[i]) return fail(ctx, AUTX_E_INVAL, "parent offsets not ascending");
       if (poff[i + 1] - poff[i] >= (1u << 24)) return fail(ctx, AUTX_E_INVAL, "too many parents");
-      auto pr = ctx->prog_row.find(calls[i].program_id);
+      const uint32_t* pr = ctx->prog_row.find(calls[i].program_id);
       for (uint32_t k = poff[i]; k < poff[i + 1]; ++k) {
         auto l = ctx->lin_of.find(pids[k]);
         if (l == ctx->lin_of.end())
@@ -711,7 +714,7 @@ static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uin
         if (ctx->call_slot.count(pids[k]))
           return fail(ctx, AUTX_E_STATE, "parent %llu of call %llu has not completed", (unsigned long long)pids[k],
                       (unsigned long long)calls[i].call_id);
-        if (pr == ctx->prog_row.end() || ctx->lin_prog[l->second] != pr->second)
+        if (!pr || ctx->lin_prog[l->second] != *pr)
           return fail(ctx, AUTX_E_INVAL, "parent %llu of call %llu is in another program",
                       (unsigned long long)pids[k], (unsigned long long)calls[i].call_id);
       }
@@ -758,9 +761,9 @@ static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uin
   for (uint32_t i = 0; i < n; ++i) {
     const autx_call_desc& d = calls[i];
     uint32_t flags = 0;
-    auto it = ctx->prog_row.find(d.program_id);
+    const uint32_t* it = ctx->prog_row.find(d.program_id);
     uint32_t row;
-    if (it == ctx->prog_row.end()) {
+    if (!it) {
       if (!ctx->prog_free.empty()) { row = ctx->prog_free.back(); ctx->prog_free.pop_back(); }
       else row = ctx->prog_next++;
       ctx->prog_row[d.program_id] = row;
@@ -769,7 +772,7 @@ static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uin
       flags = 3;  // new program, first record: the prologue zeroes its entry
       ctx->staged_new_progs.insert(d.program_id);
     } else {
-      row = it->second;
+      row = *it;
       // created earlier in this (not yet launched) step: inherit 0 without reading the entry
       if (ctx->staged_new_progs.count(d.program_id)) flags = 1;
     }
@@ -1034,7 +1037,7 @@ static autx_status compact(autx_ctx* ctx) {
   }
   if (k != n) return fail(ctx, AUTX_E_STATE, "compaction: %u live rows on the host, %u active calls", k, n);
   std::fill(ctx->slot_live.begin() + k, ctx->slot_live.begin() + ctx->tail, 0);
-  for (auto& kv : ctx->call_slot) kv.second = o2n[kv.second];
+  ctx->call_slot.for_each([&](uint64_t, uint32_t& v) { v = o2n[v]; });
   ctx->low = 0;
   ctx->tail = n;
   ++ctx->n_compactions;
@@ -1253,11 +1256,11 @@ extern "C" autx_status autx_dump_calls(autx_ctx* ctx, autx_call_state* outp, uin
 
 extern "C" autx_status autx_program_state(autx_ctx* ctx, uint64_t pid, uint32_t* svc, uint64_t* pwait) {
   if (!ctx) return AUTX_E_INVAL;
-  auto it = ctx->prog_row.find(pid);
-  if (it == ctx->prog_row.end()) return fail(ctx, AUTX_E_NOENT, "unknown program");
+  const uint32_t* it = ctx->prog_row.find(pid);
+  if (!it) return fail(ctx, AUTX_E_NOENT, "unknown program");
   CK(cudaStreamSynchronize(ctx->stream));
   PInfo pi;
-  CK(cudaMemcpy(&pi, ctx->pt.info + it->second, sizeof pi, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&pi, ctx->pt.info + *it, sizeof pi, cudaMemcpyDeviceToHost));
   if (svc) *svc = pi.svc;
   if (pwait) *pwait = pi.pwait;
   return AUTX_OK;
@@ -1357,13 +1360,13 @@ static autx_status route_common(autx_ctx* ctx, const void* d_records, const autx
       if (!std::lexicographical_compare(a, a + 4, b, b + 4))
         return fail(ctx, AUTX_E_INVAL, "routing batch not in canonical order");
     }
-    auto it = ctx->prog_row.find(d.program_id);
+    const uint32_t* it = ctx->prog_row.find(d.program_id);
     uint32_t row;
-    if (it == ctx->prog_row.end()) {
+    if (!it) {
       autx_status s2 = new_program(ctx, d.program_id, &row);
       if (s2) return s2;
     } else {
-      row = it->second;
+      row = *it;
     }
     ctx->h_rarr[i] = RouteArr{row, d.input_tokens};
   }
