@@ -538,6 +538,13 @@ def main():
         stats.append(s.step_stats())
     s.set_timing(False)
     spans = chain_spans(stamp_phase)
+    # phases inside the finalize (raw stamps dbg[0, 32) of the step just run, thread 0 of the CTA,
+    # us after the finalize's first stamp): [0, 10] the finalize body, [20, 25] its ordering
+    fin_ph = {}
+    for i in list(range(0, 11)) + list(range(20, 26)):
+        v = [int(p[i]) - int(p[0]) for p in stamp_phase if int(p[i]) and int(p[0])]
+        if v:
+            fin_ph[i] = round(float(np.median(v)) / 1e3, 2)
     total_ms = sum(ms)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -615,6 +622,7 @@ def main():
         "step_ms": {"p10": float(np.percentile(ms, 10)), "p50": float(np.percentile(ms, 50)),
                     "p90": float(np.percentile(ms, 90)), "mean": statistics.mean(ms)},
         "chain_us": spans,
+        "finalize_phases_us": fin_ph,
         "kernel_span_us": span_k,
         "kernel_event_ms": ev_mean,
         "state": {"promotions_per_step": statistics.mean(promoted),

@@ -247,6 +247,12 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   CK(dalloc(&o.tile_cnt, ntiles * MAX_K));
   CK(dalloc(&o.sup_cnt, (ntiles / SUP_TILES + 1) * MAX_K));
   CK(cudaMemsetAsync(o.sup_cnt, 0, (ntiles / SUP_TILES + 1) * MAX_K * sizeof(uint32_t), ctx->stream));
+  CK(dalloc(&o.gtile, ntiles));
+  o.gtile_cap = (uint32_t)ntiles;
+  CK(cudaMemsetAsync(o.gtile, 0, ntiles * sizeof(uint32_t), ctx->stream));
+  CK(dalloc(&o.lb, ntiles * 4));
+  CK(cudaMemsetAsync(o.lb, 0, ntiles * 4 * sizeof(unsigned long long), ctx->stream));
+  CK(dalloc(&o.cq, (size_t)MAX_K * BS));
   o.hout = reinterpret_cast<HostOut*>(ctx->h_outblk);
   o.h_batch = reinterpret_cast<uint64_t*>(ctx->h_outblk + 64);
   o.h_admit = o.h_batch + BSp;
@@ -427,7 +433,7 @@ extern "C" autx_status autx_destroy(autx_ctx* ctx) {
   }
   void* dev[] = {ctx->d_tile_live, ctx->d_old2new, ctx->out.prev_pos, ctx->pt.info, ctx->pt.last_arr, ctx->pt.last_comp, ctx->pt.crit,
                  ctx->ctl, ctx->d_outblk, ctx->out.prev_slots, ctx->out.preempt_slots,
-                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.ckvb, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
+                 ctx->out.admit_slots, ctx->out.cand, ctx->out.cand_rec, ctx->out.prev_rec, ctx->out.ckey, ctx->out.ckvb, ctx->out.skey, ctx->out.sidx, ctx->out.srec, ctx->out.tile_cnt, ctx->out.sup_cnt, ctx->out.lb, ctx->out.cq, ctx->out.gtile, ctx->d_cslots, ctx->d_arr, ctx->kv.free_stack, ctx->kv.rs_free,
                  ctx->kv.rs_nblk, ctx->kv.rs_blocks, ctx->kv.host_free, ctx->kv.plan_out,
                  ctx->kv.plan_in, ctx->kv.plan_out_blocks, ctx->kv.plan_in_blocks,
                  ctx->kv.bt_offsets, ctx->kv.bt_blocks, ctx->d_pools, ctx->staging,

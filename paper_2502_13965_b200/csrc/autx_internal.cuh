@@ -121,6 +121,7 @@ struct Ctl {
   uint32_t s_t, s_n_rows, s_seqno, s_n_active;
   uint32_t s_tail_prev;  // rows older than this step's arrivals (finalize / compaction): the scan
                          // may read them before its PDL wait
+  uint32_t scan_ticket;  // k_scan_emit: tile ticket (look-back order); reset by finalize
   alignas(128) uint32_t qpart[QP_LINES][32];
   unsigned long long dbg[96];  // [32, 64) live chain stamps, [64, 96) last step's (AUTX_CHAIN_STAMPS)  // %globaltimer stamps of kernel phases (autx_phase_times)
 };
@@ -212,10 +213,16 @@ struct Outputs {
   uint32_t use_prev_pos;     // finalize tests batch membership of the previous batch by prev_pos
   uint32_t rank_lists;       // k_rank writes batch / admit lists and accounting (no KV allocator)
   uint32_t rank_wide;        // k_rank: a warp per key when the candidates fill <= half its grid
+  uint32_t rank_buckets;     // k_rank: O(BS) bucket ranks when region B is empty (else all-pairs count)
   uint32_t* ckvb;            // [2 BS] kvb of each key in ckey (R14)
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* sup_cnt;         // [ceil(ntiles_cap / SUP_TILES) * MAX_K] per-queue counts of super-tiles
                              // (scan: atomics; gather: prefix; finalize: reset)
+  uint32_t* gtile;           // [ntiles_cap] k_gather_ss: 1 if the tile held candidates last step (prefetch hint)
+  uint32_t gtile_cap;
+  unsigned long long* lb;    // [ntiles_cap * 4] k_scan_emit look-back words (4 queues each; finalize: reset)
+  CandRec* cq;               // [MAX_K * max_batch] k_scan_emit: the first max_batch live calls of each
+                             // queue, in table order (queue q at q * max_batch)
   HostOut* hout;             // host-visible counts (pinned)
   HostOut* d_hout;           // device copy of the counts (copied out with the lists by one DMA)
   int zero_copy;             // 1: finalize stores the host mirrors itself over PCIe (A/B switch)

@@ -16,6 +16,7 @@
 // Every step of Alg. 1 runs here; the host only stages records.  Citations: see autx.h.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "autx_internal.cuh"
 #include "block_prims.cuh"
@@ -485,7 +486,7 @@ __device__ __forceinline__ void dense_rows(const Policy& pol, CallTable& ct, con
 // Per-tile and per-super-tile queue counts + promotion / live totals of one CTA.
 template <int NT = SCAN_THREADS>
 __device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs& out, uint32_t tile, uint64_t hq,
-                                            uint32_t npromo, uint32_t nlive) {
+                                            uint32_t npromo, uint32_t nlive, uint32_t* s_cnt_out = nullptr) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t wq16[NW][MAX_K / 2];  // per warp: 16-bit counts of queues 2w, 2w + 1
   __shared__ uint32_t wn[NW];
@@ -511,7 +512,8 @@ __device__ __forceinline__ void tile_counts(const Policy& pol, Ctl* ctl, Outputs
       for (int w = 0; w < NW; ++w) c += (wq16[w][tid >> 1] >> (16 * (tid & 1))) & 0xFFFFu;
     }
     out.tile_cnt[(size_t)tile * MAX_K + tid] = c;
-    if (c) atomicAdd(out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, c);
+    if (s_cnt_out) s_cnt_out[tid] = c;
+    else if (c) atomicAdd(out.sup_cnt + (tile / SUP_TILES) * MAX_K + tid, c);
   } else if (tid == 32) {
     uint32_t a = 0, b = 0;
 #pragma unroll
@@ -588,6 +590,193 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallT
     dense_rows<8>(pol, ct, pt, t, row0, qfs, prog, base, mtim, hq, npromo, nlive);
   }
   tile_counts(pol, ctl, out, tile, hq, npromo, nlive);
+  CHAIN_END(1);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Dense pass that also emits region A's raw material (default select pipeline; AUTX_GATHER=1 keeps
+// k_gather_ss + k_rank): every tile learns, per queue, how many live calls of that queue the
+// earlier tiles hold, saturated at the resident capacity BS (single-pass decoupled look-back,
+// tiles taken by ticket so that every tile waited on has started), and writes each live call
+// whose rank inside its queue is below BS to cq[q][rank].  Region A is then the concatenation of
+// cq[q] for q < q* and the first m' of cq[q*]; the finalize reads q*, m' from the last tile's
+// inclusive prefix.  Only the first BS calls of each queue are ever emitted, so the pass writes
+// O(K BS) records whatever the table size.
+//   Look-back word (one per 4 queues and tile): four 13-bit saturated counts (bits 0, 13, 26, 39;
+//   BS <= 2048, so a sum of two fits before it is clamped) and a 2-bit flag (62-63): 0 = not yet,
+//   1 = this tile's own counts, 2 = inclusive prefix.  The word carries its own data, so a relaxed
+//   load needs no fence.  The finalize zeroes the words after the step.
+// ---------------------------------------------------------------------------------------------
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_PRE = 2ull << 62, LB_VAL = (1ull << 52) - 1;
+constexpr uint32_t LB_SPIN_LIMIT = 1u << 22;
+__device__ __forceinline__ unsigned long long lb_sat(unsigned long long v, uint32_t cap) {
+  unsigned long long r = 0;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) r |= (unsigned long long)min((uint32_t)(v >> (13 * f)) & 0x1FFFu, cap) << (13 * f);
+  return r;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_emit(Policy pol, CallTable ct, ProgTable pt, Ctl* ctl,
+                                                               Outputs out, uint32_t pre) {
+  constexpr uint32_t FULL = 0xffffffffu;
+  __shared__ uint32_t s_tile, s_emit, s_ne;
+  __shared__ uint32_t s_es[TILE], s_er[TILE];  // emitted rows: slot; queue << 16 | rank
+  __shared__ uint32_t s_cnt[MAX_K];
+  __shared__ unsigned long long s_ex[4];  // this tile's exclusive prefix words
+  __shared__ unsigned long long red64[33];
+  const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  if (tid == 0) { s_tile = atomicAdd(&ctl->scan_ticket, 1u); s_ne = 0; }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t row0 = tile * TILE + tid * ROWS_PER_THREAD;
+  const uint32_t first_new = ctl->s_tail_prev;  // written before this step's chain
+  const bool early = pre != 0 && row0 + ROWS_PER_THREAD <= first_new;
+  uint4 p0, p1;
+  if (early) {
+    p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+    p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    if (pol.beta_den != 0) {
+      const uint32_t pr[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j == 0 || pr[j] != pr[j - 1]) prefetch_l2(pt.info + pr[j]);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  CHAIN_BEGIN(1);
+  const uint32_t t = ctl->s_t, n_rows = ctl->s_n_rows;
+  const uint32_t K = pol.K, cap = pol.max_batch, nwd = (K + 3) / 4;
+  uint64_t hq = 0;
+  uint32_t npromo = 0, nlive = 0;
+  uint32_t qfs[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) qfs[j] = QF_DEAD;
+  if (row0 < n_rows) {
+    const uint2 qv = __ldcs(reinterpret_cast<const uint2*>(ct.qf + row0));
+    if (!early) {
+      p0 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0));
+      p1 = __ldcs(reinterpret_cast<const uint4*>(ct.prog + row0 + 4));
+    }
+    const uint4 b0 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0));
+    const uint4 b1 = __ldcs(reinterpret_cast<const uint4*>(ct.base + row0 + 4));
+    const uint4 m0 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0));
+    const uint4 m1 = __ldcs(reinterpret_cast<const uint4*>(ct.mtime + row0 + 4));
+    uint32_t prog[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    uint32_t base[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint32_t mtim[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) qfs[j] = ((j < 4 ? qv.x : qv.y) >> (8 * (j & 3))) & 0xffu;
+    dense_rows<8>(pol, ct, pt, t, row0, qfs, prog, base, mtim, hq, npromo, nlive);
+  }
+  tile_counts(pol, ctl, out, tile, hq, npromo, nlive, s_cnt);
+  __syncthreads();
+  // publish this tile's counts (tile 0: they are its inclusive prefix), then look back
+  // (lane 0 of warp w owns word w: its own-count store precedes its prefix store)
+  if (w < nwd && lane == 0) {
+    unsigned long long own = 0;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) own |= (unsigned long long)min(s_cnt[4 * w + f], cap) << (13 * f);
+    st_relaxed_u64(out.lb + (size_t)tile * 4 + w, own | (tile == 0 ? LB_PRE : LB_AGG));
+    if (tile == 0) s_ex[w] = 0;
+  }
+  if (tile > 0 && w < nwd) {
+    // warp w looks back over word w, 32 predecessors per round, to the nearest inclusive prefix
+    // (measured: a block-wide 256-tile window was slower, 17 vs 11.7 us for the pass)
+    unsigned long long acc = 0;
+    int32_t base = (int32_t)tile;
+    uint32_t spins = 0;
+    while (true) {
+      const int32_t p = base - 1 - (int32_t)lane;
+      unsigned long long v = p >= 0 ? ld_relaxed_u64(out.lb + (size_t)p * 4 + w) : LB_PRE;
+      while (!__all_sync(FULL, (v >> 62) != 0)) {
+        if ((v >> 62) == 0) v = ld_relaxed_u64(out.lb + (size_t)p * 4 + w);
+        if (++spins > LB_SPIN_LIMIT && (v >> 62) == 0) {  // a predecessor never published: fail the step
+          set_err(ctl, AUTX_E_CUDA, 0xB0000000u | tile);
+          v = LB_PRE;
+        }
+      }
+      const uint32_t pm = __ballot_sync(FULL, (v >> 62) == 2);
+      const uint32_t upto = pm ? __ffs(pm) - 1 : 31;
+      unsigned long long x = lane <= upto ? (v & LB_VAL) : 0ull;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) x = lb_sat(x + __shfl_xor_sync(FULL, x, d), cap);
+      acc = lb_sat(acc + x, cap);
+      if (pm) break;
+      base -= 32;
+    }
+    if (lane == 0) {
+      unsigned long long o = 0;
+#pragma unroll
+      for (int f = 0; f < 4; ++f) o |= (unsigned long long)min(s_cnt[4 * w + f], cap) << (13 * f);
+      s_ex[w] = acc;
+      st_relaxed_u64(out.lb + (size_t)tile * 4 + w, lb_sat(acc + o, cap) | LB_PRE);
+    }
+  }
+  __syncthreads();
+  // queues this tile emits: live calls here and fewer than BS before it
+  if (tid < 32) {
+    const uint32_t ex = tid < K ? (uint32_t)(s_ex[tid >> 2] >> (13 * (tid & 3))) & 0x1FFFu : cap;
+    const uint32_t b = __ballot_sync(FULL, tid < K && s_cnt[tid] > 0 && ex < cap);
+    if (tid == 0) s_emit = b;
+  }
+  __syncthreads();
+  const uint32_t emit = s_emit;
+  if (emit) {
+    // rank of each of this thread's rows inside its queue: the earlier tiles (s_ex), the earlier
+    // threads (block scans of 16-bit fields, 4 queues per scan), the earlier rows of this thread
+    for (uint32_t g = 0; g < nwd; ++g) {
+      if (!((emit >> (4 * g)) & 0xFu)) continue;
+      unsigned long long v = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t q = qfs[j] & QF_QMASK;
+        if (!(qfs[j] & QF_DEAD) && (q >> 2) == g) v += 1ull << (16 * (q & 3));
+      }
+      unsigned long long ex = block_excl_scan<unsigned long long, SCAN_THREADS>(v, red64, nullptr);
+      const unsigned long long exw = s_ex[g];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t q = qfs[j] & QF_QMASK;
+        if (!(qfs[j] & QF_DEAD) && (q >> 2) == g) {
+          const uint32_t f = q & 3;
+          const uint32_t r = ((uint32_t)(exw >> (13 * f)) & 0x1FFFu) + ((uint32_t)(ex >> (16 * f)) & 0xFFFFu);
+          ex += 1ull << (16 * f);
+          if (((emit >> q) & 1u) && r < cap) {
+            // the emitted rows go through a shared-memory list so that one thread loads one
+            // record (all in one round, no per-row register arrays in this 64-register kernel)
+            const uint32_t pos = atomicAdd(&s_ne, 1u);
+            s_es[pos] = row0 + j;
+            s_er[pos] = q << 16 | r;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t ne = s_ne;
+    for (uint32_t i = tid; i < ne; i += SCAN_THREADS) {
+      const uint32_t sl = s_es[i], qr = s_er[i];
+      CandRec r;
+      r.cid = ct.cid[sl];
+      r.slot = sl;
+      r.arr = ct.arr[sl];
+      r.tok = ct.tok[sl];
+      r.exec = ct.exec[sl];
+      r.mtime = ct.mtime[sl];    // the dense pass's writes (this CTA, before the barriers above)
+      r.quanta = ct.quanta[sl];
+      r.qf = ct.qf[sl];
+      r._pad = (r.qf & QF_RES) ? ct.bidx[sl] : NONE;  // previous resident index
+      out.cq[(size_t)(qr >> 16) * cap + (qr & 0xFFFFu)] = r;
+    }
+  }
   CHAIN_END(1);
 }
 
@@ -727,6 +916,7 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
   // tiles without candidates leave now (their SM slots go to the next kernel's CTAs); the
   // boundary row is always in a tile with candidates
   if (STAMPS_ON && tile == 0 && tid == 0) ctl->dbg[57] = globaltimer();
+  if (tid == 0 && out.gtile) out.gtile[tile] = s_has;
   if (!s_has) return;
   const uint32_t qs = s_qs, m = s_m;
   uint32_t qfs[8], na = 0, nq = 0;
@@ -809,6 +999,23 @@ __device__ __forceinline__ void gather_ss_body(Policy& pol, CallTable& ct, Ctl* 
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS, 4) k_gather_ss(Policy pol, CallTable ct, Ctl* ctl, Outputs out) {
+  // a tile that held candidates in the previous step likely holds them again (region A is the
+  // head of q* in table order): pull its record columns into L2 while the dense pass runs, so
+  // that the emission below reads them from L2 instead of DRAM (2 prefetches per thread)
+  if (out.gtile && blockIdx.x < out.gtile_cap && out.gtile[blockIdx.x]) {
+    const size_t r0 = (size_t)blockIdx.x * TILE;
+#pragma unroll
+    for (uint32_t k = 0; k < 2; ++k) {  // 128-B lines: 128 of cid, then 64 of each 4-byte column
+      const uint32_t L = threadIdx.x + k * SCAN_THREADS;
+      if (L < 128) {
+        prefetch_l2(ct.cid + r0 + 16 * L);
+      } else {
+        const uint32_t c = (L - 128) >> 6, o = 32 * ((L - 128) & 63);
+        const uint32_t* col = c == 0 ? ct.arr : c == 1 ? ct.tok : c == 2 ? ct.exec : c == 3 ? ct.mtime : c == 4 ? ct.quanta : ct.bidx;
+        prefetch_l2(col + r0 + o);
+      }
+    }
+  }
   pdl_wait();
   pdl_trigger();
   const uint32_t t = ctl->s_t, n_rows = ctl->s_n_rows;
@@ -828,9 +1035,9 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_gather_ss(Policy pol, CallT
 // (Alg. 1 l.20-23), allocate KV blocks and build the swap plan.
 // ---------------------------------------------------------------------------------------------
 extern __shared__ unsigned char fin_smem[];
-template <int NT, int R, bool LISTS = false>
+template <int NT, int R, bool LISTS = false, bool ORD = false, bool SEL = false>
 __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
-                              uint32_t t, uint32_t np, uint32_t seqno);
+                              uint32_t t, uint32_t np, uint32_t seqno, const CandRec (&pp)[R], uint32_t n_prev_pre);
 
 __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
@@ -861,7 +1068,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   // cover the buffer's capacity, so they need not wait for the counts above (one round trip).
   constexpr int RK = 8;
   const uint32_t cap = 2 * pol.max_batch;
-  uint32_t nv = 0;
+  uint32_t nv = 0, nbv = 0;
   for (uint32_t c0 = 0; c0 < cap; c0 += RK * RANK_THREADS) {
     uint64_t kk[RK];
     uint32_t kb[RK];
@@ -878,12 +1085,146 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
         uint64_t k = kk[r];
         if (i >= na && (uint32_t)(k & 0x7FFFFFFFu) < bnd1) k = ~0ull;
         nv += k != ~0ull ? 1u : 0u;
+        nbv += (i >= na && k != ~0ull) ? 1u : 0u;
         rk[i] = k;
         rkv[i] = kb[r];
       }
     }
   }
-  if (blockIdx.x * (RANK_PER_CTA / 2) < n) {
+  // region B holds a valid key (a previous-list call of q* past region A's boundary: empty in
+  // every bench workload): the general all-pairs count below; else the O(BS) bucket ranks
+  const bool fast = !__syncthreads_or(nbv != 0) && out.rank_buckets;
+  bool lead = false;
+  uint32_t cnt = 0, eo = 0, kvs = 0, nad = 0, own_kvb = 0;
+  uint64_t x = 0;
+  CandRec rec;
+  if (fast && e0 < na) {
+    // Region A is sorted inside each of its 2K (queue, not-running) buckets (table order, or the
+    // radix order), so a key's rank is sum_{q' < q} |A_q'| + its index in its bucket + its lower
+    // bound in the other bucket of its queue; the kvb prefix and the admit rank follow from the
+    // kvb prefix sums in bucket order and the not-running bucket sizes.  Every CTA splits the
+    // <= BS keys (8 per thread) and ranks its own RANK_PER_CTA keys with one thread each.
+    constexpr int IPT = MAX_BATCH / RANK_THREADS;
+    constexpr int NWR = RANK_THREADS / 32;
+    __shared__ uint32_t f_bcnt[32][NWR], f_boff[33], f_nr[MAX_K + 1], f_present;
+    const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+    const uint32_t ek = e0 + tid;
+    lead = tid < RANK_PER_CTA && ek < na;
+    if (lead) rec = out.cand_rec[ek];  // issued first: its latency hides behind the split
+    uint64_t* s_sub = ck;   // keys in bucket order
+    uint32_t* s_pos = ci;   // table index -> bucket-order position
+    uint32_t* s_kvp = ckv;  // exclusive kvb prefix in bucket order, [na] = total
+    if (STAMPS_ON && blockIdx.x == 0 && tid == 0) ctl->dbg[54] = globaltimer();
+    if (tid == 0) f_present = 0;
+    __syncthreads();
+    uint32_t bk[IPT], loc[IPT], pres = 0;
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+      const uint32_t i = tid * IPT + r;
+      bk[r] = 32;
+      if (i < na) {
+        const uint64_t k = rk[i];
+        bk[r] = (uint32_t)(k >> 59) * 2u + (uint32_t)((k >> 31) & 1u);
+        pres |= 1u << bk[r];
+      }
+    }
+    pres = __reduce_or_sync(0xffffffffu, pres);
+    if (lane == 0 && pres) atomicOr(&f_present, pres);
+    __syncthreads();
+    const uint32_t present = f_present;
+    {
+      const uint32_t lt = (1u << lane) - 1u;
+      for (uint32_t pm = present; pm; pm &= pm - 1u) {
+        const uint32_t b = __ffs(pm) - 1u;
+        uint32_t below = 0, tot = 0, own = 0;
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+          const uint32_t bl = __ballot_sync(0xffffffffu, bk[r] == b);
+          below += __popc(bl & lt);
+          tot += __popc(bl);
+        }
+#pragma unroll
+        for (int r = 0; r < IPT; ++r)
+          if (bk[r] == b) loc[r] = below + own++;
+        if (lane == 0) f_bcnt[b][w] = tot;
+      }
+    }
+    __syncthreads();
+    for (uint32_t b = w; b < 32; b += NWR) {
+      const bool on = (present >> b) & 1u;
+      const uint32_t v = on && lane < (uint32_t)NWR ? f_bcnt[b][lane] : 0u;
+      const uint32_t inc = warp_incl_scan(v);
+      if (on && lane < (uint32_t)NWR) f_bcnt[b][lane] = inc - v;
+      if (lane == 31) f_boff[b] = inc;  // the bucket's size, for now
+    }
+    __syncthreads();
+    if (w == 0) {
+      const uint32_t sz = f_boff[lane];
+      const uint32_t inc = warp_incl_scan(sz);
+      f_boff[lane] = inc - sz;
+      if (lane == 31) f_boff[32] = inc;
+      // not-running calls of the queues before q: the sizes of buckets 2 q' + 1, q' < q
+      const uint32_t nrs = (lane & 1u) ? sz : 0u;
+      const uint32_t nri = warp_incl_scan(nrs);
+      if (lane & 1u) f_nr[(lane >> 1) + 1] = nri;
+      if (lane == 0) f_nr[0] = 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+      const uint32_t i = tid * IPT + r;
+      if (bk[r] < 32) {
+        const uint32_t p = f_boff[bk[r]] + f_bcnt[bk[r]][w] + loc[r];
+        s_sub[p] = rk[i];
+        s_pos[i] = p;
+        s_kvp[p] = rkv[i];
+      }
+    }
+    __syncthreads();
+    if (lists) {  // kvb prefix sums in bucket order
+      uint32_t kv[IPT], sum = 0;
+#pragma unroll
+      for (int r = 0; r < IPT; ++r) {
+        const uint32_t i = tid * IPT + r;
+        kv[r] = i < na ? s_kvp[i] : 0u;
+        sum += kv[r];
+      }
+      uint32_t tot;
+      uint32_t run = block_excl_scan<uint32_t, RANK_THREADS>(sum, red_r, &tot);
+#pragma unroll
+      for (int r = 0; r < IPT; ++r) {
+        const uint32_t i = tid * IPT + r;
+        if (i < na) s_kvp[i] = run;
+        run += kv[r];
+      }
+      if (tid == 0) s_kvp[na] = tot;
+      __syncthreads();
+    }
+    if (STAMPS_ON && blockIdx.x == 0 && tid == 0) ctl->dbg[55] = globaltimer();
+    if (blockIdx.x == 0 && tid == 0) {
+      ctl->n_cand_b = 0;
+      if (STAMPS_ON) { ctl->dbg[52] = na; ctl->dbg[53] = n; }
+    }
+    if (lead) {
+      x = rk[ek];
+      eo = ek;
+      own_kvb = rkv[ek];
+      const uint32_t q = (uint32_t)(x >> 59), nr = (uint32_t)((x >> 31) & 1u);
+      const uint32_t b = 2 * q + nr, o = b ^ 1u, pos = s_pos[ek];
+      const uint32_t ob = f_boff[o], on = f_boff[o + 1] - ob;
+      uint32_t lb = 0;  // keys of the other bucket below x
+#pragma unroll
+      for (uint32_t step = (uint32_t)MAX_BATCH; step > 0; step >>= 1)
+        if (lb + step <= on && s_sub[ob + lb + step - 1] < x) lb += step;
+      const uint32_t idx = pos - f_boff[b];
+      cnt = f_boff[2 * q] + idx + lb;
+      if (lists) {
+        kvs = s_kvp[f_boff[2 * q]] + (s_kvp[pos] - s_kvp[f_boff[b]]) + (s_kvp[ob + lb] - s_kvp[ob]);
+        nad = f_nr[q] + (nr ? idx : lb);
+      }
+    }
+    if (STAMPS_ON && blockIdx.x == 0 && tid == 0) ctl->dbg[56] = globaltimer();
+  } else if (!fast && blockIdx.x * (RANK_PER_CTA / 2) < n) {
     // (2) compact the candidates (same deterministic order in every CTA): sentinels rank last and
     // nobody reads them, so only the n_valid candidates are ranked and compared against
     if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[54] = globaltimer();
@@ -907,12 +1248,10 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     const bool wide = 2 * n_valid <= gridDim.x * RANK_PER_CTA && out.rank_wide;
     const uint32_t subn = wide ? 32u : (uint32_t)RANK_SUB;
     const uint32_t e = (wide ? blockIdx.x * (RANK_PER_CTA / 2) : e0) + threadIdx.x / subn, sub = threadIdx.x % subn;
-    uint32_t cnt = 0, eo = 0, kvs = 0, nad = 0;
-    uint64_t x = 0;
-    CandRec rec;
     if (e < n_valid) {
       x = ck[e];
       eo = ci[e];
+      own_kvb = ckv[e];
       if (sub == 0) rec = eo < na ? out.cand_rec[eo] : out.prev_rec[eo - na];
       if (lists) {
         // with the rank, the kvb prefix (Alg. 1 l.34-37) and the admit rank (smaller keys of
@@ -940,7 +1279,10 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
       }
     }
     if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[56] = globaltimer();
-    if (sub == 0 && e < n_valid) {
+    lead = sub == 0 && e < n_valid;
+  }
+  {
+    if (lead) {
       out.skey[cnt] = x;
       out.sidx[cnt] = eo;
       out.srec[cnt] = rec;
@@ -951,7 +1293,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
         // Alg. 1 l.32-39 for this key alone: kvb >= 1 makes the inclusive prefix strictly
         // increasing, so "count <= BS and sum kvb <= P" holds exactly on a prefix of the order
         // (the first misfit stops, R13); the batch entries write their lists and accounting
-        const uint32_t incl = kvs + ckv[e];
+        const uint32_t incl = kvs + own_kvb;
         const uint32_t BS = pol.max_batch;
         if (cnt < BS && (pol.kv_budget == AUTX_INF || incl <= pol.kv_budget)) {
           const uint32_t sl = rec.slot;
@@ -990,13 +1332,285 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   CHAIN_END(4);
 }
 
-template <int NT, int R, bool LISTS>
+// ---------------------------------------------------------------------------------------------
+// a5 inside the finalize (default select pipeline; AUTX_RANK_KERNEL=1 keeps k_rank): the order of
+// the <= 2 BS candidates in O(BS) work on one CTA, no all-pairs count.
+//   Region A (the gather's candidates) is in table order, i.e. (arrival, seq) order (rows are
+//   registered in arrival order, R11).  Split it into 2K sub-lists by (q, not-running): inside one
+//   sub-list the key (q, arrival, not-running, seq) orders exactly as the table does, so each
+//   sub-list is sorted as it stands.  A key's rank is then
+//       sum_{q' < q} |A_q'|  +  its index in its own sub-list  +  lower_bound in the other
+//       sub-list of its queue  (+ lower_bound in the sorted region B when q = q*).
+//   Region B (previous-resident calls of q* past region A's boundary, <= BS; empty in every bench
+//   workload) is sorted by a bitonic network in shared memory; a B key's rank is its index in B
+//   plus its lower bounds in the two sub-lists of q*.
+// Writes the first m = min(BS, |A| + |B|) keys (uk) and records (s_rec) in key order and, per
+// previous-resident entry, its sorted position (s_ppos; NONE if it is no candidate).  Returns
+// |B|.  pr: the previous resident list's records (finalize's preempt input), loaded here.
+// ---------------------------------------------------------------------------------------------
+// SEL (k_scan_emit ran instead of k_gather_ss): the selection itself is derived here.  q* is the
+// first queue whose inclusive total reaches BS (the last tile's saturated inclusive prefix holds
+// the totals: only whether a total reaches BS matters past the boundary), m' = BS - the totals
+// before it, and region A = cq[q] for q < q* plus the first m' of cq[q*], concatenated in queue
+// order (so each queue's calls stay in table order).  The previous resident list's records are
+// read from the call table (its slots were loaded before the PDL wait: ps).
+template <int NT, int R, bool SEL>
+__device__ __forceinline__ uint32_t order_candidates(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out,
+                                                     uint32_t t, uint64_t* uk, CandRec* s_rec, uint64_t* s_sub,
+                                                     uint64_t* s_bk, uint32_t* s_ppos, CandRec (&pr)[R],
+                                                     const CandRec (&pp)[R], uint32_t n_prev_pre,
+                                                     uint32_t& live_out, uint32_t& promo_out) {
+  constexpr int NW = NT / 32;
+  constexpr uint32_t FULL = 0xffffffffu;
+  __shared__ uint32_t s_bcnt[32][NW];  // per (bucket, warp): items, then the warp's exclusive offset
+  __shared__ uint32_t s_boff[33];      // bucket start in s_sub (bucket b = 2 q + not-running)
+  __shared__ uint32_t s_present, s_nb;
+  __shared__ uint32_t s_qoff[MAX_K + 1], s_sel[4];  // SEL: region A's queue offsets; nA, q*, m', bnd1
+  const uint32_t tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const uint32_t BS = pol.max_batch, K = pol.K;
+  uint32_t nA, n_prev, bnd1, qs;
+  uint64_t ka[R];
+  CandRec ra[R];
+  STAMP(20);
+  if constexpr (SEL) {
+    n_prev = n_prev_pre;
+    // (1) one round: the totals, the step's counters and the previous list's records
+    if (w == 0) {
+      const uint32_t n_rows = ctl->s_n_rows, ntiles = n_rows ? (n_rows + TILE - 1) / TILE : 1u;
+      const unsigned long long v = lane < (K + 3) / 4 ? ld_relaxed_u64(out.lb + (size_t)(ntiles - 1) * 4 + lane) : 0ull;
+      uint32_t stat = lane < 2 * QP_LINES ? __ldcg(&ctl->qpart[lane >> 1][MAX_K + (lane & 1)]) : 0u;
+#pragma unroll
+      for (int d = 2; d < 32; d <<= 1) stat += __shfl_xor_sync(FULL, stat, d);
+      const unsigned long long vq = __shfl_sync(FULL, v, (lane >> 2) & 3);
+      const uint32_t tq = lane < K ? (uint32_t)(vq >> (13 * (lane & 3))) & 0x1FFFu : 0u;
+      const uint32_t incl = warp_incl_scan(tq);
+      const uint32_t b = __ballot_sync(FULL, lane < K && incl >= BS);
+      const uint32_t q_s = b ? __ffs(b) - 1 : K;
+      const uint32_t excl_s = __shfl_sync(FULL, incl - tq, q_s & 31);
+      const uint32_t tot = __shfl_sync(FULL, incl, 31);
+      const uint32_t m = q_s < K ? BS - excl_s : 0u;
+      const uint32_t take = lane < q_s ? tq : (lane == q_s ? m : 0u);
+      const uint32_t ti = warp_incl_scan(take);
+      if (lane <= MAX_K) s_qoff[lane] = ti - take;
+      const uint32_t live = __shfl_sync(FULL, stat, 1);  // even lanes: promotions, odd: live rows
+      if (lane == 0) {
+        s_sel[0] = q_s < K ? BS : tot;
+        s_sel[1] = q_s;
+        s_sel[2] = m;
+        promo_out = stat;
+        live_out = live;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (tid * R + r < n_prev) {
+        // the fields the dense pass may change; the others were read before the PDL wait
+        const uint32_t sl = pp[r].slot;
+        pr[r] = pp[r];
+        pr[r].qf = ct.qf[sl];
+        pr[r].mtime = ct.mtime[sl];
+        pr[r].quanta = ct.quanta[sl];
+        pr[r]._pad = (pr[r].qf & QF_RES) ? pp[r]._pad : NONE;
+      }
+    if (tid == 0) { s_present = 0; s_nb = 0; }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (tid * R + r < n_prev) s_ppos[tid * R + r] = NONE;
+    __syncthreads();
+    STAMP(21);
+    nA = s_sel[0];
+    qs = s_sel[1];
+    // (2) region A's records (dependent on the totals: one more round)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t i = tid * R + r;
+      if (i < nA) {
+        uint32_t q = 0;
+        for (uint32_t k = 1; k < K; ++k) q = i >= s_qoff[k] ? k : q;  // offsets are non-decreasing
+        ra[r] = out.cq[(size_t)q * BS + (i - s_qoff[q])];
+        ka[r] = cand_key(ra[r], t);
+        if (i + 1 == nA && qs < K) s_sel[3] = ra[r].slot + 1;  // region A's last q* call
+      }
+    }
+    if (tid == 0) {
+      ctl->qstar = qs;
+      ctl->mprime = s_sel[2];
+      ctl->n_cand_a = nA;
+    }
+    __syncthreads();
+    bnd1 = qs < K ? s_sel[3] : 0u;
+  } else {
+    nA = ctl->n_cand_a; n_prev = ctl->n_prev; bnd1 = ctl->qs_bnd1; qs = ctl->qstar;
+    // (1) one round of loads, unconditional below BS (the buffers hold >= BS entries)
+    {
+      const uint64_t* __restrict__ ck = out.ckey;
+      const CandRec* __restrict__ cr = out.cand_rec;
+      const CandRec* __restrict__ prc = out.prev_rec;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t i = tid * R + r;
+        if (i < BS) {
+          ka[r] = ck[i];
+          ra[r] = cr[i];
+          pr[r] = prc[i];
+        }
+      }
+    }
+    if (tid == 0) { s_present = 0; s_nb = 0; }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (tid * R + r < n_prev) s_ppos[tid * R + r] = NONE;
+    __syncthreads();
+  }
+  uint32_t bk[R], pres = 0, nbl = 0;
+  uint64_t kb[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t i = tid * R + r;
+    bk[r] = 32;  // no item
+    if (i < nA) {
+      bk[r] = (uint32_t)(ka[r] >> 59) * 2u + (uint32_t)((ka[r] >> 31) & 1u);
+      pres |= 1u << bk[r];
+    }
+    // region B: the gather's rule (live, queue q*, past region A's boundary slot)
+    kb[r] = ~0ull;
+    if (i < n_prev && !(pr[r].qf & QF_DEAD) && (pr[r].qf & QF_QMASK) == qs && pr[r].slot >= bnd1) {
+      kb[r] = cand_key(pr[r], t);
+      ++nbl;
+    }
+  }
+  pres = __reduce_or_sync(FULL, pres);
+  nbl = __reduce_add_sync(FULL, nbl);
+  if (lane == 0) {
+    if (pres) atomicOr(&s_present, pres);
+    if (nbl) atomicAdd(&s_nb, nbl);
+  }
+  __syncthreads();
+  STAMP(22);
+  const uint32_t present = s_present, nB = s_nb;
+  // (2) stable position inside the warp per present bucket (items ordered by (lane, r))
+  uint32_t loc[R];
+  {
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t pm = present; pm; pm &= pm - 1u) {
+      const uint32_t b = __ffs(pm) - 1u;
+      uint32_t below = 0, tot = 0, own = 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t bl = __ballot_sync(FULL, bk[r] == b);
+        below += __popc(bl & lt);
+        tot += __popc(bl);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (bk[r] == b) loc[r] = below + own++;
+      if (lane == 0) s_bcnt[b][w] = tot;
+    }
+  }
+  __syncthreads();
+  // (3) per bucket, the warps' exclusive offsets (warp w: buckets w, w + NW, ...); then the
+  // bucket starts
+  for (uint32_t b = w; b < 32; b += NW) {
+    const bool on = (present >> b) & 1u;
+    const uint32_t v = on && lane < (uint32_t)NW ? s_bcnt[b][lane] : 0u;
+    const uint32_t inc = warp_incl_scan(v);
+    if (on && lane < (uint32_t)NW) s_bcnt[b][lane] = inc - v;
+    if (lane == 31) s_boff[b] = inc;  // the bucket's size, for now
+  }
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t sz = s_boff[lane];
+    const uint32_t inc = warp_incl_scan(sz);
+    s_boff[lane] = inc - sz;
+    if (lane == 31) s_boff[32] = inc;
+  }
+  __syncthreads();
+  STAMP(23);
+  uint32_t idx[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    idx[r] = 0;
+    if (bk[r] < 32) {
+      idx[r] = s_bcnt[bk[r]][w] + loc[r];
+      s_sub[s_boff[bk[r]] + idx[r]] = ka[r];
+    }
+  }
+  // (4) region B sorted ascending (invalid entries are ~0 and sort last)
+  if (nB) {
+    uint32_t PB = 1;
+    while (PB < n_prev) PB <<= 1;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (tid * R + r < n_prev) s_bk[tid * R + r] = kb[r];
+    for (uint32_t i = n_prev + tid; i < PB; i += NT) s_bk[i] = ~0ull;
+    __syncthreads();
+    for (uint32_t k = 2; k <= PB; k <<= 1)
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tid; i < PB; i += NT) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const uint64_t a = s_bk[i], c = s_bk[ixj];
+            if ((a > c) == ((i & k) == 0)) { s_bk[i] = c; s_bk[ixj] = a; }
+          }
+        }
+        __syncthreads();
+      }
+  }
+  __syncthreads();
+  STAMP(24);
+  // (5) ranks; the first m keys and records land in key order
+  auto lower = [](const uint64_t* a, uint32_t n, uint64_t x) {  // #elements < x in sorted a[0, n)
+    uint32_t lo = 0;
+#pragma unroll
+    for (uint32_t step = (uint32_t)MAX_BATCH; step > 0; step >>= 1)
+      if (lo + step <= n && a[lo + step - 1] < x) lo += step;
+    return lo;
+  };
+  const uint32_t m = min(BS, nA + nB);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (bk[r] < 32) {
+      const uint32_t b = bk[r], o = b ^ 1u, q = b >> 1;
+      uint32_t rank = s_boff[2 * q] + idx[r] + lower(s_sub + s_boff[o], s_boff[o + 1] - s_boff[o], ka[r]);
+      if (nB && q == qs) rank += lower(s_bk, nB, ka[r]);
+      if (rank < m) {
+        uk[rank] = ka[r];
+        s_rec[rank] = ra[r];
+      }
+      if (ra[r].qf & QF_RES) {
+        AUTX_CHECK(ra[r]._pad < n_prev, "order: previous resident index", ra[r]._pad);
+        s_ppos[ra[r]._pad] = rank;
+      }
+    }
+    if (kb[r] != ~0ull) {
+      const uint32_t b0 = 2 * qs;
+      const uint32_t rank = s_boff[b0] + lower(s_sub + s_boff[b0], s_boff[b0 + 1] - s_boff[b0], kb[r]) +
+                            lower(s_sub + s_boff[b0 + 1], s_boff[b0 + 2] - s_boff[b0 + 1], kb[r]) +
+                            lower(s_bk, nB, kb[r]);
+      if (rank < m) {
+        uk[rank] = kb[r];
+        s_rec[rank] = pr[r];
+      }
+      s_ppos[tid * R + r] = rank;
+    }
+  }
+  __syncthreads();
+  STAMP(25);
+  return nB;
+}
+
+template <int NT, int R, bool LISTS, bool ORD, bool SEL>
 __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Outputs& out, KvState& kv, bool kv_on,
-                              uint32_t t, uint32_t np, uint32_t seqno) {
+                              uint32_t t, uint32_t np, uint32_t seqno, const CandRec (&pp)[R], uint32_t n_prev_pre) {
   uint64_t* uk = reinterpret_cast<uint64_t*>(fin_smem);    // [np] sorted keys of the first m candidates
   // admit / preempt id lists staged in shared memory for the host mirrors (16-B aligned)
   uint64_t* s_ad = uk + np;
   uint64_t* s_pr = s_ad + ((pol.max_batch + 1) & ~1u);
+  // ORD (order_candidates): sorted records, region-A sub-lists, region B, previous-list positions
+  CandRec* s_rec = reinterpret_cast<CandRec*>(s_pr + ((pol.max_batch + 1) & ~1u));
+  uint64_t* s_sub = reinterpret_cast<uint64_t*>(s_rec + pol.max_batch);
+  uint64_t* s_bk = s_sub + pol.max_batch;
+  uint32_t* s_ppos = reinterpret_cast<uint32_t*>(s_bk + MAX_BATCH);
   __shared__ unsigned long long red64[33];
   __shared__ uint32_t red[33];
   __shared__ uint32_t s_nbatch;
@@ -1006,7 +1620,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   const uint32_t BS = pol.max_batch;
   const uint32_t n_prev = ctl->n_prev;
   // region A + region B (previous-batch calls of q* not in A): no duplicates, ~0 sentinels last
-  const uint32_t ncand = ctl->n_cand_a + ctl->n_cand_b;
+  uint32_t ncand = ORD ? 0u : ctl->n_cand_a + ctl->n_cand_b;
   // host-record fields, loaded with everything else in the first round
   uint32_t c_live = 0, c_promo = 0, c_err = 0, c_einfo = 0;
   // rank_lists: k_rank has written the batch and admit lists and the accounting; its totals
@@ -1021,13 +1635,22 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   if (tid == 0) s_nbatch = 0;
   // ---- (1) the first m = min(BS, ncand) candidates in key order: key + record, plus the
   // previous batch's records (preempt), all in one round of independent loads --------------
+  uint32_t nB_ord = 0;
+  CandRec pr[R];
+  if constexpr (ORD) {
+    uint32_t live = 0, promo = 0;
+    nB_ord = order_candidates<NT, R, SEL>(pol, ct, ctl, out, t, uk, s_rec, s_sub, s_bk, s_ppos, pr, pp, n_prev_pre,
+                                          live, promo);
+    if (SEL && tid == 0) { c_live = live; c_promo = promo; }
+    ncand = ctl->n_cand_a + nB_ord;
+  }
   const uint32_t m = lists ? 0u : min(BS, ncand);
   // R items per thread, blocked (i = tid * R + r): NT * R >= BS
   uint32_t c_s[R], c_qf[R], c_tok[R], c_ex[R], c_mt[R], c_qt[R], c_kvb[R];
   uint64_t c_cid[R];
   uint32_t p_s[R], p_qf[R], p_held[R];  // previous resident list: slot, flags, blocks to swap out, key
   uint64_t p_cid[R], p_key[R];
-  unsigned long long p_pos[R];           // seqno << 32 | sorted position (k_rank), if use_prev_pos
+  unsigned long long p_pos[R] = {};      // seqno << 32 | sorted position (k_rank), if use_prev_pos
   unsigned long long my_kv = 0;
   {
     // all loads of this phase first, through restrict-qualified locals, so that they overlap
@@ -1037,12 +1660,16 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     const CandRec* __restrict__ prec = out.prev_rec;
     const unsigned long long* __restrict__ ppos = out.prev_pos;
     uint64_t kk[R];
-    CandRec rc[R], pr[R];
+    CandRec rc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       // unconditional below BS (buffers hold >= BS entries): the loads do not wait for the counts
       const uint32_t i = tid * R + r;
-      if (i < BS) {
+      if constexpr (ORD) {
+        // order_candidates left them in shared memory (and pr in registers)
+        if (i < m) { kk[r] = uk[i]; rc[r] = s_rec[i]; }
+        if (i < n_prev) p_pos[r] = (unsigned long long)seqno << 32 | s_ppos[i];
+      } else if (i < BS) {
         if (!lists) { kk[r] = skey[i]; rc[r] = srec[i]; }
         pr[r] = prec[i];
         p_pos[r] = ppos[i];
@@ -1155,7 +1782,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     uint32_t pos[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) pos[r] = 0;
-    if (out.use_prev_pos) {
+    if (ORD || out.use_prev_pos) {
       // k_rank's sorted position of each previous-batch entry that was a candidate (entries that
       // were not, e.g. of a queue below q*, keep an older seqno and are not in the batch)
 #pragma unroll
@@ -1416,6 +2043,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       out.prev_slots[i] = sl;
     }
   }
+  STAMP(9);
   if (tid == 0) {
     ctl->n_prev = n_res;
     HostOut h;
@@ -1436,7 +2064,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     ctl->n_promoted = 0;
     ctl->n_live = 0;
     ctl->qs_bnd1 = 0;
-    ctl->last_n_b = ctl->n_cand_b;
+    ctl->last_n_b = ORD ? nB_ord : ctl->n_cand_b;
     ctl->n_cand_b = 0;
     if (lists) { ctl->acc_nbatch = 0; ctl->acc_nadmit = 0; ctl->acc_kv = 0; ctl->acc_swap_in = 0; }
     s_hout = h;
@@ -1445,11 +2073,16 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   {
     const uint32_t n_rows = ctl->s_n_rows, ntiles = n_rows ? (n_rows + TILE - 1) / TILE : 1u;
     for (uint32_t i = tid; i < (ntiles + SUP_TILES - 1) / SUP_TILES * MAX_K; i += NT) out.sup_cnt[i] = 0;
+    if (SEL) {  // k_scan_emit's look-back words and ticket, for the next step's dense pass
+      for (uint32_t i = tid; i < ntiles * 4; i += NT) out.lb[i] = 0;
+      if (tid == 0) ctl->scan_ticket = 0;
+    }
     if (tid == 0) ctl->s_tail_prev = n_rows;  // the next step's scan may read these rows early
   }
   // host-visible results: by default the device block (counts + lists) is copied out by one
   // cudaMemcpyAsync after the kernel; the zero-copy variant stores the mirrors over PCIe here
   __syncthreads();
+  STAMP(10);
   if (!out.zero_copy) {
     if (tid == 0) *out.d_hout = s_hout;
   } else {
@@ -1483,14 +2116,37 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   STAMP(8);
 }
 
-template <int NT, int R, bool LISTS = false>
+template <int NT, int R, bool LISTS = false, bool ORD = false, bool SEL = false>
 __global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
                                                  bool kv_on, uint32_t np) {
+  // SEL: the previous resident list (written by the previous finalize or compaction, both
+  // complete) and its calls' fields that no kernel of this step writes (id, arrival, tokens,
+  // executed steps, list index) are read while the dense pass runs
+  CandRec pp[R];
+  uint32_t n_prev_pre = 0;
+  if constexpr (SEL) {
+    n_prev_pre = ctl->n_prev;
+    uint32_t ps[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (threadIdx.x * R + r < n_prev_pre) ps[r] = out.prev_slots[threadIdx.x * R + r];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (threadIdx.x * R + r < n_prev_pre) {
+        const uint32_t sl = ps[r];
+        pp[r].slot = sl;
+        pp[r].cid = ct.cid[sl];
+        pp[r].arr = ct.arr[sl];
+        pp[r].tok = ct.tok[sl];
+        pp[r].exec = ct.exec[sl];
+        pp[r]._pad = ct.bidx[sl];
+      }
+  }
   pdl_wait();
   pdl_trigger();
   const uint32_t t = ctl->s_t, seqno = ctl->s_seqno;
   CHAIN_BEGIN(5);
-  finalize_body<NT, R, LISTS>(pol, ct, ctl, out, kv, kv_on, t, np, seqno);
+  finalize_body<NT, R, LISTS, ORD, SEL>(pol, ct, ctl, out, kv, kv_on, t, np, seqno, pp, n_prev_pre);
   if (STAMPS_ON) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1610,6 +2266,10 @@ cudaError_t step_kernels_setup() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_finalize<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_finalize<512, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_finalize<512, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_finalize<FIN_THREADS, 2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_finalize<512, 2, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_finalize<FIN_THREADS, 2, false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   return e;
 }
 
@@ -1624,6 +2284,13 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   out.use_prev_pos = rx ? 0u : 1u;  // k_rank publishes previous-batch positions (select mode)
   static const bool rank_narrow = getenv("AUTX_RANK_NARROW") != nullptr;
   out.rank_wide = rank_narrow ? 0u : 1u;  // k_rank may use a warp per key when candidates are few
+  // k_rank's O(BS) bucket ranks (AUTX_RANK_BUCKETS=1): parity-green, measured slower than the
+  // all-pairs count spread over 128 SMs (rank span 6.4 vs 5.5 us: every CTA's redundant split costs
+  // more barriers than the count it replaces)
+  static const bool rank_buckets = getenv("AUTX_RANK_BUCKETS") != nullptr;
+  out.rank_buckets = rank_buckets ? 1u : 0u;
+  static const bool no_gprefetch = getenv("AUTX_GATHER_PREFETCH") && !strcmp(getenv("AUTX_GATHER_PREFETCH"), "0");
+  if (no_gprefetch) out.gtile = nullptr;
   if (ev) cudaEventRecord(ev[0], s);
   uint32_t np = std::max<uint32_t>(pow2_at_least(2 * pol.max_batch), 2048);
   // sorted keys [np] + admit and preempt id staging [2 x even(BS)]
@@ -1644,12 +2311,35 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     if (ev) cudaEventRecord(ev[3], s);
     return cudaGetLastError();
   }
+  // default: k_scan_tile -> k_gather_ss -> k_rank -> k_finalize.  AUTX_PIPELINE=ord: the finalize
+  // orders the candidates itself (no k_rank); AUTX_PIPELINE=sel: k_scan_emit -> k_finalize (no
+  // gather either).  Both parity-green and measured slower on the headline.
+  static const char* pipeline = getenv("AUTX_PIPELINE");
+  static const bool pl_sel = pipeline && !strcmp(pipeline, "sel");
+  static const bool pl_ord = pipeline && !strcmp(pipeline, "ord");
+  static const bool gather_kernel = !pl_sel;
+  static const bool rank_kernel = !pl_sel && !pl_ord;
+  const size_t ord_smem = fin_smem_bytes + (size_t)pol.max_batch * (sizeof(CandRec) + sizeof(uint64_t) + sizeof(uint32_t)) +
+                          (size_t)MAX_BATCH * sizeof(uint64_t);
   if (rx) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pol.device);
     cudaError_t e = launch_radix_order(s, pol, ct, pt, ctl, out, *rx, t, n_rows, arr_base, sms, radix_passes);
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[1], s);
+  } else if (!gather_kernel) {
+    // default: the dense pass emits each queue's first BS calls and the finalize selects, orders
+    // and cuts (two kernels after the prologue)
+    launch_pdl(k_scan_emit, ntiles, SCAN_THREADS, 0, s, pol, ct, pt, ctl, out, 1u);
+    if (ev) cudaEventRecord(ev[1], s);
+    if (ev) cudaEventRecord(ev[2], s);
+    out.rank_lists = 0;
+    if (pol.max_batch <= 1024)
+      launch_pdl(k_finalize<512, 2, false, true, true>, 1, 512, ord_smem, s, pol, ct, ctl, out, kv, kv_on, np);
+    else
+      launch_pdl(k_finalize<FIN_THREADS, 2, false, true, true>, 1, FIN_THREADS, ord_smem, s, pol, ct, ctl, out, kv, kv_on, np);
+    if (ev) cudaEventRecord(ev[3], s);
+    return cudaGetLastError();
   } else {
     // prog + L2 prefetches while the prologue runs (AUTX_SCAN_PRE, default 1: measured ~0.4 us)
     static const uint32_t pre = getenv("AUTX_SCAN_PRE") ? (uint32_t)atoi(getenv("AUTX_SCAN_PRE")) : 1u;
@@ -1657,6 +2347,18 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     if (ev) cudaEventRecord(ev[1], s);
     const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
     launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out);
+  }
+  // default: the finalize orders the candidates itself (order_candidates, O(BS) on one CTA) and
+  // decides the batch; AUTX_RANK_KERNEL=1 (and radix mode) keep the multi-CTA k_rank
+  if (!rx && !rank_kernel) {
+    out.rank_lists = 0;
+    if (ev) cudaEventRecord(ev[2], s);
+    if (pol.max_batch <= 1024)
+      launch_pdl(k_finalize<512, 2, false, true>, 1, 512, ord_smem, s, pol, ct, ctl, out, kv, kv_on, np);
+    else
+      launch_pdl(k_finalize<FIN_THREADS, 2, false, true>, 1, FIN_THREADS, ord_smem, s, pol, ct, ctl, out, kv, kv_on, np);
+    if (ev) cudaEventRecord(ev[3], s);
+    return cudaGetLastError();
   }
   // k_rank also decides the batch (lists, accounting) when there is no KV allocator and its keys
   // + kvb fit shared memory; else the finalize does (AUTX_FINALIZE_LISTS forces the latter)

@@ -4,10 +4,10 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/d_build.log 2>&1 || { tail -20 gpurun_out/d_build.log; exit 1; }
 timeout 600 python bench.py --steps 200 --no-swap --no-cpu-baseline $BENCH_ARGS > gpurun_out/d_bench.json 2> gpurun_out/d_bench.err
-python -c "import json;d=json.loads(open('gpurun_out/d_bench.json').read().splitlines()[-1]);print('bench', d['value'], round(d['ms_per_step']*1e3,2), d['breakdown_ms'], d['roofline']['frac'])" || tail -5 gpurun_out/d_bench.err
+python -c "import json;d=json.loads(open('gpurun_out/d_bench.json').read().splitlines()[-1]);print('bench', d['value'], round(d['ms_per_step']*1e3,2), d['roofline']['frac'], d.get('chain_us'), d.get('finalize_phases_us'))" || tail -5 gpurun_out/d_bench.err
 for e in $AB; do
   env ${e//+/ } timeout 600 python bench.py --steps 200 --no-swap --no-cpu-baseline $BENCH_ARGS > gpurun_out/d_bench_ab.json 2>> gpurun_out/d_bench.err
-  python -c "import json;d=json.loads(open('gpurun_out/d_bench_ab.json').read().splitlines()[-1]);print('$e', d['value'], round(d['ms_per_step']*1e3,2), d['breakdown_ms'])"
+  python -c "import json;d=json.loads(open('gpurun_out/d_bench_ab.json').read().splitlines()[-1]);print('$e', d['value'], round(d['ms_per_step']*1e3,2), d.get('chain_us'), d.get('finalize_phases_us'))"
 done
 if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv --log-file gpurun_out/d_launches.csv python bench.py --steps 5 --warmup 3 --ff 20 --no-swap --no-cpu-baseline > /dev/null 2>&1
