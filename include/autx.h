@@ -201,6 +201,17 @@ autx_status autx_register_call_dag(autx_ctx* ctx, const autx_call_desc* calls, u
  * active call may be skipped). */
 autx_status autx_sched_step(autx_ctx* ctx, uint32_t step, autx_step_out* out);
 autx_status autx_step_wait(autx_ctx* ctx, autx_step_out* out);  /* waits for out->done, fills counts */
+/* One whole engine step in one call (Alg. 1 l.1-39 for step t): exactly autx_complete(completed,
+ * n_completed) if n_completed > 0, then autx_end_program for each of ended_programs[n_ended],
+ * then autx_register_call(arrivals, n_arrivals) if n_arrivals > 0, then autx_sched_step(t) and
+ * autx_step_wait — the same operations, arguments and errors as those calls, in that order,
+ * stopping at the first error.  All arrays are host memory owned by the caller (may be NULL
+ * when their count is 0).  For the serving loop that has nothing to overlap with the step:
+ * one boundary crossing instead of five.  Not for AUTX_ATLAS_EQ2 arrivals with parents (use
+ * autx_register_call_dag) or multi-engine contexts (autx_route must run between them: E_STATE). */
+autx_status autx_step(autx_ctx* ctx, uint32_t step, const uint64_t* completed, uint32_t n_completed,
+                      const uint64_t* ended_programs, uint32_t n_ended, const autx_call_desc* arrivals,
+                      uint32_t n_arrivals, autx_step_out* out);
 
 /* ---- KV swap (a7) --------------------------------------------------------------------- */
 /* Executes the last step's swap plan: swap-out (GPU blocks -> host arena) of every preempted

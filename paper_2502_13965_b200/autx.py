@@ -103,6 +103,7 @@ def load_library(path=LIB_PATH):
         "autx_register_call_dag": ([P, P, u32, P, P], i32),
         "autx_sched_step": ([P, u32, C.POINTER(StepOut)], i32),
         "autx_step_wait": ([P, C.POINTER(StepOut)], i32),
+        "autx_step": ([P, u32, P, u32, P, u32, P, u32, C.POINTER(StepOut)], i32),
         "autx_kv_swap": ([P, C.POINTER(KvLayout), i32, C.POINTER(SwapStats)], i32),
         "autx_block_table": ([P, C.POINTER(P), C.POINTER(P)], i32),
         "autx_block_table_host": ([P, P, P, u32, C.POINTER(u32)], i32),
@@ -135,7 +136,7 @@ def exported_symbols():
     return [
         "autx_create", "autx_destroy", "autx_last_error", "autx_version", "autx_start_program",
         "autx_end_program", "autx_complete", "autx_register_call", "autx_register_call_dag", "autx_sched_step",
-        "autx_step_wait", "autx_kv_swap", "autx_block_table", "autx_block_table_host", "autx_route_record_bytes",
+        "autx_step_wait", "autx_step", "autx_kv_swap", "autx_block_table", "autx_block_table_host", "autx_route_record_bytes",
         "autx_route_pack", "autx_route_apply", "autx_route", "autx_comm_unique_id", "autx_comm_init",
         "autx_comm_destroy", "autx_dump_calls", "autx_program_state",
         "autx_last_step_timing", "autx_step_stats", "autx_set_timing", "autx_num_active", "autx_phase_times", "autx_kernel_launches",
@@ -262,6 +263,16 @@ class Scheduler:
         self._check(self.lib.autx_sched_step(self.ctx, int(t), C.byref(self.out)))
         if wait:
             self._check(self.lib.autx_step_wait(self.ctx, C.byref(self.out)))
+        return self.out
+
+    def step(self, t, call_ids=None, ended_programs=(), descs=None):
+        """One whole step in one ABI call (autx_step): completions, session ends, arrivals,
+        sched_step and wait.  Returns the filled step record."""
+        c = np.ascontiguousarray(call_ids if call_ids is not None else (), dtype=np.uint64)
+        e = np.ascontiguousarray(ended_programs, dtype=np.uint64)
+        a = np.ascontiguousarray(descs if descs is not None else np.zeros(0, CALL_DESC), dtype=CALL_DESC)
+        self._check(self.lib.autx_step(self.ctx, int(t), _ptr(c), len(c), _ptr(e), len(e), _ptr(a), len(a),
+                                       C.byref(self.out)))
         return self.out
 
     def step_wait(self):

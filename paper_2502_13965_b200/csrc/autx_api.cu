@@ -1017,6 +1017,19 @@ extern "C" autx_status autx_step_wait(autx_ctx* ctx, autx_step_out* out) {
   return AUTX_OK;
 }
 
+extern "C" autx_status autx_step(autx_ctx* ctx, uint32_t t, const uint64_t* completed, uint32_t n_completed,
+                                 const uint64_t* ended_programs, uint32_t n_ended, const autx_call_desc* arrivals,
+                                 uint32_t n_arrivals, autx_step_out* out) {
+  if (!ctx || !out) return AUTX_E_INVAL;
+  autx_status s = AUTX_OK;
+  if (n_completed) s = autx_complete(ctx, completed, n_completed);
+  for (uint32_t i = 0; s == AUTX_OK && i < n_ended; ++i) s = autx_end_program(ctx, ended_programs[i]);
+  if (s == AUTX_OK && n_arrivals) s = autx_register_call(ctx, arrivals, n_arrivals);
+  if (s == AUTX_OK) s = autx_sched_step(ctx, t, out);
+  if (s == AUTX_OK) s = autx_step_wait(ctx, out);
+  return s;
+}
+
 // G8: stable compaction on the device into the other half of the double-buffered call table
 // (k_live_count, k_compact, k_remap_prev: no host sort, no allocation, no synchronisation).  The
 // host remaps its own id maps in parallel: a live row's new index is its rank among the live rows,

@@ -132,7 +132,6 @@ class TraceDriver:
     def finish(self):
         """Waits for the step, logs it and runs the engine model (one decode step per batch
         call; calls whose hidden decode length is reached complete)."""
-        t = self.t
         s = self.s
         t0 = time.perf_counter()
         out = s.step_wait()
@@ -142,6 +141,31 @@ class TraceDriver:
         self.api_s += t2 - t0
         self.api_split["step_wait"] = self.api_split.get("step_wait", 0.0) + t1 - t0
         self.api_split["lists"] = self.api_split.get("lists", 0.0) + t2 - t1
+        return self._record(out, batch, admit, preempt)
+
+    def run_fused(self):
+        """One engine step through the single-call entry point autx_step (completions, session
+        ends, arrivals, sched_step, wait in one boundary crossing), then the lists.  Single
+        engine, scalar ATLAS/PLAS/FCFS/MLFQ (EQ2 arrivals with parents use issue/finish)."""
+        if getattr(self, "_prepared", None) is None or self._prepared[0] != self.t:
+            self.prepare()
+        t, ids, ended, arr = self._prepared
+        self._prepared = None
+        s = self.s
+        pc = time.perf_counter
+        t0 = pc()
+        out = s.step(t, ids, ended, arr)
+        t1 = pc()
+        batch, admit, preempt = s.lists()
+        t2 = pc()
+        self.api_s += t2 - t0
+        self.api_split["step"] = self.api_split.get("step", 0.0) + t1 - t0
+        self.api_split["lists"] = self.api_split.get("lists", 0.0) + t2 - t1
+        return len(ids), len(arr), self._record(out, batch, admit, preempt)
+
+    def _record(self, out, batch, admit, preempt):
+        s = self.s
+        t = self.t
         rec = dict(t=t, n_batch=int(out.n_batch), swap_out_blocks=int(out.swap_out_blocks),
                    swap_in_blocks=int(out.swap_in_blocks), kv_blocks=int(out.kv_blocks),
                    n_active=int(out.n_active), n_promoted=int(out.n_promoted),
@@ -173,9 +197,13 @@ class TraceDriver:
         self.issue()
         return self.finish()
 
-    def run(self, max_steps=10 ** 9):
+    def run(self, max_steps=10 ** 9, fused=False):
+        """Runs the trace; fused: one autx_step call per step instead of the five-call sequence."""
         for _ in range(max_steps):
             if not self.skip_idle():
                 break
-            self.step()
+            if fused:
+                self.run_fused()
+            else:
+                self.step()
         return self.log

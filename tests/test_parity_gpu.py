@@ -28,11 +28,11 @@ def oracle_records(tr, cfg):
             for r in log if r["batch"] or r["preempt"]], m
 
 
-def gpu_records(tr, cfg, **kw):
+def gpu_records(tr, cfg, fused=False, **kw):
     from paper_2502_13965_b200 import TraceDriver
     s = make_sched(cfg, **kw)
     d = TraceDriver(tr, s)
-    log = d.run()
+    log = d.run(fused=fused)
     s.close()
     return [(r["t"], r["batch"], r["admit"], r["preempt"], r["swap_out_blocks"], r["swap_in_blocks"],
              r["kv_blocks"]) for r in log if r["batch"] or r["preempt"]]
@@ -88,6 +88,22 @@ def test_random_tiny(seed):
         except ValueError:
             continue  # a call's initial kvb exceeds P: the ABI rejects it too (tested below)
         assert_same(gpu_records(tr, tiny_cfg(seed * 4 + p, policy)), want)
+
+
+@pytest.mark.parametrize("seed", [3, 11, 29, 57])
+def test_fused_step_entry_point(seed):
+    """autx_step (one call per step) reaches the oracle's decisions like the five-call sequence."""
+    tr = random_tiny(seed)
+    n = 0
+    for p, policy in enumerate((FCFS, MLFQ, PLAS, ATLAS)):
+        cfg = tiny_cfg(seed * 4 + p, policy)
+        try:
+            want, _ = oracle_records(tr, cfg)
+        except CapacityError:
+            continue
+        assert_same(gpu_records(tr, tiny_cfg(seed * 4 + p, policy), fused=True), want)
+        n += 1
+    assert n > 0
 
 
 @pytest.mark.parametrize("seed", range(24))
