@@ -49,6 +49,7 @@ struct autx_ctx {
   bool kv_on = false;
   // pinned staging (device reads it through UVA)
   uint32_t* h_cslots = nullptr;  // [max_batch * 4] completion slots
+  std::vector<uint32_t> cprog;    // process-table row of each staged completion (prologue prefetch hint)
   uint32_t cslots_cap = 0;
   ArrivalRec* h_arr = nullptr;
   uint32_t arr_cap = 0;
@@ -260,6 +261,7 @@ static autx_status alloc_tables(autx_ctx* ctx) {
   o.h_batch_slots = reinterpret_cast<uint32_t*>(o.h_preempt + BSp);
   ctx->ran_seq.assign(rows, 0);
   ctx->cslots_cap = 4 * BS;
+  ctx->cprog.assign(PRO_INLINE, 0);
   CK(cudaHostAlloc((void**)&ctx->h_cslots, ctx->cslots_cap * 4, cudaHostAllocMapped));
   ctx->arr_cap = 4 * BS;
   CK(cudaHostAlloc((void**)&ctx->h_arr, ctx->arr_cap * sizeof(ArrivalRec), cudaHostAllocMapped));
@@ -553,6 +555,7 @@ extern "C" autx_status autx_complete(autx_ctx* ctx, const uint64_t* ids, uint32_
   for (uint32_t i = 0; i < n; ++i) {
     const uint32_t slot = sl[i];
     ctx->h_cslots[i] = slot;
+    if (i < (uint32_t)PRO_INLINE) ctx->cprog[i] = ctx->slot_prog[slot];
     if (ctx->eq2) ctx->h_clin[i] = ctx->lin_of.at(ids[i]);
     ctx->slot_live[slot] = 0;
     ctx->prog_active[ctx->slot_prog[slot]] -= 1;
@@ -603,6 +606,7 @@ static autx_status flush_staged(autx_ctx* ctx, uint32_t t, bool always = false) 
   // HBM instead of one PCIe round trip per record
   if (a.n_comp <= (uint32_t)PRO_INLINE) {
     memcpy(a.comp, ctx->h_cslots, a.n_comp * sizeof(uint32_t));
+    memcpy(a.comp_prog, ctx->cprog.data(), a.n_comp * sizeof(uint32_t));
   } else {
     CK(cudaMemcpyAsync(ctx->d_cslots, ctx->h_cslots, (size_t)a.n_comp * 4, cudaMemcpyHostToDevice, ctx->stream));
     a.comp_ptr = ctx->d_cslots;

@@ -339,6 +339,7 @@ struct PrologueArgs {
   const uint32_t* comp_lin;  // AUTX_ATLAS_EQ2: lineage index of each completion (mapped pinned)
   const uint32_t* par;       // AUTX_ATLAS_EQ2: parents' lineage indices (mapped pinned)
   uint32_t comp[PRO_INLINE];
+  uint32_t comp_prog[PRO_INLINE];  // their programs' process-table rows (the host knows them): prefetched
   ArrivalRec arr[PRO_INLINE];
 };
 

@@ -54,6 +54,10 @@ __device__ __forceinline__ uint32_t place_queue(const Policy& pol, uint32_t svc)
     if (blockIdx.x == 0) ctl->dbg[32 + 3 * (k)] = g_; atomicMax(&ctl->dbg[34 + 3 * (k)], g_); } } while (0)
 #define CHAIN_END(k) do { if (STAMPS_ON && threadIdx.x == 0) atomicMax(&ctl->dbg[33 + 3 * (k)], globaltimer()); } while (0)
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // ceil(tokens / block_tokens) (R14, R28): a shift when block_tokens is a power of two
 __device__ __forceinline__ uint32_t blocks_for(const Policy& pol, uint32_t tokens) {
   return pol.bt_shift != 0xFFu ? (tokens + pol.block_tokens - 1) >> pol.bt_shift
@@ -301,7 +305,12 @@ __global__ void __launch_bounds__(PRO_THREADS) k_prologue(Policy pol, CallTable 
   const uint32_t tid = threadIdx.x;
   const bool comp_inline = a.n_comp <= PRO_INLINE, arr_inline = a.n_arr <= PRO_INLINE;
   if (comp_inline)
-    for (uint32_t i = tid; i < a.n_comp; i += PRO_THREADS) s_comp[i] = a.comp[i];
+    for (uint32_t i = tid; i < a.n_comp; i += PRO_THREADS) {
+      s_comp[i] = a.comp[i];
+      // the completions' program rows, which the reductions below read-modify-write: into L2 now,
+      // in parallel with the completion rows' loads, instead of one more DRAM round trip after them
+      prefetch_l2(&pt.info[a.comp_prog[i]]);
+    }
   if (arr_inline)
     for (uint32_t i = tid; i < a.n_arr; i += PRO_THREADS) s_arr[i] = a.arr[i];
   pdl_wait();
@@ -378,10 +387,6 @@ cudaError_t launch_prologue(cudaStream_t s, const Policy& pol, CallTable ct, Pro
 // The dense pass runs one tile per CTA, sized for one wave: 256 threads x 8 rows, <= 64
 // registers so that 4 CTAs fit per SM (592 tiles = 1.2M rows resident at once).  Every row's
 // program-row gather is issued in one round, which is what bounds this latency-bound pass.
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 // Per-row core of the dense pass over one thread's 8 rows (Alg. 1 l.24-30): program-row gather,
 // anti-starvation, promotion writes, queue histogram.
 template <int R>
