@@ -540,6 +540,18 @@ def main():
     spans = chain_spans(stamp_phase)
     # phases inside the finalize (raw stamps dbg[0, 32) of the step just run, thread 0 of the CTA,
     # us after the finalize's first stamp): [0, 10] the finalize body, [20, 25] its ordering
+    # phases inside k_gather_ss (tile 0: selection known, positions known, records emitted) and
+    # k_rank (CTA 0: keys in shared memory, compacted / split, ranked), us after each kernel's CTA 0
+    # passed its PDL wait (dbg[57..59] and dbg[54..56], moved to [89..91] and [86..88] by finalize)
+    sub_ph = {}
+    for name, k, idx in (("gather", 3, (89, 90, 91)), ("rank", 4, (86, 87, 88))):
+        vals = []
+        for p in stamp_phase:
+            b = int(p[64 + 3 * k])
+            if b and all(int(p[i]) for i in idx):
+                vals.append([int(p[i]) - b for i in idx])
+        if vals:
+            sub_ph[name] = [round(float(np.median([v[j] for v in vals])) / 1e3, 2) for j in range(3)]
     fin_ph = {}
     for i in list(range(0, 11)) + list(range(20, 26)):
         v = [int(p[i]) - int(p[0]) for p in stamp_phase if int(p[i]) and int(p[0])]
@@ -630,6 +642,7 @@ def main():
                     "p90": float(np.percentile(ms, 90)), "mean": statistics.mean(ms)},
         "chain_us": spans,
         "finalize_phases_us": fin_ph,
+        "gather_rank_phases_us": sub_ph,
         "kernel_span_us": span_k,
         "kernel_event_ms": ev_mean,
         "state": {"promotions_per_step": statistics.mean(promoted),

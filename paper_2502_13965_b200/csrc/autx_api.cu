@@ -23,6 +23,7 @@ using namespace autx;
 
 unsigned long long autx::g_kernel_launches = 0;
 thread_local std::vector<autx::LaunchRec>* autx::g_launch_rec = nullptr;
+thread_local size_t autx::g_launch_n = 0;
 
 extern "C" uint64_t autx_kernel_launches(void) {
   return __atomic_load_n(&g_kernel_launches, __ATOMIC_RELAXED);
@@ -50,6 +51,7 @@ struct autx_ctx {
   // pinned staging (device reads it through UVA)
   uint32_t* h_cslots = nullptr;  // [max_batch * 4] completion slots
   std::vector<uint32_t> cprog;    // process-table row of each staged completion (prologue prefetch hint)
+  std::vector<autx::LaunchRec> rec_pool;  // the step's recorded launches (graph replay), reused
   uint32_t cslots_cap = 0;
   ArrivalRec* h_arr = nullptr;
   uint32_t arr_cap = 0;
@@ -831,16 +833,16 @@ static autx_status register_impl(autx_ctx* ctx, const autx_call_desc* calls, uin
 // a few small kernels, and one graph launch plus per-node parameter updates costs the host a
 // fraction of the separate launches.  The graph of a new launch signature is captured once (with
 // the PDL attribute, so consecutive kernel nodes keep their programmatic edges).
-static autx_status step_graph_run(autx_ctx* ctx, std::vector<LaunchRec>& recs) {
+static autx_status step_graph_run(autx_ctx* ctx, std::vector<LaunchRec>& recs, size_t n_recs) {
   autx_ctx::StepGraph* sg = nullptr;
   for (auto& g : ctx->graphs) {
-    bool same = g.funcs.size() == recs.size();
-    for (size_t i = 0; same && i < recs.size(); ++i)
+    bool same = g.funcs.size() == n_recs;
+    for (size_t i = 0; same && i < n_recs; ++i)
       same = g.funcs[i] == recs[i].func && g.blocks[i].x == recs[i].block.x && g.smem[i] == recs[i].smem;
     if (same) { sg = &g; break; }
   }
   if (sg) {
-    for (size_t i = 0; i < recs.size(); ++i) {
+    for (size_t i = 0; i < n_recs; ++i) {
       // only nodes whose parameters or grid changed: the chain reads the step's scalars from
       // the control block, so a typical step re-parameterises the prologue alone
       const dim3& g = recs[i].grid;
@@ -866,7 +868,8 @@ static autx_status step_graph_run(autx_ctx* ctx, std::vector<LaunchRec>& recs) {
     autx_ctx::StepGraph g;
     CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
     cudaError_t err = cudaSuccess;
-    for (auto& r : recs) {
+    for (size_t ri = 0; ri < n_recs; ++ri) {
+      LaunchRec& r = recs[ri];
       std::vector<void*> ptrs = r.ptrs();
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = r.grid;
@@ -929,7 +932,7 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   // the step's kernels as one graph replay (AUTX_NO_GRAPH: separate launches); not with the
   // per-kernel timing events, the radix pipeline (host-synchronised passes) or a bulk burst (DMA)
   static const bool no_graph = getenv("AUTX_NO_GRAPH") != nullptr;
-  std::vector<LaunchRec> recs;
+  std::vector<LaunchRec>& recs = ctx->rec_pool;  // reused: no allocation per recorded launch
   const bool graph = !no_graph && !ctx->timing && !ctx->radix && ctx->n_arr_staged <= 4096;
   // R32: a window step keeps the resident list; the ordering runs at the first step, every N-th
   // step after the last scheduling point, and whenever the carried list is empty (the previous
@@ -942,7 +945,7 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
     window = ctx->since != 0 && ctx->since < ctx->cfg.sched_every && carried > 0;
     ctx->since = window ? ctx->since + 1 : 1;
   }
-  if (graph) g_launch_rec = &recs;
+  if (graph) { g_launch_rec = &recs; g_launch_n = 0; }
   ++ctx->seqno;
   g_hp.lap(0);
   s = flush_staged(ctx, t, true);  // the prologue, always: it hands t, n_rows, seqno to the chain
@@ -955,7 +958,7 @@ extern "C" autx_status autx_sched_step(autx_ctx* ctx, uint32_t t, autx_step_out*
   CK(le);
   g_hp.lap(2);
   if (graph) {
-    s = step_graph_run(ctx, recs);
+    s = step_graph_run(ctx, recs, g_launch_n);
     if (s) return s;
   }
   g_hp.lap(3);

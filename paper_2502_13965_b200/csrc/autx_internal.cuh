@@ -298,19 +298,22 @@ struct LaunchRec {
     return p;
   }
 };
-extern thread_local std::vector<LaunchRec>* g_launch_rec;  // non-null: launch_pdl records
+extern thread_local std::vector<LaunchRec>* g_launch_rec;  // non-null: launch_pdl records into it
+extern thread_local size_t g_launch_n;                      // ... at [g_launch_n++] (a pool reused every step)
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args) {
   if (g_launch_rec) {
-    LaunchRec r;
+    if (g_launch_n == g_launch_rec->size()) g_launch_rec->emplace_back();
+    LaunchRec& r = (*g_launch_rec)[g_launch_n++];
+    r.blob.clear();
+    r.off.clear();
     r.func = reinterpret_cast<const void*>(k);
     r.grid = grid;
     r.block = block;
     r.smem = smem;
     (r.push(static_cast<KArgs>(args)), ...);
-    g_launch_rec->push_back(std::move(r));
     __atomic_fetch_add(&g_kernel_launches, 1ull, __ATOMIC_RELAXED);  // runs in the graph replay
     return cudaSuccess;
   }
