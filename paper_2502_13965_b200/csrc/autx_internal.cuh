@@ -333,7 +333,10 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
 
 // Inputs of the fused step prologue (completions + arrivals), passed by value as kernel
 // parameters when they fit (PRO_INLINE each), else through the pointers.
-constexpr int PRO_INLINE = 96;
+#ifndef AUTX_PRO_INLINE
+#define AUTX_PRO_INLINE 96
+#endif
+constexpr int PRO_INLINE = AUTX_PRO_INLINE;
 struct PrologueArgs {
   uint32_t n_comp, n_arr, first_slot, t;
   uint32_t n_prog_rows, n_rows, seqno, n_active;  // process-table rows in use; table rows, step seqno, active calls

@@ -1050,7 +1050,13 @@ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) { return x <= 1 ? 0 : 
 // any block sort (measured: scripts/micro/sort_bench.cu), so the order is computed across many
 // SMs instead: every CTA holds all n <= 2 BS keys in shared memory and each key's output index is
 // the number of keys before it (the keys are unique), RANK_SUB threads per key.
-constexpr int RANK_THREADS = 256, RANK_SUB = 16, RANK_PER_CTA = RANK_THREADS / RANK_SUB;
+// 16 keys per CTA; AUTX_RANK_THREADS threads per CTA (RANK_SUB per key, twice that per key in the
+// wide mode): more warps per SM hide the count loop's shared-memory latency
+#ifndef AUTX_RANK_THREADS
+#define AUTX_RANK_THREADS 512
+#endif
+constexpr int RANK_THREADS = AUTX_RANK_THREADS, RANK_PER_CTA = 16, RANK_SUB = RANK_THREADS / RANK_PER_CTA;
+static_assert(RANK_SUB <= 32 && (RANK_SUB & (RANK_SUB - 1)) == 0, "threads per key: a power of two, <= a warp");
 __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct, Ctl* ctl, Outputs out, KvState kv,
                                                        bool kv_on, uint32_t np) {
   pdl_wait();
@@ -1251,7 +1257,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     // when the candidates fill at most half the grid's capacity, a full warp per key (8 keys per
     // CTA) keeps every CTA busy and halves each thread's compares; else half a warp per key
     const bool wide = 2 * n_valid <= gridDim.x * RANK_PER_CTA && out.rank_wide;
-    const uint32_t subn = wide ? 32u : (uint32_t)RANK_SUB;
+    const uint32_t subn = wide ? 2u * RANK_SUB : (uint32_t)RANK_SUB;
     const uint32_t e = (wide ? blockIdx.x * (RANK_PER_CTA / 2) : e0) + threadIdx.x / subn, sub = threadIdx.x % subn;
     if (e < n_valid) {
       x = ck[e];
@@ -1282,6 +1288,13 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
         kvs += __shfl_xor_sync(0xffffffffu, kvs, d);
         nad += __shfl_xor_sync(0xffffffffu, nad, d);
       }
+    }
+    if (subn > 32) {  // two warps per key: the odd warp's sums join the even warp's
+      __shared__ uint32_t x_part[RANK_THREADS / 64][3];
+      const uint32_t w = threadIdx.x >> 5;
+      if ((w & 1u) && lane_id() == 0) { x_part[w >> 1][0] = cnt; x_part[w >> 1][1] = kvs; x_part[w >> 1][2] = nad; }
+      __syncthreads();
+      if (!(w & 1u)) { cnt += x_part[w >> 1][0]; kvs += x_part[w >> 1][1]; nad += x_part[w >> 1][2]; }
     }
     if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[56] = globaltimer();
     lead = sub == 0 && e < n_valid;
