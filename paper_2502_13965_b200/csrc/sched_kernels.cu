@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) k_scan_tile(Policy pol, CallT
 }
 
 // ---------------------------------------------------------------------------------------------
-// Dense pass that also emits region A's raw material (default select pipeline; AUTX_GATHER=1 keeps
+// Dense pass that also emits region A's raw material (AUTX_PIPELINE=sel; the default keeps
 // k_gather_ss + k_rank): every tile learns, per queue, how many live calls of that queue the
 // earlier tiles hold, saturated at the resident capacity BS (single-pass decoupled look-back,
 // tiles taken by ticket so that every tile waited on has started), and writes each live call
@@ -1351,7 +1351,7 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
 }
 
 // ---------------------------------------------------------------------------------------------
-// a5 inside the finalize (default select pipeline; AUTX_RANK_KERNEL=1 keeps k_rank): the order of
+// a5 inside the finalize (AUTX_PIPELINE=ord or sel; the default keeps k_rank): the order of
 // the <= 2 BS candidates in O(BS) work on one CTA, no all-pairs count.
 //   Region A (the gather's candidates) is in table order, i.e. (arrival, seq) order (rows are
 //   registered in arrival order, R11).  Split it into 2K sub-lists by (q, not-running): inside one
@@ -1638,7 +1638,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   const uint32_t BS = pol.max_batch;
   const uint32_t n_prev = ctl->n_prev;
   // region A + region B (previous-batch calls of q* not in A): no duplicates, ~0 sentinels last
-  uint32_t ncand = ORD ? 0u : ctl->n_cand_a + ctl->n_cand_b;
+  uint32_t ncand = ORD ? 0u : ctl->n_cand_a + __ldcg(&ctl->n_cand_b);
   // host-record fields, loaded with everything else in the first round
   uint32_t c_live = 0, c_promo = 0, c_err = 0, c_einfo = 0;
   // rank_lists: k_rank has written the batch and admit lists and the accounting; its totals
@@ -1647,7 +1647,11 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
   unsigned long long a_kv = 0, a_si = 0;
   if (tid == 0) {
     c_live = ctl->n_live; c_promo = ctl->n_promoted; c_err = ctl->err; c_einfo = ctl->err_info;
-    if (lists) { a_nb = ctl->acc_nbatch; a_na = ctl->acc_nadmit; a_kv = ctl->acc_kv; a_si = ctl->acc_swap_in; }
+    // L2 reads: with the finalize fused into k_rank's last CTA these were written in this kernel
+    if (lists) {
+      a_nb = __ldcg(&ctl->acc_nbatch); a_na = __ldcg(&ctl->acc_nadmit);
+      a_kv = __ldcg(&ctl->acc_kv); a_si = __ldcg(&ctl->acc_swap_in);
+    }
   }
   STAMP(0);
   if (tid == 0) s_nbatch = 0;
@@ -1690,7 +1694,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
       } else if (i < BS) {
         if (!lists) { kk[r] = skey[i]; rc[r] = srec[i]; }
         pr[r] = prec[i];
-        p_pos[r] = ppos[i];
+        p_pos[r] = __ldcg(ppos + i);  // (written by k_rank: in this kernel when fused)
       }
     }
 #pragma unroll
@@ -2082,7 +2086,7 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
     ctl->n_promoted = 0;
     ctl->n_live = 0;
     ctl->qs_bnd1 = 0;
-    ctl->last_n_b = ORD ? nB_ord : ctl->n_cand_b;
+    ctl->last_n_b = ORD ? nB_ord : __ldcg(&ctl->n_cand_b);
     ctl->n_cand_b = 0;
     if (lists) { ctl->acc_nbatch = 0; ctl->acc_nadmit = 0; ctl->acc_kv = 0; ctl->acc_swap_in = 0; }
     s_hout = h;
@@ -2366,8 +2370,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
     const uint32_t ggrid = ntiles + (pol.max_batch + SCAN_THREADS - 1) / SCAN_THREADS;
     launch_pdl(k_gather_ss, ggrid, SCAN_THREADS, 0, s, pol, ct, ctl, out);
   }
-  // default: the finalize orders the candidates itself (order_candidates, O(BS) on one CTA) and
-  // decides the batch; AUTX_RANK_KERNEL=1 (and radix mode) keep the multi-CTA k_rank
+  // AUTX_PIPELINE=ord: the finalize orders the candidates itself (order_candidates, O(BS) on one CTA) and
+  // decides the batch; the default (and radix mode) keep the multi-CTA k_rank
   if (!rx && !rank_kernel) {
     out.rank_lists = 0;
     if (ev) cudaEventRecord(ev[2], s);
