@@ -214,6 +214,7 @@ struct Outputs {
   uint32_t rank_lists;       // k_rank writes batch / admit lists and accounting (no KV allocator)
   uint32_t rank_wide;        // k_rank: a warp per key when the candidates fill <= half its grid
   uint32_t rank_buckets;     // k_rank: O(BS) bucket ranks when region B is empty (else all-pairs count)
+  uint32_t prev_early;       // k_finalize: prev_rec was written two kernels back (read before the PDL wait)
   uint32_t* ckvb;            // [2 BS] kvb of each key in ckey (R14)
   uint32_t* tile_cnt;        // [ntiles_cap * MAX_K]
   uint32_t* sup_cnt;         // [ceil(ntiles_cap / SUP_TILES) * MAX_K] per-queue counts of super-tiles

@@ -1693,8 +1693,8 @@ __device__ void finalize_body(const Policy& pol, CallTable& ct, Ctl* ctl, Output
         if (i < n_prev) p_pos[r] = (unsigned long long)seqno << 32 | s_ppos[i];
       } else if (i < BS) {
         if (!lists) { kk[r] = skey[i]; rc[r] = srec[i]; }
-        pr[r] = prec[i];
-        p_pos[r] = __ldcg(ppos + i);  // (written by k_rank: in this kernel when fused)
+        pr[r] = out.prev_early ? pp[r] : prec[i];
+        p_pos[r] = __ldcg(ppos + i);
       }
     }
 #pragma unroll
@@ -2146,6 +2146,19 @@ __global__ void __launch_bounds__(NT) k_finalize(Policy pol, CallTable ct, Ctl* 
   // executed steps, list index) are read while the dense pass runs
   CandRec pp[R];
   uint32_t n_prev_pre = 0;
+  if (!SEL && !ORD && out.prev_early) {
+    // the previous list's records come from k_gather_ss (or k_take), two kernels back: this grid
+    // launched only after every k_rank CTA passed its own PDL wait, so they are complete and in L2
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (threadIdx.x * R + r < pol.max_batch) {
+        const unsigned long long* q = reinterpret_cast<const unsigned long long*>(out.prev_rec + threadIdx.x * R + r);
+        unsigned long long w[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) w[k] = __ldcg(q + k);
+        memcpy(&pp[r], w, sizeof(CandRec));
+      }
+  }
   if constexpr (SEL) {
     n_prev_pre = ctl->n_prev;
     uint32_t ps[R];
@@ -2304,6 +2317,7 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   uint32_t ntiles = (n_rows + TILE - 1) / TILE;
   if (ntiles == 0) ntiles = 1;
   out.use_prev_pos = rx ? 0u : 1u;  // k_rank publishes previous-batch positions (select mode)
+  out.prev_early = 0;               // set below for the finalize that follows k_rank
   static const bool rank_narrow = getenv("AUTX_RANK_NARROW") != nullptr;
   out.rank_wide = rank_narrow ? 0u : 1u;  // k_rank may use a warp per key when candidates are few
   // k_rank's O(BS) bucket ranks (AUTX_RANK_BUCKETS=1): parity-green, measured slower than the
@@ -2398,6 +2412,8 @@ cudaError_t launch_step(cudaStream_t s, const Policy& pol, CallTable ct, ProgTab
   launch_pdl(k_rank, rank_grid, RANK_THREADS, rank_smem, s, pol, ct, ctl, out, kv, kv_on, np);
   // 512 threads x 2 candidates: 4 warps per scheduler to hide the phase's latency chains (1024
   // threads hit the 64-register cap and spill); BS > 1024 takes 1024 threads x 4
+  static const bool no_prev_early = getenv("AUTX_FIN_PREV_EARLY") && !strcmp(getenv("AUTX_FIN_PREV_EARLY"), "0");
+  out.prev_early = no_prev_early ? 0u : 1u;  // prev_rec is two kernels back here
   if (pol.max_batch <= 1024)
     launch_pdl(out.rank_lists ? k_finalize<512, 2, true> : k_finalize<512, 2>, 1, 512, fin_smem_bytes, s, pol, ct,
                ctl, out, kv, kv_on, np);

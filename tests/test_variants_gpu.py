@@ -19,7 +19,7 @@ VARIANTS = {
     "finalize_lists": {"AUTX_FINALIZE_LISTS": "1"},  # finalize cuts the batch and writes the lists (not k_rank)
     "rank_narrow": {"AUTX_RANK_NARROW": "1"},    # half a warp per key in k_rank whatever the candidate count
     "rank_buckets": {"AUTX_RANK_BUCKETS": "1"},  # k_rank's O(BS) bucket ranks instead of the all-pairs count
-    "no_gather_prefetch": {"AUTX_GATHER_PREFETCH": "0"},  # no L2 prefetch of last step's candidate tiles
+    "no_gather_prefetch": {"AUTX_GATHER_PREFETCH": "0", "AUTX_FIN_PREV_EARLY": "0"},  # no early reads / prefetches
     "pipeline_ord": {"AUTX_PIPELINE": "ord"},    # no k_rank: the finalize orders the candidates in O(BS)
     "pipeline_sel": {"AUTX_PIPELINE": "sel"},    # no gather, no k_rank: the dense pass emits, the finalize selects
 }
