@@ -1104,7 +1104,8 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
   }
   // region B holds a valid key (a previous-list call of q* past region A's boundary: empty in
   // every bench workload): the general all-pairs count below; else the O(BS) bucket ranks
-  const bool fast = !__syncthreads_or(nbv != 0) && out.rank_buckets;
+  const bool no_b = !__syncthreads_or(nbv != 0);
+  const bool fast = no_b && out.rank_buckets;
   bool lead = false;
   uint32_t cnt = 0, eo = 0, kvs = 0, nad = 0, own_kvb = 0;
   uint64_t x = 0;
@@ -1239,10 +1240,17 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     // (2) compact the candidates (same deterministic order in every CTA): sentinels rank last and
     // nobody reads them, so only the n_valid candidates are ranked and compared against
     if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[54] = globaltimer();
-    uint32_t n_valid;
-    uint32_t off = block_excl_scan<uint32_t, RANK_THREADS>(nv, red_r, &n_valid);
-    for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS)
-      if (rk[i] != ~0ull) { ck[off] = rk[i]; ci[off] = i; ckv[off] = rkv[i]; ++off; }
+    // without region-B keys the candidates are region A, [0, na) of rk: nothing to compact
+    uint32_t n_valid = na;
+    const uint64_t* kp = rk;
+    const uint32_t* kvp = rkv;
+    if (!no_b) {
+      uint32_t off = block_excl_scan<uint32_t, RANK_THREADS>(nv, red_r, &n_valid);
+      for (uint32_t i = threadIdx.x; i < n; i += RANK_THREADS)
+        if (rk[i] != ~0ull) { ck[off] = rk[i]; ci[off] = i; ckv[off] = rkv[i]; ++off; }
+      kp = ck;
+      kvp = ckv;
+    }
     __syncthreads();
     if (STAMPS_ON && blockIdx.x == 0 && threadIdx.x == 0) ctl->dbg[55] = globaltimer();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1260,24 +1268,24 @@ __global__ void __launch_bounds__(RANK_THREADS) k_rank(Policy pol, CallTable ct,
     const uint32_t subn = wide ? 2u * RANK_SUB : (uint32_t)RANK_SUB;
     const uint32_t e = (wide ? blockIdx.x * (RANK_PER_CTA / 2) : e0) + threadIdx.x / subn, sub = threadIdx.x % subn;
     if (e < n_valid) {
-      x = ck[e];
-      eo = ci[e];
-      own_kvb = ckv[e];
+      x = kp[e];
+      eo = no_b ? e : ci[e];
+      own_kvb = kvp[e];
       if (sub == 0) rec = eo < na ? out.cand_rec[eo] : out.prev_rec[eo - na];
       if (lists) {
         // with the rank, the kvb prefix (Alg. 1 l.34-37) and the admit rank (smaller keys of
         // calls that did not run: not resident under eager eviction)
 #pragma unroll 4
         for (uint32_t j = sub; j < n_valid; j += subn) {  // (4 independent smem chains in flight)
-          const uint64_t y = ck[j];
+          const uint64_t y = kp[j];
           const bool lt = y < x;
           cnt += lt ? 1u : 0u;
-          kvs += lt ? ckv[j] : 0u;
+          kvs += lt ? kvp[j] : 0u;
           nad += (lt && ((y >> 31) & 1u)) ? 1u : 0u;
         }
       } else {
 #pragma unroll 4
-        for (uint32_t j = sub; j < n_valid; j += subn) cnt += ck[j] < x ? 1u : 0u;
+        for (uint32_t j = sub; j < n_valid; j += subn) cnt += kp[j] < x ? 1u : 0u;
       }
     }
 #pragma unroll
